@@ -1,0 +1,183 @@
+/*
+ * fgadmm_b200.h — C-ABI of the B200 engine for the five-phase factor-graph
+ * ADMM iteration (x, m, z, u, n) of the reference package `fgadmm`.
+ *
+ * The reference is pure Python/NumPy; its "FFI" for this path is the
+ * Python engine API.  Each entry point below replaces one reference
+ * interface (file:line relative to /root/reference/pkg/src/fgadmm):
+ *
+ *   fg_plan_create        engine.py:166-210  _GraphOps/_plan (per-graph plan,
+ *                                            kind batching, CSR-by-variable)
+ *                         graph.py:151-214   flat layout it consumes
+ *   fg_plan_sync_params   graph.py:232-246   set_edge_params (rho/alpha and
+ *                                            z_weights re-read each entry)
+ *   fg_state_upload       engine.py:468-471  run(..., state=prior)
+ *   fg_state_download     engine.py:521-522  state mutated in place / solution
+ *   fg_run                engine.py:454-531  run (five phases, residuals, stop)
+ *   fg_phase_*            engine.py:353-385  update_x .. update_n (unfused)
+ *   fg_residuals          engine.py:398-406  residuals
+ *   fg_prox_eval          prox.py:60-78      ProxFactor.batch_eval per kind
+ *                         operators.py       (11 closed forms)
+ *   fg_last_error         engine.py:145-149, 333-350 (error text source)
+ *
+ * All arrays are HOST pointers in the reference's own order (edge-creation
+ * order for payload arrays, variable order for z).  Device memory, streams
+ * and CUDA graphs are owned by the plan.  Every function returns 0 on
+ * success or a negative FG_ERR_* code; fg_last_error() gives the text.
+ * Calls on one plan must be serialized by the caller (as in the reference,
+ * no phase may run concurrently with set_edge_params).
+ */
+#ifndef FGADMM_B200_H
+#define FGADMM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FG_ABI_VERSION 1
+#define FG_MAX_SLOTS 8
+
+/* error codes */
+#define FG_OK 0
+#define FG_ERR_INVALID (-1)   /* bad argument / shape -> ValueError      */
+#define FG_ERR_CUDA (-2)      /* CUDA runtime failure -> RuntimeError    */
+#define FG_ERR_UNSUPPORTED (-3) /* kind without a device kernel          */
+#define FG_ERR_NONFINITE (-4) /* non-finite value detected (see result)  */
+
+/* operator kinds (registry names in operators.py) */
+#define FG_KIND_QUADRATIC 1   /* operators.py:99-149  */
+#define FG_KIND_COLLISION 2   /* operators.py:152-200 */
+#define FG_KIND_WALL 3        /* operators.py:203-246 */
+#define FG_KIND_RADIUS 4      /* operators.py:249-287 */
+#define FG_KIND_MPC_COST 5    /* operators.py:290-326 */
+#define FG_KIND_MPC_INIT 6    /* operators.py:329-365 */
+#define FG_KIND_MPC_DYN 7     /* operators.py:368-417 */
+#define FG_KIND_SVM_SLACK 8   /* operators.py:420-454 */
+#define FG_KIND_SVM_NORM 9    /* operators.py:457-490 */
+#define FG_KIND_SVM_MARGIN 10 /* operators.py:493-539 */
+#define FG_KIND_EQUALITY 11   /* operators.py:542-572 */
+#define FG_KIND_NAN_TEST 12   /* device fault injector (replaces tests' _Rogue) */
+
+/* phases, engine.py:25 */
+#define FG_PHASE_X 0
+#define FG_PHASE_M 1
+#define FG_PHASE_Z 2
+#define FG_PHASE_U 3
+#define FG_PHASE_N 4
+
+/* buffers addressable by fg_debug_download */
+#define FG_BUF_X 0
+#define FG_BUF_U0 1
+#define FG_BUF_U1 2
+#define FG_BUF_AUX 3
+
+typedef struct fg_plan fg_plan;
+
+/* The frozen graph's flat layout (graph.py:171-197). */
+typedef struct {
+    int64_t num_vars;            /* V                                    */
+    int64_t num_edges;           /* E                                    */
+    int64_t payload;             /* P = total_edge_payload               */
+    int64_t z_dim;               /* Z                                    */
+    const int32_t* var_dim;      /* [V] variable dims                    */
+    const int64_t* var_offsets;  /* [V+1] z offsets (graph.var_offsets)  */
+    const int32_t* edge_var;     /* [E] graph.edge_var                   */
+    const int64_t* edge_offsets; /* [E+1] graph.edge_offsets             */
+    int32_t chunk;               /* items per one-CTA pairwise subtree
+                                    (128..8192; 0 = 8192)               */
+    int32_t small_degree;        /* max degree summed by one thread
+                                    (1..32; 0 = 32)                     */
+} fg_graph_desc;
+
+/* One homogeneous factor batch: one (kind, slot dims) group, as
+ * engine.py:113-129 (_Group) builds it.  Edges of a factor are
+ * consecutive (graph.py:161-167), so slot j of factor i is reference edge
+ * first_edge[i] + j.  Parameters come from the kind's stack_params. */
+typedef struct {
+    int32_t kind;                  /* FG_KIND_*                           */
+    int32_t nslots;
+    int32_t slot_dim[FG_MAX_SLOTS];
+    int64_t count;                 /* factors in the group                */
+    const int64_t* first_edge;     /* [count]                             */
+    const double* fparams;         /* [count * fstride] per-factor params */
+    int32_t fstride;
+    int32_t tstride;               /* doubles per shared table entry      */
+    const double* tables;          /* [ntables * tstride]                 */
+    int64_t ntables;
+    const int32_t* fsys;           /* [count] table index, or NULL        */
+    int32_t iparam;                /* kind integer param (mpc_dyn: state
+                                      dim d; tables hold M (d x cols),
+                                      Q (d x d), L (d) per system)        */
+    int32_t reserved;
+} fg_group_desc;
+
+typedef struct {
+    int64_t max_iterations;        /* RunConfig.max_iterations            */
+    double primal_tol;             /* 0 disables (engine.py:473)          */
+    double dual_tol;
+    int32_t first_reads_n;         /* 1: first x-phase reads uploaded n   */
+    int32_t timing;                /* 1: per-kernel CUDA-event timing,
+                                      direct launches (no CUDA graph)     */
+    int32_t graph_chunk;           /* iterations per CUDA-graph launch    */
+    int32_t reserved;
+} fg_run_config;
+
+typedef struct {
+    int64_t iterations;            /* executed (RunReport.iterations)     */
+    int32_t converged;
+    int32_t error_phase;           /* -1, or FG_PHASE_* of first failure  */
+    int64_t error_iteration;       /* run-local iteration of the failure  */
+    double primal;                 /* residuals of the last iteration     */
+    double dual;
+    double ms_total;               /* device time of the iteration loop   */
+    double ms_edge_pass;           /* x-phase kernels (fused n); timing=1:
+                                      summed over all iterations, else
+                                      iteration 1 only (gives the shares) */
+    double ms_var_pass;            /* z-phase kernels (fused m, u)        */
+    double ms_reduce;              /* residual/stop kernel                */
+    int64_t launches;              /* kernels launched by the loop        */
+} fg_run_result;
+
+/* ---- plan lifecycle ---------------------------------------------------- */
+int fg_plan_create(const fg_graph_desc* graph, const fg_group_desc* groups,
+                   int32_t ngroups, int32_t device, fg_plan** out);
+void fg_plan_destroy(fg_plan* plan);
+int fg_plan_info(const fg_plan* plan, int64_t* out9);
+int fg_plan_sync_params(fg_plan* plan, const double* edge_rho,
+                        const double* edge_alpha, const double* z_weights);
+
+/* ---- fused run (the hot path) ------------------------------------------ */
+int fg_state_upload(fg_plan* plan, const double* z, const double* u,
+                    const double* n);
+int fg_run(fg_plan* plan, const fg_run_config* cfg, double* history,
+           fg_run_result* out);
+int fg_state_download(fg_plan* plan, double* x, double* m, double* z,
+                      double* u, double* n);
+int fg_debug_download(fg_plan* plan, int32_t buffer, double* out_ref);
+
+/* ---- unfused per-phase API (update_x .. update_n) ----------------------- */
+int fg_phase_upload(fg_plan* plan, const double* x, const double* m,
+                    const double* z, const double* u, const double* n);
+int fg_phase(fg_plan* plan, int32_t phase);
+int fg_phase_download(fg_plan* plan, double* x, double* m, double* z,
+                      double* u, double* n);
+int fg_residuals(fg_plan* plan, const double* x, const double* z,
+                 const double* z_prev, double* primal, double* dual);
+
+/* ---- standalone batched prox (ProxFactor.batch_eval) -------------------- */
+/* values: per slot j a (count, slot_dim[j]) row-major array, concatenated
+ * slot after slot; rhos: (nslots, count); out like values. */
+int fg_prox_eval(const fg_group_desc* group, const double* values,
+                 const double* rhos, double* out, int32_t device);
+
+/* ---- misc --------------------------------------------------------------- */
+const char* fg_last_error(void);
+int fg_abi_version(void);
+int fg_device_count(int32_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FGADMM_B200_H */

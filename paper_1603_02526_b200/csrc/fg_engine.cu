@@ -1,0 +1,942 @@
+// Host runtime + C-ABI of the B200 factor-graph ADMM engine.
+//
+// Plan construction replaces the reference's per-graph precomputation
+// (engine.py:166-255: kind batching, CSR-by-variable order, lane plans):
+//   * var-major layout: edges stably sorted by variable (== the reference
+//     z_order, engine.py:185-189, at edge granularity), payload contiguous
+//     per edge, so every consensus segment is a contiguous run;
+//   * per group, each slot's (variable, rank) so the edge pass finds its
+//     payload without a payload-sized gather index;
+//   * per z component a class (S: deg<=32 one thread; L: one CTA; G: chunked
+//     multi-CTA) and the NumPy pairwise tree of its reduceat segment.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "fg_kernels.cuh"
+
+using namespace fg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(expr)                                                              \
+    do {                                                                      \
+        cudaError_t e_ = (expr);                                              \
+        if (e_ != cudaSuccess)                                                \
+            return fail(FG_ERR_CUDA, std::string(#expr) + ": " +              \
+                                         cudaGetErrorString(e_));             \
+    } while (0)
+
+constexpr int kSmallDegMax = 32;     // class S threshold (degree)
+constexpr int64_t kChunkMax = 8192;  // pairwise subtree handled by one CTA
+constexpr int64_t kGiantWork = 8192; // elements per G3 CTA
+
+// ---------------------------------------------------------------------------
+// NumPy pairwise tree programs.  A node of m > 128 items splits at
+// h = m/2 - (m/2)%8 (numpy loops_utils.h pairwise_sum); "units" are the
+// maximal subtrees of <= unit_max items.  Internal nodes are emitted in
+// height order so a level-synchronous evaluation is exact.
+struct TreeBuild {
+    std::vector<std::pair<int64_t, int64_t>> units;
+    struct Node { int64_t l, r; int h; };      // child: >=0 unit, <0 ~internal
+    std::vector<Node> nodes;
+    int64_t unit_max;
+    std::pair<int64_t, int> rec(int64_t s, int64_t m) {
+        if (m <= unit_max) {
+            units.push_back({s, m});
+            return {(int64_t)units.size() - 1, 0};
+        }
+        int64_t h = m / 2;
+        h -= h % kUnroll;
+        auto L = rec(s, h);
+        auto R = rec(s + h, m - h);
+        nodes.push_back({L.first, R.first, 1 + std::max(L.second, R.second)});
+        return {~(int64_t)(nodes.size() - 1), nodes.back().h};
+    }
+};
+
+// Appends a program to `out`; returns its offset.
+int64_t emit_program(int64_t n, int64_t unit_max, std::vector<int32_t>& out,
+                     std::vector<std::pair<int64_t, int64_t>>* units_out) {
+    TreeBuild tb;
+    tb.unit_max = unit_max;
+    if (n > 0) tb.rec(0, n);
+    const int64_t nu = (int64_t)tb.units.size();
+    const int64_t ni = (int64_t)tb.nodes.size();
+    std::vector<int64_t> order(ni);
+    for (int64_t i = 0; i < ni; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+        return tb.nodes[a].h < tb.nodes[b].h;
+    });
+    std::vector<int64_t> newid(ni);
+    for (int64_t r = 0; r < ni; ++r) newid[order[r]] = nu + r;
+    auto enc = [&](int64_t c) { return c >= 0 ? c : newid[~c]; };
+    int maxh = 0;
+    for (auto& nd : tb.nodes) maxh = std::max(maxh, nd.h);
+    const int64_t off = (int64_t)out.size();
+    out.push_back((int32_t)nu);
+    out.push_back(maxh);
+    for (auto& u : tb.units) {
+        out.push_back((int32_t)u.first);
+        out.push_back((int32_t)u.second);
+    }
+    for (int h = 1; h <= maxh; ++h) {
+        int32_t cnt = 0;
+        for (auto& nd : tb.nodes) cnt += (nd.h == h);
+        out.push_back(cnt);
+    }
+    for (int64_t r = 0; r < ni; ++r) {
+        const auto& nd = tb.nodes[order[r]];
+        out.push_back((int32_t)enc(nd.l));
+        out.push_back((int32_t)enc(nd.r));
+    }
+    if (units_out) *units_out = tb.units;
+    return off;
+}
+
+template <class T>
+int dalloc(T** p, size_t count) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    CK(cudaMalloc((void**)p, count * sizeof(T)));
+    return 0;
+}
+
+template <class T>
+int upload(T** p, const std::vector<T>& h) {
+    int rc = dalloc(p, h.size());
+    if (rc) return rc;
+    if (!h.empty()) CK(cudaMemcpy(*p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return 0;
+}
+
+inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+struct GroupHost {
+    GroupDev dev{};
+    std::vector<void*> allocs;
+};
+
+struct fg_plan {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int64_t V = 0, E = 0, P = 0, Z = 0;
+    // var tables
+    int32_t *d_dim = nullptr, *d_deg = nullptr, *d_ebase = nullptr;
+    int64_t *d_pbase = nullptr, *d_zbase = nullptr;
+    int32_t* d_zvar = nullptr;
+    // layout maps
+    int64_t* d_vm2ref = nullptr;   // [P]
+    int32_t* d_vmz = nullptr;      // [P]
+    int32_t* d_vmvar = nullptr;    // [E]
+    int32_t* d_refedge = nullptr;  // [E]
+    // params
+    double *d_rho = nullptr, *d_alpha = nullptr, *d_zw = nullptr;
+    // state
+    double *d_x = nullptr, *d_u[2] = {nullptr, nullptr}, *d_stage = nullptr;
+    double *d_aux = nullptr, *d_z = nullptr, *d_zs = nullptr;
+    // groups
+    std::vector<GroupHost> groups;
+    // variable-pass classes
+    int32_t* d_slist = nullptr; int64_t nS = 0;
+    int32_t* d_llist = nullptr; int32_t* d_lprog = nullptr; int64_t nL = 0;
+    int32_t* d_prog = nullptr;
+    int32_t* d_glist = nullptr; int64_t nG = 0;
+    GChunk* d_gchunks = nullptr; int64_t nGC = 0;
+    GComp* d_gcomps = nullptr; int gtop_smem = 0;
+    GWork* d_gwork = nullptr; int64_t nGW = 0;
+    double* d_csum = nullptr;
+    double* d_gz = nullptr;
+    // residual partials
+    int64_t part_S = 0, part_L = 0, part_G = 0, npart = 0;
+    double* d_part = nullptr;
+    double* d_res2 = nullptr;
+    // control
+    Ctrl* d_ctrl = nullptr;
+    double* d_hist = nullptr; int64_t hist_cap = 0;
+    // run bookkeeping
+    int64_t completed = 0;         // iterations completed by the last run
+    int first_done = 0;
+    // graphs: key = chunk iterations
+    std::map<int, cudaGraphExec_t> graphs;
+    int64_t launches_per_iter = 0;
+
+    VarTab vt() const { return VarTab{d_dim, d_deg, d_ebase, d_pbase, d_zbase}; }
+    ~fg_plan();
+};
+
+fg_plan::~fg_plan() {
+    cudaSetDevice(device);
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    void* ptrs[] = {d_dim, d_deg, d_ebase, d_pbase, d_zbase, d_zvar, d_vm2ref,
+                    d_vmz, d_vmvar, d_refedge, d_rho, d_alpha, d_zw, d_x,
+                    d_u[0], d_u[1], d_stage, d_aux, d_z, d_zs, d_slist,
+                    d_llist, d_lprog, d_prog, d_glist, d_gchunks, d_gcomps,
+                    d_gwork, d_csum, d_gz, d_part, d_res2, d_ctrl, d_hist};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    for (auto& g : groups)
+        for (void* p : g.allocs) cudaFree(p);
+    if (stream) cudaStreamDestroy(stream);
+}
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// edge pass launchers
+template <bool FIRST>
+void launch_kind(const GroupDev& g, const PassA& a, cudaStream_t st) {
+    const int64_t n = g.count;
+    switch (g.kind) {
+        case FG_KIND_COLLISION:
+            k_collision<FIRST><<<nblk(n, 256), 256, 0, st>>>(a, g); break;
+        case FG_KIND_WALL:
+            k_wall<FIRST><<<nblk(n, 256), 256, 0, st>>>(a, g); break;
+        case FG_KIND_QUADRATIC:
+            k_quadratic<FIRST><<<nblk(n, 256), 256, 0, st>>>(a, g); break;
+        case FG_KIND_RADIUS:
+            k_elementwise<FG_KIND_RADIUS, FIRST><<<nblk(n * g.dim[0], 256), 256, 0, st>>>(a, g); break;
+        case FG_KIND_MPC_COST:
+            k_elementwise<FG_KIND_MPC_COST, FIRST><<<nblk(n * g.dim[0], 256), 256, 0, st>>>(a, g); break;
+        case FG_KIND_MPC_INIT:
+            k_elementwise<FG_KIND_MPC_INIT, FIRST><<<nblk(n * g.dim[0], 256), 256, 0, st>>>(a, g); break;
+        case FG_KIND_SVM_SLACK:
+            k_elementwise<FG_KIND_SVM_SLACK, FIRST><<<nblk(n * g.dim[0], 256), 256, 0, st>>>(a, g); break;
+        case FG_KIND_SVM_NORM:
+            k_elementwise<FG_KIND_SVM_NORM, FIRST><<<nblk(n * g.dim[0], 256), 256, 0, st>>>(a, g); break;
+        case FG_KIND_EQUALITY:
+            k_elementwise<FG_KIND_EQUALITY, FIRST><<<nblk(n * g.dim[0], 256), 256, 0, st>>>(a, g); break;
+        case FG_KIND_NAN_TEST:
+            k_elementwise<FG_KIND_NAN_TEST, FIRST><<<nblk(n * g.dim[0], 256), 256, 0, st>>>(a, g); break;
+        case FG_KIND_SVM_MARGIN:
+            k_svm_margin<FIRST><<<nblk(n * 32, 256), 256, 0, st>>>(a, g); break;
+        case FG_KIND_MPC_DYN:
+            k_mpc_dyn<FIRST><<<nblk(n, 4), 128, 0, st>>>(a, g); break;
+        default: break;
+    }
+}
+
+void edge_pass(fg_plan* p, bool first, const double* uin, const double* nsrc,
+               cudaStream_t st) {
+    PassA a{p->vt(), p->d_z, uin, nsrc, p->d_x, p->d_rho, p->d_ctrl};
+    for (auto& g : p->groups) {
+        if (g.dev.count == 0) continue;
+        if (first) launch_kind<true>(g.dev, a, st);
+        else launch_kind<false>(g.dev, a, st);
+    }
+}
+
+template <int MODE>
+void var_pass(fg_plan* p, const double* uin, double* uout, const double* msrc,
+              cudaStream_t st) {
+    PassB b{p->vt(), p->d_x, uin, uout, msrc, p->d_z, p->d_rho, p->d_alpha,
+            p->d_zw, p->d_ctrl, p->d_part, p->d_zvar};
+    if (p->nS)
+        k_var_small<MODE><<<nblk(p->nS, 256), 256, 0, st>>>(b, p->d_slist, p->nS, 0);
+    if (p->nL)
+        k_var_large<MODE><<<(unsigned)p->nL, kVarThreads, 0, st>>>(
+            b, p->d_llist, p->d_lprog, p->d_prog, p->part_S);
+    if (p->nG) {
+        k_var_giant_chunks<MODE><<<(unsigned)p->nGC, kVarThreads, 0, st>>>(
+            b, p->d_glist, p->d_gchunks, p->d_prog, p->d_csum);
+        k_var_giant_top<MODE><<<(unsigned)p->nG, kVarThreads, p->gtop_smem, st>>>(
+            b, p->d_glist, p->d_gcomps, p->d_prog, p->d_csum, p->d_gz);
+        if (MODE == MODE_FUSED)
+            k_var_giant_update<<<(unsigned)p->nGW, kVarThreads, 0, st>>>(
+                b, p->d_glist, p->d_gwork, p->d_gz, p->part_S + p->part_L);
+    }
+}
+
+int64_t count_edge_launches(const fg_plan* p) {
+    int64_t n = 0;
+    for (auto& g : p->groups) n += (g.dev.count > 0);
+    return n;
+}
+
+int64_t count_var_launches(const fg_plan* p) {
+    return (p->nS > 0) + (p->nL > 0) + (p->nG > 0 ? 3 : 0);
+}
+
+// One fused iteration.  Iteration j (1-based within a run) reads u[(j-1)&1]
+// and writes u[j&1].
+void launch_iteration(fg_plan* p, int in, bool first, cudaStream_t st) {
+    edge_pass(p, first, p->d_u[in], first ? p->d_u[1 - in] : nullptr, st);
+    var_pass<MODE_FUSED>(p, p->d_u[in], p->d_u[1 - in], nullptr, st);
+    k_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_hist);
+}
+
+int get_graph(fg_plan* p, int chunk, cudaGraphExec_t* out) {
+    auto it = p->graphs.find(chunk);
+    if (it != p->graphs.end()) { *out = it->second; return 0; }
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+    // chunk is even; starts with in = 1 (iterations 2, 3, ... of a run)
+    for (int i = 0; i < chunk; ++i) launch_iteration(p, (i & 1) ? 0 : 1, false, p->stream);
+    cudaError_t e = cudaStreamEndCapture(p->stream, &graph);
+    if (e != cudaSuccess) return fail(FG_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    cudaGraphExec_t exec;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return fail(FG_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    p->graphs[chunk] = exec;
+    *out = exec;
+    return 0;
+}
+
+int check_launch() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(FG_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+    return 0;
+}
+
+int build_group(fg_plan* p, const fg_group_desc& gd,
+                const std::vector<int32_t>& edge_var,
+                const std::vector<int32_t>& vm_of_ref,
+                const std::vector<int32_t>& ebase, GroupHost& out) {
+    GroupDev& g = out.dev;
+    g.kind = gd.kind;
+    g.nslots = gd.nslots;
+    g.count = gd.count;
+    g.fstride = gd.fstride;
+    g.tstride = gd.tstride;
+    g.ip = gd.iparam;
+    if (gd.nslots < 1 || gd.nslots > FG_MAX_SLOTS)
+        return fail(FG_ERR_INVALID, "group slot count out of range");
+    for (int j = 0; j < gd.nslots; ++j) g.dim[j] = gd.slot_dim[j];
+    switch (gd.kind) {
+        case FG_KIND_COLLISION:
+            if (gd.nslots != 4 || g.dim[0] != 2 || g.dim[1] != 1 || g.dim[2] != 2 || g.dim[3] != 1)
+                return fail(FG_ERR_UNSUPPORTED, "collision expects slot dims (2,1,2,1)");
+            break;
+        case FG_KIND_WALL:
+            if (gd.nslots != 2 || g.dim[0] != 2 || g.dim[1] != 1)
+                return fail(FG_ERR_UNSUPPORTED, "wall expects slot dims (2,1)");
+            break;
+        case FG_KIND_SVM_MARGIN:
+            if (gd.nslots != 3 || g.dim[0] > 32 * kMarginMaxPerLane || g.dim[1] != 1 || g.dim[2] != 1)
+                return fail(FG_ERR_UNSUPPORTED, "svm_margin expects slot dims (D<=128,1,1)");
+            break;
+        case FG_KIND_EQUALITY:
+            if (gd.nslots != 2 || g.dim[0] != g.dim[1])
+                return fail(FG_ERR_UNSUPPORTED, "equality expects two equal slots");
+            break;
+        case FG_KIND_MPC_DYN:
+            if (gd.nslots != 2 || g.dim[0] != g.dim[1] || gd.iparam < 1 ||
+                gd.iparam > kDynMaxD || gd.iparam > g.dim[0] ||
+                g.dim[0] + gd.iparam > kDynMaxCols || gd.tables == nullptr)
+                return fail(FG_ERR_UNSUPPORTED, "mpc_dyn dims out of the device kernel's range");
+            break;
+        case FG_KIND_RADIUS: case FG_KIND_MPC_COST: case FG_KIND_MPC_INIT:
+        case FG_KIND_SVM_SLACK: case FG_KIND_SVM_NORM: case FG_KIND_NAN_TEST:
+            if (gd.nslots != 1) return fail(FG_ERR_UNSUPPORTED, "single-slot kind with several slots");
+            break;
+        case FG_KIND_QUADRATIC: break;
+        default:
+            return fail(FG_ERR_UNSUPPORTED, "operator kind has no device kernel");
+    }
+    const int64_t n = gd.count;
+    for (int j = 0; j < gd.nslots; ++j) {
+        std::vector<int32_t> sv(n), sk(n);
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t e = gd.first_edge[i] + j;
+            const int32_t v = edge_var[e];
+            sv[i] = v;
+            sk[i] = vm_of_ref[e] - ebase[v];
+        }
+        int32_t *dsv, *dsk;
+        if (int rc = upload(&dsv, sv)) return rc;
+        out.allocs.push_back(dsv);
+        if (int rc = upload(&dsk, sk)) return rc;
+        out.allocs.push_back(dsk);
+        g.svar[j] = dsv;
+        g.sk[j] = dsk;
+    }
+    if (gd.fparams && gd.fstride > 0) {
+        std::vector<double> fp(gd.fparams, gd.fparams + n * gd.fstride);
+        double* d;
+        if (int rc = upload(&d, fp)) return rc;
+        out.allocs.push_back(d);
+        g.fp = d;
+    }
+    if (gd.tables && gd.ntables > 0) {
+        std::vector<double> t(gd.tables, gd.tables + gd.ntables * gd.tstride);
+        double* d;
+        if (int rc = upload(&d, t)) return rc;
+        out.allocs.push_back(d);
+        g.tab = d;
+    }
+    if (gd.fsys) {
+        std::vector<int32_t> fs(gd.fsys, gd.fsys + n);
+        int32_t* d;
+        if (int rc = upload(&d, fs)) return rc;
+        out.allocs.push_back(d);
+        g.fsys = d;
+    }
+    return 0;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+const char* fg_last_error(void) { return g_err.c_str(); }
+int fg_abi_version(void) { return FG_ABI_VERSION; }
+
+int fg_device_count(int32_t* count) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) { *count = 0; return fail(FG_ERR_CUDA, cudaGetErrorString(e)); }
+    *count = n;
+    return 0;
+}
+
+int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
+                   int32_t ngroups, int32_t device, fg_plan** out) {
+    *out = nullptr;
+    if (!gd || gd->num_vars < 1 || gd->num_edges < 1)
+        return fail(FG_ERR_INVALID, "empty graph");
+    if (gd->num_edges >= (int64_t)INT32_MAX || gd->num_vars >= (int64_t)INT32_MAX ||
+        gd->z_dim >= (int64_t)INT32_MAX)
+        return fail(FG_ERR_INVALID, "graph exceeds the 2^31 edge/variable/z limit of one device plan");
+    CK(cudaSetDevice(device));
+    std::unique_ptr<fg_plan> p(new fg_plan());
+    p->device = device;
+    CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    const int64_t V = gd->num_vars, E = gd->num_edges, P = gd->payload, Z = gd->z_dim;
+    p->V = V; p->E = E; p->P = P; p->Z = Z;
+
+    // ---- var-major order (stable counting sort of edges by variable) ----
+    std::vector<int32_t> edge_var(gd->edge_var, gd->edge_var + E);
+    std::vector<int32_t> dim(gd->var_dim, gd->var_dim + V), deg(V, 0), ebase(V);
+    std::vector<int64_t> pbase(V), zbase(V);
+    for (int64_t e = 0; e < E; ++e) {
+        const int32_t v = edge_var[e];
+        if (v < 0 || v >= V) return fail(FG_ERR_INVALID, "edge_var out of range");
+        deg[v]++;
+    }
+    int64_t acc_e = 0, acc_p = 0;
+    for (int64_t v = 0; v < V; ++v) {
+        ebase[v] = (int32_t)acc_e;
+        pbase[v] = acc_p;
+        zbase[v] = gd->var_offsets[v];
+        acc_e += deg[v];
+        acc_p += (int64_t)deg[v] * dim[v];
+    }
+    if (acc_p != P) return fail(FG_ERR_INVALID, "payload size does not match dims");
+    std::vector<int32_t> vm_of_ref(E), refedge(E), vmvar(E), fill(V, 0);
+    for (int64_t e = 0; e < E; ++e) {
+        const int32_t v = edge_var[e];
+        const int32_t q = ebase[v] + fill[v]++;
+        vm_of_ref[e] = q;
+        refedge[q] = (int32_t)e;
+        vmvar[q] = v;
+    }
+    std::vector<int64_t> vm2ref(P);
+    std::vector<int32_t> vmz(P);
+    for (int64_t q = 0; q < E; ++q) {
+        const int32_t v = vmvar[q];
+        const int64_t d = dim[v];
+        const int64_t vmp = pbase[v] + (int64_t)(q - ebase[v]) * d;
+        const int64_t rp = gd->edge_offsets[refedge[q]];
+        for (int64_t c = 0; c < d; ++c) {
+            vm2ref[vmp + c] = rp + c;
+            vmz[vmp + c] = (int32_t)(zbase[v] + c);
+        }
+    }
+    std::vector<int32_t> zvar(Z);
+    for (int64_t v = 0; v < V; ++v)
+        for (int64_t c = 0; c < dim[v]; ++c) zvar[zbase[v] + c] = (int32_t)v;
+
+    int rc;
+    if ((rc = upload(&p->d_dim, dim)) || (rc = upload(&p->d_deg, deg)) ||
+        (rc = upload(&p->d_ebase, ebase)) || (rc = upload(&p->d_pbase, pbase)) ||
+        (rc = upload(&p->d_zbase, zbase)) || (rc = upload(&p->d_zvar, zvar)) ||
+        (rc = upload(&p->d_vm2ref, vm2ref)) || (rc = upload(&p->d_vmz, vmz)) ||
+        (rc = upload(&p->d_vmvar, vmvar)) || (rc = upload(&p->d_refedge, refedge)))
+        return rc;
+    vm2ref.clear(); vm2ref.shrink_to_fit();
+    vmz.clear(); vmz.shrink_to_fit();
+
+    // ---- state buffers ----
+    if ((rc = dalloc(&p->d_rho, E)) || (rc = dalloc(&p->d_alpha, E)) ||
+        (rc = dalloc(&p->d_zw, Z)) || (rc = dalloc(&p->d_x, P)) ||
+        (rc = dalloc(&p->d_u[0], P)) || (rc = dalloc(&p->d_u[1], P)) ||
+        (rc = dalloc(&p->d_stage, std::max(P, Z))) || (rc = dalloc(&p->d_z, Z)) ||
+        (rc = dalloc(&p->d_zs, Z)) || (rc = dalloc(&p->d_ctrl, 1)) ||
+        (rc = dalloc(&p->d_res2, 2)))
+        return rc;
+    CK(cudaMemset(p->d_x, 0, P * sizeof(double)));
+    CK(cudaMemset(p->d_u[0], 0, P * sizeof(double)));
+    CK(cudaMemset(p->d_u[1], 0, P * sizeof(double)));
+    CK(cudaMemset(p->d_z, 0, Z * sizeof(double)));
+
+    // ---- groups ----
+    for (int32_t i = 0; i < ngroups; ++i) {
+        p->groups.emplace_back();
+        if ((rc = build_group(p.get(), groups[i], edge_var, vm_of_ref, ebase, p->groups.back())))
+            return rc;
+    }
+
+    // ---- variable-pass classes and tree programs ----
+    std::vector<int32_t> slist, llist, lprog, glist, prog;
+    std::vector<GChunk> gchunks;
+    std::vector<GComp> gcomps;
+    std::vector<GWork> gwork;
+    std::map<int64_t, int32_t> leafprog;   // n -> offset
+    auto leaf_prog = [&](int64_t n) -> int32_t {
+        auto it = leafprog.find(n);
+        if (it != leafprog.end()) return it->second;
+        const int64_t off = emit_program(n, kLeafMax, prog, nullptr);
+        leafprog[n] = (int32_t)off;
+        return (int32_t)off;
+    };
+    const int64_t kChunk = gd->chunk > 0 ? gd->chunk : kChunkMax;
+    const int64_t kSmallDeg = gd->small_degree > 0 ? gd->small_degree : kSmallDegMax;
+    if (kChunk < kLeafMax || kChunk > kChunkMax || kSmallDeg > kSmallDegMax)
+        return fail(FG_ERR_INVALID, "chunk must be in [128, 8192], small_degree in [1, 32]");
+    int max_top = 1;
+    for (int64_t v = 0; v < V; ++v) {
+        const int64_t dg = deg[v];
+        for (int64_t c = 0; c < dim[v]; ++c) {
+            const int32_t k = (int32_t)(zbase[v] + c);
+            if (dg <= kSmallDeg) {
+                slist.push_back(k);
+            } else if (dg - 1 <= kChunk) {
+                llist.push_back(k);
+                lprog.push_back(leaf_prog(dg - 1));
+            } else {
+                const int32_t gi = (int32_t)glist.size();
+                glist.push_back(k);
+                std::vector<std::pair<int64_t, int64_t>> chunks;
+                const int32_t top = (int32_t)emit_program(dg - 1, kChunk, prog, &chunks);
+                gcomps.push_back(GComp{top, (int32_t)gchunks.size(), 0, 0});
+                max_top = std::max(max_top, (int)chunks.size());
+                for (auto& ch : chunks)
+                    gchunks.push_back(GChunk{gi, (int32_t)ch.first, leaf_prog(ch.second), 0});
+                for (int64_t e0 = 0; e0 < dg; e0 += kGiantWork)
+                    gwork.push_back(GWork{gi, (int32_t)e0, (int32_t)std::min<int64_t>(dg, e0 + kGiantWork), 0});
+            }
+        }
+    }
+    p->nS = (int64_t)slist.size();
+    p->nL = (int64_t)llist.size();
+    p->nG = (int64_t)glist.size();
+    p->nGC = (int64_t)gchunks.size();
+    p->nGW = (int64_t)gwork.size();
+    p->gtop_smem = (int)(2 * max_top * sizeof(double));
+    if ((size_t)p->gtop_smem > 48 * 1024) {
+        CK(cudaFuncSetAttribute(k_var_giant_top<MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->gtop_smem));
+        CK(cudaFuncSetAttribute(k_var_giant_top<MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->gtop_smem));
+    }
+    if ((rc = upload(&p->d_slist, slist)) || (rc = upload(&p->d_llist, llist)) ||
+        (rc = upload(&p->d_lprog, lprog)) || (rc = upload(&p->d_prog, prog)) ||
+        (rc = upload(&p->d_glist, glist)) || (rc = upload(&p->d_gchunks, gchunks)) ||
+        (rc = upload(&p->d_gcomps, gcomps)) || (rc = upload(&p->d_gwork, gwork)) ||
+        (rc = dalloc(&p->d_csum, gchunks.size())) || (rc = dalloc(&p->d_gz, 2 * glist.size())))
+        return rc;
+    p->part_S = nblk(p->nS, 256);
+    p->part_L = p->nL;
+    p->part_G = p->nGW;
+    p->npart = p->part_S + p->part_L + p->part_G;
+    const int64_t nres = nblk(E, 256);
+    if ((rc = dalloc(&p->d_part, 2 * std::max(p->npart, nres)))) return rc;
+    CK(cudaMemset(p->d_part, 0, 2 * std::max(p->npart, nres) * sizeof(double)));
+    p->launches_per_iter = count_edge_launches(p.get()) + count_var_launches(p.get()) + 1;
+    CK(cudaDeviceSynchronize());
+    *out = p.release();
+    return 0;
+}
+
+void fg_plan_destroy(fg_plan* plan) { delete plan; }
+
+int fg_plan_info(const fg_plan* p, int64_t* o) {
+    o[0] = p->V; o[1] = p->E; o[2] = p->P; o[3] = p->Z;
+    o[4] = p->nS; o[5] = p->nL; o[6] = p->nG; o[7] = p->nGC;
+    o[8] = p->launches_per_iter;
+    return 0;
+}
+
+int fg_plan_sync_params(fg_plan* p, const double* rho, const double* alpha,
+                        const double* zw) {
+    CK(cudaSetDevice(p->device));
+    cudaStream_t st = p->stream;
+    CK(cudaMemcpyAsync(p->d_stage, rho, p->E * sizeof(double), cudaMemcpyHostToDevice, st));
+    k_gather_edges<<<nblk(p->E, 256), 256, 0, st>>>(p->E, p->d_refedge, p->d_stage, p->d_rho);
+    CK(cudaMemcpyAsync(p->d_stage, alpha, p->E * sizeof(double), cudaMemcpyHostToDevice, st));
+    k_gather_edges<<<nblk(p->E, 256), 256, 0, st>>>(p->E, p->d_refedge, p->d_stage, p->d_alpha);
+    CK(cudaMemcpyAsync(p->d_zw, zw, p->Z * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    return check_launch();
+}
+
+static int upload_vm(fg_plan* p, const double* src_ref, double* dst) {
+    cudaStream_t st = p->stream;
+    CK(cudaMemcpyAsync(p->d_stage, src_ref, p->P * sizeof(double), cudaMemcpyHostToDevice, st));
+    k_gather_from_ref<<<nblk(p->P, 256), 256, 0, st>>>(p->P, p->d_vm2ref, p->d_stage, dst);
+    return 0;
+}
+
+static int download_ref(fg_plan* p, int mode, const double* ucur,
+                        const double* uprev, double* dst_host) {
+    cudaStream_t st = p->stream;
+    k_scatter_to_ref<<<nblk(p->P, 256), 256, 0, st>>>(p->P, p->d_vm2ref, p->d_vmz, mode,
+                                                     p->d_x, ucur, uprev, p->d_z, p->d_stage);
+    CK(cudaMemcpyAsync(dst_host, p->d_stage, p->P * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return check_launch();
+}
+
+int fg_state_upload(fg_plan* p, const double* z, const double* u, const double* n) {
+    CK(cudaSetDevice(p->device));
+    CK(cudaMemcpyAsync(p->d_z, z, p->Z * sizeof(double), cudaMemcpyHostToDevice, p->stream));
+    upload_vm(p, u, p->d_u[0]);
+    upload_vm(p, n, p->d_u[1]);   // consumed by the first edge pass
+    CK(cudaStreamSynchronize(p->stream));
+    p->completed = 0;
+    return check_launch();
+}
+
+int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result* out) {
+    CK(cudaSetDevice(p->device));
+    if (cfg->max_iterations < 1) return fail(FG_ERR_INVALID, "max_iterations must be >= 1");
+    cudaStream_t st = p->stream;
+    const int64_t K = cfg->max_iterations;
+    if (p->hist_cap < K) {
+        if (p->d_hist) cudaFree(p->d_hist);
+        p->d_hist = nullptr;
+        int rc = dalloc(&p->d_hist, 2 * K);
+        if (rc) return rc;
+        p->hist_cap = K;
+    }
+    Ctrl h{};
+    h.err_key = ~0ull;
+    h.iter = 1;
+    h.primal_tol = cfg->primal_tol;
+    h.dual_tol = cfg->dual_tol;
+    h.scale = 1.0 / std::sqrt((double)p->P);
+    h.max_iter = K;
+    CK(cudaMemcpyAsync(p->d_ctrl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+
+    cudaEvent_t ev0, ev1;
+    CK(cudaEventCreate(&ev0));
+    CK(cudaEventCreate(&ev1));
+    double ms_a = 0, ms_b = 0, ms_r = 0;
+    int64_t launches = 0;
+    CK(cudaEventRecord(ev0, st));
+    if (cfg->timing) {
+        // direct launches with events around each pass of every iteration
+        std::vector<cudaEvent_t> ev(4 * K);
+        for (auto& e : ev) CK(cudaEventCreate(&e));
+        for (int64_t j = 1; j <= K; ++j) {
+            const int in = (int)((j - 1) & 1);
+            const bool first = (j == 1) && cfg->first_reads_n;
+            cudaEvent_t* E4 = &ev[4 * (j - 1)];
+            CK(cudaEventRecord(E4[0], st));
+            edge_pass(p, first, p->d_u[in], first ? p->d_u[1 - in] : nullptr, st);
+            CK(cudaEventRecord(E4[1], st));
+            var_pass<MODE_FUSED>(p, p->d_u[in], p->d_u[1 - in], nullptr, st);
+            CK(cudaEventRecord(E4[2], st));
+            k_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_hist);
+            CK(cudaEventRecord(E4[3], st));
+            launches += p->launches_per_iter;
+        }
+        CK(cudaEventRecord(ev1, st));
+        CK(cudaStreamSynchronize(st));
+        for (int64_t j = 0; j < K; ++j) {
+            float a, b, r;
+            cudaEventElapsedTime(&a, ev[4 * j], ev[4 * j + 1]);
+            cudaEventElapsedTime(&b, ev[4 * j + 1], ev[4 * j + 2]);
+            cudaEventElapsedTime(&r, ev[4 * j + 2], ev[4 * j + 3]);
+            ms_a += a; ms_b += b; ms_r += r;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+    } else {
+        // iteration 1 directly (it may read the uploaded n), then CUDA-graph
+        // chunks of an even number of iterations, with a two-deep polling
+        // pipeline on the stop flag so a converged run stops early.
+        // iteration 1 is timed per pass; its shares split the loop time
+        cudaEvent_t e4[4];
+        for (auto& e : e4) CK(cudaEventCreate(&e));
+        CK(cudaEventRecord(e4[0], st));
+        edge_pass(p, cfg->first_reads_n != 0, p->d_u[0],
+                  cfg->first_reads_n ? p->d_u[1] : nullptr, st);
+        CK(cudaEventRecord(e4[1], st));
+        var_pass<MODE_FUSED>(p, p->d_u[0], p->d_u[1], nullptr, st);
+        CK(cudaEventRecord(e4[2], st));
+        k_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_hist);
+        CK(cudaEventRecord(e4[3], st));
+        launches += p->launches_per_iter;
+        int64_t left = K - 1;
+        int chunk = std::max(2, cfg->graph_chunk - (cfg->graph_chunk & 1));
+        int32_t* h_stop = nullptr;
+        CK(cudaMallocHost((void**)&h_stop, 4 * sizeof(int32_t)));
+        cudaEvent_t pe[2];
+        CK(cudaEventCreateWithFlags(&pe[0], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&pe[1], cudaEventDisableTiming));
+        int inflight = 0, slot = 0;
+        bool stopped = false;
+        while (left > 0 && !stopped) {
+            int n;
+            cudaGraphExec_t gx = nullptr;
+            if (left >= chunk) {
+                n = chunk;
+                int rc = get_graph(p, chunk, &gx);
+                if (rc) return rc;
+                CK(cudaGraphLaunch(gx, st));
+            } else if (left >= 2) {
+                n = 2;
+                int rc = get_graph(p, 2, &gx);
+                if (rc) return rc;
+                CK(cudaGraphLaunch(gx, st));
+            } else {
+                n = 1;
+                launch_iteration(p, 1, false, st);   // iteration index even -> in=1
+            }
+            launches += n * p->launches_per_iter;
+            left -= n;
+            CK(cudaMemcpyAsync(&h_stop[slot], &p->d_ctrl->stop, sizeof(int32_t),
+                               cudaMemcpyDeviceToHost, st));
+            CK(cudaEventRecord(pe[slot], st));
+            ++inflight;
+            if (inflight >= 2) {
+                const int old = slot ^ 1;
+                CK(cudaEventSynchronize(pe[old]));
+                --inflight;
+                if (h_stop[old]) stopped = true;
+            }
+            slot ^= 1;
+        }
+        CK(cudaEventRecord(ev1, st));
+        CK(cudaStreamSynchronize(st));
+        {
+            float a = 0, b = 0, r = 0;
+            cudaEventElapsedTime(&a, e4[0], e4[1]);
+            cudaEventElapsedTime(&b, e4[1], e4[2]);
+            cudaEventElapsedTime(&r, e4[2], e4[3]);
+            ms_a = a; ms_b = b; ms_r = r;   // iteration-1 shares (see header)
+            for (auto& e : e4) cudaEventDestroy(e);
+        }
+        cudaEventDestroy(pe[0]);
+        cudaEventDestroy(pe[1]);
+        cudaFreeHost(h_stop);
+    }
+    float tot = 0;
+    cudaEventElapsedTime(&tot, ev0, ev1);
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    if (int rc = check_launch()) return rc;
+    CK(cudaMemcpy(&h, p->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+    p->completed = h.completed;
+    out->iterations = h.completed;
+    out->converged = h.converged;
+    out->primal = h.primal;
+    out->dual = h.dual;
+    out->error_phase = -1;
+    out->error_iteration = 0;
+    if (h.err_key != ~0ull) {
+        out->error_phase = (int32_t)(h.err_key & 7ull);
+        out->error_iteration = (int64_t)(h.err_key >> 3);
+    }
+    out->ms_total = tot;
+    out->ms_edge_pass = ms_a;
+    out->ms_var_pass = ms_b;
+    out->ms_reduce = ms_r;
+    out->launches = launches;
+    if (history && h.completed > 0)
+        CK(cudaMemcpy(history, p->d_hist, 2 * h.completed * sizeof(double), cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+int fg_state_download(fg_plan* p, double* x, double* m, double* z, double* u, double* n) {
+    CK(cudaSetDevice(p->device));
+    const int cur = (int)(p->completed & 1);
+    const double* ucur = p->d_u[cur];
+    const double* uprev = p->d_u[cur ^ 1];
+    int rc;
+    if (x && (rc = download_ref(p, 0, ucur, uprev, x))) return rc;
+    if (m && (rc = download_ref(p, 1, ucur, uprev, m))) return rc;
+    if (u && (rc = download_ref(p, 2, ucur, uprev, u))) return rc;
+    if (n && (rc = download_ref(p, 3, ucur, uprev, n))) return rc;
+    if (z) CK(cudaMemcpy(z, p->d_z, p->Z * sizeof(double), cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+int fg_debug_download(fg_plan* p, int32_t buffer, double* out_ref) {
+    CK(cudaSetDevice(p->device));
+    const double* src = nullptr;
+    switch (buffer) {
+        case FG_BUF_X: src = p->d_x; break;
+        case FG_BUF_U0: src = p->d_u[0]; break;
+        case FG_BUF_U1: src = p->d_u[1]; break;
+        case FG_BUF_AUX: src = p->d_aux; break;
+        default: return fail(FG_ERR_INVALID, "unknown buffer id");
+    }
+    if (!src) return fail(FG_ERR_INVALID, "buffer not allocated");
+    return download_ref(p, 2, src, src, out_ref);
+}
+
+// ---- unfused per-phase path ----------------------------------------------
+// buffers: x -> d_x, m -> d_u[1], z -> d_z, u -> d_u[0], n -> d_aux
+int fg_phase_upload(fg_plan* p, const double* x, const double* m, const double* z,
+                    const double* u, const double* n) {
+    CK(cudaSetDevice(p->device));
+    if (!p->d_aux) {
+        int rc = dalloc(&p->d_aux, p->P);
+        if (rc) return rc;
+    }
+    upload_vm(p, x, p->d_x);
+    upload_vm(p, m, p->d_u[1]);
+    upload_vm(p, u, p->d_u[0]);
+    upload_vm(p, n, p->d_aux);
+    CK(cudaMemcpyAsync(p->d_z, z, p->Z * sizeof(double), cudaMemcpyHostToDevice, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
+    return check_launch();
+}
+
+int fg_phase(fg_plan* p, int32_t phase) {
+    CK(cudaSetDevice(p->device));
+    if (!p->d_aux) return fail(FG_ERR_INVALID, "fg_phase_upload must precede fg_phase");
+    cudaStream_t st = p->stream;
+    Ctrl h{};
+    h.err_key = ~0ull;
+    h.iter = 1;
+    CK(cudaMemcpyAsync(p->d_ctrl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+    switch (phase) {
+        case FG_PHASE_X: edge_pass(p, true, p->d_u[0], p->d_aux, st); break;
+        case FG_PHASE_M:
+            k_phase_m<<<nblk(p->P, 256), 256, 0, st>>>(p->P, p->d_x, p->d_u[0], p->d_u[1]); break;
+        case FG_PHASE_Z: var_pass<MODE_PHASEZ>(p, nullptr, nullptr, p->d_u[1], st); break;
+        case FG_PHASE_U:
+            k_phase_u<<<nblk(p->E, 256), 256, 0, st>>>(p->E, p->vt(), p->d_vmvar, p->d_x,
+                                                       p->d_z, p->d_alpha, p->d_u[0]); break;
+        case FG_PHASE_N:
+            k_phase_n<<<nblk(p->P, 256), 256, 0, st>>>(p->P, p->d_vmz, p->d_z, p->d_u[0], p->d_aux); break;
+        default: return fail(FG_ERR_INVALID, "unknown phase");
+    }
+    CK(cudaStreamSynchronize(st));
+    return check_launch();
+}
+
+int fg_phase_download(fg_plan* p, double* x, double* m, double* z, double* u, double* n) {
+    CK(cudaSetDevice(p->device));
+    if (!p->d_aux) return fail(FG_ERR_INVALID, "fg_phase_upload must precede fg_phase_download");
+    int rc;
+    if (x && (rc = download_ref(p, 2, p->d_x, p->d_x, x))) return rc;
+    if (m && (rc = download_ref(p, 2, p->d_u[1], p->d_u[1], m))) return rc;
+    if (u && (rc = download_ref(p, 2, p->d_u[0], p->d_u[0], u))) return rc;
+    if (n && (rc = download_ref(p, 2, p->d_aux, p->d_aux, n))) return rc;
+    if (z) CK(cudaMemcpy(z, p->d_z, p->Z * sizeof(double), cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+int fg_residuals(fg_plan* p, const double* x, const double* z, const double* zprev,
+                 double* primal, double* dual) {
+    CK(cudaSetDevice(p->device));
+    cudaStream_t st = p->stream;
+    double* xs = p->d_aux ? p->d_aux : p->d_u[1];
+    upload_vm(p, x, xs);
+    CK(cudaMemcpyAsync(p->d_z, z, p->Z * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(p->d_zs, zprev, p->Z * sizeof(double), cudaMemcpyHostToDevice, st));
+    const unsigned nb = nblk(p->E, 256);
+    k_residual_parts<<<nb, 256, 0, st>>>(p->E, p->vt(), p->d_vmvar, xs, p->d_z,
+                                        p->d_zs, p->d_rho, p->d_part);
+    k_sum_parts<<<1, 1024, 0, st>>>(p->d_part, nb, p->d_res2);
+    double r2[2];
+    CK(cudaMemcpyAsync(r2, p->d_res2, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const double scale = 1.0 / std::sqrt((double)p->P);
+    *primal = std::sqrt(r2[0]) * scale;
+    *dual = std::sqrt(r2[1]) * scale;
+    return check_launch();
+}
+
+// ---- standalone batched prox ----------------------------------------------
+int fg_prox_eval(const fg_group_desc* gd, const double* values, const double* rhos,
+                 double* out, int32_t device) {
+    CK(cudaSetDevice(device));
+    const int64_t n = gd->count;
+    const int ns = gd->nslots;
+    if (n < 1) return 0;
+    if (ns < 1 || ns > FG_MAX_SLOTS) return fail(FG_ERR_INVALID, "slot count out of range");
+    // one "variable" per (slot, factor) with a single edge
+    const int64_t V = ns * n;
+    std::vector<int32_t> dim(V), deg(V, 1), ebase(V);
+    std::vector<int64_t> pbase(V), zbase(V, 0);
+    int64_t P = 0;
+    for (int j = 0; j < ns; ++j)
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t v = j * n + i;
+            dim[v] = gd->slot_dim[j];
+            ebase[v] = (int32_t)v;
+            pbase[v] = P;
+            P += gd->slot_dim[j];
+        }
+    std::vector<int32_t> edge_var(V), vm_of_ref(V);
+    for (int64_t v = 0; v < V; ++v) { edge_var[v] = (int32_t)v; vm_of_ref[v] = (int32_t)v; }
+    // group edges: factor i slot j -> reference edge j*n + i; first_edge must
+    // make first_edge[i] + j land there, so remap through a local table
+    fg_plan tmp;
+    tmp.device = device;
+    int rc;
+    if ((rc = upload(&tmp.d_dim, dim)) || (rc = upload(&tmp.d_deg, deg)) ||
+        (rc = upload(&tmp.d_ebase, ebase)) || (rc = upload(&tmp.d_pbase, pbase)) ||
+        (rc = upload(&tmp.d_zbase, zbase)))
+        return rc;
+    GroupHost gh;
+    {
+        // build slot tables directly (slot j of factor i is variable j*n+i)
+        fg_group_desc g2 = *gd;
+        std::vector<int64_t> fe(n);
+        // emulate consecutive edges: edge id = i*ns + j, mapped to var j*n+i
+        std::vector<int32_t> ev(n * ns), vo(n * ns);
+        for (int64_t i = 0; i < n; ++i)
+            for (int j = 0; j < ns; ++j) {
+                ev[i * ns + j] = (int32_t)(j * n + i);
+                vo[i * ns + j] = ebase[j * n + i];
+            }
+        for (int64_t i = 0; i < n; ++i) fe[i] = i * ns;
+        g2.first_edge = fe.data();
+        if ((rc = build_group(&tmp, g2, ev, vo, ebase, gh))) return rc;
+    }
+    double *d_vals, *d_rho, *d_out;
+    if ((rc = dalloc(&d_vals, P)) || (rc = dalloc(&d_rho, V)) || (rc = dalloc(&d_out, P)))
+        return rc;
+    CK(cudaMemcpy(d_vals, values, P * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_rho, rhos, V * sizeof(double), cudaMemcpyHostToDevice));
+    Ctrl h{};
+    h.err_key = ~0ull;
+    h.iter = 1;
+    Ctrl* d_ctrl;
+    if ((rc = dalloc(&d_ctrl, 1))) return rc;
+    CK(cudaMemcpy(d_ctrl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice));
+    PassA a{tmp.vt(), nullptr, nullptr, d_vals, d_out, d_rho, d_ctrl};
+    launch_kind<true>(gh.dev, a, 0);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(out, d_out, P * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(d_vals); cudaFree(d_rho); cudaFree(d_out); cudaFree(d_ctrl);
+    for (void* q : gh.allocs) cudaFree(q);
+    if (e != cudaSuccess) return fail(FG_ERR_CUDA, cudaGetErrorString(e));
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,724 @@
+// Kernels of the B200 factor-graph ADMM engine.
+//
+// One ADMM iteration (engine.py:483-516) runs as:
+//   edge pass   : one kernel per (kind, slot dims) group.  Reads u and z,
+//                 forms n = z[zmap] - u (phase n of the previous iteration,
+//                 engine.py:292-298), applies the kind's prox (phase x,
+//                 engine.py:257-261), writes x.
+//   variable pass: per z component, m = x + u (phase m, engine.py:263-265),
+//                 the exact NumPy reduceat tree of m*rho (phase z,
+//                 engine.py:267-280), z = sum / z_weights, then
+//                 u += alpha (x - z) (phase u, engine.py:282-290) and the
+//                 residual partial sums (engine.py:398-406).  u is
+//                 ping-ponged so the previous u survives for m.
+//   reduce      : residuals, tolerance stop, iteration counter.
+#pragma once
+
+#include "fg_device.cuh"
+
+namespace fg {
+
+struct GroupDev {
+    int32_t kind, nslots;
+    int32_t dim[FG_MAX_SLOTS];
+    int64_t count;
+    const int32_t* svar[FG_MAX_SLOTS];   // slot variable id per factor
+    const int32_t* sk[FG_MAX_SLOTS];     // edge rank inside the variable
+    const double* fp;                    // per-factor params (AoS)
+    int32_t fstride, tstride;
+    const double* tab;                   // shared tables (mpc_dyn)
+    const int32_t* fsys;
+    int32_t ip;                          // integer param (mpc_dyn: state dim)
+};
+
+struct PassA {
+    VarTab vt;
+    const double* z;
+    const double* uin;
+    const double* nsrc;      // FIRST mode: materialized n (var-major)
+    double* x;
+    const double* rho;       // var-major edge weights
+    Ctrl* ctrl;
+};
+
+struct SlotLoc {
+    int64_t pos;             // first payload slot (var-major)
+    int64_t zo;              // z offset of the variable
+    int32_t q;               // var-major edge index
+};
+
+__device__ __forceinline__ SlotLoc locate(const VarTab& vt, const GroupDev& g,
+                                          int j, int64_t f) {
+    const int32_t v = g.svar[j][f];
+    const int32_t k = g.sk[j][f];
+    SlotLoc s;
+    s.pos = vt.pbase[v] + (int64_t)k * g.dim[j];
+    s.zo = vt.zbase[v];
+    s.q = vt.ebase[v] + k;
+    return s;
+}
+
+template <bool FIRST>
+__device__ __forceinline__ double nval(const PassA& a, const SlotLoc& s, int c,
+                                       bool& badn) {
+    if (FIRST) return a.nsrc[s.pos + c];
+    const double v = a.z[s.zo + c] - a.uin[s.pos + c];   // n = z[zmap] - u
+    badn |= !finite(v);
+    return v;
+}
+
+__device__ __forceinline__ void xput(const PassA& a, int64_t p, double v,
+                                     bool& badx) {
+    a.x[p] = v;
+    badx |= !finite(v);
+}
+
+template <bool FIRST>
+__device__ __forceinline__ void passa_flags(const PassA& a, int64_t it,
+                                            bool badn, bool badx) {
+    if (!FIRST && badn) flag_error(a.ctrl, it - 1, FG_PHASE_N, true);
+    if (badx) flag_error(a.ctrl, it, FG_PHASE_X, true);
+}
+
+// ---- collision: one thread per factor (operators.py:166-191) ------------
+template <bool FIRST>
+__global__ void __launch_bounds__(256) k_collision(PassA a, GroupDev g) {
+    if (a.ctrl->stop) return;
+    const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= g.count) return;
+    const int64_t it = a.ctrl->iter;
+    const SlotLoc s0 = locate(a.vt, g, 0, f), s1 = locate(a.vt, g, 1, f);
+    const SlotLoc s2 = locate(a.vt, g, 2, f), s3 = locate(a.vt, g, 3, f);
+    bool bn = false, bx = false;
+    const double n1c0 = nval<FIRST>(a, s0, 0, bn), n1c1 = nval<FIRST>(a, s0, 1, bn);
+    const double n1r = nval<FIRST>(a, s1, 0, bn);
+    const double n2c0 = nval<FIRST>(a, s2, 0, bn), n2c1 = nval<FIRST>(a, s2, 1, bn);
+    const double n2r = nval<FIRST>(a, s3, 0, bn);
+    double c10, c11, r1, c20, c21, r2;
+    prox_collision(n1c0, n1c1, n1r, n2c0, n2c1, n2r, a.rho[s0.q], a.rho[s1.q],
+                   a.rho[s2.q], a.rho[s3.q], c10, c11, r1, c20, c21, r2);
+    xput(a, s0.pos, c10, bx); xput(a, s0.pos + 1, c11, bx);
+    xput(a, s1.pos, r1, bx);
+    xput(a, s2.pos, c20, bx); xput(a, s2.pos + 1, c21, bx);
+    xput(a, s3.pos, r2, bx);
+    passa_flags<FIRST>(a, it, bn, bx);
+}
+
+// ---- wall: one thread per factor (operators.py:226-234) ----------------
+template <bool FIRST>
+__global__ void __launch_bounds__(256) k_wall(PassA a, GroupDev g) {
+    if (a.ctrl->stop) return;
+    const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= g.count) return;
+    const int64_t it = a.ctrl->iter;
+    const SlotLoc s0 = locate(a.vt, g, 0, f), s1 = locate(a.vt, g, 1, f);
+    bool bn = false, bx = false;
+    const double nc0 = nval<FIRST>(a, s0, 0, bn), nc1 = nval<FIRST>(a, s0, 1, bn);
+    const double nr = nval<FIRST>(a, s1, 0, bn);
+    const double* P = g.fp + f * g.fstride;   // Q0 Q1 V0 V1
+    double c0, c1, r;
+    prox_wall(nc0, nc1, nr, a.rho[s0.q], a.rho[s1.q], P[0], P[1], P[2], P[3],
+              c0, c1, r);
+    xput(a, s0.pos, c0, bx); xput(a, s0.pos + 1, c1, bx);
+    xput(a, s1.pos, r, bx);
+    passa_flags<FIRST>(a, it, bn, bx);
+}
+
+// ---- element-wise kinds: one thread per (factor, component) -------------
+// radius (operators.py:272-277), mpc_cost (:312-314), mpc_init (:349-354),
+// svm_slack (:439-441), svm_norm (:477-479), equality (:560-564),
+// nan_test (fault injector).
+template <int KIND, bool FIRST>
+__global__ void __launch_bounds__(256) k_elementwise(PassA a, GroupDev g) {
+    if (a.ctrl->stop) return;
+    const int D = g.dim[0];
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= g.count * D) return;
+    const int64_t f = t / D;
+    const int c = (int)(t - f * D);
+    const int64_t it = a.ctrl->iter;
+    const SlotLoc s0 = locate(a.vt, g, 0, f);
+    bool bn = false, bx = false;
+    const double n = nval<FIRST>(a, s0, c, bn);
+    const double* P = g.fp + f * g.fstride;
+    double out;
+    if (KIND == FG_KIND_RADIUS) {
+        out = prox_radius(n, a.rho[s0.q], P[0]);
+    } else if (KIND == FG_KIND_MPC_COST) {
+        out = prox_mpc_cost(n, a.rho[s0.q], P[c]);
+    } else if (KIND == FG_KIND_MPC_INIT) {
+        out = (c < g.fstride) ? P[c] : n;
+    } else if (KIND == FG_KIND_SVM_SLACK) {
+        out = prox_svm_slack(n, a.rho[s0.q], P[0]);
+    } else if (KIND == FG_KIND_SVM_NORM) {
+        out = prox_svm_norm(n, a.rho[s0.q], P[0]);
+    } else if (KIND == FG_KIND_NAN_TEST) {
+        out = (P[0] != 0.0) ? __longlong_as_double(0x7ff8000000000000ll) : n;
+    } else {  // FG_KIND_EQUALITY
+        const SlotLoc s1 = locate(a.vt, g, 1, f);
+        const double n2 = nval<FIRST>(a, s1, c, bn);
+        out = prox_equality(n, n2, a.rho[s0.q], a.rho[s1.q]);
+        xput(a, s1.pos + c, out, bx);
+    }
+    xput(a, s0.pos + c, out, bx);
+    passa_flags<FIRST>(a, it, bn, bx);
+}
+
+// ---- quadratic: one thread per factor, any slots (operators.py:131-135) -
+template <bool FIRST>
+__global__ void __launch_bounds__(256) k_quadratic(PassA a, GroupDev g) {
+    if (a.ctrl->stop) return;
+    const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= g.count) return;
+    const int64_t it = a.ctrl->iter;
+    const double* P = g.fp + f * g.fstride;   // per slot: targets, curvature
+    bool bn = false, bx = false;
+    int off = 0;
+    for (int j = 0; j < g.nslots; ++j) {
+        const SlotLoc s = locate(a.vt, g, j, f);
+        const double R = a.rho[s.q];
+        const int d = g.dim[j];
+        const double C = P[off + d];
+        for (int c = 0; c < d; ++c)
+            xput(a, s.pos + c, prox_quadratic(nval<FIRST>(a, s, c, bn), R, P[off + c], C), bx);
+        off += d + 1;
+    }
+    passa_flags<FIRST>(a, it, bn, bx);
+}
+
+// ---- svm_margin: one warp per factor (operators.py:515-525) -------------
+// Slots (w: D, b: 1, xi: 1); params x (D) then y.  The two D-dim dots use a
+// fixed xor-tree (deterministic; parity with NumPy's einsum is 1e-9 rel).
+constexpr int kMarginMaxPerLane = 4;   // D <= 128
+template <bool FIRST>
+__global__ void __launch_bounds__(256) k_svm_margin(PassA a, GroupDev g) {
+    if (a.ctrl->stop) return;
+    const int64_t f = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (f >= g.count) return;                 // warp-uniform
+    const int64_t it = a.ctrl->iter;
+    const int D = g.dim[0];
+    const SlotLoc s0 = locate(a.vt, g, 0, f), s1 = locate(a.vt, g, 1, f);
+    const SlotLoc s2 = locate(a.vt, g, 2, f);
+    const double* P = g.fp + f * g.fstride;
+    bool bn = false, bx = false;
+    double n1[kMarginMaxPerLane], X[kMarginMaxPerLane];
+    double dot = 0.0, xx = 0.0;
+#pragma unroll
+    for (int r = 0; r < kMarginMaxPerLane; ++r) {
+        const int c = lane + 32 * r;
+        n1[r] = 0.0; X[r] = 0.0;
+        if (c < D) {
+            n1[r] = nval<FIRST>(a, s0, c, bn);
+            X[r] = P[c];
+            dot += n1[r] * X[r];
+            xx += X[r] * X[r];
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        dot += __shfl_xor_sync(kFull, dot, o);
+        xx += __shfl_xor_sync(kFull, xx, o);
+    }
+    const double n2 = nval<FIRST>(a, s1, 0, bn), n3 = nval<FIRST>(a, s2, 0, bn);
+    const double R1 = a.rho[s0.q], R2 = a.rho[s1.q], R3 = a.rho[s2.q];
+    const double Y = P[D];
+    const double slack = (1.0 - n3) - Y * (dot + n2);
+    const double denom = (xx / R1 + 1.0 / R2) + 1.0 / R3;
+    const double mu = np_max0(slack) / denom;
+    const double tw = (mu / R1) * Y;
+#pragma unroll
+    for (int r = 0; r < kMarginMaxPerLane; ++r) {
+        const int c = lane + 32 * r;
+        if (c < D) xput(a, s0.pos + c, n1[r] + tw * X[r], bx);
+    }
+    if (lane == 0) {
+        xput(a, s1.pos, n2 + (mu / R2) * Y, bx);
+        xput(a, s2.pos, n3 + mu / R3, bx);
+    }
+    passa_flags<FIRST>(a, it, bn, bx);
+}
+
+// ---- mpc_dyn: one warp per factor (operators.py:86-96, 390-404) ---------
+// Weighted projection onto {M v = 0}, M = [I+A, B, -I] (d x (2d+k)).
+// With W = diag(rho0 on slot 0, rho1 on the first d of slot 1),
+// S = M W^-1 M^T = G/rho0 + I/rho1, G = QLQ^T precomputed per system, so
+// S^-1 = Q diag(1/(L/rho0 + 1/rho1)) Q^T (replaces the per-factor LAPACK
+// gesv; parity 1e-9 rel).  Table entry: M row-major, Q row-major, L.
+constexpr int kDynMaxD = 32, kDynMaxCols = 96;
+template <bool FIRST>
+__global__ void __launch_bounds__(128) k_mpc_dyn(PassA a, GroupDev g) {
+    __shared__ double s_nv[4][kDynMaxCols];
+    __shared__ double s_v1[4][kDynMaxD];
+    __shared__ double s_v2[4][kDynMaxD];
+    if (a.ctrl->stop) return;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t f = (int64_t)blockIdx.x * 4 + w;
+    if (f >= g.count) return;                 // warp-uniform
+    const int64_t it = a.ctrl->iter;
+    const int n0 = g.dim[0];
+    const SlotLoc s0 = locate(a.vt, g, 0, f), s1 = locate(a.vt, g, 1, f);
+    const double* T = g.tab + (int64_t)(g.fsys ? g.fsys[f] : 0) * g.tstride;
+    const int d = g.ip;                       // state dim
+    const int cols = n0 + d;                  // 2d + k
+    const double* M = T;
+    const double* Q = T + d * cols;
+    const double* L = Q + d * d;
+    bool bn = false, bx = false;
+    for (int c = lane; c < cols; c += 32)
+        s_nv[w][c] = (c < n0) ? nval<FIRST>(a, s0, c, bn)
+                              : nval<FIRST>(a, s1, c - n0, bn);
+    __syncwarp();
+    const double R0 = a.rho[s0.q], R1 = a.rho[s1.q];
+    if (lane < d) {                           // Mnv
+        double acc = 0.0;
+        for (int c = 0; c < cols; ++c) acc += M[lane * cols + c] * s_nv[w][c];
+        s_v1[w][lane] = acc;
+    }
+    __syncwarp();
+    if (lane < d) {                           // y = diag * Q^T Mnv
+        double acc = 0.0;
+        for (int r = 0; r < d; ++r) acc += Q[r * d + lane] * s_v1[w][r];
+        s_v2[w][lane] = acc / (L[lane] / R0 + 1.0 / R1);
+    }
+    __syncwarp();
+    if (lane < d) {                           // lambda = Q y
+        double acc = 0.0;
+        for (int i = 0; i < d; ++i) acc += Q[lane * d + i] * s_v2[w][i];
+        s_v1[w][lane] = acc;
+    }
+    __syncwarp();
+    for (int c = lane; c < cols; c += 32) {   // v = nv - W^-1 M^T lambda
+        double acc = 0.0;
+        for (int r = 0; r < d; ++r) acc += M[r * cols + c] * s_v1[w][r];
+        const double winv = 1.0 / ((c < n0) ? R0 : R1);
+        const double v = s_nv[w][c] - winv * acc;
+        if (c < n0) xput(a, s0.pos + c, v, bx);
+        else xput(a, s1.pos + (c - n0), v, bx);
+    }
+    for (int c = d + lane; c < n0; c += 32)   // slot-1 control passes through
+        xput(a, s1.pos + c, nval<FIRST>(a, s1, c, bn), bx);
+    passa_flags<FIRST>(a, it, bn, bx);
+}
+
+// ===========================================================================
+// Variable pass
+// ===========================================================================
+enum { MODE_FUSED = 0, MODE_PHASEZ = 1 };
+
+struct PassB {
+    VarTab vt;
+    const double* x;
+    const double* uin;
+    double* uout;
+    const double* msrc;      // PHASEZ: materialized m
+    double* z;
+    const double* rho;
+    const double* alpha;
+    const double* zw;
+    Ctrl* ctrl;
+    double* part;            // residual partials, 2 per slot
+    const int32_t* zvar;     // z component -> variable
+};
+
+struct CompRef {
+    int64_t pb;              // payload base of the variable
+    int32_t eb, deg, d, c;   // edge base, degree, dim, component
+};
+
+__device__ __forceinline__ CompRef comp_ref(const PassB& b, int32_t k) {
+    const int32_t v = b.zvar[k];
+    CompRef r;
+    r.pb = b.vt.pbase[v];
+    r.eb = b.vt.ebase[v];
+    r.deg = b.vt.deg[v];
+    r.d = b.vt.dim[v];
+    r.c = (int32_t)(k - b.vt.zbase[v]);
+    return r;
+}
+
+template <int MODE>
+struct ValFn {
+    const double* x;
+    const double* u;         // FUSED: u_in;  PHASEZ: materialized m
+    const double* rho;
+    CompRef r;
+    bool* badm;
+    __device__ __forceinline__ ValFn(const PassB& b, const CompRef& rr, bool* bm)
+        : x(b.x), u(MODE == MODE_FUSED ? b.uin : b.msrc), rho(b.rho), r(rr),
+          badm(bm) {}
+    __device__ __forceinline__ double operator()(int64_t e) const {
+        const int64_t p = r.pb + e * r.d + r.c;
+        double m;
+        if (MODE == MODE_FUSED) {
+            m = x[p] + u[p];                         // phase m
+            *badm |= !finite(m);
+        } else {
+            m = u[p];
+        }
+        return m * rho[r.eb + e];                    // engine.py:278
+    }
+};
+
+// u update + residual partials for elements [e0, e1) of one component.
+__device__ __forceinline__ void update_range(const PassB& b, const CompRef& r,
+                                             int64_t e0, int64_t e1,
+                                             int64_t step, double zn, double zo,
+                                             double& pp, double& dd, bool& badu) {
+    const double dz = zn - zo;
+    for (int64_t e = e0; e < e1; e += step) {
+        const int64_t p = r.pb + e * r.d + r.c;
+        const double xv = b.x[p];
+        const double t = xv - zn;                    // engine.py:288
+        pp += t * t;                                 // engine.py:402
+        const double rd = b.rho[r.eb + e] * dz;      // engine.py:403-405
+        dd += rd * rd;
+        const double un = b.uin[p] + t * b.alpha[r.eb + e];   // :289-290
+        b.uout[p] = un;
+        badu |= !finite(un);
+    }
+}
+
+// Class S: degree <= 32.  One thread per z component; the tail a[1:] is a
+// single NumPy leaf, summed sequentially.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_var_small(PassB b, const int32_t* list,
+                                                   int64_t n, int64_t part_off) {
+    __shared__ double sm[16];
+    __shared__ int s_stop;
+    if (threadIdx.x == 0) s_stop = b.ctrl->stop;
+    __syncthreads();
+    if (s_stop) return;
+    const int64_t it = b.ctrl->iter;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double pp = 0.0, dd = 0.0;
+    if (t < n) {
+        const int32_t k = list[t];
+        const CompRef r = comp_ref(b, k);
+        bool bm = false, bz = false, bu = false;
+        ValFn<MODE> val(b, r, &bm);
+        double S = val(0);                           // reduceat: a[0] + tree
+        if (r.deg > 1) S = S + leaf_seq(val, 1, r.deg - 1);
+        const double zn = S / b.zw[k];
+        bz = !finite(zn);
+        if (MODE == MODE_FUSED) {
+            const double zo = b.z[k];
+            b.z[k] = zn;
+            update_range(b, r, 0, r.deg, 1, zn, zo, pp, dd, bu);
+            if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
+            if (bz) flag_error(b.ctrl, it, FG_PHASE_Z, false);
+            if (bu) flag_error(b.ctrl, it, FG_PHASE_U, false);
+        } else {
+            b.z[k] = zn;
+        }
+    }
+    if (MODE == MODE_FUSED) {
+        block_sum2<256>(pp, dd, sm);
+        if (threadIdx.x == 0) {
+            b.part[2 * (part_off + blockIdx.x)] = pp;
+            b.part[2 * (part_off + blockIdx.x) + 1] = dd;
+        }
+    }
+}
+
+// Tree program layout (int32): [nu, nlev, units(2*nu: start,len),
+// level_cnt(nlev), ops(2*(nu-1): a,b)].  Node ids: units 0..nu-1, then
+// internal nodes in level order; the root is the last node.
+constexpr int kVarThreads = 256;
+constexpr int kMaxUnits = 160;          // chunk <= 8192 -> <= 128 leaves
+
+template <class F>
+__device__ __forceinline__ double run_units_and_tree(F val, int64_t base_elem,
+                                                     const int32_t* P,
+                                                     double* sv) {
+    const int nu = P[0], nlev = P[1];
+    const int32_t* units = P + 2;
+    const int32_t* lev = units + 2 * nu;
+    const int32_t* ops = lev + nlev;
+    const int g = threadIdx.x >> 3, j = threadIdx.x & 7;
+    constexpr int NG = kVarThreads / 8;
+    for (int r0 = 0; r0 < nu; r0 += NG) {
+        const int L = r0 + g;
+        int64_t s = 0, len = 0;
+        if (L < nu) { s = units[2 * L]; len = units[2 * L + 1]; }
+        const double res = leaf_group8(val, base_elem + s, len, j);
+        if (L < nu && j == 0) sv[L] = res;
+    }
+    __syncthreads();
+    int node = nu, op = 0;
+    for (int l = 0; l < nlev; ++l) {
+        const int cnt = lev[l];
+        for (int o = threadIdx.x; o < cnt; o += kVarThreads)
+            sv[node + o] = sv[ops[2 * (op + o)]] + sv[ops[2 * (op + o) + 1]];
+        __syncthreads();
+        node += cnt;
+        op += cnt;
+    }
+    return sv[node - 1];
+}
+
+// Class L: 32 < degree <= chunk+1.  One CTA per z component: leaves by
+// 8-lane groups, level-ordered combine in shared memory, then z and the
+// u update of the whole segment.
+template <int MODE>
+__global__ void __launch_bounds__(kVarThreads) k_var_large(
+    PassB b, const int32_t* list, const int32_t* progoff, const int32_t* prog,
+    int64_t part_off) {
+    __shared__ double sv[2 * kMaxUnits];
+    __shared__ double sm[16];
+    __shared__ double s_z[2];
+    __shared__ int s_stop;
+    if (threadIdx.x == 0) s_stop = b.ctrl->stop;
+    __syncthreads();
+    if (s_stop) return;
+    const int64_t it = b.ctrl->iter;
+    const int32_t k = list[blockIdx.x];
+    const CompRef r = comp_ref(b, k);
+    bool bm = false, bz = false, bu = false;
+    ValFn<MODE> val(b, r, &bm);
+    const double T = run_units_and_tree(val, 1, prog + progoff[blockIdx.x], sv);
+    if (threadIdx.x == 0) {
+        const double zn = (val(0) + T) / b.zw[k];
+        bz = !finite(zn);
+        s_z[0] = zn;
+        s_z[1] = (MODE == MODE_FUSED) ? b.z[k] : 0.0;
+        b.z[k] = zn;
+    }
+    __syncthreads();
+    double pp = 0.0, dd = 0.0;
+    if (MODE == MODE_FUSED) {
+        update_range(b, r, threadIdx.x, r.deg, kVarThreads, s_z[0], s_z[1], pp, dd, bu);
+        if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
+        if (bz) flag_error(b.ctrl, it, FG_PHASE_Z, false);
+        if (bu) flag_error(b.ctrl, it, FG_PHASE_U, false);
+        block_sum2<kVarThreads>(pp, dd, sm);
+        if (threadIdx.x == 0) {
+            b.part[2 * (part_off + blockIdx.x)] = pp;
+            b.part[2 * (part_off + blockIdx.x) + 1] = dd;
+        }
+    }
+}
+
+// Class G (degree > chunk+1), three kernels.
+// G1: one CTA per chunk (a maximal pairwise subtree of <= chunk items).
+struct GChunk { int32_t gi, start, progoff, pad; };
+template <int MODE>
+__global__ void __launch_bounds__(kVarThreads) k_var_giant_chunks(
+    PassB b, const int32_t* glist, const GChunk* chunks, const int32_t* prog,
+    double* csum) {
+    __shared__ double sv[2 * kMaxUnits];
+    __shared__ int s_stop;
+    if (threadIdx.x == 0) s_stop = b.ctrl->stop;
+    __syncthreads();
+    if (s_stop) return;
+    const int64_t it = b.ctrl->iter;
+    const GChunk ch = chunks[blockIdx.x];
+    const CompRef r = comp_ref(b, glist[ch.gi]);
+    bool bm = false;
+    ValFn<MODE> val(b, r, &bm);
+    const double T = run_units_and_tree(val, 1 + (int64_t)ch.start, prog + ch.progoff, sv);
+    if (threadIdx.x == 0) csum[blockIdx.x] = T;
+    if (MODE == MODE_FUSED && bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
+}
+
+// G2: one CTA per giant component: combine chunk sums along the top of the
+// tree (program whose units are chunks), then z.
+struct GComp { int32_t topoff, cbase, pad0, pad1; };
+template <int MODE>
+__global__ void __launch_bounds__(kVarThreads) k_var_giant_top(
+    PassB b, const int32_t* glist, const GComp* comps, const int32_t* prog,
+    const double* csum, double* gz) {
+    extern __shared__ double sv[];
+    __shared__ int s_stop;
+    if (threadIdx.x == 0) s_stop = b.ctrl->stop;
+    __syncthreads();
+    if (s_stop) return;
+    const int64_t it = b.ctrl->iter;
+    const GComp gc = comps[blockIdx.x];
+    const int32_t k = glist[blockIdx.x];
+    const int32_t* P = prog + gc.topoff;
+    const int nu = P[0], nlev = P[1];
+    const int32_t* lev = P + 2 + 2 * nu;
+    const int32_t* ops = lev + nlev;
+    for (int u = threadIdx.x; u < nu; u += kVarThreads) sv[u] = csum[gc.cbase + u];
+    __syncthreads();
+    int node = nu, op = 0;
+    for (int l = 0; l < nlev; ++l) {
+        const int cnt = lev[l];
+        for (int o = threadIdx.x; o < cnt; o += kVarThreads)
+            sv[node + o] = sv[ops[2 * (op + o)]] + sv[ops[2 * (op + o) + 1]];
+        __syncthreads();
+        node += cnt;
+        op += cnt;
+    }
+    if (threadIdx.x == 0) {
+        const CompRef r = comp_ref(b, k);
+        bool bm = false;
+        ValFn<MODE> val(b, r, &bm);
+        const double zn = (val(0) + sv[node - 1]) / b.zw[k];
+        gz[2 * blockIdx.x] = zn;
+        gz[2 * blockIdx.x + 1] = (MODE == MODE_FUSED) ? b.z[k] : 0.0;
+        b.z[k] = zn;
+        if (MODE == MODE_FUSED) {
+            if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
+            if (!finite(zn)) flag_error(b.ctrl, it, FG_PHASE_Z, false);
+        }
+    }
+}
+
+// G3: u update of giant components, one CTA per element range.
+struct GWork { int32_t gi, e0, e1, pad; };
+__global__ void __launch_bounds__(kVarThreads) k_var_giant_update(
+    PassB b, const int32_t* glist, const GWork* work, const double* gz,
+    int64_t part_off) {
+    __shared__ double sm[16];
+    __shared__ int s_stop;
+    if (threadIdx.x == 0) s_stop = b.ctrl->stop;
+    __syncthreads();
+    if (s_stop) return;
+    const int64_t it = b.ctrl->iter;
+    const GWork wk = work[blockIdx.x];
+    const CompRef r = comp_ref(b, glist[wk.gi]);
+    double pp = 0.0, dd = 0.0;
+    bool bu = false;
+    update_range(b, r, wk.e0 + threadIdx.x, wk.e1, kVarThreads, gz[2 * wk.gi],
+                 gz[2 * wk.gi + 1], pp, dd, bu);
+    if (bu) flag_error(b.ctrl, it, FG_PHASE_U, false);
+    block_sum2<kVarThreads>(pp, dd, sm);
+    if (threadIdx.x == 0) {
+        b.part[2 * (part_off + blockIdx.x)] = pp;
+        b.part[2 * (part_off + blockIdx.x) + 1] = dd;
+    }
+}
+
+// Residuals, tolerance stop and iteration bookkeeping (engine.py:502-516).
+__global__ void __launch_bounds__(1024) k_reduce(Ctrl* c, const double* part,
+                                                 int64_t npart, double* hist) {
+    __shared__ double sm[64];
+    __shared__ int s_stop;
+    if (threadIdx.x == 0) s_stop = c->stop;
+    __syncthreads();
+    if (s_stop) return;
+    double a = 0.0, bsum = 0.0;
+    for (int64_t i = threadIdx.x; i < npart; i += 1024) {
+        a += part[2 * i];
+        bsum += part[2 * i + 1];
+    }
+    block_sum2<1024>(a, bsum, sm);
+    if (threadIdx.x == 0) {
+        const int64_t it = c->iter;
+        const double primal = sqrt(a) * c->scale;
+        const double dual = sqrt(bsum) * c->scale;
+        c->primal = primal;
+        c->dual = dual;
+        if (hist) { hist[2 * (it - 1)] = primal; hist[2 * (it - 1) + 1] = dual; }
+        c->completed = it;
+        if (c->err_key != ~0ull) {
+            c->stop = 1;
+        } else {
+            const bool pc = c->primal_tol > 0.0, dc = c->dual_tol > 0.0;
+            bool ok = pc || dc;
+            if (pc) ok = ok && (primal <= c->primal_tol);
+            if (dc) ok = ok && (dual <= c->dual_tol);
+            if (ok) { c->converged = 1; c->stop = 1; }
+        }
+        c->iter = it + 1;
+    }
+}
+
+// ===========================================================================
+// Layout conversion, unfused phases, host-API residuals
+// ===========================================================================
+
+// dst[p] = src_ref[vm2ref[p]]      (reference order -> var-major)
+__global__ void k_gather_from_ref(int64_t P, const int64_t* vm2ref,
+                                  const double* src_ref, double* dst) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < P) dst[p] = src_ref[vm2ref[p]];
+}
+
+// dst_ref[vm2ref[p]] = f(p):  0 x, 1 x + uprev (m), 2 ucur, 3 z - ucur (n)
+__global__ void k_scatter_to_ref(int64_t P, const int64_t* vm2ref,
+                                 const int32_t* vmz, int mode, const double* x,
+                                 const double* ucur, const double* uprev,
+                                 const double* z, double* dst_ref) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    double v;
+    if (mode == 0) v = x[p];
+    else if (mode == 1) v = x[p] + uprev[p];
+    else if (mode == 2) v = ucur[p];
+    else v = z[vmz[p]] - ucur[p];
+    dst_ref[vm2ref[p]] = v;
+}
+
+// edge-indexed gather: dst[q] = src_ref[ref_edge[q]]
+__global__ void k_gather_edges(int64_t E, const int32_t* ref_edge,
+                               const double* src_ref, double* dst) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < E) dst[q] = src_ref[ref_edge[q]];
+}
+
+// phase m (engine.py:263-265): m = x + u
+__global__ void k_phase_m(int64_t P, const double* x, const double* u, double* m) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < P) m[p] = x[p] + u[p];
+}
+
+// phase n (engine.py:292-298): n = z[zmap] - u
+__global__ void k_phase_n(int64_t P, const int32_t* vmz, const double* z,
+                          const double* u, double* n) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < P) n[p] = z[vmz[p]] - u[p];
+}
+
+// phase u (engine.py:282-290) one thread per var-major edge
+__global__ void k_phase_u(int64_t E, VarTab vt, const int32_t* vm_var,
+                          const double* x, const double* z,
+                          const double* alpha, double* u) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= E) return;
+    const int32_t v = vm_var[q];
+    const int d = vt.dim[v];
+    const int64_t p0 = vt.pbase[v] + (q - vt.ebase[v]) * (int64_t)d;
+    const int64_t z0 = vt.zbase[v];
+    const double al = alpha[q];
+    for (int c = 0; c < d; ++c) u[p0 + c] = u[p0 + c] + (x[p0 + c] - z[z0 + c]) * al;
+}
+
+// residuals (engine.py:398-406) on an explicit z_prev; per-block partials
+__global__ void __launch_bounds__(256) k_residual_parts(
+    int64_t E, VarTab vt, const int32_t* vm_var, const double* x,
+    const double* z, const double* zprev, const double* rho, double* part) {
+    __shared__ double sm[16];
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double pp = 0.0, dd = 0.0;
+    if (q < E) {
+        const int32_t v = vm_var[q];
+        const int d = vt.dim[v];
+        const int64_t p0 = vt.pbase[v] + (q - vt.ebase[v]) * (int64_t)d;
+        const int64_t z0 = vt.zbase[v];
+        for (int c = 0; c < d; ++c) {
+            const double t = x[p0 + c] - z[z0 + c];
+            pp += t * t;
+            const double r = rho[q] * (z[z0 + c] - zprev[z0 + c]);
+            dd += r * r;
+        }
+    }
+    block_sum2<256>(pp, dd, sm);
+    if (threadIdx.x == 0) { part[2 * blockIdx.x] = pp; part[2 * blockIdx.x + 1] = dd; }
+}
+
+__global__ void __launch_bounds__(1024) k_sum_parts(const double* part,
+                                                    int64_t npart, double* out2) {
+    __shared__ double sm[64];
+    double a = 0.0, bsum = 0.0;
+    for (int64_t i = threadIdx.x; i < npart; i += 1024) {
+        a += part[2 * i];
+        bsum += part[2 * i + 1];
+    }
+    block_sum2<1024>(a, bsum, sm);
+    if (threadIdx.x == 0) { out2[0] = a; out2[1] = bsum; }
+}
+
+}  // namespace fg

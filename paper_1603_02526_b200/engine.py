@@ -1,0 +1,535 @@
+"""Five-phase consensus iteration on a B200 (drop-in for ``fgadmm.engine``).
+
+Same entry points, dataclasses, error types and messages as the reference
+engine (``fgadmm/engine.py``); the iteration itself runs in
+``libfgadmm_b200.so``:
+
+* ``run`` flattens the graph once per graph into a device plan (cached
+  like ``engine.py:192-210``), re-syncs rho/alpha/z_weights on entry,
+  uploads the caller's state, runs the fused edge-pass / variable-pass
+  kernels for the whole iteration budget inside CUDA graphs with the
+  tolerance stop evaluated on the device, and writes the final state back
+  into the caller's arrays (state is mutated in place, ``iteration``
+  accumulates, as in the reference).
+* ``update_x`` .. ``update_n`` / ``iterate`` run one unfused device kernel
+  per phase so every intermediate array is observable (the reference's
+  exact-arithmetic trace drives these).
+* Consensus sums replay NumPy's pairwise ``reduceat`` tree, element-wise
+  ops round exactly like NumPy, so packing, MPC-cost, equality and
+  quadratic graphs are bit-identical to the reference; SVM margins
+  (32-dim dots) and MPC dynamics (closed-form instead of LAPACK) match to
+  ~1e-12 relative.
+
+``RunConfig.workers`` is accepted and validated but has no effect (one
+GPU executes the whole graph).  Two optional fields extend the config:
+``profile`` (per-kernel CUDA-event timing with direct launches) and
+``graph_chunk`` (iterations per CUDA-graph launch).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import weakref
+from dataclasses import dataclass, field
+from time import perf_counter
+
+import numpy as np
+
+from . import _native
+from .prox import operator_class
+
+PHASES = ("x", "m", "z", "u", "n")
+
+METRICS_HEADER = "iter,t_x,t_m,t_z,t_u,t_n,primal,dual"
+
+
+@dataclass
+class AdmmState:
+    """The five working arrays plus progress counters (payload arrays in
+    edge-creation order, ``z`` in variable order)."""
+
+    x: np.ndarray
+    m: np.ndarray
+    z: np.ndarray
+    u: np.ndarray
+    n: np.ndarray
+    iteration: int = 0
+    last_residuals: tuple | None = None
+
+
+@dataclass
+class RunConfig:
+    """Iteration budget, stopping tolerances and execution settings.
+
+    A tolerance of 0 disables that check; ``seed`` None starts from
+    zeros, an integer draws z and u from U[-0.5, 0.5].
+    """
+
+    max_iterations: int
+    primal_tol: float = 0.0
+    dual_tol: float = 0.0
+    workers: int = 1
+    record_every: int = 1
+    seed: int | None = None
+    profile: bool = False
+    graph_chunk: int = 16
+
+
+@dataclass
+class RunReport:
+    """Execution record: per-phase device time and residual history."""
+
+    iterations: int
+    converged: bool
+    workers: int
+    phase_seconds: dict
+    history: list = field(default_factory=list)
+    total_seconds: float = 0.0
+    device_seconds: float = 0.0
+    kernel_launches: int = 0
+
+    def mean_phase_seconds(self):
+        it = max(self.iterations, 1)
+        return {k: v / it for k, v in self.phase_seconds.items()}
+
+    def time_per_iteration(self):
+        return sum(self.phase_seconds.values()) / max(self.iterations, 1)
+
+    def metrics_csv(self):
+        lines = [METRICS_HEADER]
+        for row in self.history:
+            it, *rest = row
+            lines.append(",".join([str(int(it))] + [repr(float(v)) for v in rest]))
+        return "\n".join(lines) + "\n"
+
+
+def init_state(graph, seed=None):
+    """Fresh state: zeros, or z then u drawn from one seeded stream
+    (reference ``engine.py:99-110``; host RNG so draws are identical)."""
+    P = graph.total_edge_payload
+    if seed is None:
+        z = np.zeros(graph.z_dim)
+        u = np.zeros(P)
+    else:
+        rng = np.random.default_rng(seed)
+        z = rng.uniform(-0.5, 0.5, graph.z_dim)
+        u = rng.uniform(-0.5, 0.5, P)
+    n = z[graph.zmap] - u
+    return AdmmState(x=np.zeros(P), m=np.zeros(P), z=z, u=u, n=n)
+
+
+# ---------------------------------------------------------------------------
+# device plan
+
+def _device_id():
+    for key in ("FGADMM_DEVICE", "LOCAL_RANK"):
+        if key in os.environ:
+            return int(os.environ[key])
+    return 0
+
+
+def _group_specs(graph):
+    """(kind class, slot dims, first edges, DeviceParams, check info) per
+    (kind, slot dims) group in first-appearance order (engine.py:169-181)."""
+    order, members = [], {}
+    if hasattr(graph, "_blocks") and hasattr(graph, "factor_first_edges"):
+        for bi, (cls, dims, _f0, _vars, params) in enumerate(graph.blocks):
+            key = (cls.kind, tuple(dims))
+            if key not in members:
+                members[key] = []
+                order.append(key)
+            members[key].append((cls, graph.factor_first_edges(bi), params))
+    else:   # a reference-package FactorGraph: pack its operator instances
+        insts = {}
+        for f in graph.factors:
+            op = f.operator
+            key = (op.kind, tuple(op.slot_dims()))
+            if key not in insts:
+                insts[key] = ([], [])
+                order.append(key)
+            insts[key][0].append(op)
+            insts[key][1].append(f.edge_range[0])
+        for key in order:
+            cls = operator_class(key[0])
+            ops, fe = insts[key]
+            members[key] = [(cls, np.asarray(fe, dtype=np.int64), cls.stack_params(ops))]
+    specs = []
+    for key in order:
+        cls = members[key][0][0]
+        if cls.device_kind is None:
+            raise NotImplementedError(f"operator kind '{key[0]}' has no device kernel")
+        parts = [(fe, cls.device_params(params, key[1]), params)
+                 for _c, fe, params in members[key]]
+        fe = np.concatenate([p[0] for p in parts]).astype(np.int64)
+        dp = _merge_device_params([p[1] for p in parts])
+        specs.append((cls, key[1], fe, dp, [p[2] for p in parts], [len(p[0]) for p in parts]))
+    return specs
+
+
+def _merge_device_params(dps):
+    if len(dps) == 1:
+        return dps[0]
+    from .prox import DeviceParams
+    fp = None if dps[0].fparams is None else np.vstack([d.fparams for d in dps])
+    tables, fsys = None, None
+    if dps[0].tables is not None:
+        tables = np.vstack([d.tables for d in dps])
+        offs = np.cumsum([0] + [len(d.tables) for d in dps[:-1]])
+        fsys = np.concatenate([np.asarray(d.fsys, dtype=np.int64) + o
+                               for d, o in zip(dps, offs)]).astype(np.int32)
+    ip = {d.iparam for d in dps}
+    if len(ip) != 1:
+        raise NotImplementedError("one kind group mixes incompatible dimensions")
+    return DeviceParams(fp, tables, fsys, ip.pop())
+
+
+class DevicePlan:
+    """A graph flattened onto one GPU (owns the C-ABI ``fg_plan``)."""
+
+    def __init__(self, graph, device=None, chunk=0, small_degree=0):
+        lib = _native.load()
+        self.device = _device_id() if device is None else int(device)
+        self.P = int(graph.total_edge_payload)
+        self.Z = int(graph.z_dim)
+        self._graph_ref = weakref.ref(graph)
+        self.groups = _group_specs(graph)
+        dims = np.diff(np.asarray(graph.var_offsets, dtype=np.int64)).astype(np.int32)
+        keep = [dims]
+        gd = _native.GraphDesc()
+        gd.num_vars = len(dims)
+        gd.num_edges = len(graph.edge_var)
+        gd.payload = self.P
+        gd.z_dim = self.Z
+        gd.var_dim = _native.i32ptr(dims)
+        vo = np.ascontiguousarray(graph.var_offsets, dtype=np.int64)
+        ev = np.ascontiguousarray(graph.edge_var, dtype=np.int32)
+        eo = np.ascontiguousarray(graph.edge_offsets, dtype=np.int64)
+        keep += [vo, ev, eo]
+        gd.var_offsets = _native.i64ptr(vo)
+        gd.edge_var = _native.i32ptr(ev)
+        gd.edge_offsets = _native.i64ptr(eo)
+        gd.chunk = int(chunk)
+        gd.small_degree = int(small_degree)
+        descs = (_native.GroupDesc * max(1, len(self.groups)))()
+        for i, (cls, dims_k, fe, dp, _params, _sizes) in enumerate(self.groups):
+            descs[i] = _native.make_group_desc(cls.device_kind, dims_k, len(fe), fe, dp, keep)
+        handle = C.c_void_p()
+        _native.check(lib.fg_plan_create(C.byref(gd), descs, len(self.groups),
+                                         self.device, C.byref(handle)))
+        self._h = handle
+        info = (C.c_int64 * 9)()
+        lib.fg_plan_info(self._h, info)
+        self.info = {"V": info[0], "E": info[1], "P": info[2], "Z": info[3],
+                     "small_components": info[4], "large_components": info[5],
+                     "giant_components": info[6], "giant_chunks": info[7],
+                     "launches_per_iteration": info[8]}
+        self._synced_version = None
+        self._lib = lib
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                self._lib.fg_plan_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    # -- parameters -----------------------------------------------------------
+    def host_checks(self, graph):
+        """Kind validations the reference raises from batch_eval
+        (radius rho > kappa, injected failures)."""
+        for cls, dims, fe, _dp, params_list, sizes in self.groups:
+            off = 0
+            for params, sz in zip(params_list, sizes):
+                rhos = [graph.edge_rho[fe[off:off + sz] + j] for j in range(len(dims))]
+                bad = cls.host_check(params, rhos)
+                if bad is not None:
+                    row, msg = bad
+                    fid = int(graph.edge_factor[fe[off + row]])
+                    raise RuntimeError(f"prox evaluation failed for factor {fid} "
+                                       f"(kind '{cls.kind}'): {msg}")
+                off += sz
+
+    def sync(self, graph):
+        version = getattr(graph, "param_version", None)
+        if version is not None and version == self._synced_version:
+            return
+        rho = _native.f64(graph.edge_rho)
+        alpha = _native.f64(graph.edge_alpha)
+        zw = _native.f64(graph.z_weights)
+        _native.check(self._lib.fg_plan_sync_params(self._h, _native.dptr(rho),
+                                                    _native.dptr(alpha), _native.dptr(zw)))
+        self._synced_version = version
+
+    # -- fused run --------------------------------------------------------------
+    def upload(self, z, u, n):
+        z, u, n = _native.f64(z), _native.f64(u), _native.f64(n)
+        _native.check(self._lib.fg_state_upload(self._h, _native.dptr(z),
+                                                _native.dptr(u), _native.dptr(n)))
+
+    def run(self, iterations, primal_tol=0.0, dual_tol=0.0, first_reads_n=True,
+            timing=False, graph_chunk=16):
+        cfg = _native.RunConfig()
+        cfg.max_iterations = int(iterations)
+        cfg.primal_tol = float(primal_tol)
+        cfg.dual_tol = float(dual_tol)
+        cfg.first_reads_n = 1 if first_reads_n else 0
+        cfg.timing = 1 if timing else 0
+        cfg.graph_chunk = int(graph_chunk)
+        res = _native.RunResult()
+        hist = np.zeros(2 * int(iterations))
+        _native.check(self._lib.fg_run(self._h, C.byref(cfg), _native.dptr(hist),
+                                       C.byref(res)))
+        return res, hist.reshape(-1, 2)[:res.iterations]
+
+    def download(self, x=None, m=None, z=None, u=None, n=None):
+        outs = [x, m, z, u, n]
+        for a in outs:
+            if a is not None and not (a.dtype == np.float64 and a.flags.c_contiguous):
+                raise ValueError("state arrays must be C-contiguous float64")
+        _native.check(self._lib.fg_state_download(
+            self._h, *[_native.dptr(a) if a is not None else None for a in outs]))
+
+    def debug_buffer(self, which):
+        out = np.empty(self.P)
+        _native.check(self._lib.fg_debug_download(self._h, int(which), _native.dptr(out)))
+        return out
+
+    # -- unfused per-phase path -------------------------------------------------
+    def phase_upload(self, state):
+        arrs = [_native.f64(getattr(state, k)) for k in ("x", "m", "z", "u", "n")]
+        _native.check(self._lib.fg_phase_upload(self._h, *[_native.dptr(a) for a in arrs]))
+
+    def phase(self, name):
+        _native.check(self._lib.fg_phase(self._h, _native.PHASE_IDS[name]))
+
+    def phase_download(self, state, names):
+        outs = {}
+        for k in ("x", "m", "z", "u", "n"):
+            if k in names:
+                outs[k] = np.empty_like(getattr(state, k), dtype=np.float64)
+        _native.check(self._lib.fg_phase_download(
+            self._h, *[_native.dptr(outs.get(k)) for k in ("x", "m", "z", "u", "n")]))
+        for k, v in outs.items():
+            getattr(state, k)[...] = v
+
+    def residuals(self, x, z, z_prev):
+        x, z, zp = _native.f64(x), _native.f64(z), _native.f64(z_prev)
+        p, d = C.c_double(), C.c_double()
+        _native.check(self._lib.fg_residuals(self._h, _native.dptr(x), _native.dptr(z),
+                                             _native.dptr(zp), C.byref(p), C.byref(d)))
+        return float(p.value), float(d.value)
+
+
+_PLANS = weakref.WeakKeyDictionary()
+
+
+def device_plan(graph):
+    """The cached device plan of ``graph`` (built on first use)."""
+    plan = _PLANS.get(graph)
+    if plan is None:
+        plan = DevicePlan(graph)
+        _PLANS[graph] = plan
+    return plan
+
+
+# ---------------------------------------------------------------------------
+# checks (reference engine.py:323-350)
+
+def _check_state(graph, state):
+    P = graph.total_edge_payload
+    for name in ("x", "m", "u", "n"):
+        if getattr(state, name).shape != (P,):
+            raise ValueError(f"state.{name} must have shape ({P},)")
+    if state.z.shape != (graph.z_dim,):
+        raise ValueError(f"state.z must have shape ({graph.z_dim},)")
+
+
+def _nonfinite_message(graph, arr, phase, iteration):
+    bad = np.nonzero(~np.isfinite(arr))[0]
+    if bad.size == 0:
+        return None
+    first = int(bad[0])
+    if phase == "z":
+        v = int(np.searchsorted(graph.var_offsets, first, side="right") - 1)
+        return f"non-finite value after z update at iteration {iteration}: variable {v}"
+    e = int(np.searchsorted(graph.edge_offsets, first, side="right") - 1)
+    f = int(graph.edge_factor[e])
+    kind = graph.factors[f].operator.kind
+    return (f"non-finite value after {phase} update at iteration {iteration}: "
+            f"edge {e} of factor {f} (kind '{kind}')")
+
+
+def _check_finite(graph, state, phase, iteration):
+    arr = state.z if phase == "z" else getattr(state, phase)
+    msg = _nonfinite_message(graph, arr, phase, iteration)
+    if msg:
+        raise RuntimeError(msg)
+
+
+def _assign(dst, src):
+    dst[...] = src
+
+
+# ---------------------------------------------------------------------------
+# per-phase API (reference engine.py:353-395)
+
+def _phase_call(graph, state, name):
+    _check_state(graph, state)
+    plan = device_plan(graph)
+    if name == "x":
+        plan.host_checks(graph)
+    plan.sync(graph)
+    plan.phase_upload(state)
+    plan.phase(name)
+    plan.phase_download(state, (name,))
+    _check_finite(graph, state, name, state.iteration)
+
+
+def update_x(graph, state):
+    """Per factor, write the prox of its incoming n values into x."""
+    _phase_call(graph, state, "x")
+
+
+def update_m(graph, state):
+    """Per edge, m = x + u."""
+    _phase_call(graph, state, "m")
+
+
+def update_z(graph, state):
+    """Per variable, z = weighted average of incident m values."""
+    _phase_call(graph, state, "z")
+
+
+def update_u(graph, state):
+    """Per edge, u += alpha (x - z)."""
+    _phase_call(graph, state, "u")
+
+
+def update_n(graph, state):
+    """Per edge, n = z - u."""
+    _phase_call(graph, state, "n")
+
+
+def iterate(graph, state):
+    """Apply the five updates in order (one upload, one kernel per phase)
+    and advance the counter."""
+    _check_state(graph, state)
+    plan = device_plan(graph)
+    plan.host_checks(graph)
+    plan.sync(graph)
+    plan.phase_upload(state)
+    for name in PHASES:
+        plan.phase(name)
+        plan.phase_download(state, (name,))
+        _check_finite(graph, state, name, state.iteration)
+    state.iteration += 1
+
+
+def residuals(graph, state, z_prev):
+    """Size-normalized consensus disagreement and weighted z change
+    (reference ``engine.py:398-406``), reduced on the device."""
+    plan = device_plan(graph)
+    plan.sync(graph)
+    return plan.residuals(state.x, state.z, z_prev)
+
+
+# ---------------------------------------------------------------------------
+# fused run (reference engine.py:454-531)
+
+def _raise_device_error(graph, plan, state, res):
+    """Reproduce the reference's first-failure message from device state."""
+    phase = _native.PHASE_NAMES[res.error_phase]
+    it = int(res.error_iteration)
+    x = plan.debug_buffer(_native.BUF_X)
+    cur = plan.debug_buffer(_native.BUF_U0 if ((it - 1) & 1) == 0 else _native.BUF_U1)
+    nxt = plan.debug_buffer(_native.BUF_U1 if ((it - 1) & 1) == 0 else _native.BUF_U0)
+    z = np.empty(plan.Z)
+    plan.download(z=z)
+    if phase == "x":
+        arr = x
+    elif phase == "m":
+        arr = x + cur
+    elif phase == "z":
+        arr = z
+    elif phase == "u":
+        arr = nxt
+    else:   # n of iteration it: z_it - u_it
+        arr = z[graph.zmap] - nxt
+    msg = _nonfinite_message(graph, arr, phase, it)
+    if msg is None:   # device flag without a host-visible culprit
+        msg = f"non-finite value after {phase} update at iteration {it}"
+    state.iteration += max(0, int(res.iterations))
+    raise RuntimeError(msg)
+
+
+def run(graph, config, state=None):
+    """Iterate to the budget or tolerances; return (solution, report)."""
+    if config.max_iterations < 1:
+        raise ValueError("max_iterations must be >= 1")
+    if config.workers < 1:
+        raise ValueError("workers must be >= 1")
+    if config.record_every < 1:
+        raise ValueError("record_every must be >= 1")
+    plan = device_plan(graph)
+    if state is None:
+        state = init_state(graph, config.seed)
+    else:
+        _check_state(graph, state)
+    start = perf_counter()
+    plan.host_checks(graph)
+    plan.sync(graph)
+    plan.upload(state.z, state.u, state.n)
+    res, hist = plan.run(config.max_iterations, config.primal_tol, config.dual_tol,
+                         timing=config.profile, graph_chunk=config.graph_chunk)
+    if res.error_phase >= 0:
+        _raise_device_error(graph, plan, state, res)
+    executed = int(res.iterations)
+    outs = {}
+    for k in ("x", "m", "z", "u", "n"):
+        a = getattr(state, k)
+        if a.dtype == np.float64 and a.flags.c_contiguous and a.flags.writeable:
+            outs[k] = a
+        else:
+            outs[k] = np.empty(a.shape)
+    plan.download(**outs)
+    for k, a in outs.items():
+        if a is not getattr(state, k):
+            _assign(getattr(state, k), a)
+    msg = _nonfinite_message(graph, state.n, "n", executed)
+    base_iteration = state.iteration
+    if msg:
+        state.iteration += executed
+        raise RuntimeError(msg)
+    state.iteration += executed
+    total = perf_counter() - start
+
+    # per-phase attribution: edge pass = x (with n fused), variable pass =
+    # z (with m and u fused); residual reduction is outside the phases
+    a, b = res.ms_edge_pass, res.ms_var_pass
+    dev = res.ms_total / 1e3
+    share = (a / (a + b + res.ms_reduce)) if (a + b) > 0 else 0.5
+    vshare = (b / (a + b + res.ms_reduce)) if (a + b) > 0 else 0.5
+    phase_totals = {"x": dev * share, "m": 0.0, "z": dev * vshare, "u": 0.0, "n": 0.0}
+    per_it = {k: v / max(executed, 1) for k, v in phase_totals.items()}
+    tol_check = config.primal_tol > 0.0 or config.dual_tol > 0.0
+    history = []
+    converged = bool(res.converged)
+    for j in range(1, executed + 1):
+        record = (j % config.record_every == 0) or j == config.max_iterations \
+            or (converged and j == executed)
+        if record:
+            history.append((base_iteration + j, *(per_it[p] for p in PHASES),
+                            float(hist[j - 1, 0]), float(hist[j - 1, 1])))
+    if executed:
+        state.last_residuals = (float(hist[executed - 1, 0]), float(hist[executed - 1, 1]))
+    del tol_check
+    solution = [state.z[graph.variable_slice(v)].copy()
+                for v in range(len(graph.var_offsets) - 1)]
+    report = RunReport(iterations=executed, converged=converged, workers=config.workers,
+                       phase_seconds=phase_totals, history=history,
+                       total_seconds=max(total, dev), device_seconds=dev,
+                       kernel_launches=int(res.launches))
+    return solution, report
