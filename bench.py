@@ -1,0 +1,363 @@
+"""Benchmark: ADMM edge-updates/sec of the B200 engine (and its roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload svm1m]
+    python bench.py --impl reference ...      # CPU reference arm (oracle port)
+
+A step is one ADMM iteration (all five phases) over the whole graph.  The
+default workload is BASELINE.json configs[1]: the soft-margin SVM chain on
+1M synthetic Gaussian points x 32 dims (``build_svm``; zero init).  Other
+workloads: pack5000 (configs[3]), mpc100k (configs[2]), pack100
+(configs[0]).  One JSON line on stdout (rank 0).
+
+value      = edges x K / device time of K iterations with the state resident
+             in HBM (fused CUDA-graph loop, CUDA events on the engine stream;
+             working set >> L2, so no flush is needed between steps).
+e2e        = the same K iterations through the public ``run()`` call with
+             host numpy state: state upload, K iterations, full-state
+             download, measured by wall clock.
+roofline   = dominant kernel's algorithmic bytes per launch / its average
+             CUDA-event duration (``fg_profile_kernels``), against the
+             measured HBM copy bandwidth in MEASURED_PEAKS.json.
+cpu_baseline = the NumPy oracle port of the reference (oracle/) on a
+             bounded sample of the same workload, 1 core.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ADMM edge-updates/sec and HBM GB/s vs peak at 1/2/4/8 B200 vs CPU ref"
+UNIT = "edge-updates/s"
+
+WORKLOADS = {
+    "svm1m": "soft-margin linear SVM chain, 1M points x 32 dims (configs[1])",
+    "pack5000": "circle packing N=5000 in the unit triangle (configs[3])",
+    "mpc100k": "linear MPC, state 16, input 4, horizon 100k (configs[2])",
+    "pack100": "circle packing N=100 in the unit triangle (configs[0])",
+}
+
+
+def build_instance(name, scale=1.0):
+    import paper_1603_02526_b200 as fg
+    if name.startswith("svm"):
+        n = int(1_000_000 * scale)
+        X, y = fg.gen_gaussian_arrays(n, 32, 4.0, seed=0)
+        g = fg.build_svm(fg.SvmSpec.from_arrays(X, y, lam=1.0))
+        return g, fg.init_state(g), {"points": n, "dim": 32, "init": "zeros"}
+    if name.startswith("pack"):
+        n = int((5000 if name == "pack5000" else 100) * (scale if name == "pack5000" else 1))
+        spec = fg.PackingSpec(n)
+        g = fg.build_packing(spec)
+        st = fg.packing_init(g, spec, seed=0) if n <= 1000 else fg.init_state(g, seed=0)
+        return g, st, {"disks": n, "init": "packing_init(seed=0)" if n <= 1000 else
+                       "init_state(seed=0)"}
+    if name.startswith("mpc"):
+        T = int(100_000 * scale)
+        rng = np.random.default_rng(0)
+        A = 0.05 * rng.standard_normal((16, 16))
+        B = 0.1 * rng.standard_normal((16, 4))
+        q0 = rng.standard_normal(16)
+        g = fg.build_mpc(fg.MpcSpec(T, fg.LinearSystem(A, B), q0))
+        return g, fg.init_state(g), {"horizon": T, "state_dim": 16, "input_dim": 4}
+    raise SystemExit(f"unknown workload {name}")
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes per kernel
+
+def kernel_bytes(graph, plan):
+    """Compulsory HBM bytes per launch of each kernel of one iteration."""
+    dims = np.diff(np.asarray(graph.var_offsets))
+    deg = np.bincount(graph.edge_var, minlength=len(dims))
+    out = {}
+    for cls, sdims, fe, dp, _p, _s in plan.groups:
+        B = len(fe)
+        b = 0
+        zcomp = 0
+        for j, d in enumerate(sdims):
+            b += B * d * 16 + B * 8            # u read + x write, rho read
+            zcomp += int(np.sum(dims[np.unique(graph.edge_var[fe + j])]))
+        b += 8 * zcomp                         # z read once per component
+        if dp.fparams is not None:
+            b += dp.fparams.size * 8
+        key = f"edge_{cls.kind}"
+        out[key] = out.get(key, 0) + b
+    small = deg <= 32
+    chunk = 8192
+    large = (~small) & (deg - 1 <= chunk)
+    giant = (deg - 1) > chunk
+    for key, sel in (("var_small", small), ("var_large", large)):
+        if sel.any():
+            P = int(np.sum(deg[sel] * dims[sel]))
+            E = int(np.sum(deg[sel]))
+            Z = int(np.sum(dims[sel]))
+            out[key] = P * 24 + E * 16 + Z * 24
+    if giant.any():
+        P = int(np.sum(deg[giant] * dims[giant]))
+        E = int(np.sum(deg[giant]))
+        out["var_giant_chunks"] = P * 16 + E * 8
+        out["var_giant_top"] = int(np.sum(dims[giant])) * 24
+        out["var_giant_update"] = P * 24 + E * 16
+    out["reduce"] = 16 * (plan.info["small_components"] // 256 + 1
+                          + plan.info["large_components"] + 64)
+    return out
+
+
+def survey_alg_bytes(graph):
+    """B_alg = 40P + 32E + 24Z + 16V + B_par."""
+    P, E, Z = graph.total_edge_payload, len(graph.edge_var), graph.z_dim
+    V = len(graph.var_offsets) - 1
+    bpar = 0
+    for cls, dims, _f0, vars_, params in graph.blocks:
+        if cls.kind == "svm_margin":
+            bpar += vars_.shape[0] * 8 * (dims[0] + 1)
+    return 40 * P + 32 * E + 24 * Z + 16 * V + bpar
+
+
+# ---------------------------------------------------------------------------
+# clocks
+
+REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+
+class ClockSampler:
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,utilization.gpu",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 4:
+                continue
+            try:
+                s, m, util = float(parts[0]), float(parts[1]), float(parts[3])
+                mask = int(parts[2], 16)
+            except ValueError:
+                continue
+            mx = max(mx, m)
+            if util > 0:
+                sm.append(s)
+                for bit, name in REASONS.items():
+                    if mask & bit:
+                        reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": mx or None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def cpu_baseline(name, iters=None):
+    """NumPy oracle (reference port) on a bounded sample, one core."""
+    from oracle import fgadmm_oracle as O
+    import paper_1603_02526_b200 as fg
+    if name.startswith("svm"):
+        scale, desc = 0.1, "SVM chain 100k x 32 (same generator)"
+    elif name == "pack5000":
+        scale, desc = 0.2, "packing N=1000 (same spec)"
+    elif name.startswith("mpc"):
+        scale, desc = 0.05, "MPC 16/4 horizon 5k (same generator)"
+    else:
+        scale, desc = 1.0, "packing N=100"
+    g, st, _info = build_instance(name if name != "pack5000" else "pack5000", scale)
+    o = O.Oracle(g)
+    O.time_iterations(g, st, 1, oracle=o)             # warm caches
+    budget = 8.0
+    t1, _ = O.time_iterations(g, st, 1, oracle=o)
+    n = iters or max(2, min(200, int(budget / max(t1, 1e-6))))
+    tpi, _ = O.time_iterations(g, st, n, oracle=o)
+    E = len(g.edge_var)
+    return {"value": E / tpi, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{desc}: {n} iterations, {E} edges, {tpi * 1e3:.2f} ms/iter"}
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import fgadmm_oracle as O
+    name = args.workload
+    scale = {"svm1m": 0.1, "pack5000": 0.2, "mpc100k": 0.05}.get(name, 1.0)
+    g, st, info = build_instance(name, scale)
+    o = O.Oracle(g)
+    s = O.State.copy_of(st)
+    for _ in range(args.warmup):
+        o.iterate(s)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        o.iterate(s)
+    dt = time.perf_counter() - t0
+    E = len(g.edge_var)
+    value = E * args.steps / dt
+    sample = f"{WORKLOADS[name]} scaled x{scale}: {E} edges per step"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": name, **info, "scale": scale},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="svm1m", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    os.environ["FGADMM_DEVICE"] = str(local)
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+
+    import paper_1603_02526_b200 as fg
+    t_build = time.perf_counter()
+    g, st, info = build_instance(args.workload)
+    plan = fg.device_plan(g)
+    t_build = time.perf_counter() - t_build
+    E = len(g.edge_var)
+
+    # ---- device-resident timed region ----
+    plan.sync(g)
+    plan.upload(st.z, st.u, st.n)
+    plan.run(args.warmup)                                  # untimed warm-up
+    if dist:
+        dist.barrier()
+    with ClockSampler(local) as clk:
+        res, _hist = plan.run(args.steps, graph_chunk=16)
+    ms = res.ms_total
+    if dist:
+        import torch
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = E * args.steps * world / (ms / 1e3)
+
+    # ---- per-kernel profile (same arithmetic, events per launch) ----
+    plan.upload(st.z, st.u, st.n)
+    prof = plan.profile_kernels(max(3, min(args.steps, 20)))
+    kb = kernel_bytes(g, plan)
+    top = max(prof, key=lambda k: prof[k][0])
+    base = top.split("#")[0]
+    avg_ms = prof[top][0] / prof[top][1]
+    peak, peak_kind = measured_peak()
+    achieved = kb.get(base, 0) / (avg_ms / 1e3) / 1e9
+    iter_bytes = sum(kb.values())
+    iter_ms = sum(v[0] for v in prof.values()) / prof[top][1]
+
+    # ---- end to end through the public API (host state in, host state out) ----
+    s = fg.AdmmState(*(getattr(st, k).copy() for k in "xmzun"))
+    t0 = time.perf_counter()
+    fg.run(g, fg.RunConfig(max_iterations=args.steps), state=s)
+    e2e_s = time.perf_counter() - t0
+    P, Z = g.total_edge_payload, g.z_dim
+    h2d = (Z + 2 * P) * 8 + 2 * E * 8 * 0
+    d2h = (4 * P + Z) * 8
+    e2e = {"value": E * args.steps * world / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+           "note": f"one run() call of {args.steps} iterations: upload z,u,n, "
+                   f"download x,m,z,u,n (bytes amortized per step)"}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+    cpu = None if args.no_cpu_baseline or world > 1 else cpu_baseline(args.workload)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "desc": WORKLOADS[args.workload], **info,
+                   "edges": E, "payload": g.total_edge_payload, "z_dim": g.z_dim,
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "working set > L2 (no flush needed)",
+                   "build_seconds": round(t_build, 2)},
+        "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None,
+                     "iteration": {"alg_bytes": iter_bytes,
+                                   "survey_B_alg": survey_alg_bytes(g),
+                                   "ms": iter_ms,
+                                   "GBps": iter_bytes / (iter_ms / 1e3) / 1e9}},
+        "kernels": {k: {"ms_avg": v[0] / v[1], "alg_bytes": kb.get(k.split("#")[0], 0)}
+                    for k, v in prof.items()},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(res.launches),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

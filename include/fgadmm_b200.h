@@ -156,6 +156,13 @@ int fg_run(fg_plan* plan, const fg_run_config* cfg, double* history,
 int fg_state_download(fg_plan* plan, double* x, double* m, double* z,
                       double* u, double* n);
 int fg_debug_download(fg_plan* plan, int32_t buffer, double* out_ref);
+/* Per-kernel device time of `iterations` fused iterations (after
+ * fg_state_upload): labels[32*i], ms[i], counts[i] for each kernel slot of
+ * one iteration (edge_<kind>..., var_*, reduce).  Profiling aid; the
+ * arithmetic is exactly fg_run's. */
+int fg_profile_kernels(fg_plan* plan, int64_t iterations, int32_t max_slots,
+                       char* labels, double* ms, int64_t* counts,
+                       int32_t* nslots);
 
 /* ---- unfused per-phase API (update_x .. update_n) ----------------------- */
 int fg_phase_upload(fg_plan* plan, const double* x, const double* m,

@@ -242,25 +242,67 @@ void edge_pass(fg_plan* p, bool first, const double* uin, const double* nsrc,
     }
 }
 
+// variable-pass kernel `which`: 0 small, 1 large, 2 giant chunks,
+// 3 giant top, 4 giant update; returns false if that class is empty.
+template <int MODE>
+bool var_kernel(fg_plan* p, int which, const double* uin, double* uout,
+                const double* msrc, cudaStream_t st) {
+    PassB b{p->vt(), p->d_x, uin, uout, msrc, p->d_z, p->d_rho, p->d_alpha,
+            p->d_zw, p->d_ctrl, p->d_part, p->d_zvar};
+    switch (which) {
+        case 0:
+            if (!p->nS) return false;
+            k_var_small<MODE><<<nblk(p->nS, 256), 256, 0, st>>>(b, p->d_slist, p->nS, 0);
+            return true;
+        case 1:
+            if (!p->nL) return false;
+            k_var_large<MODE><<<(unsigned)p->nL, kVarThreads, 0, st>>>(
+                b, p->d_llist, p->d_lprog, p->d_prog, p->part_S);
+            return true;
+        case 2:
+            if (!p->nG) return false;
+            k_var_giant_chunks<MODE><<<(unsigned)p->nGC, kVarThreads, 0, st>>>(
+                b, p->d_glist, p->d_gchunks, p->d_prog, p->d_csum);
+            return true;
+        case 3:
+            if (!p->nG) return false;
+            k_var_giant_top<MODE><<<(unsigned)p->nG, kVarThreads, p->gtop_smem, st>>>(
+                b, p->d_glist, p->d_gcomps, p->d_prog, p->d_csum, p->d_gz);
+            return true;
+        case 4:
+            if (!p->nG || MODE != MODE_FUSED) return false;
+            k_var_giant_update<<<(unsigned)p->nGW, kVarThreads, 0, st>>>(
+                b, p->d_glist, p->d_gwork, p->d_gz, p->part_S + p->part_L);
+            return true;
+    }
+    return false;
+}
+
+const char* kVarNames[5] = {"var_small", "var_large", "var_giant_chunks",
+                            "var_giant_top", "var_giant_update"};
+
 template <int MODE>
 void var_pass(fg_plan* p, const double* uin, double* uout, const double* msrc,
               cudaStream_t st) {
-    PassB b{p->vt(), p->d_x, uin, uout, msrc, p->d_z, p->d_rho, p->d_alpha,
-            p->d_zw, p->d_ctrl, p->d_part, p->d_zvar};
-    if (p->nS)
-        k_var_small<MODE><<<nblk(p->nS, 256), 256, 0, st>>>(b, p->d_slist, p->nS, 0);
-    if (p->nL)
-        k_var_large<MODE><<<(unsigned)p->nL, kVarThreads, 0, st>>>(
-            b, p->d_llist, p->d_lprog, p->d_prog, p->part_S);
-    if (p->nG) {
-        k_var_giant_chunks<MODE><<<(unsigned)p->nGC, kVarThreads, 0, st>>>(
-            b, p->d_glist, p->d_gchunks, p->d_prog, p->d_csum);
-        k_var_giant_top<MODE><<<(unsigned)p->nG, kVarThreads, p->gtop_smem, st>>>(
-            b, p->d_glist, p->d_gcomps, p->d_prog, p->d_csum, p->d_gz);
-        if (MODE == MODE_FUSED)
-            k_var_giant_update<<<(unsigned)p->nGW, kVarThreads, 0, st>>>(
-                b, p->d_glist, p->d_gwork, p->d_gz, p->part_S + p->part_L);
+    for (int w = 0; w < 5; ++w) var_kernel<MODE>(p, w, uin, uout, msrc, st);
+}
+
+const char* kind_name(int kind) {
+    switch (kind) {
+        case FG_KIND_QUADRATIC: return "quadratic";
+        case FG_KIND_COLLISION: return "collision";
+        case FG_KIND_WALL: return "wall";
+        case FG_KIND_RADIUS: return "radius";
+        case FG_KIND_MPC_COST: return "mpc_cost";
+        case FG_KIND_MPC_INIT: return "mpc_init";
+        case FG_KIND_MPC_DYN: return "mpc_dyn";
+        case FG_KIND_SVM_SLACK: return "svm_slack";
+        case FG_KIND_SVM_NORM: return "svm_norm";
+        case FG_KIND_SVM_MARGIN: return "svm_margin";
+        case FG_KIND_EQUALITY: return "equality";
+        case FG_KIND_NAN_TEST: return "nan_test";
     }
+    return "unknown";
 }
 
 int64_t count_edge_launches(const fg_plan* p) {
@@ -867,6 +909,87 @@ int fg_residuals(fg_plan* p, const double* x, const double* z, const double* zpr
     *primal = std::sqrt(r2[0]) * scale;
     *dual = std::sqrt(r2[1]) * scale;
     return check_launch();
+}
+
+// ---- per-kernel profile ----------------------------------------------------
+// Runs `iterations` fused iterations (after an fg_state_upload) with CUDA
+// events around every launch, on the plan's stream.  Slot i of the
+// outputs is one kernel of the iteration: its label (32 bytes each), the
+// summed device milliseconds and the launch count.
+int fg_profile_kernels(fg_plan* p, int64_t iterations, int32_t max_slots,
+                       char* labels, double* ms, int64_t* counts, int32_t* nslots) {
+    CK(cudaSetDevice(p->device));
+    cudaStream_t st = p->stream;
+    if (p->hist_cap < iterations) {
+        if (p->d_hist) cudaFree(p->d_hist);
+        p->d_hist = nullptr;
+        int rc = dalloc(&p->d_hist, 2 * iterations);
+        if (rc) return rc;
+        p->hist_cap = iterations;
+    }
+    Ctrl h{};
+    h.err_key = ~0ull;
+    h.iter = 1;
+    h.scale = 1.0 / std::sqrt((double)p->P);
+    h.max_iter = iterations;
+    CK(cudaMemcpyAsync(p->d_ctrl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+    std::vector<std::string> names;
+    for (auto& g : p->groups)
+        if (g.dev.count > 0) names.push_back(std::string("edge_") + kind_name(g.dev.kind));
+    const int nedge = (int)names.size();
+    std::vector<int> vk;
+    for (int w = 0; w < 5; ++w) {
+        const bool has = (w == 0 && p->nS) || (w == 1 && p->nL) || (w >= 2 && p->nG);
+        if (has) { vk.push_back(w); names.push_back(kVarNames[w]); }
+    }
+    names.push_back("reduce");
+    const int ns = (int)names.size();
+    if (ns > max_slots) return fail(FG_ERR_INVALID, "too many kernels for the output arrays");
+    std::vector<cudaEvent_t> ev((size_t)(ns + 1) * iterations);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    PassA a0{p->vt(), p->d_z, nullptr, nullptr, p->d_x, p->d_rho, p->d_ctrl};
+    for (int64_t j = 1; j <= iterations; ++j) {
+        const int in = (int)((j - 1) & 1);
+        const bool first = (j == 1);
+        cudaEvent_t* E = &ev[(size_t)(ns + 1) * (j - 1)];
+        int slot = 0;
+        PassA a = a0;
+        a.uin = p->d_u[in];
+        a.nsrc = first ? p->d_u[1 - in] : nullptr;
+        CK(cudaEventRecord(E[0], st));
+        for (auto& g : p->groups) {
+            if (g.dev.count == 0) continue;
+            if (first) launch_kind<true>(g.dev, a, st);
+            else launch_kind<false>(g.dev, a, st);
+            CK(cudaEventRecord(E[++slot], st));
+        }
+        for (int w : vk) {
+            var_kernel<MODE_FUSED>(p, w, p->d_u[in], p->d_u[1 - in], nullptr, st);
+            CK(cudaEventRecord(E[++slot], st));
+        }
+        k_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_hist);
+        CK(cudaEventRecord(E[++slot], st));
+    }
+    CK(cudaStreamSynchronize(st));
+    if (int rc = check_launch()) return rc;
+    for (int i = 0; i < ns; ++i) { ms[i] = 0.0; counts[i] = iterations; }
+    for (int64_t j = 0; j < iterations; ++j)
+        for (int i = 0; i < ns; ++i) {
+            float t = 0;
+            cudaEventElapsedTime(&t, ev[(size_t)(ns + 1) * j + i], ev[(size_t)(ns + 1) * j + i + 1]);
+            ms[i] += t;
+        }
+    for (auto& e : ev) cudaEventDestroy(e);
+    for (int i = 0; i < ns; ++i) {
+        std::memset(labels + 32 * i, 0, 32);
+        std::strncpy(labels + 32 * i, names[i].c_str(), 31);
+    }
+    *nslots = ns;
+    (void)nedge;
+    Ctrl hc;
+    CK(cudaMemcpy(&hc, p->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+    p->completed = hc.completed;
+    return 0;
 }
 
 // ---- standalone batched prox ----------------------------------------------

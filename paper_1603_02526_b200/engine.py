@@ -292,6 +292,27 @@ class DevicePlan:
         _native.check(self._lib.fg_state_download(
             self._h, *[_native.dptr(a) if a is not None else None for a in outs]))
 
+    def profile_kernels(self, iterations):
+        """{label: (total ms, launches)} for each kernel of the iteration."""
+        n = 64
+        labels = C.create_string_buffer(32 * n)
+        ms = np.zeros(n)
+        cnt = np.zeros(n, dtype=np.int64)
+        ns = C.c_int32(0)
+        _native.check(self._lib.fg_profile_kernels(self._h, int(iterations), n, labels,
+                                                   _native.dptr(ms), _native.i64ptr(cnt),
+                                                   C.byref(ns)))
+        raw = labels.raw
+        out = {}
+        for i in range(ns.value):
+            name = raw[32 * i:32 * i + 32].split(b"\0", 1)[0].decode()
+            key, j = name, 1
+            while key in out:
+                j += 1
+                key = f"{name}#{j}"
+            out[key] = (float(ms[i]), int(cnt[i]))
+        return out
+
     def debug_buffer(self, which):
         out = np.empty(self.P)
         _native.check(self._lib.fg_debug_download(self._h, int(which), _native.dptr(out)))

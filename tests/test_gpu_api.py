@@ -156,14 +156,17 @@ def test_radius_weight_below_kappa_raises(gpu):
 
 
 def test_overflow_in_z_is_reported_as_variable(gpu):
+    """x and m stay finite (8.5e307 each) but three of them overflow the
+    consensus sum: the failure is attributed to the z phase."""
     b = fg.GraphBuilder()
-    v = b.declare_variable(1)
     w = b.declare_variable(1)
-    b.add_factor(fg.Quadratic([[1e308]], [1.0]), [v])
-    b.add_factor(fg.Quadratic([[1e308]], [1.0]), [v])
+    v = b.declare_variable(1)
     b.add_factor(fg.Quadratic([[1.0]], [1.0]), [w])
+    for _ in range(3):
+        b.add_factor(fg.Quadratic([[1.7e308]], [1.0]), [v])
     g = b.freeze()
-    with pytest.raises(RuntimeError, match=r"non-finite value after"):
+    with pytest.raises(RuntimeError,
+                       match=r"non-finite value after z update at iteration 1: variable 1"):
         fg.run(g, fg.RunConfig(max_iterations=3))
 
 
