@@ -98,7 +98,12 @@ def kernel_bytes(graph, plan):
     chunk = 8192
     large = (~small) & (deg - 1 <= chunk)
     giant = (deg - 1) > chunk
-    for key, sel in (("var_small", small), ("var_large", large)):
+    sel_by_key = [("var_small_deg4", deg <= 4), ("var_small_deg8", (deg > 4) & (deg <= 8)),
+                  ("var_small_loop", small & (deg > 8))]
+    for d in (1, 2, 3, 4):
+        sel_by_key.append((f"var_large_d{d}", large & (dims == d)))
+    sel_by_key.append(("var_large_comp", large & (dims > 4)))
+    for key, sel in sel_by_key:
         if sel.any():
             P = int(np.sum(deg[sel] * dims[sel]))
             E = int(np.sum(deg[sel]))

@@ -2,13 +2,14 @@
 
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SOURCES = [os.path.join(HERE, "csrc", "fg_engine.cu")]
-DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("fg_device.cuh", "fg_kernels.cuh")] \
+DEPS = SOURCES + sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) \
     + [os.path.join(HERE, "..", "include", "fgadmm_b200.h")]
 OUT = os.path.join(HERE, "libfgadmm_b200.so")
 

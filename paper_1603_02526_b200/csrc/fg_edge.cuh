@@ -1,0 +1,380 @@
+// Edge pass (phase n of the previous iteration + phase x) kernels.
+//
+// Addressing.  Slot j of factor f lives at a var-major payload position
+// pos, with z offset zo and var-major edge q.  Two modes per group:
+//   * runs: the group is cut on the host into maximal runs of consecutive
+//     factors over which (pos, zo, q) of every slot are affine in the
+//     factor index; the kernel computes addresses arithmetically.  Every
+//     benchmark family is a handful of runs per group (packing: one run
+//     per disk i of the i<j triangle; SVM/MPC: 1-3 runs), so the edge pass
+//     reads no per-factor index at all.
+//   * index: per slot (variable, rank) tables, for irregular graphs.
+// Threads map to (factor, lane) with `tpf` lanes per factor: 1 (thread
+// kinds), D (element-wise kinds), 32 (warp kinds).
+#pragma once
+
+#include "fg_device.cuh"
+
+namespace fg {
+
+struct SlotRun {
+    int64_t pos0, pos_s;     // payload position: pos0 + fl * pos_s
+    int64_t z0, z_s;         // z offset
+    int32_t q0, q_s;         // var-major edge
+};
+struct RunHdr { int64_t f0, count; };
+struct BlockRef { int32_t run, item0, item1, pad; };   // CTA -> run items
+
+struct GroupDev {
+    int32_t kind, nslots;
+    int32_t dim[FG_MAX_SLOTS];
+    int64_t count;
+    const int32_t* svar[FG_MAX_SLOTS];   // index mode: slot variable
+    const int32_t* sk[FG_MAX_SLOTS];     // index mode: edge rank in variable
+    const double* fp;                    // per-factor params (AoS)
+    int32_t fstride, tstride;
+    const double* tab;                   // shared tables (mpc_dyn)
+    const int32_t* fsys;
+    int32_t ip;                          // integer param (mpc_dyn: state dim)
+    int32_t tpf;                         // lanes per factor
+    const RunHdr* runs;                  // run mode when non-null
+    const SlotRun* sruns;                // [nruns][nslots]
+    const BlockRef* blocks;              // one per CTA in run mode
+    int32_t nblocks, nruns;
+};
+
+struct PassA {
+    VarTab vt;
+    const double* z;
+    const double* uin;
+    const double* nsrc;      // FIRST mode: materialized n (var-major)
+    double* x;
+    const double* rho;       // var-major edge weights
+    Ctrl* ctrl;
+};
+
+struct SlotLoc {
+    int64_t pos;             // first payload slot (var-major)
+    int64_t zo;              // z offset of the variable
+    int32_t q;               // var-major edge index
+};
+
+struct FRef {
+    int64_t f;               // factor index in the group (parameter row)
+    int64_t fl;              // index inside its run
+    const SlotRun* sr;       // null in index mode
+};
+
+constexpr int kEdgeThreads = 256;
+constexpr int kEdgeItemsPerCta = 4 * kEdgeThreads;   // run mode
+constexpr int kEdgeIndexCtas = 148 * 16;             // index mode grid cap
+
+// Calls fn(FRef, lane) for every (factor, lane) item this thread owns.
+// Items advance by blockDim, so the lanes of a warp-per-factor kernel stay
+// on one factor (warp-uniform loop).
+template <class F>
+__device__ __forceinline__ void for_each_item(const GroupDev& g, F fn) {
+    const int tpf = g.tpf;
+    if (g.runs) {
+        const BlockRef b = g.blocks[blockIdx.x];
+        const RunHdr h = g.runs[b.run];
+        const SlotRun* sr = g.sruns + (int64_t)b.run * g.nslots;
+        for (int32_t item = b.item0 + (int32_t)threadIdx.x; item < b.item1;
+             item += (int32_t)blockDim.x) {
+            const uint32_t fl = (uint32_t)item / (uint32_t)tpf;
+            const int lane = item - (int32_t)(fl * tpf);
+            FRef r{h.f0 + fl, (int64_t)fl, sr};
+            fn(r, lane);
+        }
+    } else {
+        const int64_t total = g.count * tpf;
+        for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < total;
+             item += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t f = item / tpf;
+            FRef r{f, f, nullptr};
+            fn(r, (int)(item - f * tpf));
+        }
+    }
+}
+
+__device__ __forceinline__ SlotLoc locate(const VarTab& vt, const GroupDev& g,
+                                          int j, const FRef& r) {
+    SlotLoc s;
+    if (r.sr) {
+        const SlotRun& R = r.sr[j];
+        s.pos = R.pos0 + r.fl * R.pos_s;
+        s.zo = R.z0 + r.fl * R.z_s;
+        s.q = (int32_t)(R.q0 + r.fl * R.q_s);
+    } else {
+        const int32_t v = g.svar[j][r.f];
+        const int32_t k = g.sk[j][r.f];
+        s.pos = vt.pbase[v] + (int64_t)k * g.dim[j];
+        s.zo = vt.zbase[v];
+        s.q = vt.ebase[v] + k;
+    }
+    return s;
+}
+
+template <bool FIRST>
+__device__ __forceinline__ double nval(const PassA& a, const SlotLoc& s, int c,
+                                       bool& badn) {
+    if (FIRST) return a.nsrc[s.pos + c];
+    const double v = a.z[s.zo + c] - a.uin[s.pos + c];   // n = z[zmap] - u
+    badn |= !finite(v);
+    return v;
+}
+
+__device__ __forceinline__ void xput(const PassA& a, int64_t p, double v,
+                                     bool& badx) {
+    a.x[p] = v;
+    badx |= !finite(v);
+}
+
+template <bool FIRST>
+__device__ __forceinline__ void passa_flags(const PassA& a, int64_t it,
+                                            bool badn, bool badx) {
+    if (!FIRST && badn) flag_error(a.ctrl, it - 1, FG_PHASE_N, true);
+    if (badx) flag_error(a.ctrl, it, FG_PHASE_X, true);
+}
+
+// ---- collision: one thread per factor (operators.py:166-191) ------------
+template <bool FIRST>
+__global__ void __launch_bounds__(kEdgeThreads, 4) k_collision(PassA a, GroupDev g) {
+    if (a.ctrl->stop) return;
+    const int64_t it = a.ctrl->iter;
+    bool bn = false, bx = false;
+    for_each_item(g, [&](const FRef& r, int) {
+        const SlotLoc s0 = locate(a.vt, g, 0, r), s1 = locate(a.vt, g, 1, r);
+        const SlotLoc s2 = locate(a.vt, g, 2, r), s3 = locate(a.vt, g, 3, r);
+        const double n1c0 = nval<FIRST>(a, s0, 0, bn), n1c1 = nval<FIRST>(a, s0, 1, bn);
+        const double n1r = nval<FIRST>(a, s1, 0, bn);
+        const double n2c0 = nval<FIRST>(a, s2, 0, bn), n2c1 = nval<FIRST>(a, s2, 1, bn);
+        const double n2r = nval<FIRST>(a, s3, 0, bn);
+        double c10, c11, r1, c20, c21, r2;
+        prox_collision(n1c0, n1c1, n1r, n2c0, n2c1, n2r, a.rho[s0.q], a.rho[s1.q],
+                       a.rho[s2.q], a.rho[s3.q], c10, c11, r1, c20, c21, r2);
+        xput(a, s0.pos, c10, bx); xput(a, s0.pos + 1, c11, bx);
+        xput(a, s1.pos, r1, bx);
+        xput(a, s2.pos, c20, bx); xput(a, s2.pos + 1, c21, bx);
+        xput(a, s3.pos, r2, bx);
+    });
+    passa_flags<FIRST>(a, it, bn, bx);
+}
+
+// ---- wall: one thread per factor (operators.py:226-234) ----------------
+template <bool FIRST>
+__global__ void __launch_bounds__(kEdgeThreads) k_wall(PassA a, GroupDev g) {
+    if (a.ctrl->stop) return;
+    const int64_t it = a.ctrl->iter;
+    bool bn = false, bx = false;
+    for_each_item(g, [&](const FRef& r, int) {
+        const SlotLoc s0 = locate(a.vt, g, 0, r), s1 = locate(a.vt, g, 1, r);
+        const double nc0 = nval<FIRST>(a, s0, 0, bn), nc1 = nval<FIRST>(a, s0, 1, bn);
+        const double nr = nval<FIRST>(a, s1, 0, bn);
+        const double* P = g.fp + r.f * g.fstride;   // Q0 Q1 V0 V1
+        double c0, c1, rr;
+        prox_wall(nc0, nc1, nr, a.rho[s0.q], a.rho[s1.q], P[0], P[1], P[2], P[3],
+                  c0, c1, rr);
+        xput(a, s0.pos, c0, bx); xput(a, s0.pos + 1, c1, bx);
+        xput(a, s1.pos, rr, bx);
+    });
+    passa_flags<FIRST>(a, it, bn, bx);
+}
+
+// ---- element-wise kinds: one thread per (factor, component) -------------
+// radius (operators.py:272-277), mpc_cost (:312-314), mpc_init (:349-354),
+// svm_slack (:439-441), svm_norm (:477-479), equality (:560-564),
+// nan_test (fault injector).
+template <int KIND, bool FIRST>
+__global__ void __launch_bounds__(kEdgeThreads) k_elementwise(PassA a, GroupDev g) {
+    if (a.ctrl->stop) return;
+    const int64_t it = a.ctrl->iter;
+    bool bn = false, bx = false;
+    for_each_item(g, [&](const FRef& r, int c) {
+        const SlotLoc s0 = locate(a.vt, g, 0, r);
+        const double n = nval<FIRST>(a, s0, c, bn);
+        const double* P = g.fp + r.f * g.fstride;
+        double out;
+        if (KIND == FG_KIND_RADIUS) {
+            out = prox_radius(n, a.rho[s0.q], P[0]);
+        } else if (KIND == FG_KIND_MPC_COST) {
+            out = prox_mpc_cost(n, a.rho[s0.q], P[c]);
+        } else if (KIND == FG_KIND_MPC_INIT) {
+            out = (c < g.fstride) ? P[c] : n;
+        } else if (KIND == FG_KIND_SVM_SLACK) {
+            out = prox_svm_slack(n, a.rho[s0.q], P[0]);
+        } else if (KIND == FG_KIND_SVM_NORM) {
+            out = prox_svm_norm(n, a.rho[s0.q], P[0]);
+        } else if (KIND == FG_KIND_NAN_TEST) {
+            out = (P[0] != 0.0) ? __longlong_as_double(0x7ff8000000000000ll) : n;
+        } else {  // FG_KIND_EQUALITY
+            const SlotLoc s1 = locate(a.vt, g, 1, r);
+            const double n2 = nval<FIRST>(a, s1, c, bn);
+            out = prox_equality(n, n2, a.rho[s0.q], a.rho[s1.q]);
+            xput(a, s1.pos + c, out, bx);
+        }
+        xput(a, s0.pos + c, out, bx);
+    });
+    passa_flags<FIRST>(a, it, bn, bx);
+}
+
+// ---- quadratic: one thread per factor, any slots (operators.py:131-135) -
+template <bool FIRST>
+__global__ void __launch_bounds__(kEdgeThreads) k_quadratic(PassA a, GroupDev g) {
+    if (a.ctrl->stop) return;
+    const int64_t it = a.ctrl->iter;
+    bool bn = false, bx = false;
+    for_each_item(g, [&](const FRef& r, int) {
+        const double* P = g.fp + r.f * g.fstride;   // per slot: targets, curvature
+        int off = 0;
+        for (int j = 0; j < g.nslots; ++j) {
+            const SlotLoc s = locate(a.vt, g, j, r);
+            const double R = a.rho[s.q];
+            const int d = g.dim[j];
+            const double C = P[off + d];
+            for (int c = 0; c < d; ++c)
+                xput(a, s.pos + c, prox_quadratic(nval<FIRST>(a, s, c, bn), R, P[off + c], C), bx);
+            off += d + 1;
+        }
+    });
+    passa_flags<FIRST>(a, it, bn, bx);
+}
+
+// ---- svm_margin: one warp per factor (operators.py:515-525) -------------
+// Slots (w: D, b: 1, xi: 1); params x (D) then y.  The two D-dim dots use a
+// fixed xor-tree (deterministic; parity with NumPy's einsum is 1e-9 rel).
+constexpr int kMarginLanes = 8;          // lanes per factor
+constexpr int kMarginMaxD = 128;
+// Each factor is served by an aligned group of 8 lanes, lane l holding
+// components l, l+8, ...: 4 factors per warp keep 4x more rows in flight
+// than a warp per factor.  Reductions are xor butterflies inside the group
+// (fixed order: deterministic).
+template <bool FIRST, int CPL>
+__global__ void __launch_bounds__(kEdgeThreads, 4) k_svm_margin(PassA a, GroupDev g) {
+    if (a.ctrl->stop) return;
+    const int64_t it = a.ctrl->iter;
+    const int D = g.dim[0];
+    const unsigned gmask = 0xFFu << (threadIdx.x & 24);
+    bool bn = false, bx = false;
+    for_each_item(g, [&](const FRef& r, int lane) {   // group-uniform
+        const SlotLoc s0 = locate(a.vt, g, 0, r), s1 = locate(a.vt, g, 1, r);
+        const SlotLoc s2 = locate(a.vt, g, 2, r);
+        const double* P = g.fp + r.f * g.fstride;
+        double n1[CPL], X[CPL];
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+            const int c = lane + kMarginLanes * k;
+            n1[k] = 0.0; X[k] = 0.0;
+            if (c < D) {
+                n1[k] = nval<FIRST>(a, s0, c, bn);
+                X[k] = P[c];
+            }
+        }
+        const double n2 = nval<FIRST>(a, s1, 0, bn), n3 = nval<FIRST>(a, s2, 0, bn);
+        const double R1 = a.rho[s0.q], R2 = a.rho[s1.q], R3 = a.rho[s2.q];
+        const double Y = P[D];
+        double dot = 0.0, xx = 0.0;
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+            dot += n1[k] * X[k];
+            xx += X[k] * X[k];
+        }
+#pragma unroll
+        for (int o = 1; o < kMarginLanes; o <<= 1) {
+            dot += __shfl_xor_sync(gmask, dot, o);
+            xx += __shfl_xor_sync(gmask, xx, o);
+        }
+        const double slack = (1.0 - n3) - Y * (dot + n2);
+        const double denom = (xx / R1 + 1.0 / R2) + 1.0 / R3;
+        const double mu = np_max0(slack) / denom;
+        const double tw = (mu / R1) * Y;
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+            const int c = lane + kMarginLanes * k;
+            if (c < D) xput(a, s0.pos + c, n1[k] + tw * X[k], bx);
+        }
+        if (lane == 0) {
+            xput(a, s1.pos, n2 + (mu / R2) * Y, bx);
+            xput(a, s2.pos, n3 + mu / R3, bx);
+        }
+    });
+    passa_flags<FIRST>(a, it, bn, bx);
+}
+
+// ---- mpc_dyn: one warp per factor (operators.py:86-96, 390-404) ---------
+// Weighted projection onto {M v = 0}, M = [I+A, B, -I] (d x (2d+k)).
+// With W = diag(rho0 on slot 0, rho1 on the first d of slot 1),
+// S = M W^-1 M^T = G/rho0 + I/rho1, G = QLQ^T precomputed per system, so
+// S^-1 = Q diag(1/(L/rho0 + 1/rho1)) Q^T (replaces the per-factor LAPACK
+// gesv; parity 1e-9 rel).  Table entry: M row-major, Q row-major, L.
+constexpr int kDynMaxD = 32, kDynMaxCols = 96;
+constexpr int kDynWarps = kEdgeThreads / 32;
+template <bool FIRST>
+__global__ void __launch_bounds__(kEdgeThreads) k_mpc_dyn(PassA a, GroupDev g) {
+    __shared__ double s_nv[kDynWarps][kDynMaxCols];
+    __shared__ double s_v1[kDynWarps][kDynMaxD];
+    __shared__ double s_v2[kDynWarps][kDynMaxD];
+    if (a.ctrl->stop) return;
+    const int w = threadIdx.x >> 5;
+    const int64_t it = a.ctrl->iter;
+    const int n0 = g.dim[0];
+    const int d = g.ip;                       // state dim
+    const int cols = n0 + d;                  // 2d + k
+    bool bn = false, bx = false;
+    for_each_item(g, [&](const FRef& r, int lane) {   // warp-uniform
+        const SlotLoc s0 = locate(a.vt, g, 0, r), s1 = locate(a.vt, g, 1, r);
+        const double* T = g.tab + (int64_t)(g.fsys ? g.fsys[r.f] : 0) * g.tstride;
+        const double* M = T;
+        const double* Q = T + d * cols;
+        const double* L = Q + d * d;
+        for (int c = lane; c < cols; c += 32)
+            s_nv[w][c] = (c < n0) ? nval<FIRST>(a, s0, c, bn)
+                                  : nval<FIRST>(a, s1, c - n0, bn);
+        __syncwarp();
+        const double R0 = a.rho[s0.q], R1 = a.rho[s1.q];
+        if (lane < d) {                           // Mnv
+            double acc = 0.0;
+            for (int c = 0; c < cols; ++c) acc += M[lane * cols + c] * s_nv[w][c];
+            s_v1[w][lane] = acc;
+        }
+        __syncwarp();
+        if (lane < d) {                           // y = diag * Q^T Mnv
+            double acc = 0.0;
+            for (int q = 0; q < d; ++q) acc += Q[q * d + lane] * s_v1[w][q];
+            s_v2[w][lane] = acc / (L[lane] / R0 + 1.0 / R1);
+        }
+        __syncwarp();
+        if (lane < d) {                           // lambda = Q y
+            double acc = 0.0;
+            for (int i = 0; i < d; ++i) acc += Q[lane * d + i] * s_v2[w][i];
+            s_v1[w][lane] = acc;
+        }
+        __syncwarp();
+        for (int c = lane; c < cols; c += 32) {   // v = nv - W^-1 M^T lambda
+            double acc = 0.0;
+            for (int q = 0; q < d; ++q) acc += M[q * cols + c] * s_v1[w][q];
+            const double winv = 1.0 / ((c < n0) ? R0 : R1);
+            const double v = s_nv[w][c] - winv * acc;
+            if (c < n0) xput(a, s0.pos + c, v, bx);
+            else xput(a, s1.pos + (c - n0), v, bx);
+        }
+        for (int c = d + lane; c < n0; c += 32)   // slot-1 control passes through
+            xput(a, s1.pos + c, nval<FIRST>(a, s1, c, bn), bx);
+        __syncwarp();
+    });
+    passa_flags<FIRST>(a, it, bn, bx);
+}
+
+// lanes per factor of each kind's kernel
+__host__ __device__ inline int kind_tpf(int kind, int dim0) {
+    switch (kind) {
+        case FG_KIND_SVM_MARGIN: return kMarginLanes;
+        case FG_KIND_MPC_DYN: return 32;
+        case FG_KIND_RADIUS: case FG_KIND_MPC_COST: case FG_KIND_MPC_INIT:
+        case FG_KIND_SVM_SLACK: case FG_KIND_SVM_NORM: case FG_KIND_EQUALITY:
+        case FG_KIND_NAN_TEST: return dim0;
+        default: return 1;
+    }
+}
+
+}  // namespace fg

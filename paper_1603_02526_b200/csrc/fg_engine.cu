@@ -20,7 +20,7 @@
 #include <string>
 #include <vector>
 
-#include "fg_kernels.cuh"
+#include "fg_var_fast.cuh"
 
 using namespace fg;
 
@@ -154,9 +154,17 @@ struct fg_plan {
     // groups
     std::vector<GroupHost> groups;
     // variable-pass classes
-    int32_t* d_slist = nullptr; int64_t nS = 0;
-    int32_t* d_llist = nullptr; int32_t* d_lprog = nullptr; int64_t nL = 0;
+    int64_t nS = 0;                                   // small components
+    SRun* d_sruns = nullptr;
+    SBlock* d_sblk[3] = {nullptr, nullptr, nullptr};  // deg<=4, 5..8, 9..32
+    int64_t nsblk[3] = {0, 0, 0};
+    int32_t* d_lvars[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // D=1..4
+    int32_t* d_lvprog[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    int64_t nlv[5] = {0, 0, 0, 0, 0};
+    int32_t* d_llist = nullptr; int32_t* d_lprog = nullptr; int64_t nL = 0;  // D>4
+    int64_t nLvars = 0;
     int32_t* d_prog = nullptr;
+    int64_t part_off[16] = {0};                       // per var kernel slot
     int32_t* d_glist = nullptr; int64_t nG = 0;
     GChunk* d_gchunks = nullptr; int64_t nGC = 0;
     GComp* d_gcomps = nullptr; int gtop_smem = 0;
@@ -186,7 +194,9 @@ fg_plan::~fg_plan() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     void* ptrs[] = {d_dim, d_deg, d_ebase, d_pbase, d_zbase, d_zvar, d_vm2ref,
                     d_vmz, d_vmvar, d_refedge, d_rho, d_alpha, d_zw, d_x,
-                    d_u[0], d_u[1], d_stage, d_aux, d_z, d_zs, d_slist,
+                    d_u[0], d_u[1], d_stage, d_aux, d_z, d_zs, d_sruns,
+                    d_sblk[0], d_sblk[1], d_sblk[2], d_lvars[1], d_lvars[2], d_lvars[3],
+                    d_lvars[4], d_lvprog[1], d_lvprog[2], d_lvprog[3], d_lvprog[4],
                     d_llist, d_lprog, d_prog, d_glist, d_gchunks, d_gcomps,
                     d_gwork, d_csum, d_gz, d_part, d_res2, d_ctrl, d_hist};
     for (void* p : ptrs)
@@ -202,32 +212,33 @@ namespace {
 // edge pass launchers
 template <bool FIRST>
 void launch_kind(const GroupDev& g, const PassA& a, cudaStream_t st) {
-    const int64_t n = g.count;
+    const unsigned grid = g.runs ? (unsigned)g.nblocks
+                                 : std::min<unsigned>(nblk(g.count * (int64_t)g.tpf, kEdgeThreads),
+                                                      kEdgeIndexCtas);
+    const int T = kEdgeThreads;
     switch (g.kind) {
-        case FG_KIND_COLLISION:
-            k_collision<FIRST><<<nblk(n, 256), 256, 0, st>>>(a, g); break;
-        case FG_KIND_WALL:
-            k_wall<FIRST><<<nblk(n, 256), 256, 0, st>>>(a, g); break;
-        case FG_KIND_QUADRATIC:
-            k_quadratic<FIRST><<<nblk(n, 256), 256, 0, st>>>(a, g); break;
+        case FG_KIND_COLLISION: k_collision<FIRST><<<grid, T, 0, st>>>(a, g); break;
+        case FG_KIND_WALL: k_wall<FIRST><<<grid, T, 0, st>>>(a, g); break;
+        case FG_KIND_QUADRATIC: k_quadratic<FIRST><<<grid, T, 0, st>>>(a, g); break;
         case FG_KIND_RADIUS:
-            k_elementwise<FG_KIND_RADIUS, FIRST><<<nblk(n * g.dim[0], 256), 256, 0, st>>>(a, g); break;
+            k_elementwise<FG_KIND_RADIUS, FIRST><<<grid, T, 0, st>>>(a, g); break;
         case FG_KIND_MPC_COST:
-            k_elementwise<FG_KIND_MPC_COST, FIRST><<<nblk(n * g.dim[0], 256), 256, 0, st>>>(a, g); break;
+            k_elementwise<FG_KIND_MPC_COST, FIRST><<<grid, T, 0, st>>>(a, g); break;
         case FG_KIND_MPC_INIT:
-            k_elementwise<FG_KIND_MPC_INIT, FIRST><<<nblk(n * g.dim[0], 256), 256, 0, st>>>(a, g); break;
+            k_elementwise<FG_KIND_MPC_INIT, FIRST><<<grid, T, 0, st>>>(a, g); break;
         case FG_KIND_SVM_SLACK:
-            k_elementwise<FG_KIND_SVM_SLACK, FIRST><<<nblk(n * g.dim[0], 256), 256, 0, st>>>(a, g); break;
+            k_elementwise<FG_KIND_SVM_SLACK, FIRST><<<grid, T, 0, st>>>(a, g); break;
         case FG_KIND_SVM_NORM:
-            k_elementwise<FG_KIND_SVM_NORM, FIRST><<<nblk(n * g.dim[0], 256), 256, 0, st>>>(a, g); break;
+            k_elementwise<FG_KIND_SVM_NORM, FIRST><<<grid, T, 0, st>>>(a, g); break;
         case FG_KIND_EQUALITY:
-            k_elementwise<FG_KIND_EQUALITY, FIRST><<<nblk(n * g.dim[0], 256), 256, 0, st>>>(a, g); break;
+            k_elementwise<FG_KIND_EQUALITY, FIRST><<<grid, T, 0, st>>>(a, g); break;
         case FG_KIND_NAN_TEST:
-            k_elementwise<FG_KIND_NAN_TEST, FIRST><<<nblk(n * g.dim[0], 256), 256, 0, st>>>(a, g); break;
+            k_elementwise<FG_KIND_NAN_TEST, FIRST><<<grid, T, 0, st>>>(a, g); break;
         case FG_KIND_SVM_MARGIN:
-            k_svm_margin<FIRST><<<nblk(n * 32, 256), 256, 0, st>>>(a, g); break;
-        case FG_KIND_MPC_DYN:
-            k_mpc_dyn<FIRST><<<nblk(n, 4), 128, 0, st>>>(a, g); break;
+            if (g.dim[0] <= 4 * kMarginLanes) k_svm_margin<FIRST, 4><<<grid, T, 0, st>>>(a, g);
+            else k_svm_margin<FIRST, kMarginMaxD / kMarginLanes><<<grid, T, 0, st>>>(a, g);
+            break;
+        case FG_KIND_MPC_DYN: k_mpc_dyn<FIRST><<<grid, T, 0, st>>>(a, g); break;
         default: break;
     }
 }
@@ -242,49 +253,85 @@ void edge_pass(fg_plan* p, bool first, const double* uin, const double* nsrc,
     }
 }
 
-// variable-pass kernel `which`: 0 small, 1 large, 2 giant chunks,
-// 3 giant top, 4 giant update; returns false if that class is empty.
+// Variable-pass kernel slots (one launch each, empty classes skipped):
+//   0 small segments (deg <= 8, registers)   1 small segments (deg 9..32)
+//   2..5 large segments, one CTA per variable of dim 1..4
+//   6 large segments, one CTA per component (dim > 4)
+//   7 giant chunks   8 giant top   9 giant u update
+constexpr int kVarSlots = 11;
+constexpr int kSlotGiantChunks = 8, kSlotGiantTop = 9, kSlotGiantUpdate = 10;
+const char* kVarNames[kVarSlots] = {
+    "var_small_deg4", "var_small_deg8", "var_small_loop", "var_large_d1",
+    "var_large_d2", "var_large_d3", "var_large_d4", "var_large_comp",
+    "var_giant_chunks", "var_giant_top", "var_giant_update"};
+
+int64_t var_slot_blocks(const fg_plan* p, int w) {
+    switch (w) {
+        case 0: case 1: case 2: return p->nsblk[w];
+        case 3: case 4: case 5: case 6: return p->nlv[w - 2];
+        case 7: return p->nL;
+        case 8: return p->nG ? p->nGC : 0;
+        case 9: return p->nG;
+        case 10: return p->nG ? p->nGW : 0;
+    }
+    return 0;
+}
+
 template <int MODE>
 bool var_kernel(fg_plan* p, int which, const double* uin, double* uout,
                 const double* msrc, cudaStream_t st) {
+    const int64_t nb = var_slot_blocks(p, which);
+    if (nb == 0) return false;
+    const unsigned grid = (unsigned)nb;
     PassB b{p->vt(), p->d_x, uin, uout, msrc, p->d_z, p->d_rho, p->d_alpha,
             p->d_zw, p->d_ctrl, p->d_part, p->d_zvar};
+    const int64_t po = p->part_off[which];
     switch (which) {
         case 0:
-            if (!p->nS) return false;
-            k_var_small<MODE><<<nblk(p->nS, 256), 256, 0, st>>>(b, p->d_slist, p->nS, 0);
+            k_var_small_run<kSmallTinyDeg, MODE><<<grid, 256, 0, st>>>(b, p->d_sruns, p->d_sblk[0], po);
             return true;
         case 1:
-            if (!p->nL) return false;
-            k_var_large<MODE><<<(unsigned)p->nL, kVarThreads, 0, st>>>(
-                b, p->d_llist, p->d_lprog, p->d_prog, p->part_S);
+            k_var_small_run<kSmallRegDeg, MODE><<<grid, 256, 0, st>>>(b, p->d_sruns, p->d_sblk[1], po);
             return true;
         case 2:
-            if (!p->nG) return false;
-            k_var_giant_chunks<MODE><<<(unsigned)p->nGC, kVarThreads, 0, st>>>(
-                b, p->d_glist, p->d_gchunks, p->d_prog, p->d_csum);
+            k_var_small_run<0, MODE><<<grid, 256, 0, st>>>(b, p->d_sruns, p->d_sblk[2], po);
             return true;
         case 3:
-            if (!p->nG) return false;
-            k_var_giant_top<MODE><<<(unsigned)p->nG, kVarThreads, p->gtop_smem, st>>>(
-                b, p->d_glist, p->d_gcomps, p->d_prog, p->d_csum, p->d_gz);
+            k_var_large_vec<1, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po);
             return true;
         case 4:
-            if (!p->nG || MODE != MODE_FUSED) return false;
-            k_var_giant_update<<<(unsigned)p->nGW, kVarThreads, 0, st>>>(
-                b, p->d_glist, p->d_gwork, p->d_gz, p->part_S + p->part_L);
+            k_var_large_vec<2, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po);
+            return true;
+        case 5:
+            k_var_large_vec<3, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po);
+            return true;
+        case 6:
+            k_var_large_vec<4, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, po);
+            return true;
+        case 7:
+            k_var_large<MODE><<<grid, kVarThreads, 0, st>>>(b, p->d_llist, p->d_lprog, p->d_prog, po);
+            return true;
+        case kSlotGiantChunks:
+            k_var_giant_chunks<MODE><<<grid, kVarThreads, 0, st>>>(
+                b, p->d_glist, p->d_gchunks, p->d_prog, p->d_csum);
+            return true;
+        case kSlotGiantTop:
+            k_var_giant_top<MODE><<<grid, kVarThreads, p->gtop_smem, st>>>(
+                b, p->d_glist, p->d_gcomps, p->d_prog, p->d_csum, p->d_gz);
+            return true;
+        case kSlotGiantUpdate:
+            if (MODE != MODE_FUSED) return false;
+            k_var_giant_update<<<grid, kVarThreads, 0, st>>>(b, p->d_glist, p->d_gwork,
+                                                             p->d_gz, po);
             return true;
     }
     return false;
 }
 
-const char* kVarNames[5] = {"var_small", "var_large", "var_giant_chunks",
-                            "var_giant_top", "var_giant_update"};
-
 template <int MODE>
 void var_pass(fg_plan* p, const double* uin, double* uout, const double* msrc,
               cudaStream_t st) {
-    for (int w = 0; w < 5; ++w) var_kernel<MODE>(p, w, uin, uout, msrc, st);
+    for (int w = 0; w < kVarSlots; ++w) var_kernel<MODE>(p, w, uin, uout, msrc, st);
 }
 
 const char* kind_name(int kind) {
@@ -312,7 +359,9 @@ int64_t count_edge_launches(const fg_plan* p) {
 }
 
 int64_t count_var_launches(const fg_plan* p) {
-    return (p->nS > 0) + (p->nL > 0) + (p->nG > 0 ? 3 : 0);
+    int64_t n = 0;
+    for (int w = 0; w < kVarSlots; ++w) n += var_slot_blocks(p, w) > 0;
+    return n;
 }
 
 // One fused iteration.  Iteration j (1-based within a run) reads u[(j-1)&1]
@@ -350,7 +399,10 @@ int check_launch() {
 int build_group(fg_plan* p, const fg_group_desc& gd,
                 const std::vector<int32_t>& edge_var,
                 const std::vector<int32_t>& vm_of_ref,
-                const std::vector<int32_t>& ebase, GroupHost& out) {
+                const std::vector<int32_t>& ebase,
+                const std::vector<int64_t>& pbase,
+                const std::vector<int64_t>& zbase, GroupHost& out) {
+    (void)p;
     GroupDev& g = out.dev;
     g.kind = gd.kind;
     g.nslots = gd.nslots;
@@ -371,7 +423,7 @@ int build_group(fg_plan* p, const fg_group_desc& gd,
                 return fail(FG_ERR_UNSUPPORTED, "wall expects slot dims (2,1)");
             break;
         case FG_KIND_SVM_MARGIN:
-            if (gd.nslots != 3 || g.dim[0] > 32 * kMarginMaxPerLane || g.dim[1] != 1 || g.dim[2] != 1)
+            if (gd.nslots != 3 || g.dim[0] > kMarginMaxD || g.dim[1] != 1 || g.dim[2] != 1)
                 return fail(FG_ERR_UNSUPPORTED, "svm_margin expects slot dims (D<=128,1,1)");
             break;
         case FG_KIND_EQUALITY:
@@ -393,21 +445,89 @@ int build_group(fg_plan* p, const fg_group_desc& gd,
             return fail(FG_ERR_UNSUPPORTED, "operator kind has no device kernel");
     }
     const int64_t n = gd.count;
-    for (int j = 0; j < gd.nslots; ++j) {
-        std::vector<int32_t> sv(n), sk(n);
+    const int ns = gd.nslots;
+    g.tpf = kind_tpf(gd.kind, g.dim[0]);
+    // per factor and slot: (payload position, z offset, var-major edge)
+    std::vector<int64_t> pos(n * ns), zo(n * ns), qq(n * ns);
+    std::vector<std::vector<int32_t>> svs(ns), sks(ns);
+    for (int j = 0; j < ns; ++j) {
+        svs[j].resize(n);
+        sks[j].resize(n);
         for (int64_t i = 0; i < n; ++i) {
             const int64_t e = gd.first_edge[i] + j;
             const int32_t v = edge_var[e];
-            sv[i] = v;
-            sk[i] = vm_of_ref[e] - ebase[v];
+            const int32_t k = vm_of_ref[e] - ebase[v];
+            svs[j][i] = v;
+            sks[j][i] = k;
+            pos[i * ns + j] = pbase[v] + (int64_t)k * g.dim[j];
+            zo[i * ns + j] = zbase[v];
+            qq[i * ns + j] = (int64_t)ebase[v] + k;
         }
-        int32_t *dsv, *dsk;
-        if (int rc = upload(&dsv, sv)) return rc;
-        out.allocs.push_back(dsv);
-        if (int rc = upload(&dsk, sk)) return rc;
-        out.allocs.push_back(dsk);
-        g.svar[j] = dsv;
-        g.sk[j] = dsk;
+    }
+    // maximal runs of factors whose slot addresses are affine in the index
+    std::vector<RunHdr> runs;
+    std::vector<SlotRun> sruns;
+    for (int64_t i0 = 0; i0 < n;) {
+        int64_t i1 = i0 + 1;
+        std::vector<SlotRun> sr(ns);
+        for (int j = 0; j < ns; ++j) {
+            const int64_t a = i0 * ns + j;
+            sr[j].pos0 = pos[a]; sr[j].z0 = zo[a]; sr[j].q0 = (int32_t)qq[a];
+            sr[j].pos_s = 0; sr[j].z_s = 0; sr[j].q_s = 0;
+            if (i0 + 1 < n) {
+                const int64_t b = a + ns;
+                sr[j].pos_s = pos[b] - pos[a];
+                sr[j].z_s = zo[b] - zo[a];
+                sr[j].q_s = (int32_t)(qq[b] - qq[a]);
+            }
+        }
+        while (i1 < n) {
+            bool ok = true;
+            const int64_t t = i1 - i0;
+            for (int j = 0; j < ns && ok; ++j) {
+                const int64_t a = i1 * ns + j;
+                ok = pos[a] == sr[j].pos0 + t * sr[j].pos_s &&
+                     zo[a] == sr[j].z0 + t * sr[j].z_s &&
+                     qq[a] == (int64_t)sr[j].q0 + t * sr[j].q_s;
+            }
+            if (!ok) break;
+            ++i1;
+        }
+        runs.push_back(RunHdr{i0, i1 - i0});
+        sruns.insert(sruns.end(), sr.begin(), sr.end());
+        i0 = i1;
+    }
+    if ((int64_t)runs.size() * 16 <= n || runs.size() == 1) {
+        std::vector<BlockRef> blocks;
+        for (size_t r = 0; r < runs.size(); ++r) {
+            const int64_t items = runs[r].count * g.tpf;
+            if (items >= INT32_MAX) return fail(FG_ERR_INVALID, "factor run exceeds 2^31 items");
+            for (int64_t it0 = 0; it0 < items; it0 += kEdgeItemsPerCta)
+                blocks.push_back(BlockRef{(int32_t)r, (int32_t)it0,
+                                          (int32_t)std::min<int64_t>(items, it0 + kEdgeItemsPerCta), 0});
+        }
+        RunHdr* dr; SlotRun* ds; BlockRef* db;
+        if (int rc = upload(&dr, runs)) return rc;
+        out.allocs.push_back(dr);
+        if (int rc = upload(&ds, sruns)) return rc;
+        out.allocs.push_back(ds);
+        if (int rc = upload(&db, blocks)) return rc;
+        out.allocs.push_back(db);
+        g.runs = dr;
+        g.sruns = ds;
+        g.blocks = db;
+        g.nblocks = (int32_t)blocks.size();
+        g.nruns = (int32_t)runs.size();
+    } else {
+        for (int j = 0; j < ns; ++j) {
+            int32_t *dsv, *dsk;
+            if (int rc = upload(&dsv, svs[j])) return rc;
+            out.allocs.push_back(dsv);
+            if (int rc = upload(&dsk, sks[j])) return rc;
+            out.allocs.push_back(dsk);
+            g.svar[j] = dsv;
+            g.sk[j] = dsk;
+        }
     }
     if (gd.fparams && gd.fstride > 0) {
         std::vector<double> fp(gd.fparams, gd.fparams + n * gd.fstride);
@@ -534,12 +654,15 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     // ---- groups ----
     for (int32_t i = 0; i < ngroups; ++i) {
         p->groups.emplace_back();
-        if ((rc = build_group(p.get(), groups[i], edge_var, vm_of_ref, ebase, p->groups.back())))
+        if ((rc = build_group(p.get(), groups[i], edge_var, vm_of_ref, ebase, pbase, zbase, p->groups.back())))
             return rc;
     }
 
     // ---- variable-pass classes and tree programs ----
-    std::vector<int32_t> slist, llist, lprog, glist, prog;
+    std::vector<int32_t> llist, lprog, glist, prog;
+    std::vector<int32_t> lvars[5], lvprog[5];
+    std::vector<SRun> sruns;
+    std::vector<SBlock> sblk[3];
     std::vector<GChunk> gchunks;
     std::vector<GComp> gcomps;
     std::vector<GWork> gwork;
@@ -556,16 +679,33 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     if (kChunk < kLeafMax || kChunk > kChunkMax || kSmallDeg > kSmallDegMax)
         return fail(FG_ERR_INVALID, "chunk must be in [128, 8192], small_degree in [1, 32]");
     int max_top = 1;
+    int64_t nsmall = 0, nlarge = 0;
     for (int64_t v = 0; v < V; ++v) {
         const int64_t dg = deg[v];
-        for (int64_t c = 0; c < dim[v]; ++c) {
-            const int32_t k = (int32_t)(zbase[v] + c);
-            if (dg <= kSmallDeg) {
-                slist.push_back(k);
-            } else if (dg - 1 <= kChunk) {
-                llist.push_back(k);
-                lprog.push_back(leaf_prog(dg - 1));
+        if (dg <= kSmallDeg) {
+            // runs of consecutive variables with one (dim, degree): their
+            // payload, edge and z bases are affine in the variable index
+            SRun* last = sruns.empty() ? nullptr : &sruns.back();
+            if (last && last->d == dim[v] && last->deg == dg &&
+                last->eb0 + (int64_t)last->nv * dg == ebase[v] && last->nv < (1 << 30)) {
+                last->nv++;
             } else {
+                sruns.push_back(SRun{pbase[v], zbase[v], ebase[v], 1, dim[v], (int32_t)dg});
+            }
+            nsmall += dim[v];
+        } else if (dg - 1 <= kChunk && dim[v] <= 4) {
+            lvars[dim[v]].push_back((int32_t)v);
+            lvprog[dim[v]].push_back(leaf_prog(dg - 1));
+            nlarge += dim[v];
+        } else {
+            for (int64_t c = 0; c < dim[v]; ++c) {
+                const int32_t k = (int32_t)(zbase[v] + c);
+                if (dg - 1 <= kChunk) {
+                    llist.push_back(k);
+                    lprog.push_back(leaf_prog(dg - 1));
+                    nlarge++;
+                    continue;
+                }
                 const int32_t gi = (int32_t)glist.size();
                 glist.push_back(k);
                 std::vector<std::pair<int64_t, int64_t>> chunks;
@@ -579,26 +719,46 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
             }
         }
     }
-    p->nS = (int64_t)slist.size();
+    for (size_t r = 0; r < sruns.size(); ++r) {
+        const int cls = sruns[r].deg <= kSmallTinyDeg ? 0 : (sruns[r].deg <= kSmallRegDeg ? 1 : 2);
+        const int64_t comps = (int64_t)sruns[r].nv * sruns[r].d;
+        if (comps >= INT32_MAX) return fail(FG_ERR_INVALID, "variable run exceeds 2^31 components");
+        for (int64_t c0 = 0; c0 < comps; c0 += kSmallCompsPerCta)
+            sblk[cls].push_back(SBlock{(int32_t)r, (int32_t)c0,
+                                       (int32_t)std::min<int64_t>(comps, c0 + kSmallCompsPerCta), 0});
+    }
+    p->nS = nsmall;
+    p->nLvars = nlarge;
     p->nL = (int64_t)llist.size();
     p->nG = (int64_t)glist.size();
     p->nGC = (int64_t)gchunks.size();
     p->nGW = (int64_t)gwork.size();
+    for (int c = 0; c < 3; ++c) p->nsblk[c] = (int64_t)sblk[c].size();
+    for (int d = 1; d <= 4; ++d) p->nlv[d] = (int64_t)lvars[d].size();
     p->gtop_smem = (int)(2 * max_top * sizeof(double));
     if ((size_t)p->gtop_smem > 48 * 1024) {
         CK(cudaFuncSetAttribute(k_var_giant_top<MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->gtop_smem));
         CK(cudaFuncSetAttribute(k_var_giant_top<MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->gtop_smem));
     }
-    if ((rc = upload(&p->d_slist, slist)) || (rc = upload(&p->d_llist, llist)) ||
+    if ((rc = upload(&p->d_sruns, sruns)) || (rc = upload(&p->d_sblk[0], sblk[0])) ||
+        (rc = upload(&p->d_sblk[1], sblk[1])) || (rc = upload(&p->d_sblk[2], sblk[2])) ||
+        (rc = upload(&p->d_llist, llist)) ||
         (rc = upload(&p->d_lprog, lprog)) || (rc = upload(&p->d_prog, prog)) ||
         (rc = upload(&p->d_glist, glist)) || (rc = upload(&p->d_gchunks, gchunks)) ||
         (rc = upload(&p->d_gcomps, gcomps)) || (rc = upload(&p->d_gwork, gwork)) ||
         (rc = dalloc(&p->d_csum, gchunks.size())) || (rc = dalloc(&p->d_gz, 2 * glist.size())))
         return rc;
-    p->part_S = nblk(p->nS, 256);
-    p->part_L = p->nL;
-    p->part_G = p->nGW;
-    p->npart = p->part_S + p->part_L + p->part_G;
+    for (int d = 1; d <= 4; ++d)
+        if ((rc = upload(&p->d_lvars[d], lvars[d])) || (rc = upload(&p->d_lvprog[d], lvprog[d])))
+            return rc;
+    // residual partial slots: one per CTA of every fused var kernel
+    int64_t acc_part = 0;
+    for (int w = 0; w < kVarSlots; ++w) {
+        p->part_off[w] = acc_part;
+        if (w == kSlotGiantChunks || w == kSlotGiantTop) continue;   // no partials
+        acc_part += var_slot_blocks(p.get(), w);
+    }
+    p->npart = acc_part;
     const int64_t nres = nblk(E, 256);
     if ((rc = dalloc(&p->d_part, 2 * std::max(p->npart, nres)))) return rc;
     CK(cudaMemset(p->d_part, 0, 2 * std::max(p->npart, nres) * sizeof(double)));
@@ -612,7 +772,7 @@ void fg_plan_destroy(fg_plan* plan) { delete plan; }
 
 int fg_plan_info(const fg_plan* p, int64_t* o) {
     o[0] = p->V; o[1] = p->E; o[2] = p->P; o[3] = p->Z;
-    o[4] = p->nS; o[5] = p->nL; o[6] = p->nG; o[7] = p->nGC;
+    o[4] = p->nS; o[5] = p->nLvars; o[6] = p->nG; o[7] = p->nGC;
     o[8] = p->launches_per_iter;
     return 0;
 }
@@ -938,9 +1098,8 @@ int fg_profile_kernels(fg_plan* p, int64_t iterations, int32_t max_slots,
         if (g.dev.count > 0) names.push_back(std::string("edge_") + kind_name(g.dev.kind));
     const int nedge = (int)names.size();
     std::vector<int> vk;
-    for (int w = 0; w < 5; ++w) {
-        const bool has = (w == 0 && p->nS) || (w == 1 && p->nL) || (w >= 2 && p->nG);
-        if (has) { vk.push_back(w); names.push_back(kVarNames[w]); }
+    for (int w = 0; w < kVarSlots; ++w) {
+        if (var_slot_blocks(p, w) > 0) { vk.push_back(w); names.push_back(kVarNames[w]); }
     }
     names.push_back("reduce");
     const int ns = (int)names.size();
@@ -1038,7 +1197,7 @@ int fg_prox_eval(const fg_group_desc* gd, const double* values, const double* rh
             }
         for (int64_t i = 0; i < n; ++i) fe[i] = i * ns;
         g2.first_edge = fe.data();
-        if ((rc = build_group(&tmp, g2, ev, vo, ebase, gh))) return rc;
+        if ((rc = build_group(&tmp, g2, ev, vo, ebase, pbase, zbase, gh))) return rc;
     }
     double *d_vals, *d_rho, *d_out;
     if ((rc = dalloc(&d_vals, P)) || (rc = dalloc(&d_rho, V)) || (rc = dalloc(&d_out, P)))
