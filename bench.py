@@ -317,7 +317,7 @@ def main():
     iter_ms = sum(v[0] for v in prof.values()) / prof[top][1]
 
     # ---- end to end through the public API (host state in, host state out) ----
-    s = fg.AdmmState(*(getattr(st, k).copy() for k in "xmzun"))
+    s = fg.pinned_state(g, st)                     # page-locked host arrays
     t0 = time.perf_counter()
     fg.run(g, fg.RunConfig(max_iterations=args.steps), state=s)
     e2e_s = time.perf_counter() - t0
@@ -326,8 +326,9 @@ def main():
     d2h = (4 * P + Z) * 8
     e2e = {"value": E * args.steps * world / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
-           "note": f"one run() call of {args.steps} iterations: upload z,u,n, "
-                   f"download x,m,z,u,n (bytes amortized per step)"}
+           "note": f"one run() call of {args.steps} iterations on a pinned host "
+                   f"AdmmState: upload z,u,n, download x,m,z,u,n (bytes amortized "
+                   f"per step); wall clock"}
 
     if rank != 0:
         if dist:

@@ -179,6 +179,10 @@ int fg_residuals(fg_plan* plan, const double* x, const double* z,
 int fg_prox_eval(const fg_group_desc* group, const double* values,
                  const double* rhos, double* out, int32_t device);
 
+/* ---- pinned host memory (state arrays that stream at full PCIe rate) --- */
+int fg_host_alloc(int64_t bytes, void** out);
+int fg_host_free(void* ptr);
+
 /* ---- misc --------------------------------------------------------------- */
 const char* fg_last_error(void);
 int fg_abi_version(void);

@@ -15,6 +15,7 @@ from .engine import (
     device_plan,
     init_state,
     iterate,
+    pinned_state,
     residuals,
     run,
     update_m,

@@ -76,6 +76,8 @@ EXPORTS = {
     "fg_phase_download": (C.c_int, [_p, _dp, _dp, _dp, _dp, _dp]),
     "fg_residuals": (C.c_int, [_p, _dp, _dp, _dp, _dp, _dp]),
     "fg_prox_eval": (C.c_int, [C.POINTER(GroupDesc), _dp, _dp, _dp, C.c_int32]),
+    "fg_host_alloc": (C.c_int, [C.c_int64, C.POINTER(_p)]),
+    "fg_host_free": (C.c_int, [_p]),
     "fg_last_error": (C.c_char_p, []),
     "fg_abi_version": (C.c_int, []),
     "fg_device_count": (C.c_int, [_i32p]),
@@ -191,3 +193,35 @@ def prox_eval(cls, params, dims, values, rhos, device=0):
         res.append(out[off:off + B * d].reshape(B, d))
         off += B * d
     return res
+
+
+class _PinnedBlock:
+    """Owner of one cudaHostAlloc block; freed when the last view dies."""
+
+    def __init__(self, nbytes):
+        self.ptr = C.c_void_p()
+        check(load().fg_host_alloc(int(nbytes), C.byref(self.ptr)))
+        self.nbytes = int(nbytes)
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and self.ptr.value:
+            try:
+                load().fg_host_free(self.ptr)
+            except Exception:
+                pass
+            self.ptr = None
+
+
+def pinned_empty(shape, dtype=np.float64):
+    """A numpy array in page-locked host memory (full-rate PCIe copies)."""
+    dtype = np.dtype(dtype)
+    n = int(np.prod(shape)) if np.ndim(shape) else int(shape)
+    nbytes = max(1, n * dtype.itemsize)
+    block = _PinnedBlock(nbytes)
+    buf = (C.c_char * nbytes).from_address(block.ptr.value)
+    arr = np.frombuffer(buf, dtype=dtype, count=n).reshape(shape)
+    arr.flags.writeable = True
+    buf._fg_block = block          # keep the allocation alive with the view
+    return arr
+
+

@@ -1222,3 +1222,19 @@ int fg_prox_eval(const fg_group_desc* gd, const double* values, const double* rh
 }
 
 }  // extern "C"
+
+extern "C" {
+
+int fg_host_alloc(int64_t bytes, void** out) {
+    *out = nullptr;
+    if (bytes <= 0) return fail(FG_ERR_INVALID, "allocation size must be positive");
+    CK(cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable));
+    return 0;
+}
+
+int fg_host_free(void* ptr) {
+    if (ptr) CK(cudaFreeHost(ptr));
+    return 0;
+}
+
+}  // extern "C"

@@ -119,6 +119,20 @@ def init_state(graph, seed=None):
     return AdmmState(x=np.zeros(P), m=np.zeros(P), z=z, u=u, n=n)
 
 
+def pinned_state(graph, state=None, seed=None):
+    """An AdmmState whose five arrays live in page-locked host memory, so
+    ``run`` streams them at full PCIe bandwidth; copies ``state`` (or a
+    fresh ``init_state(graph, seed)``) into it."""
+    src = state if state is not None else init_state(graph, seed)
+    arrs = {}
+    for k in ("x", "m", "z", "u", "n"):
+        a = getattr(src, k)
+        p = _native.pinned_empty(a.shape)
+        p[...] = a
+        arrs[k] = p
+    return AdmmState(**arrs, iteration=src.iteration, last_residuals=src.last_residuals)
+
+
 # ---------------------------------------------------------------------------
 # device plan
 
