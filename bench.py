@@ -139,56 +139,55 @@ REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
 
 
 class ClockSampler:
-    def __init__(self, index=0):
+    """SM clock and throttle reasons sampled every 5 ms through NVML while
+    the timed region runs (the recipe's clocks line)."""
+
+    def __init__(self, index=0, period=0.005):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.period = period
+        self.samples = []
+        self.max_mhz = None
+        self._stop = threading.Event()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index),
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,utilization.gpu",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except (FileNotFoundError, OSError):
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
+            self._t = threading.Thread(target=self._loop, daemon=True)
+            self._t.start()
+        except Exception:
+            self._nv = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _loop(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.samples.append((float(sm), int(rs)))
+            except Exception:
+                break
+            time.sleep(self.period)
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self._stop.set()
+        if getattr(self, "_t", None) is not None:
+            self._t.join(timeout=1.0)
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        for line in self.lines:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 4:
-                continue
-            try:
-                s, m, util = float(parts[0]), float(parts[1]), float(parts[3])
-                mask = int(parts[2], 16)
-            except ValueError:
-                continue
-            mx = max(mx, m)
-            if util > 0:
-                sm.append(s)
-                for bit, name in REASONS.items():
-                    if mask & bit:
-                        reasons.add(name)
+        reasons = set()
+        for _sm, mask in self.samples:
+            for bit, name in REASONS.items():
+                if mask & bit:
+                    reasons.add(name)
+        sm = [s for s, _m in self.samples]
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": mx or None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
+                "samples": len(sm), "source": "nvml"}
 
 
 # ---------------------------------------------------------------------------
@@ -258,6 +257,46 @@ def reference_arm(args):
     return 0
 
 
+def multi_gpu(args, fg, dist, rank, world, local):
+    """N ranks over NCCL: the graph is partitioned by factors (cut variables
+    all-gather their partial sums inside the iteration).  Strong scaling:
+    every N runs the same whole graph; value = its edges x K / max-rank time."""
+    import torch
+    from paper_1603_02526_b200.distributed import NcclRank
+    t_build = time.perf_counter()
+    g, st, info = build_instance(args.workload)
+    nr = NcclRank(g, rank, world, device=local)
+    t_build = time.perf_counter() - t_build
+    E = len(g.edge_var)
+    nr.upload(st)
+    nr.run(args.warmup)
+    nr.upload(st)
+    torch.cuda.synchronize()
+    dist.barrier()
+    with ClockSampler(local) as clk:
+        res, _hist = nr.run(args.steps)
+    t = torch.tensor([res.ms_total], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = E * args.steps / (ms / 1e3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "desc": WORKLOADS[args.workload], **info,
+                   "edges": E, "parallelism": f"factor partition x{world} (NCCL all-gather "
+                                              f"of {nr.part.ncut} cut components)",
+                   "local_edges": len(nr.local.edge_var), "build_seconds": round(t_build, 2)},
+        "gpu_launches": int(res.launches), "clocks": clk.summary(),
+        "converged": bool(res.converged),
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -282,6 +321,8 @@ def main():
         dist.init_process_group("nccl")
 
     import paper_1603_02526_b200 as fg
+    if world > 1:
+        return multi_gpu(args, fg, dist, rank, world, local)
     t_build = time.perf_counter()
     g, st, info = build_instance(args.workload)
     plan = fg.device_plan(g)

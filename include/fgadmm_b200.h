@@ -89,6 +89,12 @@ typedef struct {
                                     (128..8192; 0 = 8192)               */
     int32_t small_degree;        /* max degree summed by one thread
                                     (1..32; 0 = 32)                     */
+    /* Multi-GPU partitions.  For a rank's LOCAL graph:
+     * z_cut_index[k] is the position of local z component k in the
+     * all-gathered cut vector (-1: variable not cut), ncut its length.
+     * NULL / 0 for a whole graph. */
+    const int32_t* z_cut_index;
+    int64_t ncut;
 } fg_graph_desc;
 
 /* One homogeneous factor batch: one (kind, slot dims) group, as
@@ -178,6 +184,21 @@ int fg_residuals(fg_plan* plan, const double* x, const double* z,
  * slot after slot; rhos: (nslots, count); out like values. */
 int fg_prox_eval(const fg_group_desc* group, const double* values,
                  const double* rhos, double* out, int32_t device);
+
+/* ---- multi-GPU exchange of cut-variable partial sums ------------------- */
+/* NCCL (one process per GPU): rank 0 calls fg_nccl_unique_id, the id is
+ * broadcast by the caller (e.g. torch.distributed), every rank attaches it
+ * to its plan; fg_run then all-gathers the cut partials and the residual
+ * partials inside the iteration (captured in the CUDA graph).  `nccl_lib`
+ * is the libnccl.so.2 to dlopen (NULL: default search path). */
+int fg_nccl_unique_id(const char* nccl_lib, char* out128);
+int fg_plan_attach_nccl(fg_plan* plan, const char* nccl_lib, const char* id128,
+                        int32_t rank, int32_t world);
+/* Local group: the G partition plans of one graph on ONE device, exchanged
+ * by device copies (single-GPU validation of the partitioned algorithm).
+ * Results are those of rank 0 (identical on all ranks). */
+int fg_group_run(fg_plan** plans, int32_t nplans, const fg_run_config* cfg,
+                 double* history, fg_run_result* out);
 
 /* ---- pinned host memory (state arrays that stream at full PCIe rate) --- */
 int fg_host_alloc(int64_t bytes, void** out);

@@ -282,3 +282,38 @@ def time_iterations(graph, state, iterations, oracle=None):
     for _ in range(iterations):
         o.iterate(s)
     return (time.perf_counter() - t0) / iterations, s
+
+
+# ---------------------------------------------------------------------------
+# partitioned restatement (checker for the multi-GPU protocol)
+
+def run_partitioned(lg, iterations, state, allgather):
+    """The five phases on one rank's LocalGraph ``lg``: non-cut variables
+    as in ``Oracle``; cut variables from the rank-order sum of all-gathered
+    local partials.  ``allgather(vec) -> [vec_rank0, vec_rank1, ...]``.
+    Returns (local state, [(primal, dual)])."""
+    from paper_1603_02526_b200.partition import combine_partials, local_partial_sums
+    o = Oracle(lg)
+    s = State.copy_of(state)
+    cut = lg.cut_index >= 0
+    P_global = None
+    hist = []
+    for _ in range(iterations):
+        z_prev = s.z.copy()
+        o.phase_x(s)
+        o.phase_m(s)
+        o.phase_z(s)
+        if lg.ncut:
+            tot = combine_partials(allgather(local_partial_sums(lg, s.m)))
+            s.z[cut] = tot[lg.cut_index[cut]] / lg.z_weights[cut]
+        o.phase_u(s)
+        o.phase_n(s)
+        d1 = s.x - s.z[lg.zmap]
+        d2 = lg.rho_flat * (s.z - z_prev)[lg.zmap]
+        parts = allgather(np.array([float(d1 @ d1), float(d2 @ d2),
+                                    float(lg.total_edge_payload)]))
+        tot = combine_partials(parts)
+        P_global = tot[2]
+        scale = 1.0 / np.sqrt(P_global)
+        hist.append((float(np.sqrt(tot[0]) * scale), float(np.sqrt(tot[1]) * scale)))
+    return s, hist

@@ -32,7 +32,8 @@ class GraphDesc(C.Structure):
                 ("payload", C.c_int64), ("z_dim", C.c_int64),
                 ("var_dim", _i32p), ("var_offsets", _i64p),
                 ("edge_var", _i32p), ("edge_offsets", _i64p),
-                ("chunk", C.c_int32), ("small_degree", C.c_int32)]
+                ("chunk", C.c_int32), ("small_degree", C.c_int32),
+                ("z_cut_index", _i32p), ("ncut", C.c_int64)]
 
 
 class GroupDesc(C.Structure):
@@ -76,6 +77,10 @@ EXPORTS = {
     "fg_phase_download": (C.c_int, [_p, _dp, _dp, _dp, _dp, _dp]),
     "fg_residuals": (C.c_int, [_p, _dp, _dp, _dp, _dp, _dp]),
     "fg_prox_eval": (C.c_int, [C.POINTER(GroupDesc), _dp, _dp, _dp, C.c_int32]),
+    "fg_nccl_unique_id": (C.c_int, [C.c_char_p, C.c_char_p]),
+    "fg_plan_attach_nccl": (C.c_int, [_p, C.c_char_p, C.c_char_p, C.c_int32, C.c_int32]),
+    "fg_group_run": (C.c_int, [C.POINTER(_p), C.c_int32, C.POINTER(RunConfig), _dp,
+                               C.POINTER(RunResult)]),
     "fg_host_alloc": (C.c_int, [C.c_int64, C.POINTER(_p)]),
     "fg_host_free": (C.c_int, [_p]),
     "fg_last_error": (C.c_char_p, []),

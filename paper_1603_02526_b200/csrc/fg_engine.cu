@@ -171,6 +171,16 @@ struct fg_plan {
     GWork* d_gwork = nullptr; int64_t nGW = 0;
     double* d_csum = nullptr;
     double* d_gz = nullptr;
+    // partitioned runs: cut components exchange partial sums
+    int64_t ncut = 0;                  // length of the canonical cut vector
+    int32_t world = 1, rank = 0;
+    int32_t* d_cutg = nullptr;         // giant-list indices of cut components
+    int64_t ncutg = 0;
+    double* d_send = nullptr;          // [ncut] partials, then [4] residuals
+    double* d_recv = nullptr;          // [world*ncut], then [world*4]
+    void* nccl_comm = nullptr;         // ncclComm_t when attached
+    int64_t Pglobal = 0;               // payload of the whole graph
+    bool partitioned() const { return ncut > 0 || world > 1; }
     // residual partials
     int64_t part_S = 0, part_L = 0, part_G = 0, npart = 0;
     double* d_part = nullptr;
@@ -189,8 +199,11 @@ struct fg_plan {
     ~fg_plan();
 };
 
+void fg_nccl_release(void* comm);   // defined with the NCCL loader below
+
 fg_plan::~fg_plan() {
     cudaSetDevice(device);
+    if (nccl_comm) fg_nccl_release(nccl_comm);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     void* ptrs[] = {d_dim, d_deg, d_ebase, d_pbase, d_zbase, d_zvar, d_vm2ref,
                     d_vmz, d_vmvar, d_refedge, d_rho, d_alpha, d_zw, d_x,
@@ -198,7 +211,8 @@ fg_plan::~fg_plan() {
                     d_sblk[0], d_sblk[1], d_sblk[2], d_lvars[1], d_lvars[2], d_lvars[3],
                     d_lvars[4], d_lvprog[1], d_lvprog[2], d_lvprog[3], d_lvprog[4],
                     d_llist, d_lprog, d_prog, d_glist, d_gchunks, d_gcomps,
-                    d_gwork, d_csum, d_gz, d_part, d_res2, d_ctrl, d_hist};
+                    d_gwork, d_csum, d_gz, d_part, d_res2, d_ctrl, d_hist,
+                    d_cutg, d_send, d_recv};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& g : groups)
@@ -317,7 +331,7 @@ bool var_kernel(fg_plan* p, int which, const double* uin, double* uout,
             return true;
         case kSlotGiantTop:
             k_var_giant_top<MODE><<<grid, kVarThreads, p->gtop_smem, st>>>(
-                b, p->d_glist, p->d_gcomps, p->d_prog, p->d_csum, p->d_gz);
+                b, p->d_glist, p->d_gcomps, p->d_prog, p->d_csum, p->d_gz, p->d_send);
             return true;
         case kSlotGiantUpdate:
             if (MODE != MODE_FUSED) return false;
@@ -366,7 +380,50 @@ int64_t count_var_launches(const fg_plan* p) {
 
 // One fused iteration.  Iteration j (1-based within a run) reads u[(j-1)&1]
 // and writes u[j&1].
+// ---- partitioned iteration pieces ------------------------------------------
+// The exchange between ranks is pluggable: NCCL all-gathers on the plan's
+// stream (captured into the CUDA graph), or device copies inside one
+// process for a local group of plans (fg_group_run).
+int exchange_nccl(fg_plan* p, const double* send, double* recv, size_t count,
+                  cudaStream_t st);
+
+void cut_finalize(fg_plan* p, const double* uin, double* uout, cudaStream_t st) {
+    if (!p->ncutg) return;
+    PassB b{p->vt(), p->d_x, uin, uout, nullptr, p->d_z, p->d_rho, p->d_alpha,
+            p->d_zw, p->d_ctrl, p->d_part, p->d_zvar};
+    k_cut_finalize<<<nblk(p->ncutg, 256), 256, 0, st>>>(
+        b, p->d_glist, p->d_gcomps, p->d_cutg, p->ncutg, p->d_recv, p->world,
+        p->ncut, p->d_gz);
+}
+
+// Everything of a partitioned iteration up to the cut exchange.
+void part_pre(fg_plan* p, int in, bool first, cudaStream_t st) {
+    edge_pass(p, first, p->d_u[in], first ? p->d_u[1 - in] : nullptr, st);
+    for (int w = 0; w < kVarSlots; ++w)
+        if (w != kSlotGiantUpdate) var_kernel<MODE_FUSED>(p, w, p->d_u[in], p->d_u[1 - in], nullptr, st);
+}
+
+// After the cut exchange, up to the residual exchange.
+void part_mid(fg_plan* p, int in, cudaStream_t st) {
+    cut_finalize(p, p->d_u[in], p->d_u[1 - in], st);
+    var_kernel<MODE_FUSED>(p, kSlotGiantUpdate, p->d_u[in], p->d_u[1 - in], nullptr, st);
+    k_reduce_local<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_send + p->ncut);
+}
+
+void part_post(fg_plan* p, cudaStream_t st) {
+    k_reduce_final<<<1, 32, 0, st>>>(p->d_ctrl, p->d_recv + (size_t)p->world * p->ncut,
+                                     p->world, p->d_hist);
+}
+
 void launch_iteration(fg_plan* p, int in, bool first, cudaStream_t st) {
+    if (p->nccl_comm) {
+        part_pre(p, in, first, st);
+        if (p->ncut) exchange_nccl(p, p->d_send, p->d_recv, (size_t)p->ncut, st);
+        part_mid(p, in, st);
+        exchange_nccl(p, p->d_send + p->ncut, p->d_recv + (size_t)p->world * p->ncut, 4, st);
+        part_post(p, st);
+        return;
+    }
     edge_pass(p, first, p->d_u[in], first ? p->d_u[1 - in] : nullptr, st);
     var_pass<MODE_FUSED>(p, p->d_u[in], p->d_u[1 - in], nullptr, st);
     k_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_hist);
@@ -666,6 +723,7 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     std::vector<GChunk> gchunks;
     std::vector<GComp> gcomps;
     std::vector<GWork> gwork;
+    std::vector<int32_t> cutg;
     std::map<int64_t, int32_t> leafprog;   // n -> offset
     auto leaf_prog = [&](int64_t n) -> int32_t {
         auto it = leafprog.find(n);
@@ -682,7 +740,27 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     int64_t nsmall = 0, nlarge = 0;
     for (int64_t v = 0; v < V; ++v) {
         const int64_t dg = deg[v];
-        if (dg <= kSmallDeg) {
+        const int32_t cut0 = gd->z_cut_index ? gd->z_cut_index[zbase[v]] : -1;
+        if (cut0 >= 0) {
+            // a rank's local part of a cut segment: the whole local tree
+            // (from element 0) is summed into the exchange vector
+            for (int64_t c = 0; c < dim[v]; ++c) {
+                const int32_t cidx = gd->z_cut_index[zbase[v] + c];
+                if (cidx < 0 || cidx >= gd->ncut)
+                    return fail(FG_ERR_INVALID, "inconsistent z_cut_index");
+                const int32_t gi = (int32_t)glist.size();
+                glist.push_back((int32_t)(zbase[v] + c));
+                cutg.push_back(gi);
+                std::vector<std::pair<int64_t, int64_t>> chunks;
+                const int32_t top = (int32_t)emit_program(dg, kChunk, prog, &chunks);
+                gcomps.push_back(GComp{top, (int32_t)gchunks.size(), cidx, 0});
+                max_top = std::max(max_top, (int)chunks.size());
+                for (auto& ch : chunks)
+                    gchunks.push_back(GChunk{gi, (int32_t)ch.first, leaf_prog(ch.second), 0});
+                for (int64_t e0 = 0; e0 < dg; e0 += kGiantWork)
+                    gwork.push_back(GWork{gi, (int32_t)e0, (int32_t)std::min<int64_t>(dg, e0 + kGiantWork), 0});
+            }
+        } else if (dg <= kSmallDeg) {
             // runs of consecutive variables with one (dim, degree): their
             // payload, edge and z bases are affine in the variable index
             SRun* last = sruns.empty() ? nullptr : &sruns.back();
@@ -710,15 +788,21 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
                 glist.push_back(k);
                 std::vector<std::pair<int64_t, int64_t>> chunks;
                 const int32_t top = (int32_t)emit_program(dg - 1, kChunk, prog, &chunks);
-                gcomps.push_back(GComp{top, (int32_t)gchunks.size(), 0, 0});
+                gcomps.push_back(GComp{top, (int32_t)gchunks.size(), -1, 0});
                 max_top = std::max(max_top, (int)chunks.size());
                 for (auto& ch : chunks)
-                    gchunks.push_back(GChunk{gi, (int32_t)ch.first, leaf_prog(ch.second), 0});
+                    gchunks.push_back(GChunk{gi, (int32_t)ch.first, leaf_prog(ch.second), 1});
                 for (int64_t e0 = 0; e0 < dg; e0 += kGiantWork)
                     gwork.push_back(GWork{gi, (int32_t)e0, (int32_t)std::min<int64_t>(dg, e0 + kGiantWork), 0});
             }
         }
     }
+    p->ncut = gd->z_cut_index ? gd->ncut : 0;
+    p->ncutg = (int64_t)cutg.size();
+    if ((rc = upload(&p->d_cutg, cutg)) || (rc = dalloc(&p->d_send, p->ncut + 4)) ||
+        (rc = dalloc(&p->d_recv, (p->ncut + 4) * 8)))   // re-sized on attach
+        return rc;
+    CK(cudaMemset(p->d_send, 0, (p->ncut + 4) * sizeof(double)));
     for (size_t r = 0; r < sruns.size(); ++r) {
         const int cls = sruns[r].deg <= kSmallTinyDeg ? 0 : (sruns[r].deg <= kSmallRegDeg ? 1 : 2);
         const int64_t comps = (int64_t)sruns[r].nv * sruns[r].d;
@@ -836,7 +920,21 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
     h.dual_tol = cfg->dual_tol;
     h.scale = 1.0 / std::sqrt((double)p->P);
     h.max_iter = K;
+    if (p->ncut && !p->nccl_comm)
+        return fail(FG_ERR_INVALID, "a partition plan runs through fg_plan_attach_nccl + "
+                                    "fg_run or through fg_group_run");
+    if (p->nccl_comm) {
+        h.partitioned = 1;
+        h.scale = 1.0 / std::sqrt((double)p->Pglobal);
+    }
     CK(cudaMemcpyAsync(p->d_ctrl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+    if (!cfg->timing && K > 1) {
+        // capture/instantiate the CUDA graphs this run needs before timing
+        const int chunk = std::max(2, cfg->graph_chunk - (cfg->graph_chunk & 1));
+        cudaGraphExec_t gx;
+        if (K - 1 >= chunk) { if (int rc = get_graph(p, chunk, &gx)) return rc; }
+        if ((K - 1) % chunk >= 2) { if (int rc = get_graph(p, 2, &gx)) return rc; }
+    }
 
     cudaEvent_t ev0, ev1;
     CK(cudaEventCreate(&ev0));
@@ -844,7 +942,14 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
     double ms_a = 0, ms_b = 0, ms_r = 0;
     int64_t launches = 0;
     CK(cudaEventRecord(ev0, st));
-    if (cfg->timing) {
+    if (cfg->timing && p->nccl_comm) {
+        for (int64_t j = 1; j <= K; ++j) {
+            launch_iteration(p, (int)((j - 1) & 1), (j == 1) && cfg->first_reads_n, st);
+            launches += p->launches_per_iter + 1;
+        }
+        CK(cudaEventRecord(ev1, st));
+        CK(cudaStreamSynchronize(st));
+    } else if (cfg->timing) {
         // direct launches with events around each pass of every iteration
         std::vector<cudaEvent_t> ev(4 * K);
         for (auto& e : ev) CK(cudaEventCreate(&e));
@@ -879,12 +984,18 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
         cudaEvent_t e4[4];
         for (auto& e : e4) CK(cudaEventCreate(&e));
         CK(cudaEventRecord(e4[0], st));
-        edge_pass(p, cfg->first_reads_n != 0, p->d_u[0],
-                  cfg->first_reads_n ? p->d_u[1] : nullptr, st);
-        CK(cudaEventRecord(e4[1], st));
-        var_pass<MODE_FUSED>(p, p->d_u[0], p->d_u[1], nullptr, st);
-        CK(cudaEventRecord(e4[2], st));
-        k_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_hist);
+        if (p->nccl_comm) {
+            launch_iteration(p, 0, cfg->first_reads_n != 0, st);
+            CK(cudaEventRecord(e4[1], st));
+            CK(cudaEventRecord(e4[2], st));
+        } else {
+            edge_pass(p, cfg->first_reads_n != 0, p->d_u[0],
+                      cfg->first_reads_n ? p->d_u[1] : nullptr, st);
+            CK(cudaEventRecord(e4[1], st));
+            var_pass<MODE_FUSED>(p, p->d_u[0], p->d_u[1], nullptr, st);
+            CK(cudaEventRecord(e4[2], st));
+            k_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_hist);
+        }
         CK(cudaEventRecord(e4[3], st));
         launches += p->launches_per_iter;
         int64_t left = K - 1;
@@ -1234,6 +1345,208 @@ int fg_host_alloc(int64_t bytes, void** out) {
 
 int fg_host_free(void* ptr) {
     if (ptr) CK(cudaFreeHost(ptr));
+    return 0;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// Multi-GPU exchange
+// ===========================================================================
+#include <dlfcn.h>
+
+namespace {
+
+struct NcclId { char internal[128]; };
+struct NcclApi {
+    void* h = nullptr;
+    int (*GetUniqueId)(NcclId*) = nullptr;
+    int (*CommInitRank)(void**, int, NcclId, int) = nullptr;
+    int (*AllGather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+    int (*CommDestroy)(void*) = nullptr;
+    const char* (*GetErrorString)(int) = nullptr;
+};
+NcclApi g_nccl;
+constexpr int kNcclFloat64 = 8;
+
+int nccl_load(const char* lib) {
+    if (g_nccl.h) return 0;
+    void* h = dlopen(lib && *lib ? lib : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return fail(FG_ERR_CUDA, std::string("cannot load NCCL: ") + dlerror());
+    g_nccl.GetUniqueId = (int (*)(NcclId*))dlsym(h, "ncclGetUniqueId");
+    g_nccl.CommInitRank = (int (*)(void**, int, NcclId, int))dlsym(h, "ncclCommInitRank");
+    g_nccl.AllGather = (int (*)(const void*, void*, size_t, int, void*, cudaStream_t))dlsym(h, "ncclAllGather");
+    g_nccl.CommDestroy = (int (*)(void*))dlsym(h, "ncclCommDestroy");
+    g_nccl.GetErrorString = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+    if (!g_nccl.GetUniqueId || !g_nccl.CommInitRank || !g_nccl.AllGather || !g_nccl.CommDestroy)
+        return fail(FG_ERR_CUDA, "NCCL library lacks the required symbols");
+    g_nccl.h = h;
+    return 0;
+}
+
+int nccl_check(int r, const char* what) {
+    if (r == 0) return 0;
+    return fail(FG_ERR_CUDA, std::string(what) + ": " +
+                (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "NCCL error"));
+}
+
+}  // namespace
+
+void fg_nccl_release(void* comm) {
+    if (g_nccl.CommDestroy && comm) g_nccl.CommDestroy(comm);
+}
+
+namespace {
+int exchange_nccl(fg_plan* p, const double* send, double* recv, size_t count, cudaStream_t st) {
+    return nccl_check(g_nccl.AllGather(send, recv, count, kNcclFloat64, p->nccl_comm, st),
+                      "ncclAllGather");
+}
+}  // namespace
+
+extern "C" {
+
+int fg_nccl_unique_id(const char* nccl_lib, char* out128) {
+    if (int rc = nccl_load(nccl_lib)) return rc;
+    NcclId id;
+    if (int rc = nccl_check(g_nccl.GetUniqueId(&id), "ncclGetUniqueId")) return rc;
+    std::memcpy(out128, id.internal, 128);
+    return 0;
+}
+
+int fg_plan_attach_nccl(fg_plan* p, const char* nccl_lib, const char* id128, int32_t rank,
+                        int32_t world) {
+    CK(cudaSetDevice(p->device));
+    if (int rc = nccl_load(nccl_lib)) return rc;
+    if (world < 1 || rank < 0 || rank >= world) return fail(FG_ERR_INVALID, "bad rank/world");
+    NcclId id;
+    std::memcpy(id.internal, id128, 128);
+    void* comm = nullptr;
+    if (int rc = nccl_check(g_nccl.CommInitRank(&comm, world, id, rank), "ncclCommInitRank"))
+        return rc;
+    p->nccl_comm = comm;
+    p->world = world;
+    p->rank = rank;
+    {   // global payload = sum of the ranks' local payloads (disjoint edges)
+        double* d_pp = nullptr;
+        if (int rc = dalloc(&d_pp, 1 + (size_t)world)) return rc;
+        const double mine = (double)p->P;
+        CK(cudaMemcpy(d_pp, &mine, sizeof(double), cudaMemcpyHostToDevice));
+        if (int rc = exchange_nccl(p, d_pp, d_pp + 1, 1, p->stream)) return rc;
+        std::vector<double> all(world);
+        CK(cudaMemcpyAsync(all.data(), d_pp + 1, world * sizeof(double), cudaMemcpyDeviceToHost,
+                           p->stream));
+        CK(cudaStreamSynchronize(p->stream));
+        cudaFree(d_pp);
+        double tot = 0;
+        for (double v : all) tot += v;
+        p->Pglobal = (int64_t)tot;
+    }
+    if (p->d_recv) cudaFree(p->d_recv);
+    p->d_recv = nullptr;
+    if (int rc = dalloc(&p->d_recv, (size_t)world * (p->ncut + 4))) return rc;
+    for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
+    p->graphs.clear();
+    return 0;
+}
+
+// Local group: G partition plans on one device, one stream (plan 0's),
+// exchange by device copies.  Direct launches, iteration by iteration.
+int fg_group_run(fg_plan** plans, int32_t G, const fg_run_config* cfg, double* history,
+                 fg_run_result* out) {
+    if (G < 1) return fail(FG_ERR_INVALID, "empty group");
+    fg_plan* p0 = plans[0];
+    CK(cudaSetDevice(p0->device));
+    const int64_t K = cfg->max_iterations;
+    if (K < 1) return fail(FG_ERR_INVALID, "max_iterations must be >= 1");
+    const int64_t ncut = p0->ncut;
+    for (int r = 0; r < G; ++r) {
+        fg_plan* p = plans[r];
+        if (p->device != p0->device || p->ncut != ncut)
+            return fail(FG_ERR_INVALID, "group plans must share one device and cut vector");
+        p->world = G;
+        p->rank = r;
+        if (p->d_recv) cudaFree(p->d_recv);
+        p->d_recv = nullptr;
+        if (int rc = dalloc(&p->d_recv, (size_t)G * (ncut + 4))) return rc;
+        if (p->hist_cap < K) {
+            if (p->d_hist) cudaFree(p->d_hist);
+            p->d_hist = nullptr;
+            if (int rc = dalloc(&p->d_hist, 2 * K)) return rc;
+            p->hist_cap = K;
+        }
+        Ctrl h{};
+        h.err_key = ~0ull;
+        h.iter = 1;
+        h.primal_tol = cfg->primal_tol;
+        h.dual_tol = cfg->dual_tol;
+        h.scale = 1.0 / std::sqrt((double)0 + 1.0);   // set below
+        h.max_iter = K;
+        h.partitioned = 1;
+        // global P = sum of local payloads (edges are disjoint across ranks)
+        int64_t Ptot = 0;
+        for (int q = 0; q < G; ++q) Ptot += plans[q]->P;
+        h.scale = 1.0 / std::sqrt((double)Ptot);
+        CK(cudaMemcpy(p->d_ctrl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice));
+    }
+    cudaStream_t st = p0->stream;
+    CK(cudaDeviceSynchronize());
+    cudaEvent_t ev0, ev1;
+    CK(cudaEventCreate(&ev0));
+    CK(cudaEventCreate(&ev1));
+    CK(cudaEventRecord(ev0, st));
+    int64_t launches = 0;
+    auto gather = [&](size_t off_send, size_t count, size_t off_recv) -> int {
+        for (int q = 0; q < G; ++q)
+            for (int r = 0; r < G; ++r)
+                CK(cudaMemcpyAsync(plans[q]->d_recv + off_recv + (size_t)r * count,
+                                   plans[r]->d_send + off_send, count * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, st));
+        return 0;
+    };
+    for (int64_t j = 1; j <= K; ++j) {
+        const int in = (int)((j - 1) & 1);
+        const bool first = (j == 1) && cfg->first_reads_n;
+        for (int r = 0; r < G; ++r) part_pre(plans[r], in, first, st);
+        if (ncut) { if (int rc = gather(0, (size_t)ncut, 0)) return rc; }
+        for (int r = 0; r < G; ++r) part_mid(plans[r], in, st);
+        if (int rc = gather((size_t)ncut, 4, (size_t)G * ncut)) return rc;
+        for (int r = 0; r < G; ++r) part_post(plans[r], st);
+        for (int r = 0; r < G; ++r) launches += plans[r]->launches_per_iter + 1;
+        if ((j & 15) == 0 || j == K) {   // stop early once every rank stopped
+            int32_t stop = 0;
+            CK(cudaMemcpyAsync(&stop, &p0->d_ctrl->stop, sizeof(int32_t),
+                               cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            if (stop == 1) break;
+        }
+    }
+    CK(cudaEventRecord(ev1, st));
+    CK(cudaStreamSynchronize(st));
+    if (int rc = check_launch()) return rc;
+    float tot = 0;
+    cudaEventElapsedTime(&tot, ev0, ev1);
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    Ctrl h;
+    for (int r = 0; r < G; ++r) {
+        CK(cudaMemcpy(&h, plans[r]->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+        plans[r]->completed = h.completed;
+    }
+    CK(cudaMemcpy(&h, p0->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+    std::memset(out, 0, sizeof(*out));
+    out->iterations = h.completed;
+    out->converged = h.converged;
+    out->primal = h.primal;
+    out->dual = h.dual;
+    out->error_phase = -1;
+    if (h.err_key != ~0ull) {
+        out->error_phase = (int32_t)(h.err_key & 7ull);
+        out->error_iteration = (int64_t)(h.err_key >> 3);
+    }
+    out->ms_total = tot;
+    out->launches = launches;
+    if (history && h.completed > 0)
+        CK(cudaMemcpy(history, p0->d_hist, 2 * h.completed * sizeof(double), cudaMemcpyDeviceToHost));
     return 0;
 }
 

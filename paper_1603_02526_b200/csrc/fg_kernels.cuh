@@ -234,18 +234,22 @@ __global__ void __launch_bounds__(kVarThreads) k_var_giant_chunks(
     const CompRef r = comp_ref(b, glist[ch.gi]);
     bool bm = false;
     ValFn<MODE> val(b, r, &bm);
-    const double T = run_units_and_tree(val, 1 + (int64_t)ch.start, prog + ch.progoff, sv);
+    // pad = first element of the tree: 1 for a whole segment (a[0] is the
+    // reduceat initial value), 0 for a rank's local part of a cut segment
+    const double T = run_units_and_tree(val, (int64_t)ch.pad + ch.start, prog + ch.progoff, sv);
     if (threadIdx.x == 0) csum[blockIdx.x] = T;
     if (MODE == MODE_FUSED && bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
 }
 
 // G2: one CTA per giant component: combine chunk sums along the top of the
-// tree (program whose units are chunks), then z.
+// tree (program whose units are chunks), then z.  A cut component (pad0 =
+// its position in the exchange vector) instead stores its local partial
+// sum in `send`; z follows after the exchange (k_cut_finalize).
 struct GComp { int32_t topoff, cbase, pad0, pad1; };
 template <int MODE>
 __global__ void __launch_bounds__(kVarThreads) k_var_giant_top(
     PassB b, const int32_t* glist, const GComp* comps, const int32_t* prog,
-    const double* csum, double* gz) {
+    const double* csum, double* gz, double* send) {
     extern __shared__ double sv[];
     __shared__ int s_stop;
     if (threadIdx.x == 0) s_stop = b.ctrl->stop;
@@ -268,6 +272,10 @@ __global__ void __launch_bounds__(kVarThreads) k_var_giant_top(
         __syncthreads();
         node += cnt;
         op += cnt;
+    }
+    if (gc.pad0 >= 0) {
+        if (threadIdx.x == 0) send[gc.pad0] = (nu > 0) ? sv[node - 1] : 0.0;
+        return;
     }
     if (threadIdx.x == 0) {
         const CompRef r = comp_ref(b, k);
@@ -342,6 +350,79 @@ __global__ void __launch_bounds__(1024) k_reduce(Ctrl* c, const double* part,
         }
         c->iter = it + 1;
     }
+}
+
+// Cut components after the exchange: rank-order sum of the all-gathered
+// partials (identical on every rank), then z as for a whole segment.
+__global__ void k_cut_finalize(PassB b, const int32_t* glist, const GComp* comps,
+                               const int32_t* cutg, int64_t ncutg,
+                               const double* recv, int32_t world, int64_t ncut,
+                               double* gz) {
+    if (b.ctrl->stop == 1) return;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ncutg) return;
+    const int32_t gi = cutg[t];
+    const GComp gc = comps[gi];
+    const int32_t k = glist[gi];
+    double tot = recv[gc.pad0];
+    for (int r = 1; r < world; ++r) tot = tot + recv[(int64_t)r * ncut + gc.pad0];
+    const double zn = tot / b.zw[k];
+    gz[2 * gi] = zn;
+    gz[2 * gi + 1] = b.z[k];
+    b.z[k] = zn;
+    if (!finite(zn)) flag_error(b.ctrl, b.ctrl->iter, FG_PHASE_Z, false);
+}
+
+// Partitioned runs split the residual reduction: local sums (plus the local
+// error key) go to a 4-double send slot, are all-gathered, and every rank
+// combines them in rank order, so all ranks take the same stop decision.
+__global__ void __launch_bounds__(1024) k_reduce_local(Ctrl* c, const double* part,
+                                                       int64_t npart, double* send4) {
+    __shared__ double sm[64];
+    double a = 0.0, bsum = 0.0;
+    for (int64_t i = threadIdx.x; i < npart; i += 1024) {
+        a += part[2 * i];
+        bsum += part[2 * i + 1];
+    }
+    block_sum2<1024>(a, bsum, sm);
+    if (threadIdx.x == 0) {
+        send4[0] = a;
+        send4[1] = bsum;
+        send4[2] = __longlong_as_double((long long)c->err_key);
+        send4[3] = 0.0;
+    }
+}
+
+__global__ void k_reduce_final(Ctrl* c, const double* recv4, int32_t world,
+                               double* hist) {
+    if (threadIdx.x != 0 || c->stop == 1) return;
+    double a = recv4[0], bsum = recv4[1];
+    unsigned long long err = (unsigned long long)__double_as_longlong(recv4[2]);
+    for (int r = 1; r < world; ++r) {
+        a = a + recv4[4 * r];
+        bsum = bsum + recv4[4 * r + 1];
+        const unsigned long long e = (unsigned long long)__double_as_longlong(recv4[4 * r + 2]);
+        err = e < err ? e : err;
+    }
+    const int64_t it = c->iter;
+    const double primal = sqrt(a) * c->scale;
+    const double dual = sqrt(bsum) * c->scale;
+    c->primal = primal;
+    c->dual = dual;
+    if (hist) { hist[2 * (it - 1)] = primal; hist[2 * (it - 1) + 1] = dual; }
+    if (err != ~0ull) {
+        if (err < c->err_key) c->err_key = err;
+        c->stop = 1;
+        c->completed = it - 1;
+        return;
+    }
+    c->completed = it;
+    const bool pc = c->primal_tol > 0.0, dc = c->dual_tol > 0.0;
+    bool ok = pc || dc;
+    if (pc) ok = ok && (primal <= c->primal_tol);
+    if (dc) ok = ok && (dual <= c->dual_tol);
+    if (ok) { c->converged = 1; c->stop = 1; }
+    c->iter = it + 1;
 }
 
 // ===========================================================================

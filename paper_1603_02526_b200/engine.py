@@ -147,7 +147,7 @@ def _group_specs(graph):
     """(kind class, slot dims, first edges, DeviceParams, check info) per
     (kind, slot dims) group in first-appearance order (engine.py:169-181)."""
     order, members = [], {}
-    if hasattr(graph, "_blocks") and hasattr(graph, "factor_first_edges"):
+    if hasattr(graph, "blocks") and hasattr(graph, "factor_first_edges"):
         for bi, (cls, dims, _f0, _vars, params) in enumerate(graph.blocks):
             key = (cls.kind, tuple(dims))
             if key not in members:
@@ -225,6 +225,12 @@ class DevicePlan:
         gd.edge_offsets = _native.i64ptr(eo)
         gd.chunk = int(chunk)
         gd.small_degree = int(small_degree)
+        cut = getattr(graph, "cut_index", None)
+        if cut is not None and getattr(graph, "ncut", 0) > 0:
+            cut32 = np.ascontiguousarray(cut, dtype=np.int32)
+            keep.append(cut32)
+            gd.z_cut_index = _native.i32ptr(cut32)
+            gd.ncut = int(graph.ncut)
         descs = (_native.GroupDesc * max(1, len(self.groups)))()
         for i, (cls, dims_k, fe, dp, _params, _sizes) in enumerate(self.groups):
             descs[i] = _native.make_group_desc(cls.device_kind, dims_k, len(fe), fe, dp, keep)

@@ -1,0 +1,271 @@
+"""Factor partitioning for multi-GPU runs.
+
+Each rank owns a subset of the factors and all of their edges, so the edge
+pass (prox) is purely local.  A variable whose incident edges live on more
+than one rank is *cut*: every rank sums its own part of the variable's
+consensus segment (``m * rho`` over its local edges, in creation order),
+the partial sums are all-gathered and added in rank order, and every rank
+finalises the same z and updates its local u.  Non-cut variables are
+finished locally, exactly as on one GPU.
+
+Assignment: a factor goes to the rank that owns its *anchor* (slot-0)
+variable, and variables are split into contiguous id ranges balanced by
+the number of edges anchored in them.  That gives point ranges for the SVM
+chain (cut set: the bias ``b`` plus G-1 boundary weight copies), disk
+ranges of the collision triangle for packing (balanced by edge count), and
+time ranges for MPC.
+
+``LocalGraph`` is a frozen-graph-shaped view of one rank's part (same
+attribute names as ``FactorGraph``) so the device plan builder and the CPU
+oracle consume it unchanged.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from ._pairwise import grouped_reduce
+
+
+def _factor_first_edges(graph):
+    if hasattr(graph, "_factor_edge0"):
+        return graph._factor_edge0[:-1]
+    return np.array([f.edge_range[0] for f in graph.factors], dtype=np.int64)
+
+
+def locality_order(graph):
+    """Variable order that keeps each factor's variables together.
+
+    Hubs (degree > max(8, 4 x median degree), e.g. the SVM bias) are
+    ignored; every other variable is keyed by the smallest non-hub
+    variable id over its incident factors (one hop), ties by id.  SVM:
+    w_i and xi_i interleave by point; packing and MPC keep id order.
+    Returns (order, position-of-variable, hub mask, factor anchors)."""
+    V = len(graph.var_offsets) - 1
+    f_first = _factor_first_edges(graph)
+    E = len(graph.edge_var)
+    deg = np.bincount(graph.edge_var, minlength=V)
+    hub = deg > max(8.0, 4.0 * float(np.median(deg)))
+    ev = graph.edge_var
+    ef = np.repeat(np.arange(len(f_first)), np.diff(np.append(f_first, E)))
+    big = np.iinfo(np.int64).max
+    cand = np.where(hub[ev], big, ev)
+    fmin = np.full(len(f_first), big, dtype=np.int64)
+    np.minimum.at(fmin, ef, cand)
+    allmin = np.full(len(f_first), big, dtype=np.int64)
+    np.minimum.at(allmin, ef, ev)
+    fmin = np.where(fmin == big, allmin, fmin)
+    key = np.full(V, big, dtype=np.int64)
+    np.minimum.at(key, ev, fmin[ef])
+    key = np.where(hub, np.arange(V), key)
+    order = np.lexsort((np.arange(V), key))
+    pos = np.empty(V, dtype=np.int64)
+    pos[order] = np.arange(V)
+    # anchor: the non-hub slot variable earliest in the order
+    epos = np.where(hub[ev], big, pos[ev])
+    amin = np.full(len(f_first), big, dtype=np.int64)
+    np.minimum.at(amin, ef, epos)
+    apos_all = np.full(len(f_first), big, dtype=np.int64)
+    np.minimum.at(apos_all, ef, pos[ev])
+    anchor_pos = np.where(amin == big, apos_all, amin)
+    return order, pos, hub, anchor_pos
+
+
+def factor_owner(graph, world):
+    """Rank of every factor: variables are cut into `world` contiguous
+    ranges of the locality order, balanced by the edges of the factors
+    anchored in them; a factor goes to its anchor's rank."""
+    V = len(graph.var_offsets) - 1
+    f_first = _factor_first_edges(graph)
+    arity = np.diff(np.append(f_first, len(graph.edge_var)))
+    _order, _pos, _hub, anchor_pos = locality_order(graph)
+    load = np.bincount(anchor_pos, weights=arity, minlength=V)
+    cum = np.cumsum(load)
+    total = cum[-1] if V else 0.0
+    bounds = np.array([int(np.searchsorted(cum, total * r / world, side="left")) + 1
+                       for r in range(1, world)], dtype=np.int64)
+    return np.searchsorted(bounds, anchor_pos, side="right").astype(np.int64)
+
+
+class LocalGraph:
+    """One rank's factors and the variables they touch.
+
+    Attributes mirror ``FactorGraph`` (``edge_var``, ``edge_offsets``,
+    ``var_offsets``, ``zmap``, ``rho_flat``, ``z_weights``, ``blocks`` ...)
+    in LOCAL numbering; ``global_var``, ``global_edge``, ``global_factor``
+    map back.  ``z_weights`` are the GLOBAL weights of each variable.
+    ``cut_index[k]`` is the canonical position of local z component k in
+    the all-gathered cut vector (-1 when the variable is not cut).
+    """
+
+    def __init__(self, graph, owner, rank):
+        self.rank = rank
+        f_first = _factor_first_edges(graph)
+        F = len(f_first)
+        arity = np.diff(np.append(f_first, len(graph.edge_var)))
+        mine = np.nonzero(owner == rank)[0]
+        self.global_factor = mine
+        edges = (np.repeat(f_first[mine], arity[mine])
+                 + _ragged_arange(arity[mine]))
+        self.global_edge = edges
+        gvars = graph.edge_var[edges]
+        self.global_var = np.unique(gvars)
+        lv = np.searchsorted(self.global_var, gvars)
+        dims_all = np.diff(graph.var_offsets)
+        dims = dims_all[self.global_var]
+        self.edge_var = lv.astype(np.int64)
+        self.edge_rho = graph.edge_rho[edges].copy()
+        self.edge_alpha = graph.edge_alpha[edges].copy()
+        payload = dims[lv]
+        self.edge_offsets = np.zeros(len(edges) + 1, dtype=np.int64)
+        np.cumsum(payload, out=self.edge_offsets[1:])
+        self.total_edge_payload = int(self.edge_offsets[-1])
+        self.var_offsets = np.zeros(len(dims) + 1, dtype=np.int64)
+        np.cumsum(dims, out=self.var_offsets[1:])
+        self.z_dim = int(self.var_offsets[-1])
+        shift = self.var_offsets[lv] - self.edge_offsets[:-1]
+        self.zmap = np.repeat(shift, payload) + np.arange(self.total_edge_payload)
+        self.rho_flat = np.repeat(self.edge_rho, payload)
+        self.alpha_flat = np.repeat(self.edge_alpha, payload)
+        # global payload positions of the local payload (for state scatter)
+        gstart = graph.edge_offsets[edges]
+        self.global_payload = np.repeat(gstart - self.edge_offsets[:-1], payload) + \
+            np.arange(self.total_edge_payload)
+        gz = graph.var_offsets[self.global_var]
+        self.global_z = np.repeat(gz - self.var_offsets[:-1], dims) + np.arange(self.z_dim)
+        self.z_weights = graph.z_weights[self.global_z].copy()
+        # cut variables: local degree < global degree
+        gdeg = np.bincount(graph.edge_var, minlength=len(dims_all))
+        ldeg = np.bincount(lv, minlength=len(dims))
+        self.var_cut = ldeg < gdeg[self.global_var]
+        self._dims = dims
+        # factor blocks restricted to this rank (creation order kept)
+        self._blocks_local = []
+        fe_local = np.zeros(len(mine) + 1, dtype=np.int64)
+        np.cumsum(arity[mine], out=fe_local[1:])
+        self._factor_edge0 = fe_local
+        for cls, sdims, f0, vars_, params in graph.blocks:
+            sel = np.nonzero((mine >= f0) & (mine < f0 + len(vars_)))[0]
+            if sel.size == 0:
+                continue
+            rows = mine[sel] - f0
+            lvars = np.searchsorted(self.global_var, vars_[rows])
+            self._blocks_local.append((cls, sdims, int(sel[0]), lvars,
+                                       _take_params(params, rows), sel))
+
+    # ---- FactorGraph-compatible surface ------------------------------------
+    @property
+    def blocks(self):
+        return [(c, d, f0, v, p) for c, d, f0, v, p, _s in self._blocks_local]
+
+    def factor_first_edges(self, block_index):
+        sel = self._blocks_local[block_index][5]
+        return self._factor_edge0[sel]
+
+    @property
+    def param_version(self):
+        return 0
+
+    def variable_slice(self, v):
+        return slice(int(self.var_offsets[v]), int(self.var_offsets[v + 1]))
+
+    def counts(self):
+        return (len(self._dims), len(self.global_factor), len(self.edge_var))
+
+    @property
+    def edge_factor(self):
+        return np.repeat(np.arange(len(self.global_factor)), np.diff(self._factor_edge0))
+
+
+def _ragged_arange(lengths):
+    lengths = np.asarray(lengths, dtype=np.int64)
+    if lengths.size == 0:
+        return np.zeros(0, dtype=np.int64)
+    starts = np.repeat(np.cumsum(lengths) - lengths, lengths)
+    return np.arange(int(lengths.sum()), dtype=np.int64) - starts
+
+
+def _take_params(params, rows):
+    out = {}
+    for k, v in params.items():
+        if k == "systems":
+            out[k] = v
+        elif isinstance(v, list):
+            out[k] = [np.asarray(a)[rows] for a in v]
+        else:
+            out[k] = np.asarray(v)[rows]
+    return out
+
+
+class Partition:
+    """A world-size split of one graph, identical on every rank."""
+
+    def __init__(self, graph, world):
+        self.world = int(world)
+        self.owner = factor_owner(graph, self.world)
+        self.locals = None
+        self.graph = graph
+        # canonical cut components: global z indices of cut variables, sorted
+        gdeg = np.bincount(graph.edge_var, minlength=len(graph.var_offsets) - 1)
+        edge_owner = np.repeat(self.owner, np.diff(np.append(_factor_first_edges(graph),
+                                                             len(graph.edge_var))))
+        V = len(graph.var_offsets) - 1
+        first_owner = np.full(V, -1, dtype=np.int64)
+        order = np.argsort(graph.edge_var, kind="stable")
+        ev_sorted = graph.edge_var[order]
+        starts = np.searchsorted(ev_sorted, np.arange(V))
+        first_owner = edge_owner[order[starts]]
+        differs = np.zeros(V, dtype=bool)
+        np.logical_or.at(differs, ev_sorted, edge_owner[order] != first_owner[ev_sorted])
+        self.var_cut = differs
+        del gdeg
+        dims = np.diff(graph.var_offsets)
+        cut_vars = np.nonzero(differs)[0]
+        self.cut_z = (np.repeat(graph.var_offsets[cut_vars], dims[cut_vars])
+                      + _ragged_arange(dims[cut_vars]))
+        self.ncut = len(self.cut_z)
+
+    def local(self, rank):
+        lg = LocalGraph(self.graph, self.owner, rank)
+        lg.cut_index = np.full(lg.z_dim, -1, dtype=np.int64)
+        pos = np.searchsorted(self.cut_z, lg.global_z)
+        hit = (pos < self.ncut) & (self.cut_z[np.minimum(pos, max(self.ncut - 1, 0))]
+                                   == lg.global_z) if self.ncut else np.zeros(lg.z_dim, bool)
+        lg.cut_index[hit] = pos[hit]
+        lg.ncut = self.ncut
+        assert np.array_equal(lg.var_cut, self.var_cut[lg.global_var])
+        return lg
+
+
+def local_partial_sums(lg, m):
+    """Per cut component of ``lg``: NumPy pairwise sum of m*rho over the
+    local part of its segment (creation order); returns the canonical
+    (ncut,) vector with zeros elsewhere (the rank's send buffer)."""
+    vals = m * lg.rho_flat
+    order = np.argsort(lg.zmap, kind="stable")
+    ptr = np.searchsorted(lg.zmap[order], np.arange(lg.z_dim + 1))
+    comps = np.nonzero(lg.cut_index >= 0)[0]
+    sums = grouped_reduce(vals[order], ptr[comps], ptr[comps + 1] - ptr[comps])
+    send = np.zeros(lg.ncut)
+    send[lg.cut_index[comps]] = sums
+    return send
+
+
+def combine_partials(gathered):
+    """Rank-order sum of all-gathered partials (G, ncut) -> (ncut,)."""
+    out = np.array(gathered[0], dtype=np.float64, copy=True)
+    for r in range(1, len(gathered)):
+        out = out + gathered[r]
+    return out
+
+
+def local_weight_check(lg):
+    """z_weights recomputed from local rho where the variable is not cut
+    equal the global ones (same edges, same creation order)."""
+    order = np.argsort(lg.edge_var, kind="stable")
+    deg = np.bincount(lg.edge_var, minlength=len(lg.var_offsets) - 1)
+    start = np.concatenate([[0], np.cumsum(deg)[:-1]])
+    w = grouped_reduce(lg.edge_rho[order], start, deg)
+    full = np.repeat(w, np.diff(lg.var_offsets))
+    cut = np.repeat(lg.var_cut, np.diff(lg.var_offsets))
+    return np.array_equal(full[~cut], lg.z_weights[~cut])

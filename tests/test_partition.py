@@ -1,0 +1,162 @@
+"""Multi-GPU partition logic on the CPU: partition invariants,
+and the partitioned protocol (local partial sums, all-gather, rank-order
+combine) checked against the single-process oracle, both in-process and
+across real processes with the gloo backend (world size 2)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import paper_1603_02526_b200 as fg
+from paper_1603_02526_b200.partition import Partition, local_weight_check
+from oracle import fgadmm_oracle as O
+
+
+def _graphs():
+    X, y = fg.gen_gaussian_arrays(40, 5, 4.0, seed=2)
+    svm = fg.build_svm(fg.SvmSpec.from_arrays(X, y))
+    pack = fg.build_packing(fg.PackingSpec(12))
+    mpc = fg.build_mpc(fg.MpcSpec(15, fg.LinearSystem(*fg.pendulum_linearization()),
+                                  np.array([0.0, 0.0, 0.1, 0.0])))
+    return {"svm": svm, "pack": pack, "mpc": mpc}
+
+
+@pytest.mark.parametrize("name", ["svm", "pack", "mpc"])
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_partition_covers_graph_and_marks_cuts(name, world):
+    g = _graphs()[name]
+    part = Partition(g, world)
+    locs = [part.local(r) for r in range(world)]
+    edges = np.sort(np.concatenate([lg.global_edge for lg in locs]))
+    np.testing.assert_array_equal(edges, np.arange(len(g.edge_var)))
+    pay = np.sort(np.concatenate([lg.global_payload for lg in locs]))
+    np.testing.assert_array_equal(pay, np.arange(g.total_edge_payload))
+    for lg in locs:
+        # local layout is the global one restricted to the rank
+        np.testing.assert_array_equal(lg.global_z[lg.zmap], g.zmap[lg.global_payload])
+        np.testing.assert_array_equal(lg.rho_flat, g.rho_flat[lg.global_payload])
+        assert local_weight_check(lg)
+        assert (lg.cut_index >= 0).sum() == np.repeat(lg.var_cut, np.diff(lg.var_offsets)).sum()
+    counts = np.zeros(len(g.var_offsets) - 1, dtype=int)
+    for lg in locs:
+        counts[lg.global_var] += 1
+    np.testing.assert_array_equal(counts > 1, part.var_cut)
+
+
+def test_svm_cut_set_is_bias_plus_boundaries():
+    X, y = fg.gen_gaussian_arrays(40, 5, 4.0, seed=2)
+    g = fg.build_svm(fg.SvmSpec.from_arrays(X, y))
+    part = Partition(g, 4)
+    cut_vars = np.nonzero(part.var_cut)[0]
+    assert 40 in cut_vars                     # the bias b
+    assert len(cut_vars) <= 1 + 3 * 3         # plus a few per rank boundary
+
+
+def _partitioned_vs_single(g, world, iters, st):
+    """Run the ranks as threads in lock step (all-gather = barrier + shared
+    slots) and assemble the global state."""
+    import threading
+    part = Partition(g, world)
+    locs = [part.local(r) for r in range(world)]
+    ref, ref_hist, _ = O.run(g, iters, st)
+    states = [O.State(*(np.array(getattr(st, k), dtype=float)[lg.global_payload]
+                        if k != "z" else np.array(st.z)[lg.global_z] for k in "xmzun"))
+              for lg in locs]
+    barrier = threading.Barrier(world)
+    slots, lock = {}, threading.Lock()
+    results = [None] * world
+
+    def worker(r):
+        counter = [0]
+
+        def allgather(vec):
+            key = counter[0]
+            counter[0] += 1
+            with lock:
+                slots.setdefault(key, [None] * world)[r] = np.asarray(vec, dtype=float)
+            barrier.wait()
+            out = list(slots[key])
+            barrier.wait()
+            return out
+        results[r] = O.run_partitioned(locs[r], iters, states[r], allgather)
+
+    threads = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    full = O.State(*(np.zeros_like(getattr(ref, k)) for k in "xmzun"))
+    for lg, (s, _h) in zip(locs, results):
+        for k in "xmun":
+            getattr(full, k)[lg.global_payload] = getattr(s, k)
+        full.z[lg.global_z] = s.z
+    return ref, ref_hist, full, results[0][1]
+
+
+@pytest.mark.parametrize("name", ["svm", "pack", "mpc"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_partitioned_protocol_matches_single_process(name, world):
+    g = _graphs()[name]
+    st = fg.init_state(g, seed=4)
+    ref, ref_hist, full, hist = _partitioned_vs_single(g, world, 12, st)
+    for k in "xmzun":
+        a, b = getattr(full, k), getattr(ref, k)
+        assert np.max(np.abs(a - b)) <= 1e-12 * max(1.0, np.max(np.abs(b))), k
+    np.testing.assert_allclose(np.array(hist), np.array(ref_hist), rtol=1e-10)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _gloo_rank(rank, world, port, out_path):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = _graphs()["svm"]
+    st = fg.init_state(g, seed=4)
+    part = Partition(g, world)
+    lg = part.local(rank)
+    ls = O.State(*(np.array(getattr(st, k))[lg.global_payload] if k != "z"
+                   else np.array(st.z)[lg.global_z] for k in "xmzun"))
+
+    def ag(vec):
+        t = torch.as_tensor(np.asarray(vec, dtype=np.float64))
+        outs = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(outs, t)
+        return [o.numpy() for o in outs]
+
+    s, hist = O.run_partitioned(lg, 12, ls, ag)
+    parts = [None] * world
+    dist.all_gather_object(parts, (rank, {k: getattr(s, k) for k in "xmzun"}, hist))
+    if rank == 0:
+        np.savez(out_path, **{f"{r}_{k}": v for r, arrs, _h in parts for k, v in arrs.items()},
+                 hist=np.array(parts[0][2]))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_partitioned_svm_matches_single(tmp_path):
+    import torch.multiprocessing as mp
+    world = 2
+    out = str(tmp_path / "res.npz")
+    mp.spawn(_gloo_rank, args=(world, _free_port(), out), nprocs=world, join=True)
+    g = _graphs()["svm"]
+    st = fg.init_state(g, seed=4)
+    ref, ref_hist, _ = O.run(g, 12, st)
+    res = np.load(out)
+    part = Partition(g, world)
+    full = {k: np.zeros_like(getattr(ref, k)) for k in "xmzun"}
+    for r in range(world):
+        lg = part.local(r)
+        for k in "xmun":
+            full[k][lg.global_payload] = res[f"{r}_{k}"]
+        full["z"][lg.global_z] = res[f"{r}_z"]
+    for k in "xmzun":
+        np.testing.assert_allclose(full[k], getattr(ref, k), rtol=1e-11, atol=1e-13)
+    np.testing.assert_allclose(res["hist"], np.array(ref_hist), rtol=1e-10)
