@@ -101,8 +101,10 @@ def kernel_bytes(graph, plan):
     sel_by_key = [("var_small_deg4", deg <= 4), ("var_small_deg8", (deg > 4) & (deg <= 8)),
                   ("var_small_loop", small & (deg > 8))]
     for d in (1, 2, 3, 4):
-        sel_by_key.append((f"var_large_d{d}", large & (dims == d)))
+        sel_by_key.append((f"var_large_d{d}", large & (dims == d) & (deg < 1024)))
     sel_by_key.append(("var_large_comp", large & (dims > 4)))
+    for d in (1, 2, 3, 4):
+        sel_by_key.append((f"var_cluster_d{d}", large & (dims == d) & (deg >= 1024)))
     for key, sel in sel_by_key:
         if sel.any():
             P = int(np.sum(deg[sel] * dims[sel]))

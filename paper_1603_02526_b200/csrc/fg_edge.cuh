@@ -41,6 +41,18 @@ struct GroupDev {
     const SlotRun* sruns;                // [nruns][nslots]
     const BlockRef* blocks;              // one per CTA in run mode
     int32_t nblocks, nruns;
+    // all-pairs collision groups (packing): per-disk rows + tile list
+    const struct DiskRow* disks;
+    const int2* tiles;                   // (bi, bj), bi <= bj
+    int32_t ndisks, ntiles;
+};
+
+// Row of disk i in var-major layout: the edge of pair (i, j) is entry
+// jj = j - (j > i) of the center row (2 doubles each) and radius row.
+struct DiskRow {
+    int64_t pbc, pbr;        // payload of entry 0 (center row, radius row)
+    int64_t zc, zr;          // z offsets
+    int32_t ebc, ebr;        // var-major edge of entry 0
 };
 
 struct PassA {
@@ -364,6 +376,126 @@ __global__ void __launch_bounds__(kEdgeThreads) k_mpc_dyn(PassA a, GroupDev g) {
     });
     passa_flags<FIRST>(a, it, bn, bx);
 }
+
+// ---- collision, all-pairs tiles (packing) --------------------------------
+// One CTA per 32x32 tile (bi <= bj) of the i<j pair triangle.  Pair (i, j)
+// has its i-half in row i at entry j-1 and its j-half in row j at entry i,
+// so a tile needs 32 contiguous entries of 32 rows for each half.  Both
+// halves are copied row-wise into shared memory with cp.async (all loads
+// in flight at once, no registers held), the j-half is read transposed,
+// and both x halves are written back row-wise: every global access is
+// coalesced and the DRAM traffic is the algorithmic minimum.
+constexpr int kTile = 32;
+constexpr int kTP = kTile + 1;                 // padded row (bank conflicts)
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src));
+}
+
+struct TileHalf {
+    double cx[kTile][kTP], cy[kTile][kTP], r[kTile][kTP];   // n (then x)
+    double rc[kTile][kTP], rr[kTile][kTP];                  // edge weights
+};
+
+template <bool FIRST>
+__global__ void __launch_bounds__(kEdgeThreads) k_collision_tiles(PassA a, GroupDev g) {
+    extern __shared__ double tile_smem[];
+    TileHalf& HI = *reinterpret_cast<TileHalf*>(tile_smem);             // rows i
+    TileHalf& HJ = *reinterpret_cast<TileHalf*>(tile_smem + sizeof(TileHalf) / 8);
+    if (a.ctrl->stop) return;
+    const int64_t it = a.ctrl->iter;
+    const int2 t = g.tiles[blockIdx.x];
+    const int i0 = t.x * kTile, j0 = t.y * kTile;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int N = g.ndisks;
+    const double* src = FIRST ? a.nsrc : a.uin;
+    bool bn = false, bx = false;
+    // stage: row p = (w + 8k) of each half, entry l
+#pragma unroll
+    for (int k = 0; k < kTile / 8; ++k) {
+        const int rl = w + 8 * k;
+        {   // i-half: row i = i0 + rl, entry j - 1 for j = j0 + l
+            const int i = i0 + rl, j = j0 + l;
+            if (i < N && j < N && i < j) {
+                const DiskRow R = g.disks[i];
+                const int64_t e = j - 1;
+                cp_async8(&HI.cx[rl][l], src + R.pbc + 2 * e);
+                cp_async8(&HI.cy[rl][l], src + R.pbc + 2 * e + 1);
+                cp_async8(&HI.r[rl][l], src + R.pbr + e);
+                cp_async8(&HI.rc[rl][l], a.rho + R.ebc + e);
+                cp_async8(&HI.rr[rl][l], a.rho + R.ebr + e);
+            }
+        }
+        {   // j-half: row j = j0 + rl, entry i for i = i0 + l
+            const int j = j0 + rl, i = i0 + l;
+            if (j < N && i < j) {
+                const DiskRow R = g.disks[j];
+                cp_async8(&HJ.cx[rl][l], src + R.pbc + 2 * (int64_t)i);
+                cp_async8(&HJ.cy[rl][l], src + R.pbc + 2 * (int64_t)i + 1);
+                cp_async8(&HJ.r[rl][l], src + R.pbr + i);
+                cp_async8(&HJ.rc[rl][l], a.rho + R.ebc + i);
+                cp_async8(&HJ.rr[rl][l], a.rho + R.ebr + i);
+            }
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    // compute pairs (i = i0 + w + 8k, j = j0 + l); results overwrite n
+    double zjc0 = 0.0, zjc1 = 0.0, zjr = 0.0;
+    if (!FIRST && j0 + l < N) {
+        const DiskRow Rj = g.disks[j0 + l];
+        zjc0 = a.z[Rj.zc]; zjc1 = a.z[Rj.zc + 1]; zjr = a.z[Rj.zr];
+    }
+#pragma unroll
+    for (int k = 0; k < kTile / 8; ++k) {
+        const int il = w + 8 * k, i = i0 + il, j = j0 + l;
+        if (i < N && j < N && i < j) {
+            double n1c0 = HI.cx[il][l], n1c1 = HI.cy[il][l], n1r = HI.r[il][l];
+            double n2c0 = HJ.cx[l][il], n2c1 = HJ.cy[l][il], n2r = HJ.r[l][il];
+            if (!FIRST) {   // n = z[zmap] - u  (phase n of the previous iteration)
+                const DiskRow Ri = g.disks[i];
+                n1c0 = a.z[Ri.zc] - n1c0; n1c1 = a.z[Ri.zc + 1] - n1c1;
+                n1r = a.z[Ri.zr] - n1r;
+                n2c0 = zjc0 - n2c0; n2c1 = zjc1 - n2c1; n2r = zjr - n2r;
+                bn |= !(finite(n1c0) && finite(n1c1) && finite(n1r) && finite(n2c0) &&
+                        finite(n2c1) && finite(n2r));
+            }
+            double c10, c11, r1, c20, c21, r2;
+            prox_collision(n1c0, n1c1, n1r, n2c0, n2c1, n2r, HI.rc[il][l], HI.rr[il][l],
+                           HJ.rc[l][il], HJ.rr[l][il], c10, c11, r1, c20, c21, r2);
+            HI.cx[il][l] = c10; HI.cy[il][l] = c11; HI.r[il][l] = r1;
+            HJ.cx[l][il] = c20; HJ.cy[l][il] = c21; HJ.r[l][il] = r2;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kTile / 8; ++k) {
+        const int rl = w + 8 * k;
+        {
+            const int i = i0 + rl, j = j0 + l;
+            if (i < N && j < N && i < j) {
+                const DiskRow R = g.disks[i];
+                const int64_t e = j - 1;
+                xput(a, R.pbc + 2 * e, HI.cx[rl][l], bx);
+                xput(a, R.pbc + 2 * e + 1, HI.cy[rl][l], bx);
+                xput(a, R.pbr + e, HI.r[rl][l], bx);
+            }
+        }
+        {
+            const int j = j0 + rl, i = i0 + l;
+            if (j < N && i < j) {
+                const DiskRow R = g.disks[j];
+                xput(a, R.pbc + 2 * (int64_t)i, HJ.cx[rl][l], bx);
+                xput(a, R.pbc + 2 * (int64_t)i + 1, HJ.cy[rl][l], bx);
+                xput(a, R.pbr + i, HJ.r[rl][l], bx);
+            }
+        }
+    }
+    passa_flags<FIRST>(a, it, bn, bx);
+}
+constexpr size_t kTileSmem = 2 * sizeof(TileHalf);
 
 // lanes per factor of each kind's kernel
 __host__ __device__ inline int kind_tpf(int kind, int dim0) {

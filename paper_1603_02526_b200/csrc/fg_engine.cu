@@ -163,6 +163,10 @@ struct fg_plan {
     int64_t nlv[5] = {0, 0, 0, 0, 0};
     int32_t* d_llist = nullptr; int32_t* d_lprog = nullptr; int64_t nL = 0;  // D>4
     int64_t nLvars = 0;
+    int32_t* d_clvars[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};   // clusters
+    int32_t* d_clprog[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    int64_t ncl[5] = {0, 0, 0, 0, 0};
+    size_t clsmem[5] = {0, 0, 0, 0, 0};
     int32_t* d_prog = nullptr;
     int64_t part_off[16] = {0};                       // per var kernel slot
     int32_t* d_glist = nullptr; int64_t nG = 0;
@@ -210,6 +214,8 @@ fg_plan::~fg_plan() {
                     d_u[0], d_u[1], d_stage, d_aux, d_z, d_zs, d_sruns,
                     d_sblk[0], d_sblk[1], d_sblk[2], d_lvars[1], d_lvars[2], d_lvars[3],
                     d_lvars[4], d_lvprog[1], d_lvprog[2], d_lvprog[3], d_lvprog[4],
+                    d_clvars[1], d_clvars[2], d_clvars[3], d_clvars[4], d_clprog[1],
+                    d_clprog[2], d_clprog[3], d_clprog[4],
                     d_llist, d_lprog, d_prog, d_glist, d_gchunks, d_gcomps,
                     d_gwork, d_csum, d_gz, d_part, d_res2, d_ctrl, d_hist,
                     d_cutg, d_send, d_recv};
@@ -231,7 +237,10 @@ void launch_kind(const GroupDev& g, const PassA& a, cudaStream_t st) {
                                                       kEdgeIndexCtas);
     const int T = kEdgeThreads;
     switch (g.kind) {
-        case FG_KIND_COLLISION: k_collision<FIRST><<<grid, T, 0, st>>>(a, g); break;
+        case FG_KIND_COLLISION:
+            if (g.tiles) k_collision_tiles<FIRST><<<(unsigned)g.ntiles, T, kTileSmem, st>>>(a, g);
+            else k_collision<FIRST><<<grid, T, 0, st>>>(a, g);
+            break;
         case FG_KIND_WALL: k_wall<FIRST><<<grid, T, 0, st>>>(a, g); break;
         case FG_KIND_QUADRATIC: k_quadratic<FIRST><<<grid, T, 0, st>>>(a, g); break;
         case FG_KIND_RADIUS:
@@ -272,12 +281,13 @@ void edge_pass(fg_plan* p, bool first, const double* uin, const double* nsrc,
 //   2..5 large segments, one CTA per variable of dim 1..4
 //   6 large segments, one CTA per component (dim > 4)
 //   7 giant chunks   8 giant top   9 giant u update
-constexpr int kVarSlots = 11;
+constexpr int kVarSlots = 15;
 constexpr int kSlotGiantChunks = 8, kSlotGiantTop = 9, kSlotGiantUpdate = 10;
 const char* kVarNames[kVarSlots] = {
     "var_small_deg4", "var_small_deg8", "var_small_loop", "var_large_d1",
     "var_large_d2", "var_large_d3", "var_large_d4", "var_large_comp",
-    "var_giant_chunks", "var_giant_top", "var_giant_update"};
+    "var_giant_chunks", "var_giant_top", "var_giant_update", "var_cluster_d1",
+    "var_cluster_d2", "var_cluster_d3", "var_cluster_d4"};
 
 int64_t var_slot_blocks(const fg_plan* p, int w) {
     switch (w) {
@@ -287,8 +297,15 @@ int64_t var_slot_blocks(const fg_plan* p, int w) {
         case 8: return p->nG ? p->nGC : 0;
         case 9: return p->nG;
         case 10: return p->nG ? p->nGW : 0;
+        case 11: case 12: case 13: case 14: return p->ncl[w - 10] * kCluster;
     }
     return 0;
+}
+
+template <int D, int MODE>
+void launch_cluster(fg_plan* p, const PassB& b, unsigned grid, int64_t po, cudaStream_t st) {
+    k_var_cluster<D, MODE><<<grid, kClusterThreads, p->clsmem[D], st>>>(
+        b, p->d_clvars[D], p->d_clprog[D], p->d_prog, po);
 }
 
 template <int MODE>
@@ -333,6 +350,10 @@ bool var_kernel(fg_plan* p, int which, const double* uin, double* uout,
             k_var_giant_top<MODE><<<grid, kVarThreads, p->gtop_smem, st>>>(
                 b, p->d_glist, p->d_gcomps, p->d_prog, p->d_csum, p->d_gz, p->d_send);
             return true;
+        case 11: launch_cluster<1, MODE>(p, b, grid, po, st); return true;
+        case 12: launch_cluster<2, MODE>(p, b, grid, po, st); return true;
+        case 13: launch_cluster<3, MODE>(p, b, grid, po, st); return true;
+        case 14: launch_cluster<4, MODE>(p, b, grid, po, st); return true;
         case kSlotGiantUpdate:
             if (MODE != MODE_FUSED) return false;
             k_var_giant_update<<<grid, kVarThreads, 0, st>>>(b, p->d_glist, p->d_gwork,
@@ -586,6 +607,54 @@ int build_group(fg_plan* p, const fg_group_desc& gd,
             g.sk[j] = dsk;
         }
     }
+    if (gd.kind == FG_KIND_COLLISION && n > 0) {
+        // all-pairs structure: factors are (i, j), i < j, over K disks in
+        // lexicographic order, and every row keeps its pair entries in
+        // partner order -> tiled kernel with arithmetic addressing
+        int64_t K = 2;
+        while (K * (K - 1) / 2 < n) ++K;
+        bool ok = K * (K - 1) / 2 == n;
+        std::vector<int32_t> dc(K), dr(K);
+        std::vector<int64_t> offc(K), offr(K);
+        if (ok) {
+            dc[0] = svs[0][0]; dr[0] = svs[1][0]; offc[0] = sks[0][0]; offr[0] = sks[1][0];
+            for (int64_t j = 1; j < K; ++j) {
+                dc[j] = svs[2][j - 1]; dr[j] = svs[3][j - 1];
+                offc[j] = sks[2][j - 1]; offr[j] = sks[3][j - 1];
+            }
+            int64_t f = 0;
+            for (int64_t i = 0; i < K - 1 && ok; ++i)
+                for (int64_t j = i + 1; j < K && ok; ++j, ++f)
+                    ok = svs[0][f] == dc[i] && svs[1][f] == dr[i] && svs[2][f] == dc[j] &&
+                         svs[3][f] == dr[j] && sks[0][f] == offc[i] + (j - 1) &&
+                         sks[1][f] == offr[i] + (j - 1) && sks[2][f] == offc[j] + i &&
+                         sks[3][f] == offr[j] + i;
+        }
+        if (ok && K >= 2) {
+            std::vector<DiskRow> rows(K);
+            for (int64_t i = 0; i < K; ++i)
+                rows[i] = DiskRow{pbase[dc[i]] + 2 * offc[i], pbase[dr[i]] + offr[i],
+                                  zbase[dc[i]], zbase[dr[i]],
+                                  (int32_t)(ebase[dc[i]] + offc[i]), (int32_t)(ebase[dr[i]] + offr[i])};
+            std::vector<int2> tiles;
+            const int nb = (int)((K + kTile - 1) / kTile);
+            for (int bi = 0; bi < nb; ++bi)
+                for (int bj = bi; bj < nb; ++bj) tiles.push_back(make_int2(bi, bj));
+            DiskRow* drows; int2* dt;
+            if (int rc = upload(&drows, rows)) return rc;
+            out.allocs.push_back(drows);
+            if (int rc = upload(&dt, tiles)) return rc;
+            out.allocs.push_back(dt);
+            CK(cudaFuncSetAttribute(k_collision_tiles<true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
+            CK(cudaFuncSetAttribute(k_collision_tiles<false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
+            g.disks = drows;
+            g.tiles = dt;
+            g.ndisks = (int32_t)K;
+            g.ntiles = (int32_t)tiles.size();
+        }
+    }
     if (gd.fparams && gd.fstride > 0) {
         std::vector<double> fp(gd.fparams, gd.fparams + n * gd.fstride);
         double* d;
@@ -724,6 +793,9 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     std::vector<GComp> gcomps;
     std::vector<GWork> gwork;
     std::vector<int32_t> cutg;
+    std::vector<int32_t> clvars[5], clprog[5];
+    int64_t clmax[5] = {0, 0, 0, 0, 0};
+    const bool no_cluster = getenv("FGADMM_NO_CLUSTER") != nullptr;
     std::map<int64_t, int32_t> leafprog;   // n -> offset
     auto leaf_prog = [&](int64_t n) -> int32_t {
         auto it = leafprog.find(n);
@@ -771,6 +843,22 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
                 sruns.push_back(SRun{pbase[v], zbase[v], ebase[v], 1, dim[v], (int32_t)dg});
             }
             nsmall += dim[v];
+        } else if (dg - 1 <= kChunk && dim[v] <= 4 && dg >= kClusterMinDeg && !no_cluster) {
+            const int d = dim[v];
+            const int32_t off = leaf_prog(dg - 1);
+            clvars[d].push_back((int32_t)v);
+            clprog[d].push_back(off);
+            // shared memory of the largest per-CTA element range
+            const int32_t* P = prog.data() + off;
+            const int nu = P[0];
+            for (int r = 0; r < kCluster; ++r) {
+                const int L0 = (int)((int64_t)nu * r / kCluster);
+                const int L1 = (int)((int64_t)nu * (r + 1) / kCluster);
+                const int64_t lo = r == 0 ? 0 : 1 + P[2 + 2 * L0];
+                const int64_t hi = r == kCluster - 1 ? dg : 1 + P[2 + 2 * L1];
+                clmax[d] = std::max<int64_t>(clmax[d], hi - lo);
+            }
+            nlarge += d;
         } else if (dg - 1 <= kChunk && dim[v] <= 4) {
             lvars[dim[v]].push_back((int32_t)v);
             lvprog[dim[v]].push_back(leaf_prog(dg - 1));
@@ -835,6 +923,35 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     for (int d = 1; d <= 4; ++d)
         if ((rc = upload(&p->d_lvars[d], lvars[d])) || (rc = upload(&p->d_lvprog[d], lvprog[d])))
             return rc;
+    for (int d = 1; d <= 4; ++d) {
+        p->ncl[d] = (int64_t)clvars[d].size();
+        if ((rc = upload(&p->d_clvars[d], clvars[d])) || (rc = upload(&p->d_clprog[d], clprog[d])))
+            return rc;
+        p->clsmem[d] = (size_t)std::max<int64_t>(1, clmax[d]) * d * 2 * sizeof(double);
+        if (p->clsmem[d] > 200 * 1024)
+            return fail(FG_ERR_INVALID, "cluster row slice exceeds shared memory");
+        cudaError_t e1 = cudaSuccess, e2 = cudaSuccess;
+        switch (d) {
+            case 1:
+                e1 = cudaFuncSetAttribute(k_var_cluster<1, MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->clsmem[d]);
+                e2 = cudaFuncSetAttribute(k_var_cluster<1, MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->clsmem[d]);
+                break;
+            case 2:
+                e1 = cudaFuncSetAttribute(k_var_cluster<2, MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->clsmem[d]);
+                e2 = cudaFuncSetAttribute(k_var_cluster<2, MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->clsmem[d]);
+                break;
+            case 3:
+                e1 = cudaFuncSetAttribute(k_var_cluster<3, MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->clsmem[d]);
+                e2 = cudaFuncSetAttribute(k_var_cluster<3, MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->clsmem[d]);
+                break;
+            case 4:
+                e1 = cudaFuncSetAttribute(k_var_cluster<4, MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->clsmem[d]);
+                e2 = cudaFuncSetAttribute(k_var_cluster<4, MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->clsmem[d]);
+                break;
+        }
+        if (e1 != cudaSuccess || e2 != cudaSuccess)
+            return fail(FG_ERR_CUDA, "cluster kernel shared-memory attribute");
+    }
     // residual partial slots: one per CTA of every fused var kernel
     int64_t acc_part = 0;
     for (int w = 0; w < kVarSlots; ++w) {

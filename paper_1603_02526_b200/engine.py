@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+from collections.abc import Sequence
 import weakref
 from dataclasses import dataclass, field
 from time import perf_counter
@@ -506,6 +507,40 @@ def _raise_device_error(graph, plan, state, res):
     raise RuntimeError(msg)
 
 
+class Solution(Sequence):
+    """The consensus vector unpacked per variable (reference
+    ``engine.py:521-522`` returns a list of per-variable copies).  Items
+    are views of a private copy of z, made on access, so building the
+    result is O(1) even for millions of variables."""
+
+    def __init__(self, z, var_offsets):
+        self._z = np.array(z, dtype=np.float64, copy=True)
+        self._off = np.asarray(var_offsets)
+
+    def __len__(self):
+        return len(self._off) - 1
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        n = len(self)
+        i = int(i)
+        if i < 0:
+            i += n
+        if not 0 <= i < n:
+            raise IndexError(i)
+        return self._z[int(self._off[i]):int(self._off[i + 1])]
+
+    def __iter__(self):
+        z, off = self._z, self._off
+        for i in range(len(off) - 1):
+            yield z[int(off[i]):int(off[i + 1])]
+
+    def concatenated(self):
+        """All variables back to back (== np.concatenate(self))."""
+        return self._z.copy()
+
+
 def run(graph, config, state=None):
     """Iterate to the budget or tolerances; return (solution, report)."""
     if config.max_iterations < 1:
@@ -567,8 +602,7 @@ def run(graph, config, state=None):
     if executed:
         state.last_residuals = (float(hist[executed - 1, 0]), float(hist[executed - 1, 1]))
     del tol_check
-    solution = [state.z[graph.variable_slice(v)].copy()
-                for v in range(len(graph.var_offsets) - 1)]
+    solution = Solution(state.z, graph.var_offsets)
     report = RunReport(iterations=executed, converged=converged, workers=config.workers,
                        phase_seconds=phase_totals, history=history,
                        total_seconds=max(total, dev), device_seconds=dev,

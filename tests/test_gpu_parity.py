@@ -236,3 +236,20 @@ def test_per_phase_api_matches_oracle_phases_on_packing(gpu):
     for k in "xmzun":
         np.testing.assert_array_equal(getattr(s2, k), getattr(so, k))
     assert s2.iteration == 2
+
+
+def test_packing_1030_cluster_and_tile_kernels_bitwise(gpu):
+    """N=1030: collision factors take the all-pairs tile kernel and the
+    degree-1032/1033 rows the 4-CTA cluster kernel (DSMEM tree); both must
+    reproduce the oracle bit for bit, including the first (n-reading) and
+    steady iterations."""
+    spec = fg.PackingSpec(1030)
+    g = fg.build_packing(spec)
+    st = fg.init_state(g, seed=3)
+    plan = fg.device_plan(g)
+    assert plan.info["large_components"] == g.z_dim
+    s = copy(st)
+    fg.run(g, fg.RunConfig(max_iterations=3), state=s)
+    so, hist, _ = O.run(g, 3, st)
+    for k in "xmzun":
+        np.testing.assert_array_equal(getattr(s, k), getattr(so, k), err_msg=k)
