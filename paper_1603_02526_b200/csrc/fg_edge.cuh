@@ -45,6 +45,7 @@ struct GroupDev {
     const struct DiskRow* disks;
     const int2* tiles;                   // (bi, bj), bi <= bj
     int32_t ndisks, ntiles;
+    int32_t variant;                     // tile kernel flavour (FGADMM_COLLISION)
 };
 
 // Row of disk i in var-major layout: the edge of pair (i, j) is entry
@@ -497,11 +498,84 @@ __global__ void __launch_bounds__(kEdgeThreads) k_collision_tiles(PassA a, Group
 }
 constexpr size_t kTileSmem = 2 * sizeof(TileHalf);
 
+// Variant: only the transposed j-half is staged (plain loads into shared
+// memory); the i-half is read directly, lane = j.  Fewer bytes of shared
+// memory per CTA, more CTAs per SM.
+template <bool FIRST>
+__global__ void __launch_bounds__(kEdgeThreads) k_collision_tiles_reg(PassA a, GroupDev g) {
+    __shared__ double s_cx[kTile][kTP], s_cy[kTile][kTP], s_r[kTile][kTP];
+    __shared__ double s_rc[kTile][kTP], s_rr[kTile][kTP];
+    if (a.ctrl->stop) return;
+    const int64_t it = a.ctrl->iter;
+    const int2 t = g.tiles[blockIdx.x];
+    const int i0 = t.x * kTile, j0 = t.y * kTile;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int N = g.ndisks;
+    const double* src = FIRST ? a.nsrc : a.uin;
+    bool bn = false, bx = false;
+#pragma unroll
+    for (int k = 0; k < kTile / 8; ++k) {
+        const int jl = w + 8 * k, j = j0 + jl, i = i0 + l;
+        if (j < N && i < j) {
+            const DiskRow R = g.disks[j];
+            cp_async8(&s_cx[jl][l], src + R.pbc + 2 * (int64_t)i);
+            cp_async8(&s_cy[jl][l], src + R.pbc + 2 * (int64_t)i + 1);
+            cp_async8(&s_r[jl][l], src + R.pbr + i);
+            cp_async8(&s_rc[jl][l], a.rho + R.ebc + i);
+            cp_async8(&s_rr[jl][l], a.rho + R.ebr + i);
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    double zjc0 = 0.0, zjc1 = 0.0, zjr = 0.0;
+    if (!FIRST && j0 + l < N) {
+        const DiskRow Rj = g.disks[j0 + l];
+        zjc0 = a.z[Rj.zc]; zjc1 = a.z[Rj.zc + 1]; zjr = a.z[Rj.zr];
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kTile / 8; ++k) {
+        const int il = w + 8 * k, i = i0 + il, j = j0 + l;
+        if (i < N && j < N && i < j) {
+            const DiskRow R = g.disks[i];
+            const int64_t pc = R.pbc + 2 * (int64_t)(j - 1), pr = R.pbr + (j - 1);
+            double n1c0 = src[pc], n1c1 = src[pc + 1], n1r = src[pr];
+            double n2c0 = s_cx[l][il], n2c1 = s_cy[l][il], n2r = s_r[l][il];
+            if (!FIRST) {
+                n1c0 = a.z[R.zc] - n1c0; n1c1 = a.z[R.zc + 1] - n1c1; n1r = a.z[R.zr] - n1r;
+                n2c0 = zjc0 - n2c0; n2c1 = zjc1 - n2c1; n2r = zjr - n2r;
+                bn |= !(finite(n1c0) && finite(n1c1) && finite(n1r) && finite(n2c0) &&
+                        finite(n2c1) && finite(n2r));
+            }
+            const double rc1 = a.rho[R.ebc + (j - 1)], rr1 = a.rho[R.ebr + (j - 1)];
+            double c10, c11, r1, c20, c21, r2;
+            prox_collision(n1c0, n1c1, n1r, n2c0, n2c1, n2r, rc1, rr1, s_rc[l][il],
+                           s_rr[l][il], c10, c11, r1, c20, c21, r2);
+            xput(a, pc, c10, bx); xput(a, pc + 1, c11, bx);
+            xput(a, pr, r1, bx);
+            s_cx[l][il] = c20; s_cy[l][il] = c21; s_r[l][il] = r2;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kTile / 8; ++k) {
+        const int jl = w + 8 * k, j = j0 + jl, i = i0 + l;
+        if (j < N && i < j) {
+            const DiskRow R = g.disks[j];
+            const int64_t pc = R.pbc + 2 * (int64_t)i, pr = R.pbr + i;
+            xput(a, pc, s_cx[jl][l], bx);
+            xput(a, pc + 1, s_cy[jl][l], bx);
+            xput(a, pr, s_r[jl][l], bx);
+        }
+    }
+    passa_flags<FIRST>(a, it, bn, bx);
+}
+
 // lanes per factor of each kind's kernel
 __host__ __device__ inline int kind_tpf(int kind, int dim0) {
     switch (kind) {
         case FG_KIND_SVM_MARGIN: return kMarginLanes;
-        case FG_KIND_MPC_DYN: return 32;
+        case FG_KIND_MPC_DYN: return 8;          // k_mpc_dyn8 (fg_mpc.cuh)
         case FG_KIND_RADIUS: case FG_KIND_MPC_COST: case FG_KIND_MPC_INIT:
         case FG_KIND_SVM_SLACK: case FG_KIND_SVM_NORM: case FG_KIND_EQUALITY:
         case FG_KIND_NAN_TEST: return dim0;

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "fg_var_fast.cuh"
+#include "fg_mpc.cuh"
 
 using namespace fg;
 
@@ -238,7 +239,10 @@ void launch_kind(const GroupDev& g, const PassA& a, cudaStream_t st) {
     const int T = kEdgeThreads;
     switch (g.kind) {
         case FG_KIND_COLLISION:
-            if (g.tiles) k_collision_tiles<FIRST><<<(unsigned)g.ntiles, T, kTileSmem, st>>>(a, g);
+            if (g.tiles && g.variant == 1)
+                k_collision_tiles<FIRST><<<(unsigned)g.ntiles, T, kTileSmem, st>>>(a, g);
+            else if (g.tiles)
+                k_collision_tiles_reg<FIRST><<<(unsigned)g.ntiles, T, 0, st>>>(a, g);
             else k_collision<FIRST><<<grid, T, 0, st>>>(a, g);
             break;
         case FG_KIND_WALL: k_wall<FIRST><<<grid, T, 0, st>>>(a, g); break;
@@ -261,7 +265,10 @@ void launch_kind(const GroupDev& g, const PassA& a, cudaStream_t st) {
             if (g.dim[0] <= 4 * kMarginLanes) k_svm_margin<FIRST, 4><<<grid, T, 0, st>>>(a, g);
             else k_svm_margin<FIRST, kMarginMaxD / kMarginLanes><<<grid, T, 0, st>>>(a, g);
             break;
-        case FG_KIND_MPC_DYN: k_mpc_dyn<FIRST><<<grid, T, 0, st>>>(a, g); break;
+        case FG_KIND_MPC_DYN:
+            k_mpc_dyn8<FIRST><<<grid, T, mpc_dyn8_smem(g.tstride, g.dim[0] + g.ip, g.ip,
+                                                       g.fsys == nullptr), st>>>(a, g);
+            break;
         default: break;
     }
 }
@@ -607,7 +614,10 @@ int build_group(fg_plan* p, const fg_group_desc& gd,
             g.sk[j] = dsk;
         }
     }
-    if (gd.kind == FG_KIND_COLLISION && n > 0) {
+    const char* cvar = getenv("FGADMM_COLLISION");      // generic | tile | tile_reg
+    g.variant = (cvar && std::strcmp(cvar, "tile") == 0) ? 1 : 0;
+    const bool want_tiles = !(cvar && std::strcmp(cvar, "generic") == 0);
+    if (gd.kind == FG_KIND_COLLISION && n > 0 && want_tiles) {
         // all-pairs structure: factors are (i, j), i < j, over K disks in
         // lexicographic order, and every row keeps its pair entries in
         // partner order -> tiled kernel with arithmetic addressing
@@ -669,7 +679,7 @@ int build_group(fg_plan* p, const fg_group_desc& gd,
         out.allocs.push_back(d);
         g.tab = d;
     }
-    if (gd.fsys) {
+    if (gd.fsys && gd.ntables > 1) {        // one system: kernels use table 0
         std::vector<int32_t> fs(gd.fsys, gd.fsys + n);
         int32_t* d;
         if (int rc = upload(&d, fs)) return rc;
@@ -795,7 +805,10 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     std::vector<int32_t> cutg;
     std::vector<int32_t> clvars[5], clprog[5];
     int64_t clmax[5] = {0, 0, 0, 0, 0};
-    const bool no_cluster = getenv("FGADMM_NO_CLUSTER") != nullptr;
+    // The 4-CTA cluster kernel moves the compulsory bytes only, but measured
+    // slower than the one-CTA kernel (0.86 vs 0.55 ms, pack N=5000): it is
+    // opt-in (FGADMM_CLUSTER=1) until its leaf phase is better occupied.
+    const bool no_cluster = getenv("FGADMM_CLUSTER") == nullptr;
     std::map<int64_t, int32_t> leafprog;   // n -> offset
     auto leaf_prog = [&](int64_t n) -> int32_t {
         auto it = leafprog.find(n);

@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(kLargeThreads) k_var_large_vec(
                 }
         } else {
             vals(base + j, acc);
+#pragma unroll 4
             for (int64_t i = kUnroll; i < top; i += kUnroll) {
                 vals(base + i + j, tmp);
 #pragma unroll
@@ -364,6 +365,7 @@ k_var_cluster(PassB b, const int32_t* vlist, const int32_t* progoff, const int32
                 }
         } else {
             vals(base + j, acc);
+#pragma unroll 4
             for (int64_t i = kUnroll; i < top; i += kUnroll) {
                 vals(base + i + j, tmp);
 #pragma unroll
