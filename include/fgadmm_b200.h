@@ -178,6 +178,9 @@ int fg_phase_download(fg_plan* plan, double* x, double* m, double* z,
                       double* u, double* n);
 int fg_residuals(fg_plan* plan, const double* x, const double* z,
                  const double* z_prev, double* primal, double* dual);
+/* Objective sum and largest constraint violation at z (graph.py:253-263);
+ * z == NULL evaluates the plan's current device z.  out2 = {obj, viol}. */
+int fg_evaluate(fg_plan* plan, const double* z, double* out2);
 
 /* ---- standalone batched prox (ProxFactor.batch_eval) -------------------- */
 /* values: per slot j a (count, slot_dim[j]) row-major array, concatenated

@@ -76,6 +76,7 @@ EXPORTS = {
     "fg_phase": (C.c_int, [_p, C.c_int32]),
     "fg_phase_download": (C.c_int, [_p, _dp, _dp, _dp, _dp, _dp]),
     "fg_residuals": (C.c_int, [_p, _dp, _dp, _dp, _dp, _dp]),
+    "fg_evaluate": (C.c_int, [_p, _dp, _dp]),
     "fg_prox_eval": (C.c_int, [C.POINTER(GroupDesc), _dp, _dp, _dp, C.c_int32]),
     "fg_nccl_unique_id": (C.c_int, [C.c_char_p, C.c_char_p]),
     "fg_plan_attach_nccl": (C.c_int, [_p, C.c_char_p, C.c_char_p, C.c_int32, C.c_int32]),

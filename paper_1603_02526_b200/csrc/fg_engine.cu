@@ -1681,3 +1681,41 @@ int fg_group_run(fg_plan** plans, int32_t G, const fg_run_config* cfg, double* h
 }
 
 }  // extern "C"
+
+// ===========================================================================
+// Objective / constraint violation (graph.py:253-263) on the device
+// ===========================================================================
+#include "fg_eval.cuh"
+
+extern "C" int fg_evaluate(fg_plan* p, const double* z_host, double* out2) {
+    CK(cudaSetDevice(p->device));
+    cudaStream_t st = p->stream;
+    const double* z = p->d_z;
+    if (z_host) {
+        CK(cudaMemcpyAsync(p->d_zs, z_host, p->Z * sizeof(double), cudaMemcpyHostToDevice, st));
+        z = p->d_zs;
+    }
+    constexpr int kEvalCtas = 148 * 8;
+    double obj = 0.0, vio = 0.0;
+    std::vector<double> part(2 * kEvalCtas);
+    double* d_part = nullptr;
+    if (int rc = dalloc(&d_part, 2 * kEvalCtas)) return rc;
+    for (auto& gh : p->groups) {
+        const GroupDev& g = gh.dev;
+        if (g.count == 0) continue;
+        const unsigned grid = std::min<unsigned>(nblk(g.count, 256), kEvalCtas);
+        k_evaluate<<<grid, 256, 0, st>>>(g, p->vt(), z, d_part);
+        cudaError_t e = cudaMemcpyAsync(part.data(), d_part, 2 * grid * sizeof(double),
+                                        cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) { cudaFree(d_part); return fail(FG_ERR_CUDA, cudaGetErrorString(e)); }
+        for (unsigned b = 0; b < grid; ++b) {
+            obj += part[2 * b];
+            vio = std::max(vio, part[2 * b + 1]);
+        }
+    }
+    cudaFree(d_part);
+    out2[0] = obj;
+    out2[1] = vio;
+    return check_launch();
+}

@@ -313,6 +313,13 @@ class DevicePlan:
         _native.check(self._lib.fg_state_download(
             self._h, *[_native.dptr(a) if a is not None else None for a in outs]))
 
+    def evaluate(self, z=None):
+        """(objective, max violation) at z (None: the device's current z)."""
+        out = np.zeros(2)
+        zz = None if z is None else _native.f64(z)
+        _native.check(self._lib.fg_evaluate(self._h, _native.dptr(zz), _native.dptr(out)))
+        return float(out[0]), float(out[1])
+
     def profile_kernels(self, iterations):
         """{label: (total ms, launches)} for each kernel of the iteration."""
         n = 64
@@ -468,6 +475,18 @@ def iterate(graph, state):
         plan.phase_download(state, (name,))
         _check_finite(graph, state, name, state.iteration)
     state.iteration += 1
+
+
+def objective_value(graph, z):
+    """Sum of factor objectives at ``z``, evaluated on the device
+    (``FactorGraph.objective_value``, graph.py:253-257, at any graph size)."""
+    return device_plan(graph).evaluate(z)[0]
+
+
+def constraint_violation(graph, z):
+    """Largest factor constraint violation at ``z``, on the device
+    (``FactorGraph.constraint_violation``, graph.py:259-263)."""
+    return device_plan(graph).evaluate(z)[1]
 
 
 def residuals(graph, state, z_prev):

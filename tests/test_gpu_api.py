@@ -275,3 +275,31 @@ def test_batch_eval_matches_single_eval_bitwise(gpu, kind):
         single = op.eval([v[i] for v in vals], [r[i] for r in rhos])
         for j, s in enumerate(single):
             np.testing.assert_array_equal(batch[j][i], s)
+
+
+@pytest.mark.parametrize("name", ["pack", "svm", "mpc", "quad"])
+def test_device_objective_and_violation_match_graph_helpers(gpu, name):
+    """On-device objective / violation equal the host helpers (reference
+    graph.py:253-263 restated per kind in operators.py)."""
+    from paper_1603_02526_b200.engine import constraint_violation, objective_value
+    rng = np.random.default_rng(3)
+    if name == "pack":
+        g = fg.build_packing(fg.PackingSpec(25))
+    elif name == "svm":
+        X, y = fg.gen_gaussian_arrays(60, 6, 4.0, seed=1)
+        g = fg.build_svm(fg.SvmSpec.from_arrays(X, y))
+    elif name == "mpc":
+        g = fg.build_mpc(fg.MpcSpec(12, fg.LinearSystem(*fg.pendulum_linearization()),
+                                    np.array([0.0, 0.0, 0.1, 0.0])))
+    else:
+        b = fg.GraphBuilder()
+        v = b.declare_variable(2)
+        w = b.declare_variable(1)
+        b.add_factor(fg.Quadratic([[1.0, 2.0], [3.0]], [0.5, 2.0]), [v, w])
+        b.add_factor(fg.Quadratic([[-1.0, 0.0]], [1.5]), [v])
+        g = b.freeze()
+    z = rng.normal(size=g.z_dim)
+    obj = objective_value(g, z)
+    vio = constraint_violation(g, z)
+    assert obj == pytest.approx(g.objective_value(z), rel=1e-12, abs=1e-12)
+    assert vio == pytest.approx(g.constraint_violation(z), rel=1e-12, abs=1e-13)
