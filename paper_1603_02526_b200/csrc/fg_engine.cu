@@ -22,6 +22,7 @@
 
 #include "fg_var_fast.cuh"
 #include "fg_mpc.cuh"
+#include "fg_tma.cuh"
 
 using namespace fg;
 
@@ -45,6 +46,10 @@ int fail(int code, const std::string& msg) {
 constexpr int kSmallDegMax = 32;     // class S threshold (degree)
 constexpr int64_t kChunkMax = 8192;  // pairwise subtree handled by one CTA
 constexpr int64_t kGiantWork = 8192; // elements per G3 CTA
+// Dynamic shared-memory limit set on every kernel that uses it: the
+// attribute is per function, not per launch, so plans of different sizes
+// must not lower it under one another.
+constexpr int kMaxDynSmem = 200 * 1024;
 
 // ---------------------------------------------------------------------------
 // NumPy pairwise tree programs.  A node of m > 128 items splits at
@@ -168,6 +173,10 @@ struct fg_plan {
     int32_t* d_clprog[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     int64_t ncl[5] = {0, 0, 0, 0, 0};
     size_t clsmem[5] = {0, 0, 0, 0, 0};
+    STile* d_stiles = nullptr;         // TMA pipeline tiles over the small runs
+    int64_t ntiles = 0, tma_grid = 0;
+    int32_t tma_stage = 0;             // doubles per pipeline stage
+    size_t tma_smem = 0;
     int32_t* d_prog = nullptr;
     int64_t part_off[16] = {0};                       // per var kernel slot
     int32_t* d_glist = nullptr; int64_t nG = 0;
@@ -215,6 +224,7 @@ fg_plan::~fg_plan() {
                     d_u[0], d_u[1], d_stage, d_aux, d_z, d_zs, d_sruns,
                     d_sblk[0], d_sblk[1], d_sblk[2], d_lvars[1], d_lvars[2], d_lvars[3],
                     d_lvars[4], d_lvprog[1], d_lvprog[2], d_lvprog[3], d_lvprog[4],
+                    d_stiles,
                     d_clvars[1], d_clvars[2], d_clvars[3], d_clvars[4], d_clprog[1],
                     d_clprog[2], d_clprog[3], d_clprog[4],
                     d_llist, d_lprog, d_prog, d_glist, d_gchunks, d_gcomps,
@@ -288,16 +298,24 @@ void edge_pass(fg_plan* p, bool first, const double* uin, const double* nsrc,
 //   2..5 large segments, one CTA per variable of dim 1..4
 //   6 large segments, one CTA per component (dim > 4)
 //   7 giant chunks   8 giant top   9 giant u update
-constexpr int kVarSlots = 15;
+constexpr int kVarSlots = 16;
 constexpr int kSlotGiantChunks = 8, kSlotGiantTop = 9, kSlotGiantUpdate = 10;
+constexpr int kSlotSmallTma = 15;
 const char* kVarNames[kVarSlots] = {
     "var_small_deg4", "var_small_deg8", "var_small_loop", "var_large_d1",
     "var_large_d2", "var_large_d3", "var_large_d4", "var_large_comp",
     "var_giant_chunks", "var_giant_top", "var_giant_update", "var_cluster_d1",
-    "var_cluster_d2", "var_cluster_d3", "var_cluster_d4"};
+    "var_cluster_d2", "var_cluster_d3", "var_cluster_d4", "var_small_tma"};
+
+// slots that run in a fused iteration (the TMA pipeline replaces 0..2)
+bool fused_slot(const fg_plan* p, int w) {
+    if (p->tma_grid > 0 && w <= 2) return false;
+    return true;
+}
 
 int64_t var_slot_blocks(const fg_plan* p, int w) {
     switch (w) {
+        case 15: return p->tma_grid;
         case 0: case 1: case 2: return p->nsblk[w];
         case 3: case 4: case 5: case 6: return p->nlv[w - 2];
         case 7: return p->nL;
@@ -320,6 +338,7 @@ bool var_kernel(fg_plan* p, int which, const double* uin, double* uout,
                 const double* msrc, cudaStream_t st) {
     const int64_t nb = var_slot_blocks(p, which);
     if (nb == 0) return false;
+    if (MODE == MODE_FUSED && !fused_slot(p, which)) return false;
     const unsigned grid = (unsigned)nb;
     PassB b{p->vt(), p->d_x, uin, uout, msrc, p->d_z, p->d_rho, p->d_alpha,
             p->d_zw, p->d_ctrl, p->d_part, p->d_zvar};
@@ -356,6 +375,11 @@ bool var_kernel(fg_plan* p, int which, const double* uin, double* uout,
         case kSlotGiantTop:
             k_var_giant_top<MODE><<<grid, kVarThreads, p->gtop_smem, st>>>(
                 b, p->d_glist, p->d_gcomps, p->d_prog, p->d_csum, p->d_gz, p->d_send);
+            return true;
+        case kSlotSmallTma:
+            if (MODE != MODE_FUSED) return false;
+            k_var_small_tma<<<grid, kTmaThreads, p->tma_smem, st>>>(
+                b, p->d_sruns, p->d_stiles, (int32_t)p->ntiles, p->tma_stage, po);
             return true;
         case 11: launch_cluster<1, MODE>(p, b, grid, po, st); return true;
         case 12: launch_cluster<2, MODE>(p, b, grid, po, st); return true;
@@ -402,7 +426,7 @@ int64_t count_edge_launches(const fg_plan* p) {
 
 int64_t count_var_launches(const fg_plan* p) {
     int64_t n = 0;
-    for (int w = 0; w < kVarSlots; ++w) n += var_slot_blocks(p, w) > 0;
+    for (int w = 0; w < kVarSlots; ++w) n += var_slot_blocks(p, w) > 0 && fused_slot(p, w);
     return n;
 }
 
@@ -775,10 +799,12 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     vmz.clear(); vmz.shrink_to_fit();
 
     // ---- state buffers ----
-    if ((rc = dalloc(&p->d_rho, E)) || (rc = dalloc(&p->d_alpha, E)) ||
-        (rc = dalloc(&p->d_zw, Z)) || (rc = dalloc(&p->d_x, P)) ||
-        (rc = dalloc(&p->d_u[0], P)) || (rc = dalloc(&p->d_u[1], P)) ||
-        (rc = dalloc(&p->d_stage, std::max(P, Z))) || (rc = dalloc(&p->d_z, Z)) ||
+    // +kPad: 16-byte-rounded bulk copies may read one double past the end
+    constexpr int64_t kPad = 16;
+    if ((rc = dalloc(&p->d_rho, E + kPad)) || (rc = dalloc(&p->d_alpha, E + kPad)) ||
+        (rc = dalloc(&p->d_zw, Z + kPad)) || (rc = dalloc(&p->d_x, P + kPad)) ||
+        (rc = dalloc(&p->d_u[0], P + kPad)) || (rc = dalloc(&p->d_u[1], P + kPad)) ||
+        (rc = dalloc(&p->d_stage, std::max(P, Z))) || (rc = dalloc(&p->d_z, Z + kPad)) ||
         (rc = dalloc(&p->d_zs, Z)) || (rc = dalloc(&p->d_ctrl, 1)) ||
         (rc = dalloc(&p->d_res2, 2)))
         return rc;
@@ -919,11 +945,49 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     p->nGC = (int64_t)gchunks.size();
     p->nGW = (int64_t)gwork.size();
     for (int c = 0; c < 3; ++c) p->nsblk[c] = (int64_t)sblk[c].size();
+    // The bulk-copy pipeline measured slower than the register kernel on the
+    // degree-4 SVM segments (0.86 vs 0.76 ms): opt-in via FGADMM_TMA=1.
+    if (getenv("FGADMM_TMA") && !sruns.empty()) {
+        // TMA pipeline: tiles of whole variables, ~256 components each
+        std::vector<STile> tiles;
+        int64_t stage = 0;
+        auto span = [](int64_t a, int64_t b) {
+            const int64_t lo = a & ~int64_t(1), hi = (b + 1) & ~int64_t(1);
+            return hi - lo;
+        };
+        for (size_t r = 0; r < sruns.size(); ++r) {
+            const SRun& R = sruns[r];
+            const int32_t per = std::max<int32_t>(1, kTmaThreads / R.d);
+            const int64_t pe = (int64_t)R.deg * R.d;
+            for (int32_t v0 = 0; v0 < R.nv; v0 += per) {
+                const int32_t nv = std::min<int32_t>(per, R.nv - v0);
+                tiles.push_back(STile{(int32_t)r, v0, nv, 0});
+                const int64_t need =
+                    2 * span(R.pb0 + v0 * pe, R.pb0 + (v0 + nv) * pe) +
+                    2 * span(R.eb0 + (int64_t)v0 * R.deg, R.eb0 + (int64_t)(v0 + nv) * R.deg) +
+                    2 * span(R.zb0 + (int64_t)v0 * R.d, R.zb0 + (int64_t)(v0 + nv) * R.d);
+                stage = std::max(stage, need);
+            }
+        }
+        const size_t smem = (size_t)stage * kTmaStages * sizeof(double);
+        if (smem <= 200 * 1024) {
+            p->ntiles = (int64_t)tiles.size();
+            p->tma_stage = (int32_t)stage;
+            p->tma_smem = smem;
+            int dev_sms = 148;
+            cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
+            const int per_sm = std::max<int>(1, (int)((200 * 1024) / std::max<size_t>(smem, 1)));
+            p->tma_grid = std::min<int64_t>(p->ntiles, (int64_t)dev_sms * std::min(per_sm, 2));
+            if ((rc = upload(&p->d_stiles, tiles))) return rc;
+            CK(cudaFuncSetAttribute(k_var_small_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kMaxDynSmem));
+        }
+    }
     for (int d = 1; d <= 4; ++d) p->nlv[d] = (int64_t)lvars[d].size();
     p->gtop_smem = (int)(2 * max_top * sizeof(double));
     if ((size_t)p->gtop_smem > 48 * 1024) {
-        CK(cudaFuncSetAttribute(k_var_giant_top<MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->gtop_smem));
-        CK(cudaFuncSetAttribute(k_var_giant_top<MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->gtop_smem));
+        CK(cudaFuncSetAttribute(k_var_giant_top<MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+        CK(cudaFuncSetAttribute(k_var_giant_top<MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
     }
     if ((rc = upload(&p->d_sruns, sruns)) || (rc = upload(&p->d_sblk[0], sblk[0])) ||
         (rc = upload(&p->d_sblk[1], sblk[1])) || (rc = upload(&p->d_sblk[2], sblk[2])) ||
@@ -946,20 +1010,20 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
         cudaError_t e1 = cudaSuccess, e2 = cudaSuccess;
         switch (d) {
             case 1:
-                e1 = cudaFuncSetAttribute(k_var_cluster<1, MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->clsmem[d]);
-                e2 = cudaFuncSetAttribute(k_var_cluster<1, MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->clsmem[d]);
+                e1 = cudaFuncSetAttribute(k_var_cluster<1, MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+                e2 = cudaFuncSetAttribute(k_var_cluster<1, MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
                 break;
             case 2:
-                e1 = cudaFuncSetAttribute(k_var_cluster<2, MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->clsmem[d]);
-                e2 = cudaFuncSetAttribute(k_var_cluster<2, MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->clsmem[d]);
+                e1 = cudaFuncSetAttribute(k_var_cluster<2, MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+                e2 = cudaFuncSetAttribute(k_var_cluster<2, MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
                 break;
             case 3:
-                e1 = cudaFuncSetAttribute(k_var_cluster<3, MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->clsmem[d]);
-                e2 = cudaFuncSetAttribute(k_var_cluster<3, MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->clsmem[d]);
+                e1 = cudaFuncSetAttribute(k_var_cluster<3, MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+                e2 = cudaFuncSetAttribute(k_var_cluster<3, MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
                 break;
             case 4:
-                e1 = cudaFuncSetAttribute(k_var_cluster<4, MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->clsmem[d]);
-                e2 = cudaFuncSetAttribute(k_var_cluster<4, MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->clsmem[d]);
+                e1 = cudaFuncSetAttribute(k_var_cluster<4, MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+                e2 = cudaFuncSetAttribute(k_var_cluster<4, MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
                 break;
         }
         if (e1 != cudaSuccess || e2 != cudaSuccess)
@@ -1340,7 +1404,10 @@ int fg_profile_kernels(fg_plan* p, int64_t iterations, int32_t max_slots,
     const int nedge = (int)names.size();
     std::vector<int> vk;
     for (int w = 0; w < kVarSlots; ++w) {
-        if (var_slot_blocks(p, w) > 0) { vk.push_back(w); names.push_back(kVarNames[w]); }
+        if (var_slot_blocks(p, w) > 0 && fused_slot(p, w)) {
+            vk.push_back(w);
+            names.push_back(kVarNames[w]);
+        }
     }
     names.push_back("reduce");
     const int ns = (int)names.size();

@@ -253,3 +253,33 @@ def test_packing_1030_cluster_and_tile_kernels_bitwise(gpu):
     so, hist, _ = O.run(g, 3, st)
     for k in "xmzun":
         np.testing.assert_array_equal(getattr(s, k), getattr(so, k), err_msg=k)
+
+
+@pytest.mark.parametrize("env", [{"FGADMM_TMA": "1"}, {"FGADMM_CLUSTER": "1"},
+                                 {"FGADMM_COLLISION": "tile"},
+                                 {"FGADMM_COLLISION": "generic"}])
+def test_opt_in_kernel_variants_match_oracle(gpu, env, monkeypatch):
+    """The alternative kernels selected at plan creation (TMA bulk-copy
+    pipeline for small segments, 4-CTA DSMEM cluster rows, cp.async
+    two-half collision tiles, generic collision) stay exact."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    from paper_1603_02526_b200.engine import DevicePlan, _PLANS
+    spec = fg.PackingSpec(1030)
+    g = fg.build_packing(spec)
+    _PLANS[g] = DevicePlan(g)
+    st = fg.init_state(g, seed=8)
+    s = copy(st)
+    fg.run(g, fg.RunConfig(max_iterations=2), state=s)
+    so, _h, _ = O.run(g, 2, st)
+    for k in "xmzun":
+        np.testing.assert_array_equal(getattr(s, k), getattr(so, k), err_msg=k)
+    X, y = fg.gen_gaussian_arrays(3000, 32, 4.0, seed=4)
+    g2 = fg.build_svm(fg.SvmSpec.from_arrays(X, y))
+    _PLANS[g2] = DevicePlan(g2)
+    st2 = fg.init_state(g2, seed=2)
+    s2 = copy(st2)
+    fg.run(g2, fg.RunConfig(max_iterations=6), state=s2)
+    so2, _h, _ = O.run(g2, 6, st2)
+    for k in "xmzun":
+        assert_close(getattr(s2, k), getattr(so2, k), what=k)
