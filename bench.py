@@ -100,11 +100,13 @@ def kernel_bytes(graph, plan):
     giant = (deg - 1) > chunk
     sel_by_key = [("var_small_deg4", deg <= 4), ("var_small_deg8", (deg > 4) & (deg <= 8)),
                   ("var_small_loop", small & (deg > 8))]
+    # the 4-CTA cluster kernel is opt-in (FGADMM_CLUSTER=1) for degree >= 1024
+    cl_min = 1024 if os.environ.get("FGADMM_CLUSTER") else 1 << 62
     for d in (1, 2, 3, 4):
-        sel_by_key.append((f"var_large_d{d}", large & (dims == d) & (deg < 1024)))
+        sel_by_key.append((f"var_large_d{d}", large & (dims == d) & (deg < cl_min)))
     sel_by_key.append(("var_large_comp", large & (dims > 4)))
     for d in (1, 2, 3, 4):
-        sel_by_key.append((f"var_cluster_d{d}", large & (dims == d) & (deg >= 1024)))
+        sel_by_key.append((f"var_cluster_d{d}", large & (dims == d) & (deg >= cl_min)))
     for key, sel in sel_by_key:
         if sel.any():
             P = int(np.sum(deg[sel] * dims[sel]))
@@ -119,7 +121,28 @@ def kernel_bytes(graph, plan):
         out["var_giant_update"] = P * 24 + E * 16
     out["reduce"] = 16 * (plan.info["small_components"] // 256 + 1
                           + plan.info["large_components"] + 64)
+    if plan.info.get("fused_chain"):
+        out["chain_svm"] = chain_bytes(graph, dims, deg)
     return out
+
+
+def chain_bytes(graph, dims, deg):
+    """Compulsory bytes of one fused SVM-chain launch (csrc/fg_chain.cuh):
+    per weight copy w_i (dim D, degree 3-4) u read+write, z read+write,
+    z_weights, rho+alpha per edge; per slack xi_i the same at dim 1,
+    degree 2; per point the margin data (x_i, y_i), norm scale and slack
+    lam, plus b's u and rho read and x write.  Neighbours' equality edges
+    are re-reads of the same arrays (L2), not counted."""
+    n = int(np.sum(deg == 2))                  # xi's (b has degree n > 32)
+    wsel = (deg >= 3) & (deg <= 4)
+    P_w = int(np.sum(deg[wsel] * dims[wsel]))
+    Z_w = int(np.sum(dims[wsel]))
+    E_w = int(np.sum(deg[wsel]))
+    D = int(dims[wsel][0]) if wsel.any() else 0
+    w = P_w * 16 + Z_w * 24 + E_w * 16
+    xi = n * (2 * 16 + 24 + 2 * 16)
+    per_point = (D + 3) * 8 + 24
+    return w + xi + n * per_point
 
 
 def survey_alg_bytes(graph):

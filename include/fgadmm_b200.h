@@ -72,6 +72,8 @@ extern "C" {
 #define FG_BUF_U0 1
 #define FG_BUF_U1 2
 #define FG_BUF_AUX 3
+#define FG_BUF_Z0 4   /* z ping-pong slots (Z doubles, variable order):     */
+#define FG_BUF_Z1 5   /* iteration j of a run reads slot (j-1)&1, writes j&1 */
 
 typedef struct fg_plan fg_plan;
 
@@ -150,7 +152,9 @@ typedef struct {
 int fg_plan_create(const fg_graph_desc* graph, const fg_group_desc* groups,
                    int32_t ngroups, int32_t device, fg_plan** out);
 void fg_plan_destroy(fg_plan* plan);
-int fg_plan_info(const fg_plan* plan, int64_t* out9);
+/* out[0..10]: V, E, P, Z, small / large / giant components, giant chunks,
+ * launches of iteration 1, launches of later iterations, fused SVM chain on */
+int fg_plan_info(const fg_plan* plan, int64_t* out11);
 int fg_plan_sync_params(fg_plan* plan, const double* edge_rho,
                         const double* edge_alpha, const double* z_weights);
 
@@ -161,6 +165,9 @@ int fg_run(fg_plan* plan, const fg_run_config* cfg, double* history,
            fg_run_result* out);
 int fg_state_download(fg_plan* plan, double* x, double* m, double* z,
                       double* u, double* n);
+/* x/u/aux buffers are P doubles in reference edge order; FG_BUF_Z0/1 are Z
+ * doubles.  After a failed fg_run, FG_BUF_X holds x of the failing
+ * iteration (materialized when that iteration ran fused kernels). */
 int fg_debug_download(fg_plan* plan, int32_t buffer, double* out_ref);
 /* Per-kernel device time of `iterations` fused iterations (after
  * fg_state_upload): labels[32*i], ms[i], counts[i] for each kernel slot of

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libfgadmm_b200.so")
 FG_MAX_SLOTS = 8
 PHASE_IDS = {"x": 0, "m": 1, "z": 2, "u": 3, "n": 4}
 PHASE_NAMES = ("x", "m", "z", "u", "n")
-BUF_X, BUF_U0, BUF_U1, BUF_AUX = 0, 1, 2, 3
+BUF_X, BUF_U0, BUF_U1, BUF_AUX, BUF_Z0, BUF_Z1 = 0, 1, 2, 3, 4, 5
 
 ERR_INVALID, ERR_CUDA, ERR_UNSUPPORTED = -1, -2, -3
 

@@ -25,6 +25,14 @@ struct SlotRun {
 struct RunHdr { int64_t f0, count; };
 struct BlockRef { int32_t run, item0, item1, pad; };   // CTA -> run items
 
+// Row of disk i in var-major layout: the edge of pair (i, j) is entry
+// jj = j - (j > i) of the center row (2 doubles each) and radius row.
+struct DiskRow {
+    int64_t pbc, pbr;        // payload of entry 0 (center row, radius row)
+    int64_t zc, zr;          // z offsets
+    int32_t ebc, ebr;        // var-major edge of entry 0
+};
+
 struct GroupDev {
     int32_t kind, nslots;
     int32_t dim[FG_MAX_SLOTS];
@@ -46,14 +54,10 @@ struct GroupDev {
     const int2* tiles;                   // (bi, bj), bi <= bj
     int32_t ndisks, ntiles;
     int32_t variant;                     // tile kernel flavour (FGADMM_COLLISION)
-};
-
-// Row of disk i in var-major layout: the edge of pair (i, j) is entry
-// jj = j - (j > i) of the center row (2 doubles each) and radius row.
-struct DiskRow {
-    int64_t pbc, pbr;        // payload of entry 0 (center row, radius row)
-    int64_t zc, zr;          // z offsets
-    int32_t ebc, ebr;        // var-major edge of entry 0
+    // rows affine in the disk index (every packing graph): row i = row0 +
+    // i * rowS field by field, so the tile kernel computes addresses
+    int32_t rows_affine, rows_even;      // rows_even: center rows 16-byte aligned
+    DiskRow row0, rowS;
 };
 
 struct PassA {
@@ -298,17 +302,17 @@ __global__ void __launch_bounds__(kEdgeThreads, 4) k_svm_margin(PassA a, GroupDe
             xx += __shfl_xor_sync(gmask, xx, o);
         }
         const double slack = (1.0 - n3) - Y * (dot + n2);
-        const double denom = (xx / R1 + 1.0 / R2) + 1.0 / R3;
-        const double mu = np_max0(slack) / denom;
-        const double tw = (mu / R1) * Y;
+        const double denom = (ddiv(xx, R1) + ddiv(1.0, R2)) + ddiv(1.0, R3);
+        const double mu = ddiv(np_max0(slack), denom);
+        const double tw = ddiv(mu, R1) * Y;
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
             const int c = lane + kMarginLanes * k;
             if (c < D) xput(a, s0.pos + c, n1[k] + tw * X[k], bx);
         }
         if (lane == 0) {
-            xput(a, s1.pos, n2 + (mu / R2) * Y, bx);
-            xput(a, s2.pos, n3 + mu / R3, bx);
+            xput(a, s1.pos, n2 + ddiv(mu, R2) * Y, bx);
+            xput(a, s2.pos, n3 + ddiv(mu, R3), bx);
         }
     });
     passa_flags<FIRST>(a, it, bn, bx);
@@ -354,7 +358,7 @@ __global__ void __launch_bounds__(kEdgeThreads) k_mpc_dyn(PassA a, GroupDev g) {
         if (lane < d) {                           // y = diag * Q^T Mnv
             double acc = 0.0;
             for (int q = 0; q < d; ++q) acc += Q[q * d + lane] * s_v1[w][q];
-            s_v2[w][lane] = acc / (L[lane] / R0 + 1.0 / R1);
+            s_v2[w][lane] = ddiv(acc, ddiv(L[lane], R0) + ddiv(1.0, R1));
         }
         __syncwarp();
         if (lane < d) {                           // lambda = Q y
@@ -366,7 +370,7 @@ __global__ void __launch_bounds__(kEdgeThreads) k_mpc_dyn(PassA a, GroupDev g) {
         for (int c = lane; c < cols; c += 32) {   // v = nv - W^-1 M^T lambda
             double acc = 0.0;
             for (int q = 0; q < d; ++q) acc += M[q * cols + c] * s_v1[w][q];
-            const double winv = 1.0 / ((c < n0) ? R0 : R1);
+            const double winv = ddiv(1.0, (c < n0) ? R0 : R1);
             const double v = s_nv[w][c] - winv * acc;
             if (c < n0) xput(a, s0.pos + c, v, bx);
             else xput(a, s1.pos + (c - n0), v, bx);
@@ -566,6 +570,146 @@ __global__ void __launch_bounds__(kEdgeThreads) k_collision_tiles_reg(PassA a, G
             xput(a, pc, s_cx[jl][l], bx);
             xput(a, pc + 1, s_cy[jl][l], bx);
             xput(a, pr, s_r[jl][l], bx);
+        }
+    }
+    passa_flags<FIRST>(a, it, bn, bx);
+}
+
+__device__ __forceinline__ DiskRow disk_row(const GroupDev& g, int i) {
+    if (!g.rows_affine) return g.disks[i];
+    DiskRow R;
+    R.pbc = g.row0.pbc + (int64_t)i * g.rowS.pbc;
+    R.pbr = g.row0.pbr + (int64_t)i * g.rowS.pbr;
+    R.zc = g.row0.zc + (int64_t)i * g.rowS.zc;
+    R.zr = g.row0.zr + (int64_t)i * g.rowS.zr;
+    R.ebc = g.row0.ebc + i * g.rowS.ebc;
+    R.ebr = g.row0.ebr + i * g.rowS.ebr;
+    return R;
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src));
+}
+
+// Variant 3 (default when the rows are affine and 16-byte aligned):
+//  * no per-row table loads: row addresses are arithmetic;
+//  * the j-half (row j, entries i0..i0+31) goes to shared memory by
+//    cp.async, centers as one 16-byte copy per pair;
+//  * the i-half (row i, entries j0-1..) is loaded into registers for all
+//    four rows of a thread BEFORE anything is stored (16-byte center loads),
+//    and z of the tile's 64 rows is staged in shared memory, so a tile costs
+//    one memory round trip;
+//  * divisions by unit edge weights are skipped exactly (ddiv).
+// A16: center entries 16-byte aligned (one 16-byte access per center pair);
+// otherwise two 8-byte accesses.
+template <bool FIRST, bool A16>
+__global__ void __launch_bounds__(kEdgeThreads, 3) k_collision_tiles_v3(PassA a, GroupDev g) {
+    __shared__ double2 s_c[kTile][kTile + 1];       // [jl][il]: j-half centers
+    __shared__ double s_r[kTile][kTP], s_rc[kTile][kTP], s_rr[kTile][kTP];
+    __shared__ double s_z[2][kTile][3];             // z of rows i0.. and j0..
+    if (a.ctrl->stop) return;
+    const int64_t it = a.ctrl->iter;
+    const int2 t = g.tiles[blockIdx.x];
+    const int i0 = t.x * kTile, j0 = t.y * kTile;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int N = g.ndisks;
+    const double* __restrict__ src = FIRST ? a.nsrc : a.uin;
+    const double* __restrict__ rho = a.rho;
+    double* __restrict__ xo = a.x;
+    bool bn = false, bx = false;
+#pragma unroll
+    for (int k = 0; k < kTile / 8; ++k) {
+        const int jl = w + 8 * k, j = j0 + jl, i = i0 + l;
+        if (j < N && i < j) {
+            const DiskRow R = disk_row(g, j);
+            if (A16) {
+                cp_async16(&s_c[jl][l], src + R.pbc + 2 * (int64_t)i);
+            } else {
+                cp_async8(&s_c[jl][l].x, src + R.pbc + 2 * (int64_t)i);
+                cp_async8(&s_c[jl][l].y, src + R.pbc + 2 * (int64_t)i + 1);
+            }
+            cp_async8(&s_r[jl][l], src + R.pbr + i);
+            cp_async8(&s_rc[jl][l], rho + R.ebc + i);
+            cp_async8(&s_rr[jl][l], rho + R.ebr + i);
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    if (!FIRST && threadIdx.x < 2 * kTile) {
+        const int h = threadIdx.x >> 5, r = (h ? j0 : i0) + l;
+        if (r < N) {
+            const DiskRow R = disk_row(g, r);
+            s_z[h][l][0] = a.z[R.zc];
+            s_z[h][l][1] = a.z[R.zc + 1];
+            s_z[h][l][2] = a.z[R.zr];
+        }
+    }
+    double2 nc[kTile / 8];
+    double nr[kTile / 8], rc1[kTile / 8], rr1[kTile / 8];
+#pragma unroll
+    for (int k = 0; k < kTile / 8; ++k) {
+        const int i = i0 + w + 8 * k, j = j0 + l;
+        nc[k] = make_double2(0.0, 0.0); nr[k] = 0.0; rc1[k] = 1.0; rr1[k] = 1.0;
+        if (i < N && j < N && i < j) {
+            const DiskRow R = disk_row(g, i);
+            const int64_t e = j - 1;
+            if (A16) nc[k] = *reinterpret_cast<const double2*>(src + R.pbc + 2 * e);
+            else nc[k] = make_double2(src[R.pbc + 2 * e], src[R.pbc + 2 * e + 1]);
+            nr[k] = src[R.pbr + e];
+            rc1[k] = rho[R.ebc + e];
+            rr1[k] = rho[R.ebr + e];
+        }
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kTile / 8; ++k) {
+        const int il = w + 8 * k, i = i0 + il, j = j0 + l;
+        if (i < N && j < N && i < j) {
+            double n1c0 = nc[k].x, n1c1 = nc[k].y, n1r = nr[k];
+            const double2 c2 = s_c[l][il];
+            double n2c0 = c2.x, n2c1 = c2.y, n2r = s_r[l][il];
+            if (!FIRST) {   // n = z[zmap] - u  (phase n of the previous iteration)
+                n1c0 = s_z[0][il][0] - n1c0; n1c1 = s_z[0][il][1] - n1c1;
+                n1r = s_z[0][il][2] - n1r;
+                n2c0 = s_z[1][l][0] - n2c0; n2c1 = s_z[1][l][1] - n2c1;
+                n2r = s_z[1][l][2] - n2r;
+                bn |= !(finite(n1c0) && finite(n1c1) && finite(n1r) && finite(n2c0) &&
+                        finite(n2c1) && finite(n2r));
+            }
+            double c10, c11, r1, c20, c21, r2;
+            prox_collision(n1c0, n1c1, n1r, n2c0, n2c1, n2r, rc1[k], rr1[k], s_rc[l][il],
+                           s_rr[l][il], c10, c11, r1, c20, c21, r2);
+            const DiskRow R = disk_row(g, i);
+            const int64_t e = j - 1;
+            if (A16) {
+                *reinterpret_cast<double2*>(xo + R.pbc + 2 * e) = make_double2(c10, c11);
+            } else {
+                xo[R.pbc + 2 * e] = c10;
+                xo[R.pbc + 2 * e + 1] = c11;
+            }
+            xo[R.pbr + e] = r1;
+            bx |= !(finite(c10) && finite(c11) && finite(r1));
+            s_c[l][il] = make_double2(c20, c21);
+            s_r[l][il] = r2;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kTile / 8; ++k) {
+        const int jl = w + 8 * k, j = j0 + jl, i = i0 + l;
+        if (j < N && i < j) {
+            const DiskRow R = disk_row(g, j);
+            const double2 c = s_c[jl][l];
+            const double r = s_r[jl][l];
+            if (A16) {
+                *reinterpret_cast<double2*>(xo + R.pbc + 2 * (int64_t)i) = c;
+            } else {
+                xo[R.pbc + 2 * (int64_t)i] = c.x;
+                xo[R.pbc + 2 * (int64_t)i + 1] = c.y;
+            }
+            xo[R.pbr + i] = r;
+            bx |= !(finite(c.x) && finite(c.y) && finite(r));
         }
     }
     passa_flags<FIRST>(a, it, bn, bx);

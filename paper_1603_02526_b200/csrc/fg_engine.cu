@@ -23,6 +23,7 @@
 #include "fg_var_fast.cuh"
 #include "fg_mpc.cuh"
 #include "fg_tma.cuh"
+#include "fg_chain.cuh"
 
 using namespace fg;
 
@@ -137,6 +138,9 @@ inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 struct GroupHost {
     GroupDev dev{};
     std::vector<void*> allocs;
+    // per slot: (variable, rank in its segment) of every factor; kept until
+    // the plan's topology detection ran (fused SVM chain)
+    std::vector<std::vector<int32_t>> hsv, hsk;
 };
 
 struct fg_plan {
@@ -156,7 +160,11 @@ struct fg_plan {
     double *d_rho = nullptr, *d_alpha = nullptr, *d_zw = nullptr;
     // state
     double *d_x = nullptr, *d_u[2] = {nullptr, nullptr}, *d_stage = nullptr;
-    double *d_aux = nullptr, *d_z = nullptr, *d_zs = nullptr;
+    // z is ping-ponged like u: iteration j reads d_zb[(j-1)&1] and writes
+    // d_zb[j&1], so a pass may read any variable's previous z while others
+    // are being finalized (the fused chain kernel reads its neighbours')
+    double *d_aux = nullptr, *d_zb[2] = {nullptr, nullptr}, *d_zs = nullptr;
+    double* zcur() const { return d_zb[completed & 1]; }
     // groups
     std::vector<GroupHost> groups;
     // variable-pass classes
@@ -203,11 +211,22 @@ struct fg_plan {
     Ctrl* d_ctrl = nullptr;
     double* d_hist = nullptr; int64_t hist_cap = 0;
     // run bookkeeping
+    // fused SVM chain (fg_chain.cuh): replaces the edge pass and the small
+    // variable classes from the second iteration of a run on
+    bool chain_on = false;
+    ChainDev chain{};
+    int64_t chain_grid = 0;
+    int chain_minb = 2;                // CTAs/SM the kernel is compiled for (A/B)
+    // iteration (of the last run) whose x is not in d_x because the chain
+    // kernel keeps it in registers; 0 = d_x is current
+    int64_t x_stale = 0;
     int64_t completed = 0;         // iterations completed by the last run
+    int n_valid = 0;               // d_u[1] holds an uploaded n (fresh upload)
     int first_done = 0;
     // graphs: key = chunk iterations
     std::map<int, cudaGraphExec_t> graphs;
-    int64_t launches_per_iter = 0;
+    int64_t launches_per_iter = 0;     // iteration 1 of a run
+    int64_t launches_later = 0;        // iterations 2.. (fused chain when on)
 
     VarTab vt() const { return VarTab{d_dim, d_deg, d_ebase, d_pbase, d_zbase}; }
     ~fg_plan();
@@ -221,7 +240,7 @@ fg_plan::~fg_plan() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     void* ptrs[] = {d_dim, d_deg, d_ebase, d_pbase, d_zbase, d_zvar, d_vm2ref,
                     d_vmz, d_vmvar, d_refedge, d_rho, d_alpha, d_zw, d_x,
-                    d_u[0], d_u[1], d_stage, d_aux, d_z, d_zs, d_sruns,
+                    d_u[0], d_u[1], d_stage, d_aux, d_zb[0], d_zb[1], d_zs, d_sruns,
                     d_sblk[0], d_sblk[1], d_sblk[2], d_lvars[1], d_lvars[2], d_lvars[3],
                     d_lvars[4], d_lvprog[1], d_lvprog[2], d_lvprog[3], d_lvprog[4],
                     d_stiles,
@@ -249,7 +268,11 @@ void launch_kind(const GroupDev& g, const PassA& a, cudaStream_t st) {
     const int T = kEdgeThreads;
     switch (g.kind) {
         case FG_KIND_COLLISION:
-            if (g.tiles && g.variant == 1)
+            if (g.tiles && g.variant == 3 && g.rows_even)
+                k_collision_tiles_v3<FIRST, true><<<(unsigned)g.ntiles, T, 0, st>>>(a, g);
+            else if (g.tiles && g.variant == 3)
+                k_collision_tiles_v3<FIRST, false><<<(unsigned)g.ntiles, T, 0, st>>>(a, g);
+            else if (g.tiles && g.variant == 1)
                 k_collision_tiles<FIRST><<<(unsigned)g.ntiles, T, kTileSmem, st>>>(a, g);
             else if (g.tiles)
                 k_collision_tiles_reg<FIRST><<<(unsigned)g.ntiles, T, 0, st>>>(a, g);
@@ -283,9 +306,9 @@ void launch_kind(const GroupDev& g, const PassA& a, cudaStream_t st) {
     }
 }
 
-void edge_pass(fg_plan* p, bool first, const double* uin, const double* nsrc,
-               cudaStream_t st) {
-    PassA a{p->vt(), p->d_z, uin, nsrc, p->d_x, p->d_rho, p->d_ctrl};
+void edge_pass(fg_plan* p, bool first, const double* zin, const double* uin,
+               const double* nsrc, cudaStream_t st) {
+    PassA a{p->vt(), zin, uin, nsrc, p->d_x, p->d_rho, p->d_ctrl};
     for (auto& g : p->groups) {
         if (g.dev.count == 0) continue;
         if (first) launch_kind<true>(g.dev, a, st);
@@ -334,13 +357,13 @@ void launch_cluster(fg_plan* p, const PassB& b, unsigned grid, int64_t po, cudaS
 }
 
 template <int MODE>
-bool var_kernel(fg_plan* p, int which, const double* uin, double* uout,
-                const double* msrc, cudaStream_t st) {
+bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const double* uin,
+                double* uout, const double* msrc, cudaStream_t st) {
     const int64_t nb = var_slot_blocks(p, which);
     if (nb == 0) return false;
     if (MODE == MODE_FUSED && !fused_slot(p, which)) return false;
     const unsigned grid = (unsigned)nb;
-    PassB b{p->vt(), p->d_x, uin, uout, msrc, p->d_z, p->d_rho, p->d_alpha,
+    PassB b{p->vt(), p->d_x, uin, uout, msrc, zout, zin, p->d_rho, p->d_alpha,
             p->d_zw, p->d_ctrl, p->d_part, p->d_zvar};
     const int64_t po = p->part_off[which];
     switch (which) {
@@ -395,9 +418,9 @@ bool var_kernel(fg_plan* p, int which, const double* uin, double* uout,
 }
 
 template <int MODE>
-void var_pass(fg_plan* p, const double* uin, double* uout, const double* msrc,
-              cudaStream_t st) {
-    for (int w = 0; w < kVarSlots; ++w) var_kernel<MODE>(p, w, uin, uout, msrc, st);
+void var_pass(fg_plan* p, const double* zin, double* zout, const double* uin, double* uout,
+              const double* msrc, cudaStream_t st) {
+    for (int w = 0; w < kVarSlots; ++w) var_kernel<MODE>(p, w, zin, zout, uin, uout, msrc, st);
 }
 
 const char* kind_name(int kind) {
@@ -439,10 +462,10 @@ int64_t count_var_launches(const fg_plan* p) {
 int exchange_nccl(fg_plan* p, const double* send, double* recv, size_t count,
                   cudaStream_t st);
 
-void cut_finalize(fg_plan* p, const double* uin, double* uout, cudaStream_t st) {
+void cut_finalize(fg_plan* p, int in, cudaStream_t st) {
     if (!p->ncutg) return;
-    PassB b{p->vt(), p->d_x, uin, uout, nullptr, p->d_z, p->d_rho, p->d_alpha,
-            p->d_zw, p->d_ctrl, p->d_part, p->d_zvar};
+    PassB b{p->vt(), p->d_x, p->d_u[in], p->d_u[1 - in], nullptr, p->d_zb[1 - in],
+            p->d_zb[in], p->d_rho, p->d_alpha, p->d_zw, p->d_ctrl, p->d_part, p->d_zvar};
     k_cut_finalize<<<nblk(p->ncutg, 256), 256, 0, st>>>(
         b, p->d_glist, p->d_gcomps, p->d_cutg, p->ncutg, p->d_recv, p->world,
         p->ncut, p->d_gz);
@@ -450,21 +473,45 @@ void cut_finalize(fg_plan* p, const double* uin, double* uout, cudaStream_t st) 
 
 // Everything of a partitioned iteration up to the cut exchange.
 void part_pre(fg_plan* p, int in, bool first, cudaStream_t st) {
-    edge_pass(p, first, p->d_u[in], first ? p->d_u[1 - in] : nullptr, st);
+    edge_pass(p, first, p->d_zb[in], p->d_u[in], first ? p->d_u[1 - in] : nullptr, st);
     for (int w = 0; w < kVarSlots; ++w)
-        if (w != kSlotGiantUpdate) var_kernel<MODE_FUSED>(p, w, p->d_u[in], p->d_u[1 - in], nullptr, st);
+        if (w != kSlotGiantUpdate)
+            var_kernel<MODE_FUSED>(p, w, p->d_zb[in], p->d_zb[1 - in], p->d_u[in],
+                                   p->d_u[1 - in], nullptr, st);
 }
 
 // After the cut exchange, up to the residual exchange.
 void part_mid(fg_plan* p, int in, cudaStream_t st) {
-    cut_finalize(p, p->d_u[in], p->d_u[1 - in], st);
-    var_kernel<MODE_FUSED>(p, kSlotGiantUpdate, p->d_u[in], p->d_u[1 - in], nullptr, st);
+    cut_finalize(p, in, st);
+    var_kernel<MODE_FUSED>(p, kSlotGiantUpdate, p->d_zb[in], p->d_zb[1 - in], p->d_u[in],
+                           p->d_u[1 - in], nullptr, st);
     k_reduce_local<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_send + p->ncut);
 }
 
 void part_post(fg_plan* p, cudaStream_t st) {
     k_reduce_final<<<1, 32, 0, st>>>(p->d_ctrl, p->d_recv + (size_t)p->world * p->ncut,
                                      p->world, p->d_hist);
+}
+
+// fused SVM chain: one kernel for the edge pass and the w/xi variables ...
+void chain_pass(fg_plan* p, int in, cudaStream_t st) {
+    PassB b{p->vt(), p->d_x, p->d_u[in], p->d_u[1 - in], nullptr, p->d_zb[1 - in],
+            p->d_zb[in], p->d_rho, p->d_alpha, p->d_zw, p->d_ctrl, p->d_part, p->d_zvar};
+    if (p->chain_minb == 3)
+        k_svm_chain<3><<<(unsigned)p->chain_grid, kChainThreads, 0, st>>>(b, p->chain, p->d_x,
+                                                                          p->part_off[0]);
+    else
+        k_svm_chain<2><<<(unsigned)p->chain_grid, kChainThreads, 0, st>>>(b, p->chain, p->d_x,
+                                                                          p->part_off[0]);
+}
+
+// ... then the remaining (large / giant) variable classes: the bias
+bool chain_rest_slot(int w) { return w > 2 && w != kSlotSmallTma; }
+void chain_rest(fg_plan* p, int in, cudaStream_t st) {
+    for (int w = 0; w < kVarSlots; ++w)
+        if (chain_rest_slot(w))
+            var_kernel<MODE_FUSED>(p, w, p->d_zb[in], p->d_zb[1 - in], p->d_u[in],
+                                   p->d_u[1 - in], nullptr, st);
 }
 
 void launch_iteration(fg_plan* p, int in, bool first, cudaStream_t st) {
@@ -476,8 +523,14 @@ void launch_iteration(fg_plan* p, int in, bool first, cudaStream_t st) {
         part_post(p, st);
         return;
     }
-    edge_pass(p, first, p->d_u[in], first ? p->d_u[1 - in] : nullptr, st);
-    var_pass<MODE_FUSED>(p, p->d_u[in], p->d_u[1 - in], nullptr, st);
+    if (p->chain_on && !first) {
+        chain_pass(p, in, st);
+        chain_rest(p, in, st);
+    } else {
+        edge_pass(p, first, p->d_zb[in], p->d_u[in], first ? p->d_u[1 - in] : nullptr, st);
+        var_pass<MODE_FUSED>(p, p->d_zb[in], p->d_zb[1 - in], p->d_u[in], p->d_u[1 - in],
+                             nullptr, st);
+    }
     k_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_hist);
 }
 
@@ -497,6 +550,100 @@ int get_graph(fg_plan* p, int chunk, cudaGraphExec_t* out) {
     p->graphs[chunk] = exec;
     *out = exec;
     return 0;
+}
+
+// A run continuing from the previous one starts from slot 0 of the
+// ping-pong buffers (the captured graphs address fixed slots).
+int rebase_slots(fg_plan* p) {
+    if (p->completed & 1) {
+        CK(cudaMemcpyAsync(p->d_u[0], p->d_u[1], p->P * sizeof(double),
+                           cudaMemcpyDeviceToDevice, p->stream));
+        CK(cudaMemcpyAsync(p->d_zb[0], p->d_zb[1], p->Z * sizeof(double),
+                           cudaMemcpyDeviceToDevice, p->stream));
+    }
+    p->completed = 0;
+    return 0;
+}
+
+// The fused SVM chain applies when the plan is exactly build_svm's graph
+// (problems.py:218-239): groups norm(w_i), slack(xi_i), margin(w_i, b, xi_i),
+// equality(w_i, w_{i+1}) over N points in point order; W(i) = w0 + i and
+// XI(i) = xi0 + i; w_i's segment ranks are [norm, margin, eq(i-1,i),
+// eq(i,i+1)]; b's rank of margin i is i; and the small variable class holds
+// exactly the w's and xi's (b has degree > 32).  Anything else keeps the
+// generic per-kind path.
+void detect_svm_chain(fg_plan* p, const std::vector<int32_t>& dim,
+                      const std::vector<int32_t>& deg) {
+    p->chain_on = false;
+    if (getenv("FGADMM_NO_CHAIN") || p->partitioned() || p->tma_grid > 0) return;
+    const GroupHost *gn = nullptr, *gs = nullptr, *gm = nullptr, *ge = nullptr;
+    for (auto& g : p->groups) {
+        if (g.dev.count == 0) continue;
+        const GroupHost** slot = nullptr;
+        switch (g.dev.kind) {
+            case FG_KIND_SVM_NORM: slot = &gn; break;
+            case FG_KIND_SVM_SLACK: slot = &gs; break;
+            case FG_KIND_SVM_MARGIN: slot = &gm; break;
+            case FG_KIND_EQUALITY: slot = &ge; break;
+            default: return;
+        }
+        if (*slot) return;
+        *slot = &g;
+    }
+    if (!gn || !gs || !gm || !ge) return;
+    const int64_t n = gn->dev.count;
+    const int D = gn->dev.dim[0];
+    if (n < 2 || gs->dev.count != n || gm->dev.count != n || ge->dev.count != n - 1) return;
+    if (D < 1 || D > 32 || gm->dev.dim[0] != D || gm->dev.dim[1] != 1 || gm->dev.dim[2] != 1 ||
+        ge->dev.dim[0] != D || gs->dev.dim[0] != 1)
+        return;
+    if (!gn->dev.fp || !gs->dev.fp || !gm->dev.fp || gm->dev.fstride < D + 1) return;
+    if (gn->hsv.size() != 1 || gs->hsv.size() != 1 || gm->hsv.size() != 3 || ge->hsv.size() != 2)
+        return;
+    const int32_t w0 = gn->hsv[0][0], xi0 = gs->hsv[0][0], bv = gm->hsv[1][0];
+    if (deg[bv] != n || dim[bv] != 1 || n <= 32) return;
+    for (int64_t i = 0; i < n; ++i) {
+        const int32_t w = w0 + (int32_t)i, xi = xi0 + (int32_t)i;
+        const bool hp = i > 0, hn = i + 1 < n;
+        if (gn->hsv[0][i] != w || gn->hsk[0][i] != 0) return;
+        if (gs->hsv[0][i] != xi || gs->hsk[0][i] != 0) return;
+        if (gm->hsv[0][i] != w || gm->hsk[0][i] != 1) return;
+        if (gm->hsv[1][i] != bv || gm->hsk[1][i] != i) return;
+        if (gm->hsv[2][i] != xi || gm->hsk[2][i] != 1) return;
+        if (dim[w] != D || deg[w] != 2 + (int)hp + (int)hn) return;
+        if (dim[xi] != 1 || deg[xi] != 2) return;
+        if (hn && (ge->hsv[0][i] != w || ge->hsk[0][i] != (hp ? 3 : 2) ||
+                   ge->hsv[1][i] != w + 1 || ge->hsk[1][i] != 2))
+            return;
+    }
+    if (p->nS != (int64_t)(D + 1) * n) return;      // small class == chain vars
+    // affine addresses (fg_chain.cuh): host copies of the var tables
+    std::vector<int64_t> pb(p->V), zb(p->V);
+    std::vector<int32_t> eb(p->V);
+    if (cudaMemcpy(pb.data(), p->d_pbase, p->V * sizeof(int64_t), cudaMemcpyDeviceToHost) ||
+        cudaMemcpy(zb.data(), p->d_zbase, p->V * sizeof(int64_t), cudaMemcpyDeviceToHost) ||
+        cudaMemcpy(eb.data(), p->d_ebase, p->V * sizeof(int32_t), cudaMemcpyDeviceToHost))
+        return;
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t ow = i ? 4 * i - 1 : 0;
+        if (pb[w0 + i] != pb[w0] + ow * D || eb[w0 + i] != eb[w0] + ow ||
+            zb[w0 + i] != zb[w0] + i * D || pb[xi0 + i] != pb[xi0] + 2 * i ||
+            eb[xi0 + i] != eb[xi0] + 2 * i || zb[xi0 + i] != zb[xi0] + i)
+            return;
+    }
+    ChainDev& c = p->chain;
+    c.n = (int32_t)n;
+    c.D = D;
+    c.pW = pb[w0]; c.zW = zb[w0]; c.eW = eb[w0];
+    c.pX = pb[xi0]; c.zX = zb[xi0]; c.eX = eb[xi0];
+    c.pB = pb[bv]; c.zB = zb[bv]; c.eB = eb[bv];
+    c.fp_norm = gn->dev.fp; c.st_norm = gn->dev.fstride;
+    c.fp_slack = gs->dev.fp; c.st_slack = gs->dev.fstride;
+    c.fp_margin = gm->dev.fp; c.st_margin = gm->dev.fstride;
+    // one CTA per partial slot of the small classes it replaces
+    p->chain_grid = p->nsblk[0] + p->nsblk[1] + p->nsblk[2];
+    p->chain_minb = getenv("FGADMM_CHAIN_OCC3") ? 3 : 2;
+    p->chain_on = p->chain_grid > 0;
 }
 
 int check_launch() {
@@ -687,7 +834,33 @@ int build_group(fg_plan* p, const fg_group_desc& gd,
             g.tiles = dt;
             g.ndisks = (int32_t)K;
             g.ntiles = (int32_t)tiles.size();
+            // affine rows + 16-byte aligned center entries -> variant 3
+            bool aff = K >= 2, even = true;
+            const DiskRow& r0 = rows[0];
+            DiskRow rs{};
+            if (aff) {
+                rs.pbc = rows[1].pbc - r0.pbc; rs.pbr = rows[1].pbr - r0.pbr;
+                rs.zc = rows[1].zc - r0.zc; rs.zr = rows[1].zr - r0.zr;
+                rs.ebc = rows[1].ebc - r0.ebc; rs.ebr = rows[1].ebr - r0.ebr;
+            }
+            for (int64_t i = 0; i < K && aff; ++i) {
+                const DiskRow& r = rows[i];
+                aff = r.pbc == r0.pbc + i * rs.pbc && r.pbr == r0.pbr + i * rs.pbr &&
+                      r.zc == r0.zc + i * rs.zc && r.zr == r0.zr + i * rs.zr &&
+                      r.ebc == r0.ebc + i * rs.ebc && r.ebr == r0.ebr + i * rs.ebr;
+            }
+            for (int64_t i = 0; i < K; ++i) even = even && (rows[i].pbc % 2 == 0);
+            g.rows_affine = aff ? 1 : 0;
+            g.rows_even = even ? 1 : 0;
+            g.row0 = r0;
+            g.rowS = rs;
+            if (!cvar || std::strcmp(cvar, "v3") == 0) g.variant = 3;
         }
+    }
+    if (gd.kind == FG_KIND_SVM_NORM || gd.kind == FG_KIND_SVM_SLACK ||
+        gd.kind == FG_KIND_SVM_MARGIN || gd.kind == FG_KIND_EQUALITY) {
+        out.hsv = std::move(svs);
+        out.hsk = std::move(sks);
     }
     if (gd.fparams && gd.fstride > 0) {
         std::vector<double> fp(gd.fparams, gd.fparams + n * gd.fstride);
@@ -804,14 +977,16 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     if ((rc = dalloc(&p->d_rho, E + kPad)) || (rc = dalloc(&p->d_alpha, E + kPad)) ||
         (rc = dalloc(&p->d_zw, Z + kPad)) || (rc = dalloc(&p->d_x, P + kPad)) ||
         (rc = dalloc(&p->d_u[0], P + kPad)) || (rc = dalloc(&p->d_u[1], P + kPad)) ||
-        (rc = dalloc(&p->d_stage, std::max(P, Z))) || (rc = dalloc(&p->d_z, Z + kPad)) ||
+        (rc = dalloc(&p->d_stage, std::max(P, Z))) || (rc = dalloc(&p->d_zb[0], Z + kPad)) ||
+        (rc = dalloc(&p->d_zb[1], Z + kPad)) ||
         (rc = dalloc(&p->d_zs, Z)) || (rc = dalloc(&p->d_ctrl, 1)) ||
         (rc = dalloc(&p->d_res2, 2)))
         return rc;
     CK(cudaMemset(p->d_x, 0, P * sizeof(double)));
     CK(cudaMemset(p->d_u[0], 0, P * sizeof(double)));
     CK(cudaMemset(p->d_u[1], 0, P * sizeof(double)));
-    CK(cudaMemset(p->d_z, 0, Z * sizeof(double)));
+    CK(cudaMemset(p->d_zb[0], 0, Z * sizeof(double)));
+    CK(cudaMemset(p->d_zb[1], 0, Z * sizeof(double)));
 
     // ---- groups ----
     for (int32_t i = 0; i < ngroups; ++i) {
@@ -1029,7 +1204,13 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
         if (e1 != cudaSuccess || e2 != cudaSuccess)
             return fail(FG_ERR_CUDA, "cluster kernel shared-memory attribute");
     }
-    // residual partial slots: one per CTA of every fused var kernel
+    detect_svm_chain(p.get(), dim, deg);
+    for (auto& g : p->groups) {
+        g.hsv.clear(); g.hsv.shrink_to_fit();
+        g.hsk.clear(); g.hsk.shrink_to_fit();
+    }
+    // residual partial slots: one per CTA of every fused var kernel (the
+    // chain kernel reuses the small classes' slots 0..2, which come first)
     int64_t acc_part = 0;
     for (int w = 0; w < kVarSlots; ++w) {
         p->part_off[w] = acc_part;
@@ -1041,6 +1222,12 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     if ((rc = dalloc(&p->d_part, 2 * std::max(p->npart, nres)))) return rc;
     CK(cudaMemset(p->d_part, 0, 2 * std::max(p->npart, nres) * sizeof(double)));
     p->launches_per_iter = count_edge_launches(p.get()) + count_var_launches(p.get()) + 1;
+    p->launches_later = p->launches_per_iter;
+    if (p->chain_on) {
+        int64_t n = 2;                                   // chain kernel + reduce
+        for (int w = 0; w < kVarSlots; ++w) n += chain_rest_slot(w) && var_slot_blocks(p.get(), w) > 0;
+        p->launches_later = n;
+    }
     CK(cudaDeviceSynchronize());
     *out = p.release();
     return 0;
@@ -1052,6 +1239,8 @@ int fg_plan_info(const fg_plan* p, int64_t* o) {
     o[0] = p->V; o[1] = p->E; o[2] = p->P; o[3] = p->Z;
     o[4] = p->nS; o[5] = p->nLvars; o[6] = p->nG; o[7] = p->nGC;
     o[8] = p->launches_per_iter;
+    o[9] = p->launches_later;
+    o[10] = p->chain_on ? 1 : 0;
     return 0;
 }
 
@@ -1079,7 +1268,7 @@ static int download_ref(fg_plan* p, int mode, const double* ucur,
                         const double* uprev, double* dst_host) {
     cudaStream_t st = p->stream;
     k_scatter_to_ref<<<nblk(p->P, 256), 256, 0, st>>>(p->P, p->d_vm2ref, p->d_vmz, mode,
-                                                     p->d_x, ucur, uprev, p->d_z, p->d_stage);
+                                                     p->d_x, ucur, uprev, p->zcur(), p->d_stage);
     CK(cudaMemcpyAsync(dst_host, p->d_stage, p->P * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return check_launch();
@@ -1087,11 +1276,13 @@ static int download_ref(fg_plan* p, int mode, const double* ucur,
 
 int fg_state_upload(fg_plan* p, const double* z, const double* u, const double* n) {
     CK(cudaSetDevice(p->device));
-    CK(cudaMemcpyAsync(p->d_z, z, p->Z * sizeof(double), cudaMemcpyHostToDevice, p->stream));
+    CK(cudaMemcpyAsync(p->d_zb[0], z, p->Z * sizeof(double), cudaMemcpyHostToDevice, p->stream));
     upload_vm(p, u, p->d_u[0]);
     upload_vm(p, n, p->d_u[1]);   // consumed by the first edge pass
     CK(cudaStreamSynchronize(p->stream));
     p->completed = 0;
+    p->n_valid = 1;
+    p->x_stale = 0;
     return check_launch();
 }
 
@@ -1121,6 +1312,10 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
         h.partitioned = 1;
         h.scale = 1.0 / std::sqrt((double)p->Pglobal);
     }
+    if (int rc = rebase_slots(p)) return rc;
+    // the first iteration reads the uploaded n only right after an upload
+    const bool first_n = cfg->first_reads_n && p->n_valid;
+    p->n_valid = 0;
     CK(cudaMemcpyAsync(p->d_ctrl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
     if (!cfg->timing && K > 1) {
         // capture/instantiate the CUDA graphs this run needs before timing
@@ -1138,7 +1333,7 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
     CK(cudaEventRecord(ev0, st));
     if (cfg->timing && p->nccl_comm) {
         for (int64_t j = 1; j <= K; ++j) {
-            launch_iteration(p, (int)((j - 1) & 1), (j == 1) && cfg->first_reads_n, st);
+            launch_iteration(p, (int)((j - 1) & 1), (j == 1) && first_n, st);
             launches += p->launches_per_iter + 1;
         }
         CK(cudaEventRecord(ev1, st));
@@ -1149,16 +1344,24 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
         for (auto& e : ev) CK(cudaEventCreate(&e));
         for (int64_t j = 1; j <= K; ++j) {
             const int in = (int)((j - 1) & 1);
-            const bool first = (j == 1) && cfg->first_reads_n;
+            const bool first = (j == 1) && first_n;
             cudaEvent_t* E4 = &ev[4 * (j - 1)];
             CK(cudaEventRecord(E4[0], st));
-            edge_pass(p, first, p->d_u[in], first ? p->d_u[1 - in] : nullptr, st);
-            CK(cudaEventRecord(E4[1], st));
-            var_pass<MODE_FUSED>(p, p->d_u[in], p->d_u[1 - in], nullptr, st);
+            if (p->chain_on && j > 1) {
+                chain_pass(p, in, st);
+                CK(cudaEventRecord(E4[1], st));
+                chain_rest(p, in, st);
+            } else {
+                edge_pass(p, first, p->d_zb[in], p->d_u[in], first ? p->d_u[1 - in] : nullptr,
+                          st);
+                CK(cudaEventRecord(E4[1], st));
+                var_pass<MODE_FUSED>(p, p->d_zb[in], p->d_zb[1 - in], p->d_u[in],
+                                     p->d_u[1 - in], nullptr, st);
+            }
             CK(cudaEventRecord(E4[2], st));
             k_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_hist);
             CK(cudaEventRecord(E4[3], st));
-            launches += p->launches_per_iter;
+            launches += j > 1 ? p->launches_later : p->launches_per_iter;
         }
         CK(cudaEventRecord(ev1, st));
         CK(cudaStreamSynchronize(st));
@@ -1179,14 +1382,13 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
         for (auto& e : e4) CK(cudaEventCreate(&e));
         CK(cudaEventRecord(e4[0], st));
         if (p->nccl_comm) {
-            launch_iteration(p, 0, cfg->first_reads_n != 0, st);
+            launch_iteration(p, 0, first_n, st);
             CK(cudaEventRecord(e4[1], st));
             CK(cudaEventRecord(e4[2], st));
         } else {
-            edge_pass(p, cfg->first_reads_n != 0, p->d_u[0],
-                      cfg->first_reads_n ? p->d_u[1] : nullptr, st);
+            edge_pass(p, first_n, p->d_zb[0], p->d_u[0], first_n ? p->d_u[1] : nullptr, st);
             CK(cudaEventRecord(e4[1], st));
-            var_pass<MODE_FUSED>(p, p->d_u[0], p->d_u[1], nullptr, st);
+            var_pass<MODE_FUSED>(p, p->d_zb[0], p->d_zb[1], p->d_u[0], p->d_u[1], nullptr, st);
             CK(cudaEventRecord(e4[2], st));
             k_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_hist);
         }
@@ -1218,7 +1420,7 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
                 n = 1;
                 launch_iteration(p, 1, false, st);   // iteration index even -> in=1
             }
-            launches += n * p->launches_per_iter;
+            launches += n * p->launches_later;
             left -= n;
             CK(cudaMemcpyAsync(&h_stop[slot], &p->d_ctrl->stop, sizeof(int32_t),
                                cudaMemcpyDeviceToHost, st));
@@ -1253,6 +1455,13 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
     if (int rc = check_launch()) return rc;
     CK(cudaMemcpy(&h, p->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
     p->completed = h.completed;
+    // x of the last (or failing) iteration stays in registers when the
+    // chain kernel ran it; fg_state_download / fg_debug_download recompute it
+    p->x_stale = 0;
+    if (p->chain_on && !p->nccl_comm) {
+        const int64_t need = h.err_key != ~0ull ? (int64_t)(h.err_key >> 3) : h.completed;
+        if (need >= 2) p->x_stale = need;
+    }
     out->iterations = h.completed;
     out->converged = h.converged;
     out->primal = h.primal;
@@ -1273,8 +1482,32 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
     return 0;
 }
 
+// Recompute x of iteration `x_stale` of the last run into d_x: the edge
+// pass of that iteration from its inputs (z and u slots (it-1)&1, which
+// the iteration did not overwrite) -- the same arithmetic the chain kernel
+// used, so x is bitwise the value the iteration consumed.
+static int materialize_x(fg_plan* p) {
+    if (!p->x_stale) return 0;
+    const int64_t it = p->x_stale;
+    const int in = (int)((it - 1) & 1);
+    Ctrl h{};
+    h.err_key = ~0ull;
+    h.iter = it;
+    h.max_iter = it;
+    h.scale = 1.0 / std::sqrt((double)p->P);
+    cudaStream_t st = p->stream;
+    CK(cudaMemcpyAsync(p->d_ctrl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+    edge_pass(p, false, p->d_zb[in], p->d_u[in], nullptr, st);
+    CK(cudaStreamSynchronize(st));
+    p->x_stale = 0;
+    return check_launch();
+}
+
 int fg_state_download(fg_plan* p, double* x, double* m, double* z, double* u, double* n) {
     CK(cudaSetDevice(p->device));
+    if (x || m) {
+        if (int rc = materialize_x(p)) return rc;
+    }
     const int cur = (int)(p->completed & 1);
     const double* ucur = p->d_u[cur];
     const double* uprev = p->d_u[cur ^ 1];
@@ -1283,7 +1516,7 @@ int fg_state_download(fg_plan* p, double* x, double* m, double* z, double* u, do
     if (m && (rc = download_ref(p, 1, ucur, uprev, m))) return rc;
     if (u && (rc = download_ref(p, 2, ucur, uprev, u))) return rc;
     if (n && (rc = download_ref(p, 3, ucur, uprev, n))) return rc;
-    if (z) CK(cudaMemcpy(z, p->d_z, p->Z * sizeof(double), cudaMemcpyDeviceToHost));
+    if (z) CK(cudaMemcpy(z, p->zcur(), p->Z * sizeof(double), cudaMemcpyDeviceToHost));
     return 0;
 }
 
@@ -1291,10 +1524,17 @@ int fg_debug_download(fg_plan* p, int32_t buffer, double* out_ref) {
     CK(cudaSetDevice(p->device));
     const double* src = nullptr;
     switch (buffer) {
-        case FG_BUF_X: src = p->d_x; break;
+        case FG_BUF_X:
+            if (int rc = materialize_x(p)) return rc;
+            src = p->d_x;
+            break;
         case FG_BUF_U0: src = p->d_u[0]; break;
         case FG_BUF_U1: src = p->d_u[1]; break;
         case FG_BUF_AUX: src = p->d_aux; break;
+        case FG_BUF_Z0: case FG_BUF_Z1:
+            CK(cudaMemcpy(out_ref, p->d_zb[buffer - FG_BUF_Z0], p->Z * sizeof(double),
+                          cudaMemcpyDeviceToHost));
+            return 0;
         default: return fail(FG_ERR_INVALID, "unknown buffer id");
     }
     if (!src) return fail(FG_ERR_INVALID, "buffer not allocated");
@@ -1302,7 +1542,7 @@ int fg_debug_download(fg_plan* p, int32_t buffer, double* out_ref) {
 }
 
 // ---- unfused per-phase path ----------------------------------------------
-// buffers: x -> d_x, m -> d_u[1], z -> d_z, u -> d_u[0], n -> d_aux
+// buffers: x -> d_x, m -> d_u[1], z -> d_zb[0], u -> d_u[0], n -> d_aux
 int fg_phase_upload(fg_plan* p, const double* x, const double* m, const double* z,
                     const double* u, const double* n) {
     CK(cudaSetDevice(p->device));
@@ -1314,8 +1554,11 @@ int fg_phase_upload(fg_plan* p, const double* x, const double* m, const double* 
     upload_vm(p, m, p->d_u[1]);
     upload_vm(p, u, p->d_u[0]);
     upload_vm(p, n, p->d_aux);
-    CK(cudaMemcpyAsync(p->d_z, z, p->Z * sizeof(double), cudaMemcpyHostToDevice, p->stream));
+    CK(cudaMemcpyAsync(p->d_zb[0], z, p->Z * sizeof(double), cudaMemcpyHostToDevice, p->stream));
     CK(cudaStreamSynchronize(p->stream));
+    p->completed = 0;
+    p->n_valid = 0;
+    p->x_stale = 0;
     return check_launch();
 }
 
@@ -1328,15 +1571,18 @@ int fg_phase(fg_plan* p, int32_t phase) {
     h.iter = 1;
     CK(cudaMemcpyAsync(p->d_ctrl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
     switch (phase) {
-        case FG_PHASE_X: edge_pass(p, true, p->d_u[0], p->d_aux, st); break;
+        case FG_PHASE_X: edge_pass(p, true, p->d_zb[0], p->d_u[0], p->d_aux, st); break;
         case FG_PHASE_M:
             k_phase_m<<<nblk(p->P, 256), 256, 0, st>>>(p->P, p->d_x, p->d_u[0], p->d_u[1]); break;
-        case FG_PHASE_Z: var_pass<MODE_PHASEZ>(p, nullptr, nullptr, p->d_u[1], st); break;
+        case FG_PHASE_Z:
+            var_pass<MODE_PHASEZ>(p, p->d_zb[0], p->d_zb[0], nullptr, nullptr, p->d_u[1], st);
+            break;
         case FG_PHASE_U:
             k_phase_u<<<nblk(p->E, 256), 256, 0, st>>>(p->E, p->vt(), p->d_vmvar, p->d_x,
-                                                       p->d_z, p->d_alpha, p->d_u[0]); break;
+                                                       p->d_zb[0], p->d_alpha, p->d_u[0]); break;
         case FG_PHASE_N:
-            k_phase_n<<<nblk(p->P, 256), 256, 0, st>>>(p->P, p->d_vmz, p->d_z, p->d_u[0], p->d_aux); break;
+            k_phase_n<<<nblk(p->P, 256), 256, 0, st>>>(p->P, p->d_vmz, p->d_zb[0], p->d_u[0],
+                                                       p->d_aux); break;
         default: return fail(FG_ERR_INVALID, "unknown phase");
     }
     CK(cudaStreamSynchronize(st));
@@ -1351,7 +1597,7 @@ int fg_phase_download(fg_plan* p, double* x, double* m, double* z, double* u, do
     if (m && (rc = download_ref(p, 2, p->d_u[1], p->d_u[1], m))) return rc;
     if (u && (rc = download_ref(p, 2, p->d_u[0], p->d_u[0], u))) return rc;
     if (n && (rc = download_ref(p, 2, p->d_aux, p->d_aux, n))) return rc;
-    if (z) CK(cudaMemcpy(z, p->d_z, p->Z * sizeof(double), cudaMemcpyDeviceToHost));
+    if (z) CK(cudaMemcpy(z, p->d_zb[0], p->Z * sizeof(double), cudaMemcpyDeviceToHost));
     return 0;
 }
 
@@ -1361,10 +1607,14 @@ int fg_residuals(fg_plan* p, const double* x, const double* z, const double* zpr
     cudaStream_t st = p->stream;
     double* xs = p->d_aux ? p->d_aux : p->d_u[1];
     upload_vm(p, x, xs);
-    CK(cudaMemcpyAsync(p->d_z, z, p->Z * sizeof(double), cudaMemcpyHostToDevice, st));
+    double* zd = p->d_zb[0];
+    p->completed = 0;
+    p->n_valid = 0;
+    p->x_stale = 0;
+    CK(cudaMemcpyAsync(zd, z, p->Z * sizeof(double), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(p->d_zs, zprev, p->Z * sizeof(double), cudaMemcpyHostToDevice, st));
     const unsigned nb = nblk(p->E, 256);
-    k_residual_parts<<<nb, 256, 0, st>>>(p->E, p->vt(), p->d_vmvar, xs, p->d_z,
+    k_residual_parts<<<nb, 256, 0, st>>>(p->E, p->vt(), p->d_vmvar, xs, zd,
                                         p->d_zs, p->d_rho, p->d_part);
     k_sum_parts<<<1, 1024, 0, st>>>(p->d_part, nb, p->d_res2);
     double r2[2];
@@ -1397,41 +1647,68 @@ int fg_profile_kernels(fg_plan* p, int64_t iterations, int32_t max_slots,
     h.iter = 1;
     h.scale = 1.0 / std::sqrt((double)p->P);
     h.max_iter = iterations;
+    if (int rc = rebase_slots(p)) return rc;
+    const bool first_n = p->n_valid != 0;
+    p->n_valid = 0;
     CK(cudaMemcpyAsync(p->d_ctrl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+    // Generic plans time every iteration; with the fused chain on, iteration
+    // 1 runs the generic path untimed and iterations 2.. are timed.
+    const bool chain = p->chain_on;
     std::vector<std::string> names;
-    for (auto& g : p->groups)
-        if (g.dev.count > 0) names.push_back(std::string("edge_") + kind_name(g.dev.kind));
-    const int nedge = (int)names.size();
     std::vector<int> vk;
-    for (int w = 0; w < kVarSlots; ++w) {
-        if (var_slot_blocks(p, w) > 0 && fused_slot(p, w)) {
-            vk.push_back(w);
-            names.push_back(kVarNames[w]);
-        }
+    if (chain) {
+        names.push_back("chain_svm");
+        for (int w = 0; w < kVarSlots; ++w)
+            if (chain_rest_slot(w) && var_slot_blocks(p, w) > 0) {
+                vk.push_back(w);
+                names.push_back(kVarNames[w]);
+            }
+    } else {
+        for (auto& g : p->groups)
+            if (g.dev.count > 0) names.push_back(std::string("edge_") + kind_name(g.dev.kind));
+        for (int w = 0; w < kVarSlots; ++w)
+            if (var_slot_blocks(p, w) > 0 && fused_slot(p, w)) {
+                vk.push_back(w);
+                names.push_back(kVarNames[w]);
+            }
     }
     names.push_back("reduce");
     const int ns = (int)names.size();
     if (ns > max_slots) return fail(FG_ERR_INVALID, "too many kernels for the output arrays");
-    std::vector<cudaEvent_t> ev((size_t)(ns + 1) * iterations);
+    const int64_t j0 = chain ? 2 : 1;
+    const int64_t timed = iterations - j0 + 1;
+    if (timed < 1) return fail(FG_ERR_INVALID, "profile needs at least 2 iterations (fused chain)");
+    std::vector<cudaEvent_t> ev((size_t)(ns + 1) * timed);
     for (auto& e : ev) CK(cudaEventCreate(&e));
-    PassA a0{p->vt(), p->d_z, nullptr, nullptr, p->d_x, p->d_rho, p->d_ctrl};
+    PassA a0{p->vt(), nullptr, nullptr, nullptr, p->d_x, p->d_rho, p->d_ctrl};
     for (int64_t j = 1; j <= iterations; ++j) {
         const int in = (int)((j - 1) & 1);
-        const bool first = (j == 1);
-        cudaEvent_t* E = &ev[(size_t)(ns + 1) * (j - 1)];
+        const bool first = (j == 1) && first_n;
+        if (j < j0) {
+            launch_iteration(p, in, first, st);
+            continue;
+        }
+        cudaEvent_t* E = &ev[(size_t)(ns + 1) * (j - j0)];
         int slot = 0;
-        PassA a = a0;
-        a.uin = p->d_u[in];
-        a.nsrc = first ? p->d_u[1 - in] : nullptr;
         CK(cudaEventRecord(E[0], st));
-        for (auto& g : p->groups) {
-            if (g.dev.count == 0) continue;
-            if (first) launch_kind<true>(g.dev, a, st);
-            else launch_kind<false>(g.dev, a, st);
+        if (chain) {
+            chain_pass(p, in, st);
             CK(cudaEventRecord(E[++slot], st));
+        } else {
+            PassA a = a0;
+            a.z = p->d_zb[in];
+            a.uin = p->d_u[in];
+            a.nsrc = first ? p->d_u[1 - in] : nullptr;
+            for (auto& g : p->groups) {
+                if (g.dev.count == 0) continue;
+                if (first) launch_kind<true>(g.dev, a, st);
+                else launch_kind<false>(g.dev, a, st);
+                CK(cudaEventRecord(E[++slot], st));
+            }
         }
         for (int w : vk) {
-            var_kernel<MODE_FUSED>(p, w, p->d_u[in], p->d_u[1 - in], nullptr, st);
+            var_kernel<MODE_FUSED>(p, w, p->d_zb[in], p->d_zb[1 - in], p->d_u[in],
+                                   p->d_u[1 - in], nullptr, st);
             CK(cudaEventRecord(E[++slot], st));
         }
         k_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_hist);
@@ -1439,8 +1716,8 @@ int fg_profile_kernels(fg_plan* p, int64_t iterations, int32_t max_slots,
     }
     CK(cudaStreamSynchronize(st));
     if (int rc = check_launch()) return rc;
-    for (int i = 0; i < ns; ++i) { ms[i] = 0.0; counts[i] = iterations; }
-    for (int64_t j = 0; j < iterations; ++j)
+    for (int i = 0; i < ns; ++i) { ms[i] = 0.0; counts[i] = timed; }
+    for (int64_t j = 0; j < timed; ++j)
         for (int i = 0; i < ns; ++i) {
             float t = 0;
             cudaEventElapsedTime(&t, ev[(size_t)(ns + 1) * j + i], ev[(size_t)(ns + 1) * j + i + 1]);
@@ -1452,10 +1729,10 @@ int fg_profile_kernels(fg_plan* p, int64_t iterations, int32_t max_slots,
         std::strncpy(labels + 32 * i, names[i].c_str(), 31);
     }
     *nslots = ns;
-    (void)nedge;
     Ctrl hc;
     CK(cudaMemcpy(&hc, p->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
     p->completed = hc.completed;
+    p->x_stale = 0;
     return 0;
 }
 
@@ -1621,6 +1898,8 @@ int fg_plan_attach_nccl(fg_plan* p, const char* nccl_lib, const char* id128, int
     if (int rc = nccl_check(g_nccl.CommInitRank(&comm, world, id, rank), "ncclCommInitRank"))
         return rc;
     p->nccl_comm = comm;
+    p->chain_on = false;               // the fused chain is single-device only
+    p->launches_later = p->launches_per_iter;
     p->world = world;
     p->rank = rank;
     {   // global payload = sum of the ranks' local payloads (disjoint edges)
@@ -1656,12 +1935,16 @@ int fg_group_run(fg_plan** plans, int32_t G, const fg_run_config* cfg, double* h
     const int64_t K = cfg->max_iterations;
     if (K < 1) return fail(FG_ERR_INVALID, "max_iterations must be >= 1");
     const int64_t ncut = p0->ncut;
+    bool first_n = cfg->first_reads_n != 0;
     for (int r = 0; r < G; ++r) {
         fg_plan* p = plans[r];
         if (p->device != p0->device || p->ncut != ncut)
             return fail(FG_ERR_INVALID, "group plans must share one device and cut vector");
         p->world = G;
         p->rank = r;
+        if (int rc = rebase_slots(p)) return rc;
+        if (!p->n_valid) first_n = false;
+        p->n_valid = 0;
         if (p->d_recv) cudaFree(p->d_recv);
         p->d_recv = nullptr;
         if (int rc = dalloc(&p->d_recv, (size_t)G * (ncut + 4))) return rc;
@@ -1702,7 +1985,7 @@ int fg_group_run(fg_plan** plans, int32_t G, const fg_run_config* cfg, double* h
     };
     for (int64_t j = 1; j <= K; ++j) {
         const int in = (int)((j - 1) & 1);
-        const bool first = (j == 1) && cfg->first_reads_n;
+        const bool first = (j == 1) && first_n;
         for (int r = 0; r < G; ++r) part_pre(plans[r], in, first, st);
         if (ncut) { if (int rc = gather(0, (size_t)ncut, 0)) return rc; }
         for (int r = 0; r < G; ++r) part_mid(plans[r], in, st);
@@ -1757,7 +2040,7 @@ int fg_group_run(fg_plan** plans, int32_t G, const fg_run_config* cfg, double* h
 extern "C" int fg_evaluate(fg_plan* p, const double* z_host, double* out2) {
     CK(cudaSetDevice(p->device));
     cudaStream_t st = p->stream;
-    const double* z = p->d_z;
+    const double* z = p->zcur();
     if (z_host) {
         CK(cudaMemcpyAsync(p->d_zs, z_host, p->Z * sizeof(double), cudaMemcpyHostToDevice, st));
         z = p->d_zs;

@@ -30,7 +30,8 @@ struct PassB {
     const double* uin;
     double* uout;
     const double* msrc;      // PHASEZ: materialized m
-    double* z;
+    double* z;               // z written by this pass
+    const double* zin;       // z of the previous iteration (== z in PHASEZ)
     const double* rho;
     const double* alpha;
     const double* zw;
@@ -117,10 +118,10 @@ __global__ void __launch_bounds__(256) k_var_small(PassB b, const int32_t* list,
         ValFn<MODE> val(b, r, &bm);
         double S = val(0);                           // reduceat: a[0] + tree
         if (r.deg > 1) S = S + leaf_seq(val, 1, r.deg - 1);
-        const double zn = S / b.zw[k];
+        const double zn = ddiv(S, b.zw[k]);
         bz = !finite(zn);
         if (MODE == MODE_FUSED) {
-            const double zo = b.z[k];
+            const double zo = b.zin[k];
             b.z[k] = zn;
             update_range(b, r, 0, r.deg, 1, zn, zo, pp, dd, bu);
             if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
@@ -196,10 +197,10 @@ __global__ void __launch_bounds__(kVarThreads) k_var_large(
     ValFn<MODE> val(b, r, &bm);
     const double T = run_units_and_tree(val, 1, prog + progoff[blockIdx.x], sv);
     if (threadIdx.x == 0) {
-        const double zn = (val(0) + T) / b.zw[k];
+        const double zn = ddiv(val(0) + T, b.zw[k]);
         bz = !finite(zn);
         s_z[0] = zn;
-        s_z[1] = (MODE == MODE_FUSED) ? b.z[k] : 0.0;
+        s_z[1] = (MODE == MODE_FUSED) ? b.zin[k] : 0.0;
         b.z[k] = zn;
     }
     __syncthreads();
@@ -281,9 +282,9 @@ __global__ void __launch_bounds__(kVarThreads) k_var_giant_top(
         const CompRef r = comp_ref(b, k);
         bool bm = false;
         ValFn<MODE> val(b, r, &bm);
-        const double zn = (val(0) + sv[node - 1]) / b.zw[k];
+        const double zn = ddiv(val(0) + sv[node - 1], b.zw[k]);
         gz[2 * blockIdx.x] = zn;
-        gz[2 * blockIdx.x + 1] = (MODE == MODE_FUSED) ? b.z[k] : 0.0;
+        gz[2 * blockIdx.x + 1] = (MODE == MODE_FUSED) ? b.zin[k] : 0.0;
         b.z[k] = zn;
         if (MODE == MODE_FUSED) {
             if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
@@ -366,9 +367,9 @@ __global__ void k_cut_finalize(PassB b, const int32_t* glist, const GComp* comps
     const int32_t k = glist[gi];
     double tot = recv[gc.pad0];
     for (int r = 1; r < world; ++r) tot = tot + recv[(int64_t)r * ncut + gc.pad0];
-    const double zn = tot / b.zw[k];
+    const double zn = ddiv(tot, b.zw[k]);
     gz[2 * gi] = zn;
-    gz[2 * gi + 1] = b.z[k];
+    gz[2 * gi + 1] = b.zin[k];
     b.z[k] = zn;
     if (!finite(zn)) flag_error(b.ctrl, b.ctrl->iter, FG_PHASE_Z, false);
 }

@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(kEdgeThreads) k_mpc_dyn8(PassA a, GroupDev g) 
         for (int i = l; i < d; i += kDynLanes) {               // y = diag Q^T (M nv)
             double acc = 0.0;
             for (int q = 0; q < d; ++q) acc += Q[q * d + i] * v1[q];
-            v2[i] = acc / (Lam[i] / R0 + 1.0 / R1);
+            v2[i] = ddiv(acc, ddiv(Lam[i], R0) + ddiv(1.0, R1));
         }
         __syncwarp(gmask);
         for (int q = l; q < d; q += kDynLanes) {               // lambda = Q y
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kEdgeThreads) k_mpc_dyn8(PassA a, GroupDev g) 
         for (int c = l; c < cols; c += kDynLanes) {            // v = nv - W^-1 M^T lambda
             double acc = 0.0;
             for (int q = 0; q < d; ++q) acc += M[q * cols + c] * v1[q];
-            const double winv = 1.0 / ((c < n0) ? R0 : R1);
+            const double winv = ddiv(1.0, (c < n0) ? R0 : R1);
             const double vv = nv[c] - winv * acc;
             if (c < n0) xput(a, s0.pos + c, vv, bx);
             else xput(a, s1.pos + (c - n0), vv, bx);

@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(kTmaThreads) k_var_small_tma(
         bulk_g2s(p, b.uin + sx.lo, bx, &full[s]);   p += sx.n;
         bulk_g2s(p, b.rho + se.lo, be, &full[s]);   p += se.n;
         bulk_g2s(p, b.alpha + se.lo, be, &full[s]); p += se.n;
-        bulk_g2s(p, b.z + sz.lo, bz, &full[s]);     p += sz.n;
+        bulk_g2s(p, b.zin + sz.lo, bz, &full[s]);     p += sz.n;
         bulk_g2s(p, b.zw + sz.lo, bz, &full[s]);
     };
 
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kTmaThreads) k_var_small_tma(
             };
             double S = val(0);                                    // reduceat a[0]
             if (deg > 1) S = S + leaf_seq(val, 1, deg - 1);
-            const double zn = S / ZW[q];
+            const double zn = ddiv(S, ZW[q]);
             const double zo = ZO[q];
             const int64_t kz = R.zb0 + (int64_t)T.v0 * d + q;
             b.z[kz] = zn;

@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(256, 4) k_var_small_run(PassB b, const SRun* r
             double xv[NR], uv[NR], rv[NR], av[NR];
             // z_old and z_weights are issued with the segment loads so the
             // whole component costs one memory round trip
-            const double zo = (MODE == MODE_FUSED) ? b.z[k] : 0.0;
+            const double zo = (MODE == MODE_FUSED) ? b.zin[k] : 0.0;
             const double zw = b.zw[k];
 #pragma unroll
             for (int e = 0; e < DMAX; ++e) {
@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(256, 4) k_var_small_run(PassB b, const SRun* r
                 }
             }
             if (deg > 1) S = S + res;                        // a[0] + tree
-            const double zn = S / zw;
+            const double zn = ddiv(S, zw);
             if (MODE == MODE_FUSED) {
                 b.z[k] = zn;
                 const double dz = zn - zo;
@@ -113,9 +113,9 @@ __global__ void __launch_bounds__(256, 4) k_var_small_run(PassB b, const SRun* r
             ValFn<MODE> val(b, r, &bm);
             double S = val(0);
             if (deg > 1) S = S + leaf_seq(val, 1, deg - 1);
-            const double zn = S / b.zw[k];
+            const double zn = ddiv(S, b.zw[k]);
             if (MODE == MODE_FUSED) {
-                const double zo = b.z[k];
+                const double zo = b.zin[k];
                 b.z[k] = zn;
                 update_range(b, r, 0, deg, 1, zn, zo, pp, dd, bu);
                 if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(256, 4) k_var_small_run(PassB b, const SRun* r
 
 // Class L, one CTA per variable with D components.
 template <int D, int MODE>
-__global__ void __launch_bounds__(kLargeThreads) k_var_large_vec(
+__global__ void __launch_bounds__(kLargeThreads, 2) k_var_large_vec(
     PassB b, const int32_t* vlist, const int32_t* progoff, const int32_t* prog,
     int64_t part_off) {
     __shared__ double sv[D][2 * kMaxUnits];
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(kLargeThreads) k_var_large_vec(
                 }
         } else {
             vals(base + j, acc);
-#pragma unroll 4
+#pragma unroll 8
             for (int64_t i = kUnroll; i < top; i += kUnroll) {
                 vals(base + i + j, tmp);
 #pragma unroll
@@ -236,9 +236,9 @@ __global__ void __launch_bounds__(kLargeThreads) k_var_large_vec(
         vals(0, a0);
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-            const double zn = (a0[c] + sv[c][node - 1]) / b.zw[zb + c];
+            const double zn = ddiv(a0[c] + sv[c][node - 1], b.zw[zb + c]);
             s_z[0][c] = zn;
-            s_z[1][c] = (MODE == MODE_FUSED) ? b.z[zb + c] : 0.0;
+            s_z[1][c] = (MODE == MODE_FUSED) ? b.zin[zb + c] : 0.0;
             b.z[zb + c] = zn;
             if (MODE == MODE_FUSED && !finite(zn)) flag_error(b.ctrl, it, FG_PHASE_Z, false);
         }
@@ -249,18 +249,40 @@ __global__ void __launch_bounds__(kLargeThreads) k_var_large_vec(
 #pragma unroll
         for (int c = 0; c < D; ++c) { zn[c] = s_z[0][c]; dz[c] = zn[c] - s_z[1][c]; }
         double pp = 0.0, dd = 0.0;
-        for (int64_t e = threadIdx.x; e < deg; e += kLargeThreads) {
-            const double r = b.rho[eb + e], al = b.alpha[eb + e];
+        // batches of kUB elements per thread: all loads of a batch are issued
+        // before its stores (the compiler cannot prove uout aliases nothing
+        // read here), one memory round trip per batch
+        constexpr int kUB = D == 1 ? 4 : 2;
+        for (int64_t e0 = threadIdx.x; e0 < deg; e0 += kUB * kLargeThreads) {
+            double xr[kUB][D], ur[kUB][D], rr[kUB], ar[kUB];
 #pragma unroll
-            for (int c = 0; c < D; ++c) {
-                const int64_t p = pb + e * D + c;
-                const double t = b.x[p] - zn[c];
-                pp += t * t;
-                const double rd = r * dz[c];
-                dd += rd * rd;
-                const double un = b.uin[p] + t * al;
-                b.uout[p] = un;
-                bu |= !finite(un);
+            for (int k = 0; k < kUB; ++k) {
+                const int64_t e = e0 + (int64_t)k * kLargeThreads;
+                if (e < deg) {
+                    rr[k] = b.rho[eb + e];
+                    ar[k] = b.alpha[eb + e];
+#pragma unroll
+                    for (int c = 0; c < D; ++c) {
+                        xr[k][c] = b.x[pb + e * D + c];
+                        ur[k][c] = b.uin[pb + e * D + c];
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < kUB; ++k) {
+                const int64_t e = e0 + (int64_t)k * kLargeThreads;
+                if (e < deg) {
+#pragma unroll
+                    for (int c = 0; c < D; ++c) {
+                        const double t = xr[k][c] - zn[c];
+                        pp += t * t;
+                        const double rd = rr[k] * dz[c];
+                        dd += rd * rd;
+                        const double un = ur[k][c] + t * ar[k];
+                        b.uout[pb + e * D + c] = un;
+                        bu |= !finite(un);
+                    }
+                }
             }
         }
         if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
@@ -407,8 +429,8 @@ k_var_cluster(PassB b, const int32_t* vlist, const int32_t* progoff, const int32
         }
         if (threadIdx.x == 0) {
             for (int c = 0; c < D; ++c) {
-                const double zn = (a0[c] + sv[c][node - 1]) / b.zw[zb + c];
-                const double zo = (MODE == MODE_FUSED) ? b.z[zb + c] : 0.0;
+                const double zn = ddiv(a0[c] + sv[c][node - 1], b.zw[zb + c]);
+                const double zo = (MODE == MODE_FUSED) ? b.zin[zb + c] : 0.0;
                 b.z[zb + c] = zn;
                 if (MODE == MODE_FUSED && !finite(zn)) flag_error(b.ctrl, it, FG_PHASE_Z, false);
                 for (int q = 0; q < kCluster; ++q) {

@@ -239,12 +239,14 @@ class DevicePlan:
         _native.check(lib.fg_plan_create(C.byref(gd), descs, len(self.groups),
                                          self.device, C.byref(handle)))
         self._h = handle
-        info = (C.c_int64 * 9)()
+        info = (C.c_int64 * 11)()
         lib.fg_plan_info(self._h, info)
         self.info = {"V": info[0], "E": info[1], "P": info[2], "Z": info[3],
                      "small_components": info[4], "large_components": info[5],
                      "giant_components": info[6], "giant_chunks": info[7],
-                     "launches_per_iteration": info[8]}
+                     "launches_per_iteration": info[8],
+                     "launches_later_iterations": info[9],
+                     "fused_chain": bool(info[10])}
         self._synced_version = None
         self._lib = lib
 
@@ -342,7 +344,8 @@ class DevicePlan:
         return out
 
     def debug_buffer(self, which):
-        out = np.empty(self.P)
+        z_slot = which in (_native.BUF_Z0, _native.BUF_Z1)
+        out = np.empty(self.Z if z_slot else self.P)
         _native.check(self._lib.fg_debug_download(self._h, int(which), _native.dptr(out)))
         return out
 
@@ -507,8 +510,8 @@ def _raise_device_error(graph, plan, state, res):
     x = plan.debug_buffer(_native.BUF_X)
     cur = plan.debug_buffer(_native.BUF_U0 if ((it - 1) & 1) == 0 else _native.BUF_U1)
     nxt = plan.debug_buffer(_native.BUF_U1 if ((it - 1) & 1) == 0 else _native.BUF_U0)
-    z = np.empty(plan.Z)
-    plan.download(z=z)
+    # z after iteration it's z update lives in ping-pong slot it & 1
+    z = plan.debug_buffer(_native.BUF_Z1 if (it & 1) else _native.BUF_Z0)
     if phase == "x":
         arr = x
     elif phase == "m":
