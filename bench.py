@@ -122,26 +122,27 @@ def kernel_bytes(graph, plan):
     out["reduce"] = 16 * (plan.info["small_components"] // 256 + 1
                           + plan.info["large_components"] + 64)
     if plan.info.get("fused_chain"):
-        out["chain_svm"] = chain_bytes(graph, dims, deg)
+        out["chain_svm"] = chain_bytes(graph, dims, deg, plan.chain_form() == "unit")
     return out
 
 
-def chain_bytes(graph, dims, deg):
+def chain_bytes(graph, dims, deg, unit):
     """Compulsory bytes of one fused SVM-chain launch (csrc/fg_chain.cuh):
-    per weight copy w_i (dim D, degree 3-4) u read+write, z read+write,
-    z_weights, rho+alpha per edge; per slack xi_i the same at dim 1,
-    degree 2; per point the margin data (x_i, y_i), norm scale and slack
-    lam, plus b's u and rho read and x write.  Neighbours' equality edges
-    are re-reads of the same arrays (L2), not counted."""
+    per weight copy w_i (dim D, degree 3-4) u read+write and z read+write;
+    per slack xi_i the same at dim 1, degree 2; per point the margin data
+    (x_i, y_i), x.x, the norm and slack parameters, b's u read and x write.
+    The general-weight forms also read z weights and rho/alpha per edge (and
+    b's rho); the unit-weight form reads none of them.  Neighbours'
+    equality edges are re-reads of the same arrays (L2), not counted."""
     n = int(np.sum(deg == 2))                  # xi's (b has degree n > 32)
     wsel = (deg >= 3) & (deg <= 4)
     P_w = int(np.sum(deg[wsel] * dims[wsel]))
     Z_w = int(np.sum(dims[wsel]))
     E_w = int(np.sum(deg[wsel]))
     D = int(dims[wsel][0]) if wsel.any() else 0
-    w = P_w * 16 + Z_w * 24 + E_w * 16
-    xi = n * (2 * 16 + 24 + 2 * 16)
-    per_point = (D + 3) * 8 + 24
+    w = P_w * 16 + Z_w * 16 + (0 if unit else Z_w * 8 + E_w * 16)
+    xi = n * (2 * 16 + 16 + (0 if unit else 8 + 2 * 16))
+    per_point = (D + 1) * 8 + 3 * 8 + 8 + 8 + (0 if unit else 8)
     return w + xi + n * per_point
 
 
@@ -216,6 +217,18 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
+
+def ncu_traffic(workload, kernel):
+    """Per-launch DRAM bytes (read + write) of `kernel` from the committed
+    ncu --set full capture summary (profiles/traffic.json, written by
+    tools/traffic_json.py from the round's final_<workload>.ncu-rep)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            data = json.load(fh)
+        return float(data[workload]["bytes_per_launch"][kernel])
+    except (OSError, KeyError, ValueError):
+        return None
+
 
 def measured_peak():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -379,7 +392,7 @@ def main():
     avg_ms = prof[top][0] / prof[top][1]
     peak, peak_kind = measured_peak()
     achieved = kb.get(base, 0) / (avg_ms / 1e3) / 1e9
-    iter_bytes = sum(kb.values())
+    iter_bytes = sum(kb.get(k.split("#")[0], 0) for k in prof)
     iter_ms = sum(v[0] for v in prof.values()) / prof[top][1]
 
     # ---- end to end through the public API (host state in, host state out) ----
@@ -413,7 +426,8 @@ def main():
                    "build_seconds": round(t_build, 2)},
         "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None,
+                     "traffic": ncu_traffic(args.workload, base),
+                     "alg_bytes": kb.get(base, 0),
                      "iteration": {"alg_bytes": iter_bytes,
                                    "survey_B_alg": survey_alg_bytes(g),
                                    "ms": iter_ms,

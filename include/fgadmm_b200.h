@@ -152,9 +152,11 @@ typedef struct {
 int fg_plan_create(const fg_graph_desc* graph, const fg_group_desc* groups,
                    int32_t ngroups, int32_t device, fg_plan** out);
 void fg_plan_destroy(fg_plan* plan);
-/* out[0..10]: V, E, P, Z, small / large / giant components, giant chunks,
- * launches of iteration 1, launches of later iterations, fused SVM chain on */
-int fg_plan_info(const fg_plan* plan, int64_t* out11);
+/* out[0..11]: V, E, P, Z, small / large / giant components, giant chunks,
+ * launches of iteration 1, launches of later iterations, fused SVM chain on,
+ * chain form (0 off, 1 generic, 2 fast, 3 unit-weight; the unit form is
+ * re-decided at every fg_plan_sync_params) */
+int fg_plan_info(const fg_plan* plan, int64_t* out12);
 int fg_plan_sync_params(fg_plan* plan, const double* edge_rho,
                         const double* edge_alpha, const double* z_weights);
 

@@ -42,6 +42,8 @@ struct ChainDev {
     const double* fp_norm;        // per point: scale
     const double* fp_slack;       // per point: lam
     const double* fp_margin;      // per point: x (D), y
+    const double* xx;             // per point: x.x (plan-time, margin order)
+    const double* fnorm;          // per point: 1/(1+scale) (unit-weight form)
 };
 
 constexpr int kChainThreads = 256;
@@ -57,10 +59,14 @@ enum : int {
     kSZB = 20, kSUB = 21, kSRB = 22
 };
 
+// Generic form (any D <= 32, end points): handles points ilo, ilo + istep,
+// ... < ihi, spread over the grid.
 template <int MINB>
 __global__ void __launch_bounds__(kChainThreads, MINB) k_svm_chain(PassB b, ChainDev c,
                                                                 double* xb_out,
-                                                                int64_t part_off) {
+                                                                int64_t part_off,
+                                                                int32_t ilo, int32_t ihi,
+                                                                int32_t istep) {
     __shared__ double sm[16];
     if (b.ctrl->stop) return;                        // uniform
     const int64_t it = b.ctrl->iter;
@@ -68,9 +74,10 @@ __global__ void __launch_bounds__(kChainThreads, MINB) k_svm_chain(PassB b, Chai
     const int D = c.D;
     const bool act = lane < D;
     const int cl = act ? lane : 0;                   // clamped component
-    const int32_t per_cta = (c.n + gridDim.x - 1) / gridDim.x;
-    const int32_t i0 = blockIdx.x * per_cta;
-    const int32_t i1 = min(c.n, i0 + per_cta);
+    const int32_t npts = (ihi - ilo + istep - 1) / istep;
+    const int32_t per_cta = (npts + gridDim.x - 1) / gridDim.x;
+    const int32_t j0 = blockIdx.x * per_cta;
+    const int32_t j1 = min(npts, j0 + per_cta);
     double pp = 0.0, dd = 0.0;
     bool bn = false, bx = false, bm = false, bz = false, bu = false;
     auto S = [&](double v, int src) { return __shfl_sync(kFull, v, src); };
@@ -97,7 +104,8 @@ __global__ void __launch_bounds__(kChainThreads, MINB) k_svm_chain(PassB b, Chai
             else if (lane < kSRP) sb = b.alpha + c.eW;
             break;
     }
-    for (int32_t i = i0 + warp; i < i1; i += kChainThreads / 32) {
+    for (int32_t jj = j0 + warp; jj < j1; jj += kChainThreads / 32) {
+        const int32_t i = ilo + jj * istep;
         const bool hasP = i > 0, hasN = i + 1 < c.n;
         const int32_t ow = i ? 4 * i - 1 : 0;        // first element of w_i
         const int64_t pw = c.pW + (int64_t)ow * D, zwi = c.zW + (int64_t)i * D + cl;
@@ -264,6 +272,327 @@ __global__ void __launch_bounds__(kChainThreads, MINB) k_svm_chain(PassB b, Chai
         b.part[2 * (part_off + blockIdx.x)] = pp;
         b.part[2 * (part_off + blockIdx.x) + 1] = dd;
     }
+}
+
+// ---------------------------------------------------------------------------
+// Fast form: D = 32 (one lane per component, no inactive lanes) and interior
+// points 1 <= i <= n-2 (degree 4: norm, margin, eq(i-1,i), eq(i,i+1)).
+// Every address is a per-point base plus a compile-time offset, the 24
+// per-point scalars are one load per lane (base + i * stride, set up once
+// per thread), and x.x of the margin (constant per point) comes from a
+// table computed at plan time in k_svm_margin's order.  Same arithmetic as
+// the generic form operation by operation.
+enum : int { kSZWX = 23, kSXX = 24 };
+
+template <int D>
+__global__ void __launch_bounds__(kChainThreads, 2) k_svm_chain_fast(PassB b, ChainDev c,
+                                                                    double* xb_out,
+                                                                    int64_t part_off) {
+    static_assert(D == 32, "one lane per component");
+    __shared__ double sm[16];
+    if (b.ctrl->stop) return;
+    const int64_t it = b.ctrl->iter;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int32_t nin = c.n - 2;                     // interior points 1..n-2
+    const int32_t per_cta = (nin + gridDim.x - 1) / gridDim.x;
+    const int32_t i0 = 1 + blockIdx.x * per_cta;
+    const int32_t i1 = min(c.n - 1, i0 + per_cta);
+    // lane scalar: sb + i * ss (w_i's edges start at 4i - 1)
+    const double* sb = b.rho;
+    int64_t ss = 0;
+    switch (lane) {
+        case 0: case 1: case 2: case 3: sb = b.rho + c.eW - 1 + lane; ss = 4; break;
+        case 4: case 5: case 6: case 7: sb = b.alpha + c.eW - 1 + (lane - 4); ss = 4; break;
+        case kSRP: sb = b.rho + c.eW - 2; ss = 4; break;           // w_{i-1}'s eq
+        case kSRN: sb = b.rho + c.eW - 1 + 6; ss = 4; break;       // w_{i+1}'s eq
+        case kSY: sb = c.fp_margin + D; ss = c.st_margin; break;
+        case kSScale: sb = c.fp_norm; ss = c.st_norm; break;
+        case kSLam: sb = c.fp_slack; ss = c.st_slack; break;
+        case kSZX: sb = b.zin + c.zX; ss = 1; break;
+        case kSUX0: sb = b.uin + c.pX; ss = 2; break;
+        case kSUX1: sb = b.uin + c.pX + 1; ss = 2; break;
+        case kSRX0: sb = b.rho + c.eX; ss = 2; break;
+        case kSRX1: sb = b.rho + c.eX + 1; ss = 2; break;
+        case kSAX0: sb = b.alpha + c.eX; ss = 2; break;
+        case kSAX1: sb = b.alpha + c.eX + 1; ss = 2; break;
+        case kSZB: sb = b.zin + c.zB; ss = 0; break;
+        case kSUB: sb = b.uin + c.pB; ss = 1; break;
+        case kSRB: sb = b.rho + c.eB; ss = 1; break;
+        case kSZWX: sb = b.zw + c.zX; ss = 1; break;
+        case kSXX: sb = c.xx; ss = 1; break;
+        default: break;
+    }
+    double pp = 0.0, dd = 0.0;
+    bool bn = false, bx = false, bm = false, bz = false, bu = false;
+    auto S = [&](double v, int src) { return __shfl_sync(kFull, v, src); };
+    for (int32_t i = i0 + warp; i < i1; i += kChainThreads / 32) {
+        // w_i's segment: elements 4i-1 .. 4i+2 of the w block
+        const int64_t wo = c.pW + (int64_t)(4 * i - 1) * D + lane;
+        const double* __restrict__ U = b.uin + wo;
+        const double* __restrict__ Z = b.zin + c.zW + (int64_t)i * D + lane;
+        const double u0 = U[0], u1 = U[D], u2 = U[2 * D], u3 = U[3 * D];
+        const double up = U[-D];                     // w_{i-1}: eq(i-1, i)
+        const double un_ = U[6 * D];                 // w_{i+1}: eq(i, i+1)
+        const double zi = Z[0], zp = Z[-D], zn_ = Z[D];
+        const double zwv = b.zw[c.zW + (int64_t)i * D + lane];
+        const double X = c.fp_margin[(int64_t)i * c.st_margin + lane];
+        const double sv = sb[(int64_t)i * ss];
+        // ---- phase n ----
+        const double n0 = zi - u0, n1 = zi - u1, n2 = zi - u2, n3 = zi - u3;
+        const double np_ = zp - up, nn_ = zn_ - un_;
+        const double zxi = S(sv, kSZX), ux0 = S(sv, kSUX0), ux1 = S(sv, kSUX1);
+        const double nb = S(sv, kSZB) - S(sv, kSUB), nx0 = zxi - ux0, nx1 = zxi - ux1;
+        bn |= !(finite(n0) && finite(n1) && finite(n2) && finite(n3) && finite(np_) &&
+                finite(nn_) && finite(nb) && finite(nx0) && finite(nx1));
+        // ---- phase x ----
+        const double r0 = S(sv, 0), r1 = S(sv, 1), r2 = S(sv, 2), r3 = S(sv, 3);
+        const double x0 = prox_svm_norm(n0, r0, S(sv, kSScale));
+        const double pr = n1 * X;
+        const int g = lane & 7;
+        double dot = 0.0;
+        dot += S(pr, g);
+        dot += S(pr, g + 8);
+        dot += S(pr, g + 16);
+        dot += S(pr, g + 24);
+        dot += __shfl_xor_sync(kFull, dot, 1);
+        dot += __shfl_xor_sync(kFull, dot, 2);
+        dot += __shfl_xor_sync(kFull, dot, 4);
+        const double Y = S(sv, kSY), rb = S(sv, kSRB), R3 = S(sv, kSRX1);
+        const double slack = (1.0 - nx1) - Y * (dot + nb);
+        const double denom = (ddiv(S(sv, kSXX), r1) + ddiv(1.0, rb)) + ddiv(1.0, R3);
+        const double mu = ddiv(np_max0(slack), denom);
+        const double tw = ddiv(mu, r1) * Y;
+        const double x1 = n1 + tw * X;
+        const double xbv = nb + ddiv(mu, rb) * Y;
+        const double xx1 = nx1 + ddiv(mu, R3);
+        const double rx0 = S(sv, kSRX0);
+        const double xx0 = prox_svm_slack(nx0, rx0, S(sv, kSLam));
+        const double x2 = prox_equality(np_, n2, S(sv, kSRP), r2);
+        const double x3 = prox_equality(n3, nn_, r3, S(sv, kSRN));
+        bx |= !(finite(x0) && finite(x1) && finite(x2) && finite(x3) && finite(xbv) &&
+                finite(xx0) && finite(xx1));
+        // ---- phases m, z, u of w_i ----
+        const double m0 = x0 + u0, m1 = x1 + u1, m2 = x2 + u2, m3 = x3 + u3;
+        bm |= !(finite(m0) && finite(m1) && finite(m2) && finite(m3));
+        double res = 0.0;
+        res += m1 * r1;
+        res += m2 * r2;
+        res += m3 * r3;
+        const double zn = ddiv(m0 * r0 + res, zwv);
+        bz |= !finite(zn);
+        b.z[c.zW + (int64_t)i * D + lane] = zn;
+        const double dz = zn - zi;
+        const double a0 = S(sv, 4), a1 = S(sv, 5), a2 = S(sv, 6), a3 = S(sv, 7);
+        double* __restrict__ UO = b.uout + wo;
+        {
+            const double t0 = x0 - zn, t1 = x1 - zn, t2 = x2 - zn, t3 = x3 - zn;
+            const double d0 = r0 * dz, d1 = r1 * dz, d2 = r2 * dz, d3 = r3 * dz;
+            pp += t0 * t0; dd += d0 * d0;
+            pp += t1 * t1; dd += d1 * d1;
+            pp += t2 * t2; dd += d2 * d2;
+            pp += t3 * t3; dd += d3 * d3;
+            const double v0 = u0 + t0 * a0, v1 = u1 + t1 * a1;
+            const double v2 = u2 + t2 * a2, v3 = u3 + t3 * a3;
+            UO[0] = v0; UO[D] = v1; UO[2 * D] = v2; UO[3 * D] = v3;
+            bu |= !(finite(v0) && finite(v1) && finite(v2) && finite(v3));
+        }
+        // ---- phases m, z, u of xi_i (degree 2: slack, margin) ----
+        const double ax0 = S(sv, kSAX0), ax1 = S(sv, kSAX1), zwx = S(sv, kSZWX);
+        if (lane == 0) {
+            const double mx0 = xx0 + ux0, mx1 = xx1 + ux1;
+            bm |= !(finite(mx0) && finite(mx1));
+            double rs = 0.0;
+            rs += mx1 * R3;
+            const double zx = ddiv(mx0 * rx0 + rs, zwx);
+            bz |= !finite(zx);
+            b.z[c.zX + i] = zx;
+            const double dzx = zx - zxi;
+            const double t0 = xx0 - zx, t1 = xx1 - zx;
+            const double d0 = rx0 * dzx, d1 = R3 * dzx;
+            pp += t0 * t0; dd += d0 * d0;
+            pp += t1 * t1; dd += d1 * d1;
+            const double v0 = ux0 + t0 * ax0, v1 = ux1 + t1 * ax1;
+            b.uout[c.pX + 2 * (int64_t)i] = v0;
+            b.uout[c.pX + 2 * (int64_t)i + 1] = v1;
+            bu |= !(finite(v0) && finite(v1));
+            xb_out[c.pB + i] = xbv;
+        }
+    }
+    if (bn) flag_error(b.ctrl, it - 1, FG_PHASE_N, true);
+    if (bx) flag_error(b.ctrl, it, FG_PHASE_X, true);
+    if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
+    if (bz) flag_error(b.ctrl, it, FG_PHASE_Z, false);
+    if (bu) flag_error(b.ctrl, it, FG_PHASE_U, false);
+    block_sum2<kChainThreads>(pp, dd, sm);
+    if (threadIdx.x == 0) {
+        b.part[2 * (part_off + blockIdx.x)] = pp;
+        b.part[2 * (part_off + blockIdx.x) + 1] = dd;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Unit-weight form: every edge weight rho and relaxation alpha of the graph
+// is exactly 1.0 and the z weights are the degrees (4 for interior w_i, 2
+// for xi_i) -- checked on the host at every parameter sync.  Then each
+// IEEE operation involving a weight is an exact identity (r * 1.0 == r,
+// r / 1.0 == r, r / 4.0 == r * 0.25, (1*a + 1*b) / 2 == (a + b) * 0.5), so
+// the kernel drops them, reads no rho/alpha/z weights, and stays bitwise
+// equal to the general forms.  The norm factor 1 / (1 + scale_i) is a
+// per-point table built at sync time with the same division.
+enum : int { kUY = 0, kUFN = 1, kULam = 2, kUZX = 3, kUUX0 = 4, kUUX1 = 5, kUZB = 6,
+             kUUB = 7, kUXX = 8 };
+
+template <int D, int MINB>
+__global__ void __launch_bounds__(kChainThreads, MINB) k_svm_chain_unit(PassB b, ChainDev c,
+                                                                    double* xb_out,
+                                                                    int64_t part_off) {
+    static_assert(D == 32, "one lane per component");
+    __shared__ double sm[16];
+    if (b.ctrl->stop) return;
+    const int64_t it = b.ctrl->iter;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int32_t nin = c.n - 2;
+    const int32_t per_cta = (nin + gridDim.x - 1) / gridDim.x;
+    const int32_t i0 = 1 + blockIdx.x * per_cta;
+    const int32_t i1 = min(c.n - 1, i0 + per_cta);
+    const double* sb = c.xx;
+    int32_t ss = 0;
+    switch (lane) {
+        case kUY: sb = c.fp_margin + D; ss = c.st_margin; break;
+        case kUFN: sb = c.fnorm; ss = 1; break;
+        case kULam: sb = c.fp_slack; ss = c.st_slack; break;
+        case kUZX: sb = b.zin + c.zX; ss = 1; break;
+        case kUUX0: sb = b.uin + c.pX; ss = 2; break;
+        case kUUX1: sb = b.uin + c.pX + 1; ss = 2; break;
+        case kUZB: sb = b.zin + c.zB; ss = 0; break;
+        case kUUB: sb = b.uin + c.pB; ss = 1; break;
+        case kUXX: sb = c.xx; ss = 1; break;
+        default: break;
+    }
+    double pp = 0.0, dd = 0.0;
+    bool bn = false, bx = false, bm = false, bz = false, bu = false;
+    auto S = [&](double v, int src) { return __shfl_sync(kFull, v, src); };
+#pragma unroll 1
+    for (int32_t i = i0 + warp; i < i1; i += kChainThreads / 32) {
+        const int64_t wo = c.pW + (int64_t)(4 * i - 1) * D + lane;
+        const double* __restrict__ U = b.uin + wo;
+        const int64_t zo = c.zW + (int64_t)i * D + lane;
+        const double* __restrict__ Z = b.zin + zo;
+        const double u0 = U[0], u1 = U[D], u2 = U[2 * D], u3 = U[3 * D];
+        const double up = U[-D], un_ = U[6 * D];
+        const double zi = Z[0], zp = Z[-D], zn_ = Z[D];
+        const double X = c.fp_margin[(int64_t)i * c.st_margin + lane];
+        const double sv = sb[(int64_t)i * ss];
+        // ---- phase n ----
+        const double n0 = zi - u0, n1 = zi - u1, n2 = zi - u2, n3 = zi - u3;
+        const double np_ = zp - up, nn_ = zn_ - un_;
+        const double zxi = S(sv, kUZX), ux0 = S(sv, kUUX0), ux1 = S(sv, kUUX1);
+        const double nb = S(sv, kUZB) - S(sv, kUUB), nx0 = zxi - ux0, nx1 = zxi - ux1;
+        bn |= !(finite(n0) && finite(n1) && finite(n2) && finite(n3) && finite(np_) &&
+                finite(nn_) && finite(nb) && finite(nx0) && finite(nx1));
+        // ---- phase x ----
+        const double x0 = S(sv, kUFN) * n0;                    // prox_svm_norm
+        const double pr = n1 * X;
+        const int g = lane & 7;
+        double dot = 0.0;
+        dot += S(pr, g);
+        dot += S(pr, g + 8);
+        dot += S(pr, g + 16);
+        dot += S(pr, g + 24);
+        dot += __shfl_xor_sync(kFull, dot, 1);
+        dot += __shfl_xor_sync(kFull, dot, 2);
+        dot += __shfl_xor_sync(kFull, dot, 4);
+        const double Y = S(sv, kUY);
+        const double slack = (1.0 - nx1) - Y * (dot + nb);
+        const double denom = (S(sv, kUXX) + 1.0) + 1.0;
+        const double mu = ddiv(np_max0(slack), denom);
+        const double x1 = n1 + (mu * Y) * X;
+        const double xbv = nb + mu * Y;
+        const double xx1 = nx1 + mu;
+        const double xx0 = np_max0(nx0 - S(sv, kULam));       // prox_svm_slack
+        const double x2 = (np_ + n2) * 0.5;                    // prox_equality
+        const double x3 = (n3 + nn_) * 0.5;
+        // ---- phases m, z, u of w_i: z weight 4 ----
+        const double m0 = x0 + u0, m1 = x1 + u1, m2 = x2 + u2, m3 = x3 + u3;
+        double res = 0.0;
+        res += m1;
+        res += m2;
+        res += m3;
+        const double zn = (m0 + res) * 0.25;
+        b.z[zo] = zn;
+        const double dz = zn - zi;
+        const double t0 = x0 - zn, t1 = x1 - zn, t2 = x2 - zn, t3 = x3 - zn;
+        const double v0 = u0 + t0, v1 = u1 + t1, v2 = u2 + t2, v3 = u3 + t3;
+        double* __restrict__ UO = b.uout + wo;
+        UO[0] = v0; UO[D] = v1; UO[2 * D] = v2; UO[3 * D] = v3;
+        pp += t0 * t0; pp += t1 * t1; pp += t2 * t2; pp += t3 * t3;
+        const double dz2 = dz * dz;
+        dd += dz2; dd += dz2; dd += dz2; dd += dz2;
+        // x non-finite => m non-finite (u is finite: it passed last
+        // iteration's check), so x is only inspected when m is bad
+        const bool mbad = !(finite(m0) && finite(m1) && finite(m2) && finite(m3));
+        if (mbad) bx |= !(finite(x0) && finite(x1) && finite(x2) && finite(x3));
+        bm |= mbad;
+        bz |= !finite(zn);
+        bu |= !(finite(v0) && finite(v1) && finite(v2) && finite(v3));
+        // ---- xi_i (slack, margin; z weight 2) and b's margin x ----
+        if (lane == 0) {
+            const double mx0 = xx0 + ux0, mx1 = xx1 + ux1;
+            double rs = 0.0;
+            rs += mx1;
+            const double zx = (mx0 + rs) * 0.5;
+            b.z[c.zX + i] = zx;
+            const double dzx = zx - zxi;
+            const double s0 = xx0 - zx, s1 = xx1 - zx;
+            const double w0 = ux0 + s0, w1 = ux1 + s1;
+            b.uout[c.pX + 2 * (int64_t)i] = w0;
+            b.uout[c.pX + 2 * (int64_t)i + 1] = w1;
+            xb_out[c.pB + i] = xbv;
+            pp += s0 * s0; pp += s1 * s1;
+            dd += dzx * dzx; dd += dzx * dzx;
+            bx |= !(finite(xbv) && finite(xx0) && finite(xx1));
+            bm |= !(finite(mx0) && finite(mx1));
+            bz |= !finite(zx);
+            bu |= !(finite(w0) && finite(w1));
+        }
+    }
+    if (bn) flag_error(b.ctrl, it - 1, FG_PHASE_N, true);
+    if (bx) flag_error(b.ctrl, it, FG_PHASE_X, true);
+    if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
+    if (bz) flag_error(b.ctrl, it, FG_PHASE_Z, false);
+    if (bu) flag_error(b.ctrl, it, FG_PHASE_U, false);
+    block_sum2<kChainThreads>(pp, dd, sm);
+    if (threadIdx.x == 0) {
+        b.part[2 * (part_off + blockIdx.x)] = pp;
+        b.part[2 * (part_off + blockIdx.x) + 1] = dd;
+    }
+}
+
+// 1 / (1 + scale_i): prox_svm_norm's factor at unit edge weight
+// (ddiv(R, R + scale) with R = 1.0, the same IEEE division)
+__global__ void k_chain_fnorm(ChainDev c, double* fnorm) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= c.n) return;
+    fnorm[i] = ddiv(1.0, 1.0 + c.fp_norm[i * c.st_norm]);
+}
+
+// x.x of every point's margin data in k_svm_margin's order (8-lane groups,
+// lane l summing components l, l+8, l+16, l+24 from 0.0, then xor 1/2/4).
+__global__ void k_chain_xx(ChainDev c, double* xx) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= c.n) return;
+    const double* P = c.fp_margin + i * c.st_margin;
+    double r[8];
+    for (int g = 0; g < 8; ++g) {
+        double a = 0.0;
+        for (int k = 0; k < 4; ++k) {
+            const int cc = g + 8 * k;
+            const double v = cc < c.D ? P[cc] : 0.0;
+            a += v * v;
+        }
+        r[g] = a;
+    }
+    xx[i] = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
 }
 
 }  // namespace fg

@@ -217,6 +217,11 @@ struct fg_plan {
     ChainDev chain{};
     int64_t chain_grid = 0;
     int chain_minb = 2;                // CTAs/SM the kernel is compiled for (A/B)
+    bool chain_fast = false;           // D == 32: fast form for interior points
+    bool chain_unit = false;           // all weights 1 (checked at every sync)
+    double* d_chain_xx = nullptr;      // per point x.x of the margin data
+    double* d_chain_fnorm = nullptr;   // per point 1/(1+scale) (unit form)
+    int32_t* d_flag = nullptr;         // scratch device flag
     // iteration (of the last run) whose x is not in d_x because the chain
     // kernel keeps it in registers; 0 = d_x is current
     int64_t x_stale = 0;
@@ -247,7 +252,8 @@ fg_plan::~fg_plan() {
                     d_clvars[1], d_clvars[2], d_clvars[3], d_clvars[4], d_clprog[1],
                     d_clprog[2], d_clprog[3], d_clprog[4],
                     d_llist, d_lprog, d_prog, d_glist, d_gchunks, d_gcomps,
-                    d_gwork, d_csum, d_gz, d_part, d_res2, d_ctrl, d_hist,
+                    d_gwork, d_csum, d_gz, d_part, d_res2, d_ctrl, d_hist, d_chain_xx,
+                    d_chain_fnorm, d_flag,
                     d_cutg, d_send, d_recv};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -497,12 +503,23 @@ void part_post(fg_plan* p, cudaStream_t st) {
 void chain_pass(fg_plan* p, int in, cudaStream_t st) {
     PassB b{p->vt(), p->d_x, p->d_u[in], p->d_u[1 - in], nullptr, p->d_zb[1 - in],
             p->d_zb[in], p->d_rho, p->d_alpha, p->d_zw, p->d_ctrl, p->d_part, p->d_zvar};
-    if (p->chain_minb == 3)
-        k_svm_chain<3><<<(unsigned)p->chain_grid, kChainThreads, 0, st>>>(b, p->chain, p->d_x,
-                                                                          p->part_off[0]);
-    else
-        k_svm_chain<2><<<(unsigned)p->chain_grid, kChainThreads, 0, st>>>(b, p->chain, p->d_x,
-                                                                          p->part_off[0]);
+    const unsigned G = (unsigned)p->chain_grid;
+    if (p->chain_fast) {
+        // interior points on the fast (or unit-weight) form, the two end
+        // points (degree 3) on the generic form in the last partial slot
+        if (p->chain_unit && p->chain_minb == 3)
+            k_svm_chain_unit<32, 3><<<G - 1, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
+        else if (p->chain_unit)
+            k_svm_chain_unit<32, 4><<<G - 1, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
+        else
+            k_svm_chain_fast<32><<<G - 1, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
+        k_svm_chain<2><<<1, kChainThreads, 0, st>>>(b, p->chain, p->d_x, G - 1, 0,
+                                                     p->chain.n, p->chain.n - 1);
+    } else if (p->chain_minb == 3) {
+        k_svm_chain<3><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0, 0, p->chain.n, 1);
+    } else {
+        k_svm_chain<2><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0, 0, p->chain.n, 1);
+    }
 }
 
 // ... then the remaining (large / giant) variable classes: the bias
@@ -547,6 +564,11 @@ int get_graph(fg_plan* p, int chunk, cudaGraphExec_t* out) {
     e = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return fail(FG_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    // upload now: the first launch of a fresh executable graph otherwise
+    // pays the upload inside the caller's timed region
+    e = cudaGraphUpload(exec, p->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+    if (e != cudaSuccess) return fail(FG_ERR_CUDA, std::string("graph upload: ") + cudaGetErrorString(e));
     p->graphs[chunk] = exec;
     *out = exec;
     return 0;
@@ -642,7 +664,17 @@ void detect_svm_chain(fg_plan* p, const std::vector<int32_t>& dim,
     c.fp_margin = gm->dev.fp; c.st_margin = gm->dev.fstride;
     // one CTA per partial slot of the small classes it replaces
     p->chain_grid = p->nsblk[0] + p->nsblk[1] + p->nsblk[2];
+    // CTAs/SM the kernels are compiled for (A/B in profiles/): generic form
+    // 2 (3 spills heavily); unit form 4 (0.59 ms vs 0.67 ms at 3, SVM 1M)
     p->chain_minb = getenv("FGADMM_CHAIN_OCC3") ? 3 : 2;
+    if (cudaMalloc((void**)&p->d_chain_xx, n * sizeof(double)) != cudaSuccess) return;
+    c.xx = p->d_chain_xx;
+    k_chain_xx<<<(unsigned)((n + 255) / 256), 256, 0, p->stream>>>(c, p->d_chain_xx);
+    if (cudaMalloc((void**)&p->d_chain_fnorm, n * sizeof(double)) != cudaSuccess) return;
+    c.fnorm = p->d_chain_fnorm;
+    k_chain_fnorm<<<(unsigned)((n + 255) / 256), 256, 0, p->stream>>>(c, p->d_chain_fnorm);
+    if (cudaStreamSynchronize(p->stream) != cudaSuccess) return;
+    p->chain_fast = D == 32 && n >= 3 && p->chain_grid >= 2 && !getenv("FGADMM_CHAIN_GENERIC");
     p->chain_on = p->chain_grid > 0;
 }
 
@@ -980,6 +1012,7 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
         (rc = dalloc(&p->d_stage, std::max(P, Z))) || (rc = dalloc(&p->d_zb[0], Z + kPad)) ||
         (rc = dalloc(&p->d_zb[1], Z + kPad)) ||
         (rc = dalloc(&p->d_zs, Z)) || (rc = dalloc(&p->d_ctrl, 1)) ||
+        (rc = dalloc(&p->d_flag, 1)) ||
         (rc = dalloc(&p->d_res2, 2)))
         return rc;
     CK(cudaMemset(p->d_x, 0, P * sizeof(double)));
@@ -1224,7 +1257,7 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     p->launches_per_iter = count_edge_launches(p.get()) + count_var_launches(p.get()) + 1;
     p->launches_later = p->launches_per_iter;
     if (p->chain_on) {
-        int64_t n = 2;                                   // chain kernel + reduce
+        int64_t n = p->chain_fast ? 3 : 2;               // chain kernel(s) + reduce
         for (int w = 0; w < kVarSlots; ++w) n += chain_rest_slot(w) && var_slot_blocks(p.get(), w) > 0;
         p->launches_later = n;
     }
@@ -1241,6 +1274,7 @@ int fg_plan_info(const fg_plan* p, int64_t* o) {
     o[8] = p->launches_per_iter;
     o[9] = p->launches_later;
     o[10] = p->chain_on ? 1 : 0;
+    o[11] = p->chain_on ? (p->chain_unit ? 3 : (p->chain_fast ? 2 : 1)) : 0;
     return 0;
 }
 
@@ -1253,6 +1287,21 @@ int fg_plan_sync_params(fg_plan* p, const double* rho, const double* alpha,
     CK(cudaMemcpyAsync(p->d_stage, alpha, p->E * sizeof(double), cudaMemcpyHostToDevice, st));
     k_gather_edges<<<nblk(p->E, 256), 256, 0, st>>>(p->E, p->d_refedge, p->d_stage, p->d_alpha);
     CK(cudaMemcpyAsync(p->d_zw, zw, p->Z * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (p->chain_fast) {
+        // unit-weight form of the chain: every rho and alpha exactly 1 and
+        // the z weights equal to the degrees (fg_chain.cuh)
+        bool unit = !getenv("FGADMM_CHAIN_NO_UNIT");
+        for (int64_t e = 0; e < p->E && unit; ++e) unit = rho[e] == 1.0 && alpha[e] == 1.0;
+        const ChainDev& c = p->chain;
+        for (int64_t i = 1; i + 1 < c.n && unit; ++i)
+            for (int k = 0; k < c.D && unit; ++k) unit = zw[c.zW + i * c.D + k] == 4.0;
+        for (int64_t i = 0; i < c.n && unit; ++i) unit = zw[c.zX + i] == 2.0;
+        if (unit != p->chain_unit) {
+            p->chain_unit = unit;
+            for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
+            p->graphs.clear();
+        }
+    }
     CK(cudaStreamSynchronize(st));
     return check_launch();
 }
@@ -1279,9 +1328,20 @@ int fg_state_upload(fg_plan* p, const double* z, const double* u, const double* 
     CK(cudaMemcpyAsync(p->d_zb[0], z, p->Z * sizeof(double), cudaMemcpyHostToDevice, p->stream));
     upload_vm(p, u, p->d_u[0]);
     upload_vm(p, n, p->d_u[1]);   // consumed by the first edge pass
+    int32_t incons = 1;
+    if (p->chain_on) {
+        // n == z[zmap] - u bitwise (every state init_state or a run
+        // produced): the first iteration need not read n, so it can run on
+        // the fused chain too
+        CK(cudaMemsetAsync(p->d_flag, 0, sizeof(int32_t), p->stream));
+        k_n_mismatch<<<std::min<unsigned>(nblk(p->P, 256), 148 * 16), 256, 0, p->stream>>>(
+            p->P, p->d_vmz, p->d_zb[0], p->d_u[0], p->d_u[1], p->d_flag);
+        CK(cudaMemcpyAsync(&incons, p->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                           p->stream));
+    }
     CK(cudaStreamSynchronize(p->stream));
     p->completed = 0;
-    p->n_valid = 1;
+    p->n_valid = incons ? 1 : 0;
     p->x_stale = 0;
     return check_launch();
 }
@@ -1347,7 +1407,7 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
             const bool first = (j == 1) && first_n;
             cudaEvent_t* E4 = &ev[4 * (j - 1)];
             CK(cudaEventRecord(E4[0], st));
-            if (p->chain_on && j > 1) {
+            if (p->chain_on && !first) {
                 chain_pass(p, in, st);
                 CK(cudaEventRecord(E4[1], st));
                 chain_rest(p, in, st);
@@ -1361,7 +1421,7 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
             CK(cudaEventRecord(E4[2], st));
             k_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_hist);
             CK(cudaEventRecord(E4[3], st));
-            launches += j > 1 ? p->launches_later : p->launches_per_iter;
+            launches += (p->chain_on && !first) ? p->launches_later : p->launches_per_iter;
         }
         CK(cudaEventRecord(ev1, st));
         CK(cudaStreamSynchronize(st));
@@ -1385,6 +1445,12 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
             launch_iteration(p, 0, first_n, st);
             CK(cudaEventRecord(e4[1], st));
             CK(cudaEventRecord(e4[2], st));
+        } else if (p->chain_on && !first_n) {
+            chain_pass(p, 0, st);
+            CK(cudaEventRecord(e4[1], st));
+            chain_rest(p, 0, st);
+            CK(cudaEventRecord(e4[2], st));
+            k_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_hist);
         } else {
             edge_pass(p, first_n, p->d_zb[0], p->d_u[0], first_n ? p->d_u[1] : nullptr, st);
             CK(cudaEventRecord(e4[1], st));
@@ -1393,7 +1459,7 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
             k_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_hist);
         }
         CK(cudaEventRecord(e4[3], st));
-        launches += p->launches_per_iter;
+        launches += (p->chain_on && !first_n) ? p->launches_later : p->launches_per_iter;
         int64_t left = K - 1;
         int chunk = std::max(2, cfg->graph_chunk - (cfg->graph_chunk & 1));
         int32_t* h_stop = nullptr;
@@ -1460,7 +1526,7 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
     p->x_stale = 0;
     if (p->chain_on && !p->nccl_comm) {
         const int64_t need = h.err_key != ~0ull ? (int64_t)(h.err_key >> 3) : h.completed;
-        if (need >= 2) p->x_stale = need;
+        if (need >= (first_n ? 2 : 1)) p->x_stale = need;
     }
     out->iterations = h.completed;
     out->converged = h.converged;

@@ -460,6 +460,16 @@ __global__ void k_gather_edges(int64_t E, const int32_t* ref_edge,
 }
 
 // phase m (engine.py:263-265): m = x + u
+// Any payload slot whose uploaded n differs (bitwise) from z[zmap] - u.
+__global__ void k_n_mismatch(int64_t P, const int32_t* vmz, const double* z,
+                             const double* u, const double* n, int32_t* flag) {
+    bool bad = false;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < P;
+         q += (int64_t)gridDim.x * blockDim.x)
+        bad |= __double_as_longlong(z[vmz[q]] - u[q]) != __double_as_longlong(n[q]);
+    if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
 __global__ void k_phase_m(int64_t P, const double* x, const double* u, double* m) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p < P) m[p] = x[p] + u[p];

@@ -173,6 +173,17 @@ __global__ void __launch_bounds__(kLargeThreads, 2) k_var_large_vec(
     const int32_t* units = P + 2;
     const int32_t* lev = units + 2 * nu;
     const int32_t* ops = lev + nlev;
+    // thread 0 prefetches what z needs besides the tree: a[0], z weights and
+    // the previous z (independent loads, issued before the leaf phase)
+    double a0[D], zw0[D], zo0[D];
+    if (threadIdx.x == 0) {
+        vals(0, a0);
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            zw0[c] = b.zw[zb + c];
+            zo0[c] = (MODE == MODE_FUSED) ? b.zin[zb + c] : 0.0;
+        }
+    }
     const int g = threadIdx.x >> 3, j = threadIdx.x & 7;
     constexpr int NG = kLargeThreads / 8;
     for (int r0 = 0; r0 < nu; r0 += NG) {
@@ -220,27 +231,30 @@ __global__ void __launch_bounds__(kLargeThreads, 2) k_var_large_vec(
         }
     }
     __syncthreads();
-    int node = nu, op = 0;
-    for (int l = 0; l < nlev; ++l) {
-        const int cnt = lev[l];
-        for (int o = threadIdx.x; o < cnt * D; o += kLargeThreads) {
-            const int c = o / cnt, oo = o - c * cnt;
-            sv[c][node + oo] = sv[c][ops[2 * (op + oo)]] + sv[c][ops[2 * (op + oo) + 1]];
+    // The top of the tree is small (~2 nodes per leaf): warp 0 evaluates it
+    // level by level with warp barriers, then thread 0 forms z with the
+    // element-0 value and z weights it prefetched above.
+    if (threadIdx.x < 32) {
+        int node = nu, op = 0;
+        for (int l = 0; l < nlev; ++l) {
+            const int cnt = lev[l];
+            for (int o = threadIdx.x; o < cnt * D; o += 32) {
+                const int c = o / cnt, oo = o - c * cnt;
+                sv[c][node + oo] = sv[c][ops[2 * (op + oo)]] + sv[c][ops[2 * (op + oo) + 1]];
+            }
+            __syncwarp();
+            node += cnt;
+            op += cnt;
         }
-        __syncthreads();
-        node += cnt;
-        op += cnt;
-    }
-    if (threadIdx.x == 0) {
-        double a0[D];
-        vals(0, a0);
+        if (threadIdx.x == 0) {
 #pragma unroll
-        for (int c = 0; c < D; ++c) {
-            const double zn = ddiv(a0[c] + sv[c][node - 1], b.zw[zb + c]);
-            s_z[0][c] = zn;
-            s_z[1][c] = (MODE == MODE_FUSED) ? b.zin[zb + c] : 0.0;
-            b.z[zb + c] = zn;
-            if (MODE == MODE_FUSED && !finite(zn)) flag_error(b.ctrl, it, FG_PHASE_Z, false);
+            for (int c = 0; c < D; ++c) {
+                const double zn = ddiv(a0[c] + sv[c][node - 1], zw0[c]);
+                s_z[0][c] = zn;
+                s_z[1][c] = zo0[c];
+                b.z[zb + c] = zn;
+                if (MODE == MODE_FUSED && !finite(zn)) flag_error(b.ctrl, it, FG_PHASE_Z, false);
+            }
         }
     }
     __syncthreads();

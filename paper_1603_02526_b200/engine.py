@@ -239,7 +239,7 @@ class DevicePlan:
         _native.check(lib.fg_plan_create(C.byref(gd), descs, len(self.groups),
                                          self.device, C.byref(handle)))
         self._h = handle
-        info = (C.c_int64 * 11)()
+        info = (C.c_int64 * 12)()
         lib.fg_plan_info(self._h, info)
         self.info = {"V": info[0], "E": info[1], "P": info[2], "Z": info[3],
                      "small_components": info[4], "large_components": info[5],
@@ -342,6 +342,13 @@ class DevicePlan:
                 key = f"{name}#{j}"
             out[key] = (float(ms[i]), int(cnt[i]))
         return out
+
+    def chain_form(self):
+        """Form of the fused SVM-chain kernel the next run uses: 'off',
+        'generic', 'fast' or 'unit' (unit weights; decided at every sync)."""
+        info = (C.c_int64 * 12)()
+        self._lib.fg_plan_info(self._h, info)
+        return ("off", "generic", "fast", "unit")[info[11]]
 
     def debug_buffer(self, which):
         z_slot = which in (_native.BUF_Z0, _native.BUF_Z1)

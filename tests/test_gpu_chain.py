@@ -130,3 +130,39 @@ def test_chain_profile_labels(gpu, monkeypatch):
     prof = plan.profile_kernels(4)
     assert "chain_svm" in prof and prof["chain_svm"][1] == 3
     assert not any(k.startswith("edge_") for k in prof)
+
+
+@pytest.mark.parametrize("rho,alpha", [(2.0, 1.0), (1.0, 1.5), (0.7, 1.3)])
+def test_chain_general_weights_bitwise(gpu, monkeypatch, rho, alpha):
+    """Non-unit weights take the general fast form (weights loaded per
+    edge); it stays bitwise equal to the per-kind path."""
+    X, y = fg.gen_gaussian_arrays(3000, 32, 4.0, seed=12)
+    g = fg.build_svm(fg.SvmSpec.from_arrays(X, y, rho=rho, alpha=alpha))
+    st = fg.init_state(g, seed=6)
+    (sc, _), (sg, _) = run_both(g, st, monkeypatch, [fg.RunConfig(max_iterations=8)])
+    for k in "xmzun":
+        np.testing.assert_array_equal(getattr(sc, k), getattr(sg, k), err_msg=k)
+
+
+def test_chain_unit_form_follows_set_edge_params(gpu, monkeypatch):
+    """A run with unit weights, then one edge re-weighted (the plan leaves the
+    unit-weight form), then restored: every run bitwise equal to the
+    per-kind path on the same sequence of weights."""
+    g = svm_graph(2500, 32, seed=13)
+    st = fg.init_state(g, seed=2)
+    e = int(np.flatnonzero(g.edge_var == g.edge_var[0])[0])
+
+    def seq(chain):
+        plan_for(g, monkeypatch, chain)
+        s = copy(st)
+        g.set_edge_params(e, 1.0, 1.0)
+        fg.run(g, fg.RunConfig(max_iterations=4), state=s)
+        g.set_edge_params(e, 3.0, 0.5)
+        fg.run(g, fg.RunConfig(max_iterations=5), state=s)
+        g.set_edge_params(e, 1.0, 1.0)
+        fg.run(g, fg.RunConfig(max_iterations=3), state=s)
+        return s
+
+    a, b = seq(True), seq(False)
+    for k in "xmzun":
+        np.testing.assert_array_equal(getattr(a, k), getattr(b, k), err_msg=k)
