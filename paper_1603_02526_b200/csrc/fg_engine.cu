@@ -46,7 +46,11 @@ int fail(int code, const std::string& msg) {
 
 constexpr int kSmallDegMax = 32;     // class S threshold (degree)
 constexpr int64_t kChunkMax = 8192;  // pairwise subtree handled by one CTA
-constexpr int64_t kGiantWork = 8192; // elements per G3 CTA
+constexpr int64_t kGiantWork = 2048; // elements per G3 CTA
+// Giant segments are cut into maximal pairwise subtrees of <= kGiantChunk
+// items (one CTA each); smaller than the class-L limit so a degree-1M
+// segment spreads over ~1000 CTAs instead of ~128.
+constexpr int64_t kGiantChunk = 1024;
 // Dynamic shared-memory limit set on every kernel that uses it: the
 // attribute is per function, not per launch, so plans of different sizes
 // must not lower it under one another.
@@ -1052,6 +1056,12 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
         return (int32_t)off;
     };
     const int64_t kChunk = gd->chunk > 0 ? gd->chunk : kChunkMax;
+    // giant subtree size: kGiantChunk, larger for huge segments so the top
+    // of the tree (2 doubles per chunk) fits the top kernel's shared memory
+    int64_t maxdeg = 0;
+    for (int64_t v = 0; v < V; ++v) maxdeg = std::max<int64_t>(maxdeg, deg[v]);
+    int64_t kGChunk = std::min(kChunk, kGiantChunk);
+    while (kGChunk < kChunk && maxdeg / kGChunk > 4096) kGChunk *= 2;
     const int64_t kSmallDeg = gd->small_degree > 0 ? gd->small_degree : kSmallDegMax;
     if (kChunk < kLeafMax || kChunk > kChunkMax || kSmallDeg > kSmallDegMax)
         return fail(FG_ERR_INVALID, "chunk must be in [128, 8192], small_degree in [1, 32]");
@@ -1071,7 +1081,7 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
                 glist.push_back((int32_t)(zbase[v] + c));
                 cutg.push_back(gi);
                 std::vector<std::pair<int64_t, int64_t>> chunks;
-                const int32_t top = (int32_t)emit_program(dg, kChunk, prog, &chunks);
+                const int32_t top = (int32_t)emit_program(dg, kGChunk, prog, &chunks);
                 gcomps.push_back(GComp{top, (int32_t)gchunks.size(), cidx, 0});
                 max_top = std::max(max_top, (int)chunks.size());
                 for (auto& ch : chunks)
@@ -1122,7 +1132,7 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
                 const int32_t gi = (int32_t)glist.size();
                 glist.push_back(k);
                 std::vector<std::pair<int64_t, int64_t>> chunks;
-                const int32_t top = (int32_t)emit_program(dg - 1, kChunk, prog, &chunks);
+                const int32_t top = (int32_t)emit_program(dg - 1, kGChunk, prog, &chunks);
                 gcomps.push_back(GComp{top, (int32_t)gchunks.size(), -1, 0});
                 max_top = std::max(max_top, (int)chunks.size());
                 for (auto& ch : chunks)
