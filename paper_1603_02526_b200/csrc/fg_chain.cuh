@@ -448,6 +448,7 @@ __global__ void __launch_bounds__(kChainThreads, MINB) k_svm_chain_unit(PassB b,
                                                                     int64_t part_off) {
     static_assert(D == 32, "one lane per component");
     __shared__ double sm[16];
+    __shared__ double s_sc[kChainThreads / 32][32];     // per-warp point scalars
     if (b.ctrl->stop) return;
     const int64_t it = b.ctrl->iter;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -472,6 +473,7 @@ __global__ void __launch_bounds__(kChainThreads, MINB) k_svm_chain_unit(PassB b,
     double pp = 0.0, dd = 0.0;
     bool bn = false, bx = false, bm = false, bz = false, bu = false;
     auto S = [&](double v, int src) { return __shfl_sync(kFull, v, src); };
+    double* sc = s_sc[warp];
 #pragma unroll 1
     for (int32_t i = i0 + warp; i < i1; i += kChainThreads / 32) {
         const int64_t wo = c.pW + (int64_t)(4 * i - 1) * D + lane;
@@ -483,15 +485,22 @@ __global__ void __launch_bounds__(kChainThreads, MINB) k_svm_chain_unit(PassB b,
         const double zi = Z[0], zp = Z[-D], zn_ = Z[D];
         const double X = c.fp_margin[(int64_t)i * c.st_margin + lane];
         const double sv = sb[(int64_t)i * ss];
+        __syncwarp();                                  // previous point's reads done
+        sc[lane] = sv;
+        __syncwarp();
         // ---- phase n ----
         const double n0 = zi - u0, n1 = zi - u1, n2 = zi - u2, n3 = zi - u3;
         const double np_ = zp - up, nn_ = zn_ - un_;
-        const double zxi = S(sv, kUZX), ux0 = S(sv, kUUX0), ux1 = S(sv, kUUX1);
-        const double nb = S(sv, kUZB) - S(sv, kUUB), nx0 = zxi - ux0, nx1 = zxi - ux1;
-        bn |= !(finite(n0) && finite(n1) && finite(n2) && finite(n3) && finite(np_) &&
-                finite(nn_) && finite(nb) && finite(nx0) && finite(nx1));
+        const double zxi = sc[kUZX], ux0 = sc[kUUX0], ux1 = sc[kUUX1];
+        const double nb = sc[kUZB] - sc[kUUB], nx0 = zxi - ux0, nx1 = zxi - ux1;
+        // a finite sum proves every term finite (NaN and inf propagate);
+        // only a non-finite sum pays for the per-value check
+        const double sn = ((n0 + n1) + (n2 + n3)) + ((np_ + nn_) + ((nb + nx0) + nx1));
+        if (!finite(sn))
+            bn |= !(finite(n0) && finite(n1) && finite(n2) && finite(n3) && finite(np_) &&
+                    finite(nn_) && finite(nb) && finite(nx0) && finite(nx1));
         // ---- phase x ----
-        const double x0 = S(sv, kUFN) * n0;                    // prox_svm_norm
+        const double x0 = sc[kUFN] * n0;                    // prox_svm_norm
         const double pr = n1 * X;
         const int g = lane & 7;
         double dot = 0.0;
@@ -502,14 +511,14 @@ __global__ void __launch_bounds__(kChainThreads, MINB) k_svm_chain_unit(PassB b,
         dot += __shfl_xor_sync(kFull, dot, 1);
         dot += __shfl_xor_sync(kFull, dot, 2);
         dot += __shfl_xor_sync(kFull, dot, 4);
-        const double Y = S(sv, kUY);
+        const double Y = sc[kUY];
         const double slack = (1.0 - nx1) - Y * (dot + nb);
-        const double denom = (S(sv, kUXX) + 1.0) + 1.0;
+        const double denom = (sc[kUXX] + 1.0) + 1.0;
         const double mu = ddiv(np_max0(slack), denom);
         const double x1 = n1 + (mu * Y) * X;
         const double xbv = nb + mu * Y;
         const double xx1 = nx1 + mu;
-        const double xx0 = np_max0(nx0 - S(sv, kULam));       // prox_svm_slack
+        const double xx0 = np_max0(nx0 - sc[kULam]);       // prox_svm_slack
         const double x2 = (np_ + n2) * 0.5;                    // prox_equality
         const double x3 = (n3 + nn_) * 0.5;
         // ---- phases m, z, u of w_i: z weight 4 ----
@@ -530,11 +539,14 @@ __global__ void __launch_bounds__(kChainThreads, MINB) k_svm_chain_unit(PassB b,
         dd += dz2; dd += dz2; dd += dz2; dd += dz2;
         // x non-finite => m non-finite (u is finite: it passed last
         // iteration's check), so x is only inspected when m is bad
-        const bool mbad = !(finite(m0) && finite(m1) && finite(m2) && finite(m3));
-        if (mbad) bx |= !(finite(x0) && finite(x1) && finite(x2) && finite(x3));
-        bm |= mbad;
+        if (!finite((m0 + m1) + (m2 + m3))) {
+            const bool mbad = !(finite(m0) && finite(m1) && finite(m2) && finite(m3));
+            if (mbad) bx |= !(finite(x0) && finite(x1) && finite(x2) && finite(x3));
+            bm |= mbad;
+        }
         bz |= !finite(zn);
-        bu |= !(finite(v0) && finite(v1) && finite(v2) && finite(v3));
+        if (!finite((v0 + v1) + (v2 + v3)))
+            bu |= !(finite(v0) && finite(v1) && finite(v2) && finite(v3));
         // ---- xi_i (slack, margin; z weight 2) and b's margin x ----
         if (lane == 0) {
             const double mx0 = xx0 + ux0, mx1 = xx1 + ux1;

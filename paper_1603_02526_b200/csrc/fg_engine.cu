@@ -504,26 +504,45 @@ void part_post(fg_plan* p, cudaStream_t st) {
 }
 
 // fused SVM chain: one kernel for the edge pass and the w/xi variables ...
+// CTAs of the chain kernel for interior points: one resident wave (the
+// kernels loop over their points), at most the partial slots it replaces
+// minus the end-point slot.
+int64_t chain_main_grid(const fg_plan* p) {
+    const int64_t wave = p->chain_fast ? (p->chain_unit ? 148 * 4 : 148 * 2) : 148 * 2;
+    return std::max<int64_t>(1, std::min(wave, p->chain_grid - 1));
+}
+
 void chain_pass(fg_plan* p, int in, cudaStream_t st) {
     PassB b{p->vt(), p->d_x, p->d_u[in], p->d_u[1 - in], nullptr, p->d_zb[1 - in],
             p->d_zb[in], p->d_rho, p->d_alpha, p->d_zw, p->d_ctrl, p->d_part, p->d_zvar};
-    const unsigned G = (unsigned)p->chain_grid;
+    const unsigned G = (unsigned)chain_main_grid(p);
     if (p->chain_fast) {
         // interior points on the fast (or unit-weight) form, the two end
-        // points (degree 3) on the generic form in the last partial slot
+        // points (degree 3) on the generic form in the next partial slot
         if (p->chain_unit && p->chain_minb == 3)
-            k_svm_chain_unit<32, 3><<<G - 1, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
+            k_svm_chain_unit<32, 3><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
         else if (p->chain_unit)
-            k_svm_chain_unit<32, 4><<<G - 1, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
+            k_svm_chain_unit<32, 4><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
         else
-            k_svm_chain_fast<32><<<G - 1, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
-        k_svm_chain<2><<<1, kChainThreads, 0, st>>>(b, p->chain, p->d_x, G - 1, 0,
+            k_svm_chain_fast<32><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
+        k_svm_chain<2><<<1, kChainThreads, 0, st>>>(b, p->chain, p->d_x, G, 0,
                                                      p->chain.n, p->chain.n - 1);
     } else if (p->chain_minb == 3) {
-        k_svm_chain<3><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0, 0, p->chain.n, 1);
+        k_svm_chain<3><<<G + 1, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0, 0, p->chain.n, 1);
     } else {
-        k_svm_chain<2><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0, 0, p->chain.n, 1);
+        k_svm_chain<2><<<G + 1, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0, 0, p->chain.n, 1);
     }
+}
+
+// residual reduction of one iteration: a chain iteration leaves the small
+// classes' partial slots beyond its own grid unwritten
+void launch_reduce(fg_plan* p, bool chain_iter, cudaStream_t st) {
+    int64_t lo = 0, hi = 0;
+    if (chain_iter) {
+        lo = chain_main_grid(p) + 1;
+        hi = p->chain_grid;
+    }
+    k_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_hist, lo, hi);
 }
 
 // ... then the remaining (large / giant) variable classes: the bias
@@ -544,7 +563,8 @@ void launch_iteration(fg_plan* p, int in, bool first, cudaStream_t st) {
         part_post(p, st);
         return;
     }
-    if (p->chain_on && !first) {
+    const bool chain = p->chain_on && !first;
+    if (chain) {
         chain_pass(p, in, st);
         chain_rest(p, in, st);
     } else {
@@ -552,7 +572,7 @@ void launch_iteration(fg_plan* p, int in, bool first, cudaStream_t st) {
         var_pass<MODE_FUSED>(p, p->d_zb[in], p->d_zb[1 - in], p->d_u[in], p->d_u[1 - in],
                              nullptr, st);
     }
-    k_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_hist);
+    launch_reduce(p, chain, st);
 }
 
 int get_graph(fg_plan* p, int chunk, cudaGraphExec_t* out) {
@@ -1429,7 +1449,7 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
                                      p->d_u[1 - in], nullptr, st);
             }
             CK(cudaEventRecord(E4[2], st));
-            k_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_hist);
+            launch_reduce(p, p->chain_on && !first, st);
             CK(cudaEventRecord(E4[3], st));
             launches += (p->chain_on && !first) ? p->launches_later : p->launches_per_iter;
         }
@@ -1460,13 +1480,13 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
             CK(cudaEventRecord(e4[1], st));
             chain_rest(p, 0, st);
             CK(cudaEventRecord(e4[2], st));
-            k_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_hist);
+            launch_reduce(p, true, st);
         } else {
             edge_pass(p, first_n, p->d_zb[0], p->d_u[0], first_n ? p->d_u[1] : nullptr, st);
             CK(cudaEventRecord(e4[1], st));
             var_pass<MODE_FUSED>(p, p->d_zb[0], p->d_zb[1], p->d_u[0], p->d_u[1], nullptr, st);
             CK(cudaEventRecord(e4[2], st));
-            k_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_hist);
+            launch_reduce(p, false, st);
         }
         CK(cudaEventRecord(e4[3], st));
         launches += (p->chain_on && !first_n) ? p->launches_later : p->launches_per_iter;
@@ -1787,7 +1807,7 @@ int fg_profile_kernels(fg_plan* p, int64_t iterations, int32_t max_slots,
                                    p->d_u[1 - in], nullptr, st);
             CK(cudaEventRecord(E[++slot], st));
         }
-        k_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_hist);
+        launch_reduce(p, chain, st);
         CK(cudaEventRecord(E[++slot], st));
     }
     CK(cudaStreamSynchronize(st));

@@ -319,8 +319,11 @@ __global__ void __launch_bounds__(kVarThreads) k_var_giant_update(
 }
 
 // Residuals, tolerance stop and iteration bookkeeping (engine.py:502-516).
+// Partial slots [skip_lo, skip_hi) are not written by this iteration's
+// kernels (the fused chain uses fewer slots than the classes it replaces).
 __global__ void __launch_bounds__(1024) k_reduce(Ctrl* c, const double* part,
-                                                 int64_t npart, double* hist) {
+                                                 int64_t npart, double* hist,
+                                                 int64_t skip_lo = 0, int64_t skip_hi = 0) {
     __shared__ double sm[64];
     __shared__ int s_stop;
     if (threadIdx.x == 0) s_stop = c->stop;
@@ -328,6 +331,7 @@ __global__ void __launch_bounds__(1024) k_reduce(Ctrl* c, const double* part,
     if (s_stop) return;
     double a = 0.0, bsum = 0.0;
     for (int64_t i = threadIdx.x; i < npart; i += 1024) {
+        if (i >= skip_lo && i < skip_hi) continue;
         a += part[2 * i];
         bsum += part[2 * i + 1];
     }
