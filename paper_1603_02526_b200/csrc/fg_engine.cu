@@ -150,6 +150,8 @@ struct GroupHost {
 struct fg_plan {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t stream2 = nullptr;     // forked branch (chain end points)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t V = 0, E = 0, P = 0, Z = 0;
     // var tables
     int32_t *d_dim = nullptr, *d_deg = nullptr, *d_ebase = nullptr;
@@ -234,6 +236,12 @@ struct fg_plan {
     int first_done = 0;
     // graphs: key = chunk iterations
     std::map<int, cudaGraphExec_t> graphs;
+    // fused giant kernels: the chunk kernel's last CTA per component runs the
+    // top of the tree; in chain iterations the update's last CTA reduces
+    bool giant_fused = true;
+    unsigned* d_gcnt = nullptr;        // per giant component chunk counter
+    unsigned* d_ucnt = nullptr;        // giant update CTA counter
+    FusedReduce fr_next{nullptr, 0, 0, 0, nullptr};   // set by chain_rest
     int64_t launches_per_iter = 0;     // iteration 1 of a run
     int64_t launches_later = 0;        // iterations 2.. (fused chain when on)
 
@@ -257,12 +265,15 @@ fg_plan::~fg_plan() {
                     d_clprog[2], d_clprog[3], d_clprog[4],
                     d_llist, d_lprog, d_prog, d_glist, d_gchunks, d_gcomps,
                     d_gwork, d_csum, d_gz, d_part, d_res2, d_ctrl, d_hist, d_chain_xx,
-                    d_chain_fnorm, d_flag,
+                    d_chain_fnorm, d_flag, d_gcnt, d_ucnt,
                     d_cutg, d_send, d_recv};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& g : groups)
         for (void* p : g.allocs) cudaFree(p);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (stream2) cudaStreamDestroy(stream2);
     if (stream) cudaStreamDestroy(stream);
 }
 
@@ -353,7 +364,7 @@ int64_t var_slot_blocks(const fg_plan* p, int w) {
         case 3: case 4: case 5: case 6: return p->nlv[w - 2];
         case 7: return p->nL;
         case 8: return p->nG ? p->nGC : 0;
-        case 9: return p->nG;
+        case 9: return p->giant_fused ? 0 : p->nG;
         case 10: return p->nG ? p->nGW : 0;
         case 11: case 12: case 13: case 14: return p->ncl[w - 10] * kCluster;
     }
@@ -402,8 +413,13 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
             k_var_large<MODE><<<grid, kVarThreads, 0, st>>>(b, p->d_llist, p->d_lprog, p->d_prog, po);
             return true;
         case kSlotGiantChunks:
-            k_var_giant_chunks<MODE><<<grid, kVarThreads, 0, st>>>(
-                b, p->d_glist, p->d_gchunks, p->d_prog, p->d_csum);
+            if (p->giant_fused)
+                k_var_giant_chunks<MODE><<<grid, kVarThreads, p->gtop_smem, st>>>(
+                    b, p->d_glist, p->d_gchunks, p->d_prog, p->d_csum, p->d_gcomps, p->d_gz,
+                    p->d_send, p->d_gcnt);
+            else
+                k_var_giant_chunks<MODE><<<grid, kVarThreads, 0, st>>>(
+                    b, p->d_glist, p->d_gchunks, p->d_prog, p->d_csum);
             return true;
         case kSlotGiantTop:
             k_var_giant_top<MODE><<<grid, kVarThreads, p->gtop_smem, st>>>(
@@ -421,7 +437,7 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
         case kSlotGiantUpdate:
             if (MODE != MODE_FUSED) return false;
             k_var_giant_update<<<grid, kVarThreads, 0, st>>>(b, p->d_glist, p->d_gwork,
-                                                             p->d_gz, po);
+                                                             p->d_gz, po, p->fr_next);
             return true;
     }
     return false;
@@ -517,6 +533,7 @@ void chain_pass(fg_plan* p, int in, cudaStream_t st) {
             p->d_zb[in], p->d_rho, p->d_alpha, p->d_zw, p->d_ctrl, p->d_part, p->d_zvar};
     const unsigned G = (unsigned)chain_main_grid(p);
     if (p->chain_fast) {
+        cudaEventRecord(p->ev_fork, st);
         // interior points on the fast (or unit-weight) form, the two end
         // points (degree 3) on the generic form in the next partial slot
         if (p->chain_unit && p->chain_minb == 3)
@@ -525,8 +542,13 @@ void chain_pass(fg_plan* p, int in, cudaStream_t st) {
             k_svm_chain_unit<32, 4><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
         else
             k_svm_chain_fast<32><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
-        k_svm_chain<2><<<1, kChainThreads, 0, st>>>(b, p->chain, p->d_x, G, 0,
-                                                     p->chain.n, p->chain.n - 1);
+        // the two end points run on a forked stream, concurrently with the
+        // interior (a parallel branch when captured into a CUDA graph)
+        cudaStreamWaitEvent(p->stream2, p->ev_fork, 0);
+        k_svm_chain<2><<<1, kChainThreads, 0, p->stream2>>>(b, p->chain, p->d_x, G, 0,
+                                                              p->chain.n, p->chain.n - 1);
+        cudaEventRecord(p->ev_join, p->stream2);
+        cudaStreamWaitEvent(st, p->ev_join, 0);
     } else if (p->chain_minb == 3) {
         k_svm_chain<3><<<G + 1, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0, 0, p->chain.n, 1);
     } else {
@@ -547,11 +569,22 @@ void launch_reduce(fg_plan* p, bool chain_iter, cudaStream_t st) {
 
 // ... then the remaining (large / giant) variable classes: the bias
 bool chain_rest_slot(int w) { return w > 2 && w != kSlotSmallTma; }
-void chain_rest(fg_plan* p, int in, cudaStream_t st) {
+// Returns true when the residual reduction ran fused into the last CTA of
+// the giant u update (the update is then the iteration's last kernel).
+bool chain_rest(fg_plan* p, int in, cudaStream_t st) {
+    int last = -1;
+    for (int w = 0; w < kVarSlots; ++w)
+        if (chain_rest_slot(w) && var_slot_blocks(p, w) > 0) last = w;
+    const bool fuse = last == kSlotGiantUpdate && p->giant_fused;
+    if (fuse)
+        p->fr_next = FusedReduce{p->d_ucnt, p->npart, chain_main_grid(p) + 1, p->chain_grid,
+                                 p->d_hist};
     for (int w = 0; w < kVarSlots; ++w)
         if (chain_rest_slot(w))
             var_kernel<MODE_FUSED>(p, w, p->d_zb[in], p->d_zb[1 - in], p->d_u[in],
                                    p->d_u[1 - in], nullptr, st);
+    p->fr_next = FusedReduce{nullptr, 0, 0, 0, nullptr};
+    return fuse;
 }
 
 void launch_iteration(fg_plan* p, int in, bool first, cudaStream_t st) {
@@ -564,15 +597,16 @@ void launch_iteration(fg_plan* p, int in, bool first, cudaStream_t st) {
         return;
     }
     const bool chain = p->chain_on && !first;
+    bool reduced = false;
     if (chain) {
         chain_pass(p, in, st);
-        chain_rest(p, in, st);
+        reduced = chain_rest(p, in, st);
     } else {
         edge_pass(p, first, p->d_zb[in], p->d_u[in], first ? p->d_u[1 - in] : nullptr, st);
         var_pass<MODE_FUSED>(p, p->d_zb[in], p->d_zb[1 - in], p->d_u[in], p->d_u[1 - in],
                              nullptr, st);
     }
-    launch_reduce(p, chain, st);
+    if (!reduced) launch_reduce(p, chain, st);
 }
 
 int get_graph(fg_plan* p, int chunk, cudaGraphExec_t* out) {
@@ -972,6 +1006,9 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     std::unique_ptr<fg_plan> p(new fg_plan());
     p->device = device;
     CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
     const int64_t V = gd->num_vars, E = gd->num_edges, P = gd->payload, Z = gd->z_dim;
     p->V = V; p->E = E; p->P = P; p->Z = Z;
 
@@ -1223,10 +1260,17 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     }
     for (int d = 1; d <= 4; ++d) p->nlv[d] = (int64_t)lvars[d].size();
     p->gtop_smem = (int)(2 * max_top * sizeof(double));
-    if ((size_t)p->gtop_smem > 48 * 1024) {
+    p->giant_fused = getenv("FGADMM_GIANT_UNFUSED") == nullptr;
+    if ((size_t)p->gtop_smem > 40 * 1024) {
         CK(cudaFuncSetAttribute(k_var_giant_top<MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
         CK(cudaFuncSetAttribute(k_var_giant_top<MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+        CK(cudaFuncSetAttribute(k_var_giant_chunks<MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+        CK(cudaFuncSetAttribute(k_var_giant_chunks<MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
     }
+    if ((rc = dalloc(&p->d_gcnt, std::max<size_t>(1, glist.size()))) || (rc = dalloc(&p->d_ucnt, 1)))
+        return rc;
+    CK(cudaMemset(p->d_gcnt, 0, std::max<size_t>(1, glist.size()) * sizeof(unsigned)));
+    CK(cudaMemset(p->d_ucnt, 0, sizeof(unsigned)));
     if ((rc = upload(&p->d_sruns, sruns)) || (rc = upload(&p->d_sblk[0], sblk[0])) ||
         (rc = upload(&p->d_sblk[1], sblk[1])) || (rc = upload(&p->d_sblk[2], sblk[2])) ||
         (rc = upload(&p->d_llist, llist)) ||
@@ -1287,8 +1331,11 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     p->launches_per_iter = count_edge_launches(p.get()) + count_var_launches(p.get()) + 1;
     p->launches_later = p->launches_per_iter;
     if (p->chain_on) {
-        int64_t n = p->chain_fast ? 3 : 2;               // chain kernel(s) + reduce
-        for (int w = 0; w < kVarSlots; ++w) n += chain_rest_slot(w) && var_slot_blocks(p.get(), w) > 0;
+        int64_t n = p->chain_fast ? 2 : 1;               // chain kernel(s)
+        int last = -1;
+        for (int w = 0; w < kVarSlots; ++w)
+            if (chain_rest_slot(w) && var_slot_blocks(p.get(), w) > 0) { ++n; last = w; }
+        if (!(last == kSlotGiantUpdate && p->giant_fused)) ++n;   // separate reduce
         p->launches_later = n;
     }
     CK(cudaDeviceSynchronize());
@@ -1437,10 +1484,11 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
             const bool first = (j == 1) && first_n;
             cudaEvent_t* E4 = &ev[4 * (j - 1)];
             CK(cudaEventRecord(E4[0], st));
+            bool reduced = false;
             if (p->chain_on && !first) {
                 chain_pass(p, in, st);
                 CK(cudaEventRecord(E4[1], st));
-                chain_rest(p, in, st);
+                reduced = chain_rest(p, in, st);
             } else {
                 edge_pass(p, first, p->d_zb[in], p->d_u[in], first ? p->d_u[1 - in] : nullptr,
                           st);
@@ -1449,7 +1497,7 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
                                      p->d_u[1 - in], nullptr, st);
             }
             CK(cudaEventRecord(E4[2], st));
-            launch_reduce(p, p->chain_on && !first, st);
+            if (!reduced) launch_reduce(p, p->chain_on && !first, st);
             CK(cudaEventRecord(E4[3], st));
             launches += (p->chain_on && !first) ? p->launches_later : p->launches_per_iter;
         }
@@ -1478,9 +1526,9 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
         } else if (p->chain_on && !first_n) {
             chain_pass(p, 0, st);
             CK(cudaEventRecord(e4[1], st));
-            chain_rest(p, 0, st);
+            const bool reduced = chain_rest(p, 0, st);
             CK(cudaEventRecord(e4[2], st));
-            launch_reduce(p, true, st);
+            if (!reduced) launch_reduce(p, true, st);
         } else {
             edge_pass(p, first_n, p->d_zb[0], p->d_u[0], first_n ? p->d_u[1] : nullptr, st);
             CK(cudaEventRecord(e4[1], st));

@@ -221,10 +221,24 @@ __global__ void __launch_bounds__(kVarThreads) k_var_large(
 // Class G (degree > chunk+1), three kernels.
 // G1: one CTA per chunk (a maximal pairwise subtree of <= chunk items).
 struct GChunk { int32_t gi, start, progoff, pad; };
+// G2 descriptor: top program offset, first chunk, cut slot (or -1)
+struct GComp { int32_t topoff, cbase, pad0, pad1; };
+__device__ __forceinline__ int32_t comps_topoff(const GComp* c, int gi) { return c[gi].topoff; }
+template <int MODE>
+__device__ void giant_top_body(const PassB& b, const int32_t* glist, const GComp* comps,
+                               const int32_t* prog, const double* csum, double* gz,
+                               double* send, int gi, double* sv, int64_t it);
+// With `comps` non-null the last CTA to finish a component's chunks (an
+// atomic counter per component, reset by that CTA) also evaluates the top
+// of its tree: the separate top launch disappears.  The top program is the
+// same whichever CTA runs it, so the result is deterministic.
 template <int MODE>
 __global__ void __launch_bounds__(kVarThreads) k_var_giant_chunks(
     PassB b, const int32_t* glist, const GChunk* chunks, const int32_t* prog,
-    double* csum) {
+    double* csum, const GComp* comps = nullptr, double* gz = nullptr, double* send = nullptr,
+    unsigned* counters = nullptr) {
+    extern __shared__ double sv_top[];
+    __shared__ int s_last;
     __shared__ double sv[2 * kMaxUnits];
     __shared__ int s_stop;
     if (threadIdx.x == 0) s_stop = b.ctrl->stop;
@@ -240,30 +254,38 @@ __global__ void __launch_bounds__(kVarThreads) k_var_giant_chunks(
     const double T = run_units_and_tree(val, (int64_t)ch.pad + ch.start, prog + ch.progoff, sv);
     if (threadIdx.x == 0) csum[blockIdx.x] = T;
     if (MODE == MODE_FUSED && bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
+    if (comps) {
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const int nu = prog[comps_topoff(comps, ch.gi)];
+            s_last = atomicAdd(counters + ch.gi, 1u) == (unsigned)(nu - 1);
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            giant_top_body<MODE>(b, glist, comps, prog, csum, gz, send, ch.gi, sv_top, it);
+            if (threadIdx.x == 0) counters[ch.gi] = 0u;
+        }
+    }
 }
 
 // G2: one CTA per giant component: combine chunk sums along the top of the
 // tree (program whose units are chunks), then z.  A cut component (pad0 =
 // its position in the exchange vector) instead stores its local partial
 // sum in `send`; z follows after the exchange (k_cut_finalize).
-struct GComp { int32_t topoff, cbase, pad0, pad1; };
+// Top of giant component gi's tree from its chunk sums -> z (or the cut
+// partial); one CTA, `sv` holds 2 doubles per chunk.
 template <int MODE>
-__global__ void __launch_bounds__(kVarThreads) k_var_giant_top(
-    PassB b, const int32_t* glist, const GComp* comps, const int32_t* prog,
-    const double* csum, double* gz, double* send) {
-    extern __shared__ double sv[];
-    __shared__ int s_stop;
-    if (threadIdx.x == 0) s_stop = b.ctrl->stop;
-    __syncthreads();
-    if (s_stop) return;
-    const int64_t it = b.ctrl->iter;
-    const GComp gc = comps[blockIdx.x];
-    const int32_t k = glist[blockIdx.x];
+__device__ void giant_top_body(const PassB& b, const int32_t* glist, const GComp* comps,
+                               const int32_t* prog, const double* csum, double* gz,
+                               double* send, int gi, double* sv, int64_t it) {
+    const GComp gc = comps[gi];
+    const int32_t k = glist[gi];
     const int32_t* P = prog + gc.topoff;
     const int nu = P[0], nlev = P[1];
     const int32_t* lev = P + 2 + 2 * nu;
     const int32_t* ops = lev + nlev;
-    for (int u = threadIdx.x; u < nu; u += kVarThreads) sv[u] = csum[gc.cbase + u];
+    for (int u = threadIdx.x; u < nu; u += kVarThreads) sv[u] = __ldcg(csum + gc.cbase + u);
     __syncthreads();
     int node = nu, op = 0;
     for (int l = 0; l < nlev; ++l) {
@@ -283,8 +305,8 @@ __global__ void __launch_bounds__(kVarThreads) k_var_giant_top(
         bool bm = false;
         ValFn<MODE> val(b, r, &bm);
         const double zn = ddiv(val(0) + sv[node - 1], b.zw[k]);
-        gz[2 * blockIdx.x] = zn;
-        gz[2 * blockIdx.x + 1] = (MODE == MODE_FUSED) ? b.zin[k] : 0.0;
+        gz[2 * gi] = zn;
+        gz[2 * gi + 1] = (MODE == MODE_FUSED) ? b.zin[k] : 0.0;
         b.z[k] = zn;
         if (MODE == MODE_FUSED) {
             if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
@@ -293,49 +315,31 @@ __global__ void __launch_bounds__(kVarThreads) k_var_giant_top(
     }
 }
 
-// G3: u update of giant components, one CTA per element range.
-struct GWork { int32_t gi, e0, e1, pad; };
-__global__ void __launch_bounds__(kVarThreads) k_var_giant_update(
-    PassB b, const int32_t* glist, const GWork* work, const double* gz,
-    int64_t part_off) {
-    __shared__ double sm[16];
+template <int MODE>
+__global__ void __launch_bounds__(kVarThreads) k_var_giant_top(
+    PassB b, const int32_t* glist, const GComp* comps, const int32_t* prog,
+    const double* csum, double* gz, double* send) {
+    extern __shared__ double sv[];
     __shared__ int s_stop;
     if (threadIdx.x == 0) s_stop = b.ctrl->stop;
     __syncthreads();
     if (s_stop) return;
-    const int64_t it = b.ctrl->iter;
-    const GWork wk = work[blockIdx.x];
-    const CompRef r = comp_ref(b, glist[wk.gi]);
-    double pp = 0.0, dd = 0.0;
-    bool bu = false;
-    update_range(b, r, wk.e0 + threadIdx.x, wk.e1, kVarThreads, gz[2 * wk.gi],
-                 gz[2 * wk.gi + 1], pp, dd, bu);
-    if (bu) flag_error(b.ctrl, it, FG_PHASE_U, false);
-    block_sum2<kVarThreads>(pp, dd, sm);
-    if (threadIdx.x == 0) {
-        b.part[2 * (part_off + blockIdx.x)] = pp;
-        b.part[2 * (part_off + blockIdx.x) + 1] = dd;
-    }
+    giant_top_body<MODE>(b, glist, comps, prog, csum, gz, send, blockIdx.x, sv, b.ctrl->iter);
 }
 
-// Residuals, tolerance stop and iteration bookkeeping (engine.py:502-516).
-// Partial slots [skip_lo, skip_hi) are not written by this iteration's
-// kernels (the fused chain uses fewer slots than the classes it replaces).
-__global__ void __launch_bounds__(1024) k_reduce(Ctrl* c, const double* part,
-                                                 int64_t npart, double* hist,
-                                                 int64_t skip_lo = 0, int64_t skip_hi = 0) {
-    __shared__ double sm[64];
-    __shared__ int s_stop;
-    if (threadIdx.x == 0) s_stop = c->stop;
-    __syncthreads();
-    if (s_stop) return;
+// Residuals, tolerance stop and iteration bookkeeping (engine.py:502-516)
+// over partial slots [0, npart) minus [skip_lo, skip_hi), by one CTA of NT
+// threads.
+template <int NT>
+__device__ void reduce_body(Ctrl* c, const double* part, int64_t npart, double* hist,
+                            int64_t skip_lo, int64_t skip_hi, double* sm) {
     double a = 0.0, bsum = 0.0;
-    for (int64_t i = threadIdx.x; i < npart; i += 1024) {
+    for (int64_t i = threadIdx.x; i < npart; i += NT) {
         if (i >= skip_lo && i < skip_hi) continue;
-        a += part[2 * i];
-        bsum += part[2 * i + 1];
+        a += __ldcg(part + 2 * i);
+        bsum += __ldcg(part + 2 * i + 1);
     }
-    block_sum2<1024>(a, bsum, sm);
+    block_sum2<NT>(a, bsum, sm);
     if (threadIdx.x == 0) {
         const int64_t it = c->iter;
         const double primal = sqrt(a) * c->scale;
@@ -355,6 +359,66 @@ __global__ void __launch_bounds__(1024) k_reduce(Ctrl* c, const double* part,
         }
         c->iter = it + 1;
     }
+}
+
+// Optional fused reduction: the last CTA of the update runs reduce_body
+// (when the update is the iteration's last variable kernel).
+struct FusedReduce {
+    unsigned* counter;             // null: no fused reduction
+    int64_t npart, skip_lo, skip_hi;
+    double* hist;
+};
+
+// G3: u update of giant components, one CTA per element range.
+struct GWork { int32_t gi, e0, e1, pad; };
+__global__ void __launch_bounds__(kVarThreads) k_var_giant_update(
+    PassB b, const int32_t* glist, const GWork* work, const double* gz,
+    int64_t part_off, FusedReduce fr = FusedReduce{nullptr, 0, 0, 0, nullptr}) {
+    __shared__ double sm[16];
+    __shared__ int s_last;
+    __shared__ int s_stop;
+    if (threadIdx.x == 0) s_stop = b.ctrl->stop;
+    __syncthreads();
+    if (s_stop) return;
+    const int64_t it = b.ctrl->iter;
+    const GWork wk = work[blockIdx.x];
+    const CompRef r = comp_ref(b, glist[wk.gi]);
+    double pp = 0.0, dd = 0.0;
+    bool bu = false;
+    update_range(b, r, wk.e0 + threadIdx.x, wk.e1, kVarThreads, gz[2 * wk.gi],
+                 gz[2 * wk.gi + 1], pp, dd, bu);
+    if (bu) flag_error(b.ctrl, it, FG_PHASE_U, false);
+    block_sum2<kVarThreads>(pp, dd, sm);
+    if (threadIdx.x == 0) {
+        b.part[2 * (part_off + blockIdx.x)] = pp;
+        b.part[2 * (part_off + blockIdx.x) + 1] = dd;
+    }
+    if (fr.counter) {
+        if (threadIdx.x == 0) {
+            __threadfence();
+            s_last = atomicAdd(fr.counter, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            reduce_body<kVarThreads>(b.ctrl, b.part, fr.npart, fr.hist, fr.skip_lo, fr.skip_hi, sm);
+            if (threadIdx.x == 0) *fr.counter = 0u;
+        }
+    }
+}
+
+// Residuals, tolerance stop and iteration bookkeeping (engine.py:502-516).
+// Partial slots [skip_lo, skip_hi) are not written by this iteration's
+// kernels (the fused chain uses fewer slots than the classes it replaces).
+__global__ void __launch_bounds__(1024) k_reduce(Ctrl* c, const double* part,
+                                                 int64_t npart, double* hist,
+                                                 int64_t skip_lo = 0, int64_t skip_hi = 0) {
+    __shared__ double sm[64];
+    __shared__ int s_stop;
+    if (threadIdx.x == 0) s_stop = c->stop;
+    __syncthreads();
+    if (s_stop) return;
+    reduce_body<1024>(c, part, npart, hist, skip_lo, skip_hi, sm);
 }
 
 // Cut components after the exchange: rank-order sum of the all-gathered

@@ -1,0 +1,9 @@
+#!/bin/bash
+for v in fused unfused; do
+  unset FGADMM_GIANT_UNFUSED
+  [ $v = unfused ] && export FGADMM_GIANT_UNFUSED=1
+  timeout 300 python bench.py --workload svm1m --steps 50 --warmup 5 --no-cpu-baseline > gpurun_out/ab_giant_$v.json 2>gpurun_out/ab_giant_$v.err
+  python -c "
+import json; d=json.load(open('gpurun_out/ab_giant_$v.json'))
+print('$v', round(d['ms_per_step'],4), '%.3e'%d['value'], d['gpu_launches'], {k: round(v['ms_avg'],4) for k,v in d['kernels'].items()})"
+done
