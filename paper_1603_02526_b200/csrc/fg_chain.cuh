@@ -38,6 +38,11 @@ struct ChainDev {
     int32_t n, D;                 // points, weight dimension (<= 32)
     int64_t pW, zW, pX, zX, pB, zB;   // payload / z bases: w block, xi block, b
     int32_t eW, eX, eB, pad;          // edge bases
+    // partitioned plans: w_0 is a cut variable (its x goes to memory for the
+    // cut exchange instead of a local z update), and w_{n-1}'s equality
+    // partner is the next rank's first weight copy, a cut variable whose
+    // single local edge follows w_{n-1}'s segment
+    int32_t w0_cut, has_extra;
     int32_t st_norm, st_slack, st_margin;
     const double* fp_norm;        // per point: scale
     const double* fp_slack;       // per point: lam
@@ -106,7 +111,9 @@ __global__ void __launch_bounds__(kChainThreads, MINB) k_svm_chain(PassB b, Chai
     }
     for (int32_t jj = j0 + warp; jj < j1; jj += kChainThreads / 32) {
         const int32_t i = ilo + jj * istep;
-        const bool hasP = i > 0, hasN = i + 1 < c.n;
+        const bool hasP = i > 0;
+        const bool toExtra = c.has_extra && i == c.n - 1;   // partner: next rank's w
+        const bool hasN = i + 1 < c.n || toExtra;
         const int32_t ow = i ? 4 * i - 1 : 0;        // first element of w_i
         const int64_t pw = c.pW + (int64_t)ow * D, zwi = c.zW + (int64_t)i * D + cl;
         const int deg = 2 + (int)hasP + (int)hasN;
@@ -118,7 +125,7 @@ __global__ void __launch_bounds__(kChainThreads, MINB) k_svm_chain(PassB b, Chai
         for (int k = 0; k < 4; ++k) u[k] = (k < deg) ? b.uin[pw + (int64_t)k * D + cl] : 0.0;
         const double up = hasP ? b.uin[pw - D + cl] : 0.0;                 // w_{i-1}'s eq
         const double zp = hasP ? b.zin[zwi - D] : 0.0;
-        const double un_ = hasN ? b.uin[pw + (int64_t)(deg + 2) * D + cl] : 0.0;  // w_{i+1}'s
+        const double un_ = hasN ? b.uin[pw + (int64_t)(toExtra ? deg : deg + 2) * D + cl] : 0.0;  // w_{i+1}'s
         const double zn_ = hasN ? b.zin[zwi + D] : 0.0;
         const double zwv = b.zw[zwi];                 // z weights (phase z)
         const double zwx = b.zw[c.zX + i];
@@ -133,7 +140,7 @@ __global__ void __launch_bounds__(kChainThreads, MINB) k_svm_chain(PassB b, Chai
         } else if (lane == kSRP) {
             if (hasP) sp = sb + ow - 1; else sv = 1.0;
         } else if (lane == kSRN) {
-            if (hasN) sp = sb + ow + deg + 2; else sv = 1.0;
+            if (hasN) sp = sb + ow + (toExtra ? deg : deg + 2); else sv = 1.0;
         } else if (sb) {
             sp = sb + (int64_t)i * ss;
         }
@@ -200,12 +207,18 @@ __global__ void __launch_bounds__(kChainThreads, MINB) k_svm_chain(PassB b, Chai
             bx |= !f;
         }
         bx |= !(finite(xbv) && finite(xx0) && finite(xx1));
+        if (toExtra && act) xb_out[pw + (int64_t)deg * D + cl] = xe;   // partner's x
         // ---- phases m, z, u of w_i (k_var_small_run<4> arithmetic) ----
         double al[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) al[k] = S(sv, kSA + k);
         const double ax0 = S(sv, kSAX0), ax1 = S(sv, kSAX1);
-        if (act) {
+        if (act && c.w0_cut && i == 0) {
+            // cut w_0: x goes to memory; the cut exchange finishes z and u
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (k < deg) xb_out[pw + (int64_t)k * D + cl] = x[k];
+        } else if (act) {
             double Ssum = 0.0, res = 0.0;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {

@@ -498,20 +498,35 @@ void cut_finalize(fg_plan* p, int in, cudaStream_t st) {
 }
 
 // Everything of a partitioned iteration up to the cut exchange.
+void chain_pass(fg_plan* p, int in, cudaStream_t st);
+bool chain_rest_slot(int w);
+int64_t chain_main_grid(const fg_plan* p);
+
+// A partitioned plan of build_svm's graph runs the fused chain too: its cut
+// weight copies (the rank's first w and the next rank's first w) and the
+// bias go through the cut exchange like any cut variable.
 void part_pre(fg_plan* p, int in, bool first, cudaStream_t st) {
-    edge_pass(p, first, p->d_zb[in], p->d_u[in], first ? p->d_u[1 - in] : nullptr, st);
+    const bool chain = p->chain_on && !first;
+    if (chain) chain_pass(p, in, st);
+    else edge_pass(p, first, p->d_zb[in], p->d_u[in], first ? p->d_u[1 - in] : nullptr, st);
     for (int w = 0; w < kVarSlots; ++w)
-        if (w != kSlotGiantUpdate)
+        if (w != kSlotGiantUpdate && (!chain || chain_rest_slot(w)))
             var_kernel<MODE_FUSED>(p, w, p->d_zb[in], p->d_zb[1 - in], p->d_u[in],
                                    p->d_u[1 - in], nullptr, st);
 }
 
 // After the cut exchange, up to the residual exchange.
-void part_mid(fg_plan* p, int in, cudaStream_t st) {
+void part_mid(fg_plan* p, int in, bool first, cudaStream_t st) {
     cut_finalize(p, in, st);
     var_kernel<MODE_FUSED>(p, kSlotGiantUpdate, p->d_zb[in], p->d_zb[1 - in], p->d_u[in],
                            p->d_u[1 - in], nullptr, st);
-    k_reduce_local<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_send + p->ncut);
+    int64_t lo = 0, hi = 0;
+    if (p->chain_on && !first) {           // chain leaves these slots unwritten
+        lo = chain_main_grid(p) + 1;
+        hi = p->chain_grid;
+    }
+    k_reduce_local<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_send + p->ncut,
+                                       lo, hi);
 }
 
 void part_post(fg_plan* p, cudaStream_t st) {
@@ -591,7 +606,7 @@ void launch_iteration(fg_plan* p, int in, bool first, cudaStream_t st) {
     if (p->nccl_comm) {
         part_pre(p, in, first, st);
         if (p->ncut) exchange_nccl(p, p->d_send, p->d_recv, (size_t)p->ncut, st);
-        part_mid(p, in, st);
+        part_mid(p, in, first, st);
         exchange_nccl(p, p->d_send + p->ncut, p->d_recv + (size_t)p->world * p->ncut, 4, st);
         part_post(p, st);
         return;
@@ -653,9 +668,11 @@ int rebase_slots(fg_plan* p) {
 // exactly the w's and xi's (b has degree > 32).  Anything else keeps the
 // generic per-kind path.
 void detect_svm_chain(fg_plan* p, const std::vector<int32_t>& dim,
-                      const std::vector<int32_t>& deg) {
+                      const std::vector<int32_t>& deg, const std::vector<int64_t>& zbase,
+                      const int32_t* zcut) {
     p->chain_on = false;
-    if (getenv("FGADMM_NO_CHAIN") || p->partitioned() || p->tma_grid > 0) return;
+    if (getenv("FGADMM_NO_CHAIN") || p->tma_grid > 0) return;
+    auto is_cut = [&](int32_t v) { return zcut != nullptr && zcut[zbase[v]] >= 0; };
     const GroupHost *gn = nullptr, *gs = nullptr, *gm = nullptr, *ge = nullptr;
     for (auto& g : p->groups) {
         if (g.dev.count == 0) continue;
@@ -673,7 +690,11 @@ void detect_svm_chain(fg_plan* p, const std::vector<int32_t>& dim,
     if (!gn || !gs || !gm || !ge) return;
     const int64_t n = gn->dev.count;
     const int D = gn->dev.dim[0];
-    if (n < 2 || gs->dev.count != n || gm->dev.count != n || ge->dev.count != n - 1) return;
+    // a rank's part of a partitioned graph also holds the equality to the
+    // next rank's first weight copy (the "extra" cut variable w0 + n)
+    const bool extra = ge->dev.count == n;
+    if (n < 3 || gs->dev.count != n || gm->dev.count != n || (ge->dev.count != n - 1 && !extra))
+        return;
     if (D < 1 || D > 32 || gm->dev.dim[0] != D || gm->dev.dim[1] != 1 || gm->dev.dim[2] != 1 ||
         ge->dev.dim[0] != D || gs->dev.dim[0] != 1)
         return;
@@ -682,9 +703,17 @@ void detect_svm_chain(fg_plan* p, const std::vector<int32_t>& dim,
         return;
     const int32_t w0 = gn->hsv[0][0], xi0 = gs->hsv[0][0], bv = gm->hsv[1][0];
     if (deg[bv] != n || dim[bv] != 1 || n <= 32) return;
+    const bool w0_cut = is_cut(w0);
+    if (extra) {
+        const int32_t we = w0 + (int32_t)n;
+        if (we >= (int32_t)dim.size() || dim[we] != D || deg[we] != 1 || !is_cut(we) ||
+            ge->hsv[1][n - 1] != we || ge->hsk[1][n - 1] != 0)
+            return;
+    }
     for (int64_t i = 0; i < n; ++i) {
         const int32_t w = w0 + (int32_t)i, xi = xi0 + (int32_t)i;
-        const bool hp = i > 0, hn = i + 1 < n;
+        const bool hp = i > 0, hn = i + 1 < n || extra;
+        if ((i > 0 && is_cut(w)) || is_cut(xi)) return;
         if (gn->hsv[0][i] != w || gn->hsk[0][i] != 0) return;
         if (gs->hsv[0][i] != xi || gs->hsk[0][i] != 0) return;
         if (gm->hsv[0][i] != w || gm->hsk[0][i] != 1) return;
@@ -693,10 +722,11 @@ void detect_svm_chain(fg_plan* p, const std::vector<int32_t>& dim,
         if (dim[w] != D || deg[w] != 2 + (int)hp + (int)hn) return;
         if (dim[xi] != 1 || deg[xi] != 2) return;
         if (hn && (ge->hsv[0][i] != w || ge->hsk[0][i] != (hp ? 3 : 2) ||
-                   ge->hsv[1][i] != w + 1 || ge->hsk[1][i] != 2))
+                   ge->hsv[1][i] != w + 1 || (i + 1 < n && ge->hsk[1][i] != 2)))
             return;
     }
-    if (p->nS != (int64_t)(D + 1) * n) return;      // small class == chain vars
+    // small class == the chain's uncut variables
+    if (p->nS != (int64_t)D * (n - (w0_cut ? 1 : 0)) + n) return;
     // affine addresses (fg_chain.cuh): host copies of the var tables
     std::vector<int64_t> pb(p->V), zb(p->V);
     std::vector<int32_t> eb(p->V);
@@ -704,8 +734,14 @@ void detect_svm_chain(fg_plan* p, const std::vector<int32_t>& dim,
         cudaMemcpy(zb.data(), p->d_zbase, p->V * sizeof(int64_t), cudaMemcpyDeviceToHost) ||
         cudaMemcpy(eb.data(), p->d_ebase, p->V * sizeof(int32_t), cudaMemcpyDeviceToHost))
         return;
-    for (int64_t i = 0; i < n; ++i) {
+    for (int64_t i = 0; i < n + (extra ? 1 : 0); ++i) {
         const int64_t ow = i ? 4 * i - 1 : 0;
+        if (i == n) {                               // extra: follows w_{n-1}
+            if (pb[w0 + i] != pb[w0] + ow * D || eb[w0 + i] != eb[w0] + ow ||
+                zb[w0 + i] != zb[w0] + i * D)
+                return;
+            continue;
+        }
         if (pb[w0 + i] != pb[w0] + ow * D || eb[w0 + i] != eb[w0] + ow ||
             zb[w0 + i] != zb[w0] + i * D || pb[xi0 + i] != pb[xi0] + 2 * i ||
             eb[xi0 + i] != eb[xi0] + 2 * i || zb[xi0 + i] != zb[xi0] + i)
@@ -714,6 +750,8 @@ void detect_svm_chain(fg_plan* p, const std::vector<int32_t>& dim,
     ChainDev& c = p->chain;
     c.n = (int32_t)n;
     c.D = D;
+    c.w0_cut = w0_cut ? 1 : 0;
+    c.has_extra = extra ? 1 : 0;
     c.pW = pb[w0]; c.zW = zb[w0]; c.eW = eb[w0];
     c.pX = pb[xi0]; c.zX = zb[xi0]; c.eX = eb[xi0];
     c.pB = pb[bv]; c.zB = zb[bv]; c.eB = eb[bv];
@@ -1311,7 +1349,7 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
         if (e1 != cudaSuccess || e2 != cudaSuccess)
             return fail(FG_ERR_CUDA, "cluster kernel shared-memory attribute");
     }
-    detect_svm_chain(p.get(), dim, deg);
+    detect_svm_chain(p.get(), dim, deg, zbase, gd->z_cut_index);
     for (auto& g : p->groups) {
         g.hsv.clear(); g.hsv.shrink_to_fit();
         g.hsk.clear(); g.hsk.shrink_to_fit();
@@ -1547,6 +1585,7 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
         CK(cudaEventCreateWithFlags(&pe[1], cudaEventDisableTiming));
         int inflight = 0, slot = 0;
         bool stopped = false;
+        const bool poll = cfg->primal_tol > 0.0 || cfg->dual_tol > 0.0;
         while (left > 0 && !stopped) {
             int n;
             cudaGraphExec_t gx = nullptr;
@@ -1566,6 +1605,10 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
             }
             launches += n * p->launches_later;
             left -= n;
+            // Without tolerances the run cannot converge early: everything is
+            // enqueued at once (after a failure the remaining kernels exit on
+            // the device stop flag), so host scheduling never starves the GPU.
+            if (!poll) continue;
             CK(cudaMemcpyAsync(&h_stop[slot], &p->d_ctrl->stop, sizeof(int32_t),
                                cudaMemcpyDeviceToHost, st));
             CK(cudaEventRecord(pe[slot], st));
@@ -1602,7 +1645,7 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
     // x of the last (or failing) iteration stays in registers when the
     // chain kernel ran it; fg_state_download / fg_debug_download recompute it
     p->x_stale = 0;
-    if (p->chain_on && !p->nccl_comm) {
+    if (p->chain_on) {
         const int64_t need = h.err_key != ~0ull ? (int64_t)(h.err_key >> 3) : h.completed;
         if (need >= (first_n ? 2 : 1)) p->x_stale = need;
     }
@@ -2042,8 +2085,6 @@ int fg_plan_attach_nccl(fg_plan* p, const char* nccl_lib, const char* id128, int
     if (int rc = nccl_check(g_nccl.CommInitRank(&comm, world, id, rank), "ncclCommInitRank"))
         return rc;
     p->nccl_comm = comm;
-    p->chain_on = false;               // the fused chain is single-device only
-    p->launches_later = p->launches_per_iter;
     p->world = world;
     p->rank = rank;
     {   // global payload = sum of the ranks' local payloads (disjoint edges)
@@ -2132,7 +2173,7 @@ int fg_group_run(fg_plan** plans, int32_t G, const fg_run_config* cfg, double* h
         const bool first = (j == 1) && first_n;
         for (int r = 0; r < G; ++r) part_pre(plans[r], in, first, st);
         if (ncut) { if (int rc = gather(0, (size_t)ncut, 0)) return rc; }
-        for (int r = 0; r < G; ++r) part_mid(plans[r], in, st);
+        for (int r = 0; r < G; ++r) part_mid(plans[r], in, first, st);
         if (int rc = gather((size_t)ncut, 4, (size_t)G * ncut)) return rc;
         for (int r = 0; r < G; ++r) part_post(plans[r], st);
         for (int r = 0; r < G; ++r) launches += plans[r]->launches_per_iter + 1;
@@ -2155,6 +2196,11 @@ int fg_group_run(fg_plan** plans, int32_t G, const fg_run_config* cfg, double* h
     for (int r = 0; r < G; ++r) {
         CK(cudaMemcpy(&h, plans[r]->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
         plans[r]->completed = h.completed;
+        plans[r]->x_stale = 0;
+        if (plans[r]->chain_on) {
+            const int64_t need = h.err_key != ~0ull ? (int64_t)(h.err_key >> 3) : h.completed;
+            if (need >= (first_n ? 2 : 1)) plans[r]->x_stale = need;
+        }
     }
     CK(cudaMemcpy(&h, p0->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
     std::memset(out, 0, sizeof(*out));

@@ -446,10 +446,12 @@ __global__ void k_cut_finalize(PassB b, const int32_t* glist, const GComp* comps
 // error key) go to a 4-double send slot, are all-gathered, and every rank
 // combines them in rank order, so all ranks take the same stop decision.
 __global__ void __launch_bounds__(1024) k_reduce_local(Ctrl* c, const double* part,
-                                                       int64_t npart, double* send4) {
+                                                       int64_t npart, double* send4,
+                                                       int64_t skip_lo = 0, int64_t skip_hi = 0) {
     __shared__ double sm[64];
     double a = 0.0, bsum = 0.0;
     for (int64_t i = threadIdx.x; i < npart; i += 1024) {
+        if (i >= skip_lo && i < skip_hi) continue;
         a += part[2 * i];
         bsum += part[2 * i + 1];
     }

@@ -84,7 +84,25 @@ def factor_owner(graph, world):
     total = cum[-1] if V else 0.0
     bounds = np.array([int(np.searchsorted(cum, total * r / world, side="left")) + 1
                        for r in range(1, world)], dtype=np.int64)
-    return np.searchsorted(bounds, anchor_pos, side="right").astype(np.int64)
+    owner = np.searchsorted(bounds, anchor_pos, side="right").astype(np.int64)
+    # a factor on a single variable (SVM slack, MPC cost, radius) follows
+    # the rank of that variable's other factors when they agree: it would
+    # otherwise make the variable a cut variable for no load-balance gain
+    E = len(graph.edge_var)
+    ef = np.repeat(np.arange(len(f_first)), arity)
+    ev = graph.edge_var
+    multi = arity[ef] > 1
+    big = np.iinfo(np.int64).max
+    lo = np.full(V, big, dtype=np.int64)
+    hi = np.full(V, -1, dtype=np.int64)
+    np.minimum.at(lo, ev[multi], owner[ef[multi]])
+    np.maximum.at(hi, ev[multi], owner[ef[multi]])
+    single = np.nonzero(arity == 1)[0]
+    sv = ev[f_first[single]]
+    ok = lo[sv] == hi[sv]
+    owner[single[ok]] = lo[sv[ok]]
+    del E
+    return owner
 
 
 class LocalGraph:

@@ -67,3 +67,30 @@ def test_local_group_matches_partitioned_oracle_bitwise_on_noncut(gpu):
     ref, _rh, _ = O.run(g, 5, st)
     for k in "xmzun":
         assert _close(getattr(out, k), getattr(ref, k)), k
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_svm_partition_runs_fused_chain_bitwise_vs_per_kind(gpu, monkeypatch, world):
+    """Partition plans of the SVM chain keep the fused chain kernel (cut
+    weight copies and the bias go through the exchange); the result is
+    bitwise the per-kind partitioned run and within 1e-9 of one plan."""
+    X, y = fg.gen_gaussian_arrays(2400, 32, 4.0, seed=5)
+    g = fg.build_svm(fg.SvmSpec.from_arrays(X, y))
+    st = fg.init_state(g, seed=4)
+    outs = []
+    for chain in (True, False):
+        if chain:
+            monkeypatch.delenv("FGADMM_NO_CHAIN", raising=False)
+        else:
+            monkeypatch.setenv("FGADMM_NO_CHAIN", "1")
+        grp = LocalGroup(g, world)
+        assert all(p.info["fused_chain"] == chain for p in grp.plans)
+        out, res, hist = grp.run(12, st)
+        assert res.iterations == 12 and res.error_phase == -1
+        outs.append((out, hist))
+    for k in "xmzun":
+        np.testing.assert_array_equal(getattr(outs[0][0], k), getattr(outs[1][0], k), err_msg=k)
+    single = fg.AdmmState(*(getattr(st, k).copy() for k in "xmzun"))
+    fg.run(g, fg.RunConfig(max_iterations=12), state=single)
+    for k in "xmzun":
+        assert _close(getattr(outs[0][0], k), getattr(single, k)), k
