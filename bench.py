@@ -78,16 +78,19 @@ def build_instance(name, scale=1.0):
 # algorithmic bytes per kernel
 
 def kernel_bytes(graph, plan):
-    """Compulsory HBM bytes per launch of each kernel of one iteration."""
+    """Compulsory HBM bytes per launch of each kernel of one iteration, for
+    the kernel forms the plan runs (unit-weight forms read no weights)."""
     dims = np.diff(np.asarray(graph.var_offsets))
     deg = np.bincount(graph.edge_var, minlength=len(dims))
+    forms = plan.forms()
     out = {}
     for cls, sdims, fe, dp, _p, _s in plan.groups:
         B = len(fe)
         b = 0
         zcomp = 0
+        wbytes = 0 if (cls.kind == "collision" and forms["collision_unit"]) else 8
         for j, d in enumerate(sdims):
-            b += B * d * 16 + B * 8            # u read + x write, rho read
+            b += B * d * 16 + B * wbytes       # u read + x write, rho read
             zcomp += int(np.sum(dims[np.unique(graph.edge_var[fe + j])]))
         b += 8 * zcomp                         # z read once per component
         if dp.fparams is not None:
@@ -112,7 +115,8 @@ def kernel_bytes(graph, plan):
             P = int(np.sum(deg[sel] * dims[sel]))
             E = int(np.sum(deg[sel]))
             Z = int(np.sum(dims[sel]))
-            out[key] = P * 24 + E * 16 + Z * 24
+            unit = key.startswith("var_large_d") and forms["rows_unit"][int(key[-1])]
+            out[key] = P * 24 + (0 if unit else E * 16) + Z * 24
     if giant.any():
         P = int(np.sum(deg[giant] * dims[giant]))
         E = int(np.sum(deg[giant]))

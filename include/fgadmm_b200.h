@@ -157,6 +157,12 @@ void fg_plan_destroy(fg_plan* plan);
  * chain form (0 off, 1 generic, 2 fast, 3 unit-weight; the unit form is
  * re-decided at every fg_plan_sync_params) */
 int fg_plan_info(const fg_plan* plan, int64_t* out12);
+/* Kernel forms the next run uses (decided at plan creation and at every
+ * fg_plan_sync_params): out[0] fused SVM chain (0 off, 1 generic, 2 fast,
+ * 3 unit-weight), out[1] collision tiles in unit-weight form, out[2..5]
+ * class-L rows of dim 1..4 in unit-weight form, out[6] mpc_dyn matrix
+ * form, out[7] giant top/reduce fused. */
+int fg_plan_forms(const fg_plan* plan, int32_t* out8);
 int fg_plan_sync_params(fg_plan* plan, const double* edge_rho,
                         const double* edge_alpha, const double* z_weights);
 

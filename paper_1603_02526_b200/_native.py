@@ -65,6 +65,7 @@ EXPORTS = {
                                  C.c_int32, C.POINTER(_p)]),
     "fg_plan_destroy": (None, [_p]),
     "fg_plan_info": (C.c_int, [_p, _i64p]),
+    "fg_plan_forms": (C.c_int, [_p, C.POINTER(C.c_int32)]),
     "fg_plan_sync_params": (C.c_int, [_p, _dp, _dp, _dp]),
     "fg_state_upload": (C.c_int, [_p, _dp, _dp, _dp]),
     "fg_run": (C.c_int, [_p, C.POINTER(RunConfig), _dp, C.POINTER(RunResult)]),

@@ -58,6 +58,10 @@ struct GroupDev {
     // i * rowS field by field, so the tile kernel computes addresses
     int32_t rows_affine, rows_even;      // rows_even: center rows 16-byte aligned
     DiskRow row0, rowS;
+    // mpc_dyn matrix form (uniform weights): K (cols x cols) on the device
+    const double* kmat;
+    int32_t dyn_gemm;
+    int32_t unit;                        // all edge weights 1 (collision tiles)
 };
 
 struct PassA {
@@ -603,7 +607,10 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 //  * divisions by unit edge weights are skipped exactly (ddiv).
 // A16: center entries 16-byte aligned (one 16-byte access per center pair);
 // otherwise two 8-byte accesses.
-template <bool FIRST, bool A16>
+// UNIT: every collision edge weight is exactly 1 (checked at sync): no
+// weight loads, and the prox's weight arithmetic is the exact identity
+// (1/1 = 1, mu/4 = mu*0.25, mu/1 = mu), bitwise the general form.
+template <bool FIRST, bool A16, bool UNIT = false>
 __global__ void __launch_bounds__(kEdgeThreads, 3) k_collision_tiles_v3(PassA a, GroupDev g) {
     __shared__ double2 s_c[kTile][kTile + 1];       // [jl][il]: j-half centers
     __shared__ double s_r[kTile][kTP], s_rc[kTile][kTP], s_rr[kTile][kTP];
@@ -630,8 +637,10 @@ __global__ void __launch_bounds__(kEdgeThreads, 3) k_collision_tiles_v3(PassA a,
                 cp_async8(&s_c[jl][l].y, src + R.pbc + 2 * (int64_t)i + 1);
             }
             cp_async8(&s_r[jl][l], src + R.pbr + i);
-            cp_async8(&s_rc[jl][l], rho + R.ebc + i);
-            cp_async8(&s_rr[jl][l], rho + R.ebr + i);
+            if (!UNIT) {
+                cp_async8(&s_rc[jl][l], rho + R.ebc + i);
+                cp_async8(&s_rr[jl][l], rho + R.ebr + i);
+            }
         }
     }
     asm volatile("cp.async.commit_group;\n" ::);
@@ -656,8 +665,10 @@ __global__ void __launch_bounds__(kEdgeThreads, 3) k_collision_tiles_v3(PassA a,
             if (A16) nc[k] = *reinterpret_cast<const double2*>(src + R.pbc + 2 * e);
             else nc[k] = make_double2(src[R.pbc + 2 * e], src[R.pbc + 2 * e + 1]);
             nr[k] = src[R.pbr + e];
-            rc1[k] = rho[R.ebc + e];
-            rr1[k] = rho[R.ebr + e];
+            if (!UNIT) {
+                rc1[k] = rho[R.ebc + e];
+                rr1[k] = rho[R.ebr + e];
+            }
         }
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
@@ -678,8 +689,12 @@ __global__ void __launch_bounds__(kEdgeThreads, 3) k_collision_tiles_v3(PassA a,
                         finite(n2c1) && finite(n2r));
             }
             double c10, c11, r1, c20, c21, r2;
-            prox_collision(n1c0, n1c1, n1r, n2c0, n2c1, n2r, rc1[k], rr1[k], s_rc[l][il],
-                           s_rr[l][il], c10, c11, r1, c20, c21, r2);
+            if (UNIT)
+                prox_collision(n1c0, n1c1, n1r, n2c0, n2c1, n2r, 1.0, 1.0, 1.0, 1.0, c10, c11,
+                               r1, c20, c21, r2);
+            else
+                prox_collision(n1c0, n1c1, n1r, n2c0, n2c1, n2r, rc1[k], rr1[k], s_rc[l][il],
+                               s_rr[l][il], c10, c11, r1, c20, c21, r2);
             const DiskRow R = disk_row(g, i);
             const int64_t e = j - 1;
             if (A16) {

@@ -145,6 +145,12 @@ struct GroupHost {
     // per slot: (variable, rank in its segment) of every factor; kept until
     // the plan's topology detection ran (fused SVM chain)
     std::vector<std::vector<int32_t>> hsv, hsk;
+    // mpc_dyn matrix form: host table of the single system, reference first
+    // edges (uniform-weight check at sync), device K
+    std::vector<double> tab_h;
+    std::vector<int64_t> ref_e0;
+    double* d_kmat = nullptr;
+    double kr0 = 0.0, kr1 = 0.0;       // weights K was built for
 };
 
 struct fg_plan {
@@ -239,6 +245,10 @@ struct fg_plan {
     // fused giant kernels: the chunk kernel's last CTA per component runs the
     // top of the tree; in chain iterations the update's last CTA reduces
     bool giant_fused = true;
+    bool row256 = false;               // class-L rows on 256-thread CTAs (A/B)
+    bool no_fork = false;              // edge groups serialized on one stream (A/B)
+    bool lunit[5] = {false, false, false, false, false};  // class-L rows of dim D: unit weights
+    LExc* d_lexc[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // their exception edge
     unsigned* d_gcnt = nullptr;        // per giant component chunk counter
     unsigned* d_ucnt = nullptr;        // giant update CTA counter
     FusedReduce fr_next{nullptr, 0, 0, 0, nullptr};   // set by chain_rest
@@ -265,7 +275,8 @@ fg_plan::~fg_plan() {
                     d_clprog[2], d_clprog[3], d_clprog[4],
                     d_llist, d_lprog, d_prog, d_glist, d_gchunks, d_gcomps,
                     d_gwork, d_csum, d_gz, d_part, d_res2, d_ctrl, d_hist, d_chain_xx,
-                    d_chain_fnorm, d_flag, d_gcnt, d_ucnt,
+                    d_chain_fnorm, d_flag, d_gcnt, d_ucnt, d_lexc[1], d_lexc[2], d_lexc[3],
+                    d_lexc[4],
                     d_cutg, d_send, d_recv};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -289,7 +300,11 @@ void launch_kind(const GroupDev& g, const PassA& a, cudaStream_t st) {
     const int T = kEdgeThreads;
     switch (g.kind) {
         case FG_KIND_COLLISION:
-            if (g.tiles && g.variant == 3 && g.rows_even)
+            if (g.tiles && g.variant == 3 && g.rows_even && g.unit)
+                k_collision_tiles_v3<FIRST, true, true><<<(unsigned)g.ntiles, T, 0, st>>>(a, g);
+            else if (g.tiles && g.variant == 3 && g.unit)
+                k_collision_tiles_v3<FIRST, false, true><<<(unsigned)g.ntiles, T, 0, st>>>(a, g);
+            else if (g.tiles && g.variant == 3 && g.rows_even)
                 k_collision_tiles_v3<FIRST, true><<<(unsigned)g.ntiles, T, 0, st>>>(a, g);
             else if (g.tiles && g.variant == 3)
                 k_collision_tiles_v3<FIRST, false><<<(unsigned)g.ntiles, T, 0, st>>>(a, g);
@@ -320,20 +335,42 @@ void launch_kind(const GroupDev& g, const PassA& a, cudaStream_t st) {
             else k_svm_margin<FIRST, kMarginMaxD / kMarginLanes><<<grid, T, 0, st>>>(a, g);
             break;
         case FG_KIND_MPC_DYN:
-            k_mpc_dyn8<FIRST><<<grid, T, mpc_dyn8_smem(g.tstride, g.dim[0] + g.ip, g.ip,
-                                                       g.fsys == nullptr), st>>>(a, g);
+            if (g.dyn_gemm)
+                k_mpc_dyn_gemm<FIRST><<<(unsigned)g.nblocks, T,
+                                        mpc_dyn_gemm_smem(g.dim[0] + g.ip), st>>>(a, g);
+            else
+                k_mpc_dyn8<FIRST><<<grid, T, mpc_dyn8_smem(g.tstride, g.dim[0] + g.ip, g.ip,
+                                                           g.fsys == nullptr), st>>>(a, g);
             break;
         default: break;
     }
 }
 
+// The groups write disjoint x entries and only read z and u: the first
+// group runs on the plan's stream, the others on a forked stream
+// concurrently with it (parallel branches of the captured graph), so small
+// groups (packing walls/radii, SVM slacks) hide under the big one.
 void edge_pass(fg_plan* p, bool first, const double* zin, const double* uin,
                const double* nsrc, cudaStream_t st) {
     PassA a{p->vt(), zin, uin, nsrc, p->d_x, p->d_rho, p->d_ctrl};
+    int active = 0;
+    for (auto& g : p->groups) active += g.dev.count > 0;
+    if (p->no_fork) active = 1;
+    if (active >= 2) {
+        cudaEventRecord(p->ev_fork, st);
+        cudaStreamWaitEvent(p->stream2, p->ev_fork, 0);
+    }
+    int k = 0;
     for (auto& g : p->groups) {
         if (g.dev.count == 0) continue;
-        if (first) launch_kind<true>(g.dev, a, st);
-        else launch_kind<false>(g.dev, a, st);
+        cudaStream_t gs = (k >= 1 && active >= 2) ? p->stream2 : st;
+        if (first) launch_kind<true>(g.dev, a, gs);
+        else launch_kind<false>(g.dev, a, gs);
+        ++k;
+    }
+    if (k >= 2 && active >= 2) {
+        cudaEventRecord(p->ev_join, p->stream2);
+        cudaStreamWaitEvent(st, p->ev_join, 0);
     }
 }
 
@@ -398,16 +435,36 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
             k_var_small_run<0, MODE><<<grid, 256, 0, st>>>(b, p->d_sruns, p->d_sblk[2], po);
             return true;
         case 3:
-            k_var_large_vec<1, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po);
+            if (p->row256)
+                k_var_large_vec<1, MODE, 256><<<grid, 256, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po);
+            else if (p->lunit[1])
+                k_var_large_vec<1, MODE, kLargeThreads, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po, p->d_lexc[1]);
+            else
+                k_var_large_vec<1, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po);
             return true;
         case 4:
-            k_var_large_vec<2, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po);
+            if (p->row256)
+                k_var_large_vec<2, MODE, 256><<<grid, 256, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po);
+            else if (p->lunit[2])
+                k_var_large_vec<2, MODE, kLargeThreads, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po, p->d_lexc[2]);
+            else
+                k_var_large_vec<2, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po);
             return true;
         case 5:
-            k_var_large_vec<3, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po);
+            if (p->row256)
+                k_var_large_vec<3, MODE, 256><<<grid, 256, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po);
+            else if (p->lunit[3])
+                k_var_large_vec<3, MODE, kLargeThreads, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po, p->d_lexc[3]);
+            else
+                k_var_large_vec<3, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po);
             return true;
         case 6:
-            k_var_large_vec<4, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, po);
+            if (p->row256)
+                k_var_large_vec<4, MODE, 256><<<grid, 256, 0, st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, po);
+            else if (p->lunit[4])
+                k_var_large_vec<4, MODE, kLargeThreads, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, po, p->d_lexc[4]);
+            else
+                k_var_large_vec<4, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, po);
             return true;
         case 7:
             k_var_large<MODE><<<grid, kVarThreads, 0, st>>>(b, p->d_llist, p->d_lprog, p->d_prog, po);
@@ -985,6 +1042,15 @@ int build_group(fg_plan* p, const fg_group_desc& gd,
             if (!cvar || std::strcmp(cvar, "v3") == 0) g.variant = 3;
         }
     }
+    if (gd.kind == FG_KIND_MPC_DYN && gd.tables && gd.ntables == 1 && g.runs &&
+        g.dim[0] + gd.iparam <= kDynGemmMaxCols) {
+        out.tab_h.assign(gd.tables, gd.tables + gd.tstride);
+        out.ref_e0.assign(gd.first_edge, gd.first_edge + n);
+        CK(cudaFuncSetAttribute(k_mpc_dyn_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kMaxDynSmem));
+        CK(cudaFuncSetAttribute(k_mpc_dyn_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kMaxDynSmem));
+    }
     if (gd.kind == FG_KIND_SVM_NORM || gd.kind == FG_KIND_SVM_SLACK ||
         gd.kind == FG_KIND_SVM_MARGIN || gd.kind == FG_KIND_EQUALITY) {
         out.hsv = std::move(svs);
@@ -1299,6 +1365,8 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     for (int d = 1; d <= 4; ++d) p->nlv[d] = (int64_t)lvars[d].size();
     p->gtop_smem = (int)(2 * max_top * sizeof(double));
     p->giant_fused = getenv("FGADMM_GIANT_UNFUSED") == nullptr;
+    p->row256 = getenv("FGADMM_ROW256") != nullptr;
+    p->no_fork = getenv("FGADMM_NO_FORK") != nullptr;
     if ((size_t)p->gtop_smem > 40 * 1024) {
         CK(cudaFuncSetAttribute(k_var_giant_top<MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
         CK(cudaFuncSetAttribute(k_var_giant_top<MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
@@ -1383,6 +1451,19 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
 
 void fg_plan_destroy(fg_plan* plan) { delete plan; }
 
+int fg_plan_forms(const fg_plan* p, int32_t* o) {
+    o[0] = p->chain_on ? (p->chain_unit ? 3 : (p->chain_fast ? 2 : 1)) : 0;
+    o[1] = 0;
+    o[6] = 0;
+    for (auto& g : p->groups) {
+        if (g.dev.kind == FG_KIND_COLLISION && g.dev.unit) o[1] = 1;
+        if (g.dev.kind == FG_KIND_MPC_DYN && g.dev.dyn_gemm) o[6] = 1;
+    }
+    for (int d = 1; d <= 4; ++d) o[1 + d] = p->lunit[d] ? 1 : 0;
+    o[7] = p->giant_fused ? 1 : 0;
+    return 0;
+}
+
 int fg_plan_info(const fg_plan* p, int64_t* o) {
     o[0] = p->V; o[1] = p->E; o[2] = p->P; o[3] = p->Z;
     o[4] = p->nS; o[5] = p->nLvars; o[6] = p->nG; o[7] = p->nGC;
@@ -1393,6 +1474,9 @@ int fg_plan_info(const fg_plan* p, int64_t* o) {
     return 0;
 }
 
+static int sync_dyn_matrix(fg_plan* p, GroupHost& gh, const double* rho);
+static int sync_unit_flags(fg_plan* p);
+
 int fg_plan_sync_params(fg_plan* p, const double* rho, const double* alpha,
                         const double* zw) {
     CK(cudaSetDevice(p->device));
@@ -1402,6 +1486,10 @@ int fg_plan_sync_params(fg_plan* p, const double* rho, const double* alpha,
     CK(cudaMemcpyAsync(p->d_stage, alpha, p->E * sizeof(double), cudaMemcpyHostToDevice, st));
     k_gather_edges<<<nblk(p->E, 256), 256, 0, st>>>(p->E, p->d_refedge, p->d_stage, p->d_alpha);
     CK(cudaMemcpyAsync(p->d_zw, zw, p->Z * sizeof(double), cudaMemcpyHostToDevice, st));
+    for (auto& gh : p->groups)
+        if (gh.dev.kind == FG_KIND_MPC_DYN && !gh.tab_h.empty())
+            if (int rc = sync_dyn_matrix(p, gh, rho)) return rc;
+    if (int rc = sync_unit_flags(p)) return rc;
     if (p->chain_fast) {
         // unit-weight form of the chain: every rho and alpha exactly 1 and
         // the z weights equal to the degrees (fg_chain.cuh)
@@ -1418,6 +1506,106 @@ int fg_plan_sync_params(fg_plan* p, const double* rho, const double* alpha,
         }
     }
     CK(cudaStreamSynchronize(st));
+    return check_launch();
+}
+
+// mpc_dyn matrix form: K = I - W^-1 M^T Q diag(1/(L/rho0 + 1/rho1)) Q^T M
+// when every factor of the group has the same (rho0, rho1); otherwise the
+// 8-lane kernel evaluates the staged form per factor.
+static int sync_dyn_matrix(fg_plan* p, GroupHost& gh, const double* rho) {
+    GroupDev& g = gh.dev;
+    const int64_t n = (int64_t)gh.ref_e0.size();
+    const double r0 = rho[gh.ref_e0[0]], r1 = rho[gh.ref_e0[0] + 1];
+    bool uni = n > 0 && !getenv("FGADMM_DYN_LOOP");
+    for (int64_t i = 0; i < n && uni; ++i)
+        uni = rho[gh.ref_e0[i]] == r0 && rho[gh.ref_e0[i] + 1] == r1;
+    const int32_t was = g.dyn_gemm;
+    if (uni && !(g.dyn_gemm && gh.kr0 == r0 && gh.kr1 == r1)) {
+        const int n0 = g.dim[0], d = g.ip, cols = n0 + d;
+        const double* M = gh.tab_h.data();
+        const double* Q = M + d * cols;
+        const double* L = Q + d * d;
+        std::vector<double> A(d * cols, 0.0), B(d * cols, 0.0), K(cols * cols);
+        for (int i = 0; i < d; ++i) {
+            const double dd = L[i] / r0 + 1.0 / r1;
+            for (int c = 0; c < cols; ++c) {
+                double acc = 0.0;
+                for (int q = 0; q < d; ++q) acc += Q[q * d + i] * M[q * cols + c];
+                A[i * cols + c] = acc / dd;
+            }
+        }
+        for (int q = 0; q < d; ++q)
+            for (int c = 0; c < cols; ++c) {
+                double acc = 0.0;
+                for (int i = 0; i < d; ++i) acc += Q[q * d + i] * A[i * cols + c];
+                B[q * cols + c] = acc;
+            }
+        for (int r = 0; r < cols; ++r) {
+            const double winv = 1.0 / (r < n0 ? r0 : r1);
+            for (int c = 0; c < cols; ++c) {
+                double acc = 0.0;
+                for (int q = 0; q < d; ++q) acc += M[q * cols + r] * B[q * cols + c];
+                K[r * cols + c] = (r == c ? 1.0 : 0.0) - winv * acc;
+            }
+        }
+        if (!gh.d_kmat) {
+            CK(cudaMalloc((void**)&gh.d_kmat, (size_t)cols * cols * sizeof(double)));
+            gh.allocs.push_back(gh.d_kmat);
+        }
+        CK(cudaMemcpy(gh.d_kmat, K.data(), K.size() * sizeof(double), cudaMemcpyHostToDevice));
+        g.kmat = gh.d_kmat;
+        gh.kr0 = r0;
+        gh.kr1 = r1;
+    }
+    g.dyn_gemm = uni ? 1 : 0;
+    if (g.dyn_gemm != was) {
+        // kernel parameters are baked into captured graphs
+        for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
+        p->graphs.clear();
+    }
+    return 0;
+}
+
+// Unit-weight forms of the collision tiles and the class-L rows: every
+// weight of their edges exactly 1 (re-decided at every sync; the kernels
+// drop the weight loads, which are exact identities).
+static int sync_unit_flags(fg_plan* p) {
+    cudaStream_t st = p->stream;
+    const bool off = getenv("FGADMM_NO_UNIT") != nullptr;
+    bool changed = false;
+    for (auto& gh : p->groups) {
+        GroupDev& g = gh.dev;
+        if (g.kind != FG_KIND_COLLISION || !g.tiles || !g.rows_affine) continue;
+        int32_t bad = 1;
+        if (!off) {
+            CK(cudaMemsetAsync(p->d_flag, 0, sizeof(int32_t), st));
+            k_unit_collision<<<(unsigned)g.ndisks, 256, 0, st>>>(g, p->d_rho, p->d_flag);
+            CK(cudaMemcpyAsync(&bad, p->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        }
+        const int32_t u = bad ? 0 : 1;
+        changed |= u != g.unit;
+        g.unit = u;
+    }
+    for (int d = 1; d <= 4; ++d) {
+        bool u = false;
+        if (p->nlv[d] > 0 && !off) {
+            int32_t bad = 1;
+            if (!p->d_lexc[d]) CK(cudaMalloc((void**)&p->d_lexc[d], p->nlv[d] * sizeof(LExc)));
+            CK(cudaMemsetAsync(p->d_flag, 0, sizeof(int32_t), st));
+            k_unit_rows<<<(unsigned)p->nlv[d], 128, 0, st>>>(p->d_lvars[d], p->vt(), p->d_rho,
+                                                            p->d_alpha, p->d_lexc[d], p->d_flag);
+            CK(cudaMemcpyAsync(&bad, p->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            u = bad == 0;
+        }
+        changed |= u != p->lunit[d];
+        p->lunit[d] = u;
+    }
+    if (changed) {                     // kernel choices are baked into graphs
+        for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
+        p->graphs.clear();
+    }
     return check_launch();
 }
 

@@ -530,6 +530,42 @@ __global__ void k_gather_edges(int64_t E, const int32_t* ref_edge,
 }
 
 // phase m (engine.py:263-265): m = x + u
+// Unit-weight checks (parameter sync).
+// Per class-L row (one CTA each): its single non-unit edge, if any; a row
+// with two or more raises the flag (the rows then keep the general form).
+struct LExc { int32_t rank, pad; double rho, alpha; };
+__global__ void k_unit_rows(const int32_t* vlist, VarTab vt, const double* rho,
+                            const double* alpha, LExc* out, int32_t* flag) {
+    __shared__ int s_cnt, s_rank;
+    if (threadIdx.x == 0) { s_cnt = 0; s_rank = -1; }
+    __syncthreads();
+    const int32_t v = vlist[blockIdx.x];
+    const int32_t e0 = vt.ebase[v], dg = vt.deg[v];
+    for (int32_t k = threadIdx.x; k < dg; k += blockDim.x)
+        if (rho[e0 + k] != 1.0 || alpha[e0 + k] != 1.0) {
+            atomicAdd(&s_cnt, 1);
+            s_rank = k;
+        }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        LExc o{-1, 0, 1.0, 1.0};
+        if (s_cnt == 1) o = LExc{s_rank, 0, rho[e0 + s_rank], alpha[e0 + s_rank]};
+        if (s_cnt > 1) atomicOr(flag, 1);
+        out[blockIdx.x] = o;
+    }
+}
+
+// ... and any collision edge (rows of the all-pairs triangle).
+__global__ void k_unit_collision(GroupDev g, const double* rho, int32_t* flag) {
+    const int i = blockIdx.x;
+    if (i >= g.ndisks) return;
+    const DiskRow R = disk_row(g, i);
+    bool bad = false;
+    for (int e = threadIdx.x; e < g.ndisks - 1; e += blockDim.x)
+        bad |= rho[R.ebc + e] != 1.0 || rho[R.ebr + e] != 1.0;
+    if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
 // Any payload slot whose uploaded n differs (bitwise) from z[zmap] - u.
 __global__ void k_n_mismatch(int64_t P, const int32_t* vmz, const double* z,
                              const double* u, const double* n, int32_t* flag) {

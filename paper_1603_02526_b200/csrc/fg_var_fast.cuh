@@ -136,12 +136,16 @@ __global__ void __launch_bounds__(256, 4) k_var_small_run(PassB b, const SRun* r
 }
 
 // Class L, one CTA per variable with D components.
-template <int D, int MODE>
-__global__ void __launch_bounds__(kLargeThreads, 2) k_var_large_vec(
+// Unit-weight rows: at most one edge per row has rho or alpha != 1 (its
+// rank and weights in the row's LExc, k_unit_rows; rank -1 for none).
+// UNIT: rows in unit-weight form: every other weight is exactly 1, and
+// m*1, rho*dz and t*1 are exact identities, so no rho/alpha loads.
+template <int D, int MODE, int NT = kLargeThreads, bool UNIT = false>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_var_large_vec(
     PassB b, const int32_t* vlist, const int32_t* progoff, const int32_t* prog,
-    int64_t part_off) {
+    int64_t part_off, const LExc* exc = nullptr) {
     __shared__ double sv[D][2 * kMaxUnits];
-    __shared__ double sm[2 * (kLargeThreads / 32)];
+    __shared__ double sm[2 * (NT / 32)];
     __shared__ double s_z[2][D];
     __shared__ int s_stop;
     if (threadIdx.x == 0) s_stop = b.ctrl->stop;
@@ -155,9 +159,11 @@ __global__ void __launch_bounds__(kLargeThreads, 2) k_var_large_vec(
     const int deg = b.vt.deg[v];
     const double* msrc = (MODE == MODE_FUSED) ? b.uin : b.msrc;
     bool bm = false, bu = false;
+    LExc xe{-1, 0, 1.0, 1.0};
+    if (UNIT) xe = exc[blockIdx.x];
     // element e -> D values of m*rho
     auto vals = [&](int64_t e, double* out) {
-        const double r = b.rho[eb + e];
+        const double r = UNIT ? (e == xe.rank ? xe.rho : 1.0) : b.rho[eb + e];
 #pragma unroll
         for (int c = 0; c < D; ++c) {
             double m = msrc[pb + e * D + c];
@@ -185,7 +191,7 @@ __global__ void __launch_bounds__(kLargeThreads, 2) k_var_large_vec(
         }
     }
     const int g = threadIdx.x >> 3, j = threadIdx.x & 7;
-    constexpr int NG = kLargeThreads / 8;
+    constexpr int NG = NT / 8;
     for (int r0 = 0; r0 < nu; r0 += NG) {
         const int L = r0 + g;
         int64_t s = 0, len = 0;
@@ -267,14 +273,14 @@ __global__ void __launch_bounds__(kLargeThreads, 2) k_var_large_vec(
         // before its stores (the compiler cannot prove uout aliases nothing
         // read here), one memory round trip per batch
         constexpr int kUB = D == 1 ? 4 : 2;
-        for (int64_t e0 = threadIdx.x; e0 < deg; e0 += kUB * kLargeThreads) {
+        for (int64_t e0 = threadIdx.x; e0 < deg; e0 += kUB * NT) {
             double xr[kUB][D], ur[kUB][D], rr[kUB], ar[kUB];
 #pragma unroll
             for (int k = 0; k < kUB; ++k) {
-                const int64_t e = e0 + (int64_t)k * kLargeThreads;
+                const int64_t e = e0 + (int64_t)k * NT;
                 if (e < deg) {
-                    rr[k] = b.rho[eb + e];
-                    ar[k] = b.alpha[eb + e];
+                    rr[k] = UNIT ? (e == xe.rank ? xe.rho : 1.0) : b.rho[eb + e];
+                    ar[k] = UNIT ? (e == xe.rank ? xe.alpha : 1.0) : b.alpha[eb + e];
 #pragma unroll
                     for (int c = 0; c < D; ++c) {
                         xr[k][c] = b.x[pb + e * D + c];
@@ -284,7 +290,7 @@ __global__ void __launch_bounds__(kLargeThreads, 2) k_var_large_vec(
             }
 #pragma unroll
             for (int k = 0; k < kUB; ++k) {
-                const int64_t e = e0 + (int64_t)k * kLargeThreads;
+                const int64_t e = e0 + (int64_t)k * NT;
                 if (e < deg) {
 #pragma unroll
                     for (int c = 0; c < D; ++c) {
@@ -301,7 +307,7 @@ __global__ void __launch_bounds__(kLargeThreads, 2) k_var_large_vec(
         }
         if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
         if (bu) flag_error(b.ctrl, it, FG_PHASE_U, false);
-        block_sum2<kLargeThreads>(pp, dd, sm);
+        block_sum2<NT>(pp, dd, sm);
         if (threadIdx.x == 0) {
             b.part[2 * (part_off + blockIdx.x)] = pp;
             b.part[2 * (part_off + blockIdx.x) + 1] = dd;

@@ -343,6 +343,17 @@ class DevicePlan:
             out[key] = (float(ms[i]), int(cnt[i]))
         return out
 
+    def forms(self):
+        """Kernel forms of the next run (fg_plan_forms): chain form,
+        unit-weight collision tiles / class-L rows per dim, mpc_dyn matrix
+        form, fused giant kernels."""
+        o = (C.c_int32 * 8)()
+        self._lib.fg_plan_forms(self._h, o)
+        return {"chain": ("off", "generic", "fast", "unit")[o[0]],
+                "collision_unit": bool(o[1]),
+                "rows_unit": {d: bool(o[1 + d]) for d in (1, 2, 3, 4)},
+                "mpc_dyn_matrix": bool(o[6]), "giant_fused": bool(o[7])}
+
     def chain_form(self):
         """Form of the fused SVM-chain kernel the next run uses: 'off',
         'generic', 'fast' or 'unit' (unit weights; decided at every sync)."""

@@ -257,7 +257,9 @@ def test_packing_1030_cluster_and_tile_kernels_bitwise(gpu):
 
 @pytest.mark.parametrize("env", [{"FGADMM_TMA": "1"}, {"FGADMM_CLUSTER": "1"},
                                  {"FGADMM_COLLISION": "tile"},
-                                 {"FGADMM_COLLISION": "generic"}])
+                                 {"FGADMM_COLLISION": "generic"},
+                                 {"FGADMM_NO_UNIT": "1"}, {"FGADMM_NO_FORK": "1"},
+                                 {"FGADMM_ROW256": "1"}, {"FGADMM_GIANT_UNFUSED": "1"}])
 def test_opt_in_kernel_variants_match_oracle(gpu, env, monkeypatch):
     """The alternative kernels selected at plan creation (TMA bulk-copy
     pipeline for small segments, 4-CTA DSMEM cluster rows, cp.async
@@ -283,3 +285,41 @@ def test_opt_in_kernel_variants_match_oracle(gpu, env, monkeypatch):
     so2, _h, _ = O.run(g2, 6, st2)
     for k in "xmzun":
         assert_close(getattr(s2, k), getattr(so2, k), what=k)
+
+
+def test_packing_unit_forms_follow_set_edge_params(gpu):
+    """Collision tiles and rows drop their weight loads only while every
+    weight is 1: re-weighting one collision edge (and back) keeps the run
+    bitwise equal to the oracle on the same weight sequence."""
+    from paper_1603_02526_b200.engine import DevicePlan, _PLANS
+    spec = fg.PackingSpec(300)
+    g = fg.build_packing(spec)
+    _PLANS[g] = DevicePlan(g)
+    st = fg.init_state(g, seed=3)
+    s = copy(st)
+    so = copy(st)
+    e = 7                                # an edge of the first collision factor
+    for rho in (1.0, 2.0, 1.0):
+        g.set_edge_params(e, rho, 1.0)
+        fg.run(g, fg.RunConfig(max_iterations=3), state=s)
+        so, _h, _ = O.run(g, 3, so)
+    for k in "xmzun":
+        np.testing.assert_array_equal(getattr(s, k), getattr(so, k), err_msg=k)
+
+
+@pytest.mark.parametrize("env", [{}, {"FGADMM_DYN_LOOP": "1"}])
+def test_mpc_dynamics_forms_match_oracle(gpu, env, monkeypatch):
+    """mpc_dyn: matrix form (uniform weights, K = I - W^-1 M^T S^-1 M) and
+    the per-factor staged form both within the fp64 gate of the oracle."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    from paper_1603_02526_b200.engine import DevicePlan, _PLANS
+    gd = golden("mpc16x4_T50.npz")
+    g = fg.build_mpc(fg.MpcSpec(300, fg.LinearSystem(gd["A"], gd["B"]), gd["q0"]))
+    _PLANS[g] = DevicePlan(g)
+    st = fg.init_state(g, seed=2)
+    s = copy(st)
+    fg.run(g, fg.RunConfig(max_iterations=12), state=s)
+    so, _h, _ = O.run(g, 12, st)
+    for k in "xmzun":
+        assert_close(getattr(s, k), getattr(so, k), what=k)
