@@ -24,6 +24,7 @@
 #include "fg_mpc.cuh"
 #include "fg_tma.cuh"
 #include "fg_chain.cuh"
+#include "fg_rows.cuh"
 
 using namespace fg;
 
@@ -249,6 +250,11 @@ struct fg_plan {
     bool no_fork = false;              // edge groups serialized on one stream (A/B)
     bool lunit[5] = {false, false, false, false, false};  // class-L rows of dim D: unit weights
     LExc* d_lexc[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // their exception edge
+    // class-L rows on 2-CTA clusters (unit-weight form, fg_rows.cuh)
+    Row2* d_row2[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    bool row2_ok[5] = {false, false, false, false, false};
+    size_t row2_smem[5] = {0, 0, 0, 0, 0};
+    bool no_row2 = false;
     unsigned* d_gcnt = nullptr;        // per giant component chunk counter
     unsigned* d_ucnt = nullptr;        // giant update CTA counter
     FusedReduce fr_next{nullptr, 0, 0, 0, nullptr};   // set by chain_rest
@@ -276,7 +282,7 @@ fg_plan::~fg_plan() {
                     d_llist, d_lprog, d_prog, d_glist, d_gchunks, d_gcomps,
                     d_gwork, d_csum, d_gz, d_part, d_res2, d_ctrl, d_hist, d_chain_xx,
                     d_chain_fnorm, d_flag, d_gcnt, d_ucnt, d_lexc[1], d_lexc[2], d_lexc[3],
-                    d_lexc[4],
+                    d_lexc[4], d_row2[1], d_row2[2], d_row2[3], d_row2[4],
                     d_cutg, d_send, d_recv};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -435,36 +441,44 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
             k_var_small_run<0, MODE><<<grid, 256, 0, st>>>(b, p->d_sruns, p->d_sblk[2], po);
             return true;
         case 3:
-            if (p->row256)
-                k_var_large_vec<1, MODE, 256><<<grid, 256, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po);
+            if (MODE == MODE_FUSED && p->lunit[1] && p->row2_ok[1] && !p->no_row2)
+                k_var_row2<1><<<2 * grid, kRowThreads, p->row2_smem[1], st>>>(b, p->d_row2[1], p->d_prog, p->d_lexc[1], po);
+            else if (p->row256)
+                k_var_large_vec<1, MODE, 256><<<grid, 256, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po, nullptr, p->row2_ok[1] ? po + grid : -1);
             else if (p->lunit[1])
-                k_var_large_vec<1, MODE, kLargeThreads, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po, p->d_lexc[1]);
+                k_var_large_vec<1, MODE, kLargeThreads, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po, p->d_lexc[1], p->row2_ok[1] ? po + grid : -1);
             else
-                k_var_large_vec<1, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po);
+                k_var_large_vec<1, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po, nullptr, p->row2_ok[1] ? po + grid : -1);
             return true;
         case 4:
-            if (p->row256)
-                k_var_large_vec<2, MODE, 256><<<grid, 256, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po);
+            if (MODE == MODE_FUSED && p->lunit[2] && p->row2_ok[2] && !p->no_row2)
+                k_var_row2<2><<<2 * grid, kRowThreads, p->row2_smem[2], st>>>(b, p->d_row2[2], p->d_prog, p->d_lexc[2], po);
+            else if (p->row256)
+                k_var_large_vec<2, MODE, 256><<<grid, 256, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po, nullptr, p->row2_ok[2] ? po + grid : -1);
             else if (p->lunit[2])
-                k_var_large_vec<2, MODE, kLargeThreads, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po, p->d_lexc[2]);
+                k_var_large_vec<2, MODE, kLargeThreads, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po, p->d_lexc[2], p->row2_ok[2] ? po + grid : -1);
             else
-                k_var_large_vec<2, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po);
+                k_var_large_vec<2, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po, nullptr, p->row2_ok[2] ? po + grid : -1);
             return true;
         case 5:
-            if (p->row256)
-                k_var_large_vec<3, MODE, 256><<<grid, 256, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po);
+            if (MODE == MODE_FUSED && p->lunit[3] && p->row2_ok[3] && !p->no_row2)
+                k_var_row2<3><<<2 * grid, kRowThreads, p->row2_smem[3], st>>>(b, p->d_row2[3], p->d_prog, p->d_lexc[3], po);
+            else if (p->row256)
+                k_var_large_vec<3, MODE, 256><<<grid, 256, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po, nullptr, p->row2_ok[3] ? po + grid : -1);
             else if (p->lunit[3])
-                k_var_large_vec<3, MODE, kLargeThreads, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po, p->d_lexc[3]);
+                k_var_large_vec<3, MODE, kLargeThreads, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po, p->d_lexc[3], p->row2_ok[3] ? po + grid : -1);
             else
-                k_var_large_vec<3, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po);
+                k_var_large_vec<3, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po, nullptr, p->row2_ok[3] ? po + grid : -1);
             return true;
         case 6:
-            if (p->row256)
-                k_var_large_vec<4, MODE, 256><<<grid, 256, 0, st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, po);
+            if (MODE == MODE_FUSED && p->lunit[4] && p->row2_ok[4] && !p->no_row2)
+                k_var_row2<4><<<2 * grid, kRowThreads, p->row2_smem[4], st>>>(b, p->d_row2[4], p->d_prog, p->d_lexc[4], po);
+            else if (p->row256)
+                k_var_large_vec<4, MODE, 256><<<grid, 256, 0, st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, po, nullptr, p->row2_ok[4] ? po + grid : -1);
             else if (p->lunit[4])
-                k_var_large_vec<4, MODE, kLargeThreads, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, po, p->d_lexc[4]);
+                k_var_large_vec<4, MODE, kLargeThreads, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, po, p->d_lexc[4], p->row2_ok[4] ? po + grid : -1);
             else
-                k_var_large_vec<4, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, po);
+                k_var_large_vec<4, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, po, nullptr, p->row2_ok[4] ? po + grid : -1);
             return true;
         case 7:
             k_var_large<MODE><<<grid, kVarThreads, 0, st>>>(b, p->d_llist, p->d_lprog, p->d_prog, po);
@@ -1196,6 +1210,9 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     // ---- variable-pass classes and tree programs ----
     std::vector<int32_t> llist, lprog, glist, prog;
     std::vector<int32_t> lvars[5], lvprog[5];
+    std::vector<Row2> row2[5];
+    int64_t row2_ne[5] = {0, 0, 0, 0, 0};
+    bool row2_short[5] = {false, false, false, false, false};
     std::vector<SRun> sruns;
     std::vector<SBlock> sblk[3];
     std::vector<GChunk> gchunks;
@@ -1281,6 +1298,15 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
             lvars[dim[v]].push_back((int32_t)v);
             lvprog[dim[v]].push_back(leaf_prog(dg - 1));
             nlarge += dim[v];
+            // the root's two subtrees (NumPy split h = m/2 - (m/2)%8)
+            const int64_t m = dg - 1;
+            if (m > kLeafMax) {
+                const int64_t h = m / 2 - (m / 2) % kUnroll;
+                row2[dim[v]].push_back(Row2{(int32_t)v, leaf_prog(h), leaf_prog(m - h), (int32_t)h});
+                row2_ne[dim[v]] = std::max(row2_ne[dim[v]], std::max<int64_t>(1 + h, m - h));
+            } else {
+                row2_short[dim[v]] = true;
+            }
         } else {
             for (int64_t c = 0; c < dim[v]; ++c) {
                 const int32_t k = (int32_t)(zbase[v] + c);
@@ -1363,6 +1389,23 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
         }
     }
     for (int d = 1; d <= 4; ++d) p->nlv[d] = (int64_t)lvars[d].size();
+    p->no_row2 = getenv("FGADMM_NO_ROW2") != nullptr;
+    for (int d = 1; d <= 4; ++d) {
+        if (p->nlv[d] == 0 || row2_short[d]) continue;
+        const size_t smem = 2 * (size_t)((row2_ne[d] * d + 3) & ~int64_t(1)) * sizeof(double);
+        if (smem > (size_t)kMaxDynSmem - 8 * 1024) continue;
+        if ((rc = upload(&p->d_row2[d], row2[d]))) return rc;
+        p->row2_smem[d] = smem;
+        cudaError_t e = cudaSuccess;
+        switch (d) {
+            case 1: e = cudaFuncSetAttribute(k_var_row2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
+            case 2: e = cudaFuncSetAttribute(k_var_row2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
+            case 3: e = cudaFuncSetAttribute(k_var_row2<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
+            case 4: e = cudaFuncSetAttribute(k_var_row2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
+        }
+        if (e != cudaSuccess) return fail(FG_ERR_CUDA, "row cluster kernel shared-memory attribute");
+        p->row2_ok[d] = true;
+    }
     p->gtop_smem = (int)(2 * max_top * sizeof(double));
     p->giant_fused = getenv("FGADMM_GIANT_UNFUSED") == nullptr;
     p->row256 = getenv("FGADMM_ROW256") != nullptr;
@@ -1429,6 +1472,8 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
         p->part_off[w] = acc_part;
         if (w == kSlotGiantChunks || w == kSlotGiantTop) continue;   // no partials
         acc_part += var_slot_blocks(p.get(), w);
+        // class-L rows may run on 2-CTA clusters: two partial slots per row
+        if (w >= 3 && w <= 6 && p->row2_ok[w - 2]) acc_part += var_slot_blocks(p.get(), w);
     }
     p->npart = acc_part;
     const int64_t nres = nblk(E, 256);

@@ -1,0 +1,203 @@
+// Class-L rows (packing: one row of ~5,000 edges per disk variable) on a
+// 2-CTA cluster, unit-weight form.
+//
+// The reduceat segment of a row is a[0] + pairwise(a[1:]), and NumPy's
+// pairwise tree splits its root at h = n/2 - (n/2)%8: the root is exactly
+// pairwise(left h items) + pairwise(right n-h items).  CTA rank 0 of the
+// cluster owns element 0 and the left subtree, rank 1 the right subtree:
+//   1. one elected thread bulk-copies (cp.async.bulk, SASS UBLKCP) the CTA's
+//      x and u range into shared memory -- all bytes in flight at once;
+//   2. leaf sums from shared memory (8 lanes per leaf, NumPy's 8
+//      accumulators and xor butterfly), then the subtree's level-ordered
+//      top on warp 0;
+//   3. the two subtree sums are exchanged through distributed shared
+//      memory (one cluster barrier); both CTAs form the same z;
+//   4. each CTA updates u of its range from shared memory.
+// Every payload value crosses HBM once per iteration (x, u read; u
+// written); the two CTAs of a row and the second CTA on the SM overlap
+// their load, tree and update phases.  Same arithmetic order as
+// k_var_large_vec, so bitwise equal to it.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "fg_tma.cuh"
+
+namespace fg {
+
+constexpr int kRowThreads = 256;
+
+// Per row: the two subtree programs and the split.
+struct Row2 { int32_t var, prog_l, prog_r, h; };
+
+template <int D>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kRowThreads, 2)
+k_var_row2(PassB b, const Row2* rows, const int32_t* prog, const LExc* exc, int64_t part_off) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(16) double row_smem[];
+    __shared__ double sv[D][2 * kMaxUnits];
+    __shared__ double sm[2 * (kRowThreads / 32)];
+    __shared__ double s_half[2][D];                    // [rank][c] subtree sums
+    __shared__ __align__(8) uint64_t s_bar;
+    const int rank = (int)cluster.block_rank();
+    if (b.ctrl->stop) return;                           // uniform over the grid
+    const int64_t it = b.ctrl->iter;
+    const Row2 R = rows[blockIdx.x >> 1];
+    const int32_t v = R.var;
+    const int64_t pb = b.vt.pbase[v];
+    const int64_t zb = b.vt.zbase[v];
+    const int deg = b.vt.deg[v];
+    const LExc xe = exc[blockIdx.x >> 1];
+    // element ranges: rank 0 owns [0, 1 + h) (element 0 + left subtree),
+    // rank 1 owns [1 + h, deg)
+    const int64_t e_lo = rank == 0 ? 0 : 1 + (int64_t)R.h;
+    const int64_t e_hi = rank == 0 ? 1 + (int64_t)R.h : deg;
+    const int64_t ne = e_hi - e_lo;
+    const Span sx = span16(pb + e_lo * D, pb + e_hi * D);
+    double* xs = row_smem;                              // aligned span of x
+    double* us = row_smem + ((sx.n + 1) & ~int64_t(1));
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned bytes = (unsigned)(sx.n * 8);
+        mbar_expect_tx(&s_bar, 2 * bytes);
+        bulk_g2s(xs, b.x + sx.lo, bytes, &s_bar);
+        bulk_g2s(us, b.uin + sx.lo, bytes, &s_bar);
+    }
+    // what z needs besides the tree: element 0 (m checked by rank 0, whose
+    // range holds it), z weights, previous z
+    double a0[D], zw0[D], zo0[D];
+    bool bm = false, bu = false;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            const double m0 = b.x[pb + c] + b.uin[pb + c];
+            if (rank == 0) bm |= !finite(m0);
+            a0[c] = xe.rank == 0 ? m0 * xe.rho : m0;
+            zw0[c] = b.zw[zb + c];
+            zo0[c] = b.zin[zb + c];
+        }
+    }
+    mbar_wait(&s_bar, 0);
+    const double* xr = xs + sx.off;                     // element e at (e - e_lo) * D
+    const double* ur = us + sx.off;
+    auto mval = [&](int64_t e, int c) {                 // (x + u) * rho of element e
+        const int64_t q = (e - e_lo) * D + c;
+        const double m = xr[q] + ur[q];
+        bm |= !finite(m);
+        return e == xe.rank ? m * xe.rho : m;
+    };
+    // ---- leaf sums of this CTA's subtree (elements from 1 + base) ----
+    const int32_t* P = prog + (rank == 0 ? R.prog_l : R.prog_r);
+    const int64_t base = rank == 0 ? 1 : 1 + (int64_t)R.h;
+    const int nu = P[0], nlev = P[1];
+    const int32_t* units = P + 2;
+    const int32_t* lev = units + 2 * nu;
+    const int32_t* ops = lev + nlev;
+    const int g = threadIdx.x >> 3, j = threadIdx.x & 7;
+    constexpr int NG = kRowThreads / 8;
+    for (int r0 = 0; r0 < nu; r0 += NG) {
+        const int L = r0 + g;
+        int64_t s = 0, len = 0;
+        if (L < nu) { s = units[2 * L]; len = units[2 * L + 1]; }
+        const int64_t e0 = base + s;
+        const bool small = len < kUnroll;
+        const int64_t top = len - len % kUnroll;
+        double acc[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) acc[c] = 0.0;
+        if (small) {
+            if (j == 0)
+                for (int64_t i = 0; i < len; ++i)
+#pragma unroll
+                    for (int c = 0; c < D; ++c) acc[c] += mval(e0 + i, c);
+        } else {
+#pragma unroll
+            for (int c = 0; c < D; ++c) acc[c] = mval(e0 + j, c);
+            for (int64_t i = kUnroll; i < top; i += kUnroll)
+#pragma unroll
+                for (int c = 0; c < D; ++c) acc[c] += mval(e0 + i + j, c);
+        }
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            double bsum = acc[c] + __shfl_xor_sync(kFull, acc[c], 1);
+            bsum = bsum + __shfl_xor_sync(kFull, bsum, 2);
+            bsum = bsum + __shfl_xor_sync(kFull, bsum, 4);
+            if (!small) acc[c] = bsum;
+        }
+        if (!small && j == 0)
+            for (int64_t i = top; i < len; ++i)
+#pragma unroll
+                for (int c = 0; c < D; ++c) acc[c] += mval(e0 + i, c);
+        if (L < nu && j == 0) {
+#pragma unroll
+            for (int c = 0; c < D; ++c) sv[c][L] = acc[c];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {                             // subtree top on warp 0
+        int node = nu, op = 0;
+        for (int l = 0; l < nlev; ++l) {
+            const int cnt = lev[l];
+            for (int o = threadIdx.x; o < cnt * D; o += 32) {
+                const int c = o / cnt, oo = o - c * cnt;
+                sv[c][node + oo] = sv[c][ops[2 * (op + oo)]] + sv[c][ops[2 * (op + oo) + 1]];
+            }
+            __syncwarp();
+            node += cnt;
+            op += cnt;
+        }
+        if (threadIdx.x < D) {                          // publish to both CTAs
+            const double hs = sv[threadIdx.x][node - 1];
+            s_half[rank][threadIdx.x] = hs;
+            double* peer = cluster.map_shared_rank(&s_half[0][0], rank ^ 1);
+            peer[rank * D + threadIdx.x] = hs;
+        }
+    }
+    cluster.sync();                                     // both subtree sums landed
+    __shared__ double s_z[2][D];
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            const double T = s_half[0][c] + s_half[1][c];   // the root: left + right
+            const double zn = ddiv(a0[c] + T, zw0[c]);
+            s_z[0][c] = zn;
+            s_z[1][c] = zo0[c];
+            if (rank == 0) {
+                b.z[zb + c] = zn;
+                if (!finite(zn)) flag_error(b.ctrl, it, FG_PHASE_Z, false);
+            }
+        }
+    }
+    __syncthreads();
+    // ---- u update of this CTA's range from shared memory ----
+    double zn[D], dz[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) { zn[c] = s_z[0][c]; dz[c] = zn[c] - s_z[1][c]; }
+    double pp = 0.0, dd = 0.0;
+    for (int64_t q = threadIdx.x; q < ne * D; q += kRowThreads) {
+        const int64_t e = e_lo + q / D;
+        const int c = (int)(q - (e - e_lo) * D);
+        const bool ex = e == xe.rank;
+        const double t = xr[q] - zn[c];
+        pp += t * t;
+        const double rd = ex ? xe.rho * dz[c] : dz[c];
+        dd += rd * rd;
+        const double un = ur[q] + (ex ? t * xe.alpha : t);
+        b.uout[pb + e * D + c] = un;
+        bu |= !finite(un);
+    }
+    if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
+    if (bu) flag_error(b.ctrl, it, FG_PHASE_U, false);
+    block_sum2<kRowThreads>(pp, dd, sm);
+    if (threadIdx.x == 0) {
+        b.part[2 * (part_off + blockIdx.x)] = pp;
+        b.part[2 * (part_off + blockIdx.x) + 1] = dd;
+    }
+}
+
+}  // namespace fg

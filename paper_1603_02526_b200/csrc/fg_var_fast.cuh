@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(256, 4) k_var_small_run(PassB b, const SRun* r
 template <int D, int MODE, int NT = kLargeThreads, bool UNIT = false>
 __global__ void __launch_bounds__(NT, 1024 / NT) k_var_large_vec(
     PassB b, const int32_t* vlist, const int32_t* progoff, const int32_t* prog,
-    int64_t part_off, const LExc* exc = nullptr) {
+    int64_t part_off, const LExc* exc = nullptr, int64_t zero_off = -1) {
     __shared__ double sv[D][2 * kMaxUnits];
     __shared__ double sm[2 * (NT / 32)];
     __shared__ double s_z[2][D];
@@ -311,6 +311,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_var_large_vec(
         if (threadIdx.x == 0) {
             b.part[2 * (part_off + blockIdx.x)] = pp;
             b.part[2 * (part_off + blockIdx.x) + 1] = dd;
+            if (zero_off >= 0) {          // slots reserved for the cluster form
+                b.part[2 * (zero_off + blockIdx.x)] = 0.0;
+                b.part[2 * (zero_off + blockIdx.x) + 1] = 0.0;
+            }
         }
     }
 }

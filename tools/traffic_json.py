@@ -15,7 +15,7 @@ LABELS = {
     "edge_collision": "void k_collision_tiles_v3",
     "var_large_d1": "void k_var_large_vec<1,",
     "var_large_d2": "void k_var_large_vec<2,",
-    "edge_mpc_dyn": "void k_mpc_dyn8",
+    "edge_mpc_dyn": "void k_mpc_dyn_gemm",
     "var_small_deg4": "void k_var_small_run<4,",
     "var_giant_chunks": "void k_var_giant_chunks",
 }
