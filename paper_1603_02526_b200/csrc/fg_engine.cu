@@ -1389,7 +1389,9 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
         }
     }
     for (int d = 1; d <= 4; ++d) p->nlv[d] = (int64_t)lvars[d].size();
-    p->no_row2 = getenv("FGADMM_NO_ROW2") != nullptr;
+    // measured slower than the one-CTA unit rows (pack N=5000: d1 0.257 vs
+    // 0.192 ms, d2 0.335 vs 0.328 ms; profiles/r01_rows_ab.md): opt-in
+    p->no_row2 = getenv("FGADMM_ROW2") == nullptr;
     for (int d = 1; d <= 4; ++d) {
         if (p->nlv[d] == 0 || row2_short[d]) continue;
         const size_t smem = 2 * (size_t)((row2_ne[d] * d + 3) & ~int64_t(1)) * sizeof(double);
