@@ -321,6 +321,27 @@ def multi_gpu(args, fg, dist, rank, world, local):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     value = E * args.steps / (ms / 1e3)
+    # end to end through the public per-rank API: scatter this rank's part
+    # of the host state, run, download the rank's state (wall clock, max
+    # over ranks)
+    lg = nr.local
+    ls = [np.empty(lg.total_edge_payload) for _ in range(4)]
+    lz = np.empty(lg.z_dim)
+    dist.barrier()
+    t0 = time.perf_counter()
+    nr.upload(st)
+    nr.run(args.steps)
+    nr.plan.download(x=ls[0], m=ls[1], z=lz, u=ls[2], n=ls[3])
+    e2e_s = torch.tensor([time.perf_counter() - t0], device="cuda")
+    dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    P_all = torch.tensor([lg.total_edge_payload, lg.z_dim], device="cuda", dtype=torch.float64)
+    dist.all_reduce(P_all)
+    P_tot, Z_tot = float(P_all[0].item()), float(P_all[1].item())
+    e2e = {"value": E * args.steps / float(e2e_s.item()), "unit": UNIT,
+           "h2d_bytes_per_step": int((Z_tot + 2 * P_tot) * 8 // args.steps),
+           "d2h_bytes_per_step": int((4 * P_tot + Z_tot) * 8 // args.steps),
+           "note": "per rank: upload its part of z,u,n, run, download its x,m,z,u,n; "
+                   "max over ranks of the wall clock"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -332,6 +353,10 @@ def multi_gpu(args, fg, dist, rank, world, local):
                    "local_edges": len(nr.local.edge_var), "build_seconds": round(t_build, 2)},
         "gpu_launches": int(res.launches), "clocks": clk.summary(),
         "converged": bool(res.converged),
+        "e2e": e2e,
+        "roofline": None, "cpu_baseline": None,
+        "note": "roofline and the CPU baseline are reported by the one-GPU line",
+        "chain_form": nr.plan.chain_form(),
     }
     if rank == 0:
         print(json.dumps(line))
@@ -347,6 +372,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="svm1m", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partition", action="store_true",
+                    help="take the multi-GPU (NCCL partition) path even at one rank")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
@@ -356,14 +383,14 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     os.environ["FGADMM_DEVICE"] = str(local)
     dist = None
-    if world > 1:
+    if world > 1 or args.partition:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
 
     import paper_1603_02526_b200 as fg
-    if world > 1:
+    if world > 1 or args.partition:
         return multi_gpu(args, fg, dist, rank, world, local)
     t_build = time.perf_counter()
     g, st, info = build_instance(args.workload)
