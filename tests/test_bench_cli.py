@@ -1,0 +1,35 @@
+"""The GPU backend of the reference's `fgadmm bench` (bench_cli): parser,
+exit codes and CSV schema on CPU; one real sweep on the GPU."""
+
+import numpy as np
+import pytest
+
+from paper_1603_02526_b200 import bench_cli
+
+
+def test_csv_schema_matches_reference_header():
+    r = bench_cli.BenchResult("pack", 10, 1, 5, {p: 0.001 for p in "xmzun"}, 0.1, 1.0)
+    text = bench_cli.bench_csv([r])
+    lines = text.strip().split("\n")
+    assert lines[0] == ("problem,size,workers,iters,t_x,t_m,t_z,t_u,t_n,total,"
+                        "time_per_iter,speedup")
+    cells = lines[1].split(",")
+    assert len(cells) == 12 and cells[:4] == ["pack", "10", "1", "5"]
+    assert float(cells[10]) == pytest.approx(0.005)
+
+
+@pytest.mark.parametrize("argv,code", [(["pack"], 2), (["pack", "--k", "3"], 2),
+                                       (["mpc", "--n", "3"], 2), (["bogus"], 1),
+                                       (["pack", "--n", "x"], 1)])
+def test_usage_and_error_exit_codes(argv, code, capsys):
+    assert bench_cli.main(argv) == code
+
+
+@pytest.mark.gpu
+def test_gpu_bench_sweep(gpu, capsys):
+    assert bench_cli.main(["pack", "--n", "20,40", "--workers", "1,2", "--iters", "20"]) == 0
+    out = capsys.readouterr().out.strip().split("\n")
+    assert len(out) == 5
+    rows = [line.split(",") for line in out[1:]]
+    assert all(int(r[3]) == 20 for r in rows)
+    assert all(float(r[10]) > 0.0 and np.isfinite(float(r[11])) for r in rows)
