@@ -255,6 +255,12 @@ struct fg_plan {
     bool row2_ok[5] = {false, false, false, false, false};
     size_t row2_smem[5] = {0, 0, 0, 0, 0};
     bool no_row2 = false;
+    bool row_deep = false;             // deeper u-update batches in unit rows (A/B)
+    // class-L rows through a TMA ring (unit-weight form, fg_rows.cuh)
+    int32_t* d_planoff[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    int32_t* d_plans = nullptr;
+    bool pipe_ok[5] = {false, false, false, false, false};
+    bool no_pipe = false;
     unsigned* d_gcnt = nullptr;        // per giant component chunk counter
     unsigned* d_ucnt = nullptr;        // giant update CTA counter
     FusedReduce fr_next{nullptr, 0, 0, 0, nullptr};   // set by chain_rest
@@ -283,6 +289,7 @@ fg_plan::~fg_plan() {
                     d_gwork, d_csum, d_gz, d_part, d_res2, d_ctrl, d_hist, d_chain_xx,
                     d_chain_fnorm, d_flag, d_gcnt, d_ucnt, d_lexc[1], d_lexc[2], d_lexc[3],
                     d_lexc[4], d_row2[1], d_row2[2], d_row2[3], d_row2[4],
+                    d_planoff[1], d_planoff[2], d_planoff[3], d_planoff[4], d_plans,
                     d_cutg, d_send, d_recv};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -441,40 +448,56 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
             k_var_small_run<0, MODE><<<grid, 256, 0, st>>>(b, p->d_sruns, p->d_sblk[2], po);
             return true;
         case 3:
-            if (MODE == MODE_FUSED && p->lunit[1] && p->row2_ok[1] && !p->no_row2)
+            if (MODE == MODE_FUSED && p->lunit[1] && p->pipe_ok[1] && !p->no_pipe)
+                k_var_row_pipe<1><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, p->d_planoff[1], p->d_plans, p->d_lexc[1], po);
+            else if (MODE == MODE_FUSED && p->lunit[1] && p->row2_ok[1] && !p->no_row2)
                 k_var_row2<1><<<2 * grid, kRowThreads, p->row2_smem[1], st>>>(b, p->d_row2[1], p->d_prog, p->d_lexc[1], po);
             else if (p->row256)
                 k_var_large_vec<1, MODE, 256><<<grid, 256, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po, nullptr, p->row2_ok[1] ? po + grid : -1);
+            else if (p->lunit[1] && p->row_deep)
+                k_var_large_vec<1, MODE, kLargeThreads, true, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po, p->d_lexc[1], p->row2_ok[1] ? po + grid : -1);
             else if (p->lunit[1])
                 k_var_large_vec<1, MODE, kLargeThreads, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po, p->d_lexc[1], p->row2_ok[1] ? po + grid : -1);
             else
                 k_var_large_vec<1, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po, nullptr, p->row2_ok[1] ? po + grid : -1);
             return true;
         case 4:
-            if (MODE == MODE_FUSED && p->lunit[2] && p->row2_ok[2] && !p->no_row2)
+            if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe)
+                k_var_row_pipe<2><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, p->d_planoff[2], p->d_plans, p->d_lexc[2], po);
+            else if (MODE == MODE_FUSED && p->lunit[2] && p->row2_ok[2] && !p->no_row2)
                 k_var_row2<2><<<2 * grid, kRowThreads, p->row2_smem[2], st>>>(b, p->d_row2[2], p->d_prog, p->d_lexc[2], po);
             else if (p->row256)
                 k_var_large_vec<2, MODE, 256><<<grid, 256, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po, nullptr, p->row2_ok[2] ? po + grid : -1);
+            else if (p->lunit[2] && p->row_deep)
+                k_var_large_vec<2, MODE, kLargeThreads, true, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po, p->d_lexc[2], p->row2_ok[2] ? po + grid : -1);
             else if (p->lunit[2])
                 k_var_large_vec<2, MODE, kLargeThreads, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po, p->d_lexc[2], p->row2_ok[2] ? po + grid : -1);
             else
                 k_var_large_vec<2, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po, nullptr, p->row2_ok[2] ? po + grid : -1);
             return true;
         case 5:
-            if (MODE == MODE_FUSED && p->lunit[3] && p->row2_ok[3] && !p->no_row2)
+            if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe)
+                k_var_row_pipe<3><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, p->d_planoff[3], p->d_plans, p->d_lexc[3], po);
+            else if (MODE == MODE_FUSED && p->lunit[3] && p->row2_ok[3] && !p->no_row2)
                 k_var_row2<3><<<2 * grid, kRowThreads, p->row2_smem[3], st>>>(b, p->d_row2[3], p->d_prog, p->d_lexc[3], po);
             else if (p->row256)
                 k_var_large_vec<3, MODE, 256><<<grid, 256, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po, nullptr, p->row2_ok[3] ? po + grid : -1);
+            else if (p->lunit[3] && p->row_deep)
+                k_var_large_vec<3, MODE, kLargeThreads, true, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po, p->d_lexc[3], p->row2_ok[3] ? po + grid : -1);
             else if (p->lunit[3])
                 k_var_large_vec<3, MODE, kLargeThreads, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po, p->d_lexc[3], p->row2_ok[3] ? po + grid : -1);
             else
                 k_var_large_vec<3, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po, nullptr, p->row2_ok[3] ? po + grid : -1);
             return true;
         case 6:
-            if (MODE == MODE_FUSED && p->lunit[4] && p->row2_ok[4] && !p->no_row2)
+            if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe)
+                k_var_row_pipe<4><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, p->d_planoff[4], p->d_plans, p->d_lexc[4], po);
+            else if (MODE == MODE_FUSED && p->lunit[4] && p->row2_ok[4] && !p->no_row2)
                 k_var_row2<4><<<2 * grid, kRowThreads, p->row2_smem[4], st>>>(b, p->d_row2[4], p->d_prog, p->d_lexc[4], po);
             else if (p->row256)
                 k_var_large_vec<4, MODE, 256><<<grid, 256, 0, st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, po, nullptr, p->row2_ok[4] ? po + grid : -1);
+            else if (p->lunit[4] && p->row_deep)
+                k_var_large_vec<4, MODE, kLargeThreads, true, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, po, p->d_lexc[4], p->row2_ok[4] ? po + grid : -1);
             else if (p->lunit[4])
                 k_var_large_vec<4, MODE, kLargeThreads, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, po, p->d_lexc[4], p->row2_ok[4] ? po + grid : -1);
             else
@@ -1392,6 +1415,53 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     // measured slower than the one-CTA unit rows (pack N=5000: d1 0.257 vs
     // 0.192 ms, d2 0.335 vs 0.328 ms; profiles/r01_rows_ab.md): opt-in
     p->no_row2 = getenv("FGADMM_ROW2") == nullptr;
+    p->no_pipe = getenv("FGADMM_NO_PIPE") != nullptr;
+    {   // TMA-ring row plans, one per distinct degree and dim
+        std::vector<int32_t> plans;
+        std::map<std::pair<int64_t, int>, int32_t> plan_of;
+        for (int d = 1; d <= 4; ++d) {
+            if (p->nlv[d] == 0) continue;
+            const int64_t CH = kPipeStageDoubles / d;
+            std::vector<int32_t> offs;
+            bool ok = true;
+            for (size_t r = 0; r < lvars[d].size() && ok; ++r) {
+                const int64_t dg = deg[lvars[d][r]];
+                auto key = std::make_pair(dg, d);
+                auto itp = plan_of.find(key);
+                if (itp != plan_of.end()) { offs.push_back(itp->second); continue; }
+                const int32_t* P = prog.data() + lvprog[d][r];
+                const int nu = P[0];
+                const int32_t* units = P + 2;
+                std::vector<int32_t> ch;
+                for (int L = 0; L < nu;) {
+                    const int64_t lo = 1 + units[2 * L];
+                    int L1 = L + 1;
+                    while (L1 < nu && 1 + units[2 * L1] + units[2 * L1 + 1] - lo <= CH) ++L1;
+                    const int64_t hi = 1 + units[2 * (L1 - 1)] + units[2 * (L1 - 1) + 1];
+                    if (hi - lo > CH) ok = false;
+                    ch.insert(ch.end(), {(int32_t)lo, (int32_t)hi, L, L1});
+                    L = L1;
+                }
+                const int32_t off = (int32_t)plans.size();
+                plans.push_back((int32_t)(ch.size() / 4));
+                plans.push_back((int32_t)((dg + CH - 1) / CH));
+                plans.push_back((int32_t)CH);
+                plans.insert(plans.end(), ch.begin(), ch.end());
+                plan_of[key] = off;
+                offs.push_back(off);
+            }
+            if (!ok) continue;
+            if ((rc = upload(&p->d_planoff[d], offs))) return rc;
+            p->pipe_ok[d] = true;
+        }
+        if (!plans.empty() && (rc = upload(&p->d_plans, plans))) return rc;
+        const int smem = (int)row_pipe_smem();
+        CK(cudaFuncSetAttribute(k_var_row_pipe<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CK(cudaFuncSetAttribute(k_var_row_pipe<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CK(cudaFuncSetAttribute(k_var_row_pipe<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CK(cudaFuncSetAttribute(k_var_row_pipe<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    }
+    p->row_deep = getenv("FGADMM_ROW_DEEP") != nullptr;
     for (int d = 1; d <= 4; ++d) {
         if (p->nlv[d] == 0 || row2_short[d]) continue;
         const size_t smem = 2 * (size_t)((row2_ne[d] * d + 3) & ~int64_t(1)) * sizeof(double);

@@ -200,4 +200,204 @@ k_var_row2(PassB b, const Row2* rows, const int32_t* prog, const LExc* exc, int6
     }
 }
 
+// ---------------------------------------------------------------------------
+// Class-L rows, unit-weight form, one CTA per row with a TMA ring.
+//
+// The row is streamed through NS shared-memory stages as a sequence of
+// jobs: phase-1 chunks (consecutive whole leaves of the reduceat tree,
+// <= CH elements) then phase-2 chunks (CH consecutive elements).  One
+// elected thread issues the two bulk copies (x, u) of a job into a free
+// stage; consumers wait on the stage's mbarrier.  The phase-2 copies of
+// the first NS chunks are issued while phase 1 ends and warp 0 evaluates
+// the top of the tree and z, so the load stream never stops: NS stages of
+// up to 2 x 10 KB are in flight per CTA.  Same arithmetic order as
+// k_var_large_vec (unit form): bitwise equal.
+//
+// Row plan (int32, per distinct degree): J1, J2, CH, then J1 x (elo, ehi,
+// leaf_lo, leaf_hi) for the phase-1 chunks; phase-2 chunk k is elements
+// [k*CH, min(deg, (k+1)*CH)).
+constexpr int kPipeStages = 3;
+constexpr int kPipeStageDoubles = 1280;             // per array per stage
+
+template <int D>
+__global__ void __launch_bounds__(kRowThreads, 3)
+k_var_row_pipe(PassB b, const int32_t* vlist, const int32_t* progoff, const int32_t* prog,
+               const int32_t* planoff, const int32_t* plans, const LExc* exc,
+               int64_t part_off) {
+    extern __shared__ __align__(16) double pipe_smem[];
+    __shared__ double sv[D][2 * kMaxUnits];
+    __shared__ double sm[2 * (kRowThreads / 32)];
+    __shared__ double s_z[2][D];
+    __shared__ __align__(8) uint64_t full[kPipeStages];
+    if (b.ctrl->stop) return;
+    const int64_t it = b.ctrl->iter;
+    const int32_t v = vlist[blockIdx.x];
+    const int64_t pb = b.vt.pbase[v];
+    const int64_t zb = b.vt.zbase[v];
+    const int deg = b.vt.deg[v];
+    const LExc xe = exc[blockIdx.x];
+    const int32_t* PL = plans + planoff[blockIdx.x];
+    const int J1 = PL[0], J2 = PL[1], CH = PL[2];
+    const int32_t* chunks = PL + 3;
+    const int NJ = J1 + J2;
+    constexpr int SD = kPipeStageDoubles + 4;           // array slot (span slack)
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kPipeStages; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    auto job_range = [&](int j, int64_t& lo, int64_t& hi) {
+        if (j < J1) { lo = chunks[4 * j]; hi = chunks[4 * j + 1]; }
+        else { lo = (int64_t)(j - J1) * CH; hi = lo + CH < (int64_t)deg ? lo + CH : (int64_t)deg; }
+    };
+    auto issue = [&](int j, int s) {
+        int64_t lo, hi;
+        job_range(j, lo, hi);
+        const Span sx = span16(pb + lo * D, pb + hi * D);
+        double* base = pipe_smem + (int64_t)s * 2 * SD;
+        const unsigned bytes = (unsigned)(sx.n * 8);
+        mbar_expect_tx(&full[s], 2 * bytes);
+        bulk_g2s(base, b.x + sx.lo, bytes, &full[s]);
+        bulk_g2s(base + SD, b.uin + sx.lo, bytes, &full[s]);
+    };
+    if (threadIdx.x == 0)
+        for (int k = 0; k < kPipeStages && k < NJ; ++k) issue(k, k);
+    // z needs element 0 (the reduceat initial value), z weights, previous z
+    double a0[D], zw0[D], zo0[D];
+    bool bm = false, bu = false;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            const double m0 = b.x[pb + c] + b.uin[pb + c];
+            bm |= !finite(m0);
+            a0[c] = xe.rank == 0 ? m0 * xe.rho : m0;
+            zw0[c] = b.zw[zb + c];
+            zo0[c] = b.zin[zb + c];
+        }
+    }
+    const int32_t* P = prog + progoff[blockIdx.x];
+    const int nu = P[0], nlev = P[1];
+    const int32_t* units = P + 2;
+    const int32_t* lev = units + 2 * nu;
+    const int32_t* ops = lev + nlev;
+    const int g = threadIdx.x >> 3, j8 = threadIdx.x & 7;
+    constexpr int NG = kRowThreads / 8;
+    double zn[D], dz[D];
+    double pp = 0.0, dd = 0.0;
+    for (int j = 0; j < NJ; ++j) {
+        const int s = j % kPipeStages;
+        if (j == J1) {
+            // all leaf sums are in: top of the tree on warp 0, z on thread 0
+            __syncthreads();
+            if (threadIdx.x < 32) {
+                int node = nu, op = 0;
+                for (int l = 0; l < nlev; ++l) {
+                    const int cnt = lev[l];
+                    for (int o = threadIdx.x; o < cnt * D; o += 32) {
+                        const int c = o / cnt, oo = o - c * cnt;
+                        sv[c][node + oo] = sv[c][ops[2 * (op + oo)]] + sv[c][ops[2 * (op + oo) + 1]];
+                    }
+                    __syncwarp();
+                    node += cnt;
+                    op += cnt;
+                }
+                if (threadIdx.x == 0) {
+#pragma unroll
+                    for (int c = 0; c < D; ++c) {
+                        const double z = ddiv(a0[c] + sv[c][node - 1], zw0[c]);
+                        s_z[0][c] = z;
+                        s_z[1][c] = zo0[c];
+                        b.z[zb + c] = z;
+                        if (!finite(z)) flag_error(b.ctrl, it, FG_PHASE_Z, false);
+                    }
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int c = 0; c < D; ++c) { zn[c] = s_z[0][c]; dz[c] = zn[c] - s_z[1][c]; }
+        }
+        mbar_wait(&full[s], (unsigned)((j / kPipeStages) & 1));
+        int64_t lo, hi;
+        job_range(j, lo, hi);
+        const Span sx = span16(pb + lo * D, pb + hi * D);
+        const double* X = pipe_smem + (int64_t)s * 2 * SD + sx.off;
+        const double* U = X + SD;
+        if (j < J1) {
+            // leaves [L0, L1) of this chunk; leaf elements are 1 + unit start
+            const int L0 = chunks[4 * j + 2], L1 = chunks[4 * j + 3];
+            auto mval = [&](int64_t e, int c) {
+                const int64_t q = (e - lo) * D + c;
+                const double m = X[q] + U[q];
+                bm |= !finite(m);
+                return e == xe.rank ? m * xe.rho : m;
+            };
+            for (int L = L0 + g; L < L1; L += NG) {
+                const int64_t e0 = 1 + (int64_t)units[2 * L], len = units[2 * L + 1];
+                const bool small = len < kUnroll;
+                const int64_t top = len - len % kUnroll;
+                double acc[D];
+#pragma unroll
+                for (int c = 0; c < D; ++c) acc[c] = 0.0;
+                if (small) {
+                    if (j8 == 0)
+                        for (int64_t i = 0; i < len; ++i)
+#pragma unroll
+                            for (int c = 0; c < D; ++c) acc[c] += mval(e0 + i, c);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < D; ++c) acc[c] = mval(e0 + j8, c);
+                    for (int64_t i = kUnroll; i < top; i += kUnroll)
+#pragma unroll
+                        for (int c = 0; c < D; ++c) acc[c] += mval(e0 + i + j8, c);
+                }
+                // leaf groups are warp-aligned octets: the butterfly stays
+                // inside the group (all 8 lanes take the same branch)
+                const unsigned gmask = 0xFFu << (threadIdx.x & 24);
+#pragma unroll
+                for (int c = 0; c < D; ++c) {
+                    double bs = acc[c] + __shfl_xor_sync(gmask, acc[c], 1);
+                    bs = bs + __shfl_xor_sync(gmask, bs, 2);
+                    bs = bs + __shfl_xor_sync(gmask, bs, 4);
+                    if (!small) acc[c] = bs;
+                }
+                if (!small && j8 == 0)
+                    for (int64_t i = top; i < len; ++i)
+#pragma unroll
+                        for (int c = 0; c < D; ++c) acc[c] += mval(e0 + i, c);
+                if (j8 == 0) {
+#pragma unroll
+                    for (int c = 0; c < D; ++c) sv[c][L] = acc[c];
+                }
+            }
+        } else {
+            const int64_t nq = (hi - lo) * D;
+            for (int64_t q = threadIdx.x; q < nq; q += kRowThreads) {
+                const int64_t e = lo + q / D;
+                const int c = (int)(q - (e - lo) * D);
+                const bool ex = e == xe.rank;
+                const double t = X[q] - zn[c];
+                pp += t * t;
+                const double rd = ex ? xe.rho * dz[c] : dz[c];
+                dd += rd * rd;
+                const double un = U[q] + (ex ? t * xe.alpha : t);
+                b.uout[pb + lo * D + q] = un;
+                bu |= !finite(un);
+            }
+        }
+        __syncthreads();                               // stage s consumed
+        if (threadIdx.x == 0 && j + kPipeStages < NJ) issue(j + kPipeStages, s);
+    }
+    if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
+    if (bu) flag_error(b.ctrl, it, FG_PHASE_U, false);
+    block_sum2<kRowThreads>(pp, dd, sm);
+    if (threadIdx.x == 0) {
+        b.part[2 * (part_off + blockIdx.x)] = pp;
+        b.part[2 * (part_off + blockIdx.x) + 1] = dd;
+    }
+}
+
+inline size_t row_pipe_smem() {
+    return (size_t)kPipeStages * 2 * (kPipeStageDoubles + 4) * sizeof(double);
+}
+
 }  // namespace fg

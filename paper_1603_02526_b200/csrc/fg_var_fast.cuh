@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(256, 4) k_var_small_run(PassB b, const SRun* r
 // rank and weights in the row's LExc, k_unit_rows; rank -1 for none).
 // UNIT: rows in unit-weight form: every other weight is exactly 1, and
 // m*1, rho*dz and t*1 are exact identities, so no rho/alpha loads.
-template <int D, int MODE, int NT = kLargeThreads, bool UNIT = false>
+template <int D, int MODE, int NT = kLargeThreads, bool UNIT = false, bool DEEP = false>
 __global__ void __launch_bounds__(NT, 1024 / NT) k_var_large_vec(
     PassB b, const int32_t* vlist, const int32_t* progoff, const int32_t* prog,
     int64_t part_off, const LExc* exc = nullptr, int64_t zero_off = -1) {
@@ -272,7 +272,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_var_large_vec(
         // batches of kUB elements per thread: all loads of a batch are issued
         // before its stores (the compiler cannot prove uout aliases nothing
         // read here), one memory round trip per batch
-        constexpr int kUB = D == 1 ? 4 : 2;
+        constexpr int kUB = UNIT ? (DEEP ? (D == 1 ? 6 : (D == 2 ? 3 : 2)) : (D == 1 ? 4 : 2))
+                                 : (D == 1 ? 4 : 2);
         for (int64_t e0 = threadIdx.x; e0 < deg; e0 += kUB * NT) {
             double xr[kUB][D], ur[kUB][D], rr[kUB], ar[kUB];
 #pragma unroll
