@@ -350,7 +350,7 @@ void launch_kind(const GroupDev& g, const PassA& a, cudaStream_t st) {
         case FG_KIND_MPC_DYN:
             if (g.dyn_gemm)
                 k_mpc_dyn_gemm<FIRST><<<(unsigned)g.nblocks, T,
-                                        mpc_dyn_gemm_smem(g.dim[0] + g.ip), st>>>(a, g);
+                                        mpc_dyn_gemm_smem(g.dim[0], g.ip), st>>>(a, g);
             else
                 k_mpc_dyn8<FIRST><<<grid, T, mpc_dyn8_smem(g.tstride, g.dim[0] + g.ip, g.ip,
                                                            g.fsys == nullptr), st>>>(a, g);

@@ -107,9 +107,10 @@ inline size_t mpc_dyn8_smem(int tstride, int cols, int d, bool shared_tab) {
 constexpr int kDynGemmF = 128;                      // factors per CTA (one run block)
 constexpr int kDynGemmMaxCols = 40;
 
-__host__ __device__ inline size_t mpc_dyn_gemm_smem(int cols) {
-    return ((size_t)cols * kDynGemmMaxCols + 2 * (size_t)kDynGemmF * (cols + 1)) *
-           sizeof(double);
+__host__ __device__ inline size_t mpc_dyn_gemm_smem(int n0, int d) {
+    const size_t cols = (size_t)(n0 + d);
+    return (cols * kDynGemmMaxCols + (size_t)kDynGemmF * (cols + 1) +
+            (size_t)kDynGemmF * (2 * n0 + 1)) * sizeof(double);
 }
 
 template <bool FIRST>
@@ -117,10 +118,10 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_dyn_gemm(PassA a, Group
     extern __shared__ double gsm[];
     if (a.ctrl->stop) return;
     const int64_t it = a.ctrl->iter;
-    const int n0 = g.dim[0], d = g.ip, cols = n0 + d, ld = cols + 1;
+    const int n0 = g.dim[0], d = g.ip, cols = n0 + d, ld = cols + 1, ldo = 2 * n0 + 1;
     double* Ks = gsm;                                   // [cols][cols]
     double* nvs = Ks + cols * kDynGemmMaxCols;          // [F][ld]
-    double* outs = nvs + kDynGemmF * ld;                // [F][ld]
+    double* outs = nvs + kDynGemmF * ld;                // [F][2 n0 + 1]: x of both slots
     const BlockRef bk = g.blocks[blockIdx.x];
     const RunHdr h = g.runs[bk.run];
     const SlotRun* sr = g.sruns + (int64_t)bk.run * g.nslots;
@@ -135,17 +136,29 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_dyn_gemm(PassA a, Group
         Ks[(c * 2 + (r & 1)) * KH + (r >> 1)] = g.kmat[i];
     }
     // stage n: factor f's slot 0 (n0 values) and slot 1 (n0 values, the
-    // first d enter the projection, the rest pass through to x)
+    // first d enter the projection, the rest pass through to x).  The
+    // addresses are affine in the factor (run mode), and the loop holds no
+    // global store, so its loads pipeline.
+    const SlotRun R0 = sr[0], R1 = sr[1];
+    const double* __restrict__ src = FIRST ? a.nsrc : a.uin;
+    const double* __restrict__ zz = a.z;
     const int per = 2 * n0;
     for (int idx = threadIdx.x; idx < nf * per; idx += blockDim.x) {
         const int f = idx / per, c = idx - f * per;
         const int j = c < n0 ? 0 : 1, cc = c - j * n0;
-        FRef r{h.f0 + fl0 + f, fl0 + f, sr};
-        const SlotLoc s = locate(a.vt, g, j, r);
-        const double n = nval<FIRST>(a, s, cc, bn);
+        const SlotRun& RR = j ? R1 : R0;
+        const int64_t fl = fl0 + f;
+        const int64_t pos = RR.pos0 + fl * RR.pos_s + cc;
+        double n;
+        if (FIRST) {
+            n = src[pos];
+        } else {
+            n = zz[RR.z0 + fl * RR.z_s + cc] - src[pos];
+            bn |= !finite(n);
+        }
         if (j == 0) nvs[f * ld + cc] = n;
         else if (cc < d) nvs[f * ld + n0 + cc] = n;
-        else xput(a, s.pos + cc, n, bx);                  // control of t+1
+        else outs[f * ldo + n0 + cc] = n;                  // control of t+1 passes
     }
     __syncthreads();
     // out[f][r] = sum_c K[r][c] nv[f][c]: thread -> factor f, rows r0 + 2k
@@ -171,17 +184,19 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_dyn_gemm(PassA a, Group
 #pragma unroll
             for (int k = 0; k < kDynGemmMaxCols / 2; ++k) {
                 const int r = r0 + 2 * k;
-                if (r < cols) outs[f * ld + r] = acc[k];
+                if (r < cols) outs[f * ldo + r] = acc[k];
             }
         }
     }
     __syncthreads();
-    for (int idx = threadIdx.x; idx < nf * cols; idx += blockDim.x) {
-        const int f = idx / cols, c = idx - f * cols;
+    double* __restrict__ xo = a.x;
+    for (int idx = threadIdx.x; idx < nf * per; idx += blockDim.x) {
+        const int f = idx / per, c = idx - f * per;
         const int j = c < n0 ? 0 : 1, cc = c - j * n0;
-        FRef r{h.f0 + fl0 + f, fl0 + f, sr};
-        const SlotLoc s = locate(a.vt, g, j, r);
-        xput(a, s.pos + cc, outs[f * ld + c], bx);
+        const SlotRun& RR = j ? R1 : R0;
+        const double v = outs[f * ldo + c];
+        xo[RR.pos0 + (fl0 + f) * RR.pos_s + cc] = v;
+        bx |= !finite(v);
     }
     passa_flags<FIRST>(a, it, bn, bx);
 }

@@ -338,12 +338,31 @@ k_var_row_pipe(PassB b, const int32_t* vlist, const int32_t* progoff, const int3
                 double acc[D];
 #pragma unroll
                 for (int c = 0; c < D; ++c) acc[c] = 0.0;
-                if (small) {
+                const bool exl = xe.rank >= e0 && xe.rank < e0 + len;
+                if (!small && !exl) {
+                    // fast path: fixed strides from shared memory; a finite
+                    // accumulator proves every m finite (NaN/inf propagate),
+                    // only a non-finite one pays for the per-value check
+                    const double* xp = X + (e0 + j8 - lo) * D;
+                    const double* up = U + (e0 + j8 - lo) * D;
+#pragma unroll
+                    for (int c = 0; c < D; ++c) acc[c] = xp[c] + up[c];
+                    const int nst = (int)(top / kUnroll);
+                    for (int i = 1; i < nst; ++i)
+#pragma unroll
+                        for (int c = 0; c < D; ++c)
+                            acc[c] += xp[i * kUnroll * D + c] + up[i * kUnroll * D + c];
+#pragma unroll
+                    for (int c = 0; c < D; ++c)
+                        if (!finite(acc[c]))
+                            for (int i = 0; i < nst; ++i)
+                                bm |= !finite(xp[i * kUnroll * D + c] + up[i * kUnroll * D + c]);
+                } else if (small) {
                     if (j8 == 0)
                         for (int64_t i = 0; i < len; ++i)
 #pragma unroll
                             for (int c = 0; c < D; ++c) acc[c] += mval(e0 + i, c);
-                } else {
+                } else {                                   // leaf with the exception edge
 #pragma unroll
                     for (int c = 0; c < D; ++c) acc[c] = mval(e0 + j8, c);
                     for (int64_t i = kUnroll; i < top; i += kUnroll)
