@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <array>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -261,6 +262,9 @@ struct fg_plan {
     int32_t* d_plans = nullptr;
     bool pipe_ok[5] = {false, false, false, false, false};
     bool no_pipe = false;
+    // 2 stages of twice the size: measured better for dim >= 2 rows (pack
+    // center rows 0.285 vs 0.306 ms), worse for dim 1 (0.176 vs 0.160)
+    bool pipe_big[5] = {false, false, true, true, true};
     unsigned* d_gcnt = nullptr;        // per giant component chunk counter
     unsigned* d_ucnt = nullptr;        // giant update CTA counter
     FusedReduce fr_next{nullptr, 0, 0, 0, nullptr};   // set by chain_rest
@@ -448,7 +452,9 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
             k_var_small_run<0, MODE><<<grid, 256, 0, st>>>(b, p->d_sruns, p->d_sblk[2], po);
             return true;
         case 3:
-            if (MODE == MODE_FUSED && p->lunit[1] && p->pipe_ok[1] && !p->no_pipe)
+            if (MODE == MODE_FUSED && p->lunit[1] && p->pipe_ok[1] && !p->no_pipe && p->pipe_big[1])
+                k_var_row_pipe<1, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, p->d_planoff[1], p->d_plans, p->d_lexc[1], po);
+            else if (MODE == MODE_FUSED && p->lunit[1] && p->pipe_ok[1] && !p->no_pipe)
                 k_var_row_pipe<1><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, p->d_planoff[1], p->d_plans, p->d_lexc[1], po);
             else if (MODE == MODE_FUSED && p->lunit[1] && p->row2_ok[1] && !p->no_row2)
                 k_var_row2<1><<<2 * grid, kRowThreads, p->row2_smem[1], st>>>(b, p->d_row2[1], p->d_prog, p->d_lexc[1], po);
@@ -462,7 +468,9 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
                 k_var_large_vec<1, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po, nullptr, p->row2_ok[1] ? po + grid : -1);
             return true;
         case 4:
-            if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe)
+            if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe && p->pipe_big[2])
+                k_var_row_pipe<2, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, p->d_planoff[2], p->d_plans, p->d_lexc[2], po);
+            else if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe)
                 k_var_row_pipe<2><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, p->d_planoff[2], p->d_plans, p->d_lexc[2], po);
             else if (MODE == MODE_FUSED && p->lunit[2] && p->row2_ok[2] && !p->no_row2)
                 k_var_row2<2><<<2 * grid, kRowThreads, p->row2_smem[2], st>>>(b, p->d_row2[2], p->d_prog, p->d_lexc[2], po);
@@ -476,7 +484,9 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
                 k_var_large_vec<2, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po, nullptr, p->row2_ok[2] ? po + grid : -1);
             return true;
         case 5:
-            if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe)
+            if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe && p->pipe_big[3])
+                k_var_row_pipe<3, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, p->d_planoff[3], p->d_plans, p->d_lexc[3], po);
+            else if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe)
                 k_var_row_pipe<3><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, p->d_planoff[3], p->d_plans, p->d_lexc[3], po);
             else if (MODE == MODE_FUSED && p->lunit[3] && p->row2_ok[3] && !p->no_row2)
                 k_var_row2<3><<<2 * grid, kRowThreads, p->row2_smem[3], st>>>(b, p->d_row2[3], p->d_prog, p->d_lexc[3], po);
@@ -490,7 +500,9 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
                 k_var_large_vec<3, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po, nullptr, p->row2_ok[3] ? po + grid : -1);
             return true;
         case 6:
-            if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe)
+            if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe && p->pipe_big[4])
+                k_var_row_pipe<4, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, p->d_planoff[4], p->d_plans, p->d_lexc[4], po);
+            else if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe)
                 k_var_row_pipe<4><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, p->d_planoff[4], p->d_plans, p->d_lexc[4], po);
             else if (MODE == MODE_FUSED && p->lunit[4] && p->row2_ok[4] && !p->no_row2)
                 k_var_row2<4><<<2 * grid, kRowThreads, p->row2_smem[4], st>>>(b, p->d_row2[4], p->d_prog, p->d_lexc[4], po);
@@ -1416,12 +1428,14 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     // 0.192 ms, d2 0.335 vs 0.328 ms; profiles/r01_rows_ab.md): opt-in
     p->no_row2 = getenv("FGADMM_ROW2") == nullptr;
     p->no_pipe = getenv("FGADMM_NO_PIPE") != nullptr;
+    if (getenv("FGADMM_PIPE_BIG"))
+        for (int d = 1; d <= 4; ++d) p->pipe_big[d] = std::atoi(getenv("FGADMM_PIPE_BIG")) != 0;
     {   // TMA-ring row plans, one per distinct degree and dim
         std::vector<int32_t> plans;
         std::map<std::pair<int64_t, int>, int32_t> plan_of;
         for (int d = 1; d <= 4; ++d) {
             if (p->nlv[d] == 0) continue;
-            const int64_t CH = kPipeStageDoubles / d;
+            const int64_t CH = (p->pipe_big[d] ? 2 * kPipeStageDoubles : kPipeStageDoubles) / d;
             std::vector<int32_t> offs;
             bool ok = true;
             for (size_t r = 0; r < lvars[d].size() && ok; ++r) {
@@ -1460,6 +1474,11 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
         CK(cudaFuncSetAttribute(k_var_row_pipe<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         CK(cudaFuncSetAttribute(k_var_row_pipe<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         CK(cudaFuncSetAttribute(k_var_row_pipe<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        const int smem2 = (int)row_pipe_smem(2, 2 * kPipeStageDoubles);
+        CK(cudaFuncSetAttribute(k_var_row_pipe<1, 2, 2 * kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+        CK(cudaFuncSetAttribute(k_var_row_pipe<2, 2, 2 * kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+        CK(cudaFuncSetAttribute(k_var_row_pipe<3, 2, 2 * kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+        CK(cudaFuncSetAttribute(k_var_row_pipe<4, 2, 2 * kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
     }
     p->row_deep = getenv("FGADMM_ROW_DEEP") != nullptr;
     for (int d = 1; d <= 4; ++d) {

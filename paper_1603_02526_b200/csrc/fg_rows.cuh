@@ -219,8 +219,8 @@ k_var_row2(PassB b, const Row2* rows, const int32_t* prog, const LExc* exc, int6
 constexpr int kPipeStages = 3;
 constexpr int kPipeStageDoubles = 1280;             // per array per stage
 
-template <int D>
-__global__ void __launch_bounds__(kRowThreads, 3)
+template <int D, int NS = kPipeStages, int SDB = kPipeStageDoubles>
+__global__ void __launch_bounds__(kRowThreads, NS == 3 ? 3 : 2)
 k_var_row_pipe(PassB b, const int32_t* vlist, const int32_t* progoff, const int32_t* prog,
                const int32_t* planoff, const int32_t* plans, const LExc* exc,
                int64_t part_off) {
@@ -228,7 +228,7 @@ k_var_row_pipe(PassB b, const int32_t* vlist, const int32_t* progoff, const int3
     __shared__ double sv[D][2 * kMaxUnits];
     __shared__ double sm[2 * (kRowThreads / 32)];
     __shared__ double s_z[2][D];
-    __shared__ __align__(8) uint64_t full[kPipeStages];
+    __shared__ __align__(8) uint64_t full[NS];
     if (b.ctrl->stop) return;
     const int64_t it = b.ctrl->iter;
     const int32_t v = vlist[blockIdx.x];
@@ -240,9 +240,9 @@ k_var_row_pipe(PassB b, const int32_t* vlist, const int32_t* progoff, const int3
     const int J1 = PL[0], J2 = PL[1], CH = PL[2];
     const int32_t* chunks = PL + 3;
     const int NJ = J1 + J2;
-    constexpr int SD = kPipeStageDoubles + 4;           // array slot (span slack)
+    constexpr int SD = SDB + 4;           // array slot (span slack)
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kPipeStages; ++s) mbar_init(&full[s], 1);
+        for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
@@ -261,7 +261,7 @@ k_var_row_pipe(PassB b, const int32_t* vlist, const int32_t* progoff, const int3
         bulk_g2s(base + SD, b.uin + sx.lo, bytes, &full[s]);
     };
     if (threadIdx.x == 0)
-        for (int k = 0; k < kPipeStages && k < NJ; ++k) issue(k, k);
+        for (int k = 0; k < NS && k < NJ; ++k) issue(k, k);
     // z needs element 0 (the reduceat initial value), z weights, previous z
     double a0[D], zw0[D], zo0[D];
     bool bm = false, bu = false;
@@ -285,7 +285,7 @@ k_var_row_pipe(PassB b, const int32_t* vlist, const int32_t* progoff, const int3
     double zn[D], dz[D];
     double pp = 0.0, dd = 0.0;
     for (int j = 0; j < NJ; ++j) {
-        const int s = j % kPipeStages;
+        const int s = j % NS;
         if (j == J1) {
             // all leaf sums are in: top of the tree on warp 0, z on thread 0
             __syncthreads();
@@ -316,7 +316,7 @@ k_var_row_pipe(PassB b, const int32_t* vlist, const int32_t* progoff, const int3
 #pragma unroll
             for (int c = 0; c < D; ++c) { zn[c] = s_z[0][c]; dz[c] = zn[c] - s_z[1][c]; }
         }
-        mbar_wait(&full[s], (unsigned)((j / kPipeStages) & 1));
+        mbar_wait(&full[s], (unsigned)((j / NS) & 1));
         int64_t lo, hi;
         job_range(j, lo, hi);
         const Span sx = span16(pb + lo * D, pb + hi * D);
@@ -404,7 +404,7 @@ k_var_row_pipe(PassB b, const int32_t* vlist, const int32_t* progoff, const int3
             }
         }
         __syncthreads();                               // stage s consumed
-        if (threadIdx.x == 0 && j + kPipeStages < NJ) issue(j + kPipeStages, s);
+        if (threadIdx.x == 0 && j + NS < NJ) issue(j + NS, s);
     }
     if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
     if (bu) flag_error(b.ctrl, it, FG_PHASE_U, false);
@@ -415,8 +415,8 @@ k_var_row_pipe(PassB b, const int32_t* vlist, const int32_t* progoff, const int3
     }
 }
 
-inline size_t row_pipe_smem() {
-    return (size_t)kPipeStages * 2 * (kPipeStageDoubles + 4) * sizeof(double);
+inline size_t row_pipe_smem(int ns = kPipeStages, int sdb = kPipeStageDoubles) {
+    return (size_t)ns * 2 * (sdb + 4) * sizeof(double);
 }
 
 }  // namespace fg

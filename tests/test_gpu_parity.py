@@ -261,7 +261,8 @@ def test_packing_1030_cluster_and_tile_kernels_bitwise(gpu):
                                  {"FGADMM_NO_UNIT": "1"}, {"FGADMM_NO_FORK": "1"},
                                  {"FGADMM_ROW256": "1"}, {"FGADMM_GIANT_UNFUSED": "1"},
                                  {"FGADMM_ROW2": "1", "FGADMM_NO_PIPE": "1"},
-                                 {"FGADMM_NO_PIPE": "1"}])
+                                 {"FGADMM_NO_PIPE": "1"}, {"FGADMM_PIPE_BIG": "0"},
+                                 {"FGADMM_PIPE_BIG": "1"}])
 def test_opt_in_kernel_variants_match_oracle(gpu, env, monkeypatch):
     """The alternative kernels selected at plan creation (TMA bulk-copy
     pipeline for small segments, 4-CTA DSMEM cluster rows, cp.async

@@ -13,8 +13,8 @@ import sys
 LABELS = {
     "chain_svm": "void k_svm_chain_unit",
     "edge_collision": "void k_collision_tiles_v3",
-    "var_large_d1": "void k_var_large_vec<1,",
-    "var_large_d2": "void k_var_large_vec<2,",
+    "var_large_d1": "void k_var_row_pipe<1",
+    "var_large_d2": "void k_var_row_pipe<2",
     "edge_mpc_dyn": "void k_mpc_dyn_gemm",
     "var_small_deg4": "void k_var_small_run<4,",
     "var_giant_chunks": "void k_var_giant_chunks",
