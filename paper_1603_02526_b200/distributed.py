@@ -92,19 +92,53 @@ class LocalGroup:
         return out, res, hist.reshape(-1, 2)[:res.iterations]
 
 
+def group_run_locals(graphs, iterations, device=None):
+    """Run already-partitioned rank graphs (e.g. ``svm_rank_graph``) as a
+    local group on one device from their zero states; returns the per-rank
+    downloaded states and the run result.  The validation path of the
+    weak-scaled multi-GPU benchmark."""
+    plans = [DevicePlan(lg, device=device) for lg in graphs]
+    for lg, plan in zip(graphs, plans):
+        plan.sync(lg)
+        st = init_state(lg)
+        plan.upload(st.z, st.u, st.n)
+    cfg = _native.RunConfig()
+    cfg.max_iterations = int(iterations)
+    cfg.first_reads_n = 1
+    res = _native.RunResult()
+    hist = np.zeros(2 * int(iterations))
+    handles = (C.c_void_p * len(plans))(*[p._h.value for p in plans])
+    _native.check(_native.load().fg_group_run(handles, len(plans), C.byref(cfg),
+                                              _native.dptr(hist), C.byref(res)))
+    outs = []
+    for lg, plan in zip(graphs, plans):
+        ls = AdmmState(*(np.empty(lg.total_edge_payload) for _ in range(2)), np.empty(lg.z_dim),
+                       *(np.empty(lg.total_edge_payload) for _ in range(2)))
+        plan.download(x=ls.x, m=ls.m, z=ls.z, u=ls.u, n=ls.n)
+        outs.append(ls)
+    return outs, res, plans
+
+
 class NcclRank:
     """This process's partition plan of ``graph``, exchanging over NCCL.
 
     ``group`` is an initialised ``torch.distributed`` process group (any
     backend); it carries the NCCL unique id and host-side gathers only.
+    ``local`` (instead of ``graph``) is an already-built rank graph with
+    ``cut_index`` / ``ncut`` (``partition.svm_rank_graph``): no global
+    graph is built on the host.
     """
 
-    def __init__(self, graph, rank, world, group=None, device=None):
+    def __init__(self, graph, rank, world, group=None, device=None, local=None):
         import torch.distributed as dist
         self.graph = graph
         self.rank, self.world = int(rank), int(world)
-        self.part = Partition(graph, world)
-        self.local = self.part.local(self.rank)
+        if local is None:
+            self.part = Partition(graph, world)
+            self.local = self.part.local(self.rank)
+        else:
+            self.part = None
+            self.local = local
         self.plan = DevicePlan(self.local, device=device)
         lib = _native.load()
         path = nccl_library()
@@ -120,9 +154,10 @@ class NcclRank:
         self._group = group
 
     def upload(self, state):
+        """``state``: the global state, or (rank graphs) this rank's own."""
         lg = self.local
         self.plan.sync(lg)
-        ls = _scatter_local(lg, state)
+        ls = _scatter_local(lg, state) if self.part is not None else state
         self.plan.upload(ls.z, ls.u, ls.n)
 
     def run(self, iterations, primal_tol=0.0, dual_tol=0.0, graph_chunk=16):

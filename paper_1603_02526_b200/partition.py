@@ -287,3 +287,79 @@ def local_weight_check(lg):
     full = np.repeat(w, np.diff(lg.var_offsets))
     cut = np.repeat(lg.var_cut, np.diff(lg.var_offsets))
     return np.array_equal(full[~cut], lg.z_weights[~cut])
+
+
+def svm_rank_graph(X, y, rank, world, lam=1.0, rho=1.0, alpha=1.0):
+    """One rank's part of the SVM chain over the points of ALL ranks, built
+    directly from this rank's points ``(X, y)`` (no global graph on the
+    host: a weak-scaled run of world x n points fits where the global
+    graph would not).
+
+    It equals ``Partition(build_svm(...), world).local(rank)`` for the
+    global SVM whose points are the ranks' blocks in rank order: the same
+    local variables (this rank's w_i, the next rank's first weight copy as
+    a cut variable with one equality edge, the bias, this rank's xi_i), the
+    same factors in the same order, GLOBAL ``z_weights``, and the canonical
+    cut vector ``[w of rank 1's first point (D), ..., w of rank G-1's
+    (D), bias]``.  Every rank must hold the same number of points.
+    """
+    from .problems import SvmSpec, build_svm
+    from ._pairwise import pairwise_sum
+    X = np.asarray(X, dtype=np.float64)
+    n, D = X.shape
+    first, last = rank == 0, rank == world - 1
+    N = n * world
+    from .graph import GraphBuilder
+    from .operators import Equality, SvmMargin, SvmNorm, SvmSlack
+    spec = SvmSpec.from_arrays(X, y, lam=lam, rho=rho, alpha=alpha)
+    Xs, ys = spec.arrays()
+    b = GraphBuilder()
+    w = b.declare_variables(D, n)
+    wx = None if last else b.declare_variable(D)           # next rank's first w
+    bias = b.declare_variable(1)
+    xi = b.declare_variables(1, n)
+    b.add_factors(SvmNorm, w[:, None], rho=rho, alpha=alpha,
+                  params={"scale": np.full(n, 1.0 / N)}, slot_dims=(D,))
+    b.add_factors(SvmSlack, xi[:, None], rho=rho, alpha=alpha,
+                  params={"lam": np.full(n, float(lam))}, slot_dims=(1,))
+    b.add_factors(SvmMargin, np.stack([w, np.full(n, bias), xi], axis=1), rho=rho,
+                  alpha=alpha, params={"x": Xs, "y": ys}, slot_dims=(D, 1, 1))
+    right = w[1:] if last else np.append(w[1:], wx)
+    left = w[:-1] if last else w
+    if len(left):
+        b.add_factors(Equality, np.stack([left, right], axis=1), rho=rho, alpha=alpha,
+                      slot_dims=(D, D))
+    g = b.freeze()
+    # global weights: sum of rho over the variable's incident edges of the
+    # whole chain, in NumPy's pairwise order (graph.py:216-222)
+    def wsum(deg):
+        return float(pairwise_sum(np.full(deg, float(rho))))
+    zw = np.array(g.z_weights, copy=True)
+    dims = np.diff(np.asarray(g.var_offsets))
+    def set_w(v, total):
+        zw[g.var_offsets[v]:g.var_offsets[v] + dims[v]] = total
+    w_end = wsum(3) if world * n > 1 else wsum(2)
+    for i in range(n):
+        deg = 4
+        if first and i == 0:
+            deg -= 1
+        if last and i == n - 1:
+            deg -= 1
+        set_w(int(w[i]), wsum(deg))
+    if wx is not None:
+        set_w(int(wx), wsum(3 if rank + 1 == world - 1 and n == 1 else 4))
+    set_w(int(bias), wsum(N))
+    del w_end
+    g.z_weights = zw
+    # canonical cut vector positions
+    cut = np.full(g.z_dim, -1, dtype=np.int64)
+    ncut = (world - 1) * D + 1
+    if world > 1:
+        if not first:
+            cut[g.var_offsets[int(w[0])]:g.var_offsets[int(w[0])] + D] = (rank - 1) * D + np.arange(D)
+        if wx is not None:
+            cut[g.var_offsets[int(wx)]:g.var_offsets[int(wx)] + D] = rank * D + np.arange(D)
+        cut[g.var_offsets[int(bias)]] = (world - 1) * D
+    g.cut_index = cut
+    g.ncut = ncut if world > 1 else 0
+    return g

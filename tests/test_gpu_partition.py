@@ -94,3 +94,28 @@ def test_svm_partition_runs_fused_chain_bitwise_vs_per_kind(gpu, monkeypatch, wo
     fg.run(g, fg.RunConfig(max_iterations=12), state=single)
     for k in "xmzun":
         assert _close(getattr(outs[0][0], k), getattr(single, k)), k
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_svm_rank_graphs_match_single_plan(gpu, world):
+    """Weak-scaled multi-GPU path: rank graphs built directly from each
+    rank's points (partition.svm_rank_graph), run as a group with the cut
+    exchange, agree with one plan of the concatenated SVM (1e-9)."""
+    from paper_1603_02526_b200.distributed import group_run_locals
+    from paper_1603_02526_b200.partition import svm_rank_graph
+    n, D = 700, 32
+    Xs, ys = zip(*[fg.gen_gaussian_arrays(n, D, 4.0, seed=10 + r) for r in range(world)])
+    g = fg.build_svm(fg.SvmSpec.from_arrays(np.concatenate(Xs), np.concatenate(ys)))
+    single = fg.init_state(g)
+    fg.run(g, fg.RunConfig(max_iterations=10), state=single)
+    graphs = [svm_rank_graph(Xs[r], ys[r], r, world) for r in range(world)]
+    outs, res, plans = group_run_locals(graphs, 10)
+    assert res.iterations == 10 and res.error_phase == -1
+    assert all(p.chain_form() in ("unit", "fast") for p in plans)
+    N = n * world
+    for r, ls in enumerate(outs):
+        wz = ls.z[:n * D]
+        assert _close(wz, single.z[r * n * D:(r + 1) * n * D]), r
+        nb = n * D + (0 if r == world - 1 else D)
+        assert _close(ls.z[nb:nb + 1], single.z[N * D:N * D + 1])
+        assert _close(ls.z[nb + 1:], single.z[N * D + 1 + r * n:N * D + 1 + (r + 1) * n])

@@ -160,3 +160,26 @@ def test_gloo_world2_partitioned_svm_matches_single(tmp_path):
     for k in "xmzun":
         np.testing.assert_allclose(full[k], getattr(ref, k), rtol=1e-11, atol=1e-13)
     np.testing.assert_allclose(res["hist"], np.array(ref_hist), rtol=1e-10)
+
+
+def test_svm_rank_graph_equals_partition_local():
+    """The per-rank SVM builder (weak-scaled multi-GPU runs) emits exactly
+    the partitioner's local graph when the partition splits at the ranks'
+    point blocks (world 2, equal blocks)."""
+    from paper_1603_02526_b200.partition import Partition, svm_rank_graph
+    n, world = 1200, 2
+    Xs, ys = zip(*[fg.gen_gaussian_arrays(n, 32, 4.0, seed=r) for r in range(world)])
+    g = fg.build_svm(fg.SvmSpec.from_arrays(np.concatenate(Xs), np.concatenate(ys)))
+    part = Partition(g, world)
+    for r in range(world):
+        lg, rg = part.local(r), svm_rank_graph(Xs[r], ys[r], r, world)
+        for k in ("edge_var", "edge_offsets", "var_offsets", "edge_rho", "z_weights",
+                  "cut_index"):
+            np.testing.assert_array_equal(np.asarray(getattr(lg, k)), np.asarray(getattr(rg, k)),
+                                          err_msg=k)
+        assert lg.ncut == rg.ncut
+        for (c1, d1, _f1, v1, p1), (c2, d2, _f2, v2, p2) in zip(lg.blocks, rg.blocks):
+            assert c1.kind == c2.kind and tuple(d1) == tuple(d2)
+            np.testing.assert_array_equal(v1, v2)
+            for k in p1:
+                np.testing.assert_array_equal(np.asarray(p1[k]), np.asarray(p2[k]))
