@@ -301,15 +301,33 @@ def reference_arm(args):
 
 def multi_gpu(args, fg, dist, rank, world, local):
     """N ranks over NCCL: the graph is partitioned by factors (cut variables
-    all-gather their partial sums inside the iteration).  Strong scaling:
-    every N runs the same whole graph; value = its edges x K / max-rank time."""
+    all-gather their partial sums inside the iteration).
+
+    SVM: weak scaling -- every rank holds 1M points of a world x 1M-point
+    chain and builds only its own part (partition.svm_rank_graph; cut set:
+    the bias and one weight copy per rank boundary); value = all ranks'
+    edges x K / max-rank time.  Packing / MPC: strong scaling of the one
+    graph, partitioned by partition.Partition."""
     import torch
     from paper_1603_02526_b200.distributed import NcclRank
+    from paper_1603_02526_b200.partition import svm_rank_graph
     t_build = time.perf_counter()
-    g, st, info = build_instance(args.workload)
-    nr = NcclRank(g, rank, world, device=local)
+    weak = args.workload.startswith("svm")
+    if weak:
+        n = 1_000_000
+        X, y = fg.gen_gaussian_arrays(n, 32, 4.0, seed=rank)
+        lg = svm_rank_graph(X, y, rank, world, lam=1.0)
+        nr = NcclRank(None, rank, world, device=local, local=lg)
+        st = fg.init_state(lg)
+        info = {"points": n * world, "points_per_rank": n, "dim": 32, "init": "zeros"}
+        Et = torch.tensor([len(lg.edge_var)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(Et)
+        E = int(Et.item())
+    else:
+        g, st, info = build_instance(args.workload)
+        nr = NcclRank(g, rank, world, device=local)
+        E = len(g.edge_var)
     t_build = time.perf_counter() - t_build
-    E = len(g.edge_var)
     nr.upload(st)
     nr.run(args.warmup)
     nr.upload(st)
@@ -345,11 +363,11 @@ def multi_gpu(args, fg, dist, rank, world, local):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "weak" if weak else "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.workload, "desc": WORKLOADS[args.workload], **info,
                    "edges": E, "parallelism": f"factor partition x{world} (NCCL all-gather "
-                                              f"of {nr.part.ncut} cut components)",
+                                              f"of {getattr(nr.local, 'ncut', 0)} cut components)",
                    "local_edges": len(nr.local.edge_var), "build_seconds": round(t_build, 2)},
         "gpu_launches": int(res.launches), "clocks": clk.summary(),
         "converged": bool(res.converged),

@@ -183,3 +183,51 @@ def test_svm_rank_graph_equals_partition_local():
             np.testing.assert_array_equal(v1, v2)
             for k in p1:
                 np.testing.assert_array_equal(np.asarray(p1[k]), np.asarray(p2[k]))
+
+
+def _gloo_rank_graph(rank, world, port, out_path, n):
+    import torch
+    import torch.distributed as dist
+    from paper_1603_02526_b200.partition import svm_rank_graph
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    X, y = fg.gen_gaussian_arrays(n, 8, 4.0, seed=20 + rank)
+    lg = svm_rank_graph(X, y, rank, world)          # no global graph on this rank
+    st = fg.init_state(lg, seed=None)
+    ls = O.State(*(np.array(getattr(st, k)) for k in "xmzun"))
+
+    def ag(vec):
+        t = torch.as_tensor(np.asarray(vec, dtype=np.float64))
+        outs = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(outs, t)
+        return [o.numpy() for o in outs]
+
+    s, hist = O.run_partitioned(lg, 10, ls, ag)
+    parts = [None] * world
+    dist.all_gather_object(parts, (rank, s.z, hist))
+    if rank == 0:
+        np.savez(out_path, **{f"z{r}": z for r, z, _h in parts}, hist=np.array(parts[0][2]))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_rank_graphs_match_single(tmp_path):
+    """Weak-scaled protocol over gloo: each process builds only its rank
+    graph from its own points; the exchanged run equals the single-process
+    oracle on the concatenated SVM."""
+    import torch.multiprocessing as mp
+    world, n = 2, 300
+    out = str(tmp_path / "rg.npz")
+    mp.spawn(_gloo_rank_graph, args=(world, _free_port(), out, n), nprocs=world, join=True)
+    Xs, ys = zip(*[fg.gen_gaussian_arrays(n, 8, 4.0, seed=20 + r) for r in range(world)])
+    g = fg.build_svm(fg.SvmSpec.from_arrays(np.concatenate(Xs), np.concatenate(ys)))
+    ref, ref_hist, _ = O.run(g, 10, fg.init_state(g))
+    res = np.load(out)
+    D, N = 8, n * world
+    for r in range(world):
+        z = res[f"z{r}"]
+        np.testing.assert_allclose(z[:n * D], ref.z[r * n * D:(r + 1) * n * D], rtol=1e-11,
+                                   atol=1e-13)
+        nb = n * D + (0 if r == world - 1 else D)
+        np.testing.assert_allclose(z[nb], ref.z[N * D], rtol=1e-11, atol=1e-13)
+    np.testing.assert_allclose(res["hist"], np.array(ref_hist), rtol=1e-10)
