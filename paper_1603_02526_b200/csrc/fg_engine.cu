@@ -53,6 +53,9 @@ constexpr int64_t kGiantWork = 2048; // elements per G3 CTA
 // items (one CTA each); smaller than the class-L limit so a degree-1M
 // segment spreads over ~1000 CTAs instead of ~128.
 constexpr int64_t kGiantChunk = 1024;
+// a chunk of <= 1024 items has ~8-16 leaves of 8 lanes each: 64-thread
+// CTAs (several resident per SM) instead of 256 threads mostly idle
+constexpr int kGiantChunkThreads = 64;
 // Dynamic shared-memory limit set on every kernel that uses it: the
 // attribute is per function, not per launch, so plans of different sizes
 // must not lower it under one another.
@@ -228,6 +231,11 @@ struct fg_plan {
     // fused SVM chain (fg_chain.cuh): replaces the edge pass and the small
     // variable classes from the second iteration of a run on
     bool chain_on = false;
+    bool mpc_chain = false;            // the fused iteration is the MPC chain (fg_mpc.cuh)
+    bool mpc_ok = false;               // build_mpc topology detected (unit weights checked at sync)
+    MpcChainDev mpc{};
+    int64_t mpc_tiles = 0;
+    size_t mpc_smem = 0;
     ChainDev chain{};
     int64_t chain_grid = 0;
     int chain_minb = 2;                // CTAs/SM the kernel is compiled for (A/B)
@@ -520,7 +528,7 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
             return true;
         case kSlotGiantChunks:
             if (p->giant_fused)
-                k_var_giant_chunks<MODE><<<grid, kVarThreads, p->gtop_smem, st>>>(
+                k_var_giant_chunks<MODE, kGiantChunkThreads><<<grid, kGiantChunkThreads, p->gtop_smem, st>>>(
                     b, p->d_glist, p->d_gchunks, p->d_prog, p->d_csum, p->d_gcomps, p->d_gz,
                     p->d_send, p->d_gcnt);
             else
@@ -645,6 +653,7 @@ void part_post(fg_plan* p, cudaStream_t st) {
 // kernels loop over their points), at most the partial slots it replaces
 // minus the end-point slot.
 int64_t chain_main_grid(const fg_plan* p) {
+    if (p->mpc_chain) return p->mpc_tiles - 1;   // the MPC chain writes mpc_tiles slots
     const int64_t wave = p->chain_fast ? (p->chain_unit ? 148 * 4 : 148 * 2) : 148 * 2;
     return std::max<int64_t>(1, std::min(wave, p->chain_grid - 1));
 }
@@ -652,6 +661,10 @@ int64_t chain_main_grid(const fg_plan* p) {
 void chain_pass(fg_plan* p, int in, cudaStream_t st) {
     PassB b{p->vt(), p->d_x, p->d_u[in], p->d_u[1 - in], nullptr, p->d_zb[1 - in],
             p->d_zb[in], p->d_rho, p->d_alpha, p->d_zw, p->d_ctrl, p->d_part, p->d_zvar};
+    if (p->mpc_chain) {
+        k_mpc_chain<<<(unsigned)p->mpc_tiles, kEdgeThreads, p->mpc_smem, st>>>(b, p->mpc, 0);
+        return;
+    }
     const unsigned G = (unsigned)chain_main_grid(p);
     if (p->chain_fast) {
         cudaEventRecord(p->ev_fork, st);
@@ -880,6 +893,63 @@ void detect_svm_chain(fg_plan* p, const std::vector<int32_t>& dim,
     p->chain_on = p->chain_grid > 0;
 }
 
+// build_mpc's graph (problems.py:200-215): groups cost (T+1), dyn (T, one
+// system, matrix form possible), init (1) over nodes N(t) = n0id + t with
+// segments [cost_t, dyn_{t-1} slot 1, dyn_t slot 0] (node 0: [cost_0,
+// dyn_0 slot 0, init]; node T: [cost_T, dyn_{T-1} slot 1]) laid out
+// affinely.  The unit-weight condition is decided at every sync.
+void detect_mpc_chain(fg_plan* p, const std::vector<int32_t>& dim,
+                      const std::vector<int32_t>& deg, const std::vector<int64_t>& zbase,
+                      const std::vector<int64_t>& pbase, const std::vector<int32_t>& ebase) {
+    p->mpc_ok = false;
+    if (getenv("FGADMM_NO_CHAIN") || p->partitioned() || p->tma_grid > 0) return;
+    GroupHost *gc = nullptr, *gdyn = nullptr, *gi = nullptr;
+    for (auto& g : p->groups) {
+        if (g.dev.count == 0) continue;
+        switch (g.dev.kind) {
+            case FG_KIND_MPC_COST: if (gc) return; gc = &g; break;
+            case FG_KIND_MPC_DYN: if (gdyn) return; gdyn = &g; break;
+            case FG_KIND_MPC_INIT: if (gi) return; gi = &g; break;
+            default: return;
+        }
+    }
+    if (!gc || !gdyn || !gi || gdyn->tab_h.empty() || !gdyn->dev.runs) return;
+    const int64_t T = gdyn->dev.count;
+    const int n0 = gc->dev.dim[0], d = gdyn->dev.ip;
+    if (T < 2 || gc->dev.count != T + 1 || gi->dev.count != 1 || gdyn->dev.dim[0] != n0 ||
+        gi->dev.dim[0] != n0 || n0 + d > kDynGemmMaxCols || gi->dev.fstride != d)
+        return;
+    if (gc->hsv.size() != 1 || gdyn->hsv.size() != 2 || gi->hsv.size() != 1) return;
+    const int32_t v0 = gc->hsv[0][0];
+    for (int64_t t = 0; t <= T; ++t) {
+        const int32_t v = v0 + (int32_t)t;
+        if (dim[v] != n0 || deg[v] != (t == T ? 2 : 3)) return;
+        if (gc->hsv[0][t] != v || gc->hsk[0][t] != 0) return;
+        if (pbase[v] != pbase[v0] + 3 * t * n0 || ebase[v] != ebase[v0] + 3 * t ||
+            zbase[v] != zbase[v0] + t * n0)
+            return;
+        if (t < T && (gdyn->hsv[0][t] != v || gdyn->hsk[0][t] != (t == 0 ? 1 : 2) ||
+                      gdyn->hsv[1][t] != v + 1 || gdyn->hsk[1][t] != 1))
+            return;
+    }
+    if (gi->hsv[0][0] != v0 || gi->hsk[0][0] != 2) return;
+    if (p->nS != (int64_t)n0 * (T + 1)) return;
+    MpcChainDev& c = p->mpc;
+    c.T = (int32_t)T; c.n0 = n0; c.d = d;
+    c.pN = pbase[v0]; c.zN = zbase[v0]; c.eN = ebase[v0];
+    c.cost_fp = gc->dev.fp; c.cost_st = gc->dev.fstride;
+    c.init_fp = gi->dev.fp;
+    p->mpc_tiles = (T + 1 + kMpcTile - 1) / kMpcTile;
+    p->mpc_smem = mpc_dyn_gemm_smem(n0, d);
+    p->chain_grid = p->nsblk[0] + p->nsblk[1] + p->nsblk[2];
+    const int64_t slots = p->nsblk[0] + p->nsblk[1] + p->nsblk[2];
+    if (p->mpc_tiles > slots) return;                // partial slots it reuses
+    if (cudaFuncSetAttribute(k_mpc_chain<>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kMaxDynSmem) != cudaSuccess)
+        return;
+    p->mpc_ok = true;
+}
+
 int check_launch() {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(FG_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
@@ -1101,7 +1171,9 @@ int build_group(fg_plan* p, const fg_group_desc& gd,
                                 kMaxDynSmem));
     }
     if (gd.kind == FG_KIND_SVM_NORM || gd.kind == FG_KIND_SVM_SLACK ||
-        gd.kind == FG_KIND_SVM_MARGIN || gd.kind == FG_KIND_EQUALITY) {
+        gd.kind == FG_KIND_SVM_MARGIN || gd.kind == FG_KIND_EQUALITY ||
+        gd.kind == FG_KIND_MPC_COST || gd.kind == FG_KIND_MPC_DYN ||
+        gd.kind == FG_KIND_MPC_INIT) {
         out.hsv = std::move(svs);
         out.hsk = std::move(sks);
     }
@@ -1504,8 +1576,8 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     if ((size_t)p->gtop_smem > 40 * 1024) {
         CK(cudaFuncSetAttribute(k_var_giant_top<MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
         CK(cudaFuncSetAttribute(k_var_giant_top<MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-        CK(cudaFuncSetAttribute(k_var_giant_chunks<MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-        CK(cudaFuncSetAttribute(k_var_giant_chunks<MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+        CK(cudaFuncSetAttribute(k_var_giant_chunks<MODE_FUSED, kGiantChunkThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+        CK(cudaFuncSetAttribute(k_var_giant_chunks<MODE_PHASEZ, kGiantChunkThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
     }
     if ((rc = dalloc(&p->d_gcnt, std::max<size_t>(1, glist.size()))) || (rc = dalloc(&p->d_ucnt, 1)))
         return rc;
@@ -1552,6 +1624,7 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
             return fail(FG_ERR_CUDA, "cluster kernel shared-memory attribute");
     }
     detect_svm_chain(p.get(), dim, deg, zbase, gd->z_cut_index);
+    if (!p->chain_on) detect_mpc_chain(p.get(), dim, deg, zbase, pbase, ebase);
     for (auto& g : p->groups) {
         g.hsv.clear(); g.hsv.shrink_to_fit();
         g.hsk.clear(); g.hsk.shrink_to_fit();
@@ -1588,7 +1661,7 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
 void fg_plan_destroy(fg_plan* plan) { delete plan; }
 
 int fg_plan_forms(const fg_plan* p, int32_t* o) {
-    o[0] = p->chain_on ? (p->chain_unit ? 3 : (p->chain_fast ? 2 : 1)) : 0;
+    o[0] = p->chain_on ? (p->mpc_chain ? 4 : (p->chain_unit ? 3 : (p->chain_fast ? 2 : 1))) : 0;
     o[1] = 0;
     o[6] = 0;
     for (auto& g : p->groups) {
@@ -1626,6 +1699,27 @@ int fg_plan_sync_params(fg_plan* p, const double* rho, const double* alpha,
         if (gh.dev.kind == FG_KIND_MPC_DYN && !gh.tab_h.empty())
             if (int rc = sync_dyn_matrix(p, gh, rho)) return rc;
     if (int rc = sync_unit_flags(p)) return rc;
+    if (p->mpc_ok) {
+        // MPC chain: unit weights, z weights = degrees, matrix form active
+        bool on = !getenv("FGADMM_NO_CHAIN");
+        for (int64_t e = 0; e < p->E && on; ++e) on = rho[e] == 1.0 && alpha[e] == 1.0;
+        const MpcChainDev& c = p->mpc;
+        for (int64_t t = 0; t <= c.T && on; ++t)
+            for (int q = 0; q < c.n0 && on; ++q)
+                on = zw[c.zN + t * c.n0 + q] == (t == c.T ? 2.0 : 3.0);
+        const GroupHost* gdyn = nullptr;
+        for (auto& g : p->groups)
+            if (g.dev.kind == FG_KIND_MPC_DYN && g.dev.count > 0) gdyn = &g;
+        on = on && gdyn && gdyn->dev.dyn_gemm;
+        if (on) p->mpc.kmat = gdyn->dev.kmat;
+        if (on != p->mpc_chain) {
+            p->mpc_chain = on;
+            p->chain_on = on;
+            p->launches_later = on ? 2 : p->launches_per_iter;
+            for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
+            p->graphs.clear();
+        }
+    }
     if (p->chain_fast) {
         // unit-weight form of the chain: every rho and alpha exactly 1 and
         // the z weights equal to the degrees (fg_chain.cuh)
@@ -2168,7 +2262,7 @@ int fg_profile_kernels(fg_plan* p, int64_t iterations, int32_t max_slots,
     std::vector<std::string> names;
     std::vector<int> vk;
     if (chain) {
-        names.push_back("chain_svm");
+        names.push_back(p->mpc_chain ? "chain_mpc" : "chain_svm");
         for (int w = 0; w < kVarSlots; ++w)
             if (chain_rest_slot(w) && var_slot_blocks(p, w) > 0) {
                 vk.push_back(w);

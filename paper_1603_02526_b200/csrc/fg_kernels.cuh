@@ -85,16 +85,34 @@ __device__ __forceinline__ void update_range(const PassB& b, const CompRef& r,
                                              int64_t step, double zn, double zo,
                                              double& pp, double& dd, bool& badu) {
     const double dz = zn - zo;
-    for (int64_t e = e0; e < e1; e += step) {
-        const int64_t p = r.pb + e * r.d + r.c;
-        const double xv = b.x[p];
-        const double t = xv - zn;                    // engine.py:288
-        pp += t * t;                                 // engine.py:402
-        const double rd = b.rho[r.eb + e] * dz;      // engine.py:403-405
-        dd += rd * rd;
-        const double un = b.uin[p] + t * b.alpha[r.eb + e];   // :289-290
-        b.uout[p] = un;
-        badu |= !finite(un);
+    // batches of 4 elements: all loads before the stores (the compiler
+    // cannot prove uout aliases nothing read here), one round trip each
+    for (int64_t e = e0; e < e1; e += 4 * step) {
+        double xv[4], uv[4], rv[4], av[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t ee = e + k * step;
+            if (ee < e1) {
+                const int64_t p = r.pb + ee * r.d + r.c;
+                xv[k] = b.x[p];
+                uv[k] = b.uin[p];
+                rv[k] = b.rho[r.eb + ee];
+                av[k] = b.alpha[r.eb + ee];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t ee = e + k * step;
+            if (ee < e1) {
+                const double t = xv[k] - zn;             // engine.py:288
+                pp += t * t;                             // engine.py:402
+                const double rd = rv[k] * dz;            // engine.py:403-405
+                dd += rd * rd;
+                const double un = uv[k] + t * av[k];     // :289-290
+                b.uout[r.pb + ee * r.d + r.c] = un;
+                badu |= !finite(un);
+            }
+        }
     }
 }
 
@@ -146,7 +164,7 @@ __global__ void __launch_bounds__(256) k_var_small(PassB b, const int32_t* list,
 constexpr int kVarThreads = 256;
 constexpr int kMaxUnits = 160;          // chunk <= 8192 -> <= 128 leaves
 
-template <class F>
+template <class F, int NT = kVarThreads>
 __device__ __forceinline__ double run_units_and_tree(F val, int64_t base_elem,
                                                      const int32_t* P,
                                                      double* sv) {
@@ -155,7 +173,7 @@ __device__ __forceinline__ double run_units_and_tree(F val, int64_t base_elem,
     const int32_t* lev = units + 2 * nu;
     const int32_t* ops = lev + nlev;
     const int g = threadIdx.x >> 3, j = threadIdx.x & 7;
-    constexpr int NG = kVarThreads / 8;
+    constexpr int NG = NT / 8;
     for (int r0 = 0; r0 < nu; r0 += NG) {
         const int L = r0 + g;
         int64_t s = 0, len = 0;
@@ -167,7 +185,7 @@ __device__ __forceinline__ double run_units_and_tree(F val, int64_t base_elem,
     int node = nu, op = 0;
     for (int l = 0; l < nlev; ++l) {
         const int cnt = lev[l];
-        for (int o = threadIdx.x; o < cnt; o += kVarThreads)
+        for (int o = threadIdx.x; o < cnt; o += NT)
             sv[node + o] = sv[ops[2 * (op + o)]] + sv[ops[2 * (op + o) + 1]];
         __syncthreads();
         node += cnt;
@@ -224,7 +242,7 @@ struct GChunk { int32_t gi, start, progoff, pad; };
 // G2 descriptor: top program offset, first chunk, cut slot (or -1)
 struct GComp { int32_t topoff, cbase, pad0, pad1; };
 __device__ __forceinline__ int32_t comps_topoff(const GComp* c, int gi) { return c[gi].topoff; }
-template <int MODE>
+template <int MODE, int NT = kVarThreads>
 __device__ void giant_top_body(const PassB& b, const int32_t* glist, const GComp* comps,
                                const int32_t* prog, const double* csum, double* gz,
                                double* send, int gi, double* sv, int64_t it);
@@ -232,8 +250,8 @@ __device__ void giant_top_body(const PassB& b, const int32_t* glist, const GComp
 // atomic counter per component, reset by that CTA) also evaluates the top
 // of its tree: the separate top launch disappears.  The top program is the
 // same whichever CTA runs it, so the result is deterministic.
-template <int MODE>
-__global__ void __launch_bounds__(kVarThreads) k_var_giant_chunks(
+template <int MODE, int NT = kVarThreads>
+__global__ void __launch_bounds__(NT) k_var_giant_chunks(
     PassB b, const int32_t* glist, const GChunk* chunks, const int32_t* prog,
     double* csum, const GComp* comps = nullptr, double* gz = nullptr, double* send = nullptr,
     unsigned* counters = nullptr) {
@@ -251,7 +269,8 @@ __global__ void __launch_bounds__(kVarThreads) k_var_giant_chunks(
     ValFn<MODE> val(b, r, &bm);
     // pad = first element of the tree: 1 for a whole segment (a[0] is the
     // reduceat initial value), 0 for a rank's local part of a cut segment
-    const double T = run_units_and_tree(val, (int64_t)ch.pad + ch.start, prog + ch.progoff, sv);
+    const double T = run_units_and_tree<ValFn<MODE>, NT>(val, (int64_t)ch.pad + ch.start,
+                                                         prog + ch.progoff, sv);
     if (threadIdx.x == 0) csum[blockIdx.x] = T;
     if (MODE == MODE_FUSED && bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
     if (comps) {
@@ -263,7 +282,7 @@ __global__ void __launch_bounds__(kVarThreads) k_var_giant_chunks(
         __syncthreads();
         if (s_last) {
             __threadfence();
-            giant_top_body<MODE>(b, glist, comps, prog, csum, gz, send, ch.gi, sv_top, it);
+            giant_top_body<MODE, NT>(b, glist, comps, prog, csum, gz, send, ch.gi, sv_top, it);
             if (threadIdx.x == 0) counters[ch.gi] = 0u;
         }
     }
@@ -275,7 +294,7 @@ __global__ void __launch_bounds__(kVarThreads) k_var_giant_chunks(
 // sum in `send`; z follows after the exchange (k_cut_finalize).
 // Top of giant component gi's tree from its chunk sums -> z (or the cut
 // partial); one CTA, `sv` holds 2 doubles per chunk.
-template <int MODE>
+template <int MODE, int NT>
 __device__ void giant_top_body(const PassB& b, const int32_t* glist, const GComp* comps,
                                const int32_t* prog, const double* csum, double* gz,
                                double* send, int gi, double* sv, int64_t it) {
@@ -285,12 +304,12 @@ __device__ void giant_top_body(const PassB& b, const int32_t* glist, const GComp
     const int nu = P[0], nlev = P[1];
     const int32_t* lev = P + 2 + 2 * nu;
     const int32_t* ops = lev + nlev;
-    for (int u = threadIdx.x; u < nu; u += kVarThreads) sv[u] = __ldcg(csum + gc.cbase + u);
+    for (int u = threadIdx.x; u < nu; u += NT) sv[u] = __ldcg(csum + gc.cbase + u);
     __syncthreads();
     int node = nu, op = 0;
     for (int l = 0; l < nlev; ++l) {
         const int cnt = lev[l];
-        for (int o = threadIdx.x; o < cnt; o += kVarThreads)
+        for (int o = threadIdx.x; o < cnt; o += NT)
             sv[node + o] = sv[ops[2 * (op + o)]] + sv[ops[2 * (op + o) + 1]];
         __syncthreads();
         node += cnt;

@@ -201,4 +201,170 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_dyn_gemm(PassA a, Group
     passa_flags<FIRST>(a, it, bn, bx);
 }
 
+
+
+// ===========================================================================
+// Fused MPC chain (build_mpc's graph, problems.py:200-215): one kernel per
+// iteration instead of the cost, dynamics, init and variable-pass kernels.
+//
+// Node t (state+control, dim n0) has edges [cost_t, dyn_{t-1} slot 1,
+// dyn_t slot 0] (node 0: [cost_0, dyn_0 slot 0, init], node T: [cost_T,
+// dyn_{T-1} slot 1]).  A CTA owns up to kMpcTile consecutive nodes: it
+// stages the n values of every dynamics factor touching them (<= 128,
+// one shared with each neighbouring tile and evaluated by both with
+// identical arithmetic), applies the matrix form v = K nv, then finishes
+// each node from registers: cost and init proxes, m, z (NumPy's reduceat
+// order), u and the residual partials.  x of the nodes never goes to
+// memory (it is recomputed on download, as for the SVM chain).  Unit-weight
+// form only (every rho, alpha = 1; checked at sync): the arithmetic is the
+// per-kind path's operation by operation, so bitwise equal to it.
+// ===========================================================================
+constexpr int kMpcTile = 127;                       // nodes per CTA (<= 128 factors)
+
+struct MpcChainDev {
+    int32_t T, n0, d, pad;
+    int64_t pN, zN;                                 // node 0 payload / z base
+    int32_t eN, cost_st;                            // node 0 edge base, cost fstride
+    const double* cost_fp;                          // per node: diag (n0)
+    const double* init_fp;                          // q0 (d)
+    const double* kmat;                             // K (cols x cols)
+};
+
+template <bool FIRST_UNUSED = false>
+__global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_chain(PassB b, MpcChainDev c,
+                                                               int64_t part_off) {
+    extern __shared__ double gsm[];
+    __shared__ double sm[2 * (kEdgeThreads / 32)];
+    if (b.ctrl->stop) return;
+    const int64_t it = b.ctrl->iter;
+    const int n0 = c.n0, d = c.d, cols = n0 + d, ld = cols + 1, ldo = 2 * n0 + 1;
+    constexpr int KH = kDynGemmMaxCols / 2;
+    double* Ks = gsm;                                   // [c][r0][k]
+    double* nvs = Ks + cols * kDynGemmMaxCols;          // [F][ld]
+    double* outs = nvs + kDynGemmF * ld;                // [F][ldo]
+    const int t0 = blockIdx.x * kMpcTile;
+    const int t1 = min(c.T + 1, t0 + kMpcTile);         // nodes [t0, t1)
+    const int fA = max(0, t0 - 1), fB = min(c.T, t1);   // factors [fA, fB)
+    const int nf = fB - fA;
+    bool bn = false, bx = false, bm = false, bz = false, bu = false;
+    for (int i = threadIdx.x; i < cols * cols; i += blockDim.x) {
+        const int r = i / cols, cc = i - r * cols;
+        Ks[(cc * 2 + (r & 1)) * KH + (r >> 1)] = c.kmat[i];
+    }
+    const double* __restrict__ uin = b.uin;
+    const double* __restrict__ zin = b.zin;
+    // node t: payload pN + 3 t n0 (rank k at + k n0), z zN + t n0
+    auto upos = [&](int t, int rank) { return c.pN + ((int64_t)3 * t + rank) * n0; };
+    // ---- stage n of the dynamics factors: slot 0 at node f (rank 2, or 1
+    // for f = 0), slot 1 at node f+1 (rank 1) ----
+    const int per = 2 * n0;
+    for (int idx = threadIdx.x; idx < nf * per; idx += blockDim.x) {
+        const int fl = idx / per, cc = idx - fl * per;
+        const int f = fA + fl;
+        const int j = cc < n0 ? 0 : 1, q = cc - j * n0;
+        const int node = f + j;
+        const int rank = j ? 1 : (f == 0 ? 1 : 2);
+        const double n = zin[c.zN + (int64_t)node * n0 + q] - uin[upos(node, rank) + q];
+        bn |= !finite(n);
+        if (j == 0) nvs[fl * ld + q] = n;
+        else if (q < d) nvs[fl * ld + n0 + q] = n;
+        else outs[fl * ldo + n0 + q] = n;               // control of t+1 passes
+    }
+    __syncthreads();
+    {   // v = K nv: thread -> factor slot fl, rows r0 + 2k (k_mpc_dyn_gemm order)
+        const int fl = threadIdx.x & (kDynGemmF - 1), r0 = threadIdx.x >> 7;
+        if (fl < nf) {
+            double acc[KH];
+#pragma unroll
+            for (int k = 0; k < KH; ++k) acc[k] = 0.0;
+            const double* nvf = nvs + fl * ld;
+            for (int cc = 0; cc < cols; ++cc) {
+                const double v = nvf[cc];
+                const double2* kc = reinterpret_cast<const double2*>(Ks + (cc * 2 + r0) * KH);
+#pragma unroll
+                for (int k2 = 0; k2 < KH / 2; ++k2) {
+                    const double2 kk = kc[k2];
+                    acc[2 * k2] = __fma_rn(kk.x, v, acc[2 * k2]);
+                    acc[2 * k2 + 1] = __fma_rn(kk.y, v, acc[2 * k2 + 1]);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < KH; ++k) {
+                const int r = r0 + 2 * k;
+                if (r < cols) outs[fl * ldo + r] = acc[k];
+            }
+        }
+    }
+    __syncthreads();
+    // ---- nodes: cost / init proxes, m, z, u ----
+    double pp = 0.0, dd = 0.0;
+    const int nn = t1 - t0;
+    for (int idx = threadIdx.x; idx < nn * n0; idx += blockDim.x) {
+        const int tl = idx / n0, q = idx - tl * n0;
+        const int t = t0 + tl;
+        const int deg = t == c.T ? 2 : 3;
+        const int64_t zo = c.zN + (int64_t)t * n0 + q;
+        const double zi = zin[zo];
+        double u[3], x[3];
+        u[0] = uin[upos(t, 0) + q];
+        u[1] = uin[upos(t, 1) + q];
+        u[2] = deg == 3 ? uin[upos(t, 2) + q] : 0.0;
+        // cost (rank 0): prox_mpc_cost with rho = 1
+        const double n_c = zi - u[0];
+        bn |= !finite(n_c);
+        x[0] = prox_mpc_cost(n_c, 1.0, c.cost_fp[(int64_t)t * c.cost_st + q]);
+        // rank 1: dyn_{t-1} slot 1 (node 0: dyn_0 slot 0)
+        x[1] = t == 0 ? outs[(0 - fA) * ldo + q] : outs[(t - 1 - fA) * ldo + n0 + q];
+        // rank 2: dyn_t slot 0 (node 0: init)
+        x[2] = 0.0;
+        if (deg == 3) {
+            if (t == 0) {
+                const double n_i = zi - u[2];
+                bn |= !finite(n_i);
+                x[2] = q < d ? c.init_fp[q] : n_i;
+            } else {
+                x[2] = outs[(t - fA) * ldo + q];
+            }
+        }
+        bx |= !(finite(x[0]) && finite(x[1]) && (deg == 2 || finite(x[2])));
+        // phases m, z, u (k_var_small_run<4> order, weights 1)
+        double S = 0.0, res = 0.0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if (k < deg) {
+                const double m = x[k] + u[k];
+                bm |= !finite(m);
+                if (k == 0) S = m;
+                else res += m;
+            }
+        }
+        S = S + res;
+        const double zn = ddiv(S, (double)deg);
+        bz |= !finite(zn);
+        b.z[zo] = zn;
+        const double dz = zn - zi;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if (k < deg) {
+                const double tt = x[k] - zn;
+                pp += tt * tt;
+                dd += dz * dz;
+                const double un = u[k] + tt;
+                b.uout[upos(t, k) + q] = un;
+                bu |= !finite(un);
+            }
+        }
+    }
+    if (bn) flag_error(b.ctrl, it - 1, FG_PHASE_N, true);
+    if (bx) flag_error(b.ctrl, it, FG_PHASE_X, true);
+    if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
+    if (bz) flag_error(b.ctrl, it, FG_PHASE_Z, false);
+    if (bu) flag_error(b.ctrl, it, FG_PHASE_U, false);
+    block_sum2<kEdgeThreads>(pp, dd, sm);
+    if (threadIdx.x == 0) {
+        b.part[2 * (part_off + blockIdx.x)] = pp;
+        b.part[2 * (part_off + blockIdx.x) + 1] = dd;
+    }
+}
+
 }  // namespace fg

@@ -349,7 +349,7 @@ class DevicePlan:
         form, fused giant kernels."""
         o = (C.c_int32 * 8)()
         self._lib.fg_plan_forms(self._h, o)
-        return {"chain": ("off", "generic", "fast", "unit")[o[0]],
+        return {"chain": ("off", "generic", "fast", "unit", "mpc")[o[0]],
                 "collision_unit": bool(o[1]),
                 "rows_unit": {d: bool(o[1 + d]) for d in (1, 2, 3, 4)},
                 "mpc_dyn_matrix": bool(o[6]), "giant_fused": bool(o[7])}
@@ -357,9 +357,7 @@ class DevicePlan:
     def chain_form(self):
         """Form of the fused SVM-chain kernel the next run uses: 'off',
         'generic', 'fast' or 'unit' (unit weights; decided at every sync)."""
-        info = (C.c_int64 * 12)()
-        self._lib.fg_plan_info(self._h, info)
-        return ("off", "generic", "fast", "unit")[info[11]]
+        return self.forms()["chain"]
 
     def debug_buffer(self, which):
         z_slot = which in (_native.BUF_Z0, _native.BUF_Z1)

@@ -326,3 +326,27 @@ def test_mpc_dynamics_forms_match_oracle(gpu, env, monkeypatch):
     so, _h, _ = O.run(g, 12, st)
     for k in "xmzun":
         assert_close(getattr(s, k), getattr(so, k), what=k)
+
+
+def test_mpc_chain_bitwise_equals_per_kind(gpu, monkeypatch):
+    """The fused MPC chain (one kernel per iteration: cost, dynamics in the
+    matrix form, init, and the node updates) is bitwise the per-kind path
+    with the matrix form, and runs from the plan's second sync onward."""
+    from paper_1603_02526_b200.engine import DevicePlan, _PLANS
+    gd = golden("mpc16x4_T50.npz")
+    outs = []
+    for chain in (True, False):
+        if chain:
+            monkeypatch.delenv("FGADMM_NO_CHAIN", raising=False)
+        else:
+            monkeypatch.setenv("FGADMM_NO_CHAIN", "1")
+        g = fg.build_mpc(fg.MpcSpec(400, fg.LinearSystem(gd["A"], gd["B"]), gd["q0"]))
+        _PLANS[g] = DevicePlan(g)
+        st = fg.init_state(g, seed=6)
+        s = copy(st)
+        fg.run(g, fg.RunConfig(max_iterations=9), state=s)
+        fg.run(g, fg.RunConfig(max_iterations=4), state=s)
+        assert _PLANS[g].chain_form() == ("mpc" if chain else "off")
+        outs.append(s)
+    for k in "xmzun":
+        np.testing.assert_array_equal(getattr(outs[0], k), getattr(outs[1], k), err_msg=k)
