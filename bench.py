@@ -127,6 +127,11 @@ def kernel_bytes(graph, plan):
                           + plan.info["large_components"] + 64)
     if plan.info.get("fused_chain"):
         out["chain_svm"] = chain_bytes(graph, dims, deg, plan.chain_form() == "unit")
+    if forms["chain"] == "mpc":
+        # fused MPC chain: u read + write per payload double, z read +
+        # write per component, the cost diagonal per component
+        P, Z = graph.total_edge_payload, graph.z_dim
+        out["chain_mpc"] = P * 16 + Z * 24
     return out
 
 
@@ -173,23 +178,30 @@ class ClockSampler:
     the timed region runs (the recipe's clocks line)."""
 
     def __init__(self, index=0, period=0.005):
+        # NVML is initialised here, before the caller's warm-up: nvmlInit
+        # takes milliseconds, and an idle GPU gap right before the timed
+        # region lets the clocks drop.
         self.index = index
         self.period = period
         self.samples = []
         self.max_mhz = None
         self._stop = threading.Event()
-
-    def __enter__(self):
+        self._t = None
         try:
             import pynvml
             pynvml.nvmlInit()
             self._nv = pynvml
             self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
             self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
-            self._t = threading.Thread(target=self._loop, daemon=True)
-            self._t.start()
         except Exception:
             self._nv = None
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._stop.clear()
+            self.samples = []
+            self._t = threading.Thread(target=self._loop, daemon=True)
+            self._t.start()
         return self
 
     def _loop(self):
@@ -328,12 +340,13 @@ def multi_gpu(args, fg, dist, rank, world, local):
         nr = NcclRank(g, rank, world, device=local)
         E = len(g.edge_var)
     t_build = time.perf_counter() - t_build
+    clk = ClockSampler(local)
     nr.upload(st)
     nr.run(args.warmup)
     nr.upload(st)
     torch.cuda.synchronize()
     dist.barrier()
-    with ClockSampler(local) as clk:
+    with clk:
         res, _hist = nr.run(args.steps)
     t = torch.tensor([res.ms_total], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -417,12 +430,13 @@ def main():
     E = len(g.edge_var)
 
     # ---- device-resident timed region ----
+    clk = ClockSampler(local)
     plan.sync(g)
     plan.upload(st.z, st.u, st.n)
     plan.run(args.warmup)                                  # untimed warm-up
     if dist:
         dist.barrier()
-    with ClockSampler(local) as clk:
+    with clk:
         res, _hist = plan.run(args.steps, graph_chunk=16)
     ms = res.ms_total
     if dist:
