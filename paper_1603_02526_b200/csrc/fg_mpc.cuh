@@ -299,6 +299,10 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_chain(PassB b, MpcChain
     // ---- nodes: cost / init proxes, m, z, u ----
     double pp = 0.0, dd = 0.0;
     const int nn = t1 - t0;
+    double* __restrict__ uout = b.uout;
+    double* __restrict__ zout = b.z;
+    const double* __restrict__ cfp = c.cost_fp;
+#pragma unroll 2
     for (int idx = threadIdx.x; idx < nn * n0; idx += blockDim.x) {
         const int tl = idx / n0, q = idx - tl * n0;
         const int t = t0 + tl;
@@ -312,7 +316,7 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_chain(PassB b, MpcChain
         // cost (rank 0): prox_mpc_cost with rho = 1
         const double n_c = zi - u[0];
         bn |= !finite(n_c);
-        x[0] = prox_mpc_cost(n_c, 1.0, c.cost_fp[(int64_t)t * c.cost_st + q]);
+        x[0] = prox_mpc_cost(n_c, 1.0, cfp[(int64_t)t * c.cost_st + q]);
         // rank 1: dyn_{t-1} slot 1 (node 0: dyn_0 slot 0)
         x[1] = t == 0 ? outs[(0 - fA) * ldo + q] : outs[(t - 1 - fA) * ldo + n0 + q];
         // rank 2: dyn_t slot 0 (node 0: init)
@@ -341,7 +345,7 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_chain(PassB b, MpcChain
         S = S + res;
         const double zn = ddiv(S, (double)deg);
         bz |= !finite(zn);
-        b.z[zo] = zn;
+        zout[zo] = zn;
         const double dz = zn - zi;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
@@ -350,7 +354,7 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_chain(PassB b, MpcChain
                 pp += tt * tt;
                 dd += dz * dz;
                 const double un = u[k] + tt;
-                b.uout[upos(t, k) + q] = un;
+                uout[upos(t, k) + q] = un;
                 bu |= !finite(un);
             }
         }
