@@ -258,17 +258,36 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_chain(PassB b, MpcChain
     // ---- stage n of the dynamics factors: slot 0 at node f (rank 2, or 1
     // for f = 0), slot 1 at node f+1 (rank 1) ----
     const int per = 2 * n0;
-    for (int idx = threadIdx.x; idx < nf * per; idx += blockDim.x) {
-        const int fl = idx / per, cc = idx - fl * per;
-        const int f = fA + fl;
-        const int j = cc < n0 ? 0 : 1, q = cc - j * n0;
-        const int node = f + j;
-        const int rank = j ? 1 : (f == 0 ? 1 : 2);
-        const double n = zin[c.zN + (int64_t)node * n0 + q] - uin[upos(node, rank) + q];
-        bn |= !finite(n);
-        if (j == 0) nvs[fl * ld + q] = n;
-        else if (q < d) nvs[fl * ld + n0 + q] = n;
-        else outs[fl * ldo + n0 + q] = n;               // control of t+1 passes
+    constexpr int SB = 4;                               // loads in flight per thread
+    for (int base = threadIdx.x; base < nf * per; base += SB * kEdgeThreads) {
+        double zv[SB], uv[SB];
+#pragma unroll
+        for (int k = 0; k < SB; ++k) {
+            const int idx = base + k * kEdgeThreads;
+            zv[k] = 0.0; uv[k] = 0.0;
+            if (idx < nf * per) {
+                const int fl = idx / per, cc = idx - fl * per;
+                const int f = fA + fl;
+                const int j = cc < n0 ? 0 : 1, q = cc - j * n0;
+                const int node = f + j;
+                const int rank = j ? 1 : (f == 0 ? 1 : 2);
+                zv[k] = zin[c.zN + (int64_t)node * n0 + q];
+                uv[k] = uin[upos(node, rank) + q];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < SB; ++k) {
+            const int idx = base + k * kEdgeThreads;
+            if (idx < nf * per) {
+                const int fl = idx / per, cc = idx - fl * per;
+                const int j = cc < n0 ? 0 : 1, q = cc - j * n0;
+                const double n = zv[k] - uv[k];
+                bn |= !finite(n);
+                if (j == 0) nvs[fl * ld + q] = n;
+                else if (q < d) nvs[fl * ld + n0 + q] = n;
+                else outs[fl * ldo + n0 + q] = n;   // control of t+1 passes
+            }
+        }
     }
     __syncthreads();
     {   // v = K nv: thread -> factor slot fl, rows r0 + 2k (k_mpc_dyn_gemm order)
@@ -302,21 +321,39 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_chain(PassB b, MpcChain
     double* __restrict__ uout = b.uout;
     double* __restrict__ zout = b.z;
     const double* __restrict__ cfp = c.cost_fp;
-#pragma unroll 2
-    for (int idx = threadIdx.x; idx < nn * n0; idx += blockDim.x) {
+    constexpr int NB = 2;                               // nodes' loads in flight per thread
+    for (int ib = threadIdx.x; ib < nn * n0; ib += NB * kEdgeThreads) {
+      double zl[NB], ul[NB][3], dl[NB];
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        const int idx = ib + k * kEdgeThreads;
+        if (idx < nn * n0) {
+            const int tl = idx / n0, q = idx - tl * n0;
+            const int t = t0 + tl;
+            zl[k] = zin[c.zN + (int64_t)t * n0 + q];
+            ul[k][0] = uin[upos(t, 0) + q];
+            ul[k][1] = uin[upos(t, 1) + q];
+            ul[k][2] = t < c.T ? uin[upos(t, 2) + q] : 0.0;
+            dl[k] = cfp[(int64_t)t * c.cost_st + q];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        const int idx = ib + k * kEdgeThreads;
+        if (idx >= nn * n0) continue;
         const int tl = idx / n0, q = idx - tl * n0;
         const int t = t0 + tl;
         const int deg = t == c.T ? 2 : 3;
         const int64_t zo = c.zN + (int64_t)t * n0 + q;
-        const double zi = zin[zo];
+        const double zi = zl[k];
         double u[3], x[3];
-        u[0] = uin[upos(t, 0) + q];
-        u[1] = uin[upos(t, 1) + q];
-        u[2] = deg == 3 ? uin[upos(t, 2) + q] : 0.0;
+        u[0] = ul[k][0];
+        u[1] = ul[k][1];
+        u[2] = ul[k][2];
         // cost (rank 0): prox_mpc_cost with rho = 1
         const double n_c = zi - u[0];
         bn |= !finite(n_c);
-        x[0] = prox_mpc_cost(n_c, 1.0, cfp[(int64_t)t * c.cost_st + q]);
+        x[0] = prox_mpc_cost(n_c, 1.0, dl[k]);
         // rank 1: dyn_{t-1} slot 1 (node 0: dyn_0 slot 0)
         x[1] = t == 0 ? outs[(0 - fA) * ldo + q] : outs[(t - 1 - fA) * ldo + n0 + q];
         // rank 2: dyn_t slot 0 (node 0: init)
@@ -334,11 +371,11 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_chain(PassB b, MpcChain
         // phases m, z, u (k_var_small_run<4> order, weights 1)
         double S = 0.0, res = 0.0;
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            if (k < deg) {
-                const double m = x[k] + u[k];
+        for (int kk = 0; kk < 3; ++kk) {
+            if (kk < deg) {
+                const double m = x[kk] + u[kk];
                 bm |= !finite(m);
-                if (k == 0) S = m;
+                if (kk == 0) S = m;
                 else res += m;
             }
         }
@@ -348,16 +385,17 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_chain(PassB b, MpcChain
         zout[zo] = zn;
         const double dz = zn - zi;
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            if (k < deg) {
-                const double tt = x[k] - zn;
+        for (int kk = 0; kk < 3; ++kk) {
+            if (kk < deg) {
+                const double tt = x[kk] - zn;
                 pp += tt * tt;
                 dd += dz * dz;
-                const double un = u[k] + tt;
-                uout[upos(t, k) + q] = un;
+                const double un = u[kk] + tt;
+                uout[upos(t, kk) + q] = un;
                 bu |= !finite(un);
             }
         }
+      }
     }
     if (bn) flag_error(b.ctrl, it - 1, FG_PHASE_N, true);
     if (bx) flag_error(b.ctrl, it, FG_PHASE_X, true);
