@@ -52,10 +52,10 @@ constexpr int64_t kGiantWork = 2048; // elements per G3 CTA
 // Giant segments are cut into maximal pairwise subtrees of <= kGiantChunk
 // items (one CTA each); smaller than the class-L limit so a degree-1M
 // segment spreads over ~1000 CTAs instead of ~128.
-constexpr int64_t kGiantChunk = 1024;
+constexpr int64_t kGiantChunk = 2048;
 // a chunk of <= 1024 items has ~8-16 leaves of 8 lanes each: 64-thread
 // CTAs (several resident per SM) instead of 256 threads mostly idle
-constexpr int kGiantChunkThreads = 64;
+constexpr int kGiantChunkThreads = 128;
 // Dynamic shared-memory limit set on every kernel that uses it: the
 // attribute is per function, not per launch, so plans of different sizes
 // must not lower it under one another.

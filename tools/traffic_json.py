@@ -18,6 +18,7 @@ LABELS = {
     "edge_mpc_dyn": "void k_mpc_dyn_gemm",
     "var_small_deg4": "void k_var_small_run<4,",
     "var_giant_chunks": "void k_var_giant_chunks",
+    "chain_mpc": "void k_mpc_chain",
 }
 
 
