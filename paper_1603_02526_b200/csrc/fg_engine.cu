@@ -233,6 +233,7 @@ struct fg_plan {
     bool chain_on = false;
     bool mpc_chain = false;            // the fused iteration is the MPC chain (fg_mpc.cuh)
     bool mpc_ok = false;               // build_mpc topology detected (unit weights checked at sync)
+    bool mpc_reduce_fused = true;      // chain_pass runs the reduction (set by the caller)
     MpcChainDev mpc{};
     int64_t mpc_tiles = 0;
     size_t mpc_smem = 0;
@@ -662,7 +663,11 @@ void chain_pass(fg_plan* p, int in, cudaStream_t st) {
     PassB b{p->vt(), p->d_x, p->d_u[in], p->d_u[1 - in], nullptr, p->d_zb[1 - in],
             p->d_zb[in], p->d_rho, p->d_alpha, p->d_zw, p->d_ctrl, p->d_part, p->d_zvar};
     if (p->mpc_chain) {
-        k_mpc_chain<<<(unsigned)p->mpc_tiles, kEdgeThreads, p->mpc_smem, st>>>(b, p->mpc, 0);
+        // with reduce_fused the last CTA also runs the residual reduction
+        const FusedReduce fr = p->mpc_reduce_fused
+            ? FusedReduce{p->d_ucnt, p->npart, p->mpc_tiles, p->chain_grid, p->d_hist}
+            : FusedReduce{nullptr, 0, 0, 0, nullptr};
+        k_mpc_chain<<<(unsigned)p->mpc_tiles, kEdgeThreads, p->mpc_smem, st>>>(b, p->mpc, 0, fr);
         return;
     }
     const unsigned G = (unsigned)chain_main_grid(p);
@@ -706,6 +711,7 @@ bool chain_rest_slot(int w) { return w > 2 && w != kSlotSmallTma; }
 // Returns true when the residual reduction ran fused into the last CTA of
 // the giant u update (the update is then the iteration's last kernel).
 bool chain_rest(fg_plan* p, int in, cudaStream_t st) {
+    if (p->mpc_chain) return p->mpc_reduce_fused;   // no other variable class
     int last = -1;
     for (int w = 0; w < kVarSlots; ++w)
         if (chain_rest_slot(w) && var_slot_blocks(p, w) > 0) last = w;
@@ -940,7 +946,7 @@ void detect_mpc_chain(fg_plan* p, const std::vector<int32_t>& dim,
     c.cost_fp = gc->dev.fp; c.cost_st = gc->dev.fstride;
     c.init_fp = gi->dev.fp;
     p->mpc_tiles = (T + 1 + kMpcTile - 1) / kMpcTile;
-    p->mpc_smem = mpc_dyn_gemm_smem(n0, d);
+    p->mpc_smem = mpc_chain_smem(n0, d);
     p->chain_grid = p->nsblk[0] + p->nsblk[1] + p->nsblk[2];
     const int64_t slots = p->nsblk[0] + p->nsblk[1] + p->nsblk[2];
     if (p->mpc_tiles > slots) return;                // partial slots it reuses
@@ -1715,7 +1721,7 @@ int fg_plan_sync_params(fg_plan* p, const double* rho, const double* alpha,
         if (on != p->mpc_chain) {
             p->mpc_chain = on;
             p->chain_on = on;
-            p->launches_later = on ? 2 : p->launches_per_iter;
+            p->launches_later = on ? 1 : p->launches_per_iter;
             for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
             p->graphs.clear();
         }
@@ -2257,8 +2263,14 @@ int fg_profile_kernels(fg_plan* p, int64_t iterations, int32_t max_slots,
     p->n_valid = 0;
     CK(cudaMemcpyAsync(p->d_ctrl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
     // Generic plans time every iteration; with the fused chain on, iteration
-    // 1 runs the generic path untimed and iterations 2.. are timed.
+    // 1 runs the generic path untimed and iterations 2.. are timed.  The
+    // reduction is timed as its own kernel here (not fused into the chain).
     const bool chain = p->chain_on;
+    struct Restore {
+        fg_plan* p; bool v;
+        ~Restore() { p->mpc_reduce_fused = v; }
+    } restore{p, p->mpc_reduce_fused};
+    p->mpc_reduce_fused = false;
     std::vector<std::string> names;
     std::vector<int> vk;
     if (chain) {

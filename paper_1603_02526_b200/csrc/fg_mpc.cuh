@@ -219,7 +219,16 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_dyn_gemm(PassA a, Group
 // form only (every rho, alpha = 1; checked at sync): the arithmetic is the
 // per-kind path's operation by operation, so bitwise equal to it.
 // ===========================================================================
-constexpr int kMpcTile = 127;                       // nodes per CTA (<= 128 factors)
+constexpr int kMpcTile = 63;                        // nodes per CTA (<= 64 factors)
+constexpr int kMpcF = kMpcTile + 1;                 // factor slots per CTA
+constexpr int kMpcRG = kEdgeThreads / kMpcF;        // row groups: thread rows r0 + RG k
+constexpr int kMpcKH = (kDynGemmMaxCols + kMpcRG - 1) / kMpcRG;
+
+inline size_t mpc_chain_smem(int n0, int d) {
+    const size_t cols = (size_t)(n0 + d);
+    return (cols * kMpcRG * kMpcKH + (size_t)kMpcF * (cols + 1) + (size_t)kMpcF * (2 * n0 + 1)) *
+           sizeof(double);
+}
 
 struct MpcChainDev {
     int32_t T, n0, d, pad;
@@ -231,17 +240,19 @@ struct MpcChainDev {
 };
 
 template <bool FIRST_UNUSED = false>
-__global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_chain(PassB b, MpcChainDev c,
-                                                               int64_t part_off) {
+__global__ void __launch_bounds__(kEdgeThreads, 3) k_mpc_chain(PassB b, MpcChainDev c,
+                                                               int64_t part_off,
+                                                               FusedReduce fr) {
     extern __shared__ double gsm[];
     __shared__ double sm[2 * (kEdgeThreads / 32)];
+    __shared__ int s_last;
     if (b.ctrl->stop) return;
     const int64_t it = b.ctrl->iter;
     const int n0 = c.n0, d = c.d, cols = n0 + d, ld = cols + 1, ldo = 2 * n0 + 1;
-    constexpr int KH = kDynGemmMaxCols / 2;
-    double* Ks = gsm;                                   // [c][r0][k]
-    double* nvs = Ks + cols * kDynGemmMaxCols;          // [F][ld]
-    double* outs = nvs + kDynGemmF * ld;                // [F][ldo]
+    constexpr int KH = kMpcKH, RG = kMpcRG;
+    double* Ks = gsm;                                   // [c][r0][k], row r = r0 + RG k
+    double* nvs = Ks + cols * RG * KH;                  // [F][ld]
+    double* outs = nvs + kMpcF * ld;                    // [F][ldo]
     const int t0 = blockIdx.x * kMpcTile;
     const int t1 = min(c.T + 1, t0 + kMpcTile);         // nodes [t0, t1)
     const int fA = max(0, t0 - 1), fB = min(c.T, t1);   // factors [fA, fB)
@@ -249,7 +260,7 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_chain(PassB b, MpcChain
     bool bn = false, bx = false, bm = false, bz = false, bu = false;
     for (int i = threadIdx.x; i < cols * cols; i += blockDim.x) {
         const int r = i / cols, cc = i - r * cols;
-        Ks[(cc * 2 + (r & 1)) * KH + (r >> 1)] = c.kmat[i];
+        Ks[(cc * RG + r % RG) * KH + r / RG] = c.kmat[i];
     }
     const double* __restrict__ uin = b.uin;
     const double* __restrict__ zin = b.zin;
@@ -290,8 +301,9 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_chain(PassB b, MpcChain
         }
     }
     __syncthreads();
-    {   // v = K nv: thread -> factor slot fl, rows r0 + 2k (k_mpc_dyn_gemm order)
-        const int fl = threadIdx.x & (kDynGemmF - 1), r0 = threadIdx.x >> 7;
+    {   // v = K nv: thread -> factor slot fl, rows r0 + RG k; every output is
+        // the fma chain over columns 0..cols-1 of k_mpc_dyn_gemm (bitwise)
+        const int fl = threadIdx.x % kMpcF, r0 = threadIdx.x / kMpcF;
         if (fl < nf) {
             double acc[KH];
 #pragma unroll
@@ -299,7 +311,7 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_chain(PassB b, MpcChain
             const double* nvf = nvs + fl * ld;
             for (int cc = 0; cc < cols; ++cc) {
                 const double v = nvf[cc];
-                const double2* kc = reinterpret_cast<const double2*>(Ks + (cc * 2 + r0) * KH);
+                const double2* kc = reinterpret_cast<const double2*>(Ks + (cc * RG + r0) * KH);
 #pragma unroll
                 for (int k2 = 0; k2 < KH / 2; ++k2) {
                     const double2 kk = kc[k2];
@@ -309,7 +321,7 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_chain(PassB b, MpcChain
             }
 #pragma unroll
             for (int k = 0; k < KH; ++k) {
-                const int r = r0 + 2 * k;
+                const int r = r0 + RG * k;
                 if (r < cols) outs[fl * ldo + r] = acc[k];
             }
         }
@@ -406,6 +418,18 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_chain(PassB b, MpcChain
     if (threadIdx.x == 0) {
         b.part[2 * (part_off + blockIdx.x)] = pp;
         b.part[2 * (part_off + blockIdx.x) + 1] = dd;
+    }
+    if (fr.counter) {                 // the last CTA runs the residual reduction
+        if (threadIdx.x == 0) {
+            __threadfence();
+            s_last = atomicAdd(fr.counter, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            reduce_body<kEdgeThreads>(b.ctrl, b.part, fr.npart, fr.hist, fr.skip_lo, fr.skip_hi, sm);
+            if (threadIdx.x == 0) *fr.counter = 0u;
+        }
     }
 }
 
