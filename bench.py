@@ -435,9 +435,12 @@ def main():
     plan.upload(st.z, st.u, st.n)
     wres, _ = plan.run(args.warmup)                        # untimed warm-up
     # clock settle: an idle GPU ramps its clocks back up over milliseconds,
-    # so short workloads keep warming (untimed) until ~0.3 s of device work
+    # so latency-bound workloads (< 0.25 ms per iteration) keep warming
+    # (untimed) until ~0.1 s of device work; bandwidth-bound ones are not
+    # held at full power longer than the warm-up asks (power capping)
     warm_ms, settle = wres.ms_total, 0
-    while warm_ms < 300.0 and settle < 100000:
+    short = wres.ms_total / max(args.warmup, 1) < 0.25
+    while short and warm_ms < 100.0 and settle < 100000:
         n = max(args.warmup, 20)
         wres, _ = plan.run(n)
         warm_ms += wres.ms_total
