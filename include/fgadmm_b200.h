@@ -173,6 +173,11 @@ int fg_run(fg_plan* plan, const fg_run_config* cfg, double* history,
            fg_run_result* out);
 int fg_state_download(fg_plan* plan, double* x, double* m, double* z,
                       double* u, double* n);
+/* First non-finite entry (reference edge order) of the payload arrays the
+ * last fg_state_download wrote: out4[0..3] for x, m, u, n, -1 when all
+ * finite or not downloaded.  Replaces the host scan behind the reference's
+ * final n check (engine.py:333-350, 519). */
+int fg_state_nonfinite(const fg_plan* plan, int64_t* out4);
 /* x/u/aux buffers are P doubles in reference edge order; FG_BUF_Z0/1 are Z
  * doubles.  After a failed fg_run, FG_BUF_X holds x of the failing
  * iteration (materialized when that iteration ran fused kernels). */

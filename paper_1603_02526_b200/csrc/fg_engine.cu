@@ -245,6 +245,9 @@ struct fg_plan {
     double* d_chain_xx = nullptr;      // per point x.x of the margin data
     double* d_chain_fnorm = nullptr;   // per point 1/(1+scale) (unit form)
     int32_t* d_flag = nullptr;         // scratch device flag
+    unsigned long long* d_bad = nullptr;  // first non-finite ref index of a download
+    int32_t* h_stop = nullptr;         // pinned stop-flag slots polled by fg_run
+    int64_t first_bad[4] = {-1, -1, -1, -1};  // last download of x, m, u, n
     // iteration (of the last run) whose x is not in d_x because the chain
     // kernel keeps it in registers; 0 = d_x is current
     int64_t x_stale = 0;
@@ -300,7 +303,7 @@ fg_plan::~fg_plan() {
                     d_clprog[2], d_clprog[3], d_clprog[4],
                     d_llist, d_lprog, d_prog, d_glist, d_gchunks, d_gcomps,
                     d_gwork, d_csum, d_gz, d_part, d_res2, d_ctrl, d_hist, d_chain_xx,
-                    d_chain_fnorm, d_flag, d_gcnt, d_ucnt, d_lexc[1], d_lexc[2], d_lexc[3],
+                    d_chain_fnorm, d_flag, d_bad, d_gcnt, d_ucnt, d_lexc[1], d_lexc[2], d_lexc[3],
                     d_lexc[4], d_row2[1], d_row2[2], d_row2[3], d_row2[4],
                     d_planoff[1], d_planoff[2], d_planoff[3], d_planoff[4], d_plans,
                     d_cutg, d_send, d_recv};
@@ -308,6 +311,7 @@ fg_plan::~fg_plan() {
         if (p) cudaFree(p);
     for (auto& g : groups)
         for (void* p : g.allocs) cudaFree(p);
+    if (h_stop) cudaFreeHost(h_stop);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (stream2) cudaStreamDestroy(stream2);
@@ -1304,7 +1308,7 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
         (rc = dalloc(&p->d_stage, std::max(P, Z))) || (rc = dalloc(&p->d_zb[0], Z + kPad)) ||
         (rc = dalloc(&p->d_zb[1], Z + kPad)) ||
         (rc = dalloc(&p->d_zs, Z)) || (rc = dalloc(&p->d_ctrl, 1)) ||
-        (rc = dalloc(&p->d_flag, 1)) ||
+        (rc = dalloc(&p->d_flag, 1)) || (rc = dalloc(&p->d_bad, 1)) ||
         (rc = dalloc(&p->d_res2, 2)))
         return rc;
     CK(cudaMemset(p->d_x, 0, P * sizeof(double)));
@@ -1852,13 +1856,20 @@ static int upload_vm(fg_plan* p, const double* src_ref, double* dst) {
     return 0;
 }
 
+// `slot` (0..3 = x, m, u, n; -1 none) records the first non-finite entry
 static int download_ref(fg_plan* p, int mode, const double* ucur,
-                        const double* uprev, double* dst_host) {
+                        const double* uprev, double* dst_host, int slot = -1) {
     cudaStream_t st = p->stream;
+    CK(cudaMemsetAsync(p->d_bad, 0xff, sizeof(unsigned long long), st));
     k_scatter_to_ref<<<nblk(p->P, 256), 256, 0, st>>>(p->P, p->d_vm2ref, p->d_vmz, mode,
-                                                     p->d_x, ucur, uprev, p->zcur(), p->d_stage);
+                                                     p->d_x, ucur, uprev, p->zcur(), p->d_stage,
+                                                     p->d_bad);
     CK(cudaMemcpyAsync(dst_host, p->d_stage, p->P * sizeof(double), cudaMemcpyDeviceToHost, st));
+    unsigned long long bad = ~0ull;
+    if (slot >= 0)
+        CK(cudaMemcpyAsync(&bad, p->d_bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (slot >= 0) p->first_bad[slot] = bad == ~0ull ? -1 : (int64_t)bad;
     return check_launch();
 }
 
@@ -2002,8 +2013,8 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
         launches += (p->chain_on && !first_n) ? p->launches_later : p->launches_per_iter;
         int64_t left = K - 1;
         int chunk = std::max(2, cfg->graph_chunk - (cfg->graph_chunk & 1));
-        int32_t* h_stop = nullptr;
-        CK(cudaMallocHost((void**)&h_stop, 4 * sizeof(int32_t)));
+        if (!p->h_stop) CK(cudaMallocHost((void**)&p->h_stop, 4 * sizeof(int32_t)));
+        int32_t* h_stop = p->h_stop;
         cudaEvent_t pe[2];
         CK(cudaEventCreateWithFlags(&pe[0], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&pe[1], cudaEventDisableTiming));
@@ -2057,7 +2068,6 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
         }
         cudaEventDestroy(pe[0]);
         cudaEventDestroy(pe[1]);
-        cudaFreeHost(h_stop);
     }
     float tot = 0;
     cudaEventElapsedTime(&tot, ev0, ev1);
@@ -2119,15 +2129,22 @@ int fg_state_download(fg_plan* p, double* x, double* m, double* z, double* u, do
     if (x || m) {
         if (int rc = materialize_x(p)) return rc;
     }
+    for (auto& b : p->first_bad) b = -1;
     const int cur = (int)(p->completed & 1);
     const double* ucur = p->d_u[cur];
     const double* uprev = p->d_u[cur ^ 1];
     int rc;
-    if (x && (rc = download_ref(p, 0, ucur, uprev, x))) return rc;
-    if (m && (rc = download_ref(p, 1, ucur, uprev, m))) return rc;
-    if (u && (rc = download_ref(p, 2, ucur, uprev, u))) return rc;
-    if (n && (rc = download_ref(p, 3, ucur, uprev, n))) return rc;
+    if (x && (rc = download_ref(p, 0, ucur, uprev, x, 0))) return rc;
+    if (m && (rc = download_ref(p, 1, ucur, uprev, m, 1))) return rc;
+    if (u && (rc = download_ref(p, 2, ucur, uprev, u, 2))) return rc;
+    if (n && (rc = download_ref(p, 3, ucur, uprev, n, 3))) return rc;
     if (z) CK(cudaMemcpy(z, p->zcur(), p->Z * sizeof(double), cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+int fg_state_nonfinite(const fg_plan* p, int64_t* out4) {
+    if (!p || !out4) return fail(FG_ERR_INVALID, "null argument");
+    for (int i = 0; i < 4; ++i) out4[i] = p->first_bad[i];
     return 0;
 }
 

@@ -530,7 +530,8 @@ __global__ void k_gather_from_ref(int64_t P, const int64_t* vm2ref,
 __global__ void k_scatter_to_ref(int64_t P, const int64_t* vm2ref,
                                  const int32_t* vmz, int mode, const double* x,
                                  const double* ucur, const double* uprev,
-                                 const double* z, double* dst_ref) {
+                                 const double* z, double* dst_ref,
+                                 unsigned long long* first_bad) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= P) return;
     double v;
@@ -538,7 +539,11 @@ __global__ void k_scatter_to_ref(int64_t P, const int64_t* vm2ref,
     else if (mode == 1) v = x[p] + uprev[p];
     else if (mode == 2) v = ucur[p];
     else v = z[vmz[p]] - ucur[p];
-    dst_ref[vm2ref[p]] = v;
+    const int64_t r = vm2ref[p];
+    dst_ref[r] = v;
+    // first non-finite entry in reference order (the host reports it
+    // without scanning the downloaded array)
+    if (!isfinite(v)) atomicMin(first_bad, (unsigned long long)r);
 }
 
 // edge-indexed gather: dst[q] = src_ref[ref_edge[q]]

@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import threading
 from collections.abc import Sequence
 import weakref
 from dataclasses import dataclass, field
@@ -38,7 +39,7 @@ from time import perf_counter
 import numpy as np
 
 from . import _native
-from .prox import operator_class
+from .prox import ProxFactor, operator_class
 
 PHASES = ("x", "m", "z", "u", "n")
 
@@ -262,8 +263,11 @@ class DevicePlan:
     # -- parameters -----------------------------------------------------------
     def host_checks(self, graph):
         """Kind validations the reference raises from batch_eval
-        (radius rho > kappa, injected failures)."""
+        (radius rho > kappa, injected failures).  Kinds without one are
+        skipped before their rho columns are gathered."""
         for cls, dims, fe, _dp, params_list, sizes in self.groups:
+            if getattr(cls.host_check, "__func__", None) is ProxFactor.host_check.__func__:
+                continue
             off = 0
             for params, sz in zip(params_list, sizes):
                 rhos = [graph.edge_rho[fe[off:off + sz] + j] for j in range(len(dims))]
@@ -314,6 +318,13 @@ class DevicePlan:
                 raise ValueError("state arrays must be C-contiguous float64")
         _native.check(self._lib.fg_state_download(
             self._h, *[_native.dptr(a) if a is not None else None for a in outs]))
+
+    def nonfinite(self):
+        """{name: first non-finite ref index or -1} for x, m, u, n of the
+        last download (found on the device during the scatter)."""
+        out = np.zeros(4, dtype=np.int64)
+        _native.check(self._lib.fg_state_nonfinite(self._h, _native.i64ptr(out)))
+        return dict(zip(("x", "m", "u", "n"), (int(v) for v in out)))
 
     def evaluate(self, z=None):
         """(objective, max violation) at z (None: the device's current z)."""
@@ -415,11 +426,14 @@ def _check_state(graph, state):
         raise ValueError(f"state.z must have shape ({graph.z_dim},)")
 
 
-def _nonfinite_message(graph, arr, phase, iteration):
-    bad = np.nonzero(~np.isfinite(arr))[0]
-    if bad.size == 0:
+def _nonfinite_message(graph, arr, phase, iteration, first=None):
+    """Reference text for the first non-finite entry of ``arr`` (or of the
+    entry at index ``first`` already located; -1 = none)."""
+    if first is None:
+        bad = np.nonzero(~np.isfinite(arr))[0]
+        first = int(bad[0]) if bad.size else -1
+    if first < 0:
         return None
-    first = int(bad[0])
     if phase == "z":
         v = int(np.searchsorted(graph.var_offsets, first, side="right") - 1)
         return f"non-finite value after z update at iteration {iteration}: variable {v}"
@@ -548,11 +562,11 @@ def _raise_device_error(graph, plan, state, res):
 class Solution(Sequence):
     """The consensus vector unpacked per variable (reference
     ``engine.py:521-522`` returns a list of per-variable copies).  Items
-    are views of a private copy of z, made on access, so building the
-    result is O(1) even for millions of variables."""
+    are made on access from a private copy of z, so building the result
+    is one copy even for millions of variables."""
 
-    def __init__(self, z, var_offsets):
-        self._z = np.array(z, dtype=np.float64, copy=True)
+    def __init__(self, z, var_offsets, copy=True):
+        self._z = np.array(z, dtype=np.float64, copy=True) if copy else z
         self._off = np.asarray(var_offsets)
 
     def __len__(self):
@@ -608,11 +622,22 @@ def run(graph, config, state=None):
             outs[k] = a
         else:
             outs[k] = np.empty(a.shape)
-    plan.download(**outs)
+    # z first; the solution's private copy of it is made on the host while
+    # the payload arrays stream back
+    plan.download(z=outs["z"])
+    sol_z = {}
+    copier = threading.Thread(target=lambda: sol_z.setdefault("z", outs["z"].copy()))
+    copier.start()
+    try:
+        plan.download(x=outs["x"], m=outs["m"], u=outs["u"], n=outs["n"])
+    finally:
+        copier.join()
     for k, a in outs.items():
         if a is not getattr(state, k):
             _assign(getattr(state, k), a)
-    msg = _nonfinite_message(graph, state.n, "n", executed)
+    # final n check (reference engine.py:519) from the index the device
+    # found during the download, without a host scan
+    msg = _nonfinite_message(graph, None, "n", executed, first=plan.nonfinite()["n"])
     base_iteration = state.iteration
     if msg:
         state.iteration += executed
@@ -640,7 +665,7 @@ def run(graph, config, state=None):
     if executed:
         state.last_residuals = (float(hist[executed - 1, 0]), float(hist[executed - 1, 1]))
     del tol_check
-    solution = Solution(state.z, graph.var_offsets)
+    solution = Solution(sol_z["z"], graph.var_offsets, copy=False)
     report = RunReport(iterations=executed, converged=converged, workers=config.workers,
                        phase_seconds=phase_totals, history=history,
                        total_seconds=max(total, dev), device_seconds=dev,

@@ -170,6 +170,40 @@ def test_overflow_in_z_is_reported_as_variable(gpu):
         fg.run(g, fg.RunConfig(max_iterations=3))
 
 
+def test_download_locates_first_nonfinite_entry(gpu):
+    """The device records, during the download scatter, the first
+    non-finite entry of each payload array in reference edge order; the
+    final n check (reference engine.py:519) is built from it and must name
+    the same edge a host scan of the downloaded n names."""
+    from paper_1603_02526_b200 import engine
+    g = fg.build_packing(fg.PackingSpec(30))
+    st = fg.init_state(g, seed=1)
+    P = g.total_edge_payload
+    z, u, n = st.z.copy(), st.u.copy(), st.n.copy()
+    rng = np.random.default_rng(0)
+    picks = np.sort(rng.choice(P, 5, replace=False))
+    u[picks[1:]] = -1.7e308                      # n = z - u overflows there
+    z[:] = 1.7e308
+    u[picks[0]] = np.nan
+    plan = engine.device_plan(g)
+    plan.sync(g)
+    plan.upload(z, u, n)
+    out = {k: np.empty(P) for k in "xmun"}
+    plan.download(**out, z=np.empty(g.z_dim))
+    bad = plan.nonfinite()
+    for k in "xmun":
+        scan = np.nonzero(~np.isfinite(out[k]))[0]
+        assert bad[k] == (int(scan[0]) if scan.size else -1), k
+    assert bad["u"] == picks[0] and bad["n"] == picks[0]
+    msg = engine._nonfinite_message(g, None, "n", 7, first=bad["n"])
+    assert msg == engine._nonfinite_message(g, out["n"], "n", 7)
+    assert msg.startswith("non-finite value after n update at iteration 7: edge ")
+    # a clean download resets the record
+    plan.upload(st.z, st.u, st.n)
+    plan.download(**out, z=np.empty(g.z_dim))
+    assert plan.nonfinite() == {"x": -1, "m": -1, "u": -1, "n": -1}
+
+
 # ---- operators: device batch_eval vs the reference's own outputs ----------
 
 def _params(gd, kind):
