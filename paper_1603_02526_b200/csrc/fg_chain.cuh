@@ -593,6 +593,184 @@ __global__ void __launch_bounds__(kChainThreads, MINB) k_svm_chain_unit(PassB b,
     }
 }
 
+// ---------------------------------------------------------------------------
+// Unit-weight form with a per-warp cp.async double buffer: while a warp
+// computes point i, the 9 rows point i + 8 reads from u and z (u slots
+// -1..3 and 6 of its w edges, z of w_{i-1..i+1}) are already in flight
+// into the warp's other buffer (16-byte cp.async.cg, L2 only: half a warp
+// per row), and its margin row and per-lane scalar into registers, so every
+// warp keeps one point's loads outstanding instead of stalling on them.
+// Needs 16-byte aligned u/z rows (pW, zW even; checked at plan time).
+// Arithmetic is k_svm_chain_unit's, operand for operand: bitwise equal.
+constexpr int kPfRows = 9;
+constexpr int kPfBuf = kPfRows * 32;                  // doubles per warp buffer
+
+__device__ __forceinline__ void chain_cp16(double* dst, const double* src) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src));
+}
+
+template <int D, int MINB>
+__global__ void __launch_bounds__(kChainThreads, MINB) k_svm_chain_unit_pf(PassB b, ChainDev c,
+                                                                       double* xb_out,
+                                                                       int64_t part_off) {
+    static_assert(D == 32, "one lane per component");
+    __shared__ double sm[16];
+    __shared__ __align__(16) double s_pf[kChainThreads / 32][2][kPfBuf];
+    __shared__ double s_sc[kChainThreads / 32][32];
+    if (b.ctrl->stop) return;
+    const int64_t it = b.ctrl->iter;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int32_t nin = c.n - 2;
+    const int32_t per_cta = (nin + gridDim.x - 1) / gridDim.x;
+    const int32_t i0 = 1 + blockIdx.x * per_cta;
+    const int32_t i1 = min(c.n - 1, i0 + per_cta);
+    const double* sb = c.xx;
+    int32_t ss = 0;
+    switch (lane) {
+        case kUY: sb = c.fp_margin + D; ss = c.st_margin; break;
+        case kUFN: sb = c.fnorm; ss = 1; break;
+        case kULam: sb = c.fp_slack; ss = c.st_slack; break;
+        case kUZX: sb = b.zin + c.zX; ss = 1; break;
+        case kUUX0: sb = b.uin + c.pX; ss = 2; break;
+        case kUUX1: sb = b.uin + c.pX + 1; ss = 2; break;
+        case kUZB: sb = b.zin + c.zB; ss = 0; break;
+        case kUUB: sb = b.uin + c.pB; ss = 1; break;
+        case kUXX: sb = c.xx; ss = 1; break;
+        default: break;
+    }
+    const int h = lane >> 4, c2 = (lane & 15) * 2;
+    auto issue = [&](int32_t i, double* B) {
+        const double* U = b.uin + c.pW + (int64_t)(4 * i - 1) * D + c2;
+        const double* Z = b.zin + c.zW + (int64_t)i * D + c2;
+        chain_cp16(B + h * 32 + c2, U + (h ? 0 : -D));              // u rows -1, 0
+        chain_cp16(B + (2 + h) * 32 + c2, U + (h ? 2 * D : D));     // u rows 1, 2
+        chain_cp16(B + (4 + h) * 32 + c2, U + (h ? 6 * D : 3 * D)); // u rows 3, 6
+        chain_cp16(B + (6 + h) * 32 + c2, Z + (h ? 0 : -D));        // z rows -1, 0
+        if (!h) chain_cp16(B + 8 * 32 + c2, Z + D);                 // z row 1
+    };
+    double pp = 0.0, dd = 0.0;
+    bool bn = false, bx = false, bm = false, bz = false, bu = false;
+    auto S = [&](double v, int src) { return __shfl_sync(kFull, v, src); };
+    constexpr int32_t NW = kChainThreads / 32;
+    double* sc = s_sc[warp];
+    int k = 0;
+    double Xn = 0.0, svn = 0.0;
+    if (i0 + warp < i1) {
+        issue(i0 + warp, s_pf[warp][0]);
+        Xn = c.fp_margin[(int64_t)(i0 + warp) * c.st_margin + lane];
+        svn = sb[(int64_t)(i0 + warp) * ss];
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+#pragma unroll 1
+    for (int32_t i = i0 + warp; i < i1; i += NW) {
+        const double X = Xn, sv = svn;
+        __syncwarp();                               // the other buffer's reads are done
+        if (i + NW < i1) {
+            issue(i + NW, s_pf[warp][k ^ 1]);
+            Xn = c.fp_margin[(int64_t)(i + NW) * c.st_margin + lane];
+            svn = sb[(int64_t)(i + NW) * ss];
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        sc[lane] = sv;
+        __syncwarp();
+        const double* B = s_pf[warp][k];
+        k ^= 1;
+        const double up = B[lane], u0 = B[32 + lane], u1 = B[64 + lane];
+        const double u2 = B[96 + lane], u3 = B[128 + lane], un_ = B[160 + lane];
+        const double zp = B[192 + lane], zi = B[224 + lane], zn_ = B[256 + lane];
+        const int64_t wo = c.pW + (int64_t)(4 * i - 1) * D + lane;
+        const int64_t zo = c.zW + (int64_t)i * D + lane;
+        // ---- phase n ----
+        const double n0 = zi - u0, n1 = zi - u1, n2 = zi - u2, n3 = zi - u3;
+        const double np_ = zp - up, nn_ = zn_ - un_;
+        const double zxi = sc[kUZX], ux0 = sc[kUUX0], ux1 = sc[kUUX1];
+        const double nb = sc[kUZB] - sc[kUUB], nx0 = zxi - ux0, nx1 = zxi - ux1;
+        const double sn = ((n0 + n1) + (n2 + n3)) + ((np_ + nn_) + ((nb + nx0) + nx1));
+        if (!finite(sn))
+            bn |= !(finite(n0) && finite(n1) && finite(n2) && finite(n3) && finite(np_) &&
+                    finite(nn_) && finite(nb) && finite(nx0) && finite(nx1));
+        // ---- phase x ----
+        const double x0 = sc[kUFN] * n0;                    // prox_svm_norm
+        const double pr = n1 * X;
+        const int g = lane & 7;
+        double dot = 0.0;
+        dot += S(pr, g);
+        dot += S(pr, g + 8);
+        dot += S(pr, g + 16);
+        dot += S(pr, g + 24);
+        dot += __shfl_xor_sync(kFull, dot, 1);
+        dot += __shfl_xor_sync(kFull, dot, 2);
+        dot += __shfl_xor_sync(kFull, dot, 4);
+        const double Y = sc[kUY];
+        const double slack = (1.0 - nx1) - Y * (dot + nb);
+        const double denom = (sc[kUXX] + 1.0) + 1.0;
+        const double mu = ddiv(np_max0(slack), denom);
+        const double x1 = n1 + (mu * Y) * X;
+        const double xbv = nb + mu * Y;
+        const double xx1 = nx1 + mu;
+        const double xx0 = np_max0(nx0 - sc[kULam]);       // prox_svm_slack
+        const double x2 = (np_ + n2) * 0.5;                    // prox_equality
+        const double x3 = (n3 + nn_) * 0.5;
+        // ---- phases m, z, u of w_i: z weight 4 ----
+        const double m0 = x0 + u0, m1 = x1 + u1, m2 = x2 + u2, m3 = x3 + u3;
+        double res = 0.0;
+        res += m1;
+        res += m2;
+        res += m3;
+        const double zn = (m0 + res) * 0.25;
+        b.z[zo] = zn;
+        const double dz = zn - zi;
+        const double t0 = x0 - zn, t1 = x1 - zn, t2 = x2 - zn, t3 = x3 - zn;
+        const double v0 = u0 + t0, v1 = u1 + t1, v2 = u2 + t2, v3 = u3 + t3;
+        double* __restrict__ UO = b.uout + wo;
+        UO[0] = v0; UO[D] = v1; UO[2 * D] = v2; UO[3 * D] = v3;
+        pp += t0 * t0; pp += t1 * t1; pp += t2 * t2; pp += t3 * t3;
+        const double dz2 = dz * dz;
+        dd += dz2; dd += dz2; dd += dz2; dd += dz2;
+        if (!finite((m0 + m1) + (m2 + m3))) {
+            const bool mbad = !(finite(m0) && finite(m1) && finite(m2) && finite(m3));
+            if (mbad) bx |= !(finite(x0) && finite(x1) && finite(x2) && finite(x3));
+            bm |= mbad;
+        }
+        bz |= !finite(zn);
+        if (!finite((v0 + v1) + (v2 + v3)))
+            bu |= !(finite(v0) && finite(v1) && finite(v2) && finite(v3));
+        // ---- xi_i (slack, margin; z weight 2) and b's margin x ----
+        if (lane == 0) {
+            const double mx0 = xx0 + ux0, mx1 = xx1 + ux1;
+            double rs = 0.0;
+            rs += mx1;
+            const double zx = (mx0 + rs) * 0.5;
+            b.z[c.zX + i] = zx;
+            const double dzx = zx - zxi;
+            const double s0 = xx0 - zx, s1 = xx1 - zx;
+            const double w0 = ux0 + s0, w1 = ux1 + s1;
+            b.uout[c.pX + 2 * (int64_t)i] = w0;
+            b.uout[c.pX + 2 * (int64_t)i + 1] = w1;
+            xb_out[c.pB + i] = xbv;
+            pp += s0 * s0; pp += s1 * s1;
+            dd += dzx * dzx; dd += dzx * dzx;
+            bx |= !(finite(xbv) && finite(xx0) && finite(xx1));
+            bm |= !(finite(mx0) && finite(mx1));
+            bz |= !finite(zx);
+            bu |= !(finite(w0) && finite(w1));
+        }
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    if (bn) flag_error(b.ctrl, it - 1, FG_PHASE_N, true);
+    if (bx) flag_error(b.ctrl, it, FG_PHASE_X, true);
+    if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
+    if (bz) flag_error(b.ctrl, it, FG_PHASE_Z, false);
+    if (bu) flag_error(b.ctrl, it, FG_PHASE_U, false);
+    block_sum2<kChainThreads>(pp, dd, sm);
+    if (threadIdx.x == 0) {
+        b.part[2 * (part_off + blockIdx.x)] = pp;
+        b.part[2 * (part_off + blockIdx.x) + 1] = dd;
+    }
+}
+
 // 1 / (1 + scale_i): prox_svm_norm's factor at unit edge weight
 // (ddiv(R, R + scale) with R = 1.0, the same IEEE division)
 __global__ void k_chain_fnorm(ChainDev c, double* fnorm) {

@@ -240,6 +240,7 @@ struct fg_plan {
     ChainDev chain{};
     int64_t chain_grid = 0;
     int chain_minb = 2;                // CTAs/SM the kernel is compiled for (A/B)
+    bool chain_pf = false;             // unit chain with cp.async prefetch (A/B)
     bool chain_fast = false;           // D == 32: fast form for interior points
     bool chain_unit = false;           // all weights 1 (checked at every sync)
     double* d_chain_xx = nullptr;      // per point x.x of the margin data
@@ -657,6 +658,8 @@ void part_post(fg_plan* p, cudaStream_t st) {
 // CTAs of the chain kernel for interior points: one resident wave (the
 // kernels loop over their points), at most the partial slots it replaces
 // minus the end-point slot.
+constexpr bool kChainPfDefault = false;
+
 int64_t chain_main_grid(const fg_plan* p) {
     if (p->mpc_chain) return p->mpc_tiles - 1;   // the MPC chain writes mpc_tiles slots
     const int64_t wave = p->chain_fast ? (p->chain_unit ? 148 * 4 : 148 * 2) : 148 * 2;
@@ -679,7 +682,9 @@ void chain_pass(fg_plan* p, int in, cudaStream_t st) {
         cudaEventRecord(p->ev_fork, st);
         // interior points on the fast (or unit-weight) form, the two end
         // points (degree 3) on the generic form in the next partial slot
-        if (p->chain_unit && p->chain_minb == 3)
+        if (p->chain_unit && p->chain_pf)
+            k_svm_chain_unit_pf<32, 4><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
+        else if (p->chain_unit && p->chain_minb == 3)
             k_svm_chain_unit<32, 3><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
         else if (p->chain_unit)
             k_svm_chain_unit<32, 4><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
@@ -892,6 +897,16 @@ void detect_svm_chain(fg_plan* p, const std::vector<int32_t>& dim,
     // CTAs/SM the kernels are compiled for (A/B in profiles/): generic form
     // 2 (3 spills heavily); unit form 4 (0.59 ms vs 0.67 ms at 3, SVM 1M)
     p->chain_minb = getenv("FGADMM_CHAIN_OCC3") ? 3 : 2;
+    // unit form with the per-warp cp.async double buffer (A/B)
+    {
+        const char* e = getenv("FGADMM_CHAIN_PF");
+        p->chain_pf = e ? e[0] == '1' : kChainPfDefault;
+        // 16-byte cp.async rows: w's payload and z bases must be even
+        p->chain_pf = p->chain_pf && (c.pW % 2 == 0) && (c.zW % 2 == 0);
+    }
+    if (p->chain_pf)
+        cudaFuncSetAttribute(k_svm_chain_unit_pf<32, 4>,
+                             cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (cudaMalloc((void**)&p->d_chain_xx, n * sizeof(double)) != cudaSuccess) return;
     c.xx = p->d_chain_xx;
     k_chain_xx<<<(unsigned)((n + 255) / 256), 256, 0, p->stream>>>(c, p->d_chain_xx);

@@ -62,6 +62,27 @@ def test_chain_bitwise_equals_generic(gpu, monkeypatch, n, dim, iters):
     assert rc[0].kernel_launches < rg[0].kernel_launches
 
 
+@pytest.mark.parametrize("env", [{"FGADMM_CHAIN_PF": "1"}, {"FGADMM_CHAIN_PF": "0"},
+                                 {"FGADMM_CHAIN_OCC3": "1", "FGADMM_CHAIN_PF": "0"}])
+def test_chain_variants_bitwise(gpu, monkeypatch, env):
+    """Compiled variants of the unit-weight chain (cp.async prefetch
+    buffer, occupancy) equal the generic path bitwise."""
+    g = svm_graph(20_000, 32, seed=9)
+    st = fg.init_state(g, seed=2)
+    outs = []
+    for chain in (True, False):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        plan_for(g, monkeypatch, chain)
+        s = copy(st)
+        fg.run(g, fg.RunConfig(max_iterations=11), state=s)
+        if chain:
+            assert _PLANS[g].chain_form() == "unit"
+        outs.append(s)
+    for k in "xmzun":
+        np.testing.assert_array_equal(getattr(outs[0], k), getattr(outs[1], k), err_msg=k)
+
+
 def test_chain_matches_oracle(gpu, monkeypatch):
     g = svm_graph(3000, 32, seed=11)
     plan_for(g, monkeypatch, True)
