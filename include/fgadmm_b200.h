@@ -167,6 +167,12 @@ int fg_plan_sync_params(fg_plan* plan, const double* edge_rho,
                         const double* edge_alpha, const double* z_weights);
 
 /* ---- fused run (the hot path) ------------------------------------------ */
+/* z and u are on the device when fg_state_upload returns; n may still be in
+ * flight (it is compared with z[zmap] - u on a copy stream while the next
+ * fg_run starts from n = z - u, and fg_run repeats the run from the
+ * uploaded state if they differ), so the n buffer must stay valid and
+ * unchanged until the next call on the plan.  Plans attached to NCCL (and
+ * FGADMM_SPEC_UPLOAD=0) upload all three synchronously. */
 int fg_state_upload(fg_plan* plan, const double* z, const double* u,
                     const double* n);
 int fg_run(fg_plan* plan, const fg_run_config* cfg, double* history,

@@ -162,6 +162,14 @@ struct fg_plan {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t stream2 = nullptr;     // forked branch (chain end points)
+    // speculative upload: n streams in (and is checked against z - u) on
+    // stream_copy while the run already executes with n = z - u
+    cudaStream_t stream_copy = nullptr;
+    cudaEvent_t ev_up = nullptr, ev_up2 = nullptr, ev_chk = nullptr;
+    double* d_stage2 = nullptr;         // uploaded n, reference order
+    int32_t* d_chk = nullptr;
+    int32_t* h_chk = nullptr;           // pinned copy of the check flag
+    int n_pending = 0;                  // upload check in flight
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t V = 0, E = 0, P = 0, Z = 0;
     // var tables
@@ -289,6 +297,9 @@ struct fg_plan {
 };
 
 void fg_nccl_release(void* comm);   // defined with the NCCL loader below
+extern "C" {
+static int settle_idle(fg_plan* p);  // pending upload check (defined with the upload)
+}
 
 fg_plan::~fg_plan() {
     cudaSetDevice(device);
@@ -296,7 +307,7 @@ fg_plan::~fg_plan() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     void* ptrs[] = {d_dim, d_deg, d_ebase, d_pbase, d_zbase, d_zvar, d_vm2ref,
                     d_vmz, d_vmvar, d_refedge, d_rho, d_alpha, d_zw, d_x,
-                    d_u[0], d_u[1], d_stage, d_aux, d_zb[0], d_zb[1], d_zs, d_sruns,
+                    d_u[0], d_u[1], d_stage, d_stage2, d_chk, d_aux, d_zb[0], d_zb[1], d_zs, d_sruns,
                     d_sblk[0], d_sblk[1], d_sblk[2], d_lvars[1], d_lvars[2], d_lvars[3],
                     d_lvars[4], d_lvprog[1], d_lvprog[2], d_lvprog[3], d_lvprog[4],
                     d_stiles,
@@ -313,6 +324,10 @@ fg_plan::~fg_plan() {
     for (auto& g : groups)
         for (void* p : g.allocs) cudaFree(p);
     if (h_stop) cudaFreeHost(h_stop);
+    if (h_chk) cudaFreeHost(h_chk);
+    for (cudaEvent_t e : {ev_up, ev_up2, ev_chk})
+        if (e) cudaEventDestroy(e);
+    if (stream_copy) cudaStreamDestroy(stream_copy);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (stream2) cudaStreamDestroy(stream2);
@@ -1714,6 +1729,7 @@ static int sync_unit_flags(fg_plan* p);
 int fg_plan_sync_params(fg_plan* p, const double* rho, const double* alpha,
                         const double* zw) {
     CK(cudaSetDevice(p->device));
+    if (int rc = settle_idle(p)) return rc;
     cudaStream_t st = p->stream;
     CK(cudaMemcpyAsync(p->d_stage, rho, p->E * sizeof(double), cudaMemcpyHostToDevice, st));
     k_gather_edges<<<nblk(p->E, 256), 256, 0, st>>>(p->E, p->d_refedge, p->d_stage, p->d_rho);
@@ -1888,8 +1904,102 @@ static int download_ref(fg_plan* p, int mode, const double* ucur,
     return check_launch();
 }
 
+// Wait for an in-flight upload check; *mismatch = the uploaded n differs
+// from z[zmap] - u somewhere.
+static int settle_upload(fg_plan* p, int* mismatch) {
+    *mismatch = 0;
+    if (!p->n_pending) return 0;
+    CK(cudaEventSynchronize(p->ev_chk));
+    p->n_pending = 0;
+    *mismatch = *p->h_chk != 0;
+    return check_launch();
+}
+
+// Settle before any entry point other than fg_run touches the state or
+// the staging buffers.  No iteration has run since the upload, so on a
+// mismatch only d_u[1] needs the uploaded n.
+static int settle_idle(fg_plan* p) {
+    int mism = 0;
+    if (int rc = settle_upload(p, &mism)) return rc;
+    if (mism) {
+        k_gather_from_ref<<<nblk(p->P, 256), 256, 0, p->stream>>>(p->P, p->d_vm2ref,
+                                                                 p->d_stage2, p->d_u[1]);
+        CK(cudaStreamSynchronize(p->stream));
+        p->n_valid = 1;
+    }
+    return check_launch();
+}
+
+// Upload with n in flight: z and u are copied and the first n is taken as
+// z[zmap] - u (what every state init_state or a run produced satisfies
+// bitwise), so the run can start at once; n itself follows on stream_copy
+// and k_n_check_ref compares it, from the staging buffers, concurrently
+// with the iterations.  fg_run settles the check at its end and, on a
+// mismatch, restores the uploaded state and runs again reading n.
+static int upload_speculative(fg_plan* p, const double* z, const double* u, const double* n) {
+    cudaStream_t st = p->stream;
+    if (!p->stream_copy) {
+        CK(cudaStreamCreateWithFlags(&p->stream_copy, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&p->ev_up, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&p->ev_up2, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&p->ev_chk, cudaEventDisableTiming));
+        CK(cudaMallocHost((void**)&p->h_chk, sizeof(int32_t)));
+        if (int rc = dalloc(&p->d_stage2, p->P)) return rc;
+        if (int rc = dalloc(&p->d_chk, 1)) return rc;
+    }
+    CK(cudaMemcpyAsync(p->d_zb[0], z, p->Z * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(p->d_stage, u, p->P * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(p->ev_up, st));               // z, u transferred: n may follow
+    k_gather_from_ref<<<nblk(p->P, 256), 256, 0, st>>>(p->P, p->d_vm2ref, p->d_stage, p->d_u[0]);
+    CK(cudaMemcpyAsync(p->d_zs, p->d_zb[0], p->Z * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    k_phase_n<<<nblk(p->P, 256), 256, 0, st>>>(p->P, p->d_vmz, p->d_zb[0], p->d_u[0], p->d_u[1]);
+    CK(cudaEventRecord(p->ev_up2, st));
+    cudaStream_t cs = p->stream_copy;
+    CK(cudaStreamWaitEvent(cs, p->ev_up, 0));
+    CK(cudaMemcpyAsync(p->d_stage2, n, p->P * sizeof(double), cudaMemcpyHostToDevice, cs));
+    CK(cudaStreamWaitEvent(cs, p->ev_up2, 0));
+    CK(cudaMemsetAsync(p->d_chk, 0, sizeof(int32_t), cs));
+    k_n_check_ref<<<std::min<unsigned>(nblk(p->P, 256), 148 * 8), 256, 0, cs>>>(
+        p->P, p->d_vm2ref, p->d_vmz, p->d_zs, p->d_stage, p->d_stage2, p->d_chk);
+    CK(cudaMemcpyAsync(p->h_chk, p->d_chk, sizeof(int32_t), cudaMemcpyDeviceToHost, cs));
+    CK(cudaEventRecord(p->ev_chk, cs));
+    CK(cudaStreamSynchronize(st));                   // z and u are on the device
+    p->n_pending = 1;
+    p->completed = 0;
+    p->n_valid = p->chain_on ? 0 : 1;   // chain: iteration 1 needs no n; else d_u[1] = z - u
+    p->x_stale = 0;
+    return check_launch();
+}
+
+// The uploaded state again after a speculative run found n inconsistent.
+static int restore_upload(fg_plan* p) {
+    cudaStream_t st = p->stream;
+    CK(cudaMemcpyAsync(p->d_zb[0], p->d_zs, p->Z * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    k_gather_from_ref<<<nblk(p->P, 256), 256, 0, st>>>(p->P, p->d_vm2ref, p->d_stage, p->d_u[0]);
+    k_gather_from_ref<<<nblk(p->P, 256), 256, 0, st>>>(p->P, p->d_vm2ref, p->d_stage2, p->d_u[1]);
+    CK(cudaStreamSynchronize(st));
+    p->completed = 0;
+    p->n_valid = 1;
+    p->x_stale = 0;
+    return check_launch();
+}
+
+static bool spec_upload_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("FGADMM_SPEC_UPLOAD");
+        return e ? e[0] == '1' : true;
+    }();
+    return on;
+}
+
 int fg_state_upload(fg_plan* p, const double* z, const double* u, const double* n) {
     CK(cudaSetDevice(p->device));
+    {
+        int mism = 0;                    // a previous upload's check is dropped
+        if (int rc = settle_upload(p, &mism)) return rc;
+    }
+    // multi-rank runs stay in lock step: no speculative first iterations
+    if (spec_upload_enabled() && !p->nccl_comm) return upload_speculative(p, z, u, n);
     CK(cudaMemcpyAsync(p->d_zb[0], z, p->Z * sizeof(double), cudaMemcpyHostToDevice, p->stream));
     upload_vm(p, u, p->d_u[0]);
     upload_vm(p, n, p->d_u[1]);   // consumed by the first edge pass
@@ -2089,6 +2199,16 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
     if (int rc = check_launch()) return rc;
+    if (p->n_pending) {
+        int mism = 0;
+        if (int rc = settle_upload(p, &mism)) return rc;
+        if (mism) {
+            // the uploaded n is not z - u: this run assumed otherwise, so
+            // start again from the uploaded state, reading n
+            if (int rc = restore_upload(p)) return rc;
+            return fg_run(p, cfg, history, out);
+        }
+    }
     CK(cudaMemcpy(&h, p->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
     p->completed = h.completed;
     // x of the last (or failing) iteration stays in registers when the
@@ -2141,6 +2261,7 @@ static int materialize_x(fg_plan* p) {
 
 int fg_state_download(fg_plan* p, double* x, double* m, double* z, double* u, double* n) {
     CK(cudaSetDevice(p->device));
+    if (int rc = settle_idle(p)) return rc;
     if (x || m) {
         if (int rc = materialize_x(p)) return rc;
     }
@@ -2165,6 +2286,7 @@ int fg_state_nonfinite(const fg_plan* p, int64_t* out4) {
 
 int fg_debug_download(fg_plan* p, int32_t buffer, double* out_ref) {
     CK(cudaSetDevice(p->device));
+    if (int rc = settle_idle(p)) return rc;
     const double* src = nullptr;
     switch (buffer) {
         case FG_BUF_X:
@@ -2189,6 +2311,7 @@ int fg_debug_download(fg_plan* p, int32_t buffer, double* out_ref) {
 int fg_phase_upload(fg_plan* p, const double* x, const double* m, const double* z,
                     const double* u, const double* n) {
     CK(cudaSetDevice(p->device));
+    if (int rc = settle_idle(p)) return rc;
     if (!p->d_aux) {
         int rc = dalloc(&p->d_aux, p->P);
         if (rc) return rc;
@@ -2207,6 +2330,7 @@ int fg_phase_upload(fg_plan* p, const double* x, const double* m, const double* 
 
 int fg_phase(fg_plan* p, int32_t phase) {
     CK(cudaSetDevice(p->device));
+    if (int rc = settle_idle(p)) return rc;
     if (!p->d_aux) return fail(FG_ERR_INVALID, "fg_phase_upload must precede fg_phase");
     cudaStream_t st = p->stream;
     Ctrl h{};
@@ -2234,6 +2358,7 @@ int fg_phase(fg_plan* p, int32_t phase) {
 
 int fg_phase_download(fg_plan* p, double* x, double* m, double* z, double* u, double* n) {
     CK(cudaSetDevice(p->device));
+    if (int rc = settle_idle(p)) return rc;
     if (!p->d_aux) return fail(FG_ERR_INVALID, "fg_phase_upload must precede fg_phase_download");
     int rc;
     if (x && (rc = download_ref(p, 2, p->d_x, p->d_x, x))) return rc;
@@ -2247,6 +2372,7 @@ int fg_phase_download(fg_plan* p, double* x, double* m, double* z, double* u, do
 int fg_residuals(fg_plan* p, const double* x, const double* z, const double* zprev,
                  double* primal, double* dual) {
     CK(cudaSetDevice(p->device));
+    if (int rc = settle_idle(p)) return rc;
     cudaStream_t st = p->stream;
     double* xs = p->d_aux ? p->d_aux : p->d_u[1];
     upload_vm(p, x, xs);
@@ -2277,6 +2403,7 @@ int fg_residuals(fg_plan* p, const double* x, const double* z, const double* zpr
 int fg_profile_kernels(fg_plan* p, int64_t iterations, int32_t max_slots,
                        char* labels, double* ms, int64_t* counts, int32_t* nslots) {
     CK(cudaSetDevice(p->device));
+    if (int rc = settle_idle(p)) return rc;
     cudaStream_t st = p->stream;
     if (p->hist_cap < iterations) {
         if (p->d_hist) cudaFree(p->d_hist);
@@ -2539,6 +2666,7 @@ int fg_nccl_unique_id(const char* nccl_lib, char* out128) {
 int fg_plan_attach_nccl(fg_plan* p, const char* nccl_lib, const char* id128, int32_t rank,
                         int32_t world) {
     CK(cudaSetDevice(p->device));
+    if (int rc = settle_idle(p)) return rc;
     if (int rc = nccl_load(nccl_lib)) return rc;
     if (world < 1 || rank < 0 || rank >= world) return fail(FG_ERR_INVALID, "bad rank/world");
     NcclId id;
@@ -2589,6 +2717,7 @@ int fg_group_run(fg_plan** plans, int32_t G, const fg_run_config* cfg, double* h
             return fail(FG_ERR_INVALID, "group plans must share one device and cut vector");
         p->world = G;
         p->rank = r;
+        if (int rc = settle_idle(p)) return rc;
         if (int rc = rebase_slots(p)) return rc;
         if (!p->n_valid) first_n = false;
         p->n_valid = 0;
@@ -2691,6 +2820,7 @@ int fg_group_run(fg_plan** plans, int32_t G, const fg_run_config* cfg, double* h
 
 extern "C" int fg_evaluate(fg_plan* p, const double* z_host, double* out2) {
     CK(cudaSetDevice(p->device));
+    if (int rc = settle_idle(p)) return rc;
     cudaStream_t st = p->stream;
     const double* z = p->zcur();
     if (z_host) {

@@ -600,6 +600,20 @@ __global__ void k_n_mismatch(int64_t P, const int32_t* vmz, const double* z,
     if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
 
+// The same test on the upload staging buffers (reference order), so it can
+// run concurrently with iterations that overwrite the var-major state.
+__global__ void k_n_check_ref(int64_t P, const int64_t* vm2ref, const int32_t* vmz,
+                              const double* z, const double* u_ref, const double* n_ref,
+                              int32_t* flag) {
+    bool bad = false;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < P;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = vm2ref[q];
+        bad |= __double_as_longlong(z[vmz[q]] - u_ref[r]) != __double_as_longlong(n_ref[r]);
+    }
+    if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
 __global__ void k_phase_m(int64_t P, const double* x, const double* u, double* m) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p < P) m[p] = x[p] + u[p];

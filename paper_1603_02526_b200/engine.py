@@ -293,6 +293,10 @@ class DevicePlan:
     # -- fused run --------------------------------------------------------------
     def upload(self, z, u, n):
         z, u, n = _native.f64(z), _native.f64(u), _native.f64(n)
+        # n may still be streaming to the device after the call returns (it
+        # is checked against z - u while the run starts): keep it alive
+        # until the next upload
+        self._upload_n = n
         _native.check(self._lib.fg_state_upload(self._h, _native.dptr(z),
                                                 _native.dptr(u), _native.dptr(n)))
 
