@@ -251,6 +251,7 @@ struct fg_plan {
     bool chain_pf = false;             // unit chain with cp.async prefetch (A/B)
     bool chain_fast = false;           // D == 32: fast form for interior points
     bool chain_unit = false;           // all weights 1 (checked at every sync)
+    bool giant_unit = false;           // every rho and alpha 1: giant kernels skip them
     double* d_chain_xx = nullptr;      // per point x.x of the margin data
     double* d_chain_fnorm = nullptr;   // per point 1/(1+scale) (unit form)
     int32_t* d_flag = nullptr;         // scratch device flag
@@ -283,6 +284,8 @@ struct fg_plan {
     int32_t* d_plans = nullptr;
     bool pipe_ok[5] = {false, false, false, false, false};
     bool no_pipe = false;
+    bool row_ring = false;             // persistent class-L row kernel (one job ring per CTA)
+    int64_t ring_grid[5][2] = {};      // resident CTAs of the ring kernel per dim / stage form
     // 2 stages of twice the size: measured better for dim >= 2 rows (pack
     // center rows 0.285 vs 0.306 ms), worse for dim 1 (0.176 vs 0.160)
     bool pipe_big[5] = {false, false, true, true, true};
@@ -460,6 +463,38 @@ void launch_cluster(fg_plan* p, const PassB& b, unsigned grid, int64_t po, cudaS
         b, p->d_clvars[D], p->d_clprog[D], p->d_prog, po);
 }
 
+template <int D>
+void launch_ring(fg_plan* p, const PassB& b, int64_t nrows, int64_t po, cudaStream_t st) {
+    const int big = p->pipe_big[D] ? 1 : 0;
+    const unsigned G = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nrows, p->ring_grid[D][big]));
+    if (big)
+        k_var_row_ring<D, 2, 2 * kPipeStageDoubles><<<G, kRowThreads,
+            row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_lvars[D], p->d_lvprog[D], p->d_prog,
+                                                           p->d_planoff[D], p->d_plans, p->d_lexc[D],
+                                                           po, (int32_t)nrows);
+    else
+        k_var_row_ring<D, kPipeStages, kPipeStageDoubles><<<G, kRowThreads, row_pipe_smem(), st>>>(
+            b, p->d_lvars[D], p->d_lvprog[D], p->d_prog, p->d_planoff[D], p->d_plans, p->d_lexc[D],
+            po, (int32_t)nrows);
+}
+
+template <int D>
+int ring_setup(fg_plan* p, int sms) {
+    const int s0 = (int)row_pipe_smem(), s1 = (int)row_pipe_smem(2, 2 * kPipeStageDoubles);
+    CK(cudaFuncSetAttribute(k_var_row_ring<D, kPipeStages, kPipeStageDoubles>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, s0));
+    CK(cudaFuncSetAttribute(k_var_row_ring<D, 2, 2 * kPipeStageDoubles>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
+    int n0 = 0, n1 = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &n0, k_var_row_ring<D, kPipeStages, kPipeStageDoubles>, kRowThreads, s0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &n1, k_var_row_ring<D, 2, 2 * kPipeStageDoubles>, kRowThreads, s1));
+    p->ring_grid[D][0] = (int64_t)std::max(1, n0) * sms;
+    p->ring_grid[D][1] = (int64_t)std::max(1, n1) * sms;
+    return 0;
+}
+
 template <int MODE>
 bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const double* uin,
                 double* uout, const double* msrc, cudaStream_t st) {
@@ -481,7 +516,9 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
             k_var_small_run<0, MODE><<<grid, 256, 0, st>>>(b, p->d_sruns, p->d_sblk[2], po);
             return true;
         case 3:
-            if (MODE == MODE_FUSED && p->lunit[1] && p->pipe_ok[1] && !p->no_pipe && p->pipe_big[1])
+            if (MODE == MODE_FUSED && p->lunit[1] && p->pipe_ok[1] && !p->no_pipe && p->row_ring)
+                launch_ring<1>(p, b, nb, po, st);
+            else if (MODE == MODE_FUSED && p->lunit[1] && p->pipe_ok[1] && !p->no_pipe && p->pipe_big[1])
                 k_var_row_pipe<1, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, p->d_planoff[1], p->d_plans, p->d_lexc[1], po);
             else if (MODE == MODE_FUSED && p->lunit[1] && p->pipe_ok[1] && !p->no_pipe)
                 k_var_row_pipe<1><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, p->d_planoff[1], p->d_plans, p->d_lexc[1], po);
@@ -497,7 +534,9 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
                 k_var_large_vec<1, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po, nullptr, p->row2_ok[1] ? po + grid : -1);
             return true;
         case 4:
-            if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe && p->pipe_big[2])
+            if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe && p->row_ring)
+                launch_ring<2>(p, b, nb, po, st);
+            else if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe && p->pipe_big[2])
                 k_var_row_pipe<2, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, p->d_planoff[2], p->d_plans, p->d_lexc[2], po);
             else if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe)
                 k_var_row_pipe<2><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, p->d_planoff[2], p->d_plans, p->d_lexc[2], po);
@@ -513,7 +552,9 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
                 k_var_large_vec<2, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po, nullptr, p->row2_ok[2] ? po + grid : -1);
             return true;
         case 5:
-            if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe && p->pipe_big[3])
+            if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe && p->row_ring)
+                launch_ring<3>(p, b, nb, po, st);
+            else if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe && p->pipe_big[3])
                 k_var_row_pipe<3, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, p->d_planoff[3], p->d_plans, p->d_lexc[3], po);
             else if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe)
                 k_var_row_pipe<3><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, p->d_planoff[3], p->d_plans, p->d_lexc[3], po);
@@ -529,7 +570,9 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
                 k_var_large_vec<3, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po, nullptr, p->row2_ok[3] ? po + grid : -1);
             return true;
         case 6:
-            if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe && p->pipe_big[4])
+            if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe && p->row_ring)
+                launch_ring<4>(p, b, nb, po, st);
+            else if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe && p->pipe_big[4])
                 k_var_row_pipe<4, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, p->d_planoff[4], p->d_plans, p->d_lexc[4], po);
             else if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe)
                 k_var_row_pipe<4><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, p->d_planoff[4], p->d_plans, p->d_lexc[4], po);
@@ -548,7 +591,11 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
             k_var_large<MODE><<<grid, kVarThreads, 0, st>>>(b, p->d_llist, p->d_lprog, p->d_prog, po);
             return true;
         case kSlotGiantChunks:
-            if (p->giant_fused)
+            if (p->giant_fused && p->giant_unit)
+                k_var_giant_chunks<MODE, kGiantChunkThreads, true><<<grid, kGiantChunkThreads, p->gtop_smem, st>>>(
+                    b, p->d_glist, p->d_gchunks, p->d_prog, p->d_csum, p->d_gcomps, p->d_gz,
+                    p->d_send, p->d_gcnt);
+            else if (p->giant_fused)
                 k_var_giant_chunks<MODE, kGiantChunkThreads><<<grid, kGiantChunkThreads, p->gtop_smem, st>>>(
                     b, p->d_glist, p->d_gchunks, p->d_prog, p->d_csum, p->d_gcomps, p->d_gz,
                     p->d_send, p->d_gcnt);
@@ -571,8 +618,12 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
         case 14: launch_cluster<4, MODE>(p, b, grid, po, st); return true;
         case kSlotGiantUpdate:
             if (MODE != MODE_FUSED) return false;
-            k_var_giant_update<<<grid, kVarThreads, 0, st>>>(b, p->d_glist, p->d_gwork,
-                                                             p->d_gz, po, p->fr_next);
+            if (p->giant_unit)
+                k_var_giant_update<true><<<grid, kVarThreads, 0, st>>>(b, p->d_glist, p->d_gwork,
+                                                                       p->d_gz, po, p->fr_next);
+            else
+                k_var_giant_update<false><<<grid, kVarThreads, 0, st>>>(b, p->d_glist, p->d_gwork,
+                                                                        p->d_gz, po, p->fr_next);
             return true;
     }
     return false;
@@ -674,6 +725,7 @@ void part_post(fg_plan* p, cudaStream_t st) {
 // kernels loop over their points), at most the partial slots it replaces
 // minus the end-point slot.
 constexpr bool kChainPfDefault = false;
+constexpr bool kRowRingDefault = false;
 
 int64_t chain_main_grid(const fg_plan* p) {
     if (p->mpc_chain) return p->mpc_tiles - 1;   // the MPC chain writes mpc_tiles slots
@@ -1591,6 +1643,16 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
         CK(cudaFuncSetAttribute(k_var_row_pipe<2, 2, 2 * kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
         CK(cudaFuncSetAttribute(k_var_row_pipe<3, 2, 2 * kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
         CK(cudaFuncSetAttribute(k_var_row_pipe<4, 2, 2 * kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+        if (int rc2 = ring_setup<1>(p.get(), sms)) return rc2;
+        if (int rc2 = ring_setup<2>(p.get(), sms)) return rc2;
+        if (int rc2 = ring_setup<3>(p.get(), sms)) return rc2;
+        if (int rc2 = ring_setup<4>(p.get(), sms)) return rc2;
+        {
+            const char* e = getenv("FGADMM_ROW_RING");
+            p->row_ring = e ? e[0] == '1' : kRowRingDefault;
+        }
     }
     p->row_deep = getenv("FGADMM_ROW_DEEP") != nullptr;
     for (int d = 1; d <= 4; ++d) {
@@ -1609,7 +1671,8 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
         if (e != cudaSuccess) return fail(FG_ERR_CUDA, "row cluster kernel shared-memory attribute");
         p->row2_ok[d] = true;
     }
-    p->gtop_smem = (int)(2 * max_top * sizeof(double));
+    // node values (2 per chunk) then the staged top program (int32)
+    p->gtop_smem = (int)(2 * max_top * sizeof(double) + (2 * max_top + 64) * sizeof(int32_t));
     p->giant_fused = getenv("FGADMM_GIANT_UNFUSED") == nullptr;
     p->row256 = getenv("FGADMM_ROW256") != nullptr;
     p->no_fork = getenv("FGADMM_NO_FORK") != nullptr;
@@ -1618,6 +1681,8 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
         CK(cudaFuncSetAttribute(k_var_giant_top<MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
         CK(cudaFuncSetAttribute(k_var_giant_chunks<MODE_FUSED, kGiantChunkThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
         CK(cudaFuncSetAttribute(k_var_giant_chunks<MODE_PHASEZ, kGiantChunkThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+        CK(cudaFuncSetAttribute(k_var_giant_chunks<MODE_FUSED, kGiantChunkThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+        CK(cudaFuncSetAttribute(k_var_giant_chunks<MODE_PHASEZ, kGiantChunkThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
     }
     if ((rc = dalloc(&p->d_gcnt, std::max<size_t>(1, glist.size()))) || (rc = dalloc(&p->d_ucnt, 1)))
         return rc;
@@ -1740,6 +1805,16 @@ int fg_plan_sync_params(fg_plan* p, const double* rho, const double* alpha,
         if (gh.dev.kind == FG_KIND_MPC_DYN && !gh.tab_h.empty())
             if (int rc = sync_dyn_matrix(p, gh, rho)) return rc;
     if (int rc = sync_unit_flags(p)) return rc;
+    if (p->nG) {
+        // giant segments read no weights when every rho and alpha is 1
+        bool unit = !getenv("FGADMM_NO_UNIT");
+        for (int64_t e = 0; e < p->E && unit; ++e) unit = rho[e] == 1.0 && alpha[e] == 1.0;
+        if (unit != p->giant_unit) {
+            p->giant_unit = unit;
+            for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
+            p->graphs.clear();
+        }
+    }
     if (p->mpc_ok) {
         // MPC chain: unit weights, z weights = degrees, matrix form active
         bool on = !getenv("FGADMM_NO_CHAIN");

@@ -56,7 +56,9 @@ __device__ __forceinline__ CompRef comp_ref(const PassB& b, int32_t k) {
     return r;
 }
 
-template <int MODE>
+// UNIT: every edge weight is exactly 1.0 (checked at sync), so m * rho is
+// m and the rho stream is not read.
+template <int MODE, bool UNIT = false>
 struct ValFn {
     const double* x;
     const double* u;         // FUSED: u_in;  PHASEZ: materialized m
@@ -75,40 +77,45 @@ struct ValFn {
         } else {
             m = u[p];
         }
+        if (UNIT) return m;
         return m * rho[r.eb + e];                    // engine.py:278
     }
 };
 
 // u update + residual partials for elements [e0, e1) of one component.
+// UNIT: rho = alpha = 1 exactly (rd = dz, t * alpha = t), not read.
+template <bool UNIT = false, int NB = 4>
 __device__ __forceinline__ void update_range(const PassB& b, const CompRef& r,
                                              int64_t e0, int64_t e1,
                                              int64_t step, double zn, double zo,
                                              double& pp, double& dd, bool& badu) {
     const double dz = zn - zo;
-    // batches of 4 elements: all loads before the stores (the compiler
+    // batches of NB elements: all loads before the stores (the compiler
     // cannot prove uout aliases nothing read here), one round trip each
-    for (int64_t e = e0; e < e1; e += 4 * step) {
-        double xv[4], uv[4], rv[4], av[4];
+    for (int64_t e = e0; e < e1; e += NB * step) {
+        double xv[NB], uv[NB], rv[NB], av[NB];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < NB; ++k) {
             const int64_t ee = e + k * step;
             if (ee < e1) {
                 const int64_t p = r.pb + ee * r.d + r.c;
                 xv[k] = b.x[p];
                 uv[k] = b.uin[p];
-                rv[k] = b.rho[r.eb + ee];
-                av[k] = b.alpha[r.eb + ee];
+                if (!UNIT) {
+                    rv[k] = b.rho[r.eb + ee];
+                    av[k] = b.alpha[r.eb + ee];
+                }
             }
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < NB; ++k) {
             const int64_t ee = e + k * step;
             if (ee < e1) {
                 const double t = xv[k] - zn;             // engine.py:288
                 pp += t * t;                             // engine.py:402
-                const double rd = rv[k] * dz;            // engine.py:403-405
+                const double rd = UNIT ? dz : rv[k] * dz;            // engine.py:403-405
                 dd += rd * rd;
-                const double un = uv[k] + t * av[k];     // :289-290
+                const double un = UNIT ? uv[k] + t : uv[k] + t * av[k];     // :289-290
                 b.uout[r.pb + ee * r.d + r.c] = un;
                 badu |= !finite(un);
             }
@@ -164,7 +171,7 @@ __global__ void __launch_bounds__(256) k_var_small(PassB b, const int32_t* list,
 constexpr int kVarThreads = 256;
 constexpr int kMaxUnits = 160;          // chunk <= 8192 -> <= 128 leaves
 
-template <class F, int NT = kVarThreads>
+template <class F, int NT = kVarThreads, bool BATCH = false>
 __device__ __forceinline__ double run_units_and_tree(F val, int64_t base_elem,
                                                      const int32_t* P,
                                                      double* sv) {
@@ -172,21 +179,27 @@ __device__ __forceinline__ double run_units_and_tree(F val, int64_t base_elem,
     const int32_t* units = P + 2;
     const int32_t* lev = units + 2 * nu;
     const int32_t* ops = lev + nlev;
+    // the top's level counts and operand ids, staged while the leaves load
+    // (the level loop then waits on no global memory)
+    __shared__ int32_t s_prog[2 * kMaxUnits + 64];
+    const int nops = 2 * (nu - 1);
+    for (int i = threadIdx.x; i < nops + nlev; i += NT) s_prog[i] = i < nops ? ops[i] : lev[i - nops];
     const int g = threadIdx.x >> 3, j = threadIdx.x & 7;
     constexpr int NG = NT / 8;
     for (int r0 = 0; r0 < nu; r0 += NG) {
         const int L = r0 + g;
         int64_t s = 0, len = 0;
         if (L < nu) { s = units[2 * L]; len = units[2 * L + 1]; }
-        const double res = leaf_group8(val, base_elem + s, len, j);
+        const double res = BATCH ? leaf_group8_batched(val, base_elem + s, len, j)
+                                 : leaf_group8(val, base_elem + s, len, j);
         if (L < nu && j == 0) sv[L] = res;
     }
     __syncthreads();
     int node = nu, op = 0;
     for (int l = 0; l < nlev; ++l) {
-        const int cnt = lev[l];
+        const int cnt = s_prog[nops + l];
         for (int o = threadIdx.x; o < cnt; o += NT)
-            sv[node + o] = sv[ops[2 * (op + o)]] + sv[ops[2 * (op + o) + 1]];
+            sv[node + o] = sv[s_prog[2 * (op + o)]] + sv[s_prog[2 * (op + o) + 1]];
         __syncthreads();
         node += cnt;
         op += cnt;
@@ -250,7 +263,7 @@ __device__ void giant_top_body(const PassB& b, const int32_t* glist, const GComp
 // atomic counter per component, reset by that CTA) also evaluates the top
 // of its tree: the separate top launch disappears.  The top program is the
 // same whichever CTA runs it, so the result is deterministic.
-template <int MODE, int NT = kVarThreads>
+template <int MODE, int NT = kVarThreads, bool UNIT = false>
 __global__ void __launch_bounds__(NT) k_var_giant_chunks(
     PassB b, const int32_t* glist, const GChunk* chunks, const int32_t* prog,
     double* csum, const GComp* comps = nullptr, double* gz = nullptr, double* send = nullptr,
@@ -266,10 +279,10 @@ __global__ void __launch_bounds__(NT) k_var_giant_chunks(
     const GChunk ch = chunks[blockIdx.x];
     const CompRef r = comp_ref(b, glist[ch.gi]);
     bool bm = false;
-    ValFn<MODE> val(b, r, &bm);
+    ValFn<MODE, UNIT> val(b, r, &bm);
     // pad = first element of the tree: 1 for a whole segment (a[0] is the
     // reduceat initial value), 0 for a rank's local part of a cut segment
-    const double T = run_units_and_tree<ValFn<MODE>, NT>(val, (int64_t)ch.pad + ch.start,
+    const double T = run_units_and_tree<ValFn<MODE, UNIT>, NT, true>(val, (int64_t)ch.pad + ch.start,
                                                          prog + ch.progoff, sv);
     if (threadIdx.x == 0) csum[blockIdx.x] = T;
     if (MODE == MODE_FUSED && bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
@@ -304,13 +317,27 @@ __device__ void giant_top_body(const PassB& b, const int32_t* glist, const GComp
     const int nu = P[0], nlev = P[1];
     const int32_t* lev = P + 2 + 2 * nu;
     const int32_t* ops = lev + nlev;
+    // one round trip: chunk sums, the top program (into shared memory after
+    // the 2 nu node values) and, on thread 0, element 0 and the z inputs
+    int32_t* s_prog = reinterpret_cast<int32_t*>(sv + 2 * nu);
+    const int nops = nu > 0 ? 2 * (nu - 1) : 0;
     for (int u = threadIdx.x; u < nu; u += NT) sv[u] = __ldcg(csum + gc.cbase + u);
+    for (int i = threadIdx.x; i < nops + nlev; i += NT) s_prog[i] = i < nops ? ops[i] : lev[i - nops];
+    double a0 = 0.0, zw = 1.0, zo = 0.0;
+    bool bm = false;
+    if (threadIdx.x == 0 && gc.pad0 < 0) {
+        const CompRef r = comp_ref(b, k);
+        ValFn<MODE> val(b, r, &bm);
+        a0 = val(0);
+        zw = b.zw[k];
+        zo = (MODE == MODE_FUSED) ? b.zin[k] : 0.0;
+    }
     __syncthreads();
     int node = nu, op = 0;
     for (int l = 0; l < nlev; ++l) {
-        const int cnt = lev[l];
+        const int cnt = s_prog[nops + l];
         for (int o = threadIdx.x; o < cnt; o += NT)
-            sv[node + o] = sv[ops[2 * (op + o)]] + sv[ops[2 * (op + o) + 1]];
+            sv[node + o] = sv[s_prog[2 * (op + o)]] + sv[s_prog[2 * (op + o) + 1]];
         __syncthreads();
         node += cnt;
         op += cnt;
@@ -320,12 +347,9 @@ __device__ void giant_top_body(const PassB& b, const int32_t* glist, const GComp
         return;
     }
     if (threadIdx.x == 0) {
-        const CompRef r = comp_ref(b, k);
-        bool bm = false;
-        ValFn<MODE> val(b, r, &bm);
-        const double zn = ddiv(val(0) + sv[node - 1], b.zw[k]);
+        const double zn = ddiv(a0 + sv[node - 1], zw);
         gz[2 * gi] = zn;
-        gz[2 * gi + 1] = (MODE == MODE_FUSED) ? b.zin[k] : 0.0;
+        gz[2 * gi + 1] = zo;
         b.z[k] = zn;
         if (MODE == MODE_FUSED) {
             if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
@@ -390,7 +414,8 @@ struct FusedReduce {
 
 // G3: u update of giant components, one CTA per element range.
 struct GWork { int32_t gi, e0, e1, pad; };
-__global__ void __launch_bounds__(kVarThreads) k_var_giant_update(
+template <bool UNIT = false>
+__global__ void __launch_bounds__(kVarThreads, 2) k_var_giant_update(
     PassB b, const int32_t* glist, const GWork* work, const double* gz,
     int64_t part_off, FusedReduce fr = FusedReduce{nullptr, 0, 0, 0, nullptr}) {
     __shared__ double sm[16];
@@ -404,8 +429,8 @@ __global__ void __launch_bounds__(kVarThreads) k_var_giant_update(
     const CompRef r = comp_ref(b, glist[wk.gi]);
     double pp = 0.0, dd = 0.0;
     bool bu = false;
-    update_range(b, r, wk.e0 + threadIdx.x, wk.e1, kVarThreads, gz[2 * wk.gi],
-                 gz[2 * wk.gi + 1], pp, dd, bu);
+    update_range<UNIT, UNIT ? 8 : 4>(b, r, wk.e0 + threadIdx.x, wk.e1, kVarThreads, gz[2 * wk.gi],
+                          gz[2 * wk.gi + 1], pp, dd, bu);
     if (bu) flag_error(b.ctrl, it, FG_PHASE_U, false);
     block_sum2<kVarThreads>(pp, dd, sm);
     if (threadIdx.x == 0) {

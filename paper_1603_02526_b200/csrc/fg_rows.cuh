@@ -280,6 +280,10 @@ k_var_row_pipe(PassB b, const int32_t* vlist, const int32_t* progoff, const int3
     const int32_t* units = P + 2;
     const int32_t* lev = units + 2 * nu;
     const int32_t* ops = lev + nlev;
+    // the tree top's program, staged while the first jobs load
+    __shared__ int32_t s_prog[2 * kMaxUnits + 64];
+    const int nops = 2 * (nu - 1);
+    for (int i = threadIdx.x; i < nops + nlev; i += kRowThreads) s_prog[i] = i < nops ? ops[i] : lev[i - nops];
     const int g = threadIdx.x >> 3, j8 = threadIdx.x & 7;
     constexpr int NG = kRowThreads / 8;
     double zn[D], dz[D];
@@ -292,10 +296,10 @@ k_var_row_pipe(PassB b, const int32_t* vlist, const int32_t* progoff, const int3
             if (threadIdx.x < 32) {
                 int node = nu, op = 0;
                 for (int l = 0; l < nlev; ++l) {
-                    const int cnt = lev[l];
+                    const int cnt = s_prog[nops + l];
                     for (int o = threadIdx.x; o < cnt * D; o += 32) {
                         const int c = o / cnt, oo = o - c * cnt;
-                        sv[c][node + oo] = sv[c][ops[2 * (op + oo)]] + sv[c][ops[2 * (op + oo) + 1]];
+                        sv[c][node + oo] = sv[c][s_prog[2 * (op + oo)]] + sv[c][s_prog[2 * (op + oo) + 1]];
                     }
                     __syncwarp();
                     node += cnt;
@@ -412,6 +416,235 @@ k_var_row_pipe(PassB b, const int32_t* vlist, const int32_t* progoff, const int3
     if (threadIdx.x == 0) {
         b.part[2 * (part_off + blockIdx.x)] = pp;
         b.part[2 * (part_off + blockIdx.x) + 1] = dd;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Class-L rows, unit-weight form, persistent: a grid of resident CTAs walks
+// the rows (row slot blockIdx.x, + gridDim.x, ...) through ONE job ring.
+// The producer thread keeps issuing the next jobs of the CTA's row sequence
+// -- past the end of the current row into the next row's phase-1 chunks --
+// so HBM reads continue while a row finishes its tree top, z and phase-2
+// update, and no CTA start-up gap opens between rows.  Per row the jobs and
+// arithmetic are k_var_row_pipe's (bitwise equal); residual partials
+// accumulate per CTA (slot blockIdx.x; the class's other slots are zeroed).
+template <int D, int NS, int SDB>
+__global__ void __launch_bounds__(kRowThreads, NS >= 3 ? 3 : 2)
+k_var_row_ring(PassB b, const int32_t* vlist, const int32_t* progoff, const int32_t* prog,
+               const int32_t* planoff, const int32_t* plans, const LExc* exc,
+               int64_t part_off, int32_t nrows) {
+    extern __shared__ __align__(16) double pipe_smem[];
+    __shared__ double sv[D][2 * kMaxUnits];
+    __shared__ double sm[2 * (kRowThreads / 32)];
+    __shared__ double s_z[2][D];
+    __shared__ __align__(8) uint64_t full[NS];
+    __shared__ int32_t s_prog[2 * kMaxUnits + 64];
+    if (b.ctrl->stop) return;
+    const int64_t it = b.ctrl->iter;
+    const int G = gridDim.x;
+    constexpr int SD = SDB + 4;           // array slot (span slack)
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    // producer cursor (thread 0): row slot, job index, that row's plan
+    int prs = blockIdx.x, pj = 0, pJ1 = 0, pNJ = 0, pCH = 0, pdeg = 0;
+    int64_t ppb = 0;
+    const int32_t* pch = nullptr;
+    auto prow = [&](int rs) {
+        prs = rs;
+        pj = 0;
+        if (rs >= nrows) return;
+        const int32_t v = vlist[rs];
+        ppb = b.vt.pbase[v];
+        pdeg = b.vt.deg[v];
+        const int32_t* PL = plans + planoff[rs];
+        pJ1 = PL[0];
+        pNJ = PL[0] + PL[1];
+        pCH = PL[2];
+        pch = PL + 3;
+    };
+    auto issue_next = [&](int s) {
+        if (prs >= nrows) return;
+        int64_t lo, hi;
+        if (pj < pJ1) { lo = pch[4 * pj]; hi = pch[4 * pj + 1]; }
+        else { lo = (int64_t)(pj - pJ1) * pCH; hi = lo + pCH < (int64_t)pdeg ? lo + pCH : (int64_t)pdeg; }
+        const Span sx = span16(ppb + lo * D, ppb + hi * D);
+        double* base = pipe_smem + (int64_t)s * 2 * SD;
+        const unsigned bytes = (unsigned)(sx.n * 8);
+        mbar_expect_tx(&full[s], 2 * bytes);
+        bulk_g2s(base, b.x + sx.lo, bytes, &full[s]);
+        bulk_g2s(base + SD, b.uin + sx.lo, bytes, &full[s]);
+        if (++pj == pNJ) prow(prs + G);
+    };
+    if (threadIdx.x == 0) {
+        prow(blockIdx.x);
+        for (int k = 0; k < NS; ++k) issue_next(k);
+    }
+    const int g = threadIdx.x >> 3, j8 = threadIdx.x & 7;
+    constexpr int NG = kRowThreads / 8;
+    double pp = 0.0, dd = 0.0;
+    bool bm = false, bu = false;
+    int64_t gj = 0;                       // jobs consumed by this CTA
+    for (int rs = blockIdx.x; rs < nrows; rs += G) {
+        const int32_t v = vlist[rs];
+        const int64_t pb = b.vt.pbase[v];
+        const int64_t zb = b.vt.zbase[v];
+        const int deg = b.vt.deg[v];
+        const LExc xe = exc[rs];
+        const int32_t* PL = plans + planoff[rs];
+        const int J1 = PL[0], J2 = PL[1], CH = PL[2];
+        const int32_t* chunks = PL + 3;
+        const int NJ = J1 + J2;
+        double a0[D], zw0[D], zo0[D];
+        if (threadIdx.x == 0) {
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+                const double m0 = b.x[pb + c] + b.uin[pb + c];
+                bm |= !finite(m0);
+                a0[c] = xe.rank == 0 ? m0 * xe.rho : m0;
+                zw0[c] = b.zw[zb + c];
+                zo0[c] = b.zin[zb + c];
+            }
+        }
+        const int32_t* P = prog + progoff[rs];
+        const int nu = P[0], nlev = P[1];
+        const int32_t* units = P + 2;
+        const int32_t* lev = units + 2 * nu;
+        const int32_t* ops = lev + nlev;
+        // this row's tree-top program (the previous row's top finished
+        // before its phase-2 jobs, each closed by a barrier)
+        const int nops = 2 * (nu - 1);
+        for (int i = threadIdx.x; i < nops + nlev; i += kRowThreads) s_prog[i] = i < nops ? ops[i] : lev[i - nops];
+        double zn[D], dz[D];
+        for (int j = 0; j < NJ; ++j, ++gj) {
+            const int s = (int)(gj % NS);
+            if (j == J1) {
+                __syncthreads();
+                if (threadIdx.x < 32) {
+                    int node = nu, op = 0;
+                    for (int l = 0; l < nlev; ++l) {
+                        const int cnt = s_prog[nops + l];
+                        for (int o = threadIdx.x; o < cnt * D; o += 32) {
+                            const int c = o / cnt, oo = o - c * cnt;
+                            sv[c][node + oo] = sv[c][s_prog[2 * (op + oo)]] + sv[c][s_prog[2 * (op + oo) + 1]];
+                        }
+                        __syncwarp();
+                        node += cnt;
+                        op += cnt;
+                    }
+                    if (threadIdx.x == 0) {
+#pragma unroll
+                        for (int c = 0; c < D; ++c) {
+                            const double z = ddiv(a0[c] + sv[c][node - 1], zw0[c]);
+                            s_z[0][c] = z;
+                            s_z[1][c] = zo0[c];
+                            b.z[zb + c] = z;
+                            if (!finite(z)) flag_error(b.ctrl, it, FG_PHASE_Z, false);
+                        }
+                    }
+                }
+                __syncthreads();
+#pragma unroll
+                for (int c = 0; c < D; ++c) { zn[c] = s_z[0][c]; dz[c] = zn[c] - s_z[1][c]; }
+            }
+            mbar_wait(&full[s], (unsigned)((gj / NS) & 1));
+            int64_t lo, hi;
+            if (j < J1) { lo = chunks[4 * j]; hi = chunks[4 * j + 1]; }
+            else { lo = (int64_t)(j - J1) * CH; hi = lo + CH < (int64_t)deg ? lo + CH : (int64_t)deg; }
+            const Span sx = span16(pb + lo * D, pb + hi * D);
+            const double* X = pipe_smem + (int64_t)s * 2 * SD + sx.off;
+            const double* U = X + SD;
+            if (j < J1) {
+                const int L0 = chunks[4 * j + 2], L1 = chunks[4 * j + 3];
+                auto mval = [&](int64_t e, int c) {
+                    const int64_t q = (e - lo) * D + c;
+                    const double m = X[q] + U[q];
+                    bm |= !finite(m);
+                    return e == xe.rank ? m * xe.rho : m;
+                };
+                for (int L = L0 + g; L < L1; L += NG) {
+                    const int64_t e0 = 1 + (int64_t)units[2 * L], len = units[2 * L + 1];
+                    const bool small = len < kUnroll;
+                    const int64_t top = len - len % kUnroll;
+                    double acc[D];
+#pragma unroll
+                    for (int c = 0; c < D; ++c) acc[c] = 0.0;
+                    const bool exl = xe.rank >= e0 && xe.rank < e0 + len;
+                    if (!small && !exl) {
+                        const double* xp = X + (e0 + j8 - lo) * D;
+                        const double* up = U + (e0 + j8 - lo) * D;
+#pragma unroll
+                        for (int c = 0; c < D; ++c) acc[c] = xp[c] + up[c];
+                        const int nst = (int)(top / kUnroll);
+                        for (int i = 1; i < nst; ++i)
+#pragma unroll
+                            for (int c = 0; c < D; ++c)
+                                acc[c] += xp[i * kUnroll * D + c] + up[i * kUnroll * D + c];
+#pragma unroll
+                        for (int c = 0; c < D; ++c)
+                            if (!finite(acc[c]))
+                                for (int i = 0; i < nst; ++i)
+                                    bm |= !finite(xp[i * kUnroll * D + c] + up[i * kUnroll * D + c]);
+                    } else if (small) {
+                        if (j8 == 0)
+                            for (int64_t i = 0; i < len; ++i)
+#pragma unroll
+                                for (int c = 0; c < D; ++c) acc[c] += mval(e0 + i, c);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < D; ++c) acc[c] = mval(e0 + j8, c);
+                        for (int64_t i = kUnroll; i < top; i += kUnroll)
+#pragma unroll
+                            for (int c = 0; c < D; ++c) acc[c] += mval(e0 + i + j8, c);
+                    }
+                    const unsigned gmask = 0xFFu << (threadIdx.x & 24);
+#pragma unroll
+                    for (int c = 0; c < D; ++c) {
+                        double bs = acc[c] + __shfl_xor_sync(gmask, acc[c], 1);
+                        bs = bs + __shfl_xor_sync(gmask, bs, 2);
+                        bs = bs + __shfl_xor_sync(gmask, bs, 4);
+                        if (!small) acc[c] = bs;
+                    }
+                    if (!small && j8 == 0)
+                        for (int64_t i = top; i < len; ++i)
+#pragma unroll
+                            for (int c = 0; c < D; ++c) acc[c] += mval(e0 + i, c);
+                    if (j8 == 0) {
+#pragma unroll
+                        for (int c = 0; c < D; ++c) sv[c][L] = acc[c];
+                    }
+                }
+            } else {
+                const int64_t nq = (hi - lo) * D;
+                for (int64_t q = threadIdx.x; q < nq; q += kRowThreads) {
+                    const int64_t e = lo + q / D;
+                    const int c = (int)(q - (e - lo) * D);
+                    const bool ex = e == xe.rank;
+                    const double t = X[q] - zn[c];
+                    pp += t * t;
+                    const double rd = ex ? xe.rho * dz[c] : dz[c];
+                    dd += rd * rd;
+                    const double un = U[q] + (ex ? t * xe.alpha : t);
+                    b.uout[pb + lo * D + q] = un;
+                    bu |= !finite(un);
+                }
+            }
+            __syncthreads();                               // stage s consumed
+            if (threadIdx.x == 0) issue_next(s);
+        }
+    }
+    if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
+    if (bu) flag_error(b.ctrl, it, FG_PHASE_U, false);
+    block_sum2<kRowThreads>(pp, dd, sm);
+    if (threadIdx.x == 0) {
+        b.part[2 * (part_off + blockIdx.x)] = pp;
+        b.part[2 * (part_off + blockIdx.x) + 1] = dd;
+    }
+    for (int64_t k = blockIdx.x + G + threadIdx.x * (int64_t)G; k < nrows; k += (int64_t)G * kRowThreads) {
+        b.part[2 * (part_off + k)] = 0.0;
+        b.part[2 * (part_off + k) + 1] = 0.0;
     }
 }
 
