@@ -311,12 +311,31 @@ def reference_arm(args):
     return 0
 
 
+def points_per_rank(args, world):
+    """SVM points per rank of the weak-scaled run: --points-per-rank, else
+    configs[4]'s 8M per GPU (64M at 8 GPUs) when the host can hold every
+    local rank's graph and state (measured 78 GB host RSS per rank at 8M
+    points before the page-locked state copy), else the largest whole million that fits (at least 1M)."""
+    if args.points_per_rank:
+        return args.points_per_rank
+    target, per_point = 8_000_000, 12_000          # bytes of host memory per point
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:                               # pragma: no cover
+        return 1_000_000
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    fit = int(0.85 * avail / max(1, local_world) / per_point)
+    return max(1_000_000, min(target, fit // 1_000_000 * 1_000_000))
+
+
 def multi_gpu(args, fg, dist, rank, world, local):
     """N ranks over NCCL: the graph is partitioned by factors (cut variables
     all-gather their partial sums inside the iteration).
 
-    SVM: weak scaling -- every rank holds 1M points of a world x 1M-point
-    chain and builds only its own part (partition.svm_rank_graph; cut set:
+    SVM: weak scaling -- every rank holds n points (configs[4]: 8M per GPU,
+    see points_per_rank) of a world x n-point chain and builds only its
+    own part (partition.svm_rank_graph; cut set:
     the bias and one weight copy per rank boundary); value = all ranks'
     edges x K / max-rank time.  Packing / MPC: strong scaling of the one
     graph, partitioned by partition.Partition."""
@@ -326,7 +345,7 @@ def multi_gpu(args, fg, dist, rank, world, local):
     t_build = time.perf_counter()
     weak = args.workload.startswith("svm")
     if weak:
-        n = 1_000_000
+        n = points_per_rank(args, world)
         X, y = fg.gen_gaussian_arrays(n, 32, 4.0, seed=rank)
         lg = svm_rank_graph(X, y, rank, world, lam=1.0)
         nr = NcclRank(None, rank, world, device=local, local=lg)
@@ -356,11 +375,20 @@ def multi_gpu(args, fg, dist, rank, world, local):
     # of the host state, run, download the rank's state (wall clock, max
     # over ranks)
     lg = nr.local
-    ls = [np.empty(lg.total_edge_payload) for _ in range(4)]
-    lz = np.empty(lg.z_dim)
+    if weak:
+        # rank graphs hold the rank's own state: page-locked like the 1-GPU
+        # arm, downloaded back into the same arrays (as run() does)
+        st_in = fg.pinned_state(lg, st)
+        del st
+        ls = [st_in.x, st_in.m, st_in.u, st_in.n]
+        lz = st_in.z
+    else:
+        st_in = st
+        ls = [np.empty(lg.total_edge_payload) for _ in range(4)]
+        lz = np.empty(lg.z_dim)
     dist.barrier()
     t0 = time.perf_counter()
-    nr.upload(st)
+    nr.upload(st_in)
     nr.run(args.steps)
     nr.plan.download(x=ls[0], m=ls[1], z=lz, u=ls[2], n=ls[3])
     e2e_s = torch.tensor([time.perf_counter() - t0], device="cuda")
@@ -378,10 +406,15 @@ def multi_gpu(args, fg, dist, rank, world, local):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "weak" if weak else "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "desc": WORKLOADS[args.workload], **info,
+        "config": {"workload": args.workload,
+                   "desc": (f"soft-margin linear SVM chain, {info['points_per_rank'] / 1e6:g}M points "
+                            f"per GPU x 32 dims, weak-scaled (configs[4]: 8M per GPU, 64M at 8)"
+                            if weak else WORKLOADS[args.workload]), **info,
                    "edges": E, "parallelism": f"factor partition x{world} (NCCL all-gather "
                                               f"of {getattr(nr.local, 'ncut', 0)} cut components)",
-                   "local_edges": len(nr.local.edge_var), "build_seconds": round(t_build, 2)},
+                   "local_edges": len(nr.local.edge_var), "build_seconds": round(t_build, 2),
+                   "host_max_rss_gb": round(__import__("resource").getrusage(
+                       __import__("resource").RUSAGE_SELF).ru_maxrss / 2**20, 1)},
         "gpu_launches": int(res.launches), "clocks": clk.summary(),
         "converged": bool(res.converged),
         "e2e": e2e,
@@ -405,6 +438,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--partition", action="store_true",
                     help="take the multi-GPU (NCCL partition) path even at one rank")
+    ap.add_argument("--points-per-rank", type=int, default=None,
+                    help="SVM points per rank of the weak-scaled multi-GPU run "
+                         "(default configs[4]: 8M per GPU = 64M at 8 GPUs, fewer "
+                         "when the host memory cannot hold all local ranks)")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)

@@ -729,7 +729,8 @@ constexpr bool kRowRingDefault = false;
 
 int64_t chain_main_grid(const fg_plan* p) {
     if (p->mpc_chain) return p->mpc_tiles - 1;   // the MPC chain writes mpc_tiles slots
-    const int64_t wave = p->chain_fast ? (p->chain_unit ? 148 * 4 : 148 * 2) : 148 * 2;
+    const int64_t wave = p->chain_fast
+        ? (p->chain_unit ? 148 * (p->chain_minb == 5 ? 5 : 4) : 148 * 2) : 148 * 2;
     return std::max<int64_t>(1, std::min(wave, p->chain_grid - 1));
 }
 
@@ -751,6 +752,8 @@ void chain_pass(fg_plan* p, int in, cudaStream_t st) {
         // points (degree 3) on the generic form in the next partial slot
         if (p->chain_unit && p->chain_pf)
             k_svm_chain_unit_pf<32, 4><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
+        else if (p->chain_unit && p->chain_minb == 5)
+            k_svm_chain_unit<32, 5><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
         else if (p->chain_unit && p->chain_minb == 3)
             k_svm_chain_unit<32, 3><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
         else if (p->chain_unit)
@@ -963,7 +966,7 @@ void detect_svm_chain(fg_plan* p, const std::vector<int32_t>& dim,
     p->chain_grid = p->nsblk[0] + p->nsblk[1] + p->nsblk[2];
     // CTAs/SM the kernels are compiled for (A/B in profiles/): generic form
     // 2 (3 spills heavily); unit form 4 (0.59 ms vs 0.67 ms at 3, SVM 1M)
-    p->chain_minb = getenv("FGADMM_CHAIN_OCC3") ? 3 : 2;
+    p->chain_minb = getenv("FGADMM_CHAIN_OCC3") ? 3 : getenv("FGADMM_CHAIN_OCC5") ? 5 : 2;
     // unit form with the per-warp cp.async double buffer (A/B)
     {
         const char* e = getenv("FGADMM_CHAIN_PF");
