@@ -306,7 +306,11 @@ def reference_arm(args):
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "threads_note": "the reference path is NumPy (elementwise, take, reduceat: one "
+                            "thread); its lane pool (workers > 1) runs 3-8x slower than one "
+                            "lane (GIL and barriers, SURVEY 8(a) a14), so one core is its "
+                            f"fastest configuration on this {os.cpu_count()}-thread host"}
     print(json.dumps(line))
     return 0
 
