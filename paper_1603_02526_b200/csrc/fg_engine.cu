@@ -281,10 +281,12 @@ struct fg_plan {
     bool row_deep = false;             // deeper u-update batches in unit rows (A/B)
     // class-L rows through a TMA ring (unit-weight form, fg_rows.cuh)
     int32_t* d_planoff[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    RowDesc* d_rowdesc[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     int32_t* d_plans = nullptr;
     bool pipe_ok[5] = {false, false, false, false, false};
     bool no_pipe = false;
-    bool row_ring = false;             // persistent class-L row kernel (one job ring per CTA)
+    bool row_ring[5] = {false, false, false, false, false};  // persistent row kernel per dim
+    bool pipe_deep = false;            // small-stage rows with 4 stages (A/B)
     int64_t ring_grid[5][2] = {};      // resident CTAs of the ring kernel per dim / stage form
     // 2 stages of twice the size: measured better for dim >= 2 rows (pack
     // center rows 0.285 vs 0.306 ms), worse for dim 1 (0.176 vs 0.160)
@@ -321,6 +323,7 @@ fg_plan::~fg_plan() {
                     d_chain_fnorm, d_flag, d_bad, d_gcnt, d_ucnt, d_lexc[1], d_lexc[2], d_lexc[3],
                     d_lexc[4], d_row2[1], d_row2[2], d_row2[3], d_row2[4],
                     d_planoff[1], d_planoff[2], d_planoff[3], d_planoff[4], d_plans,
+                    d_rowdesc[1], d_rowdesc[2], d_rowdesc[3], d_rowdesc[4],
                     d_cutg, d_send, d_recv};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -469,13 +472,11 @@ void launch_ring(fg_plan* p, const PassB& b, int64_t nrows, int64_t po, cudaStre
     const unsigned G = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nrows, p->ring_grid[D][big]));
     if (big)
         k_var_row_ring<D, 2, 2 * kPipeStageDoubles><<<G, kRowThreads,
-            row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_lvars[D], p->d_lvprog[D], p->d_prog,
-                                                           p->d_planoff[D], p->d_plans, p->d_lexc[D],
-                                                           po, (int32_t)nrows);
+            row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_rowdesc[D], p->d_prog, p->d_plans,
+                                                           p->d_lexc[D], po, (int32_t)nrows);
     else
         k_var_row_ring<D, kPipeStages, kPipeStageDoubles><<<G, kRowThreads, row_pipe_smem(), st>>>(
-            b, p->d_lvars[D], p->d_lvprog[D], p->d_prog, p->d_planoff[D], p->d_plans, p->d_lexc[D],
-            po, (int32_t)nrows);
+            b, p->d_rowdesc[D], p->d_prog, p->d_plans, p->d_lexc[D], po, (int32_t)nrows);
 }
 
 template <int D>
@@ -516,12 +517,14 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
             k_var_small_run<0, MODE><<<grid, 256, 0, st>>>(b, p->d_sruns, p->d_sblk[2], po);
             return true;
         case 3:
-            if (MODE == MODE_FUSED && p->lunit[1] && p->pipe_ok[1] && !p->no_pipe && p->row_ring)
+            if (MODE == MODE_FUSED && p->lunit[1] && p->pipe_ok[1] && !p->no_pipe && p->row_ring[1])
                 launch_ring<1>(p, b, nb, po, st);
             else if (MODE == MODE_FUSED && p->lunit[1] && p->pipe_ok[1] && !p->no_pipe && p->pipe_big[1])
-                k_var_row_pipe<1, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, p->d_planoff[1], p->d_plans, p->d_lexc[1], po);
+                k_var_row_pipe<1, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_rowdesc[1], p->d_prog, p->d_plans, p->d_lexc[1], po);
+            else if (MODE == MODE_FUSED && p->lunit[1] && p->pipe_ok[1] && !p->no_pipe && p->pipe_deep)
+                k_var_row_pipe<1, 4, kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(4), st>>>(b, p->d_rowdesc[1], p->d_prog, p->d_plans, p->d_lexc[1], po);
             else if (MODE == MODE_FUSED && p->lunit[1] && p->pipe_ok[1] && !p->no_pipe)
-                k_var_row_pipe<1><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, p->d_planoff[1], p->d_plans, p->d_lexc[1], po);
+                k_var_row_pipe<1><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_rowdesc[1], p->d_prog, p->d_plans, p->d_lexc[1], po);
             else if (MODE == MODE_FUSED && p->lunit[1] && p->row2_ok[1] && !p->no_row2)
                 k_var_row2<1><<<2 * grid, kRowThreads, p->row2_smem[1], st>>>(b, p->d_row2[1], p->d_prog, p->d_lexc[1], po);
             else if (p->row256)
@@ -534,12 +537,14 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
                 k_var_large_vec<1, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po, nullptr, p->row2_ok[1] ? po + grid : -1);
             return true;
         case 4:
-            if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe && p->row_ring)
+            if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe && p->row_ring[2])
                 launch_ring<2>(p, b, nb, po, st);
             else if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe && p->pipe_big[2])
-                k_var_row_pipe<2, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, p->d_planoff[2], p->d_plans, p->d_lexc[2], po);
+                k_var_row_pipe<2, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_rowdesc[2], p->d_prog, p->d_plans, p->d_lexc[2], po);
+            else if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe && p->pipe_deep)
+                k_var_row_pipe<2, 4, kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(4), st>>>(b, p->d_rowdesc[2], p->d_prog, p->d_plans, p->d_lexc[2], po);
             else if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe)
-                k_var_row_pipe<2><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, p->d_planoff[2], p->d_plans, p->d_lexc[2], po);
+                k_var_row_pipe<2><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_rowdesc[2], p->d_prog, p->d_plans, p->d_lexc[2], po);
             else if (MODE == MODE_FUSED && p->lunit[2] && p->row2_ok[2] && !p->no_row2)
                 k_var_row2<2><<<2 * grid, kRowThreads, p->row2_smem[2], st>>>(b, p->d_row2[2], p->d_prog, p->d_lexc[2], po);
             else if (p->row256)
@@ -552,12 +557,14 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
                 k_var_large_vec<2, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po, nullptr, p->row2_ok[2] ? po + grid : -1);
             return true;
         case 5:
-            if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe && p->row_ring)
+            if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe && p->row_ring[3])
                 launch_ring<3>(p, b, nb, po, st);
             else if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe && p->pipe_big[3])
-                k_var_row_pipe<3, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, p->d_planoff[3], p->d_plans, p->d_lexc[3], po);
+                k_var_row_pipe<3, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_rowdesc[3], p->d_prog, p->d_plans, p->d_lexc[3], po);
+            else if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe && p->pipe_deep)
+                k_var_row_pipe<3, 4, kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(4), st>>>(b, p->d_rowdesc[3], p->d_prog, p->d_plans, p->d_lexc[3], po);
             else if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe)
-                k_var_row_pipe<3><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, p->d_planoff[3], p->d_plans, p->d_lexc[3], po);
+                k_var_row_pipe<3><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_rowdesc[3], p->d_prog, p->d_plans, p->d_lexc[3], po);
             else if (MODE == MODE_FUSED && p->lunit[3] && p->row2_ok[3] && !p->no_row2)
                 k_var_row2<3><<<2 * grid, kRowThreads, p->row2_smem[3], st>>>(b, p->d_row2[3], p->d_prog, p->d_lexc[3], po);
             else if (p->row256)
@@ -570,12 +577,14 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
                 k_var_large_vec<3, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po, nullptr, p->row2_ok[3] ? po + grid : -1);
             return true;
         case 6:
-            if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe && p->row_ring)
+            if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe && p->row_ring[4])
                 launch_ring<4>(p, b, nb, po, st);
             else if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe && p->pipe_big[4])
-                k_var_row_pipe<4, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, p->d_planoff[4], p->d_plans, p->d_lexc[4], po);
+                k_var_row_pipe<4, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_rowdesc[4], p->d_prog, p->d_plans, p->d_lexc[4], po);
+            else if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe && p->pipe_deep)
+                k_var_row_pipe<4, 4, kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(4), st>>>(b, p->d_rowdesc[4], p->d_prog, p->d_plans, p->d_lexc[4], po);
             else if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe)
-                k_var_row_pipe<4><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, p->d_planoff[4], p->d_plans, p->d_lexc[4], po);
+                k_var_row_pipe<4><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_rowdesc[4], p->d_prog, p->d_plans, p->d_lexc[4], po);
             else if (MODE == MODE_FUSED && p->lunit[4] && p->row2_ok[4] && !p->no_row2)
                 k_var_row2<4><<<2 * grid, kRowThreads, p->row2_smem[4], st>>>(b, p->d_row2[4], p->d_prog, p->d_lexc[4], po);
             else if (p->row256)
@@ -725,7 +734,6 @@ void part_post(fg_plan* p, cudaStream_t st) {
 // kernels loop over their points), at most the partial slots it replaces
 // minus the end-point slot.
 constexpr bool kChainPfDefault = false;
-constexpr bool kRowRingDefault = false;
 
 int64_t chain_main_grid(const fg_plan* p) {
     if (p->mpc_chain) return p->mpc_tiles - 1;   // the MPC chain writes mpc_tiles slots
@@ -1597,6 +1605,9 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     p->no_pipe = getenv("FGADMM_NO_PIPE") != nullptr;
     if (getenv("FGADMM_PIPE_BIG"))
         for (int d = 1; d <= 4; ++d) p->pipe_big[d] = std::atoi(getenv("FGADMM_PIPE_BIG")) != 0;
+    p->pipe_deep = getenv("FGADMM_PIPE_DEEP") != nullptr;
+    if (p->pipe_deep)
+        for (int d = 1; d <= 4; ++d) p->pipe_big[d] = false;   // deep form uses the small stages
     {   // TMA-ring row plans, one per distinct degree and dim
         std::vector<int32_t> plans;
         std::map<std::pair<int64_t, int>, int32_t> plan_of;
@@ -1633,6 +1644,21 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
             }
             if (!ok) continue;
             if ((rc = upload(&p->d_planoff[d], offs))) return rc;
+            std::vector<RowDesc> rdv(lvars[d].size());
+            for (size_t r = 0; r < lvars[d].size(); ++r) {
+                const int32_t v = lvars[d][r];
+                RowDesc& q = rdv[r];
+                q.pb = pbase[v];
+                q.zb = zbase[v];
+                q.deg = deg[v];
+                q.planoff = offs[r];
+                q.progoff = lvprog[d][r];
+                q.J1 = plans[offs[r]];
+                q.J2 = plans[offs[r] + 1];
+                q.CH = plans[offs[r] + 2];
+                q.pad[0] = q.pad[1] = 0;
+            }
+            if ((rc = upload(&p->d_rowdesc[d], rdv))) return rc;
             p->pipe_ok[d] = true;
         }
         if (!plans.empty() && (rc = upload(&p->d_plans, plans))) return rc;
@@ -1641,6 +1667,11 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
         CK(cudaFuncSetAttribute(k_var_row_pipe<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         CK(cudaFuncSetAttribute(k_var_row_pipe<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         CK(cudaFuncSetAttribute(k_var_row_pipe<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        const int smem4 = (int)row_pipe_smem(4);
+        CK(cudaFuncSetAttribute(k_var_row_pipe<1, 4, kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4));
+        CK(cudaFuncSetAttribute(k_var_row_pipe<2, 4, kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4));
+        CK(cudaFuncSetAttribute(k_var_row_pipe<3, 4, kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4));
+        CK(cudaFuncSetAttribute(k_var_row_pipe<4, 4, kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4));
         const int smem2 = (int)row_pipe_smem(2, 2 * kPipeStageDoubles);
         CK(cudaFuncSetAttribute(k_var_row_pipe<1, 2, 2 * kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
         CK(cudaFuncSetAttribute(k_var_row_pipe<2, 2, 2 * kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
@@ -1653,8 +1684,11 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
         if (int rc2 = ring_setup<3>(p.get(), sms)) return rc2;
         if (int rc2 = ring_setup<4>(p.get(), sms)) return rc2;
         {
+            // default: the ring for big-stage rows (dim >= 2: 0.264 vs 0.269 ms
+            // at pack N=5000), one CTA per row for dim 1 (0.156 vs 0.159 ms)
             const char* e = getenv("FGADMM_ROW_RING");
-            p->row_ring = e ? e[0] == '1' : kRowRingDefault;
+            for (int d = 1; d <= 4; ++d)
+                p->row_ring[d] = e ? e[0] == '1' : p->pipe_big[d];
         }
     }
     p->row_deep = getenv("FGADMM_ROW_DEEP") != nullptr;

@@ -216,14 +216,23 @@ k_var_row2(PassB b, const Row2* rows, const int32_t* prog, const LExc* exc, int6
 // Row plan (int32, per distinct degree): J1, J2, CH, then J1 x (elo, ehi,
 // leaf_lo, leaf_hi) for the phase-1 chunks; phase-2 chunk k is elements
 // [k*CH, min(deg, (k+1)*CH)).
+// Per class-L row, everything a CTA needs before its first bulk copy in
+// one 48-byte load (built at plan creation): payload and z base, degree,
+// its TMA plan (offset, J1 phase-1 jobs, J2 phase-2 jobs, CH) and its
+// tree program.
+struct __align__(16) RowDesc {
+    int64_t pb, zb;
+    int32_t deg, planoff, progoff, J1, J2, CH;
+    int32_t pad[2];
+};
+
 constexpr int kPipeStages = 3;
 constexpr int kPipeStageDoubles = 1280;             // per array per stage
 
 template <int D, int NS = kPipeStages, int SDB = kPipeStageDoubles>
 __global__ void __launch_bounds__(kRowThreads, NS == 3 ? 3 : 2)
-k_var_row_pipe(PassB b, const int32_t* vlist, const int32_t* progoff, const int32_t* prog,
-               const int32_t* planoff, const int32_t* plans, const LExc* exc,
-               int64_t part_off) {
+k_var_row_pipe(PassB b, const RowDesc* rdesc, const int32_t* prog, const int32_t* plans,
+               const LExc* exc, int64_t part_off) {
     extern __shared__ __align__(16) double pipe_smem[];
     __shared__ double sv[D][2 * kMaxUnits];
     __shared__ double sm[2 * (kRowThreads / 32)];
@@ -231,14 +240,13 @@ k_var_row_pipe(PassB b, const int32_t* vlist, const int32_t* progoff, const int3
     __shared__ __align__(8) uint64_t full[NS];
     if (b.ctrl->stop) return;
     const int64_t it = b.ctrl->iter;
-    const int32_t v = vlist[blockIdx.x];
-    const int64_t pb = b.vt.pbase[v];
-    const int64_t zb = b.vt.zbase[v];
-    const int deg = b.vt.deg[v];
+    const RowDesc rd = rdesc[blockIdx.x];
+    const int64_t pb = rd.pb;
+    const int64_t zb = rd.zb;
+    const int deg = rd.deg;
     const LExc xe = exc[blockIdx.x];
-    const int32_t* PL = plans + planoff[blockIdx.x];
-    const int J1 = PL[0], J2 = PL[1], CH = PL[2];
-    const int32_t* chunks = PL + 3;
+    const int J1 = rd.J1, J2 = rd.J2, CH = rd.CH;
+    const int32_t* chunks = plans + rd.planoff + 3;
     const int NJ = J1 + J2;
     constexpr int SD = SDB + 4;           // array slot (span slack)
     if (threadIdx.x == 0) {
@@ -275,7 +283,7 @@ k_var_row_pipe(PassB b, const int32_t* vlist, const int32_t* progoff, const int3
             zo0[c] = b.zin[zb + c];
         }
     }
-    const int32_t* P = prog + progoff[blockIdx.x];
+    const int32_t* P = prog + rd.progoff;
     const int nu = P[0], nlev = P[1];
     const int32_t* units = P + 2;
     const int32_t* lev = units + 2 * nu;
@@ -430,9 +438,8 @@ k_var_row_pipe(PassB b, const int32_t* vlist, const int32_t* progoff, const int3
 // accumulate per CTA (slot blockIdx.x; the class's other slots are zeroed).
 template <int D, int NS, int SDB>
 __global__ void __launch_bounds__(kRowThreads, NS >= 3 ? 3 : 2)
-k_var_row_ring(PassB b, const int32_t* vlist, const int32_t* progoff, const int32_t* prog,
-               const int32_t* planoff, const int32_t* plans, const LExc* exc,
-               int64_t part_off, int32_t nrows) {
+k_var_row_ring(PassB b, const RowDesc* rdesc, const int32_t* prog, const int32_t* plans,
+               const LExc* exc, int64_t part_off, int32_t nrows) {
     extern __shared__ __align__(16) double pipe_smem[];
     __shared__ double sv[D][2 * kMaxUnits];
     __shared__ double sm[2 * (kRowThreads / 32)];
@@ -456,14 +463,13 @@ k_var_row_ring(PassB b, const int32_t* vlist, const int32_t* progoff, const int3
         prs = rs;
         pj = 0;
         if (rs >= nrows) return;
-        const int32_t v = vlist[rs];
-        ppb = b.vt.pbase[v];
-        pdeg = b.vt.deg[v];
-        const int32_t* PL = plans + planoff[rs];
-        pJ1 = PL[0];
-        pNJ = PL[0] + PL[1];
-        pCH = PL[2];
-        pch = PL + 3;
+        const RowDesc rd = rdesc[rs];
+        ppb = rd.pb;
+        pdeg = rd.deg;
+        pJ1 = rd.J1;
+        pNJ = rd.J1 + rd.J2;
+        pCH = rd.CH;
+        pch = plans + rd.planoff + 3;
     };
     auto issue_next = [&](int s) {
         if (prs >= nrows) return;
@@ -488,14 +494,13 @@ k_var_row_ring(PassB b, const int32_t* vlist, const int32_t* progoff, const int3
     bool bm = false, bu = false;
     int64_t gj = 0;                       // jobs consumed by this CTA
     for (int rs = blockIdx.x; rs < nrows; rs += G) {
-        const int32_t v = vlist[rs];
-        const int64_t pb = b.vt.pbase[v];
-        const int64_t zb = b.vt.zbase[v];
-        const int deg = b.vt.deg[v];
+        const RowDesc rd = rdesc[rs];
+        const int64_t pb = rd.pb;
+        const int64_t zb = rd.zb;
+        const int deg = rd.deg;
         const LExc xe = exc[rs];
-        const int32_t* PL = plans + planoff[rs];
-        const int J1 = PL[0], J2 = PL[1], CH = PL[2];
-        const int32_t* chunks = PL + 3;
+        const int J1 = rd.J1, J2 = rd.J2, CH = rd.CH;
+        const int32_t* chunks = plans + rd.planoff + 3;
         const int NJ = J1 + J2;
         double a0[D], zw0[D], zo0[D];
         if (threadIdx.x == 0) {
@@ -508,7 +513,7 @@ k_var_row_ring(PassB b, const int32_t* vlist, const int32_t* progoff, const int3
                 zo0[c] = b.zin[zb + c];
             }
         }
-        const int32_t* P = prog + progoff[rs];
+        const int32_t* P = prog + rd.progoff;
         const int nu = P[0], nlev = P[1];
         const int32_t* units = P + 2;
         const int32_t* lev = units + 2 * nu;

@@ -1,0 +1,70 @@
+"""bench.py's one-line JSON contract: the reference arm on the CPU, the
+device arm (small workload) on a GPU, and the weak-scaling size rule."""
+
+import json
+import os
+import subprocess
+import sys
+import types
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+             "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "e2e"}
+
+
+def _run(args, timeout=900):
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], cwd=ROOT,
+                       capture_output=True, text=True, timeout=timeout)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+def test_reference_arm_line():
+    d = _run(["--impl", "reference", "--workload", "pack100", "--steps", "2", "--warmup", "1"])
+    assert d["impl"] == "reference"
+    assert BASE_KEYS <= set(d)
+    assert d["value"] > 0 and d["higher_is_better"] is True
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}
+    assert d["config"]["workload"] == "pack100"
+
+
+def test_points_per_rank_rule(monkeypatch):
+    import bench
+    args = types.SimpleNamespace(points_per_rank=3_000_000)
+    assert bench.points_per_rank(args, 8) == 3_000_000
+    args = types.SimpleNamespace(points_per_rank=None)
+    import psutil
+
+    class VM:
+        def __init__(self, avail):
+            self.available = avail
+
+    monkeypatch.setenv("LOCAL_WORLD_SIZE", "8")
+    monkeypatch.setattr(psutil, "virtual_memory", lambda: VM(2 * 2**40))
+    assert bench.points_per_rank(args, 8) == 8_000_000          # 2 TB host: configs[4]
+    monkeypatch.setattr(psutil, "virtual_memory", lambda: VM(200 * 2**30))
+    assert bench.points_per_rank(args, 8) == 1_000_000          # floor
+    monkeypatch.setenv("LOCAL_WORLD_SIZE", "1")
+    n = bench.points_per_rank(args, 1)
+    assert 1_000_000 <= n <= 8_000_000 and n % 1_000_000 == 0
+
+
+@pytest.mark.gpu
+def test_device_arm_line(gpu):
+    d = _run(["--workload", "pack100", "--steps", "20", "--warmup", "3", "--no-cpu-baseline"])
+    assert BASE_KEYS <= set(d) and "impl" not in d
+    assert d["n_gpus"] == 1 and d["steps"] == 20 and d["warmup"] == 3
+    assert d["value"] > 0 and d["gpu_launches"] > 0
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] == r["achieved"] / r["peak"]
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
+    assert d["e2e"]["d2h_bytes_per_step"] > 0
+    assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}

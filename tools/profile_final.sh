@@ -10,7 +10,7 @@ prof() {  # workload regex skip count
   echo "ncu $1 rc=$?"
 }
 prof svm1m "k_svm_chain_unit|k_var_giant" 3 4
-prof pack5000 "k_collision_tiles_v3|k_var_row_pipe" 3 3
+prof pack5000 "k_collision_tiles_v3|k_var_row_pipe|k_var_row_ring" 3 3
 prof mpc100k "k_mpc_chain" 3 2
 for w in svm1m pack5000 mpc100k; do
   ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$w.csv \

@@ -13,8 +13,8 @@ import sys
 LABELS = {
     "chain_svm": "void k_svm_chain_unit",
     "edge_collision": "void k_collision_tiles_v3",
-    "var_large_d1": "void k_var_row_pipe<1",
-    "var_large_d2": "void k_var_row_pipe<2",
+    "var_large_d1": ("void k_var_row_pipe<1", "void k_var_row_ring<1"),
+    "var_large_d2": ("void k_var_row_pipe<2", "void k_var_row_ring<2"),
     "edge_mpc_dyn": "void k_mpc_dyn_gemm",
     "var_small_deg4": "void k_var_small_run<4,",
     "var_giant_chunks": "void k_var_giant_chunks",
@@ -35,8 +35,9 @@ def traffic(path):
             i = hdr.index(key)
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(units[i], 1)
             byt += float(r[i].replace(",", "")) * scale
-        for label, pref in LABELS.items():
-            if name.startswith(pref.replace(" ", "")):
+        for label, prefs in LABELS.items():
+            prefs = (prefs,) if isinstance(prefs, str) else prefs
+            if any(name.startswith(p.replace(" ", "")) for p in prefs):
                 out.setdefault(label, []).append(byt)
     return {k: sum(v) / len(v) for k, v in out.items()}
 
