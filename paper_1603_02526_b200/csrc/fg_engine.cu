@@ -216,6 +216,8 @@ struct fg_plan {
     GChunk* d_gchunks = nullptr; int64_t nGC = 0;
     GComp* d_gcomps = nullptr; int gtop_smem = 0;
     GWork* d_gwork = nullptr; int64_t nGW = 0;
+    CompRef* d_gcref = nullptr;        // per chunk: its component (no dependent loads)
+    CompRef* d_gwref = nullptr;        // per update CTA: its component
     double* d_csum = nullptr;
     double* d_gz = nullptr;
     // partitioned runs: cut components exchange partial sums
@@ -319,7 +321,7 @@ fg_plan::~fg_plan() {
                     d_clvars[1], d_clvars[2], d_clvars[3], d_clvars[4], d_clprog[1],
                     d_clprog[2], d_clprog[3], d_clprog[4],
                     d_llist, d_lprog, d_prog, d_glist, d_gchunks, d_gcomps,
-                    d_gwork, d_csum, d_gz, d_part, d_res2, d_ctrl, d_hist, d_chain_xx,
+                    d_gwork, d_gcref, d_gwref, d_csum, d_gz, d_part, d_res2, d_ctrl, d_hist, d_chain_xx,
                     d_chain_fnorm, d_flag, d_bad, d_gcnt, d_ucnt, d_lexc[1], d_lexc[2], d_lexc[3],
                     d_lexc[4], d_row2[1], d_row2[2], d_row2[3], d_row2[4],
                     d_planoff[1], d_planoff[2], d_planoff[3], d_planoff[4], d_plans,
@@ -603,11 +605,11 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
             if (p->giant_fused && p->giant_unit)
                 k_var_giant_chunks<MODE, kGiantChunkThreads, true><<<grid, kGiantChunkThreads, p->gtop_smem, st>>>(
                     b, p->d_glist, p->d_gchunks, p->d_prog, p->d_csum, p->d_gcomps, p->d_gz,
-                    p->d_send, p->d_gcnt);
+                    p->d_send, p->d_gcnt, p->d_gcref);
             else if (p->giant_fused)
                 k_var_giant_chunks<MODE, kGiantChunkThreads><<<grid, kGiantChunkThreads, p->gtop_smem, st>>>(
                     b, p->d_glist, p->d_gchunks, p->d_prog, p->d_csum, p->d_gcomps, p->d_gz,
-                    p->d_send, p->d_gcnt);
+                    p->d_send, p->d_gcnt, p->d_gcref);
             else
                 k_var_giant_chunks<MODE><<<grid, kVarThreads, 0, st>>>(
                     b, p->d_glist, p->d_gchunks, p->d_prog, p->d_csum);
@@ -629,10 +631,12 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
             if (MODE != MODE_FUSED) return false;
             if (p->giant_unit)
                 k_var_giant_update<true><<<grid, kVarThreads, 0, st>>>(b, p->d_glist, p->d_gwork,
-                                                                       p->d_gz, po, p->fr_next);
+                                                                       p->d_gz, po, p->fr_next,
+                                                                       p->d_gwref);
             else
                 k_var_giant_update<false><<<grid, kVarThreads, 0, st>>>(b, p->d_glist, p->d_gwork,
-                                                                        p->d_gz, po, p->fr_next);
+                                                                        p->d_gz, po, p->fr_next,
+                                                                        p->d_gwref);
             return true;
     }
     return false;
@@ -1559,6 +1563,20 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     p->nG = (int64_t)glist.size();
     p->nGC = (int64_t)gchunks.size();
     p->nGW = (int64_t)gwork.size();
+    auto comp_of = [&](int32_t gi) {
+        const int32_t k = glist[gi];
+        const int32_t v = zvar[k];
+        CompRef r;
+        r.pb = pbase[v];
+        r.eb = ebase[v];
+        r.deg = deg[v];
+        r.d = dim[v];
+        r.c = (int32_t)(k - zbase[v]);
+        return r;
+    };
+    std::vector<CompRef> gcref, gwref;
+    for (const GChunk& ch : gchunks) gcref.push_back(comp_of(ch.gi));
+    for (const GWork& w : gwork) gwref.push_back(comp_of(w.gi));
     for (int c = 0; c < 3; ++c) p->nsblk[c] = (int64_t)sblk[c].size();
     // The bulk-copy pipeline measured slower than the register kernel on the
     // degree-4 SVM segments (0.86 vs 0.76 ms): opt-in via FGADMM_TMA=1.
@@ -1731,6 +1749,7 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
         (rc = upload(&p->d_lprog, lprog)) || (rc = upload(&p->d_prog, prog)) ||
         (rc = upload(&p->d_glist, glist)) || (rc = upload(&p->d_gchunks, gchunks)) ||
         (rc = upload(&p->d_gcomps, gcomps)) || (rc = upload(&p->d_gwork, gwork)) ||
+        (rc = upload(&p->d_gcref, gcref)) || (rc = upload(&p->d_gwref, gwref)) ||
         (rc = dalloc(&p->d_csum, gchunks.size())) || (rc = dalloc(&p->d_gz, 2 * glist.size())))
         return rc;
     for (int d = 1; d <= 4; ++d)

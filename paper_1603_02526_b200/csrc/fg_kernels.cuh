@@ -258,7 +258,8 @@ __device__ __forceinline__ int32_t comps_topoff(const GComp* c, int gi) { return
 template <int MODE, int NT = kVarThreads>
 __device__ void giant_top_body(const PassB& b, const int32_t* glist, const GComp* comps,
                                const int32_t* prog, const double* csum, double* gz,
-                               double* send, int gi, double* sv, int64_t it);
+                               double* send, int gi, double* sv, int64_t it,
+                               const CompRef* known = nullptr);
 // With `comps` non-null the last CTA to finish a component's chunks (an
 // atomic counter per component, reset by that CTA) also evaluates the top
 // of its tree: the separate top launch disappears.  The top program is the
@@ -267,7 +268,7 @@ template <int MODE, int NT = kVarThreads, bool UNIT = false>
 __global__ void __launch_bounds__(NT) k_var_giant_chunks(
     PassB b, const int32_t* glist, const GChunk* chunks, const int32_t* prog,
     double* csum, const GComp* comps = nullptr, double* gz = nullptr, double* send = nullptr,
-    unsigned* counters = nullptr) {
+    unsigned* counters = nullptr, const CompRef* cref = nullptr) {
     extern __shared__ double sv_top[];
     __shared__ int s_last;
     __shared__ double sv[2 * kMaxUnits];
@@ -277,7 +278,9 @@ __global__ void __launch_bounds__(NT) k_var_giant_chunks(
     if (s_stop) return;
     const int64_t it = b.ctrl->iter;
     const GChunk ch = chunks[blockIdx.x];
-    const CompRef r = comp_ref(b, glist[ch.gi]);
+    // the per-chunk table loads with the descriptor (no dependent chain
+    // glist -> zvar -> variable table before the leaf loads)
+    const CompRef r = cref ? cref[blockIdx.x] : comp_ref(b, glist[ch.gi]);
     bool bm = false;
     ValFn<MODE, UNIT> val(b, r, &bm);
     // pad = first element of the tree: 1 for a whole segment (a[0] is the
@@ -295,7 +298,7 @@ __global__ void __launch_bounds__(NT) k_var_giant_chunks(
         __syncthreads();
         if (s_last) {
             __threadfence();
-            giant_top_body<MODE, NT>(b, glist, comps, prog, csum, gz, send, ch.gi, sv_top, it);
+            giant_top_body<MODE, NT>(b, glist, comps, prog, csum, gz, send, ch.gi, sv_top, it, &r);
             if (threadIdx.x == 0) counters[ch.gi] = 0u;
         }
     }
@@ -310,7 +313,8 @@ __global__ void __launch_bounds__(NT) k_var_giant_chunks(
 template <int MODE, int NT>
 __device__ void giant_top_body(const PassB& b, const int32_t* glist, const GComp* comps,
                                const int32_t* prog, const double* csum, double* gz,
-                               double* send, int gi, double* sv, int64_t it) {
+                               double* send, int gi, double* sv, int64_t it,
+                               const CompRef* known) {
     const GComp gc = comps[gi];
     const int32_t k = glist[gi];
     const int32_t* P = prog + gc.topoff;
@@ -326,7 +330,7 @@ __device__ void giant_top_body(const PassB& b, const int32_t* glist, const GComp
     double a0 = 0.0, zw = 1.0, zo = 0.0;
     bool bm = false;
     if (threadIdx.x == 0 && gc.pad0 < 0) {
-        const CompRef r = comp_ref(b, k);
+        const CompRef r = known ? *known : comp_ref(b, k);
         ValFn<MODE> val(b, r, &bm);
         a0 = val(0);
         zw = b.zw[k];
@@ -417,7 +421,8 @@ struct GWork { int32_t gi, e0, e1, pad; };
 template <bool UNIT = false>
 __global__ void __launch_bounds__(kVarThreads, 2) k_var_giant_update(
     PassB b, const int32_t* glist, const GWork* work, const double* gz,
-    int64_t part_off, FusedReduce fr = FusedReduce{nullptr, 0, 0, 0, nullptr}) {
+    int64_t part_off, FusedReduce fr = FusedReduce{nullptr, 0, 0, 0, nullptr},
+    const CompRef* wref = nullptr) {
     __shared__ double sm[16];
     __shared__ int s_last;
     __shared__ int s_stop;
@@ -426,7 +431,7 @@ __global__ void __launch_bounds__(kVarThreads, 2) k_var_giant_update(
     if (s_stop) return;
     const int64_t it = b.ctrl->iter;
     const GWork wk = work[blockIdx.x];
-    const CompRef r = comp_ref(b, glist[wk.gi]);
+    const CompRef r = wref ? wref[blockIdx.x] : comp_ref(b, glist[wk.gi]);
     double pp = 0.0, dd = 0.0;
     bool bu = false;
     update_range<UNIT, UNIT ? 8 : 4>(b, r, wk.e0 + threadIdx.x, wk.e1, kVarThreads, gz[2 * wk.gi],
