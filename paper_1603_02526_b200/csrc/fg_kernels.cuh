@@ -598,7 +598,7 @@ __global__ void k_unit_rows(const int32_t* vlist, VarTab vt, const double* rho,
     for (int32_t k = threadIdx.x; k < dg; k += blockDim.x)
         if (rho[e0 + k] != 1.0 || alpha[e0 + k] != 1.0) {
             atomicAdd(&s_cnt, 1);
-            s_rank = k;
+            atomicMax(&s_rank, k);         // read only when it is the single one
         }
     __syncthreads();
     if (threadIdx.x == 0) {

@@ -62,6 +62,9 @@ k_var_row2(PassB b, const Row2* rows, const int32_t* prog, const LExc* exc, int6
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
+    // split cluster barrier: arrive now, wait before the first write into
+    // the peer's shared memory (the peer CTA must have started)
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
     if (threadIdx.x == 0) {
         const unsigned bytes = (unsigned)(sx.n * 8);
         mbar_expect_tx(&s_bar, 2 * bytes);
@@ -139,6 +142,7 @@ k_var_row2(PassB b, const Row2* rows, const int32_t* prog, const LExc* exc, int6
         }
     }
     __syncthreads();
+    asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
     if (threadIdx.x < 32) {                             // subtree top on warp 0
         int node = nu, op = 0;
         for (int l = 0; l < nlev; ++l) {

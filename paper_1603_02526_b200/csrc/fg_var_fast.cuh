@@ -391,6 +391,9 @@ k_var_cluster(PassB b, const int32_t* vlist, const int32_t* progoff, const int32
         }
     };
     double* sv0 = cluster.map_shared_rank(&sv[0][0], 0);
+    // rank 0's shared memory may be written only once that CTA has started
+    // (the cluster is co-scheduled, but the model requires the barrier)
+    cluster.sync();
     const int g = threadIdx.x >> 3, j = threadIdx.x & 7;
     constexpr int NG = kClusterThreads / 8;
     for (int r0 = L0; r0 < L1; r0 += NG) {           // uniform trip count
