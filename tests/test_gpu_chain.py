@@ -63,7 +63,8 @@ def test_chain_bitwise_equals_generic(gpu, monkeypatch, n, dim, iters):
 
 
 @pytest.mark.parametrize("env", [{"FGADMM_CHAIN_PF": "1"}, {"FGADMM_CHAIN_PF": "0"},
-                                 {"FGADMM_CHAIN_OCC3": "1", "FGADMM_CHAIN_PF": "0"}])
+                                 {"FGADMM_CHAIN_OCC3": "1", "FGADMM_CHAIN_PF": "0"},
+                                 {"FGADMM_CHAIN_OCC5": "1", "FGADMM_CHAIN_PF": "0"}])
 def test_chain_variants_bitwise(gpu, monkeypatch, env):
     """Compiled variants of the unit-weight chain (cp.async prefetch
     buffer, occupancy) equal the generic path bitwise."""
