@@ -754,7 +754,11 @@ void chain_pass(fg_plan* p, int in, cudaStream_t st) {
         const FusedReduce fr = p->mpc_reduce_fused
             ? FusedReduce{p->d_ucnt, p->npart, p->mpc_tiles, p->chain_grid, p->d_hist}
             : FusedReduce{nullptr, 0, 0, 0, nullptr};
-        k_mpc_chain<<<(unsigned)p->mpc_tiles, kEdgeThreads, p->mpc_smem, st>>>(b, p->mpc, 0, fr);
+        if (p->mpc.n0 == 20 && p->mpc.d == 16)         // configs[2]: state 16, input 4
+            k_mpc_chain<false, 20, 16><<<(unsigned)p->mpc_tiles, kEdgeThreads, p->mpc_smem, st>>>(
+                b, p->mpc, 0, fr);
+        else
+            k_mpc_chain<<<(unsigned)p->mpc_tiles, kEdgeThreads, p->mpc_smem, st>>>(b, p->mpc, 0, fr);
         return;
     }
     const unsigned G = (unsigned)chain_main_grid(p);
@@ -1052,6 +1056,8 @@ void detect_mpc_chain(fg_plan* p, const std::vector<int32_t>& dim,
     const int64_t slots = p->nsblk[0] + p->nsblk[1] + p->nsblk[2];
     if (p->mpc_tiles > slots) return;                // partial slots it reuses
     if (cudaFuncSetAttribute(k_mpc_chain<>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kMaxDynSmem) != cudaSuccess ||
+        cudaFuncSetAttribute(k_mpc_chain<false, 20, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kMaxDynSmem) != cudaSuccess)
         return;
     p->mpc_ok = true;

@@ -239,7 +239,10 @@ struct MpcChainDev {
     const double* kmat;                             // K (cols x cols)
 };
 
-template <bool FIRST_UNUSED = false>
+// N0/DD > 0: the state/input sizes as compile-time constants (the index
+// arithmetic -- divisions by n0, 2 n0, cols -- folds to multiplies; the
+// generic form divides at run time).  Same operations on the doubles.
+template <bool FIRST_UNUSED = false, int N0 = 0, int DD = 0>
 __global__ void __launch_bounds__(kEdgeThreads, 3) k_mpc_chain(PassB b, MpcChainDev c,
                                                                int64_t part_off,
                                                                FusedReduce fr) {
@@ -248,7 +251,8 @@ __global__ void __launch_bounds__(kEdgeThreads, 3) k_mpc_chain(PassB b, MpcChain
     __shared__ int s_last;
     if (b.ctrl->stop) return;
     const int64_t it = b.ctrl->iter;
-    const int n0 = c.n0, d = c.d, cols = n0 + d, ld = cols + 1, ldo = 2 * n0 + 1;
+    const int n0 = N0 > 0 ? N0 : c.n0, d = N0 > 0 ? DD : c.d;
+    const int cols = n0 + d, ld = cols + 1, ldo = 2 * n0 + 1;
     constexpr int KH = kMpcKH, RG = kMpcRG;
     double* Ks = gsm;                                   // [c][r0][k], row r = r0 + RG k
     double* nvs = Ks + cols * RG * KH;                  // [F][ld]
