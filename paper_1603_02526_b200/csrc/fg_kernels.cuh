@@ -80,6 +80,28 @@ struct ValFn {
         if (UNIT) return m;
         return m * rho[r.eb + e];                    // engine.py:278
     }
+    // the same value split into its loads and its arithmetic, so a caller
+    // can issue many elements' loads before any of them is used
+    struct Raw { double x, u, w; };
+    __device__ __forceinline__ Raw load(int64_t e) const {
+        const int64_t p = r.pb + e * r.d + r.c;
+        Raw v;
+        v.x = MODE == MODE_FUSED ? x[p] : 0.0;
+        v.u = u[p];
+        v.w = UNIT ? 1.0 : rho[r.eb + e];
+        return v;
+    }
+    __device__ __forceinline__ double value(const Raw& v) const {
+        double m;
+        if (MODE == MODE_FUSED) {
+            m = v.x + v.u;
+            *badm |= !finite(m);
+        } else {
+            m = v.u;
+        }
+        if (UNIT) return m;
+        return m * v.w;
+    }
 };
 
 // u update + residual partials for elements [e0, e1) of one component.
