@@ -243,7 +243,7 @@ struct MpcChainDev {
 // arithmetic -- divisions by n0, 2 n0, cols -- folds to multiplies; the
 // generic form divides at run time).  Same operations on the doubles.
 template <bool FIRST_UNUSED = false, int N0 = 0, int DD = 0>
-__global__ void __launch_bounds__(kEdgeThreads, 3) k_mpc_chain(PassB b, MpcChainDev c,
+__global__ void __launch_bounds__(kEdgeThreads, N0 > 0 ? 4 : 3) k_mpc_chain(PassB b, MpcChainDev c,
                                                                int64_t part_off,
                                                                FusedReduce fr) {
     extern __shared__ double gsm[];
