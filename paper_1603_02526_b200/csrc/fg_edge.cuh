@@ -611,7 +611,7 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 // weight loads, and the prox's weight arithmetic is the exact identity
 // (1/1 = 1, mu/4 = mu*0.25, mu/1 = mu), bitwise the general form.
 template <bool FIRST, bool A16, bool UNIT = false>
-__global__ void __launch_bounds__(kEdgeThreads, 3) k_collision_tiles_v3(PassA a, GroupDev g) {
+__global__ void __launch_bounds__(kEdgeThreads, UNIT ? 4 : 3) k_collision_tiles_v3(PassA a, GroupDev g) {
     __shared__ double2 s_c[kTile][kTile + 1];       // [jl][il]: j-half centers
     __shared__ double s_r[kTile][kTP], s_rc[kTile][kTP], s_rr[kTile][kTP];
     __shared__ double s_z[2][kTile][3];             // z of rows i0.. and j0..
