@@ -289,6 +289,7 @@ struct fg_plan {
     bool no_pipe = false;
     bool row_ring[5] = {false, false, false, false, false};  // persistent row kernel per dim
     bool pipe_deep = false;            // small-stage rows with 4 stages (A/B)
+    bool pipe_two[5] = {false, false, false, false, false};  // 2 small stages at 4 CTAs/SM
     int64_t ring_grid[5][2] = {};      // resident CTAs of the ring kernel per dim / stage form
     // 2 stages of twice the size: measured better for dim >= 2 rows (pack
     // center rows 0.285 vs 0.306 ms), worse for dim 1 (0.176 vs 0.160)
@@ -519,7 +520,9 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
             k_var_small_run<0, MODE><<<grid, 256, 0, st>>>(b, p->d_sruns, p->d_sblk[2], po);
             return true;
         case 3:
-            if (MODE == MODE_FUSED && p->lunit[1] && p->pipe_ok[1] && !p->no_pipe && p->row_ring[1])
+            if (MODE == MODE_FUSED && p->lunit[1] && p->pipe_ok[1] && !p->no_pipe && p->pipe_two[1])
+                k_var_row_pipe<1, 2, kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2), st>>>(b, p->d_rowdesc[1], p->d_prog, p->d_plans, p->d_lexc[1], po);
+            else if (MODE == MODE_FUSED && p->lunit[1] && p->pipe_ok[1] && !p->no_pipe && p->row_ring[1])
                 launch_ring<1>(p, b, nb, po, st);
             else if (MODE == MODE_FUSED && p->lunit[1] && p->pipe_ok[1] && !p->no_pipe && p->pipe_big[1])
                 k_var_row_pipe<1, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_rowdesc[1], p->d_prog, p->d_plans, p->d_lexc[1], po);
@@ -539,7 +542,9 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
                 k_var_large_vec<1, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po, nullptr, p->row2_ok[1] ? po + grid : -1);
             return true;
         case 4:
-            if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe && p->row_ring[2])
+            if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe && p->pipe_two[2])
+                k_var_row_pipe<2, 2, kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2), st>>>(b, p->d_rowdesc[2], p->d_prog, p->d_plans, p->d_lexc[2], po);
+            else if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe && p->row_ring[2])
                 launch_ring<2>(p, b, nb, po, st);
             else if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe && p->pipe_big[2])
                 k_var_row_pipe<2, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_rowdesc[2], p->d_prog, p->d_plans, p->d_lexc[2], po);
@@ -559,7 +564,9 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
                 k_var_large_vec<2, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po, nullptr, p->row2_ok[2] ? po + grid : -1);
             return true;
         case 5:
-            if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe && p->row_ring[3])
+            if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe && p->pipe_two[3])
+                k_var_row_pipe<3, 2, kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2), st>>>(b, p->d_rowdesc[3], p->d_prog, p->d_plans, p->d_lexc[3], po);
+            else if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe && p->row_ring[3])
                 launch_ring<3>(p, b, nb, po, st);
             else if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe && p->pipe_big[3])
                 k_var_row_pipe<3, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_rowdesc[3], p->d_prog, p->d_plans, p->d_lexc[3], po);
@@ -579,7 +586,9 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
                 k_var_large_vec<3, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po, nullptr, p->row2_ok[3] ? po + grid : -1);
             return true;
         case 6:
-            if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe && p->row_ring[4])
+            if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe && p->pipe_two[4])
+                k_var_row_pipe<4, 2, kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2), st>>>(b, p->d_rowdesc[4], p->d_prog, p->d_plans, p->d_lexc[4], po);
+            else if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe && p->row_ring[4])
                 launch_ring<4>(p, b, nb, po, st);
             else if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe && p->pipe_big[4])
                 k_var_row_pipe<4, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_rowdesc[4], p->d_prog, p->d_plans, p->d_lexc[4], po);
@@ -1630,6 +1639,16 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     if (getenv("FGADMM_PIPE_BIG"))
         for (int d = 1; d <= 4; ++d) p->pipe_big[d] = std::atoi(getenv("FGADMM_PIPE_BIG")) != 0;
     p->pipe_deep = getenv("FGADMM_PIPE_DEEP") != nullptr;
+    {
+        // two 1280-double stages at 4 CTAs/SM: default for dim-1 rows (pack
+        // N=5000 radius rows 0.137 vs 0.157 ms); FGADMM_PIPE_TWO=1 all dims,
+        // =0 none
+        const char* e = getenv("FGADMM_PIPE_TWO");
+        for (int d = 1; d <= 4; ++d) {
+            p->pipe_two[d] = e ? (e[0] == '1') : (d == 1 && !getenv("FGADMM_PIPE_BIG") && !p->pipe_deep);
+            if (p->pipe_two[d]) p->pipe_big[d] = false;
+        }
+    }
     if (p->pipe_deep)
         for (int d = 1; d <= 4; ++d) p->pipe_big[d] = false;   // deep form uses the small stages
     {   // TMA-ring row plans, one per distinct degree and dim
@@ -1691,6 +1710,10 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
         CK(cudaFuncSetAttribute(k_var_row_pipe<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         CK(cudaFuncSetAttribute(k_var_row_pipe<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         CK(cudaFuncSetAttribute(k_var_row_pipe<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CK(cudaFuncSetAttribute(k_var_row_pipe<1, 2, kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2)));
+        CK(cudaFuncSetAttribute(k_var_row_pipe<2, 2, kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2)));
+        CK(cudaFuncSetAttribute(k_var_row_pipe<3, 2, kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2)));
+        CK(cudaFuncSetAttribute(k_var_row_pipe<4, 2, kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2)));
         const int smem4 = (int)row_pipe_smem(4);
         CK(cudaFuncSetAttribute(k_var_row_pipe<1, 4, kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4));
         CK(cudaFuncSetAttribute(k_var_row_pipe<2, 4, kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4));
