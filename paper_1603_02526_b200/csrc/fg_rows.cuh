@@ -230,11 +230,13 @@ struct __align__(16) RowDesc {
     int32_t pad[2];
 };
 
+constexpr int kPipeMidDoubles = 2048;             // mid stage form (3 CTAs/SM at 2 stages)
 constexpr int kPipeStages = 3;
 constexpr int kPipeStageDoubles = 1280;             // per array per stage
 
 template <int D, int NS = kPipeStages, int SDB = kPipeStageDoubles>
-__global__ void __launch_bounds__(kRowThreads, NS == 3 ? 3 : (NS == 2 && SDB <= kPipeStageDoubles ? 4 : 2))
+__global__ void __launch_bounds__(kRowThreads, NS == 3 ? 3 : (NS == 2 && SDB <= kPipeStageDoubles ? 4
+                                                    : (NS == 2 && SDB <= kPipeMidDoubles ? 3 : 2)))
 k_var_row_pipe(PassB b, const RowDesc* rdesc, const int32_t* prog, const int32_t* plans,
                const LExc* exc, int64_t part_off) {
     extern __shared__ __align__(16) double pipe_smem[];
