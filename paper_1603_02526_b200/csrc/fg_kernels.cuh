@@ -441,7 +441,7 @@ struct FusedReduce {
 // G3: u update of giant components, one CTA per element range.
 struct GWork { int32_t gi, e0, e1, pad; };
 template <bool UNIT = false>
-__global__ void __launch_bounds__(kVarThreads, 2) k_var_giant_update(
+__global__ void __launch_bounds__(kVarThreads, UNIT ? 4 : 2) k_var_giant_update(
     PassB b, const int32_t* glist, const GWork* work, const double* gz,
     int64_t part_off, FusedReduce fr = FusedReduce{nullptr, 0, 0, 0, nullptr},
     const CompRef* wref = nullptr) {
@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(kVarThreads, 2) k_var_giant_update(
     const CompRef r = wref ? wref[blockIdx.x] : comp_ref(b, glist[wk.gi]);
     double pp = 0.0, dd = 0.0;
     bool bu = false;
-    update_range<UNIT, UNIT ? 8 : 4>(b, r, wk.e0 + threadIdx.x, wk.e1, kVarThreads, gz[2 * wk.gi],
+    update_range<UNIT, 4>(b, r, wk.e0 + threadIdx.x, wk.e1, kVarThreads, gz[2 * wk.gi],
                           gz[2 * wk.gi + 1], pp, dd, bu);
     if (bu) flag_error(b.ctrl, it, FG_PHASE_U, false);
     block_sum2<kVarThreads>(pp, dd, sm);
