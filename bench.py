@@ -322,7 +322,9 @@ def points_per_rank(args, world):
     points before the page-locked state copy), else the largest whole million that fits (at least 1M)."""
     if args.points_per_rank:
         return args.points_per_rank
-    target, per_point = 8_000_000, 12_000          # bytes of host memory per point
+    # peak host bytes per point: graph build (~9.8 KB measured) plus the
+    # page-locked state copy made before the pageable one is freed
+    target, per_point = 8_000_000, 16_000
     try:
         import psutil
         avail = psutil.virtual_memory().available
