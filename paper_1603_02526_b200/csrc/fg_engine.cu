@@ -291,6 +291,7 @@ struct fg_plan {
     bool pipe_deep = false;            // small-stage rows with 4 stages (A/B)
     bool pipe_two[5] = {false, false, false, false, false};  // 2 small stages at 4 CTAs/SM
     bool pipe_mid[5] = {false, false, false, false, false};  // 2 mid stages at 3 CTAs/SM
+    bool l2hint = true;                // mid rows: L2 evict_last on phase-1 copies
     int64_t ring_grid[5][2] = {};      // resident CTAs of the ring kernel per dim / stage form
     // 2 stages of twice the size: measured better for dim >= 2 rows (pack
     // center rows 0.285 vs 0.306 ms), worse for dim 1 (0.176 vs 0.160)
@@ -543,7 +544,9 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
                 k_var_large_vec<1, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po, nullptr, p->row2_ok[1] ? po + grid : -1);
             return true;
         case 4:
-            if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe && p->pipe_mid[2])
+            if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe && p->pipe_mid[2] && p->l2hint)
+                k_var_row_pipe<2, 2, kPipeMidDoubles, true><<<grid, kRowThreads, row_pipe_smem(2, kPipeMidDoubles), st>>>(b, p->d_rowdesc[2], p->d_prog, p->d_plans, p->d_lexc[2], po);
+            else if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe && p->pipe_mid[2])
                 k_var_row_pipe<2, 2, kPipeMidDoubles><<<grid, kRowThreads, row_pipe_smem(2, kPipeMidDoubles), st>>>(b, p->d_rowdesc[2], p->d_prog, p->d_plans, p->d_lexc[2], po);
             else if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe && p->pipe_two[2])
                 k_var_row_pipe<2, 2, kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2), st>>>(b, p->d_rowdesc[2], p->d_prog, p->d_plans, p->d_lexc[2], po);
@@ -567,7 +570,9 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
                 k_var_large_vec<2, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po, nullptr, p->row2_ok[2] ? po + grid : -1);
             return true;
         case 5:
-            if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe && p->pipe_mid[3])
+            if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe && p->pipe_mid[3] && p->l2hint)
+                k_var_row_pipe<3, 2, kPipeMidDoubles, true><<<grid, kRowThreads, row_pipe_smem(2, kPipeMidDoubles), st>>>(b, p->d_rowdesc[3], p->d_prog, p->d_plans, p->d_lexc[3], po);
+            else if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe && p->pipe_mid[3])
                 k_var_row_pipe<3, 2, kPipeMidDoubles><<<grid, kRowThreads, row_pipe_smem(2, kPipeMidDoubles), st>>>(b, p->d_rowdesc[3], p->d_prog, p->d_plans, p->d_lexc[3], po);
             else if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe && p->pipe_two[3])
                 k_var_row_pipe<3, 2, kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2), st>>>(b, p->d_rowdesc[3], p->d_prog, p->d_plans, p->d_lexc[3], po);
@@ -591,7 +596,9 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
                 k_var_large_vec<3, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po, nullptr, p->row2_ok[3] ? po + grid : -1);
             return true;
         case 6:
-            if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe && p->pipe_mid[4])
+            if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe && p->pipe_mid[4] && p->l2hint)
+                k_var_row_pipe<4, 2, kPipeMidDoubles, true><<<grid, kRowThreads, row_pipe_smem(2, kPipeMidDoubles), st>>>(b, p->d_rowdesc[4], p->d_prog, p->d_plans, p->d_lexc[4], po);
+            else if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe && p->pipe_mid[4])
                 k_var_row_pipe<4, 2, kPipeMidDoubles><<<grid, kRowThreads, row_pipe_smem(2, kPipeMidDoubles), st>>>(b, p->d_rowdesc[4], p->d_prog, p->d_plans, p->d_lexc[4], po);
             else if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe && p->pipe_two[4])
                 k_var_row_pipe<4, 2, kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2), st>>>(b, p->d_rowdesc[4], p->d_prog, p->d_plans, p->d_lexc[4], po);
@@ -1663,6 +1670,9 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
         // (pack N=5000 center rows 0.254 vs 0.264 ms for 2 x 2560 at 2/SM)
         const char* e = getenv("FGADMM_PIPE_MID");
         const bool dflt = !getenv("FGADMM_PIPE_BIG") && !p->pipe_deep;
+        // phase-1 copies of the mid rows marked L2 evict_last (their bytes
+        // are read again by phase 2), phase-2 copies evict_first: default
+        p->l2hint = !(getenv("FGADMM_L2HINT") && getenv("FGADMM_L2HINT")[0] == '0');
         for (int d = 2; d <= 4; ++d)
             if (!p->pipe_two[d] && (e ? e[0] == '1' : dflt)) {
                 p->pipe_mid[d] = true;
@@ -1732,6 +1742,9 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
         CK(cudaFuncSetAttribute(k_var_row_pipe<1, 2, kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2)));
         CK(cudaFuncSetAttribute(k_var_row_pipe<2, 2, kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2)));
         CK(cudaFuncSetAttribute(k_var_row_pipe<2, 2, kPipeMidDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2, kPipeMidDoubles)));
+        CK(cudaFuncSetAttribute(k_var_row_pipe<2, 2, kPipeMidDoubles, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2, kPipeMidDoubles)));
+        CK(cudaFuncSetAttribute(k_var_row_pipe<3, 2, kPipeMidDoubles, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2, kPipeMidDoubles)));
+        CK(cudaFuncSetAttribute(k_var_row_pipe<4, 2, kPipeMidDoubles, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2, kPipeMidDoubles)));
         CK(cudaFuncSetAttribute(k_var_row_pipe<3, 2, kPipeMidDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2, kPipeMidDoubles)));
         CK(cudaFuncSetAttribute(k_var_row_pipe<4, 2, kPipeMidDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2, kPipeMidDoubles)));
         CK(cudaFuncSetAttribute(k_var_row_pipe<3, 2, kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2)));

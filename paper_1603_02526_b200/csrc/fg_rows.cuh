@@ -234,7 +234,7 @@ constexpr int kPipeMidDoubles = 2048;             // mid stage form (3 CTAs/SM a
 constexpr int kPipeStages = 3;
 constexpr int kPipeStageDoubles = 1280;             // per array per stage
 
-template <int D, int NS = kPipeStages, int SDB = kPipeStageDoubles>
+template <int D, int NS = kPipeStages, int SDB = kPipeStageDoubles, bool L2HINT = false>
 __global__ void __launch_bounds__(kRowThreads, NS == 3 ? 3 : (NS == 2 && SDB <= kPipeStageDoubles ? 4
                                                     : (NS == 2 && SDB <= kPipeMidDoubles ? 3 : 2)))
 k_var_row_pipe(PassB b, const RowDesc* rdesc, const int32_t* prog, const int32_t* plans,
@@ -271,8 +271,15 @@ k_var_row_pipe(PassB b, const RowDesc* rdesc, const int32_t* prog, const int32_t
         double* base = pipe_smem + (int64_t)s * 2 * SD;
         const unsigned bytes = (unsigned)(sx.n * 8);
         mbar_expect_tx(&full[s], 2 * bytes);
-        bulk_g2s(base, b.x + sx.lo, bytes, &full[s]);
-        bulk_g2s(base + SD, b.uin + sx.lo, bytes, &full[s]);
+        if (L2HINT) {
+            // phase-1 bytes are read again by phase 2: keep them in L2
+            const uint64_t pol = j < J1 ? l2_policy_evict_last() : l2_policy_evict_first();
+            bulk_g2s_hint(base, b.x + sx.lo, bytes, &full[s], pol);
+            bulk_g2s_hint(base + SD, b.uin + sx.lo, bytes, &full[s], pol);
+        } else {
+            bulk_g2s(base, b.x + sx.lo, bytes, &full[s]);
+            bulk_g2s(base + SD, b.uin + sx.lo, bytes, &full[s]);
+        }
     };
     if (threadIdx.x == 0)
         for (int k = 0; k < NS && k < NJ; ++k) issue(k, k);

@@ -267,7 +267,8 @@ def test_packing_1030_cluster_and_tile_kernels_bitwise(gpu):
                                  {"FGADMM_ROW_RING": "1", "FGADMM_PIPE_BIG": "1"},
                                  {"FGADMM_ROW_RING": "0"}, {"FGADMM_PIPE_DEEP": "1"},
                                  {"FGADMM_PIPE_TWO": "1"}, {"FGADMM_PIPE_MID": "0"},
-                                 {"FGADMM_PIPE_MID": "0", "FGADMM_ROW_RING": "1"}])
+                                 {"FGADMM_PIPE_MID": "0", "FGADMM_ROW_RING": "1"},
+                                 {"FGADMM_L2HINT": "0"}])
 def test_opt_in_kernel_variants_match_oracle(gpu, env, monkeypatch):
     """The alternative kernels selected at plan creation (TMA bulk-copy
     pipeline for small segments, 4-CTA DSMEM cluster rows, cp.async
