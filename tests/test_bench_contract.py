@@ -68,3 +68,25 @@ def test_device_arm_line(gpu):
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
     assert d["e2e"]["d2h_bytes_per_step"] > 0
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+
+
+@pytest.mark.gpu
+def test_multi_gpu_arm_line_at_one_rank(gpu):
+    """The torchrun / NCCL arm (factor-partitioned SVM rank graph, NCCL
+    all-gather inside the captured iteration) end to end at one rank."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "1", "--master-addr", "127.0.0.1",
+                        "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--gpus", "1", "--partition", "--points-per-rank", "200000",
+                        "--steps", "6", "--warmup", "3"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert BASE_KEYS <= set(d)
+    assert d["n_gpus"] == 1 and d["scaling"] == "weak" and d["value"] > 0
+    assert d["config"]["points_per_rank"] == 200000 and d["chain_form"] in ("unit", "fast")
+    assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
