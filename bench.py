@@ -381,15 +381,20 @@ def multi_gpu(args, fg, dist, rank, world, local):
     # of the host state, run, download the rank's state (wall clock, max
     # over ranks)
     lg = nr.local
+    pinned = True
     if weak:
         # rank graphs hold the rank's own state: page-locked like the 1-GPU
-        # arm, downloaded back into the same arrays (as run() does)
-        st_in = fg.pinned_state(lg, st)
-        del st
+        # arm, downloaded back into the same arrays (as run() does); if the
+        # host cannot pin that much, the pageable state is used (slower e2e)
+        try:
+            st_in = fg.pinned_state(lg, st)
+            del st
+        except Exception:                           # pragma: no cover
+            st_in, pinned = st, False
         ls = [st_in.x, st_in.m, st_in.u, st_in.n]
         lz = st_in.z
     else:
-        st_in = st
+        st_in, pinned = st, False
         ls = [np.empty(lg.total_edge_payload) for _ in range(4)]
         lz = np.empty(lg.z_dim)
     dist.barrier()
@@ -405,6 +410,7 @@ def multi_gpu(args, fg, dist, rank, world, local):
     e2e = {"value": E * args.steps / float(e2e_s.item()), "unit": UNIT,
            "h2d_bytes_per_step": int((Z_tot + 2 * P_tot) * 8 // args.steps),
            "d2h_bytes_per_step": int((4 * P_tot + Z_tot) * 8 // args.steps),
+           "pinned": pinned,
            "note": "per rank: upload its part of z,u,n, run, download its x,m,z,u,n; "
                    "max over ranks of the wall clock"}
     line = {
