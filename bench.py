@@ -351,7 +351,11 @@ def multi_gpu(args, fg, dist, rank, world, local):
     t_build = time.perf_counter()
     weak = args.workload.startswith("svm")
     if weak:
-        n = points_per_rank(args, world)
+        # every rank must hold the same number of points: the smallest
+        # any rank's host memory allows
+        nt = torch.tensor([points_per_rank(args, world)], device="cuda", dtype=torch.int64)
+        dist.all_reduce(nt, op=dist.ReduceOp.MIN)
+        n = int(nt.item())
         X, y = fg.gen_gaussian_arrays(n, 32, 4.0, seed=rank)
         lg = svm_rank_graph(X, y, rank, world, lam=1.0)
         nr = NcclRank(None, rank, world, device=local, local=lg)
