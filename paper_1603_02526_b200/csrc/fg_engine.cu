@@ -170,6 +170,7 @@ struct fg_plan {
     int32_t* d_chk = nullptr;
     int32_t* h_chk = nullptr;           // pinned copy of the check flag
     int n_pending = 0;                  // upload check in flight
+    bool spec_unavailable = false;      // its buffers did not fit: synchronous uploads
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t V = 0, E = 0, P = 0, Z = 0;
     // var tables
@@ -2131,17 +2132,27 @@ static int settle_idle(fg_plan* p) {
 // and k_n_check_ref compares it, from the staging buffers, concurrently
 // with the iterations.  fg_run settles the check at its end and, on a
 // mismatch, restores the uploaded state and runs again reading n.
+// Resources of the speculative upload (a second P-sized staging buffer);
+// false when the device cannot hold them -- the upload is then synchronous.
+static bool spec_resources(fg_plan* p) {
+    if (p->stream_copy) return true;
+    if (p->spec_unavailable) return false;
+    bool ok = cudaMalloc((void**)&p->d_stage2, (size_t)std::max<int64_t>(1, p->P) * sizeof(double)) == cudaSuccess &&
+              cudaMalloc((void**)&p->d_chk, sizeof(int32_t)) == cudaSuccess &&
+              cudaMallocHost((void**)&p->h_chk, sizeof(int32_t)) == cudaSuccess &&
+              cudaEventCreateWithFlags(&p->ev_up, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&p->ev_up2, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&p->ev_chk, cudaEventDisableTiming) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&p->stream_copy, cudaStreamNonBlocking) == cudaSuccess;
+    if (!ok) {
+        cudaGetLastError();                          // not sticky: allocation failures
+        p->spec_unavailable = true;
+    }
+    return ok;
+}
+
 static int upload_speculative(fg_plan* p, const double* z, const double* u, const double* n) {
     cudaStream_t st = p->stream;
-    if (!p->stream_copy) {
-        CK(cudaStreamCreateWithFlags(&p->stream_copy, cudaStreamNonBlocking));
-        CK(cudaEventCreateWithFlags(&p->ev_up, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&p->ev_up2, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&p->ev_chk, cudaEventDisableTiming));
-        CK(cudaMallocHost((void**)&p->h_chk, sizeof(int32_t)));
-        if (int rc = dalloc(&p->d_stage2, p->P)) return rc;
-        if (int rc = dalloc(&p->d_chk, 1)) return rc;
-    }
     CK(cudaMemcpyAsync(p->d_zb[0], z, p->Z * sizeof(double), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(p->d_stage, u, p->P * sizeof(double), cudaMemcpyHostToDevice, st));
     CK(cudaEventRecord(p->ev_up, st));               // z, u transferred: n may follow
@@ -2194,7 +2205,8 @@ int fg_state_upload(fg_plan* p, const double* z, const double* u, const double* 
         if (int rc = settle_upload(p, &mism)) return rc;
     }
     // multi-rank runs stay in lock step: no speculative first iterations
-    if (spec_upload_enabled() && !p->nccl_comm) return upload_speculative(p, z, u, n);
+    if (spec_upload_enabled() && !p->nccl_comm && spec_resources(p))
+        return upload_speculative(p, z, u, n);
     CK(cudaMemcpyAsync(p->d_zb[0], z, p->Z * sizeof(double), cudaMemcpyHostToDevice, p->stream));
     upload_vm(p, u, p->d_u[0]);
     upload_vm(p, n, p->d_u[1]);   // consumed by the first edge pass
