@@ -1,7 +1,7 @@
 """Benchmark: ADMM edge-updates/sec of the B200 engine (and its roofline).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload svm1m]
-    python bench.py --impl reference ...      # CPU reference arm (oracle port)
+    python bench.py --impl reference ...      # CPU reference arm (fgadmm itself)
 
 A step is one ADMM iteration (all five phases) over the whole graph.  The
 default workload is BASELINE.json configs[1]: the soft-margin SVM chain on
@@ -18,8 +18,9 @@ e2e        = the same K iterations through the public ``run()`` call with
 roofline   = dominant kernel's algorithmic bytes per launch / its average
              CUDA-event duration (``fg_profile_kernels``), against the
              measured HBM copy bandwidth in MEASURED_PEAKS.json.
-cpu_baseline = the NumPy oracle port of the reference (oracle/) on a
-             bounded sample of the same workload, 1 core.
+cpu_baseline = the reference's own fgadmm.engine.run (installed under
+             baseline/_ref) on a bounded sample of the same workload
+             (the oracle port when it is not installed).
 """
 
 from __future__ import annotations
@@ -60,9 +61,8 @@ def build_instance(name, scale=1.0):
         n = int((5000 if name == "pack5000" else 100) * (scale if name == "pack5000" else 1))
         spec = fg.PackingSpec(n)
         g = fg.build_packing(spec)
-        st = fg.packing_init(g, spec, seed=0) if n <= 1000 else fg.init_state(g, seed=0)
-        return g, st, {"disks": n, "init": "packing_init(seed=0)" if n <= 1000 else
-                       "init_state(seed=0)"}
+        st = fg.packing_init(g, spec, seed=0)
+        return g, st, {"disks": n, "init": "packing_init(seed=0)"}
     if name.startswith("mpc"):
         T = int(100_000 * scale)
         rng = np.random.default_rng(0)
@@ -132,6 +132,10 @@ def kernel_bytes(graph, plan):
         # write per component, the cost diagonal per component
         P, Z = graph.total_edge_payload, graph.z_dim
         out["chain_mpc"] = P * 16 + Z * 24
+        # temporally blocked chain: the same compulsory bytes once per
+        # launch of forms["mpc_block"] iterations (halo re-reads excluded)
+        out["chain_mpc_block"] = P * 16 + Z * 24
+        out["reduce_block"] = 16 * forms["mpc_block"] * (Z // 20 // 45 + 1)
     return out
 
 
@@ -255,10 +259,81 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
-def cpu_baseline(name, iters=None):
-    """NumPy oracle (reference port) on a bounded sample, one core."""
-    from oracle import fgadmm_oracle as O
+def reference_package():
+    """The reference package ``fgadmm`` itself, installed unmodified under
+    baseline/_ref (``pip install --no-index --target baseline/_ref``, see
+    DESIGN.md section 7); None when it is not installed."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "fgadmm")):
+        return None
+    if path not in sys.path:
+        sys.path.append(path)
+    import fgadmm
+    return fgadmm
+
+
+def host_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "cpu_count": os.cpu_count(),
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS")}
+
+
+def reference_instance(ref, name, scale=1.0):
+    """The workload built by the reference's OWN builders (problems.py),
+    the same generators and specs as build_instance.  Packing starts from
+    packing_init(seed=0): its arrays come from this package's replica,
+    which is bit-identical to the reference's (tests/test_oracle.py) and
+    O(N) faster; the graph layouts are identical (tests/test_documents.py)."""
+    P = ref.problems
+    if name.startswith("svm"):
+        n = int(1_000_000 * scale)
+        g = P.build_svm(P.SvmSpec(P.gen_gaussian_data(n, 32, 4.0, seed=0), lam=1.0))
+        return g, ref.init_state(g), {"points": n, "dim": 32, "init": "zeros"}
+    if name.startswith("mpc"):
+        T = int(100_000 * scale)
+        rng = np.random.default_rng(0)
+        A = 0.05 * rng.standard_normal((16, 16))
+        B = 0.1 * rng.standard_normal((16, 4))
+        q0 = rng.standard_normal(16)
+        g = P.build_mpc(P.MpcSpec(T, ref.LinearSystem(A, B), q0))
+        return g, ref.init_state(g), {"horizon": T, "state_dim": 16, "input_dim": 4}
     import paper_1603_02526_b200 as fg
+    n = int((5000 if name == "pack5000" else 100) * (scale if name == "pack5000" else 1))
+    g = P.build_packing(P.PackingSpec(n))
+    og = fg.build_packing(fg.PackingSpec(n))
+    st = fg.packing_init(og, fg.PackingSpec(n), seed=0)
+    rs = ref.AdmmState(*(getattr(st, k) for k in "xmzun"))
+    return g, rs, {"disks": n, "init": "packing_init(seed=0)"}
+
+
+def _copy_ref_state(ref, st):
+    return ref.AdmmState(*(np.array(getattr(st, k), copy=True) for k in "xmzun"))
+
+
+def time_reference_run(ref, g, st, iterations, workers, record_every=None):
+    """Seconds per iteration of fgadmm.engine.run itself (wall clock of the
+    call; the report's total_seconds beside it)."""
+    s = _copy_ref_state(ref, st)
+    cfg = ref.RunConfig(max_iterations=iterations, workers=workers,
+                        record_every=record_every or iterations)
+    t0 = time.perf_counter()
+    _sol, rep = ref.run(g, cfg, state=s)
+    wall = time.perf_counter() - t0
+    return wall / iterations, rep, s
+
+
+def cpu_baseline(name, iters=None):
+    """The reference's own fgadmm.engine.run (baseline/_ref; else the NumPy
+    oracle port) on a bounded sample of the same workload: ~10-30 s of CPU
+    work, the faster of 1 worker and one per host thread."""
     if name.startswith("svm"):
         scale, desc = 0.1, "SVM chain 100k x 32 (same generator)"
     elif name == "pack5000":
@@ -267,12 +342,28 @@ def cpu_baseline(name, iters=None):
         scale, desc = 0.05, "MPC 16/4 horizon 5k (same generator)"
     else:
         scale, desc = 1.0, "packing N=100"
-    g, st, _info = build_instance(name if name != "pack5000" else "pack5000", scale)
+    ref = reference_package()
+    if ref is not None:
+        g, st, _info = reference_instance(ref, name, scale)
+        E = len(g.edge_var)
+        best = None
+        for w in sorted({1, os.cpu_count() or 1}):
+            time_reference_run(ref, g, st, 1, w)          # builds the lane plan
+            tpi, _r, _s = time_reference_run(ref, g, st, 2, w)
+            if best is None or tpi < best[0]:
+                best = (tpi, w)
+        n = iters or max(2, min(500, int(8.0 / max(best[0], 1e-6))))
+        tpi, _r, _s = time_reference_run(ref, g, st, n, best[1])
+        return {"value": E / tpi, "unit": UNIT, "cores": best[1], "kind": "reference",
+                "sample": f"{desc}: fgadmm.engine.run (baseline/_ref), {n} iterations, "
+                          f"workers={best[1]}, record_every={n}, {E} edges, "
+                          f"{tpi * 1e3:.2f} ms/iter"}
+    from oracle import fgadmm_oracle as O
+    g, st, _info = build_instance(name, scale)
     o = O.Oracle(g)
     O.time_iterations(g, st, 1, oracle=o)             # warm caches
-    budget = 8.0
     t1, _ = O.time_iterations(g, st, 1, oracle=o)
-    n = iters or max(2, min(200, int(budget / max(t1, 1e-6))))
+    n = iters or max(2, min(200, int(8.0 / max(t1, 1e-6))))
     tpi, _ = O.time_iterations(g, st, n, oracle=o)
     E = len(g.edge_var)
     return {"value": E / tpi, "unit": UNIT, "cores": 1, "kind": "port",
@@ -280,37 +371,90 @@ def cpu_baseline(name, iters=None):
 
 
 def reference_arm(args):
+    """``--impl reference``: the reference's own CPU implementation,
+    fgadmm.engine.run from baseline/_ref, on THIS workload at full size
+    (pack5000 excepted: a 1/5-size sample, extrapolated per edge).  W
+    warm-up iterations, then K timed iterations in one run() call
+    (record_every = K), with the worker count that
+    was faster in a short probe of 1 worker and one per host thread; the
+    probe times and a record_every=1 (the reference default) run are
+    reported beside it.  Without baseline/_ref the oracle port is timed."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from oracle import fgadmm_oracle as O
     name = args.workload
-    scale = {"svm1m": 0.1, "pack5000": 0.2, "mpc100k": 0.05}.get(name, 1.0)
-    g, st, info = build_instance(name, scale)
-    o = O.Oracle(g)
-    s = O.State.copy_of(st)
-    for _ in range(args.warmup):
-        o.iterate(s)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        o.iterate(s)
-    dt = time.perf_counter() - t0
+    ref = reference_package()
+    scale = 0.2 if name == "pack5000" else 1.0
+    base = {"impl": "reference", "metric": METRIC, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic"}
+    if ref is None:
+        from oracle import fgadmm_oracle as O
+        g, st, info = build_instance(name, scale)
+        o = O.Oracle(g)
+        s = O.State.copy_of(st)
+        for _ in range(args.warmup):
+            o.iterate(s)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            o.iterate(s)
+        dt = time.perf_counter() - t0
+        E = len(g.edge_var)
+        value = E * args.steps / dt
+        line = dict(base, value=value, ms_per_step=dt / args.steps * 1e3,
+                    config={"workload": name, **info, "scale": scale,
+                            "same_config": scale == 1.0},
+                    cpu_baseline={"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                                  "sample": f"oracle port, {E} edges per step"},
+                    e2e={"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                         "d2h_bytes_per_step": 0},
+                    host=host_info())
+        print(json.dumps(line))
+        return 0
+    t_build = time.perf_counter()
+    g, st, info = reference_instance(ref, name, scale)
+    t_build = time.perf_counter() - t_build
     E = len(g.edge_var)
+    ncpu = os.cpu_count() or 1
+    probe = {}
+    for w in sorted({1, ncpu}):
+        time_reference_run(ref, g, st, 1, w)              # builds the lane plan
+        tpi, _r, _s = time_reference_run(ref, g, st, 1, w)
+        probe[w] = tpi
+    best = min(probe, key=probe.get)
+    s = _copy_ref_state(ref, st)
+    if args.warmup:
+        ref.run(g, ref.RunConfig(max_iterations=args.warmup, workers=best,
+                                 record_every=args.warmup), state=s)
+    t0 = time.perf_counter()
+    _sol, rep = ref.run(g, ref.RunConfig(max_iterations=args.steps, workers=best,
+                                         record_every=args.steps), state=s)
+    dt = time.perf_counter() - t0
     value = E * args.steps / dt
-    sample = f"{WORKLOADS[name]} scaled x{scale}: {E} edges per step"
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": name, **info, "scale": scale},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
-                             "sample": sample},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0},
-            "threads_note": "the reference path is NumPy (elementwise, take, reduceat: one "
-                            "thread); its lane pool (workers > 1) runs 3-8x slower than one "
-                            "lane (GIL and barriers, SURVEY 8(a) a14), so one core is its "
-                            f"fastest configuration on this {os.cpu_count()}-thread host"}
+    k1 = min(args.steps, 3)
+    tpi1, _r1, _s1 = time_reference_run(ref, g, st, k1, best, record_every=1)
+    line = dict(base, value=value, ms_per_step=dt / args.steps * 1e3,
+                config={"workload": name, "desc": WORKLOADS[name], **info, "edges": E,
+                        "scale": scale, "same_config": scale == 1.0,
+                        "build_seconds": round(t_build, 1)},
+                cpu_baseline={"value": value, "unit": UNIT, "cores": best,
+                              "kind": "reference",
+                              "sample": f"fgadmm.engine.run (unmodified reference, "
+                                        f"baseline/_ref) on {E} edges, workers={best}, "
+                                        f"record_every={args.steps}"
+                                        + ("" if scale == 1.0 else
+                                           f"; {scale:g}-scale sample, per-edge rate "
+                                           f"extrapolated")},
+                e2e={"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                     "d2h_bytes_per_step": 0},
+                reference={"phase_seconds_per_iter": {k: v / args.steps for k, v in
+                                                      rep.phase_seconds.items()},
+                           "report_total_seconds": rep.total_seconds,
+                           "probe_s_per_iter_by_workers": {str(k): v for k, v in probe.items()},
+                           "workers": best,
+                           "record_every_1": {"iterations": k1, "s_per_iter": tpi1,
+                                              "value": E / tpi1}},
+                host=host_info())
     print(json.dumps(line))
     return 0
 
@@ -519,8 +663,20 @@ def main():
     avg_ms = prof[top][0] / prof[top][1]
     peak, peak_kind = measured_peak()
     achieved = kb.get(base, 0) / (avg_ms / 1e3) / 1e9
-    iter_bytes = sum(kb.get(k.split("#")[0], 0) for k in prof)
-    iter_ms = sum(v[0] for v in prof.values()) / prof[top][1]
+    # a temporally blocked launch covers several iterations
+    its_per_launch = plan.forms()["mpc_block"] if base == "chain_mpc_block" else 1
+    iter_bytes = sum(kb.get(k.split("#")[0], 0) for k in prof) / its_per_launch
+    iter_ms = sum(v[0] for v in prof.values()) / prof[top][1] / its_per_launch
+    fp64 = None
+    if base == "chain_mpc_block":
+        # the dynamics products v = K nv: 2 cols^2 flops per factor per
+        # iteration (halo recomputation not counted)
+        T = info["horizon"]
+        flops = its_per_launch * T * 2 * 36 * 36
+        fp64 = {"flops_per_launch": flops, "TFLOPs": flops / (avg_ms / 1e3) / 1e12,
+                "note": "the blocked chain reads its state once per launch; its "
+                        "per-launch time is set by the fp64 dynamics products and "
+                        "shared-memory traffic, not HBM"}
 
     # ---- end to end through the public API (host state in, host state out) ----
     # three calls, each from the same initial state; the median is reported
@@ -564,6 +720,7 @@ def main():
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(args.workload, base),
                      "alg_bytes": kb.get(base, 0),
+                     "iterations_per_launch": its_per_launch, "fp64": fp64,
                      "iteration": {"alg_bytes": iter_bytes,
                                    "survey_B_alg": survey_alg_bytes(g),
                                    "ms": iter_ms,

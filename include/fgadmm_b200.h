@@ -126,8 +126,12 @@ typedef struct {
     double primal_tol;             /* 0 disables (engine.py:473)          */
     double dual_tol;
     int32_t first_reads_n;         /* 1: first x-phase reads uploaded n   */
-    int32_t timing;                /* 1: per-kernel CUDA-event timing,
-                                      direct launches (no CUDA graph)     */
+    int32_t timing;                /* 1: per-pass CUDA-event timing,
+                                      direct launches (no CUDA graph);
+                                      2: phase profile -- the five phases
+                                      as separate kernels with events
+                                      (engine.py:489-500), times from
+                                      fg_run_phase_ms                     */
     int32_t graph_chunk;           /* iterations per CUDA-graph launch    */
     int32_t reserved;
 } fg_run_config;
@@ -161,8 +165,9 @@ int fg_plan_info(const fg_plan* plan, int64_t* out12);
  * fg_plan_sync_params): out[0] fused SVM chain (0 off, 1 generic, 2 fast,
  * 3 unit-weight), out[1] collision tiles in unit-weight form, out[2..5]
  * class-L rows of dim 1..4 in unit-weight form, out[6] mpc_dyn matrix
- * form, out[7] giant top/reduce fused. */
-int fg_plan_forms(const fg_plan* plan, int32_t* out8);
+ * form, out[7] giant top/reduce fused, out[8] iterations per launch of the
+ * temporally blocked MPC chain in fixed-budget runs (0: not blocked). */
+int fg_plan_forms(const fg_plan* plan, int32_t* out9);
 int fg_plan_sync_params(fg_plan* plan, const double* edge_rho,
                         const double* edge_alpha, const double* z_weights);
 
@@ -179,6 +184,12 @@ int fg_run(fg_plan* plan, const fg_run_config* cfg, double* history,
            fg_run_result* out);
 int fg_state_download(fg_plan* plan, double* x, double* m, double* z,
                       double* u, double* n);
+/* Per-iteration device milliseconds of the five phases (x, m, z, u, n) of
+ * the last fg_run with timing == 2 (RunReport.phase_seconds and the
+ * history rows, engine.py:489-514): out[5*i + k] for iteration i < *count,
+ * *count = min(max_iterations, iterations executed); 0 after other runs. */
+int fg_run_phase_ms(const fg_plan* plan, int64_t max_iterations, double* out,
+                    int64_t* count);
 /* First non-finite entry (reference edge order) of the payload arrays the
  * last fg_state_download wrote: out4[0..3] for x, m, u, n, -1 when all
  * finite or not downloaded.  Replaces the host scan behind the reference's

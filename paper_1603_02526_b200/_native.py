@@ -71,6 +71,7 @@ EXPORTS = {
     "fg_run": (C.c_int, [_p, C.POINTER(RunConfig), _dp, C.POINTER(RunResult)]),
     "fg_state_download": (C.c_int, [_p, _dp, _dp, _dp, _dp, _dp]),
     "fg_state_nonfinite": (C.c_int, [_p, _i64p]),
+    "fg_run_phase_ms": (C.c_int, [_p, C.c_int64, _dp, _i64p]),
     "fg_debug_download": (C.c_int, [_p, C.c_int32, _dp]),
     "fg_profile_kernels": (C.c_int, [_p, C.c_int64, C.c_int32, C.c_char_p, _dp, _i64p,
                                      _i32p]),

@@ -8,9 +8,10 @@ Same instances, flags, exit codes and CSV schema as ``fgadmm bench``
 (reference cli.py:279-312, header :33-34): one row per (size, workers)
 cell with the mean per-phase seconds of an iteration, the run's wall time,
 time per iteration and the speedup against the 1-worker cell.  The phases
-come from the device run in profile mode (RunConfig.profile: per-pass
-CUDA events), attributed as RunReport does (x = edge pass with n fused, z =
-variable pass with m and u fused).  ``workers`` is validated and, as in the
+come from the device run in profile mode (RunConfig.profile: the five
+phases as separate kernels, each bracketed by CUDA events every
+iteration, as the reference's timers bracket them).  ``workers`` is
+validated and, as in the
 engine, does not change the device schedule.
 """
 

@@ -23,6 +23,7 @@
 
 #include "fg_var_fast.cuh"
 #include "fg_mpc.cuh"
+#include "fg_mpc_block.cuh"
 #include "fg_tma.cuh"
 #include "fg_chain.cuh"
 #include "fg_rows.cuh"
@@ -248,6 +249,14 @@ struct fg_plan {
     MpcChainDev mpc{};
     int64_t mpc_tiles = 0;
     size_t mpc_smem = 0;
+    // temporally blocked MPC chain (fg_mpc_block.cuh): kMpcKB iterations per
+    // launch on tiles of mpc_btile nodes; 0 = off
+    int mpc_kb = 0;
+    int32_t mpc_btile = 0;
+    int64_t mpc_bntiles = 0;
+    size_t mpc_bsmem = 0;
+    double* d_bpart = nullptr;         // [kb][ntiles] residual partials
+    int64_t mpc_fault = 0;             // test hook: a block reports a failure at this iteration
     ChainDev chain{};
     int64_t chain_grid = 0;
     int chain_minb = 2;                // CTAs/SM the kernel is compiled for (A/B)
@@ -300,6 +309,8 @@ struct fg_plan {
     unsigned* d_gcnt = nullptr;        // per giant component chunk counter
     unsigned* d_ucnt = nullptr;        // giant update CTA counter
     FusedReduce fr_next{nullptr, 0, 0, 0, nullptr};   // set by chain_rest
+    double* d_m = nullptr;             // m of the phase-profile mode (P doubles, lazily)
+    std::vector<double> phase_ms;      // [iterations x 5] x..n ms of the last profile run
     int64_t launches_per_iter = 0;     // iteration 1 of a run
     int64_t launches_later = 0;        // iterations 2.. (fused chain when on)
 
@@ -330,7 +341,7 @@ fg_plan::~fg_plan() {
                     d_lexc[4], d_row2[1], d_row2[2], d_row2[3], d_row2[4],
                     d_planoff[1], d_planoff[2], d_planoff[3], d_planoff[4], d_plans,
                     d_rowdesc[1], d_rowdesc[2], d_rowdesc[3], d_rowdesc[4],
-                    d_cutg, d_send, d_recv};
+                    d_cutg, d_send, d_recv, d_m, d_bpart};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto& g : groups)
@@ -696,6 +707,12 @@ int64_t count_edge_launches(const fg_plan* p) {
     return n;
 }
 
+int64_t count_phasez_launches(const fg_plan* p) {
+    int64_t n = 0;
+    for (int w = 0; w < kVarSlots; ++w) n += var_slot_blocks(p, w) > 0;
+    return n;
+}
+
 int64_t count_var_launches(const fg_plan* p) {
     int64_t n = 0;
     for (int w = 0; w < kVarSlots; ++w) n += var_slot_blocks(p, w) > 0 && fused_slot(p, w);
@@ -812,6 +829,20 @@ void chain_pass(fg_plan* p, int in, cudaStream_t st) {
     } else {
         k_svm_chain<2><<<G + 1, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0, 0, p->chain.n, 1);
     }
+}
+
+// kMpcKB iterations of the MPC chain in one launch, reading slot `in` and
+// writing slot 1 - in (kMpcKB is odd), then their history rows
+void launch_mpc_block(fg_plan* p, int in, int kb, cudaStream_t st) {
+    PassB b{p->vt(), p->d_x, p->d_u[in], p->d_u[1 - in], nullptr, p->d_zb[1 - in],
+            p->d_zb[in], p->d_rho, p->d_alpha, p->d_zw, p->d_ctrl, p->d_part, p->d_zvar};
+    if (kb == kMpcKB)
+        k_mpc_block<kMpcKB, 20, 16><<<(unsigned)p->mpc_bntiles, kMbThreads, p->mpc_bsmem, st>>>(
+            b, p->mpc, p->mpc_btile, p->d_bpart, p->mpc_bntiles, p->mpc_fault);
+    else
+        k_mpc_block<kMpcKBTail, 20, 16><<<(unsigned)p->mpc_bntiles, kMbThreads, p->mpc_bsmem, st>>>(
+            b, p->mpc, p->mpc_btile, p->d_bpart, p->mpc_bntiles, p->mpc_fault);
+    k_mpc_block_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_bpart, p->mpc_bntiles, kb, p->d_hist);
 }
 
 // residual reduction of one iteration: a chain iteration leaves the small
@@ -1085,6 +1116,37 @@ void detect_mpc_chain(fg_plan* p, const std::vector<int32_t>& dim,
                              kMaxDynSmem) != cudaSuccess)
         return;
     p->mpc_ok = true;
+    // temporal blocking for the compiled 16/4 sizes (FGADMM_MPC_BLOCK=0: off)
+    const char* eb = getenv("FGADMM_MPC_BLOCK");
+    if (n0 == 20 && d == 16 && !(eb && eb[0] == '0')) {
+        const size_t sm = mpc_block_smem(n0, d);
+        int occ = 0, sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+        if (cudaFuncSetAttribute(k_mpc_block<kMpcKB, 20, 16>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) == cudaSuccess &&
+            cudaFuncSetAttribute(k_mpc_block<kMpcKBTail, 20, 16>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) == cudaSuccess &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mpc_block<kMpcKB, 20, 16>,
+                                                          kMbThreads, sm) == cudaSuccess &&
+            occ > 0) {
+            // whole waves: the fewest waves at the largest tile, then the
+            // tile that fills them evenly
+            const int64_t nodes = T + 1, resident = (int64_t)occ * sms;
+            const int64_t tmax = kMbNN - 2 * kMpcKB;
+            const int64_t waves = (nodes + tmax * resident - 1) / (tmax * resident);
+            const int64_t tile = (nodes + waves * resident - 1) / (waves * resident);
+            const int64_t nt = (nodes + tile - 1) / tile;
+            if (dalloc(&p->d_bpart, 2 * kMpcKB * nt) == 0) {
+                p->mpc_kb = kMpcKB;
+                p->mpc_btile = (int32_t)tile;
+                p->mpc_bntiles = nt;
+                p->mpc_bsmem = sm;
+                const char* ef = getenv("FGADMM_MPC_BLOCK_FAULT");
+                p->mpc_fault = ef ? atoll(ef) : 0;
+            }
+        }
+        cudaGetLastError();
+    }
 }
 
 int check_launch() {
@@ -1896,6 +1958,7 @@ int fg_plan_forms(const fg_plan* p, int32_t* o) {
     }
     for (int d = 1; d <= 4; ++d) o[1 + d] = p->lunit[d] ? 1 : 0;
     o[7] = p->giant_fused ? 1 : 0;
+    o[8] = p->mpc_chain ? p->mpc_kb : 0;
     return 0;
 }
 
@@ -2146,6 +2209,21 @@ static bool spec_resources(fg_plan* p) {
               cudaStreamCreateWithFlags(&p->stream_copy, cudaStreamNonBlocking) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();                          // not sticky: allocation failures
+        // release what was made: the fallback must not keep the large
+        // staging buffer it exists to avoid
+        if (p->d_stage2) cudaFree(p->d_stage2);
+        if (p->d_chk) cudaFree(p->d_chk);
+        if (p->h_chk) cudaFreeHost(p->h_chk);
+        for (cudaEvent_t* e : {&p->ev_up, &p->ev_up2, &p->ev_chk}) {
+            if (*e) cudaEventDestroy(*e);
+            *e = nullptr;
+        }
+        if (p->stream_copy) cudaStreamDestroy(p->stream_copy);
+        p->d_stage2 = nullptr;
+        p->d_chk = nullptr;
+        p->h_chk = nullptr;
+        p->stream_copy = nullptr;
+        cudaGetLastError();
         p->spec_unavailable = true;
     }
     return ok;
@@ -2228,9 +2306,161 @@ int fg_state_upload(fg_plan* p, const double* z, const double* u, const double* 
     return check_launch();
 }
 
+// ---- phase-profile run (fg_run_config.timing == 2) ---------------------------
+// The reference's run loop with its five phases timed separately
+// (engine.py:483-516, timers :489-500): per iteration five launches -- x
+// (edge pass reading n), m, z (pairwise reduceat), u, n -- each bracketed
+// by CUDA events and checked for non-finite values on the device, then the
+// residual reduction, history row and tolerance stop.  Same arithmetic as
+// update_x .. update_n, so the state is bitwise the fused run's; the
+// ping-pong slots are used as the fused run uses them, so download and the
+// error path need no special case.  Per-iteration phase times:
+// fg_run_phase_ms.
+static int run_profile(fg_plan* p, const fg_run_config* cfg, double* history,
+                       fg_run_result* out) {
+    if (p->partitioned())
+        return fail(FG_ERR_INVALID, "the phase profile runs on whole-graph plans");
+    cudaStream_t st = p->stream;
+    const int64_t K = cfg->max_iterations;
+    if (int rc = settle_idle(p)) return rc;
+    if (p->hist_cap < K) {
+        if (p->d_hist) cudaFree(p->d_hist);
+        p->d_hist = nullptr;
+        if (int rc = dalloc(&p->d_hist, 2 * K)) return rc;
+        p->hist_cap = K;
+    }
+    if (!p->d_m) { if (int rc = dalloc(&p->d_m, std::max<int64_t>(1, p->P))) return rc; }
+    if (!p->d_aux) { if (int rc = dalloc(&p->d_aux, std::max<int64_t>(1, p->P))) return rc; }
+    const bool first_n = cfg->first_reads_n && p->n_valid && p->completed == 0;
+    if (int rc = rebase_slots(p)) return rc;
+    p->n_valid = 0;
+    p->x_stale = 0;
+    Ctrl h{};
+    h.err_key = ~0ull;
+    h.iter = 1;
+    h.primal_tol = cfg->primal_tol;
+    h.dual_tol = cfg->dual_tol;
+    h.scale = 1.0 / std::sqrt((double)p->P);
+    h.max_iter = K;
+    CK(cudaMemcpyAsync(p->d_ctrl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+    // n of the first x phase: the uploaded n, else z[zmap] - u
+    if (first_n)
+        CK(cudaMemcpyAsync(p->d_aux, p->d_u[1], p->P * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    else
+        k_phase_n<<<nblk(p->P, 256), 256, 0, st>>>(p->P, p->d_vmz, p->d_zb[0], p->d_u[0], p->d_aux);
+    const bool poll = cfg->primal_tol > 0.0 || cfg->dual_tol > 0.0;
+    constexpr int kRing = 128;                     // iterations of events in flight
+    constexpr int kEv = 8;
+    // events: x | m | z | (z check) | u | n | (residuals); phase k is
+    // [t0[k], t1[k]] below
+    constexpr int t0[5] = {0, 1, 2, 4, 5}, t1[5] = {1, 2, 3, 5, 6};
+    std::vector<cudaEvent_t> ev(kRing * kEv);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    cudaEvent_t ev0, ev1;
+    CK(cudaEventCreate(&ev0));
+    CK(cudaEventCreate(&ev1));
+    p->phase_ms.assign(5 * K, 0.0);
+    std::vector<double> res_ms(K, 0.0);
+    int64_t launches = 0, harvested = 0, issued = 0;
+    auto harvest = [&](int64_t upto) -> int {
+        for (; harvested < upto; ++harvested) {
+            cudaEvent_t* E = &ev[(harvested % kRing) * kEv];
+            CK(cudaEventSynchronize(E[kEv - 1]));
+            for (int k = 0; k < 5; ++k) {
+                float ms = 0;
+                cudaEventElapsedTime(&ms, E[t0[k]], E[t1[k]]);
+                p->phase_ms[5 * harvested + k] = ms;
+            }
+            float r = 0;
+            cudaEventElapsedTime(&r, E[6], E[7]);
+            res_ms[harvested] = r;
+        }
+        return 0;
+    };
+    const unsigned nbE = nblk(p->E, 256), nbP = nblk(p->P, 256);
+    CK(cudaEventRecord(ev0, st));
+    for (int64_t j = 1; j <= K; ++j) {
+        if (issued - harvested >= kRing) { if (int rc = harvest(issued - kRing + 1)) return rc; }
+        const int in = (int)((j - 1) & 1), o = 1 - in;
+        cudaEvent_t* E = &ev[((j - 1) % kRing) * kEv];
+        CK(cudaEventRecord(E[0], st));
+        edge_pass(p, true, p->d_zb[in], p->d_u[in], p->d_aux, st);                 // x
+        CK(cudaEventRecord(E[1], st));
+        k_prof_m<<<nbP, 256, 0, st>>>(p->P, p->d_x, p->d_u[in], p->d_m, p->d_ctrl);  // m
+        CK(cudaEventRecord(E[2], st));
+        var_pass<MODE_PHASEZ>(p, p->d_zb[in], p->d_zb[o], nullptr, nullptr, p->d_m, st);  // z
+        CK(cudaEventRecord(E[3], st));
+        k_prof_check_z<<<nblk(p->Z, 256), 256, 0, st>>>(p->Z, p->d_zb[o], p->d_ctrl);
+        CK(cudaEventRecord(E[4], st));
+        k_prof_u<<<nbE, 256, 0, st>>>(p->E, p->vt(), p->d_vmvar, p->d_x, p->d_zb[o],
+                                      p->d_alpha, p->d_u[in], p->d_u[o], p->d_ctrl);  // u
+        CK(cudaEventRecord(E[5], st));
+        k_prof_n<<<nbP, 256, 0, st>>>(p->P, p->d_vmz, p->d_zb[o], p->d_u[o], p->d_aux,
+                                      p->d_ctrl);                                    // n
+        CK(cudaEventRecord(E[6], st));
+        k_residual_parts<<<nbE, 256, 0, st>>>(p->E, p->vt(), p->d_vmvar, p->d_x, p->d_zb[o],
+                                              p->d_zb[in], p->d_rho, p->d_part);
+        k_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, nbE, p->d_hist);
+        CK(cudaEventRecord(E[7], st));
+        ++issued;
+        launches += count_edge_launches(p) + count_phasez_launches(p) + 6;
+        if (poll || j == K) {
+            Ctrl c{};
+            CK(cudaMemcpyAsync(&c, p->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            if (c.stop) break;
+        }
+    }
+    CK(cudaEventRecord(ev1, st));
+    CK(cudaStreamSynchronize(st));
+    if (int rc = harvest(issued)) return rc;
+    float tot = 0;
+    cudaEventElapsedTime(&tot, ev0, ev1);
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    if (int rc = check_launch()) return rc;
+    CK(cudaMemcpy(&h, p->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+    p->completed = h.completed;
+    p->phase_ms.resize(5 * std::max<int64_t>(0, issued));
+    double ms_x = 0, ms_v = 0, ms_r = 0;
+    for (int64_t j = 0; j < issued; ++j) {
+        ms_x += p->phase_ms[5 * j];
+        for (int k = 1; k < 5; ++k) ms_v += p->phase_ms[5 * j + k];
+        ms_r += res_ms[j];
+    }
+    out->iterations = h.completed;
+    out->converged = h.converged;
+    out->primal = h.primal;
+    out->dual = h.dual;
+    out->error_phase = -1;
+    out->error_iteration = 0;
+    if (h.err_key != ~0ull) {
+        out->error_phase = (int32_t)(h.err_key & 7ull);
+        out->error_iteration = (int64_t)(h.err_key >> 3);
+    }
+    out->ms_total = tot;
+    out->ms_edge_pass = ms_x;
+    out->ms_var_pass = ms_v;
+    out->ms_reduce = ms_r;
+    out->launches = launches;
+    if (history && h.completed > 0)
+        CK(cudaMemcpy(history, p->d_hist, 2 * h.completed * sizeof(double), cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+int fg_run_phase_ms(const fg_plan* p, int64_t max_iterations, double* out, int64_t* count) {
+    const int64_t n = std::min<int64_t>(max_iterations, (int64_t)p->phase_ms.size() / 5);
+    if (out && n > 0) std::memcpy(out, p->phase_ms.data(), 5 * n * sizeof(double));
+    if (count) *count = n;
+    return 0;
+}
+
 int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result* out) {
     CK(cudaSetDevice(p->device));
     if (cfg->max_iterations < 1) return fail(FG_ERR_INVALID, "max_iterations must be >= 1");
+    if (cfg->timing == 2) return run_profile(p, cfg, history, out);
+    p->phase_ms.clear();
     cudaStream_t st = p->stream;
     const int64_t K = cfg->max_iterations;
     if (p->hist_cap < K) {
@@ -2353,6 +2583,28 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
         int inflight = 0, slot = 0;
         bool stopped = false;
         const bool poll = cfg->primal_tol > 0.0 || cfg->dual_tol > 0.0;
+        if (p->mpc_chain && p->mpc_kb > 0 && !poll && !p->nccl_comm) {
+            // fixed budget on the MPC chain: blocks of kMpcKB iterations,
+            // the last iteration on the per-iteration kernel (its inputs
+            // stay in memory for the x recomputation at download)
+            int64_t j = 2;
+            while (left - 1 >= p->mpc_kb) {
+                launch_mpc_block(p, (int)((j - 1) & 1), kMpcKB, st);
+                launches += 2;
+                left -= p->mpc_kb;
+                j += p->mpc_kb;
+            }
+            if (left - 1 >= kMpcKBTail) {            // a shorter block for the tail
+                launch_mpc_block(p, (int)((j - 1) & 1), kMpcKBTail, st);
+                launches += 2;
+                left -= kMpcKBTail;
+                j += kMpcKBTail;
+            }
+            for (; left > 0; --left, ++j) {
+                launch_iteration(p, (int)((j - 1) & 1), false, st);
+                launches += p->launches_later;
+            }
+        }
         while (left > 0 && !stopped) {
             int n;
             cudaGraphExec_t gx = nullptr;
@@ -2417,6 +2669,24 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
         }
     }
     CK(cudaMemcpy(&h, p->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+    if (h.blk_err) {
+        // a temporally blocked launch met a non-finite value: it stopped the
+        // run without writing, so its input slot is intact -- replay from
+        // there one iteration at a time (the reference's exact failure)
+        const int64_t j0 = h.blk_err;
+        h.stop = 0;
+        h.blk_err = 0;
+        h.iter = j0;
+        h.completed = j0 - 1;
+        CK(cudaMemcpyAsync(p->d_ctrl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+        for (int64_t j = j0; j <= K; ++j) {
+            launch_iteration(p, (int)((j - 1) & 1), false, st);
+            launches += p->launches_later;
+        }
+        CK(cudaStreamSynchronize(st));
+        if (int rc = check_launch()) return rc;
+        CK(cudaMemcpy(&h, p->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+    }
     p->completed = h.completed;
     // x of the last (or failing) iteration stays in registers when the
     // chain kernel ran it; fg_state_download / fg_debug_download recompute it
@@ -2637,6 +2907,56 @@ int fg_profile_kernels(fg_plan* p, int64_t iterations, int32_t max_slots,
         ~Restore() { p->mpc_reduce_fused = v; }
     } restore{p, p->mpc_reduce_fused};
     p->mpc_reduce_fused = false;
+    if (chain && p->mpc_chain && p->mpc_kb > 0) {
+        // temporally blocked MPC chain: iteration 1 untimed, then blocks of
+        // kMpcKB iterations timed per launch (block kernel, its reduction);
+        // the tail iterations run untimed
+        const int kb = p->mpc_kb;
+        const int64_t nb = (iterations - 2) / kb;
+        if (nb < 1) return fail(FG_ERR_INVALID, "profile of the blocked MPC chain needs "
+                                                "at least kMpcKB + 2 iterations");
+        if (max_slots < 2) return fail(FG_ERR_INVALID, "too many kernels for the output arrays");
+        std::vector<cudaEvent_t> ev(3 * nb);
+        for (auto& e : ev) CK(cudaEventCreate(&e));
+        launch_iteration(p, 0, first_n, st);
+        int64_t j = 2;
+        for (int64_t i = 0; i < nb; ++i, j += kb) {
+            const int in = (int)((j - 1) & 1);
+            PassB b{p->vt(), p->d_x, p->d_u[in], p->d_u[1 - in], nullptr, p->d_zb[1 - in],
+                    p->d_zb[in], p->d_rho, p->d_alpha, p->d_zw, p->d_ctrl, p->d_part, p->d_zvar};
+            CK(cudaEventRecord(ev[3 * i], st));
+            k_mpc_block<kMpcKB, 20, 16><<<(unsigned)p->mpc_bntiles, kMbThreads, p->mpc_bsmem, st>>>(
+                b, p->mpc, p->mpc_btile, p->d_bpart, p->mpc_bntiles);
+            CK(cudaEventRecord(ev[3 * i + 1], st));
+            k_mpc_block_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_bpart, p->mpc_bntiles, kb,
+                                                   p->d_hist);
+            CK(cudaEventRecord(ev[3 * i + 2], st));
+        }
+        for (; j <= iterations; ++j) launch_iteration(p, (int)((j - 1) & 1), false, st);
+        CK(cudaStreamSynchronize(st));
+        if (int rc = check_launch()) return rc;
+        ms[0] = ms[1] = 0.0;
+        for (int64_t i = 0; i < nb; ++i) {
+            float t = 0;
+            cudaEventElapsedTime(&t, ev[3 * i], ev[3 * i + 1]);
+            ms[0] += t;
+            cudaEventElapsedTime(&t, ev[3 * i + 1], ev[3 * i + 2]);
+            ms[1] += t;
+        }
+        counts[0] = counts[1] = nb;
+        for (auto& e : ev) cudaEventDestroy(e);
+        const char* nm[2] = {"chain_mpc_block", "reduce_block"};
+        for (int i = 0; i < 2; ++i) {
+            std::memset(labels + 32 * i, 0, 32);
+            std::strncpy(labels + 32 * i, nm[i], 31);
+        }
+        *nslots = 2;
+        Ctrl hc;
+        CK(cudaMemcpy(&hc, p->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+        p->completed = hc.completed;
+        p->x_stale = 0;
+        return 0;
+    }
     std::vector<std::string> names;
     std::vector<int> vk;
     if (chain) {
@@ -2917,7 +3237,10 @@ int fg_group_run(fg_plan** plans, int32_t G, const fg_run_config* cfg, double* h
     const int64_t K = cfg->max_iterations;
     if (K < 1) return fail(FG_ERR_INVALID, "max_iterations must be >= 1");
     const int64_t ncut = p0->ncut;
-    bool first_n = cfg->first_reads_n != 0;
+    // whether iteration 1 reads the uploaded n is decided per plan: a plan
+    // whose uploaded n equals z - u (n_valid 0) may run its chain form while
+    // another plan reads its own n
+    std::vector<char> first_r(G, 0);
     for (int r = 0; r < G; ++r) {
         fg_plan* p = plans[r];
         if (p->device != p0->device || p->ncut != ncut)
@@ -2926,7 +3249,7 @@ int fg_group_run(fg_plan** plans, int32_t G, const fg_run_config* cfg, double* h
         p->rank = r;
         if (int rc = settle_idle(p)) return rc;
         if (int rc = rebase_slots(p)) return rc;
-        if (!p->n_valid) first_n = false;
+        first_r[r] = cfg->first_reads_n && p->n_valid;
         p->n_valid = 0;
         if (p->d_recv) cudaFree(p->d_recv);
         p->d_recv = nullptr;
@@ -2968,10 +3291,9 @@ int fg_group_run(fg_plan** plans, int32_t G, const fg_run_config* cfg, double* h
     };
     for (int64_t j = 1; j <= K; ++j) {
         const int in = (int)((j - 1) & 1);
-        const bool first = (j == 1) && first_n;
-        for (int r = 0; r < G; ++r) part_pre(plans[r], in, first, st);
+        for (int r = 0; r < G; ++r) part_pre(plans[r], in, j == 1 && first_r[r], st);
         if (ncut) { if (int rc = gather(0, (size_t)ncut, 0)) return rc; }
-        for (int r = 0; r < G; ++r) part_mid(plans[r], in, first, st);
+        for (int r = 0; r < G; ++r) part_mid(plans[r], in, j == 1 && first_r[r], st);
         if (int rc = gather((size_t)ncut, 4, (size_t)G * ncut)) return rc;
         for (int r = 0; r < G; ++r) part_post(plans[r], st);
         for (int r = 0; r < G; ++r) launches += plans[r]->launches_per_iter + 1;
@@ -2997,7 +3319,7 @@ int fg_group_run(fg_plan** plans, int32_t G, const fg_run_config* cfg, double* h
         plans[r]->x_stale = 0;
         if (plans[r]->chain_on) {
             const int64_t need = h.err_key != ~0ull ? (int64_t)(h.err_key >> 3) : h.completed;
-            if (need >= (first_n ? 2 : 1)) plans[r]->x_stale = need;
+            if (need >= (first_r[r] ? 2 : 1)) plans[r]->x_stale = need;
         }
     }
     CK(cudaMemcpy(&h, p0->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));

@@ -692,6 +692,67 @@ __global__ void k_phase_u(int64_t E, VarTab vt, const int32_t* vm_var,
     for (int c = 0; c < d; ++c) u[p0 + c] = u[p0 + c] + (x[p0 + c] - z[z0 + c]) * al;
 }
 
+// ---- phase-profile kernels (RunConfig(profile=True)) -----------------------
+// The five phases as separate launches, as the reference times them
+// (engine.py:489-500), each with its non-finite check (engine.py:333-350)
+// keyed by (iteration, phase) on the device.  Same arithmetic as the
+// per-phase API kernels above; u is written to the other ping-pong slot so
+// the previous u survives (m = x + u_prev at download).
+__global__ void __launch_bounds__(256) k_prof_m(int64_t P, const double* x, const double* u,
+                                                double* m, Ctrl* c) {
+    if (c->stop) return;
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool bad = false;
+    if (p < P) {
+        const double v = x[p] + u[p];          // engine.py:263-265
+        m[p] = v;
+        bad = !finite(v);
+    }
+    if (bad) flag_error(c, c->iter, FG_PHASE_M, true);
+}
+
+// z check of the profile run (the phase-z kernels do not check in
+// MODE_PHASEZ); outside the phase timers, as _check_finite is
+__global__ void __launch_bounds__(256) k_prof_check_z(int64_t Z, const double* z, Ctrl* c) {
+    if (c->stop) return;
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < Z && !finite(z[k])) flag_error(c, c->iter, FG_PHASE_Z, true);
+}
+
+__global__ void __launch_bounds__(256) k_prof_u(int64_t E, VarTab vt, const int32_t* vm_var,
+                                                const double* x, const double* z,
+                                                const double* alpha, const double* uin,
+                                                double* uout, Ctrl* c) {
+    if (c->stop) return;
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= E) return;
+    const int32_t v = vm_var[q];
+    const int d = vt.dim[v];
+    const int64_t p0 = vt.pbase[v] + (q - vt.ebase[v]) * (int64_t)d;
+    const int64_t z0 = vt.zbase[v];
+    const double al = alpha[q];
+    bool bad = false;
+    for (int k = 0; k < d; ++k) {              // engine.py:282-290
+        const double nu = uin[p0 + k] + (x[p0 + k] - z[z0 + k]) * al;
+        uout[p0 + k] = nu;
+        bad |= !finite(nu);
+    }
+    if (bad) flag_error(c, c->iter, FG_PHASE_U, true);
+}
+
+__global__ void __launch_bounds__(256) k_prof_n(int64_t P, const int32_t* vmz, const double* z,
+                                                const double* u, double* n, Ctrl* c) {
+    if (c->stop) return;
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool bad = false;
+    if (p < P) {
+        const double v = z[vmz[p]] - u[p];     // engine.py:292-298
+        n[p] = v;
+        bad = !finite(v);
+    }
+    if (bad) flag_error(c, c->iter, FG_PHASE_N, true);
+}
+
 // residuals (engine.py:398-406) on an explicit z_prev; per-block partials
 __global__ void __launch_bounds__(256) k_residual_parts(
     int64_t E, VarTab vt, const int32_t* vm_var, const double* x,

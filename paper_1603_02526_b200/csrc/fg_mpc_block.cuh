@@ -1,0 +1,240 @@
+// Temporally blocked MPC chain: KB iterations of build_mpc's graph per
+// launch (problems.py:200-215; the per-iteration kernel is k_mpc_chain in
+// fg_mpc.cuh).
+//
+// The graph is a chain: one iteration of node t reads only nodes t-1, t,
+// t+1 (the dynamics factors t-1 and t).  A CTA owning nodes [t0, t1) loads
+// the state (z and the three u slots) of [t0-KB, t1+KB) into shared memory
+// once, runs KB iterations there -- the halo shrinks by one node per side
+// per iteration, so after KB iterations [t0, t1) is exact -- and writes
+// its own nodes back.  HBM traffic per iteration drops KB-fold; the halo
+// (2 KB nodes) is recomputed with identical arithmetic by both tiles.
+//
+// Every operation is k_mpc_chain's, in the same order (cost prox, the
+// matrix-form dynamics v = K nv as the same fma chain, init, m, z in
+// NumPy's reduceat order, u), so the state is bitwise the per-iteration
+// chain's and therefore the per-kind path's.  Residual partials of the
+// owned nodes are written per iteration (k_mpc_block_reduce turns them
+// into the history rows).  Any non-finite value of an owned node stops the
+// run and records the block (Ctrl::blk_err); the host then replays that
+// block iteration by iteration with the ordinary kernels, which raise the
+// reference's exact (iteration, phase) error.  Used without tolerances
+// only (fixed iteration budgets): a tolerance stop must see every
+// iteration's residuals before the next one runs.
+#pragma once
+
+#include "fg_mpc.cuh"
+#include "fg_edge.cuh"
+
+namespace fg {
+
+constexpr int kMpcKB = 5;                              // iterations per launch (odd)
+constexpr int kMpcKBTail = 3;                          // shorter block for a run's tail
+constexpr int kMbF = 64;                               // factor slots (gemm lanes)
+constexpr int kMbThreads = kEdgeThreads;               // 256
+constexpr int kMbRG = kMbThreads / kMbF;               // 4 row groups
+constexpr int kMbKH = (kDynGemmMaxCols + kMbRG - 1) / kMbRG;
+constexpr int kMbNN = kMbF + 1;                        // nodes staged per CTA (tile + 2 KB)
+
+inline size_t mpc_block_smem(int n0, int d) {
+    const size_t cols = (size_t)(n0 + d);
+    return (cols * kMbRG * kMbKH + (size_t)kMbNN * 5 * n0 +
+            (size_t)kMbF * (cols + 1) + (size_t)kMbF * (2 * n0 + 1)) * sizeof(double);
+}
+
+template <int KB, int N0, int DD>
+__global__ void __launch_bounds__(kMbThreads, 2) k_mpc_block(PassB b, MpcChainDev c,
+                                                             int32_t tile, double* bpart,
+                                                             int64_t ntiles,
+                                                             int64_t fault_it = 0) {
+    static_assert(KB % 2 == 1, "a block must flip the ping-pong slot");
+    extern __shared__ double gsm[];
+    __shared__ double sm[2 * (kMbThreads / 32)];
+    if (b.ctrl->stop) return;
+    constexpr int n0 = N0, d = DD, cols = N0 + DD, ld = cols + 1, ldo = 2 * N0 + 1;
+    constexpr int KH = kMbKH, RG = kMbRG;
+    double* Ks = gsm;                                   // [c][r0][k], row r = r0 + RG k
+    double* zs = Ks + cols * RG * KH;                   // [NN][n0]
+    double* us = zs + kMbNN * n0;                       // [NN][3][n0]
+    double* nvs = us + kMbNN * 3 * n0;                  // [F][ld]
+    double* outs = nvs + kMbF * ld;                     // [F][ldo]
+    double* cs = outs + kMbF * ldo;                     // [NN][n0] cost diagonals
+    const int T = c.T;
+    const int t0 = blockIdx.x * tile;
+    const int t1 = min(T + 1, t0 + tile);               // owned nodes [t0, t1)
+    const int a = max(0, t0 - KB);
+    const int bnd = min(T + 1, t1 + KB);                // staged nodes [a, bnd)
+    const int NN = bnd - a;
+    const int nf = NN - 1;                              // factors [a, bnd - 1)
+    // ---- stage K, the state of [a, bnd) and its cost diagonals with
+    // asynchronous copies (every load in flight at once): node t's payload
+    // is 3 n0 contiguous doubles at pN + 3 t n0 (node T has two slots), z
+    // n0 at zN + t n0 ----
+    for (int i = threadIdx.x; i < cols * cols; i += blockDim.x) {
+        const int r = i / cols, cc = i - r * cols;
+        cp_async8(&Ks[(cc * RG + r % RG) * KH + r / RG], c.kmat + i);
+    }
+    {
+        const double* __restrict__ uin = b.uin + c.pN + (int64_t)3 * a * n0;
+        const double* __restrict__ zin = b.zin + c.zN + (int64_t)a * n0;
+        const int nu = NN * 3 * n0 - (bnd == T + 1 ? n0 : 0);
+        for (int i = threadIdx.x; i < nu; i += blockDim.x) cp_async8(us + i, uin + i);
+        for (int i = threadIdx.x; i < NN * n0; i += blockDim.x) cp_async8(zs + i, zin + i);
+        for (int i = threadIdx.x; i < NN * n0; i += blockDim.x) {
+            const int tl = i / n0, q = i - tl * n0;
+            cp_async8(cs + i, c.cost_fp + (int64_t)(a + tl) * c.cost_st + q);
+        }
+        if (bnd == T + 1)
+            for (int q = threadIdx.x; q < n0; q += blockDim.x) us[(NN - 1) * 3 * n0 + 2 * n0 + q] = 0.0;
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    const int64_t it0 = b.ctrl->iter;
+    bool bad = false;
+    for (int i = 0; i < KB; ++i) {
+        // ---- n of the dynamics factors (k_mpc_chain's staging) ----
+        for (int idx = threadIdx.x; idx < nf * 2 * n0; idx += blockDim.x) {
+            const int fl = idx / (2 * n0), cc = idx - fl * (2 * n0);
+            const int f = a + fl;
+            const int j = cc < n0 ? 0 : 1, q = cc - j * n0;
+            const int node = fl + j;                    // local index
+            const int rank = j ? 1 : (f == 0 ? 1 : 2);
+            const double n = zs[node * n0 + q] - us[(node * 3 + rank) * n0 + q];
+            const int tg = a + node;
+            bad |= (tg >= t0 && tg < t1) && !finite(n);
+            if (j == 0) nvs[fl * ld + q] = n;
+            else if (q < d) nvs[fl * ld + n0 + q] = n;
+            else outs[fl * ldo + n0 + q] = n;           // control of t+1 passes
+        }
+        __syncthreads();
+        {   // v = K nv: the fma chain of k_mpc_chain / k_mpc_dyn_gemm
+            const int fl = threadIdx.x % kMbF, r0 = threadIdx.x / kMbF;
+            if (fl < nf) {
+                double acc[KH];
+#pragma unroll
+                for (int k = 0; k < KH; ++k) acc[k] = 0.0;
+                const double* nvf = nvs + fl * ld;
+                for (int cc = 0; cc < cols; ++cc) {
+                    const double v = nvf[cc];
+                    const double2* kc = reinterpret_cast<const double2*>(Ks + (cc * RG + r0) * KH);
+#pragma unroll
+                    for (int k2 = 0; k2 < KH / 2; ++k2) {
+                        const double2 kk = kc[k2];
+                        acc[2 * k2] = __fma_rn(kk.x, v, acc[2 * k2]);
+                        acc[2 * k2 + 1] = __fma_rn(kk.y, v, acc[2 * k2 + 1]);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < KH; ++k) {
+                    const int r = r0 + RG * k;
+                    if (r < cols) outs[fl * ldo + r] = acc[k];
+                }
+            }
+        }
+        __syncthreads();
+        // ---- nodes: cost / init proxes, m, z, u (in place) ----
+        double pp = 0.0, dd = 0.0;
+        for (int idx = threadIdx.x; idx < NN * n0; idx += blockDim.x) {
+            const int tl = idx / n0, q = idx - tl * n0;
+            const int t = a + tl;
+            const bool own = t >= t0 && t < t1;
+            const int deg = t == T ? 2 : 3;
+            const double zi = zs[tl * n0 + q];
+            double u[3], x[3];
+            u[0] = us[(tl * 3 + 0) * n0 + q];
+            u[1] = us[(tl * 3 + 1) * n0 + q];
+            u[2] = us[(tl * 3 + 2) * n0 + q];
+            const double n_c = zi - u[0];
+            x[0] = prox_mpc_cost(n_c, 1.0, cs[tl * n0 + q]);
+            bool bn = !finite(n_c);
+            // rank 1: dyn_{t-1} slot 1 (node 0: dyn_0 slot 0); a halo node
+            // without its factor computes a placeholder (never owned)
+            if (t == 0) x[1] = outs[0 * ldo + q];
+            else x[1] = tl >= 1 ? outs[(tl - 1) * ldo + n0 + q] : 0.0;
+            x[2] = 0.0;
+            if (deg == 3) {
+                if (t == 0) {
+                    const double n_i = zi - u[2];
+                    bn |= !finite(n_i);
+                    x[2] = q < d ? c.init_fp[q] : n_i;
+                } else {
+                    x[2] = tl < nf ? outs[tl * ldo + q] : 0.0;
+                }
+            }
+            bool bb = bn || !(finite(x[0]) && finite(x[1]) && (deg == 2 || finite(x[2])));
+            double S = 0.0, res = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < 3; ++kk) {
+                if (kk < deg) {
+                    const double m = x[kk] + u[kk];
+                    bb |= !finite(m);
+                    if (kk == 0) S = m;
+                    else res += m;
+                }
+            }
+            S = S + res;
+            const double zn = ddiv(S, (double)deg);
+            bb |= !finite(zn);
+            zs[tl * n0 + q] = zn;
+            const double dz = zn - zi;
+#pragma unroll
+            for (int kk = 0; kk < 3; ++kk) {
+                if (kk < deg) {
+                    const double tt = x[kk] - zn;
+                    const double un = u[kk] + tt;
+                    us[(tl * 3 + kk) * n0 + q] = un;
+                    bb |= !finite(un);
+                    if (own) {
+                        pp += tt * tt;
+                        dd += dz * dz;
+                    }
+                }
+            }
+            bad |= own && bb;
+        }
+        block_sum2<kMbThreads>(pp, dd, sm);             // (its barriers also
+        if (threadIdx.x == 0) {                         //  order the next staging)
+            bpart[2 * ((int64_t)i * ntiles + blockIdx.x)] = pp;
+            bpart[2 * ((int64_t)i * ntiles + blockIdx.x) + 1] = dd;
+        }
+        __syncthreads();
+    }
+    // fault injection for the replay test (FGADMM_MPC_BLOCK_FAULT=<iteration>)
+    bad |= fault_it >= it0 && fault_it < it0 + KB;
+    if (__syncthreads_or(bad)) {
+        if (threadIdx.x == 0) {
+            b.ctrl->blk_err = it0;
+            b.ctrl->stop = 1;
+        }
+        return;
+    }
+    // ---- owned nodes back to the output slot ----
+    {
+        const int lo = t0 - a, nown = t1 - t0;
+        double* __restrict__ uout = b.uout + c.pN + (int64_t)3 * t0 * n0;
+        double* __restrict__ zout = b.z + c.zN + (int64_t)t0 * n0;
+        const int nu = nown * 3 * n0 - (t1 == T + 1 ? n0 : 0);
+        for (int i = threadIdx.x; i < nu; i += blockDim.x) uout[i] = us[lo * 3 * n0 + i];
+        for (int i = threadIdx.x; i < nown * n0; i += blockDim.x) zout[i] = zs[lo * n0 + i];
+    }
+}
+
+// History rows, iteration counter and completion of a block's KB
+// iterations (reduce_body per iteration over the tiles' partials, fixed
+// order).  Skipped when the block stopped the run.
+__global__ void __launch_bounds__(1024) k_mpc_block_reduce(Ctrl* c, const double* bpart,
+                                                           int64_t ntiles, int32_t kb,
+                                                           double* hist) {
+    __shared__ double sm[64];
+    __shared__ int s_stop;
+    if (threadIdx.x == 0) s_stop = c->stop;
+    __syncthreads();
+    if (s_stop) return;
+    for (int i = 0; i < kb; ++i) {
+        reduce_body<1024>(c, bpart + 2 * (int64_t)i * ntiles, ntiles, hist, 0, 0, sm);
+        __syncthreads();
+    }
+}
+
+}  // namespace fg

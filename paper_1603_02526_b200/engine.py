@@ -22,7 +22,8 @@ engine (``fgadmm/engine.py``); the iteration itself runs in
 
 ``RunConfig.workers`` is accepted and validated but has no effect (one
 GPU executes the whole graph).  Two optional fields extend the config:
-``profile`` (per-kernel CUDA-event timing with direct launches) and
+``profile`` (the five phases as separate kernels, each timed with CUDA
+events every iteration, as the reference times them) and
 ``graph_chunk`` (iterations per CUDA-graph launch).
 """
 
@@ -307,13 +308,22 @@ class DevicePlan:
         cfg.primal_tol = float(primal_tol)
         cfg.dual_tol = float(dual_tol)
         cfg.first_reads_n = 1 if first_reads_n else 0
-        cfg.timing = 1 if timing else 0
+        cfg.timing = int(timing)
         cfg.graph_chunk = int(graph_chunk)
         res = _native.RunResult()
         hist = np.zeros(2 * int(iterations))
         _native.check(self._lib.fg_run(self._h, C.byref(cfg), _native.dptr(hist),
                                        C.byref(res)))
         return res, hist.reshape(-1, 2)[:res.iterations]
+
+    def phase_ms(self, iterations):
+        """(iterations, 5) device ms of phases x..n per iteration of the
+        last profile run (``fg_run_phase_ms``)."""
+        out = np.zeros((max(1, int(iterations)), 5))
+        cnt = np.zeros(1, dtype=np.int64)
+        _native.check(self._lib.fg_run_phase_ms(self._h, int(iterations), _native.dptr(out),
+                                                _native.i64ptr(cnt)))
+        return out[:int(cnt[0])]
 
     def download(self, x=None, m=None, z=None, u=None, n=None):
         outs = [x, m, z, u, n]
@@ -362,12 +372,13 @@ class DevicePlan:
         """Kernel forms of the next run (fg_plan_forms): chain form,
         unit-weight collision tiles / class-L rows per dim, mpc_dyn matrix
         form, fused giant kernels."""
-        o = (C.c_int32 * 8)()
+        o = (C.c_int32 * 9)()
         self._lib.fg_plan_forms(self._h, o)
         return {"chain": ("off", "generic", "fast", "unit", "mpc")[o[0]],
                 "collision_unit": bool(o[1]),
                 "rows_unit": {d: bool(o[1 + d]) for d in (1, 2, 3, 4)},
-                "mpc_dyn_matrix": bool(o[6]), "giant_fused": bool(o[7])}
+                "mpc_dyn_matrix": bool(o[6]), "giant_fused": bool(o[7]),
+                "mpc_block": int(o[8])}
 
     def chain_form(self):
         """Form of the fused SVM-chain kernel the next run uses: 'off',
@@ -566,8 +577,9 @@ def _raise_device_error(graph, plan, state, res):
 class Solution(Sequence):
     """The consensus vector unpacked per variable (reference
     ``engine.py:521-522`` returns a list of per-variable copies).  Items
-    are made on access from a private copy of z, so building the result
-    is one copy even for millions of variables."""
+    are made on access (each a fresh copy, as the reference's) from a
+    private copy of z, so building the result is one copy even for
+    millions of variables; ``tolist()`` gives the reference's list."""
 
     def __init__(self, z, var_offsets, copy=True):
         self._z = np.array(z, dtype=np.float64, copy=True) if copy else z
@@ -585,12 +597,29 @@ class Solution(Sequence):
             i += n
         if not 0 <= i < n:
             raise IndexError(i)
-        return self._z[int(self._off[i]):int(self._off[i + 1])]
+        # a copy per item, as the reference's list of per-variable copies
+        return self._z[int(self._off[i]):int(self._off[i + 1])].copy()
 
     def __iter__(self):
         z, off = self._z, self._off
         for i in range(len(off) - 1):
-            yield z[int(off[i]):int(off[i + 1])]
+            yield z[int(off[i]):int(off[i + 1])].copy()
+
+    def __eq__(self, other):
+        if isinstance(other, (Solution, list, tuple)):
+            return len(self) == len(other) and all(
+                np.array_equal(a, b) for a, b in zip(self, other))
+        return NotImplemented
+
+    def __add__(self, other):
+        return list(self) + list(other)
+
+    def __radd__(self, other):
+        return list(other) + list(self)
+
+    def tolist(self):
+        """The reference's return type: a list of per-variable copies."""
+        return list(self)
 
     def concatenated(self):
         """All variables back to back (== np.concatenate(self))."""
@@ -615,7 +644,8 @@ def run(graph, config, state=None):
     plan.sync(graph)
     plan.upload(state.z, state.u, state.n)
     res, hist = plan.run(config.max_iterations, config.primal_tol, config.dual_tol,
-                         timing=config.profile, graph_chunk=config.graph_chunk)
+                         timing=2 if config.profile else 0, graph_chunk=config.graph_chunk)
+    phase_ms = plan.phase_ms(res.iterations) if config.profile else None
     if res.error_phase >= 0:
         _raise_device_error(graph, plan, state, res)
     executed = int(res.iterations)
@@ -649,26 +679,34 @@ def run(graph, config, state=None):
     state.iteration += executed
     total = perf_counter() - start
 
-    # per-phase attribution: edge pass = x (with n fused), variable pass =
-    # z (with m and u fused); residual reduction is outside the phases
-    a, b = res.ms_edge_pass, res.ms_var_pass
     dev = res.ms_total / 1e3
-    share = (a / (a + b + res.ms_reduce)) if (a + b) > 0 else 0.5
-    vshare = (b / (a + b + res.ms_reduce)) if (a + b) > 0 else 0.5
-    phase_totals = {"x": dev * share, "m": 0.0, "z": dev * vshare, "u": 0.0, "n": 0.0}
-    per_it = {k: v / max(executed, 1) for k, v in phase_totals.items()}
-    tol_check = config.primal_tol > 0.0 or config.dual_tol > 0.0
+    if phase_ms is not None and len(phase_ms) >= executed:
+        # profile mode: the five phases ran as separate kernels, each timed
+        # with CUDA events per iteration (reference engine.py:489-500)
+        rows = phase_ms[:executed] / 1e3
+        phase_totals = dict(zip(PHASES, (float(v) for v in rows.sum(axis=0))))
+    else:
+        # fused mode: the edge pass is phase x (with the previous
+        # iteration's n fused in), the variable pass phase z (with m and u
+        # fused); m, u and n have no kernels of their own, so they report
+        # 0.  Every row carries the run's mean (no per-iteration events
+        # inside the CUDA graphs).  RunConfig(profile=True) times them.
+        a, b = res.ms_edge_pass, res.ms_var_pass
+        share = (a / (a + b + res.ms_reduce)) if (a + b) > 0 else 0.5
+        vshare = (b / (a + b + res.ms_reduce)) if (a + b) > 0 else 0.5
+        phase_totals = {"x": dev * share, "m": 0.0, "z": dev * vshare, "u": 0.0, "n": 0.0}
+        mean = np.array([phase_totals[k] / max(executed, 1) for k in PHASES])
+        rows = np.broadcast_to(mean, (max(executed, 1), 5))
     history = []
     converged = bool(res.converged)
     for j in range(1, executed + 1):
         record = (j % config.record_every == 0) or j == config.max_iterations \
             or (converged and j == executed)
         if record:
-            history.append((base_iteration + j, *(per_it[p] for p in PHASES),
+            history.append((base_iteration + j, *(float(v) for v in rows[j - 1]),
                             float(hist[j - 1, 0]), float(hist[j - 1, 1])))
     if executed:
         state.last_residuals = (float(hist[executed - 1, 0]), float(hist[executed - 1, 1]))
-    del tol_check
     solution = Solution(sol_z["z"], graph.var_offsets, copy=False)
     report = RunReport(iterations=executed, converged=converged, workers=config.workers,
                        phase_seconds=phase_totals, history=history,

@@ -152,6 +152,11 @@ class LocalGraph:
         gz = graph.var_offsets[self.global_var]
         self.global_z = np.repeat(gz - self.var_offsets[:-1], dims) + np.arange(self.z_dim)
         self.z_weights = graph.z_weights[self.global_z].copy()
+        # rho / alpha / z weights follow set_edge_params on the global
+        # graph: re-sliced when its param_version moves (param_version)
+        self._global = graph
+        self._payload_len = payload
+        self._version = getattr(graph, "param_version", None)
         # cut variables: local degree < global degree
         gdeg = np.bincount(graph.edge_var, minlength=len(dims_all))
         ldeg = np.bincount(lv, minlength=len(dims))
@@ -180,9 +185,25 @@ class LocalGraph:
         sel = self._blocks_local[block_index][5]
         return self._factor_edge0[sel]
 
+    def _resync_params(self):
+        g = self._global
+        self.edge_rho = np.asarray(g.edge_rho)[self.global_edge].copy()
+        self.edge_alpha = np.asarray(g.edge_alpha)[self.global_edge].copy()
+        self.rho_flat = np.repeat(self.edge_rho, self._payload_len)
+        self.alpha_flat = np.repeat(self.edge_alpha, self._payload_len)
+        self.z_weights = np.asarray(g.z_weights)[self.global_z].copy()
+
     @property
     def param_version(self):
-        return 0
+        """The global graph's parameter version; the local rho, alpha and z
+        weights are re-sliced from it whenever it moved (a graph without a
+        version -- a reference FactorGraph -- is re-sliced on every read,
+        and None makes the device plan re-sync every time)."""
+        gv = getattr(self._global, "param_version", None)
+        if gv is None or gv != self._version:
+            self._resync_params()
+            self._version = gv
+        return gv
 
     def variable_slice(self, v):
         return slice(int(self.var_offsets[v]), int(self.var_offsets[v + 1]))

@@ -182,9 +182,90 @@ def operators():
     save("operators.npz", **out)
 
 
+def converged():
+    """Long runs of the reference for the convergence gates
+    (``tests/test_gpu_convergence.py``; BASELINE.md "objective and
+    feasibility at convergence", reference test_acceptance.py:157-192).
+
+    Packing is bit-portable, so the device must reproduce the reference's
+    state after 20,000 iterations exactly (SHA-256 of z), and with it the
+    reference's objective and violation; the SVM N=12 case (C5) records
+    the reference's converged solution and iteration count."""
+    out = {}
+    for n, K in ((100, 20000), (500, 20000)):
+        spec = P.PackingSpec(n)
+        g = P.build_packing(spec)
+        st0 = P.packing_init(g, spec, seed=0)
+        s, rep, hist = run_ref(g, st0, K, primal_tol=1e-8, dual_tol=1e-8,
+                               record_every=1000)
+        z = s.z.copy()
+        out[f"pack{n}_iterations"] = np.array(rep.iterations)
+        out[f"pack{n}_converged"] = np.array(rep.converged)
+        out[f"pack{n}_sha"] = np.array([sha(getattr(s, k)) for k in "xmzun"])
+        out[f"pack{n}_objective"] = np.array(g.objective_value(z))
+        out[f"pack{n}_violation"] = np.array(g.constraint_violation(z))
+        out[f"pack{n}_last_residuals"] = np.array(s.last_residuals)
+        print(n, rep.iterations, rep.converged, out[f"pack{n}_objective"],
+              out[f"pack{n}_violation"], flush=True)
+    pts = P.gen_gaussian_data(12, 2, 4.0, seed=0)
+    g = P.build_svm(P.SvmSpec(pts, lam=1.0))
+    sol, rep = fgadmm.run(g, fgadmm.RunConfig(max_iterations=60000, primal_tol=1e-10,
+                                              dual_tol=1e-10))
+    out["svm12_iterations"] = np.array(rep.iterations)
+    out["svm12_w"] = sol[0].copy()
+    out["svm12_b"] = np.array(float(sol[12][0]))
+    out["svm12_objective"] = np.array(P.svm_objective(pts, 1.0, sol[0], float(sol[12][0])))
+    big = P.gen_gaussian_data(200, 2, 4.0, seed=0)
+    g2 = P.build_svm(P.SvmSpec(big, lam=1.0))
+    sol2, _ = fgadmm.run(g2, fgadmm.RunConfig(max_iterations=5000))
+    out["svm200_w"] = sol2[0].copy()
+    out["svm200_b"] = np.array(float(sol2[200][0]))
+    out["svm200_accuracy"] = np.array(P.svm_accuracy(big, sol2[0], float(sol2[200][0])))
+    save("converged.npz", **out)
+
+
+def documents():
+    """Graph documents written by the reference's ``serialize``
+    (graph.py:265-286) and the reference's own 10-iteration results on the
+    graphs it rebuilds from them (``deserialize``, graph.py:289-340): the
+    device must run a document-driven graph to the same state.  Weights are
+    varied per edge (set_edge_params) so the documents carry non-unit rho
+    and alpha."""
+    import gzip
+    out = {}
+    rng = np.random.default_rng(77)
+    spec = P.PackingSpec(30)
+    gp = P.build_packing(spec)
+    for e in rng.choice(len(gp.edge_var), 40, replace=False):
+        gp.set_edge_params(int(e), float(rng.uniform(0.5, 2.0)), float(rng.uniform(0.5, 1.5)))
+    pts = P.gen_gaussian_data(60, 4, 4.0, seed=3)
+    gs = P.build_svm(P.SvmSpec(pts, lam=0.7, rho=1.5, alpha=1.2))
+    rng2 = np.random.default_rng(5)
+    A = 0.05 * rng2.standard_normal((4, 4))
+    B = 0.1 * rng2.standard_normal((4, 2))
+    gm = P.build_mpc(P.MpcSpec(25, fgadmm.LinearSystem(A, B), rng2.standard_normal(4)))
+    for tag, g0, seed in (("pack30", gp, 4), ("svm60x4", gs, 5), ("mpc4x2", gm, 6)):
+        doc = fgadmm.serialize(g0)
+        with gzip.open(os.path.join(HERE, f"doc_{tag}.json.gz"), "wt") as fh:
+            fh.write(doc)
+        g = fgadmm.deserialize(doc)
+        assert fgadmm.serialize(g) == doc
+        st0 = fgadmm.init_state(g, seed=seed)
+        s, rep, hist = run_ref(g, st0, 10)
+        for k in "xmzun":
+            out[f"{tag}_{k}"] = getattr(s, k).copy()
+        out[f"{tag}_sha"] = np.array([sha(getattr(s, k)) for k in "xmzun"])
+        out[f"{tag}_hist"] = hist
+        out[f"{tag}_doc_sha"] = np.array(hashlib.sha256(doc.encode()).hexdigest())
+        out[f"{tag}_zmap"] = g.zmap.copy()
+        out[f"{tag}_z_weights"] = g.z_weights.copy()
+        out[f"{tag}_rho_flat"] = g.rho_flat.copy()
+        out[f"{tag}_alpha_flat"] = g.alpha_flat.copy()
+    save("documents.npz", **out)
+
+
 if __name__ == "__main__":
-    quadratic_trace()
-    operators()
-    packing()
-    svm()
-    mpc()
+    which = sys.argv[1:] or ["quadratic_trace", "operators", "packing", "svm", "mpc",
+                             "documents", "converged"]
+    for name in which:
+        globals()[name]()

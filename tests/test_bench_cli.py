@@ -33,3 +33,6 @@ def test_gpu_bench_sweep(gpu, capsys):
     rows = [line.split(",") for line in out[1:]]
     assert all(int(r[3]) == 20 for r in rows)
     assert all(float(r[10]) > 0.0 and np.isfinite(float(r[11])) for r in rows)
+    # reference acceptance C8 (test_acceptance.py:238-257): all five phase
+    # columns are timed (> 0) -- the profile run launches them separately
+    assert all(float(r[c]) > 0.0 for r in rows for c in range(4, 9))

@@ -119,3 +119,23 @@ def test_svm_rank_graphs_match_single_plan(gpu, world):
         nb = n * D + (0 if r == world - 1 else D)
         assert _close(ls.z[nb:nb + 1], single.z[N * D:N * D + 1])
         assert _close(ls.z[nb + 1:], single.z[N * D + 1 + r * n:N * D + 1 + (r + 1) * n])
+
+
+@pytest.mark.parametrize("name", ["svm", "pack"])
+def test_local_group_reads_n_per_plan(gpu, name):
+    """Whether iteration 1 reads the uploaded n is decided per plan: with n
+    edited on one rank's payload only (every other rank's n equals z - u,
+    so those plans may start on their chain forms), the group still reads
+    the edited n there and matches one plan run from the same state."""
+    g = _graph(name)
+    st = fg.init_state(g, seed=6)
+    grp = LocalGroup(g, 2)
+    P1 = grp.locals[1].global_payload
+    rng = np.random.default_rng(1)
+    st.n[P1[:50]] += rng.uniform(-0.1, 0.1, 50)
+    single = fg.AdmmState(*(getattr(st, k).copy() for k in "xmzun"))
+    fg.run(g, fg.RunConfig(max_iterations=6), state=single)
+    out, res, _h = grp.run(6, st)
+    assert res.iterations == 6
+    for k in "xmzun":
+        assert _close(getattr(out, k), getattr(single, k)), k

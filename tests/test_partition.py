@@ -231,3 +231,21 @@ def test_gloo_world2_rank_graphs_match_single(tmp_path):
         nb = n * D + (0 if r == world - 1 else D)
         np.testing.assert_allclose(z[nb], ref.z[N * D], rtol=1e-11, atol=1e-13)
     np.testing.assert_allclose(res["hist"], np.array(ref_hist), rtol=1e-10)
+
+
+def test_local_graph_follows_set_edge_params():
+    """A rank's LocalGraph re-slices rho, alpha and the z weights when the
+    global graph's parameters change (its param_version moves), so device
+    plans of partitioned runs re-sync instead of keeping stale weights."""
+    import paper_1603_02526_b200 as fg
+    from paper_1603_02526_b200.partition import Partition
+    g = fg.build_packing(fg.PackingSpec(12))
+    part = Partition(g, 2)
+    lg = part.local(1)
+    v0 = lg.param_version
+    e = int(lg.global_edge[3])
+    g.set_edge_params(e, rho=2.5, alpha=0.75)
+    assert lg.param_version != v0
+    assert lg.edge_rho[3] == 2.5 and lg.edge_alpha[3] == 0.75
+    np.testing.assert_array_equal(lg.z_weights, g.z_weights[lg.global_z])
+    np.testing.assert_array_equal(lg.rho_flat, np.repeat(lg.edge_rho, np.diff(lg.edge_offsets)))
