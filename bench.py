@@ -44,10 +44,15 @@ UNIT = "edge-updates/s"
 
 WORKLOADS = {
     "svm1m": "soft-margin linear SVM chain, 1M points x 32 dims (configs[1])",
+    "svm1m_rho2": "configs[1] with rho = 2 on every edge (SvmSpec(rho=2); adaptive-rho use case)",
+    "svm1m_w": "configs[1] with rho = 1.5, alpha = 1.2 on every edge (non-power-of-two weights)",
     "pack5000": "circle packing N=5000 in the unit triangle (configs[3])",
     "mpc100k": "linear MPC, state 16, input 4, horizon 100k (configs[2])",
     "pack100": "circle packing N=100 in the unit triangle (configs[0])",
 }
+
+
+SVM_WEIGHTS = {"svm1m_rho2": (2.0, 1.0), "svm1m_w": (1.5, 1.2)}
 
 
 def build_instance(name, scale=1.0):
@@ -55,8 +60,10 @@ def build_instance(name, scale=1.0):
     if name.startswith("svm"):
         n = int(1_000_000 * scale)
         X, y = fg.gen_gaussian_arrays(n, 32, 4.0, seed=0)
-        g = fg.build_svm(fg.SvmSpec.from_arrays(X, y, lam=1.0))
-        return g, fg.init_state(g), {"points": n, "dim": 32, "init": "zeros"}
+        rho, alpha = SVM_WEIGHTS.get(name, (1.0, 1.0))
+        g = fg.build_svm(fg.SvmSpec.from_arrays(X, y, lam=1.0, rho=rho, alpha=alpha))
+        return g, fg.init_state(g), {"points": n, "dim": 32, "init": "zeros",
+                                     "rho": rho, "alpha": alpha}
     if name.startswith("pack"):
         n = int((5000 if name == "pack5000" else 100) * (scale if name == "pack5000" else 1))
         spec = fg.PackingSpec(n)
@@ -295,7 +302,9 @@ def reference_instance(ref, name, scale=1.0):
     P = ref.problems
     if name.startswith("svm"):
         n = int(1_000_000 * scale)
-        g = P.build_svm(P.SvmSpec(P.gen_gaussian_data(n, 32, 4.0, seed=0), lam=1.0))
+        rho, alpha = SVM_WEIGHTS.get(name, (1.0, 1.0))
+        g = P.build_svm(P.SvmSpec(P.gen_gaussian_data(n, 32, 4.0, seed=0), lam=1.0,
+                                  rho=rho, alpha=alpha))
         return g, ref.init_state(g), {"points": n, "dim": 32, "init": "zeros"}
     if name.startswith("mpc"):
         T = int(100_000 * scale)
