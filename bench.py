@@ -151,18 +151,21 @@ def chain_bytes(graph, dims, deg, unit):
     per weight copy w_i (dim D, degree 3-4) u read+write and z read+write;
     per slack xi_i the same at dim 1, degree 2; per point the margin data
     (x_i, y_i), x.x, the norm and slack parameters, b's u read and x write.
-    The general-weight forms also read z weights and rho/alpha per edge (and
-    b's rho); the unit-weight form reads none of them.  Neighbours'
+    The weighted form also reads rho and alpha per edge of w_i and xi_i, one
+    z weight per variable (w_i's is shared by its D components), b's rho
+    and three per-point tables (norm factor, slack threshold, margin
+    denominator); the unit-weight form reads none of them.  Neighbours'
     equality edges are re-reads of the same arrays (L2), not counted."""
     n = int(np.sum(deg == 2))                  # xi's (b has degree n > 32)
     wsel = (deg >= 3) & (deg <= 4)
     P_w = int(np.sum(deg[wsel] * dims[wsel]))
     Z_w = int(np.sum(dims[wsel]))
     E_w = int(np.sum(deg[wsel]))
+    V_w = int(np.sum(wsel))
     D = int(dims[wsel][0]) if wsel.any() else 0
-    w = P_w * 16 + Z_w * 16 + (0 if unit else Z_w * 8 + E_w * 16)
-    xi = n * (2 * 16 + 16 + (0 if unit else 8 + 2 * 16))
-    per_point = (D + 1) * 8 + 3 * 8 + 8 + 8 + (0 if unit else 8)
+    w = P_w * 16 + Z_w * 16 + (0 if unit else E_w * 16 + V_w * 8)
+    xi = n * (2 * 16 + 16 + (0 if unit else 2 * 16 + 8))
+    per_point = (D + 1) * 8 + 3 * 8 + 8 + 8 + (0 if unit else 8 + 3 * 8)
     return w + xi + n * per_point
 
 

@@ -18,6 +18,9 @@
  *   fg_residuals          engine.py:398-406  residuals
  *   fg_prox_eval          prox.py:60-78      ProxFactor.batch_eval per kind
  *                         operators.py       (11 closed forms)
+ *   fg_wproj              operators.py:86-96, 606-623  weighted null-space
+ *                                            projection (mpc_dyn_prox with
+ *                                            three weights)
  *   fg_last_error         engine.py:145-149, 333-350 (error text source)
  *
  * All arrays are HOST pointers in the reference's own order (edge-creation
@@ -224,6 +227,18 @@ int fg_evaluate(fg_plan* plan, const double* z, double* out2);
  * slot after slot; rhos: (nslots, count); out like values. */
 int fg_prox_eval(const fg_group_desc* group, const double* values,
                  const double* rhos, double* out, int32_t device);
+/* Weighted projection of each row of nv (rows x D) onto {v : M v = 0}
+ * (M is r x D, row-major, shared by all rows) minimizing sum w (v - nv)^2,
+ * operators.py:86-96.  Weights must be positive (FG_ERR_INVALID);
+ * a singular M W^-1 M^T gives FG_ERR_NONFINITE ("Singular matrix"). */
+int fg_wproj(const double* M, int32_t r, int32_t D, const double* nv,
+             const double* w, int64_t rows, double* out, int32_t device);
+
+/* ---- self-test --------------------------------------------------------- */
+/* q[i] = the engine's inline division x[i] / y[i] (fg_device.cuh qdiv),
+ * ref[i] = the CUDA runtime's x[i] / y[i]; the two must agree bitwise. */
+int fg_selftest_div(const double* x, const double* y, int64_t n, double* q,
+                    double* ref, int32_t device);
 
 /* ---- multi-GPU exchange of cut-variable partial sums ------------------- */
 /* NCCL (one process per GPU): rank 0 calls fg_nccl_unique_id, the id is

@@ -12,14 +12,15 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfgadmm_b200.so")
+# FGADMM_LIB: an alternative build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("FGADMM_LIB") or os.path.join(_HERE, "libfgadmm_b200.so")
 
 FG_MAX_SLOTS = 8
 PHASE_IDS = {"x": 0, "m": 1, "z": 2, "u": 3, "n": 4}
 PHASE_NAMES = ("x", "m", "z", "u", "n")
 BUF_X, BUF_U0, BUF_U1, BUF_AUX, BUF_Z0, BUF_Z1 = 0, 1, 2, 3, 4, 5
 
-ERR_INVALID, ERR_CUDA, ERR_UNSUPPORTED = -1, -2, -3
+ERR_INVALID, ERR_CUDA, ERR_UNSUPPORTED, ERR_NONFINITE = -1, -2, -3, -4
 
 _p = C.c_void_p
 _i32p = C.POINTER(C.c_int32)
@@ -81,6 +82,8 @@ EXPORTS = {
     "fg_residuals": (C.c_int, [_p, _dp, _dp, _dp, _dp, _dp]),
     "fg_evaluate": (C.c_int, [_p, _dp, _dp]),
     "fg_prox_eval": (C.c_int, [C.POINTER(GroupDesc), _dp, _dp, _dp, C.c_int32]),
+    "fg_wproj": (C.c_int, [_dp, C.c_int32, C.c_int32, _dp, _dp, C.c_int64, _dp, C.c_int32]),
+    "fg_selftest_div": (C.c_int, [_dp, _dp, C.c_int64, _dp, _dp, C.c_int32]),
     "fg_nccl_unique_id": (C.c_int, [C.c_char_p, C.c_char_p]),
     "fg_plan_attach_nccl": (C.c_int, [_p, C.c_char_p, C.c_char_p, C.c_int32, C.c_int32]),
     "fg_group_run": (C.c_int, [C.POINTER(_p), C.c_int32, C.POINTER(RunConfig), _dp,
@@ -202,6 +205,32 @@ def prox_eval(cls, params, dims, values, rhos, device=0):
         res.append(out[off:off + B * d].reshape(B, d))
         off += B * d
     return res
+
+
+def wproj(M, nv, w, device=0):
+    """Weighted null-space projection of the rows of ``nv`` (operators.py:
+    86-96) on the device (fg_wproj)."""
+    lib = load()
+    M = np.ascontiguousarray(M, dtype=np.float64)
+    nv = np.ascontiguousarray(np.atleast_2d(nv), dtype=np.float64)
+    w = np.ascontiguousarray(np.broadcast_to(np.atleast_2d(w), nv.shape), dtype=np.float64)
+    out = np.empty_like(nv)
+    r, D = M.shape
+    rc = lib.fg_wproj(dptr(M), int(r), int(D), dptr(nv), dptr(w), int(nv.shape[0]),
+                      dptr(out), int(device))
+    if rc == ERR_NONFINITE:
+        raise np.linalg.LinAlgError(load().fg_last_error().decode(errors="replace"))
+    check(rc)
+    return out
+
+
+def selftest_div(x, y, device=0):
+    """(engine inline division, runtime division) of x / y on the device."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    q, ref = np.empty_like(x), np.empty_like(x)
+    check(load().fg_selftest_div(dptr(x), dptr(y), int(x.size), dptr(q), dptr(ref), int(device)))
+    return q, ref
 
 
 class _PinnedBlock:

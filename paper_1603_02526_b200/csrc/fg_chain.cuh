@@ -49,9 +49,13 @@ struct ChainDev {
     const double* fp_margin;      // per point: x (D), y
     const double* xx;             // per point: x.x (plan-time, margin order)
     const double* fnorm;          // per point: 1/(1+scale) (unit-weight form)
+    const double* wtab;           // per point: 3 tables of the weighted form
 };
 
 constexpr int kChainThreads = 256;
+#ifndef FG_CHAIN_W_MINB
+#define FG_CHAIN_W_MINB 4        // CTAs/SM of the weighted form (3: 0.83 vs 0.79 ms, SVM 1M)
+#endif
 
 // Per-point scalars are spread over the lanes of the point's warp (one
 // load per lane, fetched with shuffles where used) so a lane holds only its
@@ -288,154 +292,212 @@ __global__ void __launch_bounds__(kChainThreads, MINB) k_svm_chain(PassB b, Chai
 }
 
 // ---------------------------------------------------------------------------
-// Fast form: D = 32 (one lane per component, no inactive lanes) and interior
-// points 1 <= i <= n-2 (degree 4: norm, margin, eq(i-1,i), eq(i,i+1)).
-// Every address is a per-point base plus a compile-time offset, the 24
-// per-point scalars are one load per lane (base + i * stride, set up once
-// per thread), and x.x of the margin (constant per point) comes from a
-// table computed at plan time in k_svm_margin's order.  Same arithmetic as
-// the generic form operation by operation.
-enum : int { kSZWX = 23, kSXX = 24 };
+// Weighted form: D = 32 (one lane per component) and interior points
+// 1 <= i <= n-2 (degree 4: norm, margin, eq(i-1,i), eq(i,i+1)), any edge
+// weights.  Same arithmetic as the generic form operation by operation,
+// organised like the unit-weight form below (per-warp scalar slots in
+// shared memory, 64 registers, 4 CTAs/SM):
+//  * the per-point weights (rho/alpha of the point's 8 edges, the
+//    neighbours' equality rho, b's margin rho, xi's z weight, w_i's z
+//    weight) are one load per lane; the z weight of w_i is the same for all
+//    D components (z_weights sums the per-edge rho_flat, graph.py:216-222;
+//    checked at sync), so it is a per-point scalar, not a per-lane row;
+//  * the iteration-invariant divisions are per-point tables built at every
+//    parameter sync with the same operations (k_chain_wtab): the norm
+//    factor rho0/(rho0+scale), the slack threshold lam/rho_x0 and the
+//    margin denominator (x.x/rho1 + 1/rho_b) + 1/rho_x1;
+//  * the three divisions of the margin multiplier mu (mu/rho1, mu/rho_b,
+//    mu/rho_x1) run as ONE warp-wide division, lane k dividing by the k-th
+//    weight, then shuffled back: a warp issues a division sequence once
+//    whatever each lane divides;
+//  * every division is the inline qdiv (fg_device.cuh), bitwise the
+//    runtime's `x / y`: with the runtime's slow-path call, ptxas saved the
+//    live registers around every division site.
+// Six division sequences per point instead of thirteen.
+enum : int {
+    kWR = 0,        // lanes 0..3: rho of w_i's edges k
+    kWA = 4,        // lanes 4..7: alpha of w_i's edges k
+    kWRP = 8, kWRN = 9, kWY = 10, kWFN = 11, kWLR = 12, kWZX = 13, kWUX0 = 14, kWUX1 = 15,
+    kWRX0 = 16, kWRX1 = 17, kWAX0 = 18, kWAX1 = 19, kWZB = 20, kWUB = 21, kWRB = 22,
+    kWZWX = 23, kWDEN = 24, kWZWW = 25
+};
 
+// One interior point of the weighted form.
 template <int D>
-__global__ void __launch_bounds__(kChainThreads, 2) k_svm_chain_fast(PassB b, ChainDev c,
-                                                                    double* xb_out,
-                                                                    int64_t part_off) {
-    static_assert(D == 32, "one lane per component");
-    __shared__ double sm[16];
-    if (b.ctrl->stop) return;
-    const int64_t it = b.ctrl->iter;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int32_t nin = c.n - 2;                     // interior points 1..n-2
-    const int32_t per_cta = (nin + gridDim.x - 1) / gridDim.x;
-    const int32_t i0 = 1 + blockIdx.x * per_cta;
-    const int32_t i1 = min(c.n - 1, i0 + per_cta);
-    // lane scalar: sb + i * ss (w_i's edges start at 4i - 1)
-    const double* sb = b.rho;
-    int64_t ss = 0;
-    switch (lane) {
-        case 0: case 1: case 2: case 3: sb = b.rho + c.eW - 1 + lane; ss = 4; break;
-        case 4: case 5: case 6: case 7: sb = b.alpha + c.eW - 1 + (lane - 4); ss = 4; break;
-        case kSRP: sb = b.rho + c.eW - 2; ss = 4; break;           // w_{i-1}'s eq
-        case kSRN: sb = b.rho + c.eW - 1 + 6; ss = 4; break;       // w_{i+1}'s eq
-        case kSY: sb = c.fp_margin + D; ss = c.st_margin; break;
-        case kSScale: sb = c.fp_norm; ss = c.st_norm; break;
-        case kSLam: sb = c.fp_slack; ss = c.st_slack; break;
-        case kSZX: sb = b.zin + c.zX; ss = 1; break;
-        case kSUX0: sb = b.uin + c.pX; ss = 2; break;
-        case kSUX1: sb = b.uin + c.pX + 1; ss = 2; break;
-        case kSRX0: sb = b.rho + c.eX; ss = 2; break;
-        case kSRX1: sb = b.rho + c.eX + 1; ss = 2; break;
-        case kSAX0: sb = b.alpha + c.eX; ss = 2; break;
-        case kSAX1: sb = b.alpha + c.eX + 1; ss = 2; break;
-        case kSZB: sb = b.zin + c.zB; ss = 0; break;
-        case kSUB: sb = b.uin + c.pB; ss = 1; break;
-        case kSRB: sb = b.rho + c.eB; ss = 1; break;
-        case kSZWX: sb = b.zw + c.zX; ss = 1; break;
-        case kSXX: sb = c.xx; ss = 1; break;
-        default: break;
+__device__ __forceinline__ void chain_w_point(const PassB& b, const ChainDev& c, int32_t i,
+                                              int lane, double* sc, double* su,
+                                              double* xb_out, double& pp, double& dd,
+                                              unsigned& bad) {
+    const int64_t wo = c.pW + (int64_t)(4 * i - 1) * D + lane;
+    const double* __restrict__ U = b.uin + wo;
+    const int64_t zo = c.zW + (int64_t)i * D + lane;
+    const double* __restrict__ Z = b.zin + zo;
+    double u0 = U[0], u1 = U[D], u2 = U[2 * D], u3 = U[3 * D];
+    const double up = U[-D], un_ = U[6 * D];
+    const double zi = Z[0], zp = Z[-D], zn_ = Z[D];
+    const double X = c.fp_margin[(int64_t)i * c.st_margin + lane];
+    // u rows parked in shared memory across the divisions (registers)
+    su[0] = u0; su[32] = u1; su[64] = u2; su[96] = u3;
+    // ---- phase n ----
+    const double n0 = zi - u0, n1 = zi - u1, n2 = zi - u2, n3 = zi - u3;
+    const double np_ = zp - up, nn_ = zn_ - un_;
+    const double zxi = sc[kWZX], ux0 = sc[kWUX0], ux1 = sc[kWUX1];
+    const double nb = sc[kWZB] - sc[kWUB], nx0 = zxi - ux0, nx1 = zxi - ux1;
+    {
+        const double sn = ((n0 + n1) + (n2 + n3)) + ((np_ + nn_) + ((nb + nx0) + nx1));
+        if (!finite(sn) &&
+            !(finite(n0) && finite(n1) && finite(n2) && finite(n3) && finite(np_) &&
+              finite(nn_) && finite(nb) && finite(nx0) && finite(nx1)))
+            bad |= 1u;
     }
-    double pp = 0.0, dd = 0.0;
-    bool bn = false, bx = false, bm = false, bz = false, bu = false;
-    auto S = [&](double v, int src) { return __shfl_sync(kFull, v, src); };
-    for (int32_t i = i0 + warp; i < i1; i += kChainThreads / 32) {
-        // w_i's segment: elements 4i-1 .. 4i+2 of the w block
-        const int64_t wo = c.pW + (int64_t)(4 * i - 1) * D + lane;
-        const double* __restrict__ U = b.uin + wo;
-        const double* __restrict__ Z = b.zin + c.zW + (int64_t)i * D + lane;
-        const double u0 = U[0], u1 = U[D], u2 = U[2 * D], u3 = U[3 * D];
-        const double up = U[-D];                     // w_{i-1}: eq(i-1, i)
-        const double un_ = U[6 * D];                 // w_{i+1}: eq(i, i+1)
-        const double zi = Z[0], zp = Z[-D], zn_ = Z[D];
-        const double zwv = b.zw[c.zW + (int64_t)i * D + lane];
-        const double X = c.fp_margin[(int64_t)i * c.st_margin + lane];
-        const double sv = sb[(int64_t)i * ss];
-        // ---- phase n ----
-        const double n0 = zi - u0, n1 = zi - u1, n2 = zi - u2, n3 = zi - u3;
-        const double np_ = zp - up, nn_ = zn_ - un_;
-        const double zxi = S(sv, kSZX), ux0 = S(sv, kSUX0), ux1 = S(sv, kSUX1);
-        const double nb = S(sv, kSZB) - S(sv, kSUB), nx0 = zxi - ux0, nx1 = zxi - ux1;
-        bn |= !(finite(n0) && finite(n1) && finite(n2) && finite(n3) && finite(np_) &&
-                finite(nn_) && finite(nb) && finite(nx0) && finite(nx1));
-        // ---- phase x ----
-        const double r0 = S(sv, 0), r1 = S(sv, 1), r2 = S(sv, 2), r3 = S(sv, 3);
-        const double x0 = prox_svm_norm(n0, r0, S(sv, kSScale));
-        const double pr = n1 * X;
-        const int g = lane & 7;
-        double dot = 0.0;
-        dot += S(pr, g);
-        dot += S(pr, g + 8);
-        dot += S(pr, g + 16);
-        dot += S(pr, g + 24);
-        dot += __shfl_xor_sync(kFull, dot, 1);
-        dot += __shfl_xor_sync(kFull, dot, 2);
-        dot += __shfl_xor_sync(kFull, dot, 4);
-        const double Y = S(sv, kSY), rb = S(sv, kSRB), R3 = S(sv, kSRX1);
-        const double slack = (1.0 - nx1) - Y * (dot + nb);
-        const double denom = (ddiv(S(sv, kSXX), r1) + ddiv(1.0, rb)) + ddiv(1.0, R3);
-        const double mu = ddiv(np_max0(slack), denom);
-        const double tw = ddiv(mu, r1) * Y;
-        const double x1 = n1 + tw * X;
-        const double xbv = nb + ddiv(mu, rb) * Y;
-        const double xx1 = nx1 + ddiv(mu, R3);
-        const double rx0 = S(sv, kSRX0);
-        const double xx0 = prox_svm_slack(nx0, rx0, S(sv, kSLam));
-        const double x2 = prox_equality(np_, n2, S(sv, kSRP), r2);
-        const double x3 = prox_equality(n3, nn_, r3, S(sv, kSRN));
-        bx |= !(finite(x0) && finite(x1) && finite(x2) && finite(x3) && finite(xbv) &&
-                finite(xx0) && finite(xx1));
-        // ---- phases m, z, u of w_i ----
+    // ---- phase x (equalities first: their inputs die early) ----
+    const double x2 = ddivq(sc[kWRP] * np_ + sc[kWR + 2] * n2,
+                            sc[kWRP] + sc[kWR + 2]);                 // prox_equality
+    const double x3 = ddivq(sc[kWR + 3] * n3 + sc[kWRN] * nn_, sc[kWR + 3] + sc[kWRN]);
+    const double x0 = sc[kWFN] * n0;                              // prox_svm_norm
+    const double pr = n1 * X;
+    const int g = lane & 7;
+    double dot = 0.0;
+    dot += __shfl_sync(kFull, pr, g);
+    dot += __shfl_sync(kFull, pr, g + 8);
+    dot += __shfl_sync(kFull, pr, g + 16);
+    dot += __shfl_sync(kFull, pr, g + 24);
+    dot += __shfl_xor_sync(kFull, dot, 1);
+    dot += __shfl_xor_sync(kFull, dot, 2);
+    dot += __shfl_xor_sync(kFull, dot, 4);
+    const double Y = sc[kWY];
+    const double slack = (1.0 - nx1) - Y * (dot + nb);
+    const double mu = ddivq(np_max0(slack), sc[kWDEN]);
+    // mu/rho1, mu/rho_b, mu/rho_x1 on lanes 0, 1, 2 (one division for all)
+    const double q = ddivq(mu, sc[lane == 1 ? kWRB : (lane == 2 ? kWRX1 : kWR + 1)]);
+    const double x1 = n1 + (__shfl_sync(kFull, q, 0) * Y) * X;
+    const double xbv = nb + __shfl_sync(kFull, q, 1) * Y;
+    const double xx1 = nx1 + __shfl_sync(kFull, q, 2);
+    const double xx0 = np_max0(nx0 - sc[kWLR]);                  // prox_svm_slack
+    // ---- phases m, z, u of w_i ----
+    {
+        const double r0 = sc[kWR], r1 = sc[kWR + 1], r2 = sc[kWR + 2], r3 = sc[kWR + 3];
+        u0 = su[0]; u1 = su[32]; u2 = su[64]; u3 = su[96];
         const double m0 = x0 + u0, m1 = x1 + u1, m2 = x2 + u2, m3 = x3 + u3;
-        bm |= !(finite(m0) && finite(m1) && finite(m2) && finite(m3));
         double res = 0.0;
         res += m1 * r1;
         res += m2 * r2;
         res += m3 * r3;
-        const double zn = ddiv(m0 * r0 + res, zwv);
-        bz |= !finite(zn);
-        b.z[c.zW + (int64_t)i * D + lane] = zn;
+        const double zn = ddivq(m0 * r0 + res, sc[kWZWW]);
+        b.z[zo] = zn;
         const double dz = zn - zi;
-        const double a0 = S(sv, 4), a1 = S(sv, 5), a2 = S(sv, 6), a3 = S(sv, 7);
+        const double t0 = x0 - zn, t1 = x1 - zn, t2 = x2 - zn, t3 = x3 - zn;
+        const double v0 = u0 + t0 * sc[kWA], v1 = u1 + t1 * sc[kWA + 1];
+        const double v2 = u2 + t2 * sc[kWA + 2], v3 = u3 + t3 * sc[kWA + 3];
         double* __restrict__ UO = b.uout + wo;
-        {
-            const double t0 = x0 - zn, t1 = x1 - zn, t2 = x2 - zn, t3 = x3 - zn;
-            const double d0 = r0 * dz, d1 = r1 * dz, d2 = r2 * dz, d3 = r3 * dz;
-            pp += t0 * t0; dd += d0 * d0;
-            pp += t1 * t1; dd += d1 * d1;
-            pp += t2 * t2; dd += d2 * d2;
-            pp += t3 * t3; dd += d3 * d3;
-            const double v0 = u0 + t0 * a0, v1 = u1 + t1 * a1;
-            const double v2 = u2 + t2 * a2, v3 = u3 + t3 * a3;
-            UO[0] = v0; UO[D] = v1; UO[2 * D] = v2; UO[3 * D] = v3;
-            bu |= !(finite(v0) && finite(v1) && finite(v2) && finite(v3));
+        UO[0] = v0; UO[D] = v1; UO[2 * D] = v2; UO[3 * D] = v3;
+        const double d0 = r0 * dz, d1 = r1 * dz, d2 = r2 * dz, d3 = r3 * dz;
+        pp += t0 * t0; dd += d0 * d0;
+        pp += t1 * t1; dd += d1 * d1;
+        pp += t2 * t2; dd += d2 * d2;
+        pp += t3 * t3; dd += d3 * d3;
+        if (!finite((m0 + m1) + (m2 + m3))) {
+            const bool mbad = !(finite(m0) && finite(m1) && finite(m2) && finite(m3));
+            if (mbad && !(finite(x0) && finite(x1) && finite(x2) && finite(x3))) bad |= 2u;
+            if (mbad) bad |= 4u;
         }
-        // ---- phases m, z, u of xi_i (degree 2: slack, margin) ----
-        const double ax0 = S(sv, kSAX0), ax1 = S(sv, kSAX1), zwx = S(sv, kSZWX);
-        if (lane == 0) {
-            const double mx0 = xx0 + ux0, mx1 = xx1 + ux1;
-            bm |= !(finite(mx0) && finite(mx1));
-            double rs = 0.0;
-            rs += mx1 * R3;
-            const double zx = ddiv(mx0 * rx0 + rs, zwx);
-            bz |= !finite(zx);
+        if (!finite(zn)) bad |= 8u;
+        if (!finite((v0 + v1) + (v2 + v3)) &&
+            !(finite(v0) && finite(v1) && finite(v2) && finite(v3)))
+            bad |= 16u;
+    }
+    // ---- xi_i (slack, margin) and b's margin x ----
+    if (lane == 0) {
+        const double rx0 = sc[kWRX0], R3 = sc[kWRX1];
+        const double mx0 = xx0 + ux0, mx1 = xx1 + ux1;
+        double rs = 0.0;
+        rs += mx1 * R3;
+        const double zx = ddivq(mx0 * rx0 + rs, sc[kWZWX]);
+        {
             b.z[c.zX + i] = zx;
             const double dzx = zx - zxi;
-            const double t0 = xx0 - zx, t1 = xx1 - zx;
-            const double d0 = rx0 * dzx, d1 = R3 * dzx;
-            pp += t0 * t0; dd += d0 * d0;
-            pp += t1 * t1; dd += d1 * d1;
-            const double v0 = ux0 + t0 * ax0, v1 = ux1 + t1 * ax1;
-            b.uout[c.pX + 2 * (int64_t)i] = v0;
-            b.uout[c.pX + 2 * (int64_t)i + 1] = v1;
-            bu |= !(finite(v0) && finite(v1));
+            const double s0 = xx0 - zx, s1 = xx1 - zx;
+            const double e0 = rx0 * dzx, e1 = R3 * dzx;
+            pp += s0 * s0; dd += e0 * e0;
+            pp += s1 * s1; dd += e1 * e1;
+            const double w0 = ux0 + s0 * sc[kWAX0], w1 = ux1 + s1 * sc[kWAX1];
+            b.uout[c.pX + 2 * (int64_t)i] = w0;
+            b.uout[c.pX + 2 * (int64_t)i + 1] = w1;
             xb_out[c.pB + i] = xbv;
+            if (!(finite(xbv) && finite(xx0) && finite(xx1))) bad |= 2u;
+            if (!(finite(mx0) && finite(mx1))) bad |= 4u;
+            if (!finite(zx)) bad |= 8u;
+            if (!(finite(w0) && finite(w1))) bad |= 16u;
         }
     }
-    if (bn) flag_error(b.ctrl, it - 1, FG_PHASE_N, true);
-    if (bx) flag_error(b.ctrl, it, FG_PHASE_X, true);
-    if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
-    if (bz) flag_error(b.ctrl, it, FG_PHASE_Z, false);
-    if (bu) flag_error(b.ctrl, it, FG_PHASE_U, false);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kChainThreads, FG_CHAIN_W_MINB) k_svm_chain_w(PassB b, ChainDev c,
+                                                                double* xb_out,
+                                                                int64_t part_off) {
+    static_assert(D == 32, "one lane per component");
+    __shared__ double sm[16];
+    __shared__ double s_sc[kChainThreads / 32][32];     // per-warp point scalars
+    __shared__ const double* s_sb[32];                 // lane scalar: s_sb + i * s_ss
+    __shared__ int32_t s_ss[32];
+    __shared__ double s_u[kChainThreads / 32][4][32];   // per-warp u rows of the point
+    if (b.ctrl->stop) return;
+    const int64_t it = b.ctrl->iter;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int32_t nin = c.n - 2;
+    const int32_t per_cta = (nin + gridDim.x - 1) / gridDim.x;
+    const int32_t i0 = 1 + blockIdx.x * per_cta;
+    const int32_t i1 = min(c.n - 1, i0 + per_cta);
+    // lane scalar: sb + i * ss (w_i's edges start at 4i - 1); kept in shared
+    // memory, not registers (the loop body needs all 64)
+    if (warp == 0) {
+        const double* sb = c.xx;
+        int32_t ss = 0;
+        switch (lane) {
+            case 0: case 1: case 2: case 3: sb = b.rho + c.eW - 1 + lane; ss = 4; break;
+            case 4: case 5: case 6: case 7: sb = b.alpha + c.eW - 1 + (lane - 4); ss = 4; break;
+            case kWRP: sb = b.rho + c.eW - 2; ss = 4; break;        // w_{i-1}'s eq
+            case kWRN: sb = b.rho + c.eW - 1 + 6; ss = 4; break;    // w_{i+1}'s eq
+            case kWY: sb = c.fp_margin + D; ss = c.st_margin; break;
+            case kWFN: sb = c.wtab; ss = 1; break;
+            case kWLR: sb = c.wtab + c.n; ss = 1; break;
+            case kWZX: sb = b.zin + c.zX; ss = 1; break;
+            case kWUX0: sb = b.uin + c.pX; ss = 2; break;
+            case kWUX1: sb = b.uin + c.pX + 1; ss = 2; break;
+            case kWRX0: sb = b.rho + c.eX; ss = 2; break;
+            case kWRX1: sb = b.rho + c.eX + 1; ss = 2; break;
+            case kWAX0: sb = b.alpha + c.eX; ss = 2; break;
+            case kWAX1: sb = b.alpha + c.eX + 1; ss = 2; break;
+            case kWZB: sb = b.zin + c.zB; ss = 0; break;
+            case kWUB: sb = b.uin + c.pB; ss = 1; break;
+            case kWRB: sb = b.rho + c.eB; ss = 1; break;
+            case kWZWX: sb = b.zw + c.zX; ss = 1; break;
+            case kWDEN: sb = c.wtab + 2 * (int64_t)c.n; ss = 1; break;
+            case kWZWW: sb = b.zw + c.zW; ss = D; break;
+            default: break;
+        }
+        s_sb[lane] = sb;
+        s_ss[lane] = ss;
+    }
+    __syncthreads();
+    double pp = 0.0, dd = 0.0;
+    unsigned bad = 0;                                   // 1 n, 2 x, 4 m, 8 z, 16 u
+    double* sc = s_sc[warp];
+    constexpr int32_t NW = kChainThreads / 32;
+#pragma unroll 1
+    for (int32_t i = i0 + warp; i < i1; i += NW) {
+        const double sv = s_sb[lane][(int64_t)i * s_ss[lane]];
+        __syncwarp();                                  // previous point's reads done
+        sc[lane] = sv;
+        __syncwarp();
+        chain_w_point<D>(b, c, i, lane, sc, &s_u[warp][0][lane], xb_out, pp, dd, bad);
+    }
+    if (bad & 1u) flag_error(b.ctrl, it - 1, FG_PHASE_N, true);
+    if (bad & 2u) flag_error(b.ctrl, it, FG_PHASE_X, true);
+    if (bad & 4u) flag_error(b.ctrl, it, FG_PHASE_M, false);
+    if (bad & 8u) flag_error(b.ctrl, it, FG_PHASE_Z, false);
+    if (bad & 16u) flag_error(b.ctrl, it, FG_PHASE_U, false);
     block_sum2<kChainThreads>(pp, dd, sm);
     if (threadIdx.x == 0) {
         b.part[2 * (part_off + blockIdx.x)] = pp;
@@ -455,8 +517,8 @@ __global__ void __launch_bounds__(kChainThreads, 2) k_svm_chain_fast(PassB b, Ch
 enum : int { kUY = 0, kUFN = 1, kULam = 2, kUZX = 3, kUUX0 = 4, kUUX1 = 5, kUZB = 6,
              kUUB = 7, kUXX = 8 };
 
-template <int D, int MINB>
-__global__ void __launch_bounds__(kChainThreads, MINB) k_svm_chain_unit(PassB b, ChainDev c,
+template <int D>
+__global__ void __launch_bounds__(kChainThreads, 4) k_svm_chain_unit(PassB b, ChainDev c,
                                                                     double* xb_out,
                                                                     int64_t part_off) {
     static_assert(D == 32, "one lane per component");
@@ -593,182 +655,19 @@ __global__ void __launch_bounds__(kChainThreads, MINB) k_svm_chain_unit(PassB b,
     }
 }
 
-// ---------------------------------------------------------------------------
-// Unit-weight form with a per-warp cp.async double buffer: while a warp
-// computes point i, the 9 rows point i + 8 reads from u and z (u slots
-// -1..3 and 6 of its w edges, z of w_{i-1..i+1}) are already in flight
-// into the warp's other buffer (16-byte cp.async.cg, L2 only: half a warp
-// per row), and its margin row and per-lane scalar into registers, so every
-// warp keeps one point's loads outstanding instead of stalling on them.
-// Needs 16-byte aligned u/z rows (pW, zW even; checked at plan time).
-// Arithmetic is k_svm_chain_unit's, operand for operand: bitwise equal.
-constexpr int kPfRows = 9;
-constexpr int kPfBuf = kPfRows * 32;                  // doubles per warp buffer
-
-__device__ __forceinline__ void chain_cp16(double* dst, const double* src) {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src));
-}
-
-template <int D, int MINB>
-__global__ void __launch_bounds__(kChainThreads, MINB) k_svm_chain_unit_pf(PassB b, ChainDev c,
-                                                                       double* xb_out,
-                                                                       int64_t part_off) {
-    static_assert(D == 32, "one lane per component");
-    __shared__ double sm[16];
-    __shared__ __align__(16) double s_pf[kChainThreads / 32][2][kPfBuf];
-    __shared__ double s_sc[kChainThreads / 32][32];
-    if (b.ctrl->stop) return;
-    const int64_t it = b.ctrl->iter;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int32_t nin = c.n - 2;
-    const int32_t per_cta = (nin + gridDim.x - 1) / gridDim.x;
-    const int32_t i0 = 1 + blockIdx.x * per_cta;
-    const int32_t i1 = min(c.n - 1, i0 + per_cta);
-    const double* sb = c.xx;
-    int32_t ss = 0;
-    switch (lane) {
-        case kUY: sb = c.fp_margin + D; ss = c.st_margin; break;
-        case kUFN: sb = c.fnorm; ss = 1; break;
-        case kULam: sb = c.fp_slack; ss = c.st_slack; break;
-        case kUZX: sb = b.zin + c.zX; ss = 1; break;
-        case kUUX0: sb = b.uin + c.pX; ss = 2; break;
-        case kUUX1: sb = b.uin + c.pX + 1; ss = 2; break;
-        case kUZB: sb = b.zin + c.zB; ss = 0; break;
-        case kUUB: sb = b.uin + c.pB; ss = 1; break;
-        case kUXX: sb = c.xx; ss = 1; break;
-        default: break;
-    }
-    const int h = lane >> 4, c2 = (lane & 15) * 2;
-    auto issue = [&](int32_t i, double* B) {
-        const double* U = b.uin + c.pW + (int64_t)(4 * i - 1) * D + c2;
-        const double* Z = b.zin + c.zW + (int64_t)i * D + c2;
-        chain_cp16(B + h * 32 + c2, U + (h ? 0 : -D));              // u rows -1, 0
-        chain_cp16(B + (2 + h) * 32 + c2, U + (h ? 2 * D : D));     // u rows 1, 2
-        chain_cp16(B + (4 + h) * 32 + c2, U + (h ? 6 * D : 3 * D)); // u rows 3, 6
-        chain_cp16(B + (6 + h) * 32 + c2, Z + (h ? 0 : -D));        // z rows -1, 0
-        if (!h) chain_cp16(B + 8 * 32 + c2, Z + D);                 // z row 1
-    };
-    double pp = 0.0, dd = 0.0;
-    bool bn = false, bx = false, bm = false, bz = false, bu = false;
-    auto S = [&](double v, int src) { return __shfl_sync(kFull, v, src); };
-    constexpr int32_t NW = kChainThreads / 32;
-    double* sc = s_sc[warp];
-    int k = 0;
-    double Xn = 0.0, svn = 0.0;
-    if (i0 + warp < i1) {
-        issue(i0 + warp, s_pf[warp][0]);
-        Xn = c.fp_margin[(int64_t)(i0 + warp) * c.st_margin + lane];
-        svn = sb[(int64_t)(i0 + warp) * ss];
-    }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-#pragma unroll 1
-    for (int32_t i = i0 + warp; i < i1; i += NW) {
-        const double X = Xn, sv = svn;
-        __syncwarp();                               // the other buffer's reads are done
-        if (i + NW < i1) {
-            issue(i + NW, s_pf[warp][k ^ 1]);
-            Xn = c.fp_margin[(int64_t)(i + NW) * c.st_margin + lane];
-            svn = sb[(int64_t)(i + NW) * ss];
-        }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-        sc[lane] = sv;
-        __syncwarp();
-        const double* B = s_pf[warp][k];
-        k ^= 1;
-        const double up = B[lane], u0 = B[32 + lane], u1 = B[64 + lane];
-        const double u2 = B[96 + lane], u3 = B[128 + lane], un_ = B[160 + lane];
-        const double zp = B[192 + lane], zi = B[224 + lane], zn_ = B[256 + lane];
-        const int64_t wo = c.pW + (int64_t)(4 * i - 1) * D + lane;
-        const int64_t zo = c.zW + (int64_t)i * D + lane;
-        // ---- phase n ----
-        const double n0 = zi - u0, n1 = zi - u1, n2 = zi - u2, n3 = zi - u3;
-        const double np_ = zp - up, nn_ = zn_ - un_;
-        const double zxi = sc[kUZX], ux0 = sc[kUUX0], ux1 = sc[kUUX1];
-        const double nb = sc[kUZB] - sc[kUUB], nx0 = zxi - ux0, nx1 = zxi - ux1;
-        const double sn = ((n0 + n1) + (n2 + n3)) + ((np_ + nn_) + ((nb + nx0) + nx1));
-        if (!finite(sn))
-            bn |= !(finite(n0) && finite(n1) && finite(n2) && finite(n3) && finite(np_) &&
-                    finite(nn_) && finite(nb) && finite(nx0) && finite(nx1));
-        // ---- phase x ----
-        const double x0 = sc[kUFN] * n0;                    // prox_svm_norm
-        const double pr = n1 * X;
-        const int g = lane & 7;
-        double dot = 0.0;
-        dot += S(pr, g);
-        dot += S(pr, g + 8);
-        dot += S(pr, g + 16);
-        dot += S(pr, g + 24);
-        dot += __shfl_xor_sync(kFull, dot, 1);
-        dot += __shfl_xor_sync(kFull, dot, 2);
-        dot += __shfl_xor_sync(kFull, dot, 4);
-        const double Y = sc[kUY];
-        const double slack = (1.0 - nx1) - Y * (dot + nb);
-        const double denom = (sc[kUXX] + 1.0) + 1.0;
-        const double mu = ddiv(np_max0(slack), denom);
-        const double x1 = n1 + (mu * Y) * X;
-        const double xbv = nb + mu * Y;
-        const double xx1 = nx1 + mu;
-        const double xx0 = np_max0(nx0 - sc[kULam]);       // prox_svm_slack
-        const double x2 = (np_ + n2) * 0.5;                    // prox_equality
-        const double x3 = (n3 + nn_) * 0.5;
-        // ---- phases m, z, u of w_i: z weight 4 ----
-        const double m0 = x0 + u0, m1 = x1 + u1, m2 = x2 + u2, m3 = x3 + u3;
-        double res = 0.0;
-        res += m1;
-        res += m2;
-        res += m3;
-        const double zn = (m0 + res) * 0.25;
-        b.z[zo] = zn;
-        const double dz = zn - zi;
-        const double t0 = x0 - zn, t1 = x1 - zn, t2 = x2 - zn, t3 = x3 - zn;
-        const double v0 = u0 + t0, v1 = u1 + t1, v2 = u2 + t2, v3 = u3 + t3;
-        double* __restrict__ UO = b.uout + wo;
-        UO[0] = v0; UO[D] = v1; UO[2 * D] = v2; UO[3 * D] = v3;
-        pp += t0 * t0; pp += t1 * t1; pp += t2 * t2; pp += t3 * t3;
-        const double dz2 = dz * dz;
-        dd += dz2; dd += dz2; dd += dz2; dd += dz2;
-        if (!finite((m0 + m1) + (m2 + m3))) {
-            const bool mbad = !(finite(m0) && finite(m1) && finite(m2) && finite(m3));
-            if (mbad) bx |= !(finite(x0) && finite(x1) && finite(x2) && finite(x3));
-            bm |= mbad;
-        }
-        bz |= !finite(zn);
-        if (!finite((v0 + v1) + (v2 + v3)))
-            bu |= !(finite(v0) && finite(v1) && finite(v2) && finite(v3));
-        // ---- xi_i (slack, margin; z weight 2) and b's margin x ----
-        if (lane == 0) {
-            const double mx0 = xx0 + ux0, mx1 = xx1 + ux1;
-            double rs = 0.0;
-            rs += mx1;
-            const double zx = (mx0 + rs) * 0.5;
-            b.z[c.zX + i] = zx;
-            const double dzx = zx - zxi;
-            const double s0 = xx0 - zx, s1 = xx1 - zx;
-            const double w0 = ux0 + s0, w1 = ux1 + s1;
-            b.uout[c.pX + 2 * (int64_t)i] = w0;
-            b.uout[c.pX + 2 * (int64_t)i + 1] = w1;
-            xb_out[c.pB + i] = xbv;
-            pp += s0 * s0; pp += s1 * s1;
-            dd += dzx * dzx; dd += dzx * dzx;
-            bx |= !(finite(xbv) && finite(xx0) && finite(xx1));
-            bm |= !(finite(mx0) && finite(mx1));
-            bz |= !finite(zx);
-            bu |= !(finite(w0) && finite(w1));
-        }
-    }
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    if (bn) flag_error(b.ctrl, it - 1, FG_PHASE_N, true);
-    if (bx) flag_error(b.ctrl, it, FG_PHASE_X, true);
-    if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
-    if (bz) flag_error(b.ctrl, it, FG_PHASE_Z, false);
-    if (bu) flag_error(b.ctrl, it, FG_PHASE_U, false);
-    block_sum2<kChainThreads>(pp, dd, sm);
-    if (threadIdx.x == 0) {
-        b.part[2 * (part_off + blockIdx.x)] = pp;
-        b.part[2 * (part_off + blockIdx.x) + 1] = dd;
-    }
+// Per-point tables of the weighted form (fg_chain.cuh k_svm_chain_w), rebuilt
+// at every parameter sync with the generic form's operations:
+//   wtab[i]       = rho0 / (rho0 + scale_i)                 (prox_svm_norm)
+//   wtab[n + i]   = lam_i / rho_x0                          (prox_svm_slack)
+//   wtab[2n + i]  = (x.x / rho1 + 1 / rho_b) + 1 / rho_x1  (margin denominator)
+__global__ void k_chain_wtab(ChainDev c, const double* __restrict__ rho, double* wtab) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= c.n || i == 0 || i == c.n - 1) return;     // interior points only
+    const double* r = rho + c.eW - 1 + 4 * i;
+    const double rx0 = rho[c.eX + 2 * i], rx1 = rho[c.eX + 2 * i + 1], rb = rho[c.eB + i];
+    wtab[i] = ddiv(r[0], r[0] + c.fp_norm[i * c.st_norm]);
+    wtab[c.n + i] = ddiv(c.fp_slack[i * c.st_slack], rx0);
+    wtab[2 * c.n + i] = (ddiv(c.xx[i], r[1]) + ddiv(1.0, rb)) + ddiv(1.0, rx1);
 }
 
 // 1 / (1 + scale_i): prox_svm_norm's factor at unit edge weight

@@ -259,13 +259,13 @@ struct fg_plan {
     int64_t mpc_fault = 0;             // test hook: a block reports a failure at this iteration
     ChainDev chain{};
     int64_t chain_grid = 0;
-    int chain_minb = 2;                // CTAs/SM the kernel is compiled for (A/B)
-    bool chain_pf = false;             // unit chain with cp.async prefetch (A/B)
-    bool chain_fast = false;           // D == 32: fast form for interior points
+    bool chain_fast = false;           // D == 32: unit / weighted forms for interior points
+    bool chain_wok = false;            // weighted form usable (per-variable z weights)
     bool chain_unit = false;           // all weights 1 (checked at every sync)
     bool giant_unit = false;           // every rho and alpha 1: giant kernels skip them
     double* d_chain_xx = nullptr;      // per point x.x of the margin data
     double* d_chain_fnorm = nullptr;   // per point 1/(1+scale) (unit form)
+    double* d_chain_wtab = nullptr;    // 3 x n per-point tables (weighted form)
     int32_t* d_flag = nullptr;         // scratch device flag
     unsigned long long* d_bad = nullptr;  // first non-finite ref index of a download
     int32_t* h_stop = nullptr;         // pinned stop-flag slots polled by fg_run
@@ -337,7 +337,7 @@ fg_plan::~fg_plan() {
                     d_clprog[2], d_clprog[3], d_clprog[4],
                     d_llist, d_lprog, d_prog, d_glist, d_gchunks, d_gcomps,
                     d_gwork, d_gcref, d_gwref, d_csum, d_gz, d_part, d_res2, d_ctrl, d_hist, d_chain_xx,
-                    d_chain_fnorm, d_flag, d_bad, d_gcnt, d_ucnt, d_lexc[1], d_lexc[2], d_lexc[3],
+                    d_chain_fnorm, d_chain_wtab, d_flag, d_bad, d_gcnt, d_ucnt, d_lexc[1], d_lexc[2], d_lexc[3],
                     d_lexc[4], d_row2[1], d_row2[2], d_row2[3], d_row2[4],
                     d_planoff[1], d_planoff[2], d_planoff[3], d_planoff[4], d_plans,
                     d_rowdesc[1], d_rowdesc[2], d_rowdesc[3], d_rowdesc[4],
@@ -775,15 +775,19 @@ void part_post(fg_plan* p, cudaStream_t st) {
 }
 
 // fused SVM chain: one kernel for the edge pass and the w/xi variables ...
-// CTAs of the chain kernel for interior points: one resident wave (the
-// kernels loop over their points), at most the partial slots it replaces
-// minus the end-point slot.
-constexpr bool kChainPfDefault = false;
+// interior points on the unit-weight or the weighted form (D = 32), the
+// two end points on the generic form; else every point on the generic form
+bool chain_split(const fg_plan* p) {
+    return p->chain_fast && (p->chain_unit || p->chain_wok);
+}
 
+// CTAs of the chain kernel for interior points: one resident wave (the
+// kernels loop over their points; 4 CTAs/SM for the unit and weighted
+// forms, 2 for the generic one), at most the partial slots it replaces
+// minus the end-point slot.
 int64_t chain_main_grid(const fg_plan* p) {
     if (p->mpc_chain) return p->mpc_tiles - 1;   // the MPC chain writes mpc_tiles slots
-    const int64_t wave = p->chain_fast
-        ? (p->chain_unit ? 148 * (p->chain_minb == 5 ? 5 : 4) : 148 * 2) : 148 * 2;
+    const int64_t wave = chain_split(p) ? 148 * (p->chain_unit ? 4 : FG_CHAIN_W_MINB) : 148 * 2;
     return std::max<int64_t>(1, std::min(wave, p->chain_grid - 1));
 }
 
@@ -803,20 +807,14 @@ void chain_pass(fg_plan* p, int in, cudaStream_t st) {
         return;
     }
     const unsigned G = (unsigned)chain_main_grid(p);
-    if (p->chain_fast) {
+    if (chain_split(p)) {
         cudaEventRecord(p->ev_fork, st);
-        // interior points on the fast (or unit-weight) form, the two end
+        // interior points on the unit-weight or weighted form, the two end
         // points (degree 3) on the generic form in the next partial slot
-        if (p->chain_unit && p->chain_pf)
-            k_svm_chain_unit_pf<32, 4><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
-        else if (p->chain_unit && p->chain_minb == 5)
-            k_svm_chain_unit<32, 5><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
-        else if (p->chain_unit && p->chain_minb == 3)
-            k_svm_chain_unit<32, 3><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
-        else if (p->chain_unit)
-            k_svm_chain_unit<32, 4><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
+        if (p->chain_unit)
+            k_svm_chain_unit<32><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
         else
-            k_svm_chain_fast<32><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
+            k_svm_chain_w<32><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
         // the two end points run on a forked stream, concurrently with the
         // interior (a parallel branch when captured into a CUDA graph)
         cudaStreamWaitEvent(p->stream2, p->ev_fork, 0);
@@ -824,8 +822,6 @@ void chain_pass(fg_plan* p, int in, cudaStream_t st) {
                                                               p->chain.n, p->chain.n - 1);
         cudaEventRecord(p->ev_join, p->stream2);
         cudaStreamWaitEvent(st, p->ev_join, 0);
-    } else if (p->chain_minb == 3) {
-        k_svm_chain<3><<<G + 1, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0, 0, p->chain.n, 1);
     } else {
         k_svm_chain<2><<<G + 1, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0, 0, p->chain.n, 1);
     }
@@ -1035,25 +1031,14 @@ void detect_svm_chain(fg_plan* p, const std::vector<int32_t>& dim,
     c.fp_margin = gm->dev.fp; c.st_margin = gm->dev.fstride;
     // one CTA per partial slot of the small classes it replaces
     p->chain_grid = p->nsblk[0] + p->nsblk[1] + p->nsblk[2];
-    // CTAs/SM the kernels are compiled for (A/B in profiles/): generic form
-    // 2 (3 spills heavily); unit form 4 (0.59 ms vs 0.67 ms at 3, SVM 1M)
-    p->chain_minb = getenv("FGADMM_CHAIN_OCC3") ? 3 : getenv("FGADMM_CHAIN_OCC5") ? 5 : 2;
-    // unit form with the per-warp cp.async double buffer (A/B)
-    {
-        const char* e = getenv("FGADMM_CHAIN_PF");
-        p->chain_pf = e ? e[0] == '1' : kChainPfDefault;
-        // 16-byte cp.async rows: w's payload and z bases must be even
-        p->chain_pf = p->chain_pf && (c.pW % 2 == 0) && (c.zW % 2 == 0);
-    }
-    if (p->chain_pf)
-        cudaFuncSetAttribute(k_svm_chain_unit_pf<32, 4>,
-                             cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (cudaMalloc((void**)&p->d_chain_xx, n * sizeof(double)) != cudaSuccess) return;
     c.xx = p->d_chain_xx;
     k_chain_xx<<<(unsigned)((n + 255) / 256), 256, 0, p->stream>>>(c, p->d_chain_xx);
     if (cudaMalloc((void**)&p->d_chain_fnorm, n * sizeof(double)) != cudaSuccess) return;
     c.fnorm = p->d_chain_fnorm;
     k_chain_fnorm<<<(unsigned)((n + 255) / 256), 256, 0, p->stream>>>(c, p->d_chain_fnorm);
+    if (cudaMalloc((void**)&p->d_chain_wtab, 3 * n * sizeof(double)) != cudaSuccess) return;
+    c.wtab = p->d_chain_wtab;
     if (cudaStreamSynchronize(p->stream) != cudaSuccess) return;
     p->chain_fast = D == 32 && n >= 3 && p->chain_grid >= 2 && !getenv("FGADMM_CHAIN_GENERIC");
     p->chain_on = p->chain_grid > 0;
@@ -1416,6 +1401,17 @@ int fg_device_count(int32_t* count) {
     if (e != cudaSuccess) { *count = 0; return fail(FG_ERR_CUDA, cudaGetErrorString(e)); }
     *count = n;
     return 0;
+}
+
+// launches per fused SVM-chain iteration: the chain kernel(s), the giant
+// kernels of b and the reduction (re-counted when the form changes at sync)
+int64_t svm_chain_launches(const fg_plan* p) {
+    int64_t n = chain_split(p) ? 2 : 1;
+    int last = -1;
+    for (int w = 0; w < kVarSlots; ++w)
+        if (chain_rest_slot(w) && var_slot_blocks(p, w) > 0) { ++n; last = w; }
+    if (!(last == kSlotGiantUpdate && p->giant_fused)) ++n;   // separate reduce
+    return n;
 }
 
 int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
@@ -1933,14 +1929,7 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     CK(cudaMemset(p->d_part, 0, 2 * std::max(p->npart, nres) * sizeof(double)));
     p->launches_per_iter = count_edge_launches(p.get()) + count_var_launches(p.get()) + 1;
     p->launches_later = p->launches_per_iter;
-    if (p->chain_on) {
-        int64_t n = p->chain_fast ? 2 : 1;               // chain kernel(s)
-        int last = -1;
-        for (int w = 0; w < kVarSlots; ++w)
-            if (chain_rest_slot(w) && var_slot_blocks(p.get(), w) > 0) { ++n; last = w; }
-        if (!(last == kSlotGiantUpdate && p->giant_fused)) ++n;   // separate reduce
-        p->launches_later = n;
-    }
+    if (p->chain_on) p->launches_later = svm_chain_launches(p.get());
     CK(cudaDeviceSynchronize());
     *out = p.release();
     return 0;
@@ -1949,7 +1938,7 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
 void fg_plan_destroy(fg_plan* plan) { delete plan; }
 
 int fg_plan_forms(const fg_plan* p, int32_t* o) {
-    o[0] = p->chain_on ? (p->mpc_chain ? 4 : (p->chain_unit ? 3 : (p->chain_fast ? 2 : 1))) : 0;
+    o[0] = p->chain_on ? (p->mpc_chain ? 4 : (p->chain_unit ? 3 : (chain_split(p) ? 2 : 1))) : 0;
     o[1] = 0;
     o[6] = 0;
     for (auto& g : p->groups) {
@@ -1968,7 +1957,7 @@ int fg_plan_info(const fg_plan* p, int64_t* o) {
     o[8] = p->launches_per_iter;
     o[9] = p->launches_later;
     o[10] = p->chain_on ? 1 : 0;
-    o[11] = p->chain_on ? (p->chain_unit ? 3 : (p->chain_fast ? 2 : 1)) : 0;
+    o[11] = p->chain_on ? (p->chain_unit ? 3 : (chain_split(p) ? 2 : 1)) : 0;
     return 0;
 }
 
@@ -2029,8 +2018,18 @@ int fg_plan_sync_params(fg_plan* p, const double* rho, const double* alpha,
         for (int64_t i = 1; i + 1 < c.n && unit; ++i)
             for (int k = 0; k < c.D && unit; ++k) unit = zw[c.zW + i * c.D + k] == 4.0;
         for (int64_t i = 0; i < c.n && unit; ++i) unit = zw[c.zX + i] == 2.0;
-        if (unit != p->chain_unit) {
+        // weighted form: w_i's z weight is one value for all D components
+        // (z_weights sums the per-edge rho_flat, graph.py:216-222); its
+        // per-point tables follow the weights just uploaded
+        bool wok = !unit;
+        for (int64_t i = 1; i + 1 < c.n && wok; ++i)
+            for (int k = 1; k < c.D && wok; ++k) wok = zw[c.zW + i * c.D + k] == zw[c.zW + i * c.D];
+        if (wok)
+            k_chain_wtab<<<(unsigned)((c.n + 255) / 256), 256, 0, st>>>(c, p->d_rho, p->d_chain_wtab);
+        if (unit != p->chain_unit || wok != p->chain_wok) {
             p->chain_unit = unit;
+            p->chain_wok = wok;
+            if (p->chain_on && !p->mpc_chain) p->launches_later = svm_chain_launches(p);
             for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
             p->graphs.clear();
         }
@@ -3379,4 +3378,126 @@ extern "C" int fg_evaluate(fg_plan* p, const double* z_host, double* out2) {
     out2[0] = obj;
     out2[1] = vio;
     return check_launch();
+}
+
+// ---- weighted null-space projection (three-weight mpc_dyn_prox) -----------
+// operators.py:86-96 _weighted_nullspace_projection for one shared M:
+// v = nv - W^-1 M^T S^-1 M nv, S = M W^-1 M^T, per row of (nv, w).  One CTA
+// per row: S and M nv in shared memory (products in einsum's order), S
+// solved by LU with partial pivoting (LAPACK gesv's pivot rule) on one
+// thread -- r is the state dimension (<= 64), so the solve is tiny.
+__global__ void k_wproj(const double* __restrict__ M, int r, int D,
+                        const double* __restrict__ nv, const double* __restrict__ w,
+                        double* __restrict__ out, int* bad) {
+    extern __shared__ double sh[];
+    double* S = sh;                  // r x r
+    double* lam = S + r * r;         // r (M nv, then the solution)
+    double* winv = lam + r;          // D
+    const double* n = nv + (int64_t)blockIdx.x * D;
+    const double* wr = w + (int64_t)blockIdx.x * D;
+    for (int j = threadIdx.x; j < D; j += blockDim.x) winv[j] = 1.0 / wr[j];
+    __syncthreads();
+    for (int t = threadIdx.x; t < r * r + r; t += blockDim.x) {
+        double acc = 0.0;
+        if (t < r * r) {
+            const int i = t / r, k = t - (t / r) * r;
+            for (int j = 0; j < D; ++j) acc += (M[i * D + j] * winv[j]) * M[k * D + j];
+            S[t] = acc;
+        } else {
+            const int i = t - r * r;
+            for (int j = 0; j < D; ++j) acc += M[i * D + j] * n[j];
+            lam[i] = acc;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int c = 0; c < r; ++c) {
+            int p = c;
+            for (int i = c + 1; i < r; ++i)
+                if (fabs(S[i * r + c]) > fabs(S[p * r + c])) p = i;
+            if (S[p * r + c] == 0.0) { *bad = 1; break; }
+            if (p != c) {
+                for (int k = 0; k < r; ++k) {
+                    const double t = S[c * r + k]; S[c * r + k] = S[p * r + k]; S[p * r + k] = t;
+                }
+                const double t = lam[c]; lam[c] = lam[p]; lam[p] = t;
+            }
+            for (int i = c + 1; i < r; ++i) {
+                const double f = S[i * r + c] / S[c * r + c];
+                for (int k = c + 1; k < r; ++k) S[i * r + k] -= f * S[c * r + k];
+                lam[i] -= f * lam[c];
+            }
+        }
+        for (int c = r - 1; c >= 0; --c) {
+            double s = lam[c];
+            for (int k = c + 1; k < r; ++k) s -= S[c * r + k] * lam[k];
+            lam[c] = s / S[c * r + c];
+        }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < D; j += blockDim.x) {
+        double acc = 0.0;
+        for (int i = 0; i < r; ++i) acc += M[i * D + j] * lam[i];
+        out[(int64_t)blockIdx.x * D + j] = n[j] - winv[j] * acc;
+    }
+}
+
+int fg_wproj(const double* M, int32_t r, int32_t D, const double* nv, const double* w,
+             int64_t rows, double* out, int32_t device) {
+    if (r < 1 || D < r || r > 64 || D > 4096 || rows < 0)
+        return fail(FG_ERR_INVALID, "fg_wproj: need 1 <= r <= 64, r <= D <= 4096");
+    if (rows == 0) return 0;
+    for (int64_t i = 0; i < rows * D; ++i)
+        if (!(w[i] > 0.0)) return fail(FG_ERR_INVALID, "weights must be positive");
+    CK(cudaSetDevice(device));
+    double *dM, *dn, *dw, *dout;
+    int* dbad;
+    int rc;
+    if ((rc = dalloc(&dM, (int64_t)r * D)) || (rc = dalloc(&dn, rows * D)) ||
+        (rc = dalloc(&dw, rows * D)) || (rc = dalloc(&dout, rows * D)) || (rc = dalloc(&dbad, 1)))
+        return rc;
+    CK(cudaMemcpy(dM, M, (size_t)r * D * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dn, nv, (size_t)rows * D * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dw, w, (size_t)rows * D * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemset(dbad, 0, sizeof(int)));
+    const size_t smem = ((size_t)r * r + r + D) * sizeof(double);
+    k_wproj<<<(unsigned)rows, 128, smem>>>(dM, r, D, dn, dw, dout, dbad);
+    cudaError_t e = cudaDeviceSynchronize();
+    int hbad = 0;
+    if (e == cudaSuccess) e = cudaMemcpy(out, dout, (size_t)rows * D * sizeof(double),
+                                         cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(&hbad, dbad, sizeof(int), cudaMemcpyDeviceToHost);
+    cudaFree(dM); cudaFree(dn); cudaFree(dw); cudaFree(dout); cudaFree(dbad);
+    if (e != cudaSuccess) return fail(FG_ERR_CUDA, cudaGetErrorString(e));
+    if (hbad) return fail(FG_ERR_NONFINITE, "Singular matrix");
+    return 0;
+}
+
+// ---- self-test of the inline division (fg_device.cuh qdiv) --------------
+__global__ void k_div_pair(const double* x, const double* y, int64_t n, double* q,
+                           double* ref) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    q[i] = qdiv(x[i], y[i]);
+    ref[i] = x[i] / y[i];
+}
+
+int fg_selftest_div(const double* x, const double* y, int64_t n, double* q, double* ref,
+                    int32_t device) {
+    if (n <= 0) return 0;
+    CK(cudaSetDevice(device));
+    double *dx, *dy, *dq, *dr;
+    int rc;
+    if ((rc = dalloc(&dx, n)) || (rc = dalloc(&dy, n)) || (rc = dalloc(&dq, n)) ||
+        (rc = dalloc(&dr, n)))
+        return rc;
+    CK(cudaMemcpy(dx, x, n * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dy, y, n * sizeof(double), cudaMemcpyHostToDevice));
+    k_div_pair<<<(unsigned)((n + 255) / 256), 256>>>(dx, dy, n, dq, dr);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(q, dq, n * sizeof(double), cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(ref, dr, n * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(dx); cudaFree(dy); cudaFree(dq); cudaFree(dr);
+    if (e != cudaSuccess) return fail(FG_ERR_CUDA, cudaGetErrorString(e));
+    return 0;
 }

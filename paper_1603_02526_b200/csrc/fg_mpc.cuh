@@ -251,6 +251,7 @@ __global__ void __launch_bounds__(kEdgeThreads, N0 > 0 ? 4 : 3) k_mpc_chain(Pass
     __shared__ int s_last;
     if (b.ctrl->stop) return;
     const int64_t it = b.ctrl->iter;
+    const double r3 = qdiv_rcp(3.0);                    // z = S / 3 without the runtime call
     const int n0 = N0 > 0 ? N0 : c.n0, d = N0 > 0 ? DD : c.d;
     const int cols = n0 + d, ld = cols + 1, ldo = 2 * n0 + 1;
     constexpr int KH = kMpcKH, RG = kMpcRG;
@@ -396,7 +397,7 @@ __global__ void __launch_bounds__(kEdgeThreads, N0 > 0 ? 4 : 3) k_mpc_chain(Pass
             }
         }
         S = S + res;
-        const double zn = ddiv(S, (double)deg);
+        const double zn = deg == 3 ? qdiv_r(S, 3.0, r3) : S * 0.5;   // z weights 3 / 2
         bz |= !finite(zn);
         zout[zo] = zn;
         const double dz = zn - zi;

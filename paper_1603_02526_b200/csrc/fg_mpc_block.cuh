@@ -91,6 +91,7 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mpc_block(PassB b, MpcChainDe
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
     const int64_t it0 = b.ctrl->iter;
+    const double r3 = qdiv_rcp(3.0);                    // z = S / 3 without the runtime call
     bool bad = false;
     for (int i = 0; i < KB; ++i) {
         // ---- n of the dynamics factors (k_mpc_chain's staging) ----
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mpc_block(PassB b, MpcChainDe
                 }
             }
             S = S + res;
-            const double zn = ddiv(S, (double)deg);
+            const double zn = deg == 3 ? qdiv_r(S, 3.0, r3) : S * 0.5;   // z weights 3 / 2
             bb |= !finite(zn);
             zs[tl * n0 + q] = zn;
             const double dz = zn - zi;

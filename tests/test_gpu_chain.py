@@ -62,12 +62,10 @@ def test_chain_bitwise_equals_generic(gpu, monkeypatch, n, dim, iters):
     assert rc[0].kernel_launches < rg[0].kernel_launches
 
 
-@pytest.mark.parametrize("env", [{"FGADMM_CHAIN_PF": "1"}, {"FGADMM_CHAIN_PF": "0"},
-                                 {"FGADMM_CHAIN_OCC3": "1", "FGADMM_CHAIN_PF": "0"},
-                                 {"FGADMM_CHAIN_OCC5": "1", "FGADMM_CHAIN_PF": "0"}])
-def test_chain_variants_bitwise(gpu, monkeypatch, env):
-    """Compiled variants of the unit-weight chain (cp.async prefetch
-    buffer, occupancy) equal the generic path bitwise."""
+@pytest.mark.parametrize("env", [{}, {"FGADMM_CHAIN_NO_UNIT": "1"}, {"FGADMM_CHAIN_GENERIC": "1"}])
+def test_chain_forms_bitwise(gpu, monkeypatch, env):
+    """Every form of the chain on unit weights (unit, weighted, generic)
+    equals the per-kind path bitwise."""
     g = svm_graph(20_000, 32, seed=9)
     st = fg.init_state(g, seed=2)
     outs = []
@@ -78,7 +76,8 @@ def test_chain_variants_bitwise(gpu, monkeypatch, env):
         s = copy(st)
         fg.run(g, fg.RunConfig(max_iterations=11), state=s)
         if chain:
-            assert _PLANS[g].chain_form() == "unit"
+            want = {"FGADMM_CHAIN_NO_UNIT": "fast", "FGADMM_CHAIN_GENERIC": "generic"}
+            assert _PLANS[g].chain_form() == next((want[k] for k in env), "unit")
         outs.append(s)
     for k in "xmzun":
         np.testing.assert_array_equal(getattr(outs[0], k), getattr(outs[1], k), err_msg=k)
@@ -156,14 +155,36 @@ def test_chain_profile_labels(gpu, monkeypatch):
 
 @pytest.mark.parametrize("rho,alpha", [(2.0, 1.0), (1.0, 1.5), (0.7, 1.3)])
 def test_chain_general_weights_bitwise(gpu, monkeypatch, rho, alpha):
-    """Non-unit weights take the general fast form (weights loaded per
-    edge); it stays bitwise equal to the per-kind path."""
+    """Non-unit weights take the weighted form (weights loaded per point,
+    per-point division tables); it stays bitwise equal to the per-kind
+    path."""
     X, y = fg.gen_gaussian_arrays(3000, 32, 4.0, seed=12)
     g = fg.build_svm(fg.SvmSpec.from_arrays(X, y, rho=rho, alpha=alpha))
     st = fg.init_state(g, seed=6)
     (sc, _), (sg, _) = run_both(g, st, monkeypatch, [fg.RunConfig(max_iterations=8)])
     for k in "xmzun":
         np.testing.assert_array_equal(getattr(sc, k), getattr(sg, k), err_msg=k)
+
+
+def test_chain_random_edge_weights_bitwise_and_oracle(gpu, monkeypatch):
+    """Every edge its own rho and alpha (set_edge_params on a sample, the
+    three-weight use case of PAPER.md:130): the weighted chain is bitwise the
+    per-kind path and within 1e-9 of the oracle."""
+    X, y = fg.gen_gaussian_arrays(1500, 32, 4.0, seed=21)
+    g = fg.build_svm(fg.SvmSpec.from_arrays(X, y, rho=1.3, alpha=0.9))
+    rng = np.random.default_rng(4)
+    for e in rng.choice(len(g.edge_var), 3000, replace=False):
+        g.set_edge_params(int(e), float(rng.uniform(0.3, 3.0)), float(rng.uniform(0.5, 1.7)))
+    st = fg.init_state(g, seed=8)
+    (sc, _), (sg, _) = run_both(g, st, monkeypatch, [fg.RunConfig(max_iterations=9)])
+    plan_for(g, monkeypatch, True).sync(g)
+    assert _PLANS[g].chain_form() == "fast"
+    for k in "xmzun":
+        np.testing.assert_array_equal(getattr(sc, k), getattr(sg, k), err_msg=k)
+    so, _h, _ = O.run(g, 9, st)
+    for k in "xmzun":
+        a, b = getattr(sc, k), getattr(so, k)
+        assert float(np.max(np.abs(a - b))) <= REL * max(1.0, float(np.max(np.abs(b)))), k
 
 
 def test_chain_unit_form_follows_set_edge_params(gpu, monkeypatch):

@@ -1,8 +1,9 @@
 #!/bin/bash
-# weighted SVM chain + inline division: tests, benches, ncu of the weighted kernel
+# weighted SVM chain + MPC inline z division: tests and benches
 set -u
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_division.py tests/test_gpu_chain.py tests/test_gpu_api.py -x -q > gpurun_out/pytest_chain.log 2>&1; echo "pytest rc=$?"; tail -15 gpurun_out/pytest_chain.log
-bash tools/quickbench.sh svm1m svm1m_rho2 svm1m_w
-ncu --set full --clock-control none --import-source on -k "regex:k_svm_chain_w" -s 2 -c 1 \
-    -o gpurun_out/r02_chain_w -f python bench.py --workload svm1m_w --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/r02_chain_w.log 2>&1; echo "ncu chain_w rc=$?"
+timeout 900 python -m pytest tests/test_gpu_division.py tests/test_gpu_chain.py tests/test_gpu_mpc_block.py -x -q > gpurun_out/pytest_chain.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_chain.log
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "mpc" > gpurun_out/pytest_mpc.log 2>&1; echo "pytest mpc rc=$?"; tail -2 gpurun_out/pytest_mpc.log
+bash tools/quickbench.sh svm1m_rho2 svm1m_w mpc100k
+FGADMM_MPC_BLOCK=0 timeout 300 python bench.py --workload mpc100k --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/bench_mpc_noblock.json 2>/dev/null
+python -c "import json; d=json.load(open('gpurun_out/bench_mpc_noblock.json')); print('mpc noblock', d['value'], d['ms_per_step'], {k:round(v['ms_avg'],4) for k,v in d['kernels'].items()})"
