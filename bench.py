@@ -110,13 +110,9 @@ def kernel_bytes(graph, plan):
     giant = (deg - 1) > chunk
     sel_by_key = [("var_small_deg4", deg <= 4), ("var_small_deg8", (deg > 4) & (deg <= 8)),
                   ("var_small_loop", small & (deg > 8))]
-    # the 4-CTA cluster kernel is opt-in (FGADMM_CLUSTER=1) for degree >= 1024
-    cl_min = 1024 if os.environ.get("FGADMM_CLUSTER") else 1 << 62
     for d in (1, 2, 3, 4):
-        sel_by_key.append((f"var_large_d{d}", large & (dims == d) & (deg < cl_min)))
+        sel_by_key.append((f"var_large_d{d}", large & (dims == d)))
     sel_by_key.append(("var_large_comp", large & (dims > 4)))
-    for d in (1, 2, 3, 4):
-        sel_by_key.append((f"var_cluster_d{d}", large & (dims == d) & (deg >= cl_min)))
     for key, sel in sel_by_key:
         if sel.any():
             P = int(np.sum(deg[sel] * dims[sel]))
@@ -128,7 +124,6 @@ def kernel_bytes(graph, plan):
         P = int(np.sum(deg[giant] * dims[giant]))
         E = int(np.sum(deg[giant]))
         out["var_giant_chunks"] = P * 16 + E * 8
-        out["var_giant_top"] = int(np.sum(dims[giant])) * 24
         out["var_giant_update"] = P * 24 + E * 16
     out["reduce"] = 16 * (plan.info["small_components"] // 256 + 1
                           + plan.info["large_components"] + 64)
@@ -474,13 +469,15 @@ def reference_arm(args):
 def points_per_rank(args, world):
     """SVM points per rank of the weak-scaled run: --points-per-rank, else
     configs[4]'s 8M per GPU (64M at 8 GPUs) when the host can hold every
-    local rank's graph and state (measured 78 GB host RSS per rank at 8M
-    points before the page-locked state copy), else the largest whole million that fits (at least 1M)."""
+    local rank's graph and state (~8.5 KB per point, ~68 GB per rank at 8M
+    points), else the largest whole million that fits (at least 1M)."""
     if args.points_per_rank:
         return args.points_per_rank
-    # peak host bytes per point: graph build (~9.8 KB measured) plus the
-    # page-locked state copy made before the pageable one is freed
-    target, per_point = 8_000_000, 16_000
+    # peak host bytes per point: the rank graph (~1.5 KB measured; the
+    # per-payload zmap / rho_flat / alpha_flat are never built) plus the
+    # page-locked five-array state (~5.2 KB) and the plan's transient
+    # layout maps (~1.5 KB)
+    target, per_point = 8_000_000, 8_500
     try:
         import psutil
         avail = psutil.virtual_memory().available
@@ -705,12 +702,20 @@ def main():
     P, Z = g.total_edge_payload, g.z_dim
     h2d = (Z + 2 * P) * 8 + 2 * E * 8 * 0
     d2h = (4 * P + Z) * 8
+    loop_s = ms / 1e3                              # device time of the same iterations
+    xfer_s = max(e2e_s - loop_s, 1e-9)
     e2e = {"value": E * args.steps * world / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
            "runs_s": [round(v, 4) for v in e2e_runs],
+           "device_loop_s": round(loop_s, 5),
+           "host_transfer_GBps": round((h2d + d2h) / xfer_s / 1e9, 1),
+           "bound": "pcie",
            "note": f"one run() call of {args.steps} iterations on a pinned host "
                    f"AdmmState: upload z,u,n, download x,m,z,u,n (bytes amortized "
-                   f"per step); wall clock, median of 3 calls"}
+                   f"per step); wall clock, median of 3 calls.  Transfer-dominated: "
+                   f"{(h2d + d2h) / 1e9:.2f} GB cross PCIe per call against "
+                   f"{loop_s * 1e3:.1f} ms of device loop; host_transfer_GBps is "
+                   f"the call's bytes over its non-loop time"}
 
     if rank != 0:
         if dist:

@@ -53,7 +53,6 @@ struct GroupDev {
     const struct DiskRow* disks;
     const int2* tiles;                   // (bi, bj), bi <= bj
     int32_t ndisks, ntiles;
-    int32_t variant;                     // tile kernel flavour (FGADMM_COLLISION)
     // rows affine in the disk index (every packing graph): row i = row0 +
     // i * rowS field by field, so the tile kernel computes addresses
     int32_t rows_affine, rows_even;      // rows_even: center rows 16-byte aligned
@@ -322,261 +321,28 @@ __global__ void __launch_bounds__(kEdgeThreads, 4) k_svm_margin(PassA a, GroupDe
     passa_flags<FIRST>(a, it, bn, bx);
 }
 
-// ---- mpc_dyn: one warp per factor (operators.py:86-96, 390-404) ---------
+// ---- mpc_dyn limits (operators.py:86-96, 390-404; kernels in fg_mpc.cuh) --
 // Weighted projection onto {M v = 0}, M = [I+A, B, -I] (d x (2d+k)).
 // With W = diag(rho0 on slot 0, rho1 on the first d of slot 1),
 // S = M W^-1 M^T = G/rho0 + I/rho1, G = QLQ^T precomputed per system, so
 // S^-1 = Q diag(1/(L/rho0 + 1/rho1)) Q^T (replaces the per-factor LAPACK
 // gesv; parity 1e-9 rel).  Table entry: M row-major, Q row-major, L.
 constexpr int kDynMaxD = 32, kDynMaxCols = 96;
-constexpr int kDynWarps = kEdgeThreads / 32;
-template <bool FIRST>
-__global__ void __launch_bounds__(kEdgeThreads) k_mpc_dyn(PassA a, GroupDev g) {
-    __shared__ double s_nv[kDynWarps][kDynMaxCols];
-    __shared__ double s_v1[kDynWarps][kDynMaxD];
-    __shared__ double s_v2[kDynWarps][kDynMaxD];
-    if (a.ctrl->stop) return;
-    const int w = threadIdx.x >> 5;
-    const int64_t it = a.ctrl->iter;
-    const int n0 = g.dim[0];
-    const int d = g.ip;                       // state dim
-    const int cols = n0 + d;                  // 2d + k
-    bool bn = false, bx = false;
-    for_each_item(g, [&](const FRef& r, int lane) {   // warp-uniform
-        const SlotLoc s0 = locate(a.vt, g, 0, r), s1 = locate(a.vt, g, 1, r);
-        const double* T = g.tab + (int64_t)(g.fsys ? g.fsys[r.f] : 0) * g.tstride;
-        const double* M = T;
-        const double* Q = T + d * cols;
-        const double* L = Q + d * d;
-        for (int c = lane; c < cols; c += 32)
-            s_nv[w][c] = (c < n0) ? nval<FIRST>(a, s0, c, bn)
-                                  : nval<FIRST>(a, s1, c - n0, bn);
-        __syncwarp();
-        const double R0 = a.rho[s0.q], R1 = a.rho[s1.q];
-        if (lane < d) {                           // Mnv
-            double acc = 0.0;
-            for (int c = 0; c < cols; ++c) acc += M[lane * cols + c] * s_nv[w][c];
-            s_v1[w][lane] = acc;
-        }
-        __syncwarp();
-        if (lane < d) {                           // y = diag * Q^T Mnv
-            double acc = 0.0;
-            for (int q = 0; q < d; ++q) acc += Q[q * d + lane] * s_v1[w][q];
-            s_v2[w][lane] = ddiv(acc, ddiv(L[lane], R0) + ddiv(1.0, R1));
-        }
-        __syncwarp();
-        if (lane < d) {                           // lambda = Q y
-            double acc = 0.0;
-            for (int i = 0; i < d; ++i) acc += Q[lane * d + i] * s_v2[w][i];
-            s_v1[w][lane] = acc;
-        }
-        __syncwarp();
-        for (int c = lane; c < cols; c += 32) {   // v = nv - W^-1 M^T lambda
-            double acc = 0.0;
-            for (int q = 0; q < d; ++q) acc += M[q * cols + c] * s_v1[w][q];
-            const double winv = ddiv(1.0, (c < n0) ? R0 : R1);
-            const double v = s_nv[w][c] - winv * acc;
-            if (c < n0) xput(a, s0.pos + c, v, bx);
-            else xput(a, s1.pos + (c - n0), v, bx);
-        }
-        for (int c = d + lane; c < n0; c += 32)   // slot-1 control passes through
-            xput(a, s1.pos + c, nval<FIRST>(a, s1, c, bn), bx);
-        __syncwarp();
-    });
-    passa_flags<FIRST>(a, it, bn, bx);
-}
 
 // ---- collision, all-pairs tiles (packing) --------------------------------
 // One CTA per 32x32 tile (bi <= bj) of the i<j pair triangle.  Pair (i, j)
 // has its i-half in row i at entry j-1 and its j-half in row j at entry i,
-// so a tile needs 32 contiguous entries of 32 rows for each half.  Both
-// halves are copied row-wise into shared memory with cp.async (all loads
-// in flight at once, no registers held), the j-half is read transposed,
-// and both x halves are written back row-wise: every global access is
-// coalesced and the DRAM traffic is the algorithmic minimum.
+// so a tile needs 32 contiguous entries of 32 rows for each half; every
+// global access is coalesced and the DRAM traffic is the algorithmic
+// minimum (k_collision_tiles_v3 below).  Two earlier forms (both halves in
+// shared memory; j-half only with per-row table loads) measured slower and
+// were removed (profiles/r01_pack_kernel_ab.md).
 constexpr int kTile = 32;
 constexpr int kTP = kTile + 1;                 // padded row (bank conflicts)
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src));
-}
-
-struct TileHalf {
-    double cx[kTile][kTP], cy[kTile][kTP], r[kTile][kTP];   // n (then x)
-    double rc[kTile][kTP], rr[kTile][kTP];                  // edge weights
-};
-
-template <bool FIRST>
-__global__ void __launch_bounds__(kEdgeThreads) k_collision_tiles(PassA a, GroupDev g) {
-    extern __shared__ double tile_smem[];
-    TileHalf& HI = *reinterpret_cast<TileHalf*>(tile_smem);             // rows i
-    TileHalf& HJ = *reinterpret_cast<TileHalf*>(tile_smem + sizeof(TileHalf) / 8);
-    if (a.ctrl->stop) return;
-    const int64_t it = a.ctrl->iter;
-    const int2 t = g.tiles[blockIdx.x];
-    const int i0 = t.x * kTile, j0 = t.y * kTile;
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    const int N = g.ndisks;
-    const double* src = FIRST ? a.nsrc : a.uin;
-    bool bn = false, bx = false;
-    // stage: row p = (w + 8k) of each half, entry l
-#pragma unroll
-    for (int k = 0; k < kTile / 8; ++k) {
-        const int rl = w + 8 * k;
-        {   // i-half: row i = i0 + rl, entry j - 1 for j = j0 + l
-            const int i = i0 + rl, j = j0 + l;
-            if (i < N && j < N && i < j) {
-                const DiskRow R = g.disks[i];
-                const int64_t e = j - 1;
-                cp_async8(&HI.cx[rl][l], src + R.pbc + 2 * e);
-                cp_async8(&HI.cy[rl][l], src + R.pbc + 2 * e + 1);
-                cp_async8(&HI.r[rl][l], src + R.pbr + e);
-                cp_async8(&HI.rc[rl][l], a.rho + R.ebc + e);
-                cp_async8(&HI.rr[rl][l], a.rho + R.ebr + e);
-            }
-        }
-        {   // j-half: row j = j0 + rl, entry i for i = i0 + l
-            const int j = j0 + rl, i = i0 + l;
-            if (j < N && i < j) {
-                const DiskRow R = g.disks[j];
-                cp_async8(&HJ.cx[rl][l], src + R.pbc + 2 * (int64_t)i);
-                cp_async8(&HJ.cy[rl][l], src + R.pbc + 2 * (int64_t)i + 1);
-                cp_async8(&HJ.r[rl][l], src + R.pbr + i);
-                cp_async8(&HJ.rc[rl][l], a.rho + R.ebc + i);
-                cp_async8(&HJ.rr[rl][l], a.rho + R.ebr + i);
-            }
-        }
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    __syncthreads();
-    // compute pairs (i = i0 + w + 8k, j = j0 + l); results overwrite n
-    double zjc0 = 0.0, zjc1 = 0.0, zjr = 0.0;
-    if (!FIRST && j0 + l < N) {
-        const DiskRow Rj = g.disks[j0 + l];
-        zjc0 = a.z[Rj.zc]; zjc1 = a.z[Rj.zc + 1]; zjr = a.z[Rj.zr];
-    }
-#pragma unroll
-    for (int k = 0; k < kTile / 8; ++k) {
-        const int il = w + 8 * k, i = i0 + il, j = j0 + l;
-        if (i < N && j < N && i < j) {
-            double n1c0 = HI.cx[il][l], n1c1 = HI.cy[il][l], n1r = HI.r[il][l];
-            double n2c0 = HJ.cx[l][il], n2c1 = HJ.cy[l][il], n2r = HJ.r[l][il];
-            if (!FIRST) {   // n = z[zmap] - u  (phase n of the previous iteration)
-                const DiskRow Ri = g.disks[i];
-                n1c0 = a.z[Ri.zc] - n1c0; n1c1 = a.z[Ri.zc + 1] - n1c1;
-                n1r = a.z[Ri.zr] - n1r;
-                n2c0 = zjc0 - n2c0; n2c1 = zjc1 - n2c1; n2r = zjr - n2r;
-                bn |= !(finite(n1c0) && finite(n1c1) && finite(n1r) && finite(n2c0) &&
-                        finite(n2c1) && finite(n2r));
-            }
-            double c10, c11, r1, c20, c21, r2;
-            prox_collision(n1c0, n1c1, n1r, n2c0, n2c1, n2r, HI.rc[il][l], HI.rr[il][l],
-                           HJ.rc[l][il], HJ.rr[l][il], c10, c11, r1, c20, c21, r2);
-            HI.cx[il][l] = c10; HI.cy[il][l] = c11; HI.r[il][l] = r1;
-            HJ.cx[l][il] = c20; HJ.cy[l][il] = c21; HJ.r[l][il] = r2;
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kTile / 8; ++k) {
-        const int rl = w + 8 * k;
-        {
-            const int i = i0 + rl, j = j0 + l;
-            if (i < N && j < N && i < j) {
-                const DiskRow R = g.disks[i];
-                const int64_t e = j - 1;
-                xput(a, R.pbc + 2 * e, HI.cx[rl][l], bx);
-                xput(a, R.pbc + 2 * e + 1, HI.cy[rl][l], bx);
-                xput(a, R.pbr + e, HI.r[rl][l], bx);
-            }
-        }
-        {
-            const int j = j0 + rl, i = i0 + l;
-            if (j < N && i < j) {
-                const DiskRow R = g.disks[j];
-                xput(a, R.pbc + 2 * (int64_t)i, HJ.cx[rl][l], bx);
-                xput(a, R.pbc + 2 * (int64_t)i + 1, HJ.cy[rl][l], bx);
-                xput(a, R.pbr + i, HJ.r[rl][l], bx);
-            }
-        }
-    }
-    passa_flags<FIRST>(a, it, bn, bx);
-}
-constexpr size_t kTileSmem = 2 * sizeof(TileHalf);
-
-// Variant: only the transposed j-half is staged (plain loads into shared
-// memory); the i-half is read directly, lane = j.  Fewer bytes of shared
-// memory per CTA, more CTAs per SM.
-template <bool FIRST>
-__global__ void __launch_bounds__(kEdgeThreads) k_collision_tiles_reg(PassA a, GroupDev g) {
-    __shared__ double s_cx[kTile][kTP], s_cy[kTile][kTP], s_r[kTile][kTP];
-    __shared__ double s_rc[kTile][kTP], s_rr[kTile][kTP];
-    if (a.ctrl->stop) return;
-    const int64_t it = a.ctrl->iter;
-    const int2 t = g.tiles[blockIdx.x];
-    const int i0 = t.x * kTile, j0 = t.y * kTile;
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    const int N = g.ndisks;
-    const double* src = FIRST ? a.nsrc : a.uin;
-    bool bn = false, bx = false;
-#pragma unroll
-    for (int k = 0; k < kTile / 8; ++k) {
-        const int jl = w + 8 * k, j = j0 + jl, i = i0 + l;
-        if (j < N && i < j) {
-            const DiskRow R = g.disks[j];
-            cp_async8(&s_cx[jl][l], src + R.pbc + 2 * (int64_t)i);
-            cp_async8(&s_cy[jl][l], src + R.pbc + 2 * (int64_t)i + 1);
-            cp_async8(&s_r[jl][l], src + R.pbr + i);
-            cp_async8(&s_rc[jl][l], a.rho + R.ebc + i);
-            cp_async8(&s_rr[jl][l], a.rho + R.ebr + i);
-        }
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-    double zjc0 = 0.0, zjc1 = 0.0, zjr = 0.0;
-    if (!FIRST && j0 + l < N) {
-        const DiskRow Rj = g.disks[j0 + l];
-        zjc0 = a.z[Rj.zc]; zjc1 = a.z[Rj.zc + 1]; zjr = a.z[Rj.zr];
-    }
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kTile / 8; ++k) {
-        const int il = w + 8 * k, i = i0 + il, j = j0 + l;
-        if (i < N && j < N && i < j) {
-            const DiskRow R = g.disks[i];
-            const int64_t pc = R.pbc + 2 * (int64_t)(j - 1), pr = R.pbr + (j - 1);
-            double n1c0 = src[pc], n1c1 = src[pc + 1], n1r = src[pr];
-            double n2c0 = s_cx[l][il], n2c1 = s_cy[l][il], n2r = s_r[l][il];
-            if (!FIRST) {
-                n1c0 = a.z[R.zc] - n1c0; n1c1 = a.z[R.zc + 1] - n1c1; n1r = a.z[R.zr] - n1r;
-                n2c0 = zjc0 - n2c0; n2c1 = zjc1 - n2c1; n2r = zjr - n2r;
-                bn |= !(finite(n1c0) && finite(n1c1) && finite(n1r) && finite(n2c0) &&
-                        finite(n2c1) && finite(n2r));
-            }
-            const double rc1 = a.rho[R.ebc + (j - 1)], rr1 = a.rho[R.ebr + (j - 1)];
-            double c10, c11, r1, c20, c21, r2;
-            prox_collision(n1c0, n1c1, n1r, n2c0, n2c1, n2r, rc1, rr1, s_rc[l][il],
-                           s_rr[l][il], c10, c11, r1, c20, c21, r2);
-            xput(a, pc, c10, bx); xput(a, pc + 1, c11, bx);
-            xput(a, pr, r1, bx);
-            s_cx[l][il] = c20; s_cy[l][il] = c21; s_r[l][il] = r2;
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kTile / 8; ++k) {
-        const int jl = w + 8 * k, j = j0 + jl, i = i0 + l;
-        if (j < N && i < j) {
-            const DiskRow R = g.disks[j];
-            const int64_t pc = R.pbc + 2 * (int64_t)i, pr = R.pbr + i;
-            xput(a, pc, s_cx[jl][l], bx);
-            xput(a, pc + 1, s_cy[jl][l], bx);
-            xput(a, pr, s_r[jl][l], bx);
-        }
-    }
-    passa_flags<FIRST>(a, it, bn, bx);
 }
 
 __device__ __forceinline__ DiskRow disk_row(const GroupDev& g, int i) {

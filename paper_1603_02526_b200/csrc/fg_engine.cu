@@ -204,14 +204,6 @@ struct fg_plan {
     int64_t nlv[5] = {0, 0, 0, 0, 0};
     int32_t* d_llist = nullptr; int32_t* d_lprog = nullptr; int64_t nL = 0;  // D>4
     int64_t nLvars = 0;
-    int32_t* d_clvars[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};   // clusters
-    int32_t* d_clprog[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-    int64_t ncl[5] = {0, 0, 0, 0, 0};
-    size_t clsmem[5] = {0, 0, 0, 0, 0};
-    STile* d_stiles = nullptr;         // TMA pipeline tiles over the small runs
-    int64_t ntiles = 0, tma_grid = 0;
-    int32_t tma_stage = 0;             // doubles per pipeline stage
-    size_t tma_smem = 0;
     int32_t* d_prog = nullptr;
     int64_t part_off[16] = {0};                       // per var kernel slot
     int32_t* d_glist = nullptr; int64_t nG = 0;
@@ -278,34 +270,15 @@ struct fg_plan {
     int first_done = 0;
     // graphs: key = chunk iterations
     std::map<int, cudaGraphExec_t> graphs;
-    // fused giant kernels: the chunk kernel's last CTA per component runs the
-    // top of the tree; in chain iterations the update's last CTA reduces
-    bool giant_fused = true;
-    bool row256 = false;               // class-L rows on 256-thread CTAs (A/B)
-    bool no_fork = false;              // edge groups serialized on one stream (A/B)
+    // giant kernels: the chunk kernel's last CTA per component runs the top
+    // of the tree; in chain iterations the update's last CTA reduces
     bool lunit[5] = {false, false, false, false, false};  // class-L rows of dim D: unit weights
     LExc* d_lexc[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // their exception edge
-    // class-L rows on 2-CTA clusters (unit-weight form, fg_rows.cuh)
-    Row2* d_row2[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-    bool row2_ok[5] = {false, false, false, false, false};
-    size_t row2_smem[5] = {0, 0, 0, 0, 0};
-    bool no_row2 = false;
-    bool row_deep = false;             // deeper u-update batches in unit rows (A/B)
     // class-L rows through a TMA ring (unit-weight form, fg_rows.cuh)
     int32_t* d_planoff[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     RowDesc* d_rowdesc[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     int32_t* d_plans = nullptr;
     bool pipe_ok[5] = {false, false, false, false, false};
-    bool no_pipe = false;
-    bool row_ring[5] = {false, false, false, false, false};  // persistent row kernel per dim
-    bool pipe_deep = false;            // small-stage rows with 4 stages (A/B)
-    bool pipe_two[5] = {false, false, false, false, false};  // 2 small stages at 4 CTAs/SM
-    bool pipe_mid[5] = {false, false, false, false, false};  // 2 mid stages at 3 CTAs/SM
-    bool l2hint = true;                // mid rows: L2 evict_last on phase-1 copies
-    int64_t ring_grid[5][2] = {};      // resident CTAs of the ring kernel per dim / stage form
-    // 2 stages of twice the size: measured better for dim >= 2 rows (pack
-    // center rows 0.285 vs 0.306 ms), worse for dim 1 (0.176 vs 0.160)
-    bool pipe_big[5] = {false, false, true, true, true};
     unsigned* d_gcnt = nullptr;        // per giant component chunk counter
     unsigned* d_ucnt = nullptr;        // giant update CTA counter
     FusedReduce fr_next{nullptr, 0, 0, 0, nullptr};   // set by chain_rest
@@ -332,13 +305,10 @@ fg_plan::~fg_plan() {
                     d_u[0], d_u[1], d_stage, d_stage2, d_chk, d_aux, d_zb[0], d_zb[1], d_zs, d_sruns,
                     d_sblk[0], d_sblk[1], d_sblk[2], d_lvars[1], d_lvars[2], d_lvars[3],
                     d_lvars[4], d_lvprog[1], d_lvprog[2], d_lvprog[3], d_lvprog[4],
-                    d_stiles,
-                    d_clvars[1], d_clvars[2], d_clvars[3], d_clvars[4], d_clprog[1],
-                    d_clprog[2], d_clprog[3], d_clprog[4],
                     d_llist, d_lprog, d_prog, d_glist, d_gchunks, d_gcomps,
                     d_gwork, d_gcref, d_gwref, d_csum, d_gz, d_part, d_res2, d_ctrl, d_hist, d_chain_xx,
                     d_chain_fnorm, d_chain_wtab, d_flag, d_bad, d_gcnt, d_ucnt, d_lexc[1], d_lexc[2], d_lexc[3],
-                    d_lexc[4], d_row2[1], d_row2[2], d_row2[3], d_row2[4],
+                    d_lexc[4],
                     d_planoff[1], d_planoff[2], d_planoff[3], d_planoff[4], d_plans,
                     d_rowdesc[1], d_rowdesc[2], d_rowdesc[3], d_rowdesc[4],
                     d_cutg, d_send, d_recv, d_m, d_bpart};
@@ -369,18 +339,14 @@ void launch_kind(const GroupDev& g, const PassA& a, cudaStream_t st) {
     const int T = kEdgeThreads;
     switch (g.kind) {
         case FG_KIND_COLLISION:
-            if (g.tiles && g.variant == 3 && g.rows_even && g.unit)
+            if (g.tiles && g.rows_even && g.unit)
                 k_collision_tiles_v3<FIRST, true, true><<<(unsigned)g.ntiles, T, 0, st>>>(a, g);
-            else if (g.tiles && g.variant == 3 && g.unit)
+            else if (g.tiles && g.unit)
                 k_collision_tiles_v3<FIRST, false, true><<<(unsigned)g.ntiles, T, 0, st>>>(a, g);
-            else if (g.tiles && g.variant == 3 && g.rows_even)
+            else if (g.tiles && g.rows_even)
                 k_collision_tiles_v3<FIRST, true><<<(unsigned)g.ntiles, T, 0, st>>>(a, g);
-            else if (g.tiles && g.variant == 3)
-                k_collision_tiles_v3<FIRST, false><<<(unsigned)g.ntiles, T, 0, st>>>(a, g);
-            else if (g.tiles && g.variant == 1)
-                k_collision_tiles<FIRST><<<(unsigned)g.ntiles, T, kTileSmem, st>>>(a, g);
             else if (g.tiles)
-                k_collision_tiles_reg<FIRST><<<(unsigned)g.ntiles, T, 0, st>>>(a, g);
+                k_collision_tiles_v3<FIRST, false><<<(unsigned)g.ntiles, T, 0, st>>>(a, g);
             else k_collision<FIRST><<<grid, T, 0, st>>>(a, g);
             break;
         case FG_KIND_WALL: k_wall<FIRST><<<grid, T, 0, st>>>(a, g); break;
@@ -424,7 +390,6 @@ void edge_pass(fg_plan* p, bool first, const double* zin, const double* uin,
     PassA a{p->vt(), zin, uin, nsrc, p->d_x, p->d_rho, p->d_ctrl};
     int active = 0;
     for (auto& g : p->groups) active += g.dev.count > 0;
-    if (p->no_fork) active = 1;
     if (active >= 2) {
         cudaEventRecord(p->ev_fork, st);
         cudaStreamWaitEvent(p->stream2, p->ev_fork, 0);
@@ -444,73 +409,50 @@ void edge_pass(fg_plan* p, bool first, const double* zin, const double* uin,
 }
 
 // Variable-pass kernel slots (one launch each, empty classes skipped):
-//   0 small segments (deg <= 8, registers)   1 small segments (deg 9..32)
-//   2..5 large segments, one CTA per variable of dim 1..4
-//   6 large segments, one CTA per component (dim > 4)
-//   7 giant chunks   8 giant top   9 giant u update
-constexpr int kVarSlots = 16;
-constexpr int kSlotGiantChunks = 8, kSlotGiantTop = 9, kSlotGiantUpdate = 10;
-constexpr int kSlotSmallTma = 15;
+//   0 small segments (deg <= 4, registers)   1 small segments (deg 5..8)
+//   2 small segments (deg 9..32)
+//   3..6 large segments, one CTA per variable of dim 1..4
+//   7 large segments, one CTA per component (dim > 4)
+//   8 giant chunks (+ the top of the tree in the last CTA per component)
+//   9 giant u update
+constexpr int kVarSlots = 10;
+constexpr int kSlotGiantChunks = 8, kSlotGiantUpdate = 9;
 const char* kVarNames[kVarSlots] = {
     "var_small_deg4", "var_small_deg8", "var_small_loop", "var_large_d1",
     "var_large_d2", "var_large_d3", "var_large_d4", "var_large_comp",
-    "var_giant_chunks", "var_giant_top", "var_giant_update", "var_cluster_d1",
-    "var_cluster_d2", "var_cluster_d3", "var_cluster_d4", "var_small_tma"};
-
-// slots that run in a fused iteration (the TMA pipeline replaces 0..2)
-bool fused_slot(const fg_plan* p, int w) {
-    if (p->tma_grid > 0 && w <= 2) return false;
-    return true;
-}
+    "var_giant_chunks", "var_giant_update"};
 
 int64_t var_slot_blocks(const fg_plan* p, int w) {
     switch (w) {
-        case 15: return p->tma_grid;
         case 0: case 1: case 2: return p->nsblk[w];
         case 3: case 4: case 5: case 6: return p->nlv[w - 2];
         case 7: return p->nL;
         case 8: return p->nG ? p->nGC : 0;
-        case 9: return p->giant_fused ? 0 : p->nG;
-        case 10: return p->nG ? p->nGW : 0;
-        case 11: case 12: case 13: case 14: return p->ncl[w - 10] * kCluster;
+        case 9: return p->nG ? p->nGW : 0;
     }
     return 0;
 }
 
+// class-L rows of dim D: the TMA ring in the fused unit-weight form, else
+// one 512-thread CTA per row (unit or general weights)
 template <int D, int MODE>
-void launch_cluster(fg_plan* p, const PassB& b, unsigned grid, int64_t po, cudaStream_t st) {
-    k_var_cluster<D, MODE><<<grid, kClusterThreads, p->clsmem[D], st>>>(
-        b, p->d_clvars[D], p->d_clprog[D], p->d_prog, po);
-}
-
-template <int D>
-void launch_ring(fg_plan* p, const PassB& b, int64_t nrows, int64_t po, cudaStream_t st) {
-    const int big = p->pipe_big[D] ? 1 : 0;
-    const unsigned G = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nrows, p->ring_grid[D][big]));
-    if (big)
-        k_var_row_ring<D, 2, 2 * kPipeStageDoubles><<<G, kRowThreads,
-            row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_rowdesc[D], p->d_prog, p->d_plans,
-                                                           p->d_lexc[D], po, (int32_t)nrows);
-    else
-        k_var_row_ring<D, kPipeStages, kPipeStageDoubles><<<G, kRowThreads, row_pipe_smem(), st>>>(
-            b, p->d_rowdesc[D], p->d_prog, p->d_plans, p->d_lexc[D], po, (int32_t)nrows);
-}
-
-template <int D>
-int ring_setup(fg_plan* p, int sms) {
-    const int s0 = (int)row_pipe_smem(), s1 = (int)row_pipe_smem(2, 2 * kPipeStageDoubles);
-    CK(cudaFuncSetAttribute(k_var_row_ring<D, kPipeStages, kPipeStageDoubles>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, s0));
-    CK(cudaFuncSetAttribute(k_var_row_ring<D, 2, 2 * kPipeStageDoubles>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
-    int n0 = 0, n1 = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &n0, k_var_row_ring<D, kPipeStages, kPipeStageDoubles>, kRowThreads, s0));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &n1, k_var_row_ring<D, 2, 2 * kPipeStageDoubles>, kRowThreads, s1));
-    p->ring_grid[D][0] = (int64_t)std::max(1, n0) * sms;
-    p->ring_grid[D][1] = (int64_t)std::max(1, n1) * sms;
-    return 0;
+void launch_rows(fg_plan* p, const PassB& b, unsigned grid, int64_t po, cudaStream_t st) {
+    if (MODE == MODE_FUSED && p->lunit[D] && p->pipe_ok[D]) {
+        if (D == 1)
+            k_var_row_pipe<D, kPipeStageDoubles, false><<<grid, kRowThreads,
+                row_pipe_smem(kPipeStageDoubles), st>>>(b, p->d_rowdesc[D], p->d_prog, p->d_plans,
+                                                        p->d_lexc[D], po);
+        else
+            k_var_row_pipe<D, kPipeMidDoubles, true><<<grid, kRowThreads,
+                row_pipe_smem(kPipeMidDoubles), st>>>(b, p->d_rowdesc[D], p->d_prog, p->d_plans,
+                                                      p->d_lexc[D], po);
+    } else if (p->lunit[D]) {
+        k_var_large_vec<D, MODE, true><<<grid, kLargeThreads, 0, st>>>(
+            b, p->d_lvars[D], p->d_lvprog[D], p->d_prog, po, p->d_lexc[D]);
+    } else {
+        k_var_large_vec<D, MODE><<<grid, kLargeThreads, 0, st>>>(
+            b, p->d_lvars[D], p->d_lvprog[D], p->d_prog, po);
+    }
 }
 
 template <int MODE>
@@ -518,7 +460,6 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
                 double* uout, const double* msrc, cudaStream_t st) {
     const int64_t nb = var_slot_blocks(p, which);
     if (nb == 0) return false;
-    if (MODE == MODE_FUSED && !fused_slot(p, which)) return false;
     const unsigned grid = (unsigned)nb;
     PassB b{p->vt(), p->d_x, uin, uout, msrc, zout, zin, p->d_rho, p->d_alpha,
             p->d_zw, p->d_ctrl, p->d_part, p->d_zvar};
@@ -533,135 +474,23 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
         case 2:
             k_var_small_run<0, MODE><<<grid, 256, 0, st>>>(b, p->d_sruns, p->d_sblk[2], po);
             return true;
-        case 3:
-            if (MODE == MODE_FUSED && p->lunit[1] && p->pipe_ok[1] && !p->no_pipe && p->pipe_two[1])
-                k_var_row_pipe<1, 2, kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2), st>>>(b, p->d_rowdesc[1], p->d_prog, p->d_plans, p->d_lexc[1], po);
-            else if (MODE == MODE_FUSED && p->lunit[1] && p->pipe_ok[1] && !p->no_pipe && p->row_ring[1])
-                launch_ring<1>(p, b, nb, po, st);
-            else if (MODE == MODE_FUSED && p->lunit[1] && p->pipe_ok[1] && !p->no_pipe && p->pipe_big[1])
-                k_var_row_pipe<1, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_rowdesc[1], p->d_prog, p->d_plans, p->d_lexc[1], po);
-            else if (MODE == MODE_FUSED && p->lunit[1] && p->pipe_ok[1] && !p->no_pipe && p->pipe_deep)
-                k_var_row_pipe<1, 4, kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(4), st>>>(b, p->d_rowdesc[1], p->d_prog, p->d_plans, p->d_lexc[1], po);
-            else if (MODE == MODE_FUSED && p->lunit[1] && p->pipe_ok[1] && !p->no_pipe)
-                k_var_row_pipe<1><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_rowdesc[1], p->d_prog, p->d_plans, p->d_lexc[1], po);
-            else if (MODE == MODE_FUSED && p->lunit[1] && p->row2_ok[1] && !p->no_row2)
-                k_var_row2<1><<<2 * grid, kRowThreads, p->row2_smem[1], st>>>(b, p->d_row2[1], p->d_prog, p->d_lexc[1], po);
-            else if (p->row256)
-                k_var_large_vec<1, MODE, 256><<<grid, 256, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po, nullptr, p->row2_ok[1] ? po + grid : -1);
-            else if (p->lunit[1] && p->row_deep)
-                k_var_large_vec<1, MODE, kLargeThreads, true, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po, p->d_lexc[1], p->row2_ok[1] ? po + grid : -1);
-            else if (p->lunit[1])
-                k_var_large_vec<1, MODE, kLargeThreads, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po, p->d_lexc[1], p->row2_ok[1] ? po + grid : -1);
-            else
-                k_var_large_vec<1, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[1], p->d_lvprog[1], p->d_prog, po, nullptr, p->row2_ok[1] ? po + grid : -1);
-            return true;
-        case 4:
-            if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe && p->pipe_mid[2] && p->l2hint)
-                k_var_row_pipe<2, 2, kPipeMidDoubles, true><<<grid, kRowThreads, row_pipe_smem(2, kPipeMidDoubles), st>>>(b, p->d_rowdesc[2], p->d_prog, p->d_plans, p->d_lexc[2], po);
-            else if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe && p->pipe_mid[2])
-                k_var_row_pipe<2, 2, kPipeMidDoubles><<<grid, kRowThreads, row_pipe_smem(2, kPipeMidDoubles), st>>>(b, p->d_rowdesc[2], p->d_prog, p->d_plans, p->d_lexc[2], po);
-            else if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe && p->pipe_two[2])
-                k_var_row_pipe<2, 2, kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2), st>>>(b, p->d_rowdesc[2], p->d_prog, p->d_plans, p->d_lexc[2], po);
-            else if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe && p->row_ring[2])
-                launch_ring<2>(p, b, nb, po, st);
-            else if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe && p->pipe_big[2])
-                k_var_row_pipe<2, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_rowdesc[2], p->d_prog, p->d_plans, p->d_lexc[2], po);
-            else if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe && p->pipe_deep)
-                k_var_row_pipe<2, 4, kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(4), st>>>(b, p->d_rowdesc[2], p->d_prog, p->d_plans, p->d_lexc[2], po);
-            else if (MODE == MODE_FUSED && p->lunit[2] && p->pipe_ok[2] && !p->no_pipe)
-                k_var_row_pipe<2><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_rowdesc[2], p->d_prog, p->d_plans, p->d_lexc[2], po);
-            else if (MODE == MODE_FUSED && p->lunit[2] && p->row2_ok[2] && !p->no_row2)
-                k_var_row2<2><<<2 * grid, kRowThreads, p->row2_smem[2], st>>>(b, p->d_row2[2], p->d_prog, p->d_lexc[2], po);
-            else if (p->row256)
-                k_var_large_vec<2, MODE, 256><<<grid, 256, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po, nullptr, p->row2_ok[2] ? po + grid : -1);
-            else if (p->lunit[2] && p->row_deep)
-                k_var_large_vec<2, MODE, kLargeThreads, true, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po, p->d_lexc[2], p->row2_ok[2] ? po + grid : -1);
-            else if (p->lunit[2])
-                k_var_large_vec<2, MODE, kLargeThreads, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po, p->d_lexc[2], p->row2_ok[2] ? po + grid : -1);
-            else
-                k_var_large_vec<2, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[2], p->d_lvprog[2], p->d_prog, po, nullptr, p->row2_ok[2] ? po + grid : -1);
-            return true;
-        case 5:
-            if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe && p->pipe_mid[3] && p->l2hint)
-                k_var_row_pipe<3, 2, kPipeMidDoubles, true><<<grid, kRowThreads, row_pipe_smem(2, kPipeMidDoubles), st>>>(b, p->d_rowdesc[3], p->d_prog, p->d_plans, p->d_lexc[3], po);
-            else if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe && p->pipe_mid[3])
-                k_var_row_pipe<3, 2, kPipeMidDoubles><<<grid, kRowThreads, row_pipe_smem(2, kPipeMidDoubles), st>>>(b, p->d_rowdesc[3], p->d_prog, p->d_plans, p->d_lexc[3], po);
-            else if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe && p->pipe_two[3])
-                k_var_row_pipe<3, 2, kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2), st>>>(b, p->d_rowdesc[3], p->d_prog, p->d_plans, p->d_lexc[3], po);
-            else if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe && p->row_ring[3])
-                launch_ring<3>(p, b, nb, po, st);
-            else if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe && p->pipe_big[3])
-                k_var_row_pipe<3, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_rowdesc[3], p->d_prog, p->d_plans, p->d_lexc[3], po);
-            else if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe && p->pipe_deep)
-                k_var_row_pipe<3, 4, kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(4), st>>>(b, p->d_rowdesc[3], p->d_prog, p->d_plans, p->d_lexc[3], po);
-            else if (MODE == MODE_FUSED && p->lunit[3] && p->pipe_ok[3] && !p->no_pipe)
-                k_var_row_pipe<3><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_rowdesc[3], p->d_prog, p->d_plans, p->d_lexc[3], po);
-            else if (MODE == MODE_FUSED && p->lunit[3] && p->row2_ok[3] && !p->no_row2)
-                k_var_row2<3><<<2 * grid, kRowThreads, p->row2_smem[3], st>>>(b, p->d_row2[3], p->d_prog, p->d_lexc[3], po);
-            else if (p->row256)
-                k_var_large_vec<3, MODE, 256><<<grid, 256, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po, nullptr, p->row2_ok[3] ? po + grid : -1);
-            else if (p->lunit[3] && p->row_deep)
-                k_var_large_vec<3, MODE, kLargeThreads, true, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po, p->d_lexc[3], p->row2_ok[3] ? po + grid : -1);
-            else if (p->lunit[3])
-                k_var_large_vec<3, MODE, kLargeThreads, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po, p->d_lexc[3], p->row2_ok[3] ? po + grid : -1);
-            else
-                k_var_large_vec<3, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[3], p->d_lvprog[3], p->d_prog, po, nullptr, p->row2_ok[3] ? po + grid : -1);
-            return true;
-        case 6:
-            if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe && p->pipe_mid[4] && p->l2hint)
-                k_var_row_pipe<4, 2, kPipeMidDoubles, true><<<grid, kRowThreads, row_pipe_smem(2, kPipeMidDoubles), st>>>(b, p->d_rowdesc[4], p->d_prog, p->d_plans, p->d_lexc[4], po);
-            else if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe && p->pipe_mid[4])
-                k_var_row_pipe<4, 2, kPipeMidDoubles><<<grid, kRowThreads, row_pipe_smem(2, kPipeMidDoubles), st>>>(b, p->d_rowdesc[4], p->d_prog, p->d_plans, p->d_lexc[4], po);
-            else if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe && p->pipe_two[4])
-                k_var_row_pipe<4, 2, kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2), st>>>(b, p->d_rowdesc[4], p->d_prog, p->d_plans, p->d_lexc[4], po);
-            else if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe && p->row_ring[4])
-                launch_ring<4>(p, b, nb, po, st);
-            else if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe && p->pipe_big[4])
-                k_var_row_pipe<4, 2, 2 * kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(2, 2 * kPipeStageDoubles), st>>>(b, p->d_rowdesc[4], p->d_prog, p->d_plans, p->d_lexc[4], po);
-            else if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe && p->pipe_deep)
-                k_var_row_pipe<4, 4, kPipeStageDoubles><<<grid, kRowThreads, row_pipe_smem(4), st>>>(b, p->d_rowdesc[4], p->d_prog, p->d_plans, p->d_lexc[4], po);
-            else if (MODE == MODE_FUSED && p->lunit[4] && p->pipe_ok[4] && !p->no_pipe)
-                k_var_row_pipe<4><<<grid, kRowThreads, row_pipe_smem(), st>>>(b, p->d_rowdesc[4], p->d_prog, p->d_plans, p->d_lexc[4], po);
-            else if (MODE == MODE_FUSED && p->lunit[4] && p->row2_ok[4] && !p->no_row2)
-                k_var_row2<4><<<2 * grid, kRowThreads, p->row2_smem[4], st>>>(b, p->d_row2[4], p->d_prog, p->d_lexc[4], po);
-            else if (p->row256)
-                k_var_large_vec<4, MODE, 256><<<grid, 256, 0, st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, po, nullptr, p->row2_ok[4] ? po + grid : -1);
-            else if (p->lunit[4] && p->row_deep)
-                k_var_large_vec<4, MODE, kLargeThreads, true, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, po, p->d_lexc[4], p->row2_ok[4] ? po + grid : -1);
-            else if (p->lunit[4])
-                k_var_large_vec<4, MODE, kLargeThreads, true><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, po, p->d_lexc[4], p->row2_ok[4] ? po + grid : -1);
-            else
-                k_var_large_vec<4, MODE><<<grid, kLargeThreads, 0, st>>>(b, p->d_lvars[4], p->d_lvprog[4], p->d_prog, po, nullptr, p->row2_ok[4] ? po + grid : -1);
-            return true;
+        case 3: launch_rows<1, MODE>(p, b, grid, po, st); return true;
+        case 4: launch_rows<2, MODE>(p, b, grid, po, st); return true;
+        case 5: launch_rows<3, MODE>(p, b, grid, po, st); return true;
+        case 6: launch_rows<4, MODE>(p, b, grid, po, st); return true;
         case 7:
             k_var_large<MODE><<<grid, kVarThreads, 0, st>>>(b, p->d_llist, p->d_lprog, p->d_prog, po);
             return true;
         case kSlotGiantChunks:
-            if (p->giant_fused && p->giant_unit)
+            if (p->giant_unit)
                 k_var_giant_chunks<MODE, kGiantChunkThreads, true><<<grid, kGiantChunkThreads, p->gtop_smem, st>>>(
                     b, p->d_glist, p->d_gchunks, p->d_prog, p->d_csum, p->d_gcomps, p->d_gz,
                     p->d_send, p->d_gcnt, p->d_gcref);
-            else if (p->giant_fused)
+            else
                 k_var_giant_chunks<MODE, kGiantChunkThreads><<<grid, kGiantChunkThreads, p->gtop_smem, st>>>(
                     b, p->d_glist, p->d_gchunks, p->d_prog, p->d_csum, p->d_gcomps, p->d_gz,
                     p->d_send, p->d_gcnt, p->d_gcref);
-            else
-                k_var_giant_chunks<MODE><<<grid, kVarThreads, 0, st>>>(
-                    b, p->d_glist, p->d_gchunks, p->d_prog, p->d_csum);
             return true;
-        case kSlotGiantTop:
-            k_var_giant_top<MODE><<<grid, kVarThreads, p->gtop_smem, st>>>(
-                b, p->d_glist, p->d_gcomps, p->d_prog, p->d_csum, p->d_gz, p->d_send);
-            return true;
-        case kSlotSmallTma:
-            if (MODE != MODE_FUSED) return false;
-            k_var_small_tma<<<grid, kTmaThreads, p->tma_smem, st>>>(
-                b, p->d_sruns, p->d_stiles, (int32_t)p->ntiles, p->tma_stage, po);
-            return true;
-        case 11: launch_cluster<1, MODE>(p, b, grid, po, st); return true;
-        case 12: launch_cluster<2, MODE>(p, b, grid, po, st); return true;
-        case 13: launch_cluster<3, MODE>(p, b, grid, po, st); return true;
-        case 14: launch_cluster<4, MODE>(p, b, grid, po, st); return true;
         case kSlotGiantUpdate:
             if (MODE != MODE_FUSED) return false;
             if (p->giant_unit)
@@ -715,7 +544,7 @@ int64_t count_phasez_launches(const fg_plan* p) {
 
 int64_t count_var_launches(const fg_plan* p) {
     int64_t n = 0;
-    for (int w = 0; w < kVarSlots; ++w) n += var_slot_blocks(p, w) > 0 && fused_slot(p, w);
+    for (int w = 0; w < kVarSlots; ++w) n += var_slot_blocks(p, w) > 0;
     return n;
 }
 
@@ -853,7 +682,7 @@ void launch_reduce(fg_plan* p, bool chain_iter, cudaStream_t st) {
 }
 
 // ... then the remaining (large / giant) variable classes: the bias
-bool chain_rest_slot(int w) { return w > 2 && w != kSlotSmallTma; }
+bool chain_rest_slot(int w) { return w > 2; }
 // Returns true when the residual reduction ran fused into the last CTA of
 // the giant u update (the update is then the iteration's last kernel).
 bool chain_rest(fg_plan* p, int in, cudaStream_t st) {
@@ -861,7 +690,7 @@ bool chain_rest(fg_plan* p, int in, cudaStream_t st) {
     int last = -1;
     for (int w = 0; w < kVarSlots; ++w)
         if (chain_rest_slot(w) && var_slot_blocks(p, w) > 0) last = w;
-    const bool fuse = last == kSlotGiantUpdate && p->giant_fused;
+    const bool fuse = last == kSlotGiantUpdate;
     if (fuse)
         p->fr_next = FusedReduce{p->d_ucnt, p->npart, chain_main_grid(p) + 1, p->chain_grid,
                                  p->d_hist};
@@ -942,7 +771,7 @@ void detect_svm_chain(fg_plan* p, const std::vector<int32_t>& dim,
                       const std::vector<int32_t>& deg, const std::vector<int64_t>& zbase,
                       const int32_t* zcut) {
     p->chain_on = false;
-    if (getenv("FGADMM_NO_CHAIN") || p->tma_grid > 0) return;
+    if (getenv("FGADMM_NO_CHAIN")) return;
     auto is_cut = [&](int32_t v) { return zcut != nullptr && zcut[zbase[v]] >= 0; };
     const GroupHost *gn = nullptr, *gs = nullptr, *gm = nullptr, *ge = nullptr;
     for (auto& g : p->groups) {
@@ -1053,7 +882,7 @@ void detect_mpc_chain(fg_plan* p, const std::vector<int32_t>& dim,
                       const std::vector<int32_t>& deg, const std::vector<int64_t>& zbase,
                       const std::vector<int64_t>& pbase, const std::vector<int32_t>& ebase) {
     p->mpc_ok = false;
-    if (getenv("FGADMM_NO_CHAIN") || p->partitioned() || p->tma_grid > 0) return;
+    if (getenv("FGADMM_NO_CHAIN") || p->partitioned()) return;
     GroupHost *gc = nullptr, *gdyn = nullptr, *gi = nullptr;
     for (auto& g : p->groups) {
         if (g.dev.count == 0) continue;
@@ -1273,10 +1102,7 @@ int build_group(fg_plan* p, const fg_group_desc& gd,
             g.sk[j] = dsk;
         }
     }
-    const char* cvar = getenv("FGADMM_COLLISION");      // generic | tile | tile_reg
-    g.variant = (cvar && std::strcmp(cvar, "tile") == 0) ? 1 : 0;
-    const bool want_tiles = !(cvar && std::strcmp(cvar, "generic") == 0);
-    if (gd.kind == FG_KIND_COLLISION && n > 0 && want_tiles) {
+    if (gd.kind == FG_KIND_COLLISION && n > 0) {
         // all-pairs structure: factors are (i, j), i < j, over K disks in
         // lexicographic order, and every row keeps its pair entries in
         // partner order -> tiled kernel with arithmetic addressing
@@ -1314,15 +1140,12 @@ int build_group(fg_plan* p, const fg_group_desc& gd,
             out.allocs.push_back(drows);
             if (int rc = upload(&dt, tiles)) return rc;
             out.allocs.push_back(dt);
-            CK(cudaFuncSetAttribute(k_collision_tiles<true>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
-            CK(cudaFuncSetAttribute(k_collision_tiles<false>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
             g.disks = drows;
             g.tiles = dt;
             g.ndisks = (int32_t)K;
             g.ntiles = (int32_t)tiles.size();
-            // affine rows + 16-byte aligned center entries -> variant 3
+            // affine rows: arithmetic row addresses; 16-byte aligned center
+            // entries: one 16-byte access per center pair
             bool aff = K >= 2, even = true;
             const DiskRow& r0 = rows[0];
             DiskRow rs{};
@@ -1342,7 +1165,6 @@ int build_group(fg_plan* p, const fg_group_desc& gd,
             g.rows_even = even ? 1 : 0;
             g.row0 = r0;
             g.rowS = rs;
-            if (!cvar || std::strcmp(cvar, "v3") == 0) g.variant = 3;
         }
     }
     if (gd.kind == FG_KIND_MPC_DYN && gd.tables && gd.ntables == 1 && g.runs &&
@@ -1410,7 +1232,7 @@ int64_t svm_chain_launches(const fg_plan* p) {
     int last = -1;
     for (int w = 0; w < kVarSlots; ++w)
         if (chain_rest_slot(w) && var_slot_blocks(p, w) > 0) { ++n; last = w; }
-    if (!(last == kSlotGiantUpdate && p->giant_fused)) ++n;   // separate reduce
+    if (last != kSlotGiantUpdate) ++n;   // separate reduce
     return n;
 }
 
@@ -1512,21 +1334,12 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     // ---- variable-pass classes and tree programs ----
     std::vector<int32_t> llist, lprog, glist, prog;
     std::vector<int32_t> lvars[5], lvprog[5];
-    std::vector<Row2> row2[5];
-    int64_t row2_ne[5] = {0, 0, 0, 0, 0};
-    bool row2_short[5] = {false, false, false, false, false};
     std::vector<SRun> sruns;
     std::vector<SBlock> sblk[3];
     std::vector<GChunk> gchunks;
     std::vector<GComp> gcomps;
     std::vector<GWork> gwork;
     std::vector<int32_t> cutg;
-    std::vector<int32_t> clvars[5], clprog[5];
-    int64_t clmax[5] = {0, 0, 0, 0, 0};
-    // The 4-CTA cluster kernel moves the compulsory bytes only, but measured
-    // slower than the one-CTA kernel (0.86 vs 0.55 ms, pack N=5000): it is
-    // opt-in (FGADMM_CLUSTER=1) until its leaf phase is better occupied.
-    const bool no_cluster = getenv("FGADMM_CLUSTER") == nullptr;
     std::map<int64_t, int32_t> leafprog;   // n -> offset
     auto leaf_prog = [&](int64_t n) -> int32_t {
         auto it = leafprog.find(n);
@@ -1580,35 +1393,10 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
                 sruns.push_back(SRun{pbase[v], zbase[v], ebase[v], 1, dim[v], (int32_t)dg});
             }
             nsmall += dim[v];
-        } else if (dg - 1 <= kChunk && dim[v] <= 4 && dg >= kClusterMinDeg && !no_cluster) {
-            const int d = dim[v];
-            const int32_t off = leaf_prog(dg - 1);
-            clvars[d].push_back((int32_t)v);
-            clprog[d].push_back(off);
-            // shared memory of the largest per-CTA element range
-            const int32_t* P = prog.data() + off;
-            const int nu = P[0];
-            for (int r = 0; r < kCluster; ++r) {
-                const int L0 = (int)((int64_t)nu * r / kCluster);
-                const int L1 = (int)((int64_t)nu * (r + 1) / kCluster);
-                const int64_t lo = r == 0 ? 0 : 1 + P[2 + 2 * L0];
-                const int64_t hi = r == kCluster - 1 ? dg : 1 + P[2 + 2 * L1];
-                clmax[d] = std::max<int64_t>(clmax[d], hi - lo);
-            }
-            nlarge += d;
         } else if (dg - 1 <= kChunk && dim[v] <= 4) {
             lvars[dim[v]].push_back((int32_t)v);
             lvprog[dim[v]].push_back(leaf_prog(dg - 1));
             nlarge += dim[v];
-            // the root's two subtrees (NumPy split h = m/2 - (m/2)%8)
-            const int64_t m = dg - 1;
-            if (m > kLeafMax) {
-                const int64_t h = m / 2 - (m / 2) % kUnroll;
-                row2[dim[v]].push_back(Row2{(int32_t)v, leaf_prog(h), leaf_prog(m - h), (int32_t)h});
-                row2_ne[dim[v]] = std::max(row2_ne[dim[v]], std::max<int64_t>(1 + h, m - h));
-            } else {
-                row2_short[dim[v]] = true;
-            }
         } else {
             for (int64_t c = 0; c < dim[v]; ++c) {
                 const int32_t k = (int32_t)(zbase[v] + c);
@@ -1666,85 +1454,13 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     for (const GChunk& ch : gchunks) gcref.push_back(comp_of(ch.gi));
     for (const GWork& w : gwork) gwref.push_back(comp_of(w.gi));
     for (int c = 0; c < 3; ++c) p->nsblk[c] = (int64_t)sblk[c].size();
-    // The bulk-copy pipeline measured slower than the register kernel on the
-    // degree-4 SVM segments (0.86 vs 0.76 ms): opt-in via FGADMM_TMA=1.
-    if (getenv("FGADMM_TMA") && !sruns.empty()) {
-        // TMA pipeline: tiles of whole variables, ~256 components each
-        std::vector<STile> tiles;
-        int64_t stage = 0;
-        auto span = [](int64_t a, int64_t b) {
-            const int64_t lo = a & ~int64_t(1), hi = (b + 1) & ~int64_t(1);
-            return hi - lo;
-        };
-        for (size_t r = 0; r < sruns.size(); ++r) {
-            const SRun& R = sruns[r];
-            const int32_t per = std::max<int32_t>(1, kTmaThreads / R.d);
-            const int64_t pe = (int64_t)R.deg * R.d;
-            for (int32_t v0 = 0; v0 < R.nv; v0 += per) {
-                const int32_t nv = std::min<int32_t>(per, R.nv - v0);
-                tiles.push_back(STile{(int32_t)r, v0, nv, 0});
-                const int64_t need =
-                    2 * span(R.pb0 + v0 * pe, R.pb0 + (v0 + nv) * pe) +
-                    2 * span(R.eb0 + (int64_t)v0 * R.deg, R.eb0 + (int64_t)(v0 + nv) * R.deg) +
-                    2 * span(R.zb0 + (int64_t)v0 * R.d, R.zb0 + (int64_t)(v0 + nv) * R.d);
-                stage = std::max(stage, need);
-            }
-        }
-        const size_t smem = (size_t)stage * kTmaStages * sizeof(double);
-        if (smem <= 200 * 1024) {
-            p->ntiles = (int64_t)tiles.size();
-            p->tma_stage = (int32_t)stage;
-            p->tma_smem = smem;
-            int dev_sms = 148;
-            cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
-            const int per_sm = std::max<int>(1, (int)((200 * 1024) / std::max<size_t>(smem, 1)));
-            p->tma_grid = std::min<int64_t>(p->ntiles, (int64_t)dev_sms * std::min(per_sm, 2));
-            if ((rc = upload(&p->d_stiles, tiles))) return rc;
-            CK(cudaFuncSetAttribute(k_var_small_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kMaxDynSmem));
-        }
-    }
     for (int d = 1; d <= 4; ++d) p->nlv[d] = (int64_t)lvars[d].size();
-    // measured slower than the one-CTA unit rows (pack N=5000: d1 0.257 vs
-    // 0.192 ms, d2 0.335 vs 0.328 ms; profiles/r01_rows_ab.md): opt-in
-    p->no_row2 = getenv("FGADMM_ROW2") == nullptr;
-    p->no_pipe = getenv("FGADMM_NO_PIPE") != nullptr;
-    if (getenv("FGADMM_PIPE_BIG"))
-        for (int d = 1; d <= 4; ++d) p->pipe_big[d] = std::atoi(getenv("FGADMM_PIPE_BIG")) != 0;
-    p->pipe_deep = getenv("FGADMM_PIPE_DEEP") != nullptr;
-    {
-        // two 1280-double stages at 4 CTAs/SM: default for dim-1 rows (pack
-        // N=5000 radius rows 0.137 vs 0.157 ms); FGADMM_PIPE_TWO=1 all dims,
-        // =0 none
-        const char* e = getenv("FGADMM_PIPE_TWO");
-        for (int d = 1; d <= 4; ++d) {
-            p->pipe_two[d] = e ? (e[0] == '1') : (d == 1 && !getenv("FGADMM_PIPE_BIG") && !p->pipe_deep);
-            if (p->pipe_two[d]) p->pipe_big[d] = false;
-        }
-    }
-    if (p->pipe_deep)
-        for (int d = 1; d <= 4; ++d) p->pipe_big[d] = false;   // deep form uses the small stages
-    {
-        // two 2048-double stages at 3 CTAs/SM: default for dim >= 2 rows
-        // (pack N=5000 center rows 0.254 vs 0.264 ms for 2 x 2560 at 2/SM)
-        const char* e = getenv("FGADMM_PIPE_MID");
-        const bool dflt = !getenv("FGADMM_PIPE_BIG") && !p->pipe_deep;
-        // phase-1 copies of the mid rows marked L2 evict_last (their bytes
-        // are read again by phase 2), phase-2 copies evict_first: default
-        p->l2hint = !(getenv("FGADMM_L2HINT") && getenv("FGADMM_L2HINT")[0] == '0');
-        for (int d = 2; d <= 4; ++d)
-            if (!p->pipe_two[d] && (e ? e[0] == '1' : dflt)) {
-                p->pipe_mid[d] = true;
-                p->pipe_big[d] = false;
-            }
-    }
     {   // TMA-ring row plans, one per distinct degree and dim
         std::vector<int32_t> plans;
         std::map<std::pair<int64_t, int>, int32_t> plan_of;
         for (int d = 1; d <= 4; ++d) {
             if (p->nlv[d] == 0) continue;
-            const int64_t CH = (p->pipe_big[d] ? 2 * kPipeStageDoubles
-                                : p->pipe_mid[d] ? kPipeMidDoubles : kPipeStageDoubles) / d;
+            const int64_t CH = (d == 1 ? kPipeStageDoubles : kPipeMidDoubles) / d;
             std::vector<int32_t> offs;
             bool ok = true;
             for (size_t r = 0; r < lvars[d].size() && ok; ++r) {
@@ -1793,70 +1509,15 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
             p->pipe_ok[d] = true;
         }
         if (!plans.empty() && (rc = upload(&p->d_plans, plans))) return rc;
-        const int smem = (int)row_pipe_smem();
-        CK(cudaFuncSetAttribute(k_var_row_pipe<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        CK(cudaFuncSetAttribute(k_var_row_pipe<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        CK(cudaFuncSetAttribute(k_var_row_pipe<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        CK(cudaFuncSetAttribute(k_var_row_pipe<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        CK(cudaFuncSetAttribute(k_var_row_pipe<1, 2, kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2)));
-        CK(cudaFuncSetAttribute(k_var_row_pipe<2, 2, kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2)));
-        CK(cudaFuncSetAttribute(k_var_row_pipe<2, 2, kPipeMidDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2, kPipeMidDoubles)));
-        CK(cudaFuncSetAttribute(k_var_row_pipe<2, 2, kPipeMidDoubles, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2, kPipeMidDoubles)));
-        CK(cudaFuncSetAttribute(k_var_row_pipe<3, 2, kPipeMidDoubles, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2, kPipeMidDoubles)));
-        CK(cudaFuncSetAttribute(k_var_row_pipe<4, 2, kPipeMidDoubles, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2, kPipeMidDoubles)));
-        CK(cudaFuncSetAttribute(k_var_row_pipe<3, 2, kPipeMidDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2, kPipeMidDoubles)));
-        CK(cudaFuncSetAttribute(k_var_row_pipe<4, 2, kPipeMidDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2, kPipeMidDoubles)));
-        CK(cudaFuncSetAttribute(k_var_row_pipe<3, 2, kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2)));
-        CK(cudaFuncSetAttribute(k_var_row_pipe<4, 2, kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_pipe_smem(2)));
-        const int smem4 = (int)row_pipe_smem(4);
-        CK(cudaFuncSetAttribute(k_var_row_pipe<1, 4, kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4));
-        CK(cudaFuncSetAttribute(k_var_row_pipe<2, 4, kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4));
-        CK(cudaFuncSetAttribute(k_var_row_pipe<3, 4, kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4));
-        CK(cudaFuncSetAttribute(k_var_row_pipe<4, 4, kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem4));
-        const int smem2 = (int)row_pipe_smem(2, 2 * kPipeStageDoubles);
-        CK(cudaFuncSetAttribute(k_var_row_pipe<1, 2, 2 * kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
-        CK(cudaFuncSetAttribute(k_var_row_pipe<2, 2, 2 * kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
-        CK(cudaFuncSetAttribute(k_var_row_pipe<3, 2, 2 * kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
-        CK(cudaFuncSetAttribute(k_var_row_pipe<4, 2, 2 * kPipeStageDoubles>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
-        if (int rc2 = ring_setup<1>(p.get(), sms)) return rc2;
-        if (int rc2 = ring_setup<2>(p.get(), sms)) return rc2;
-        if (int rc2 = ring_setup<3>(p.get(), sms)) return rc2;
-        if (int rc2 = ring_setup<4>(p.get(), sms)) return rc2;
-        {
-            // default: the ring for big-stage rows (dim >= 2: 0.264 vs 0.269 ms
-            // at pack N=5000), one CTA per row for dim 1 (0.156 vs 0.159 ms)
-            const char* e = getenv("FGADMM_ROW_RING");
-            for (int d = 1; d <= 4; ++d)
-                p->row_ring[d] = e ? e[0] == '1' : p->pipe_big[d];
-        }
-    }
-    p->row_deep = getenv("FGADMM_ROW_DEEP") != nullptr;
-    for (int d = 1; d <= 4; ++d) {
-        if (p->nlv[d] == 0 || row2_short[d]) continue;
-        const size_t smem = 2 * (size_t)((row2_ne[d] * d + 3) & ~int64_t(1)) * sizeof(double);
-        if (smem > (size_t)kMaxDynSmem - 8 * 1024) continue;
-        if ((rc = upload(&p->d_row2[d], row2[d]))) return rc;
-        p->row2_smem[d] = smem;
-        cudaError_t e = cudaSuccess;
-        switch (d) {
-            case 1: e = cudaFuncSetAttribute(k_var_row2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
-            case 2: e = cudaFuncSetAttribute(k_var_row2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
-            case 3: e = cudaFuncSetAttribute(k_var_row2<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
-            case 4: e = cudaFuncSetAttribute(k_var_row2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
-        }
-        if (e != cudaSuccess) return fail(FG_ERR_CUDA, "row cluster kernel shared-memory attribute");
-        p->row2_ok[d] = true;
+        const int s1 = (int)row_pipe_smem(kPipeStageDoubles), s2 = (int)row_pipe_smem(kPipeMidDoubles);
+        CK(cudaFuncSetAttribute(k_var_row_pipe<1, kPipeStageDoubles, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1));
+        CK(cudaFuncSetAttribute(k_var_row_pipe<2, kPipeMidDoubles, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2));
+        CK(cudaFuncSetAttribute(k_var_row_pipe<3, kPipeMidDoubles, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2));
+        CK(cudaFuncSetAttribute(k_var_row_pipe<4, kPipeMidDoubles, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s2));
     }
     // node values (2 per chunk) then the staged top program (int32)
     p->gtop_smem = (int)(2 * max_top * sizeof(double) + (2 * max_top + 64) * sizeof(int32_t));
-    p->giant_fused = getenv("FGADMM_GIANT_UNFUSED") == nullptr;
-    p->row256 = getenv("FGADMM_ROW256") != nullptr;
-    p->no_fork = getenv("FGADMM_NO_FORK") != nullptr;
     if ((size_t)p->gtop_smem > 40 * 1024) {
-        CK(cudaFuncSetAttribute(k_var_giant_top<MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-        CK(cudaFuncSetAttribute(k_var_giant_top<MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
         CK(cudaFuncSetAttribute(k_var_giant_chunks<MODE_FUSED, kGiantChunkThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
         CK(cudaFuncSetAttribute(k_var_giant_chunks<MODE_PHASEZ, kGiantChunkThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
         CK(cudaFuncSetAttribute(k_var_giant_chunks<MODE_FUSED, kGiantChunkThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
@@ -1878,35 +1539,6 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     for (int d = 1; d <= 4; ++d)
         if ((rc = upload(&p->d_lvars[d], lvars[d])) || (rc = upload(&p->d_lvprog[d], lvprog[d])))
             return rc;
-    for (int d = 1; d <= 4; ++d) {
-        p->ncl[d] = (int64_t)clvars[d].size();
-        if ((rc = upload(&p->d_clvars[d], clvars[d])) || (rc = upload(&p->d_clprog[d], clprog[d])))
-            return rc;
-        p->clsmem[d] = (size_t)std::max<int64_t>(1, clmax[d]) * d * 2 * sizeof(double);
-        if (p->clsmem[d] > 200 * 1024)
-            return fail(FG_ERR_INVALID, "cluster row slice exceeds shared memory");
-        cudaError_t e1 = cudaSuccess, e2 = cudaSuccess;
-        switch (d) {
-            case 1:
-                e1 = cudaFuncSetAttribute(k_var_cluster<1, MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
-                e2 = cudaFuncSetAttribute(k_var_cluster<1, MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
-                break;
-            case 2:
-                e1 = cudaFuncSetAttribute(k_var_cluster<2, MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
-                e2 = cudaFuncSetAttribute(k_var_cluster<2, MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
-                break;
-            case 3:
-                e1 = cudaFuncSetAttribute(k_var_cluster<3, MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
-                e2 = cudaFuncSetAttribute(k_var_cluster<3, MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
-                break;
-            case 4:
-                e1 = cudaFuncSetAttribute(k_var_cluster<4, MODE_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
-                e2 = cudaFuncSetAttribute(k_var_cluster<4, MODE_PHASEZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
-                break;
-        }
-        if (e1 != cudaSuccess || e2 != cudaSuccess)
-            return fail(FG_ERR_CUDA, "cluster kernel shared-memory attribute");
-    }
     detect_svm_chain(p.get(), dim, deg, zbase, gd->z_cut_index);
     if (!p->chain_on) detect_mpc_chain(p.get(), dim, deg, zbase, pbase, ebase);
     for (auto& g : p->groups) {
@@ -1918,10 +1550,8 @@ int fg_plan_create(const fg_graph_desc* gd, const fg_group_desc* groups,
     int64_t acc_part = 0;
     for (int w = 0; w < kVarSlots; ++w) {
         p->part_off[w] = acc_part;
-        if (w == kSlotGiantChunks || w == kSlotGiantTop) continue;   // no partials
+        if (w == kSlotGiantChunks) continue;   // no partials
         acc_part += var_slot_blocks(p.get(), w);
-        // class-L rows may run on 2-CTA clusters: two partial slots per row
-        if (w >= 3 && w <= 6 && p->row2_ok[w - 2]) acc_part += var_slot_blocks(p.get(), w);
     }
     p->npart = acc_part;
     const int64_t nres = nblk(E, 256);
@@ -1946,7 +1576,7 @@ int fg_plan_forms(const fg_plan* p, int32_t* o) {
         if (g.dev.kind == FG_KIND_MPC_DYN && g.dev.dyn_gemm) o[6] = 1;
     }
     for (int d = 1; d <= 4; ++d) o[1 + d] = p->lunit[d] ? 1 : 0;
-    o[7] = p->giant_fused ? 1 : 0;
+    o[7] = 1;
     o[8] = p->mpc_chain ? p->mpc_kb : 0;
     return 0;
 }
@@ -2969,7 +2599,7 @@ int fg_profile_kernels(fg_plan* p, int64_t iterations, int32_t max_slots,
         for (auto& g : p->groups)
             if (g.dev.count > 0) names.push_back(std::string("edge_") + kind_name(g.dev.kind));
         for (int w = 0; w < kVarSlots; ++w)
-            if (var_slot_blocks(p, w) > 0 && fused_slot(p, w)) {
+            if (var_slot_blocks(p, w) > 0) {
                 vk.push_back(w);
                 names.push_back(kVarNames[w]);
             }

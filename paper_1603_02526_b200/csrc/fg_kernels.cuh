@@ -145,48 +145,6 @@ __device__ __forceinline__ void update_range(const PassB& b, const CompRef& r,
     }
 }
 
-// Class S: degree <= 32.  One thread per z component; the tail a[1:] is a
-// single NumPy leaf, summed sequentially.
-template <int MODE>
-__global__ void __launch_bounds__(256) k_var_small(PassB b, const int32_t* list,
-                                                   int64_t n, int64_t part_off) {
-    __shared__ double sm[16];
-    __shared__ int s_stop;
-    if (threadIdx.x == 0) s_stop = b.ctrl->stop;
-    __syncthreads();
-    if (s_stop) return;
-    const int64_t it = b.ctrl->iter;
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    double pp = 0.0, dd = 0.0;
-    if (t < n) {
-        const int32_t k = list[t];
-        const CompRef r = comp_ref(b, k);
-        bool bm = false, bz = false, bu = false;
-        ValFn<MODE> val(b, r, &bm);
-        double S = val(0);                           // reduceat: a[0] + tree
-        if (r.deg > 1) S = S + leaf_seq(val, 1, r.deg - 1);
-        const double zn = ddiv(S, b.zw[k]);
-        bz = !finite(zn);
-        if (MODE == MODE_FUSED) {
-            const double zo = b.zin[k];
-            b.z[k] = zn;
-            update_range(b, r, 0, r.deg, 1, zn, zo, pp, dd, bu);
-            if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
-            if (bz) flag_error(b.ctrl, it, FG_PHASE_Z, false);
-            if (bu) flag_error(b.ctrl, it, FG_PHASE_U, false);
-        } else {
-            b.z[k] = zn;
-        }
-    }
-    if (MODE == MODE_FUSED) {
-        block_sum2<256>(pp, dd, sm);
-        if (threadIdx.x == 0) {
-            b.part[2 * (part_off + blockIdx.x)] = pp;
-            b.part[2 * (part_off + blockIdx.x) + 1] = dd;
-        }
-    }
-}
-
 // Tree program layout (int32): [nu, nlev, units(2*nu: start,len),
 // level_cnt(nlev), ops(2*(nu-1): a,b)].  Node ids: units 0..nu-1, then
 // internal nodes in level order; the root is the last node.
@@ -326,10 +284,11 @@ __global__ void __launch_bounds__(NT) k_var_giant_chunks(
     }
 }
 
-// G2: one CTA per giant component: combine chunk sums along the top of the
-// tree (program whose units are chunks), then z.  A cut component (pad0 =
-// its position in the exchange vector) instead stores its local partial
-// sum in `send`; z follows after the exchange (k_cut_finalize).
+// G2 (run by the last chunk CTA of each component): combine chunk sums
+// along the top of the tree (program whose units are chunks), then z.  A
+// cut component (pad0 = its position in the exchange vector) instead
+// stores its local partial sum in `send`; z follows after the exchange
+// (k_cut_finalize).
 // Top of giant component gi's tree from its chunk sums -> z (or the cut
 // partial); one CTA, `sv` holds 2 doubles per chunk.
 template <int MODE, int NT>
@@ -382,18 +341,6 @@ __device__ void giant_top_body(const PassB& b, const int32_t* glist, const GComp
             if (!finite(zn)) flag_error(b.ctrl, it, FG_PHASE_Z, false);
         }
     }
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(kVarThreads) k_var_giant_top(
-    PassB b, const int32_t* glist, const GComp* comps, const int32_t* prog,
-    const double* csum, double* gz, double* send) {
-    extern __shared__ double sv[];
-    __shared__ int s_stop;
-    if (threadIdx.x == 0) s_stop = b.ctrl->stop;
-    __syncthreads();
-    if (s_stop) return;
-    giant_top_body<MODE>(b, glist, comps, prog, csum, gz, send, blockIdx.x, sv, b.ctrl->iter);
 }
 
 // Residuals, tolerance stop and iteration bookkeeping (engine.py:502-516)

@@ -140,10 +140,10 @@ __global__ void __launch_bounds__(256, 4) k_var_small_run(PassB b, const SRun* r
 // rank and weights in the row's LExc, k_unit_rows; rank -1 for none).
 // UNIT: rows in unit-weight form: every other weight is exactly 1, and
 // m*1, rho*dz and t*1 are exact identities, so no rho/alpha loads.
-template <int D, int MODE, int NT = kLargeThreads, bool UNIT = false, bool DEEP = false>
+template <int D, int MODE, bool UNIT = false, int NT = kLargeThreads>
 __global__ void __launch_bounds__(NT, 1024 / NT) k_var_large_vec(
     PassB b, const int32_t* vlist, const int32_t* progoff, const int32_t* prog,
-    int64_t part_off, const LExc* exc = nullptr, int64_t zero_off = -1) {
+    int64_t part_off, const LExc* exc = nullptr) {
     __shared__ double sv[D][2 * kMaxUnits];
     __shared__ double sm[2 * (NT / 32)];
     __shared__ double s_z[2][D];
@@ -272,8 +272,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_var_large_vec(
         // batches of kUB elements per thread: all loads of a batch are issued
         // before its stores (the compiler cannot prove uout aliases nothing
         // read here), one memory round trip per batch
-        constexpr int kUB = UNIT ? (DEEP ? (D == 1 ? 6 : (D == 2 ? 3 : 2)) : (D == 1 ? 4 : 2))
-                                 : (D == 1 ? 4 : 2);
+        constexpr int kUB = D == 1 ? 4 : 2;
         for (int64_t e0 = threadIdx.x; e0 < deg; e0 += kUB * NT) {
             double xr[kUB][D], ur[kUB][D], rr[kUB], ar[kUB];
 #pragma unroll
@@ -309,189 +308,6 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_var_large_vec(
         if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
         if (bu) flag_error(b.ctrl, it, FG_PHASE_U, false);
         block_sum2<NT>(pp, dd, sm);
-        if (threadIdx.x == 0) {
-            b.part[2 * (part_off + blockIdx.x)] = pp;
-            b.part[2 * (part_off + blockIdx.x) + 1] = dd;
-            if (zero_off >= 0) {          // slots reserved for the cluster form
-                b.part[2 * (zero_off + blockIdx.x)] = 0.0;
-                b.part[2 * (zero_off + blockIdx.x) + 1] = 0.0;
-            }
-        }
-    }
-}
-
-}  // namespace fg
-
-// ===========================================================================
-// Class L on a thread-block CLUSTER (degree >= kClusterMinDeg, dim <= 4).
-// The row's leaves are split over the kCluster CTAs; each CTA streams its
-// leaves once from HBM, keeps their x and u in its shared memory, and
-// writes its leaf sums into rank 0's shared memory (DSMEM).  Rank 0
-// evaluates the level-ordered tree, forms z and broadcasts it through
-// DSMEM; every CTA then updates u from shared memory.  Each payload value
-// is read from HBM exactly once per iteration.
-// ===========================================================================
-#include <cooperative_groups.h>
-
-namespace fg {
-
-constexpr int kCluster = 4;
-constexpr int kClusterThreads = 256;
-constexpr int kClusterMinDeg = 1024;
-
-template <int D, int MODE>
-__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kClusterThreads)
-k_var_cluster(PassB b, const int32_t* vlist, const int32_t* progoff, const int32_t* prog,
-              int64_t part_off) {
-    namespace cg = cooperative_groups;
-    cg::cluster_group cluster = cg::this_cluster();
-    extern __shared__ double cl_smem[];              // x then u of this CTA's elements
-    __shared__ double sv[D][2 * kMaxUnits];          // rank 0: all leaf sums + tree
-    __shared__ double sm[2 * (kClusterThreads / 32)];
-    __shared__ double s_z[2][D];
-    const int rank = (int)cluster.block_rank();
-    const int stop = b.ctrl->stop;                   // uniform over the cluster
-    if (stop) return;
-    const int64_t it = b.ctrl->iter;
-    const int32_t v = vlist[blockIdx.x / kCluster];
-    const int64_t pb = b.vt.pbase[v];
-    const int64_t eb = b.vt.ebase[v];
-    const int64_t zb = b.vt.zbase[v];
-    const int deg = b.vt.deg[v];
-    const int32_t* P = prog + progoff[blockIdx.x / kCluster];
-    const int nu = P[0], nlev = P[1];
-    const int32_t* units = P + 2;
-    const int32_t* lev = units + 2 * nu;
-    const int32_t* ops = lev + nlev;
-    // this CTA's leaves and element range (element 0 belongs to rank 0)
-    const int L0 = (int)((int64_t)nu * rank / kCluster);
-    const int L1 = (int)((int64_t)nu * (rank + 1) / kCluster);
-    const int64_t e_lo = (rank == 0) ? 0 : 1 + (int64_t)units[2 * L0];
-    const int64_t e_hi = (rank == kCluster - 1) ? deg : 1 + (int64_t)units[2 * L1];
-    const int64_t ne = e_hi - e_lo;
-    double* xs = cl_smem;
-    double* us = cl_smem + ne * D;
-    const double* msrc = (MODE == MODE_FUSED) ? b.uin : b.msrc;
-    bool bm = false, bu = false;
-    auto vals = [&](int64_t e, double* out) {        // loads, stashes, m*rho
-        const double r = b.rho[eb + e];
-        const int64_t sl = (e - e_lo) * D;
-#pragma unroll
-        for (int c = 0; c < D; ++c) {
-            const double uv = msrc[pb + e * D + c];
-            double m = uv;
-            if (MODE == MODE_FUSED) {
-                const double xv = b.x[pb + e * D + c];
-                xs[sl + c] = xv;
-                us[sl + c] = uv;
-                m = xv + uv;
-                bm |= !finite(m);
-            }
-            out[c] = m * r;
-        }
-    };
-    double* sv0 = cluster.map_shared_rank(&sv[0][0], 0);
-    // rank 0's shared memory may be written only once that CTA has started
-    // (the cluster is co-scheduled, but the model requires the barrier)
-    cluster.sync();
-    const int g = threadIdx.x >> 3, j = threadIdx.x & 7;
-    constexpr int NG = kClusterThreads / 8;
-    for (int r0 = L0; r0 < L1; r0 += NG) {           // uniform trip count
-        const int L = r0 + g;
-        int64_t s = 0, len = 0;
-        if (L < L1) { s = units[2 * L]; len = units[2 * L + 1]; }
-        const int64_t base = 1 + s;
-        const bool small = len < kUnroll;
-        const int64_t top = len - len % kUnroll;
-        double acc[D], tmp[D];
-#pragma unroll
-        for (int c = 0; c < D; ++c) acc[c] = 0.0;
-        if (small) {
-            if (j == 0)
-                for (int64_t i = 0; i < len; ++i) {
-                    vals(base + i, tmp);
-#pragma unroll
-                    for (int c = 0; c < D; ++c) acc[c] += tmp[c];
-                }
-        } else {
-            vals(base + j, acc);
-#pragma unroll 4
-            for (int64_t i = kUnroll; i < top; i += kUnroll) {
-                vals(base + i + j, tmp);
-#pragma unroll
-                for (int c = 0; c < D; ++c) acc[c] += tmp[c];
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < D; ++c) {
-            double bsum = acc[c] + __shfl_xor_sync(kFull, acc[c], 1);
-            bsum = bsum + __shfl_xor_sync(kFull, bsum, 2);
-            bsum = bsum + __shfl_xor_sync(kFull, bsum, 4);
-            if (!small) acc[c] = bsum;
-        }
-        if (!small && j == 0)
-            for (int64_t i = top; i < len; ++i) {
-                vals(base + i, tmp);
-#pragma unroll
-                for (int c = 0; c < D; ++c) acc[c] += tmp[c];
-            }
-        if (L < L1 && j == 0) {
-#pragma unroll
-            for (int c = 0; c < D; ++c) sv0[c * 2 * kMaxUnits + L] = acc[c];
-        }
-    }
-    double a0[D];
-    if (rank == 0 && threadIdx.x == 0) vals(0, a0);   // element 0: reduceat initial
-    cluster.sync();
-    if (rank == 0) {
-        int node = nu, op = 0;
-        for (int l = 0; l < nlev; ++l) {
-            const int cnt = lev[l];
-            for (int o = threadIdx.x; o < cnt * D; o += kClusterThreads) {
-                const int c = o / cnt, oo = o - c * cnt;
-                sv[c][node + oo] = sv[c][ops[2 * (op + oo)]] + sv[c][ops[2 * (op + oo) + 1]];
-            }
-            __syncthreads();
-            node += cnt;
-            op += cnt;
-        }
-        if (threadIdx.x == 0) {
-            for (int c = 0; c < D; ++c) {
-                const double zn = ddiv(a0[c] + sv[c][node - 1], b.zw[zb + c]);
-                const double zo = (MODE == MODE_FUSED) ? b.zin[zb + c] : 0.0;
-                b.z[zb + c] = zn;
-                if (MODE == MODE_FUSED && !finite(zn)) flag_error(b.ctrl, it, FG_PHASE_Z, false);
-                for (int q = 0; q < kCluster; ++q) {
-                    double* dz = cluster.map_shared_rank(&s_z[0][0], q);
-                    dz[c] = zn;
-                    dz[D + c] = zo;
-                }
-            }
-        }
-    }
-    cluster.sync();
-    if (MODE == MODE_FUSED) {
-        double zn[D], dz[D];
-#pragma unroll
-        for (int c = 0; c < D; ++c) { zn[c] = s_z[0][c]; dz[c] = zn[c] - s_z[1][c]; }
-        double pp = 0.0, dd = 0.0;
-        for (int64_t e = e_lo + threadIdx.x; e < e_hi; e += kClusterThreads) {
-            const double r = b.rho[eb + e], al = b.alpha[eb + e];
-            const int64_t sl = (e - e_lo) * D;
-#pragma unroll
-            for (int c = 0; c < D; ++c) {
-                const double t = xs[sl + c] - zn[c];
-                pp += t * t;
-                const double rd = r * dz[c];
-                dd += rd * rd;
-                const double un = us[sl + c] + t * al;
-                b.uout[pb + e * D + c] = un;
-                bu |= !finite(un);
-            }
-        }
-        if (bm) flag_error(b.ctrl, it, FG_PHASE_M, false);
-        if (bu) flag_error(b.ctrl, it, FG_PHASE_U, false);
-        block_sum2<kClusterThreads>(pp, dd, sm);
         if (threadIdx.x == 0) {
             b.part[2 * (part_off + blockIdx.x)] = pp;
             b.part[2 * (part_off + blockIdx.x) + 1] = dd;

@@ -112,12 +112,12 @@ def init_state(graph, seed=None):
     (reference ``engine.py:99-110``; host RNG so draws are identical)."""
     P = graph.total_edge_payload
     if seed is None:
-        z = np.zeros(graph.z_dim)
-        u = np.zeros(P)
-    else:
-        rng = np.random.default_rng(seed)
-        z = rng.uniform(-0.5, 0.5, graph.z_dim)
-        u = rng.uniform(-0.5, 0.5, P)
+        # z[zmap] - u = 0.0 - 0.0 = +0.0 everywhere: no zmap needed
+        return AdmmState(x=np.zeros(P), m=np.zeros(P), z=np.zeros(graph.z_dim),
+                         u=np.zeros(P), n=np.zeros(P))
+    rng = np.random.default_rng(seed)
+    z = rng.uniform(-0.5, 0.5, graph.z_dim)
+    u = rng.uniform(-0.5, 0.5, P)
     n = z[graph.zmap] - u
     return AdmmState(x=np.zeros(P), m=np.zeros(P), z=z, u=u, n=n)
 
@@ -287,9 +287,18 @@ class DevicePlan:
         rho = _native.f64(graph.edge_rho)
         alpha = _native.f64(graph.edge_alpha)
         zw = _native.f64(graph.z_weights)
+        if version is None:
+            # a graph without a parameter version (the reference's own
+            # FactorGraph): compare with the last synced copy (vectorized)
+            # instead of re-running the plan's O(E) host checks every run
+            last = getattr(self, "_synced_arrays", None)
+            if last is not None and all(np.array_equal(a, b) for a, b in
+                                        zip(last, (rho, alpha, zw))):
+                return
         _native.check(self._lib.fg_plan_sync_params(self._h, _native.dptr(rho),
                                                     _native.dptr(alpha), _native.dptr(zw)))
         self._synced_version = version
+        self._synced_arrays = (rho.copy(), alpha.copy(), zw.copy()) if version is None else None
 
     # -- fused run --------------------------------------------------------------
     def upload(self, z, u, n):

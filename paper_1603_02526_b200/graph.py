@@ -313,12 +313,11 @@ class FactorGraph:
         np.cumsum(dims, out=self.var_offsets[1:])
         self.z_dim = int(self.var_offsets[-1])
 
-        # payload position -> z position (graph.py:189-194), vectorized
-        shift = self.var_offsets[self.edge_var] - self.edge_offsets[:-1]
-        self.zmap = np.repeat(shift, payload) + np.arange(self.total_edge_payload,
-                                                          dtype=np.int64)
-        self.rho_flat = np.repeat(self.edge_rho, payload)
-        self.alpha_flat = np.repeat(self.edge_alpha, payload)
+        # zmap / rho_flat / alpha_flat (graph.py:189-204) are per payload
+        # double: built on first use (the device plan never reads them), so a
+        # large graph does not hold 3 x 8 bytes per payload double it does
+        # not need
+        self._zmap = self._rho_flat = self._alpha_flat = None
 
         # incidence in creation order and averaging weights (graph.py:206-222)
         self._incident_order = np.argsort(self.edge_var, kind="stable")
@@ -331,6 +330,31 @@ class FactorGraph:
         self.z_weights = np.repeat(wsum, dims)
         self._incident_cache = None
         return self
+
+    # ---- per-payload arrays, built on first use ----------------------------
+    def _payload_len(self):
+        return self._var_dims[self.edge_var]
+
+    @property
+    def zmap(self):
+        """Payload position -> z position (graph.py:189-194), vectorized."""
+        if self._zmap is None:
+            shift = self.var_offsets[self.edge_var] - self.edge_offsets[:-1]
+            self._zmap = np.repeat(shift, self._payload_len()) + np.arange(
+                self.total_edge_payload, dtype=np.int64)
+        return self._zmap
+
+    @property
+    def rho_flat(self):
+        if self._rho_flat is None:
+            self._rho_flat = np.repeat(self.edge_rho, self._payload_len())
+        return self._rho_flat
+
+    @property
+    def alpha_flat(self):
+        if self._alpha_flat is None:
+            self._alpha_flat = np.repeat(self.edge_alpha, self._payload_len())
+        return self._alpha_flat
 
     # ---- lazy reference views ---------------------------------------------
     @property
@@ -410,8 +434,10 @@ class FactorGraph:
         self.edge_rho[e] = rho
         self.edge_alpha[e] = alpha
         lo, hi = self.edge_offsets[e], self.edge_offsets[e + 1]
-        self.rho_flat[lo:hi] = rho
-        self.alpha_flat[lo:hi] = alpha
+        if self._rho_flat is not None:
+            self._rho_flat[lo:hi] = rho
+        if self._alpha_flat is not None:
+            self._alpha_flat[lo:hi] = alpha
         f = int(self.edge_factor[e])
         b, i = self._factor_block(f)
         j = e - int(self._factor_edge0[f])

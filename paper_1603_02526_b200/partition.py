@@ -141,10 +141,7 @@ class LocalGraph:
         self.var_offsets = np.zeros(len(dims) + 1, dtype=np.int64)
         np.cumsum(dims, out=self.var_offsets[1:])
         self.z_dim = int(self.var_offsets[-1])
-        shift = self.var_offsets[lv] - self.edge_offsets[:-1]
-        self.zmap = np.repeat(shift, payload) + np.arange(self.total_edge_payload)
-        self.rho_flat = np.repeat(self.edge_rho, payload)
-        self.alpha_flat = np.repeat(self.edge_alpha, payload)
+        self._zmap = self._rho_flat = self._alpha_flat = None   # built on first use
         # global payload positions of the local payload (for state scatter)
         gstart = graph.edge_offsets[edges]
         self.global_payload = np.repeat(gstart - self.edge_offsets[:-1], payload) + \
@@ -189,9 +186,29 @@ class LocalGraph:
         g = self._global
         self.edge_rho = np.asarray(g.edge_rho)[self.global_edge].copy()
         self.edge_alpha = np.asarray(g.edge_alpha)[self.global_edge].copy()
-        self.rho_flat = np.repeat(self.edge_rho, self._payload_len)
-        self.alpha_flat = np.repeat(self.edge_alpha, self._payload_len)
+        self._rho_flat = self._alpha_flat = None
         self.z_weights = np.asarray(g.z_weights)[self.global_z].copy()
+
+    @property
+    def zmap(self):
+        if self._zmap is None:
+            shift = self.var_offsets[self.edge_var] - self.edge_offsets[:-1]
+            self._zmap = np.repeat(shift, self._payload_len) + np.arange(self.total_edge_payload)
+        return self._zmap
+
+    @property
+    def rho_flat(self):
+        self.param_version                      # re-slice after set_edge_params
+        if self._rho_flat is None:
+            self._rho_flat = np.repeat(self.edge_rho, self._payload_len)
+        return self._rho_flat
+
+    @property
+    def alpha_flat(self):
+        self.param_version
+        if self._alpha_flat is None:
+            self._alpha_flat = np.repeat(self.edge_alpha, self._payload_len)
+        return self._alpha_flat
 
     @property
     def param_version(self):

@@ -1,0 +1,63 @@
+"""Run under torchrun (one rank per GPU): each rank runs its partition plan
+of a small packing / MPC / SVM graph through ``NcclRank`` (NCCL attached,
+cut partials all-gathered inside the captured iteration), the global state
+is gathered, and rank 0 prints one JSON line with the max relative error
+against the single-plan run.  Used by tests/test_gpu_nccl.py at world 1
+(the pool gives one GPU); the same script runs unchanged at world N."""
+
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def graph(name):
+    import paper_1603_02526_b200 as fg
+    if name == "pack":
+        return fg.build_packing(fg.PackingSpec(150))
+    if name == "mpc":
+        rng = np.random.default_rng(0)
+        A = 0.05 * rng.standard_normal((16, 16))
+        B = 0.1 * rng.standard_normal((16, 4))
+        return fg.build_mpc(fg.MpcSpec(2000, fg.LinearSystem(A, B), rng.standard_normal(16)))
+    X, y = fg.gen_gaussian_arrays(3000, 32, 4.0, seed=3)
+    return fg.build_svm(fg.SvmSpec.from_arrays(X, y))
+
+
+def main():
+    import torch.distributed as dist
+    import paper_1603_02526_b200 as fg
+    from paper_1603_02526_b200.distributed import NcclRank
+    name, iters = sys.argv[1], int(sys.argv[2])
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    g = graph(name)
+    st = fg.init_state(g, seed=7)
+    nr = NcclRank(g, rank, world, device=local)
+    nr.upload(st)
+    res, hist = nr.run(iters)
+    out = nr.gather_state(st)
+    if rank == 0:
+        single = fg.AdmmState(*(getattr(st, k).copy() for k in "xmzun"))
+        _sol, rep = fg.run(g, fg.RunConfig(max_iterations=iters), state=single)
+        err = {}
+        for k in "xmzun":
+            a, b = getattr(out, k), getattr(single, k)
+            err[k] = float(np.max(np.abs(a - b)) / max(1.0, float(np.max(np.abs(b)))))
+        print(json.dumps({"name": name, "world": world, "iterations": int(res.iterations),
+                          "ncut": int(getattr(nr.local, "ncut", 0)),
+                          "local_edges": int(len(nr.local.edge_var)),
+                          "launches": int(res.launches), "rel_err": err,
+                          "bitwise": all(np.array_equal(getattr(out, k), getattr(single, k))
+                                         for k in "xmzun"),
+                          "history_rows": int(len(hist))}))
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -54,7 +54,11 @@ def test_points_per_rank_rule(monkeypatch):
     monkeypatch.setenv("LOCAL_WORLD_SIZE", "8")
     monkeypatch.setattr(psutil, "virtual_memory", lambda: VM(2 * 2**40))
     assert bench.points_per_rank(args, 8) == 8_000_000          # 2 TB host: configs[4]
+    monkeypatch.setattr(psutil, "virtual_memory", lambda: VM(2**40))
+    assert bench.points_per_rank(args, 8) == 8_000_000          # 1 TB host: configs[4]
     monkeypatch.setattr(psutil, "virtual_memory", lambda: VM(200 * 2**30))
+    assert bench.points_per_rank(args, 8) == 2_000_000
+    monkeypatch.setattr(psutil, "virtual_memory", lambda: VM(50 * 2**30))
     assert bench.points_per_rank(args, 8) == 1_000_000          # floor
     monkeypatch.setenv("LOCAL_WORLD_SIZE", "1")
     n = bench.points_per_rank(args, 1)
