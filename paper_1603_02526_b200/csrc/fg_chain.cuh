@@ -50,6 +50,11 @@ struct ChainDev {
     const double* xx;             // per point: x.x (plan-time, margin order)
     const double* fnorm;          // per point: 1/(1+scale) (unit-weight form)
     const double* wtab;           // per point: 3 tables of the weighted form
+    // weighted form with uniform weights (every rho one value, every alpha
+    // one value, so every interior w_i / xi_i z weight one value): {rho,
+    // alpha, z weight of w_i, z weight of xi_i}; the weight lanes read it
+    // with stride 0 (an L1 hit) instead of the per-edge arrays; else null
+    const double* wuni;
 };
 
 constexpr int kChainThreads = 256;
@@ -323,19 +328,39 @@ enum : int {
 };
 
 // One interior point of the weighted form.
+// The point's loads (u rows, z of w_{i-1..i+1}, margin data, the lane
+// scalar) are issued together by the caller before the warp barrier, so a
+// point costs one memory round trip (the lane scalar used to be a second,
+// dependent one).
+struct ChainWLoads {
+    double u0, u1, u2, u3, up, un_, zi, zp, zn_, X;
+};
+
+template <int D>
+__device__ __forceinline__ ChainWLoads chain_w_load(const PassB& b, const ChainDev& c,
+                                                   int32_t i, int lane) {
+    const double* __restrict__ U = b.uin + c.pW + (int64_t)(4 * i - 1) * D + lane;
+    const double* __restrict__ Z = b.zin + c.zW + (int64_t)i * D + lane;
+    ChainWLoads L;
+    L.u0 = U[0]; L.u1 = U[D]; L.u2 = U[2 * D]; L.u3 = U[3 * D];
+    L.up = U[-D]; L.un_ = U[6 * D];
+    L.zi = Z[0]; L.zp = Z[-D]; L.zn_ = Z[D];
+    L.X = c.fp_margin[(int64_t)i * c.st_margin + lane];
+    return L;
+}
+
 template <int D>
 __device__ __forceinline__ void chain_w_point(const PassB& b, const ChainDev& c, int32_t i,
                                               int lane, double* sc, double* su,
+                                              const ChainWLoads& L,
                                               double* xb_out, double& pp, double& dd,
                                               unsigned& bad) {
     const int64_t wo = c.pW + (int64_t)(4 * i - 1) * D + lane;
-    const double* __restrict__ U = b.uin + wo;
     const int64_t zo = c.zW + (int64_t)i * D + lane;
-    const double* __restrict__ Z = b.zin + zo;
-    double u0 = U[0], u1 = U[D], u2 = U[2 * D], u3 = U[3 * D];
-    const double up = U[-D], un_ = U[6 * D];
-    const double zi = Z[0], zp = Z[-D], zn_ = Z[D];
-    const double X = c.fp_margin[(int64_t)i * c.st_margin + lane];
+    double u0 = L.u0, u1 = L.u1, u2 = L.u2, u3 = L.u3;
+    const double up = L.up, un_ = L.un_;
+    const double zi = L.zi, zp = L.zp, zn_ = L.zn_;
+    const double X = L.X;
     // u rows parked in shared memory across the divisions (registers)
     su[0] = u0; su[32] = u1; su[64] = u2; su[96] = u3;
     // ---- phase n ----
@@ -477,6 +502,17 @@ __global__ void __launch_bounds__(kChainThreads, FG_CHAIN_W_MINB) k_svm_chain_w(
             case kWZWW: sb = b.zw + c.zW; ss = D; break;
             default: break;
         }
+        if (c.wuni) {                                  // uniform weights: stride 0
+            switch (lane) {
+                case 0: case 1: case 2: case 3: case kWRP: case kWRN: case kWRX0: case kWRX1:
+                case kWRB: sb = c.wuni; ss = 0; break;
+                case 4: case 5: case 6: case 7: case kWAX0: case kWAX1:
+                    sb = c.wuni + 1; ss = 0; break;
+                case kWZWW: sb = c.wuni + 2; ss = 0; break;
+                case kWZWX: sb = c.wuni + 3; ss = 0; break;
+                default: break;
+            }
+        }
         s_sb[lane] = sb;
         s_ss[lane] = ss;
     }
@@ -487,11 +523,12 @@ __global__ void __launch_bounds__(kChainThreads, FG_CHAIN_W_MINB) k_svm_chain_w(
     constexpr int32_t NW = kChainThreads / 32;
 #pragma unroll 1
     for (int32_t i = i0 + warp; i < i1; i += NW) {
+        const ChainWLoads L = chain_w_load<D>(b, c, i, lane);
         const double sv = s_sb[lane][(int64_t)i * s_ss[lane]];
         __syncwarp();                                  // previous point's reads done
         sc[lane] = sv;
         __syncwarp();
-        chain_w_point<D>(b, c, i, lane, sc, &s_u[warp][0][lane], xb_out, pp, dd, bad);
+        chain_w_point<D>(b, c, i, lane, sc, &s_u[warp][0][lane], L, xb_out, pp, dd, bad);
     }
     if (bad & 1u) flag_error(b.ctrl, it - 1, FG_PHASE_N, true);
     if (bad & 2u) flag_error(b.ctrl, it, FG_PHASE_X, true);

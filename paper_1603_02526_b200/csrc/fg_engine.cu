@@ -258,6 +258,7 @@ struct fg_plan {
     double* d_chain_xx = nullptr;      // per point x.x of the margin data
     double* d_chain_fnorm = nullptr;   // per point 1/(1+scale) (unit form)
     double* d_chain_wtab = nullptr;    // 3 x n per-point tables (weighted form)
+    double* d_chain_wuni = nullptr;    // {rho, alpha, zw_w, zw_xi} when uniform
     int32_t* d_flag = nullptr;         // scratch device flag
     unsigned long long* d_bad = nullptr;  // first non-finite ref index of a download
     int32_t* h_stop = nullptr;         // pinned stop-flag slots polled by fg_run
@@ -307,7 +308,7 @@ fg_plan::~fg_plan() {
                     d_lvars[4], d_lvprog[1], d_lvprog[2], d_lvprog[3], d_lvprog[4],
                     d_llist, d_lprog, d_prog, d_glist, d_gchunks, d_gcomps,
                     d_gwork, d_gcref, d_gwref, d_csum, d_gz, d_part, d_res2, d_ctrl, d_hist, d_chain_xx,
-                    d_chain_fnorm, d_chain_wtab, d_flag, d_bad, d_gcnt, d_ucnt, d_lexc[1], d_lexc[2], d_lexc[3],
+                    d_chain_fnorm, d_chain_wtab, d_chain_wuni, d_flag, d_bad, d_gcnt, d_ucnt, d_lexc[1], d_lexc[2], d_lexc[3],
                     d_lexc[4],
                     d_planoff[1], d_planoff[2], d_planoff[3], d_planoff[4], d_plans,
                     d_rowdesc[1], d_rowdesc[2], d_rowdesc[3], d_rowdesc[4],
@@ -625,7 +626,8 @@ void chain_pass(fg_plan* p, int in, cudaStream_t st) {
             p->d_zb[in], p->d_rho, p->d_alpha, p->d_zw, p->d_ctrl, p->d_part, p->d_zvar};
     if (p->mpc_chain) {
         // with reduce_fused the last CTA also runs the residual reduction
-        const FusedReduce fr = p->mpc_reduce_fused
+        // (not on an NCCL rank: part_mid / part_post reduce across ranks)
+        const FusedReduce fr = p->mpc_reduce_fused && !p->nccl_comm
             ? FusedReduce{p->d_ucnt, p->npart, p->mpc_tiles, p->chain_grid, p->d_hist}
             : FusedReduce{nullptr, 0, 0, 0, nullptr};
         if (p->mpc.n0 == 20 && p->mpc.d == 16)         // configs[2]: state 16, input 4
@@ -868,6 +870,8 @@ void detect_svm_chain(fg_plan* p, const std::vector<int32_t>& dim,
     k_chain_fnorm<<<(unsigned)((n + 255) / 256), 256, 0, p->stream>>>(c, p->d_chain_fnorm);
     if (cudaMalloc((void**)&p->d_chain_wtab, 3 * n * sizeof(double)) != cudaSuccess) return;
     c.wtab = p->d_chain_wtab;
+    if (cudaMalloc((void**)&p->d_chain_wuni, 4 * sizeof(double)) != cudaSuccess) return;
+    c.wuni = nullptr;                  // set at sync when the weights are uniform
     if (cudaStreamSynchronize(p->stream) != cudaSuccess) return;
     p->chain_fast = D == 32 && n >= 3 && p->chain_grid >= 2 && !getenv("FGADMM_CHAIN_GENERIC");
     p->chain_on = p->chain_grid > 0;
@@ -1656,6 +1660,20 @@ int fg_plan_sync_params(fg_plan* p, const double* rho, const double* alpha,
             for (int k = 1; k < c.D && wok; ++k) wok = zw[c.zW + i * c.D + k] == zw[c.zW + i * c.D];
         if (wok)
             k_chain_wtab<<<(unsigned)((c.n + 255) / 256), 256, 0, st>>>(c, p->d_rho, p->d_chain_wtab);
+        // uniform weights: the weighted form reads them from a 4-double table
+        bool uni = wok && p->d_chain_wuni != nullptr && c.n >= 3;
+        for (int64_t e = 1; e < p->E && uni; ++e) uni = rho[e] == rho[0] && alpha[e] == alpha[0];
+        const double zww = uni ? zw[c.zW + c.D] : 0.0, zwx = uni ? zw[c.zX + 1] : 0.0;
+        for (int64_t i = 1; i + 1 < c.n && uni; ++i) uni = zw[c.zW + i * c.D] == zww && zw[c.zX + i] == zwx;
+        if (uni) {
+            const double h[4] = {rho[0], alpha[0], zww, zwx};
+            CK(cudaMemcpyAsync(p->d_chain_wuni, h, sizeof(h), cudaMemcpyHostToDevice, st));
+        }
+        if ((uni ? p->d_chain_wuni : nullptr) != p->chain.wuni) {
+            p->chain.wuni = uni ? p->d_chain_wuni : nullptr;
+            for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
+            p->graphs.clear();
+        }
         if (unit != p->chain_unit || wok != p->chain_wok) {
             p->chain_unit = unit;
             p->chain_wok = wok;

@@ -1,6 +1,8 @@
 """Per-launch DRAM traffic of each profiled kernel -> profiles/traffic.json.
 
-usage: python tools/traffic_json.py profiles/traffic.json svm1m=gpurun_out/final_svm1m.ncu-rep ...
+usage: python tools/traffic_json.py profiles/traffic.json svm1m=<report.ncu-rep | raw.csv> ...
+(a .csv is an `ncu -i <rep> --page raw --csv` export, as tools/r02_evidence.sh
+writes on the GPU box)
 bench.py reads the file to fill roofline.traffic (ncu --set full capture:
 dram__bytes_read.sum + dram__bytes_write.sum of one launch)."""
 import csv
@@ -11,20 +13,25 @@ import sys
 
 # bench.py kernel label -> ncu kernel-name prefix
 LABELS = {
-    "chain_svm": "void k_svm_chain_unit",
+    "chain_svm": ("void k_svm_chain_unit", "void k_svm_chain_w"),
     "edge_collision": "void k_collision_tiles_v3",
-    "var_large_d1": ("void k_var_row_pipe<1", "void k_var_row_ring<1"),
-    "var_large_d2": ("void k_var_row_pipe<2", "void k_var_row_ring<2"),
+    "var_large_d1": "void k_var_row_pipe<1",
+    "var_large_d2": "void k_var_row_pipe<2",
     "edge_mpc_dyn": "void k_mpc_dyn_gemm",
     "var_small_deg4": "void k_var_small_run<4,",
     "var_giant_chunks": "void k_var_giant_chunks",
     "chain_mpc": "void k_mpc_chain",
+    "chain_mpc_block": "void k_mpc_block<",
 }
 
 
 def traffic(path):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    if path.endswith(".csv"):
+        with open(path) as fh:
+            raw = fh.read()
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     out = {}
