@@ -128,7 +128,8 @@ def kernel_bytes(graph, plan):
     out["reduce"] = 16 * (plan.info["small_components"] // 256 + 1
                           + plan.info["large_components"] + 64)
     if plan.info.get("fused_chain"):
-        out["chain_svm"] = chain_bytes(graph, dims, deg, plan.chain_form() == "unit")
+        out["chain_svm"] = chain_bytes(graph, dims, deg, plan.chain_form() == "unit",
+                                       forms.get("chain_uniform", False))
     if forms["chain"] == "mpc":
         # fused MPC chain: u read + write per payload double, z read +
         # write per component, the cost diagonal per component
@@ -141,7 +142,7 @@ def kernel_bytes(graph, plan):
     return out
 
 
-def chain_bytes(graph, dims, deg, unit):
+def chain_bytes(graph, dims, deg, unit, uniform=False):
     """Compulsory bytes of one fused SVM-chain launch (csrc/fg_chain.cuh):
     per weight copy w_i (dim D, degree 3-4) u read+write and z read+write;
     per slack xi_i the same at dim 1, degree 2; per point the margin data
@@ -149,8 +150,10 @@ def chain_bytes(graph, dims, deg, unit):
     The weighted form also reads rho and alpha per edge of w_i and xi_i, one
     z weight per variable (w_i's is shared by its D components), b's rho
     and three per-point tables (norm factor, slack threshold, margin
-    denominator); the unit-weight form reads none of them.  Neighbours'
-    equality edges are re-reads of the same arrays (L2), not counted."""
+    denominator); the unit-weight form reads none of them, and with uniform
+    weights the weighted form reads the weights from a 4-double table
+    (only the per-point tables are streamed).  Neighbours' equality edges
+    are re-reads of the same arrays (L2), not counted."""
     n = int(np.sum(deg == 2))                  # xi's (b has degree n > 32)
     wsel = (deg >= 3) & (deg <= 4)
     P_w = int(np.sum(deg[wsel] * dims[wsel]))
@@ -158,9 +161,10 @@ def chain_bytes(graph, dims, deg, unit):
     E_w = int(np.sum(deg[wsel]))
     V_w = int(np.sum(wsel))
     D = int(dims[wsel][0]) if wsel.any() else 0
-    w = P_w * 16 + Z_w * 16 + (0 if unit else E_w * 16 + V_w * 8)
-    xi = n * (2 * 16 + 16 + (0 if unit else 2 * 16 + 8))
-    per_point = (D + 1) * 8 + 3 * 8 + 8 + 8 + (0 if unit else 8 + 3 * 8)
+    weights = not unit and not uniform
+    w = P_w * 16 + Z_w * 16 + (E_w * 16 + V_w * 8 if weights else 0)
+    xi = n * (2 * 16 + 16 + (2 * 16 + 8 if weights else 0))
+    per_point = (D + 1) * 8 + 3 * 8 + 8 + 8 + (8 if weights else 0) + (0 if unit else 3 * 8)
     return w + xi + n * per_point
 
 

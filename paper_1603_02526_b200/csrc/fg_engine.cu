@@ -1580,7 +1580,7 @@ int fg_plan_forms(const fg_plan* p, int32_t* o) {
         if (g.dev.kind == FG_KIND_MPC_DYN && g.dev.dyn_gemm) o[6] = 1;
     }
     for (int d = 1; d <= 4; ++d) o[1 + d] = p->lunit[d] ? 1 : 0;
-    o[7] = 1;
+    o[7] = p->chain.wuni != nullptr ? 1 : 0;
     o[8] = p->mpc_chain ? p->mpc_kb : 0;
     return 0;
 }

@@ -380,13 +380,14 @@ class DevicePlan:
     def forms(self):
         """Kernel forms of the next run (fg_plan_forms): chain form,
         unit-weight collision tiles / class-L rows per dim, mpc_dyn matrix
-        form, fused giant kernels."""
+        form, uniform-weight table of the weighted SVM chain, MPC block
+        length."""
         o = (C.c_int32 * 9)()
         self._lib.fg_plan_forms(self._h, o)
         return {"chain": ("off", "generic", "fast", "unit", "mpc")[o[0]],
                 "collision_unit": bool(o[1]),
                 "rows_unit": {d: bool(o[1 + d]) for d in (1, 2, 3, 4)},
-                "mpc_dyn_matrix": bool(o[6]), "giant_fused": bool(o[7]),
+                "mpc_dyn_matrix": bool(o[6]), "chain_uniform": bool(o[7]),
                 "mpc_block": int(o[8])}
 
     def chain_form(self):

@@ -162,6 +162,11 @@ def test_chain_general_weights_bitwise(gpu, monkeypatch, rho, alpha):
     g = fg.build_svm(fg.SvmSpec.from_arrays(X, y, rho=rho, alpha=alpha))
     st = fg.init_state(g, seed=6)
     (sc, _), (sg, _) = run_both(g, st, monkeypatch, [fg.RunConfig(max_iterations=8)])
+    plan_for(g, monkeypatch, True).sync(g)
+    forms = _PLANS[g].forms()
+    # one rho and one alpha everywhere: the weight lanes read the 4-double
+    # uniform table (unit weights take the unit form instead)
+    assert forms["chain"] == "fast" and forms["chain_uniform"]
     for k in "xmzun":
         np.testing.assert_array_equal(getattr(sc, k), getattr(sg, k), err_msg=k)
 
@@ -178,7 +183,7 @@ def test_chain_random_edge_weights_bitwise_and_oracle(gpu, monkeypatch):
     st = fg.init_state(g, seed=8)
     (sc, _), (sg, _) = run_both(g, st, monkeypatch, [fg.RunConfig(max_iterations=9)])
     plan_for(g, monkeypatch, True).sync(g)
-    assert _PLANS[g].chain_form() == "fast"
+    assert _PLANS[g].chain_form() == "fast" and not _PLANS[g].forms()["chain_uniform"]
     for k in "xmzun":
         np.testing.assert_array_equal(getattr(sc, k), getattr(sg, k), err_msg=k)
     so, _h, _ = O.run(g, 9, st)
