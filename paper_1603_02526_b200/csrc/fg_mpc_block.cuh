@@ -30,10 +30,16 @@ namespace fg {
 
 constexpr int kMpcKB = 5;                              // iterations per launch (odd)
 constexpr int kMpcKBTail = 3;                          // shorter block for a run's tail
-constexpr int kMbF = 64;                               // factor slots (gemm lanes)
+constexpr int kMbF = 64;                               // factor slots
 constexpr int kMbThreads = kEdgeThreads;               // 256
-constexpr int kMbRG = kMbThreads / kMbF;               // 4 row groups
-constexpr int kMbKH = (kDynGemmMaxCols + kMbRG - 1) / kMbRG;
+// K nv register tile: a thread computes 2 factors (lane, lane + 32) x the 5
+// rows r0 + 8k of its warp r0, so per column it loads 2 nv values (lane-
+// distinct) and 5 K values (warp-uniform broadcasts) for 10 FMAs: 9
+// shared-memory wavefronts instead of 12 for the 1-factor x 10-row tile
+// (ncu: the block kernel is bound by the shared-memory pipe).  Every
+// output is the same fma chain over the columns in the same order.
+constexpr int kMbRG = kMbThreads / 32;                 // 8 row groups (one per warp)
+constexpr int kMbKH = (kDynGemmMaxCols + kMbRG - 1) / kMbRG;   // 5 rows per thread
 constexpr int kMbNN = kMbF + 1;                        // nodes staged per CTA (tile + 2 KB)
 
 inline size_t mpc_block_smem(int n0, int d) {
@@ -110,26 +116,29 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mpc_block(PassB b, MpcChainDe
         }
         __syncthreads();
         {   // v = K nv: the fma chain of k_mpc_chain / k_mpc_dyn_gemm
-            const int fl = threadIdx.x % kMbF, r0 = threadIdx.x / kMbF;
-            if (fl < nf) {
-                double acc[KH];
+            const int fa = threadIdx.x & 31, fb = fa + 32, r0 = threadIdx.x >> 5;
+            const bool ha = fa < nf, hb = fb < nf;
+            double aa[KH], ab[KH];
 #pragma unroll
-                for (int k = 0; k < KH; ++k) acc[k] = 0.0;
-                const double* nvf = nvs + fl * ld;
-                for (int cc = 0; cc < cols; ++cc) {
-                    const double v = nvf[cc];
-                    const double2* kc = reinterpret_cast<const double2*>(Ks + (cc * RG + r0) * KH);
-#pragma unroll
-                    for (int k2 = 0; k2 < KH / 2; ++k2) {
-                        const double2 kk = kc[k2];
-                        acc[2 * k2] = __fma_rn(kk.x, v, acc[2 * k2]);
-                        acc[2 * k2 + 1] = __fma_rn(kk.y, v, acc[2 * k2 + 1]);
-                    }
-                }
+            for (int k = 0; k < KH; ++k) aa[k] = ab[k] = 0.0;
+            const double* nva = nvs + (ha ? fa : 0) * ld;
+            const double* nvb = nvs + (hb ? fb : 0) * ld;
+            for (int cc = 0; cc < cols; ++cc) {
+                const double va = nva[cc], vb = nvb[cc];
+                const double* kc = Ks + (cc * RG + r0) * KH;
 #pragma unroll
                 for (int k = 0; k < KH; ++k) {
-                    const int r = r0 + RG * k;
-                    if (r < cols) outs[fl * ldo + r] = acc[k];
+                    const double kk = kc[k];
+                    aa[k] = __fma_rn(kk, va, aa[k]);
+                    ab[k] = __fma_rn(kk, vb, ab[k]);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < KH; ++k) {
+                const int r = r0 + RG * k;
+                if (r < cols) {
+                    if (ha) outs[fa * ldo + r] = aa[k];
+                    if (hb) outs[fb * ldo + r] = ab[k];
                 }
             }
         }
