@@ -510,7 +510,24 @@ bool var_kernel(fg_plan* p, int which, const double* zin, double* zout, const do
 template <int MODE>
 void var_pass(fg_plan* p, const double* zin, double* zout, const double* uin, double* uout,
               const double* msrc, cudaStream_t st) {
-    for (int w = 0; w < kVarSlots; ++w) var_kernel<MODE>(p, w, zin, zout, uin, uout, msrc, st);
+    // class-L rows of dim 1 and of dim >= 2 are different variables: the
+    // dim-1 rows run on the forked stream concurrently with the others (a
+    // parallel branch of the captured graph), so each kernel's tail and
+    // launch gap hides under the other; joined before the giant classes
+    // (whose last CTA may run the residual reduction)
+    const bool fork = MODE == MODE_FUSED && var_slot_blocks(p, 3) > 0 &&
+                      (var_slot_blocks(p, 4) > 0 || var_slot_blocks(p, 5) > 0 ||
+                       var_slot_blocks(p, 6) > 0 || var_slot_blocks(p, 7) > 0);
+    if (fork) {
+        cudaEventRecord(p->ev_fork, st);
+        cudaStreamWaitEvent(p->stream2, p->ev_fork, 0);
+        var_kernel<MODE>(p, 3, zin, zout, uin, uout, msrc, p->stream2);
+        cudaEventRecord(p->ev_join, p->stream2);
+    }
+    for (int w = 0; w < kVarSlots; ++w) {
+        if (fork && w == kSlotGiantChunks) cudaStreamWaitEvent(st, p->ev_join, 0);
+        if (!(fork && w == 3)) var_kernel<MODE>(p, w, zin, zout, uin, uout, msrc, st);
+    }
 }
 
 const char* kind_name(int kind) {
