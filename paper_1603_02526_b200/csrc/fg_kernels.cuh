@@ -346,6 +346,8 @@ __device__ void giant_top_body(const PassB& b, const int32_t* glist, const GComp
 // Residuals, tolerance stop and iteration bookkeeping (engine.py:502-516)
 // over partial slots [0, npart) minus [skip_lo, skip_hi), by one CTA of NT
 // threads.
+__device__ __forceinline__ void reduce_commit(Ctrl* c, double a, double bsum, double* hist);
+
 template <int NT>
 __device__ void reduce_body(Ctrl* c, const double* part, int64_t npart, double* hist,
                             int64_t skip_lo, int64_t skip_hi, double* sm) {
@@ -356,7 +358,13 @@ __device__ void reduce_body(Ctrl* c, const double* part, int64_t npart, double* 
         bsum += __ldcg(part + 2 * i + 1);
     }
     block_sum2<NT>(a, bsum, sm);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) reduce_commit(c, a, bsum, hist);
+}
+
+// Thread 0's part of reduce_body: residual norms, history row, completion,
+// stop decision and the iteration counter from the two summed partials.
+__device__ __forceinline__ void reduce_commit(Ctrl* c, double a, double bsum, double* hist) {
+    {
         const int64_t it = c->iter;
         const double primal = sqrt(a) * c->scale;
         const double dual = sqrt(bsum) * c->scale;
