@@ -346,43 +346,86 @@ __device__ void giant_top_body(const PassB& b, const int32_t* glist, const GComp
 // Residuals, tolerance stop and iteration bookkeeping (engine.py:502-516)
 // over partial slots [0, npart) minus [skip_lo, skip_hi), by one CTA of NT
 // threads.
-__device__ __forceinline__ void reduce_commit(Ctrl* c, double a, double bsum, double* hist);
+// The control fields the commit reads, loaded by thread 0 BEFORE the
+// partial sums so their round trip overlaps the partials' loads.
+struct CtrlIn {
+    int64_t it;
+    double scale, ptol, dtol;
+    bool err;
+};
+__device__ __forceinline__ CtrlIn ctrl_in(const Ctrl* c) {
+    CtrlIn r;
+    r.it = c->iter;
+    r.scale = c->scale;
+    r.ptol = c->primal_tol;
+    r.dtol = c->dual_tol;
+    r.err = c->err_key != ~0ull;
+    return r;
+}
 
+// Thread 0's part of the reduction: residual norms, history row,
+// completion, stop decision and the iteration counter from the two summed
+// partials.
+__device__ __forceinline__ void reduce_commit(Ctrl* c, const CtrlIn& in, double a, double bsum,
+                                              double* hist) {
+    const int64_t it = in.it;
+    const double primal = sqrt(a) * in.scale;
+    const double dual = sqrt(bsum) * in.scale;
+    c->primal = primal;
+    c->dual = dual;
+    if (hist) { hist[2 * (it - 1)] = primal; hist[2 * (it - 1) + 1] = dual; }
+    c->completed = it;
+    if (in.err) {
+        c->stop = 1;
+    } else {
+        const bool pc = in.ptol > 0.0, dc = in.dtol > 0.0;
+        bool ok = pc || dc;
+        if (pc) ok = ok && (primal <= in.ptol);
+        if (dc) ok = ok && (dual <= in.dtol);
+        if (ok) { c->converged = 1; c->stop = 1; }
+    }
+    c->iter = it + 1;
+}
+
+// Residuals, tolerance stop and iteration bookkeeping (engine.py:502-516)
+// over partial slots [0, npart) minus [skip_lo, skip_hi), by one CTA of NT
+// threads.  Each thread sums its slots in index order (loads unrolled by
+// 4, additions in the same order), then the fixed block tree.
 template <int NT>
 __device__ void reduce_body(Ctrl* c, const double* part, int64_t npart, double* hist,
                             int64_t skip_lo, int64_t skip_hi, double* sm) {
+    CtrlIn in{};
+    if (threadIdx.x == 0) in = ctrl_in(c);
     double a = 0.0, bsum = 0.0;
-    for (int64_t i = threadIdx.x; i < npart; i += NT) {
-        if (i >= skip_lo && i < skip_hi) continue;
-        a += __ldcg(part + 2 * i);
-        bsum += __ldcg(part + 2 * i + 1);
-    }
-    block_sum2<NT>(a, bsum, sm);
-    if (threadIdx.x == 0) reduce_commit(c, a, bsum, hist);
-}
-
-// Thread 0's part of reduce_body: residual norms, history row, completion,
-// stop decision and the iteration counter from the two summed partials.
-__device__ __forceinline__ void reduce_commit(Ctrl* c, double a, double bsum, double* hist) {
-    {
-        const int64_t it = c->iter;
-        const double primal = sqrt(a) * c->scale;
-        const double dual = sqrt(bsum) * c->scale;
-        c->primal = primal;
-        c->dual = dual;
-        if (hist) { hist[2 * (it - 1)] = primal; hist[2 * (it - 1) + 1] = dual; }
-        c->completed = it;
-        if (c->err_key != ~0ull) {
-            c->stop = 1;
-        } else {
-            const bool pc = c->primal_tol > 0.0, dc = c->dual_tol > 0.0;
-            bool ok = pc || dc;
-            if (pc) ok = ok && (primal <= c->primal_tol);
-            if (dc) ok = ok && (dual <= c->dual_tol);
-            if (ok) { c->converged = 1; c->stop = 1; }
+    // slots i = tid, tid + NT, ... below `hi`, loads 4 at a time
+    auto range = [&](int64_t i, int64_t hi) {
+        for (; i + 3 * NT < hi; i += 4 * NT) {
+            double v[8];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                v[2 * k] = __ldcg(part + 2 * (i + k * NT));
+                v[2 * k + 1] = __ldcg(part + 2 * (i + k * NT) + 1);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                a += v[2 * k];
+                bsum += v[2 * k + 1];
+            }
         }
-        c->iter = it + 1;
+        for (; i < hi; i += NT) {
+            a += __ldcg(part + 2 * i);
+            bsum += __ldcg(part + 2 * i + 1);
+        }
+        return i;
+    };
+    int64_t i = threadIdx.x;
+    if (skip_hi > skip_lo) {
+        i = range(i, skip_lo < npart ? skip_lo : npart);
+        if (i < skip_hi) i += (skip_hi - i + NT - 1) / NT * NT;   // same progression
     }
+    range(i, npart);
+    block_sum2<NT>(a, bsum, sm);
+    if (threadIdx.x == 0) reduce_commit(c, in, a, bsum, hist);
 }
 
 // Optional fused reduction: the last CTA of the update runs reduce_body

@@ -257,42 +257,18 @@ __global__ void __launch_bounds__(1024) k_mpc_block_reduce(Ctrl* c, const double
         }
     }
     // thread 0 keeps the control block in registers across the KB commits
-    // (reduce_commit's logic; no other kernel runs in between)
-    int64_t it = 0;
-    double scale = 0.0, ptol = 0.0, dtol = 0.0, primal = 0.0, dual = 0.0;
-    bool err = false, conv = false, stop = false;
-    if (threadIdx.x == 0) {
-        it = c->iter; scale = c->scale; ptol = c->primal_tol; dtol = c->dual_tol;
-        err = c->err_key != ~0ull;
-    }
+    // (reduce_commit per iteration; no other kernel runs in between)
+    CtrlIn in{};
+    if (threadIdx.x == 0) in = ctrl_in(c);
 #pragma unroll
     for (int k = 0; k < kMpcKB; ++k) {
         if (k < kb) {
             block_sum2<1024>(a[k], bs[k], sm);
             if (threadIdx.x == 0) {
-                primal = sqrt(a[k]) * scale;
-                dual = sqrt(bs[k]) * scale;
-                if (hist) { hist[2 * (it - 1)] = primal; hist[2 * (it - 1) + 1] = dual; }
-                if (err) {
-                    stop = true;
-                } else {
-                    const bool pc = ptol > 0.0, dc = dtol > 0.0;
-                    bool ok = pc || dc;
-                    if (pc) ok = ok && (primal <= ptol);
-                    if (dc) ok = ok && (dual <= dtol);
-                    if (ok) { conv = true; stop = true; }
-                }
-                ++it;
+                reduce_commit(c, in, a[k], bs[k], hist);
+                ++in.it;
             }
         }
-    }
-    if (threadIdx.x == 0) {
-        c->primal = primal;
-        c->dual = dual;
-        c->completed = it - 1;
-        if (conv) c->converged = 1;
-        if (stop) c->stop = 1;
-        c->iter = it;
     }
 }
 
