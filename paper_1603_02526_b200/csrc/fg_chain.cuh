@@ -50,12 +50,22 @@ struct ChainDev {
     const double* xx;             // per point: x.x (plan-time, margin order)
     const double* fnorm;          // per point: 1/(1+scale) (unit-weight form)
     const double* wtab;           // per point: 3 tables of the weighted form
-    // weighted form with uniform weights (every rho one value, every alpha
-    // one value, so every interior w_i / xi_i z weight one value): {rho,
-    // alpha, z weight of w_i, z weight of xi_i}; the weight lanes read it
-    // with stride 0 (an L1 hit) instead of the per-edge arrays; else null
-    const double* wuni;
 };
+
+// Weighted form with uniform weights (every rho one value r, every alpha one
+// value a, so every interior w_i / xi_i z weight one value): the weights are
+// kernel arguments instead of per-point lane scalars, and each division by
+// a constant divisor carries its exact power-of-two inverse (0: none).
+struct WUni {
+    double r, a, zww, zwx;        // rho, alpha, z weight of w_i, of xi_i
+    double inv2r, invr, invzww, invzwx;
+};
+
+// x / y with the caller's exact power-of-two inverse of y (ddivq's test
+// made once per run): bitwise ddivq(x, y)
+__device__ __forceinline__ double dq_c(double x, double y, double inv) {
+    return inv != 0.0 ? x * inv : qdiv(x, y);
+}
 
 constexpr int kChainThreads = 256;
 #ifndef FG_CHAIN_W_MINB
@@ -349,12 +359,18 @@ __device__ __forceinline__ ChainWLoads chain_w_load(const PassB& b, const ChainD
     return L;
 }
 
-template <int D>
+template <int D, bool UNI>
 __device__ __forceinline__ void chain_w_point(const PassB& b, const ChainDev& c, int32_t i,
                                               int lane, double* sc, double* su,
-                                              const ChainWLoads& L,
+                                              const ChainWLoads& L, const WUni& W,
                                               double* xb_out, double& pp, double& dd,
                                               unsigned& bad) {
+    // weights: kernel arguments (UNI) or the point's lane scalars
+    auto WR = [&](int k) { return UNI ? W.r : sc[kWR + k]; };
+    auto WA = [&](int k) { return UNI ? W.a : sc[kWA + k]; };
+    auto WS = [&](int slot) { return UNI ? (slot == kWZWW ? W.zww : slot == kWZWX ? W.zwx
+                                            : (slot == kWAX0 || slot == kWAX1) ? W.a : W.r)
+                                         : sc[slot]; };
     const int64_t wo = c.pW + (int64_t)(4 * i - 1) * D + lane;
     const int64_t zo = c.zW + (int64_t)i * D + lane;
     double u0 = L.u0, u1 = L.u1, u2 = L.u2, u3 = L.u3;
@@ -376,9 +392,14 @@ __device__ __forceinline__ void chain_w_point(const PassB& b, const ChainDev& c,
             bad |= 1u;
     }
     // ---- phase x (equalities first: their inputs die early) ----
-    const double x2 = ddivq(sc[kWRP] * np_ + sc[kWR + 2] * n2,
-                            sc[kWRP] + sc[kWR + 2]);                 // prox_equality
-    const double x3 = ddivq(sc[kWR + 3] * n3 + sc[kWRN] * nn_, sc[kWR + 3] + sc[kWRN]);
+    double x2, x3;
+    if (UNI) {                                                    // prox_equality
+        x2 = dq_c(W.r * np_ + W.r * n2, W.r + W.r, W.inv2r);
+        x3 = dq_c(W.r * n3 + W.r * nn_, W.r + W.r, W.inv2r);
+    } else {
+        x2 = ddivq(sc[kWRP] * np_ + sc[kWR + 2] * n2, sc[kWRP] + sc[kWR + 2]);
+        x3 = ddivq(sc[kWR + 3] * n3 + sc[kWRN] * nn_, sc[kWR + 3] + sc[kWRN]);
+    }
     const double x0 = sc[kWFN] * n0;                              // prox_svm_norm
     const double pr = n1 * X;
     const int g = lane & 7;
@@ -393,27 +414,36 @@ __device__ __forceinline__ void chain_w_point(const PassB& b, const ChainDev& c,
     const double Y = sc[kWY];
     const double slack = (1.0 - nx1) - Y * (dot + nb);
     const double mu = ddivq(np_max0(slack), sc[kWDEN]);
-    // mu/rho1, mu/rho_b, mu/rho_x1 on lanes 0, 1, 2 (one division for all)
-    const double q = ddivq(mu, sc[lane == 1 ? kWRB : (lane == 2 ? kWRX1 : kWR + 1)]);
-    const double x1 = n1 + (__shfl_sync(kFull, q, 0) * Y) * X;
-    const double xbv = nb + __shfl_sync(kFull, q, 1) * Y;
-    const double xx1 = nx1 + __shfl_sync(kFull, q, 2);
+    double x1, xbv, xx1;
+    if (UNI) {                         // mu / rho: one divisor for all three
+        const double q = dq_c(mu, W.r, W.invr);
+        x1 = n1 + (q * Y) * X;
+        xbv = nb + q * Y;
+        xx1 = nx1 + q;
+    } else {
+        // mu/rho1, mu/rho_b, mu/rho_x1 on lanes 0, 1, 2 (one division for all)
+        const double q = ddivq(mu, sc[lane == 1 ? kWRB : (lane == 2 ? kWRX1 : kWR + 1)]);
+        x1 = n1 + (__shfl_sync(kFull, q, 0) * Y) * X;
+        xbv = nb + __shfl_sync(kFull, q, 1) * Y;
+        xx1 = nx1 + __shfl_sync(kFull, q, 2);
+    }
     const double xx0 = np_max0(nx0 - sc[kWLR]);                  // prox_svm_slack
     // ---- phases m, z, u of w_i ----
     {
-        const double r0 = sc[kWR], r1 = sc[kWR + 1], r2 = sc[kWR + 2], r3 = sc[kWR + 3];
+        const double r0 = WR(0), r1 = WR(1), r2 = WR(2), r3 = WR(3);
         u0 = su[0]; u1 = su[32]; u2 = su[64]; u3 = su[96];
         const double m0 = x0 + u0, m1 = x1 + u1, m2 = x2 + u2, m3 = x3 + u3;
         double res = 0.0;
         res += m1 * r1;
         res += m2 * r2;
         res += m3 * r3;
-        const double zn = ddivq(m0 * r0 + res, sc[kWZWW]);
+        const double zn = UNI ? dq_c(m0 * r0 + res, W.zww, W.invzww)
+                              : ddivq(m0 * r0 + res, sc[kWZWW]);
         b.z[zo] = zn;
         const double dz = zn - zi;
         const double t0 = x0 - zn, t1 = x1 - zn, t2 = x2 - zn, t3 = x3 - zn;
-        const double v0 = u0 + t0 * sc[kWA], v1 = u1 + t1 * sc[kWA + 1];
-        const double v2 = u2 + t2 * sc[kWA + 2], v3 = u3 + t3 * sc[kWA + 3];
+        const double v0 = u0 + t0 * WA(0), v1 = u1 + t1 * WA(1);
+        const double v2 = u2 + t2 * WA(2), v3 = u3 + t3 * WA(3);
         double* __restrict__ UO = b.uout + wo;
         UO[0] = v0; UO[D] = v1; UO[2 * D] = v2; UO[3 * D] = v3;
         const double d0 = r0 * dz, d1 = r1 * dz, d2 = r2 * dz, d3 = r3 * dz;
@@ -433,11 +463,12 @@ __device__ __forceinline__ void chain_w_point(const PassB& b, const ChainDev& c,
     }
     // ---- xi_i (slack, margin) and b's margin x ----
     if (lane == 0) {
-        const double rx0 = sc[kWRX0], R3 = sc[kWRX1];
+        const double rx0 = WS(kWRX0), R3 = WS(kWRX1);
         const double mx0 = xx0 + ux0, mx1 = xx1 + ux1;
         double rs = 0.0;
         rs += mx1 * R3;
-        const double zx = ddivq(mx0 * rx0 + rs, sc[kWZWX]);
+        const double zx = UNI ? dq_c(mx0 * rx0 + rs, W.zwx, W.invzwx)
+                              : ddivq(mx0 * rx0 + rs, sc[kWZWX]);
         {
             b.z[c.zX + i] = zx;
             const double dzx = zx - zxi;
@@ -445,7 +476,7 @@ __device__ __forceinline__ void chain_w_point(const PassB& b, const ChainDev& c,
             const double e0 = rx0 * dzx, e1 = R3 * dzx;
             pp += s0 * s0; dd += e0 * e0;
             pp += s1 * s1; dd += e1 * e1;
-            const double w0 = ux0 + s0 * sc[kWAX0], w1 = ux1 + s1 * sc[kWAX1];
+            const double w0 = ux0 + s0 * WS(kWAX0), w1 = ux1 + s1 * WS(kWAX1);
             b.uout[c.pX + 2 * (int64_t)i] = w0;
             b.uout[c.pX + 2 * (int64_t)i + 1] = w1;
             xb_out[c.pB + i] = xbv;
@@ -457,10 +488,10 @@ __device__ __forceinline__ void chain_w_point(const PassB& b, const ChainDev& c,
     }
 }
 
-template <int D>
+template <int D, bool UNI>
 __global__ void __launch_bounds__(kChainThreads, FG_CHAIN_W_MINB) k_svm_chain_w(PassB b, ChainDev c,
                                                                 double* xb_out,
-                                                                int64_t part_off) {
+                                                                int64_t part_off, WUni W) {
     static_assert(D == 32, "one lane per component");
     __shared__ double sm[16];
     __shared__ double s_sc[kChainThreads / 32][32];     // per-warp point scalars
@@ -502,17 +533,6 @@ __global__ void __launch_bounds__(kChainThreads, FG_CHAIN_W_MINB) k_svm_chain_w(
             case kWZWW: sb = b.zw + c.zW; ss = D; break;
             default: break;
         }
-        if (c.wuni) {                                  // uniform weights: stride 0
-            switch (lane) {
-                case 0: case 1: case 2: case 3: case kWRP: case kWRN: case kWRX0: case kWRX1:
-                case kWRB: sb = c.wuni; ss = 0; break;
-                case 4: case 5: case 6: case 7: case kWAX0: case kWAX1:
-                    sb = c.wuni + 1; ss = 0; break;
-                case kWZWW: sb = c.wuni + 2; ss = 0; break;
-                case kWZWX: sb = c.wuni + 3; ss = 0; break;
-                default: break;
-            }
-        }
         s_sb[lane] = sb;
         s_ss[lane] = ss;
     }
@@ -528,7 +548,7 @@ __global__ void __launch_bounds__(kChainThreads, FG_CHAIN_W_MINB) k_svm_chain_w(
         __syncwarp();                                  // previous point's reads done
         sc[lane] = sv;
         __syncwarp();
-        chain_w_point<D>(b, c, i, lane, sc, &s_u[warp][0][lane], L, xb_out, pp, dd, bad);
+        chain_w_point<D, UNI>(b, c, i, lane, sc, &s_u[warp][0][lane], L, W, xb_out, pp, dd, bad);
     }
     if (bad & 1u) flag_error(b.ctrl, it - 1, FG_PHASE_N, true);
     if (bad & 2u) flag_error(b.ctrl, it, FG_PHASE_X, true);

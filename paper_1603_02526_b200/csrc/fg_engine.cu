@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <array>
 #include <cstdio>
 #include <cstdlib>
@@ -258,7 +259,8 @@ struct fg_plan {
     double* d_chain_xx = nullptr;      // per point x.x of the margin data
     double* d_chain_fnorm = nullptr;   // per point 1/(1+scale) (unit form)
     double* d_chain_wtab = nullptr;    // 3 x n per-point tables (weighted form)
-    double* d_chain_wuni = nullptr;    // {rho, alpha, zw_w, zw_xi} when uniform
+    bool chain_uni = false;            // weighted form with uniform weights
+    WUni wuni{};                       // its weights (fg_chain.cuh)
     int32_t* d_flag = nullptr;         // scratch device flag
     unsigned long long* d_bad = nullptr;  // first non-finite ref index of a download
     int32_t* h_stop = nullptr;         // pinned stop-flag slots polled by fg_run
@@ -308,7 +310,7 @@ fg_plan::~fg_plan() {
                     d_lvars[4], d_lvprog[1], d_lvprog[2], d_lvprog[3], d_lvprog[4],
                     d_llist, d_lprog, d_prog, d_glist, d_gchunks, d_gcomps,
                     d_gwork, d_gcref, d_gwref, d_csum, d_gz, d_part, d_res2, d_ctrl, d_hist, d_chain_xx,
-                    d_chain_fnorm, d_chain_wtab, d_chain_wuni, d_flag, d_bad, d_gcnt, d_ucnt, d_lexc[1], d_lexc[2], d_lexc[3],
+                    d_chain_fnorm, d_chain_wtab, d_flag, d_bad, d_gcnt, d_ucnt, d_lexc[1], d_lexc[2], d_lexc[3],
                     d_lexc[4],
                     d_planoff[1], d_planoff[2], d_planoff[3], d_planoff[4], d_plans,
                     d_rowdesc[1], d_rowdesc[2], d_rowdesc[3], d_rowdesc[4],
@@ -661,8 +663,10 @@ void chain_pass(fg_plan* p, int in, cudaStream_t st) {
         // points (degree 3) on the generic form in the next partial slot
         if (p->chain_unit)
             k_svm_chain_unit<32><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
+        else if (p->chain_uni)
+            k_svm_chain_w<32, true><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0, p->wuni);
         else
-            k_svm_chain_w<32><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
+            k_svm_chain_w<32, false><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0, p->wuni);
         // the two end points run on a forked stream, concurrently with the
         // interior (a parallel branch when captured into a CUDA graph)
         cudaStreamWaitEvent(p->stream2, p->ev_fork, 0);
@@ -887,8 +891,6 @@ void detect_svm_chain(fg_plan* p, const std::vector<int32_t>& dim,
     k_chain_fnorm<<<(unsigned)((n + 255) / 256), 256, 0, p->stream>>>(c, p->d_chain_fnorm);
     if (cudaMalloc((void**)&p->d_chain_wtab, 3 * n * sizeof(double)) != cudaSuccess) return;
     c.wtab = p->d_chain_wtab;
-    if (cudaMalloc((void**)&p->d_chain_wuni, 4 * sizeof(double)) != cudaSuccess) return;
-    c.wuni = nullptr;                  // set at sync when the weights are uniform
     if (cudaStreamSynchronize(p->stream) != cudaSuccess) return;
     p->chain_fast = D == 32 && n >= 3 && p->chain_grid >= 2 && !getenv("FGADMM_CHAIN_GENERIC");
     p->chain_on = p->chain_grid > 0;
@@ -1597,7 +1599,7 @@ int fg_plan_forms(const fg_plan* p, int32_t* o) {
         if (g.dev.kind == FG_KIND_MPC_DYN && g.dev.dyn_gemm) o[6] = 1;
     }
     for (int d = 1; d <= 4; ++d) o[1 + d] = p->lunit[d] ? 1 : 0;
-    o[7] = p->chain.wuni != nullptr ? 1 : 0;
+    o[7] = p->chain_uni ? 1 : 0;
     o[8] = p->mpc_chain ? p->mpc_kb : 0;
     return 0;
 }
@@ -1677,17 +1679,25 @@ int fg_plan_sync_params(fg_plan* p, const double* rho, const double* alpha,
             for (int k = 1; k < c.D && wok; ++k) wok = zw[c.zW + i * c.D + k] == zw[c.zW + i * c.D];
         if (wok)
             k_chain_wtab<<<(unsigned)((c.n + 255) / 256), 256, 0, st>>>(c, p->d_rho, p->d_chain_wtab);
-        // uniform weights: the weighted form reads them from a 4-double table
-        bool uni = wok && p->d_chain_wuni != nullptr && c.n >= 3;
+        // uniform weights: the weighted form takes them as kernel arguments
+        bool uni = wok && c.n >= 3;
         for (int64_t e = 1; e < p->E && uni; ++e) uni = rho[e] == rho[0] && alpha[e] == alpha[0];
         const double zww = uni ? zw[c.zW + c.D] : 0.0, zwx = uni ? zw[c.zX + 1] : 0.0;
         for (int64_t i = 1; i + 1 < c.n && uni; ++i) uni = zw[c.zW + i * c.D] == zww && zw[c.zX + i] == zwx;
+        WUni w{};
         if (uni) {
-            const double h[4] = {rho[0], alpha[0], zww, zwx};
-            CK(cudaMemcpyAsync(p->d_chain_wuni, h, sizeof(h), cudaMemcpyHostToDevice, st));
+            auto inv = [](double y) {             // exact inverse of a normal power of two
+                int ex = 0;
+                const double m = std::frexp(y, &ex);
+                return (m == 0.5 && y == std::ldexp(1.0, ex - 1) && std::isnormal(y) &&
+                        std::isnormal(1.0 / y)) ? 1.0 / y : 0.0;
+            };
+            const double r = rho[0];
+            w = WUni{r, alpha[0], zww, zwx, inv(r + r), inv(r), inv(zww), inv(zwx)};
         }
-        if ((uni ? p->d_chain_wuni : nullptr) != p->chain.wuni) {
-            p->chain.wuni = uni ? p->d_chain_wuni : nullptr;
+        if (uni != p->chain_uni || std::memcmp(&w, &p->wuni, sizeof(w)) != 0) {
+            p->chain_uni = uni;
+            p->wuni = w;
             for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
             p->graphs.clear();
         }
