@@ -18,12 +18,12 @@ if [ "${SKIP_REF:-0}" != 1 ]; then
 fi
 for w in svm1m svm1m_rho2 pack5000 mpc100k; do
   ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r02_launches_$w.csv \
-      python bench.py --workload $w --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/r02_launches_$w.log 2>&1
+      python bench.py --workload $w --steps 12 --warmup 3 --no-cpu-baseline > gpurun_out/r02_launches_$w.log 2>&1
   echo "launch list $w rc=$?"; tail -2 gpurun_out/r02_launches_$w.log
 done
 prof() {  # workload regex skip count
   timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$2" -s "$3" -c "$4" \
-      -o "gpurun_out/r02_$1" -f python bench.py --workload "$1" --steps 3 --warmup 3 --no-cpu-baseline \
+      -o "gpurun_out/r02_$1" -f python bench.py --workload "$1" --steps 12 --warmup 3 --no-cpu-baseline \
       > "gpurun_out/r02_ncu_$1.log" 2>&1
   echo "ncu $1 rc=$?"; tail -2 "gpurun_out/r02_ncu_$1.log"
   if [ -f "gpurun_out/r02_$1.ncu-rep" ]; then
@@ -33,7 +33,7 @@ prof() {  # workload regex skip count
   fi
 }
 prof svm1m "k_svm_chain|k_var_giant" 3 3
-prof svm1m_rho2 "k_svm_chain" 3 1
+prof svm1m_rho2 "^k_svm_chain_w$" 1 1
 prof pack5000 "k_collision_tiles_v3|k_var_row_pipe" 3 3
-prof mpc100k "k_mpc_block" 2 1
+prof mpc100k "^k_mpc_block$" 1 1
 du -sh gpurun_out
