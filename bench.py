@@ -689,7 +689,9 @@ def main():
         fp64 = {"flops_per_launch": flops, "TFLOPs": flops / (avg_ms / 1e3) / 1e12,
                 "note": "the blocked chain reads its state once per launch; its "
                         "per-launch time is set by the fp64 dynamics products and "
-                        "shared-memory traffic, not HBM"}
+                        "shared-memory traffic, not HBM",
+                "limiter": "shared-memory pipe: ncu L1/TEX 75% of peak, issue slots 54%, "
+                           "DRAM 4.6% (profiles/r02_ncu_mpc_block.md)"}
 
     # ---- end to end through the public API (host state in, host state out) ----
     # three calls, each from the same initial state; the median is reported
