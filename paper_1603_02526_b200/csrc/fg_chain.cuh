@@ -533,6 +533,16 @@ __global__ void __launch_bounds__(kChainThreads, FG_CHAIN_W_MINB) k_svm_chain_w(
             case kWZWW: sb = b.zw + c.zW; ss = D; break;
             default: break;
         }
+        if (UNI) {
+            // the weights are kernel arguments: their lanes read one cached
+            // double (stride 0) instead of streaming the per-edge arrays
+            switch (lane) {
+                case 0: case 1: case 2: case 3: case 4: case 5: case 6: case 7:
+                case kWRP: case kWRN: case kWRX0: case kWRX1: case kWAX0: case kWAX1:
+                case kWRB: case kWZWX: case kWZWW: sb = c.xx; ss = 0; break;
+                default: break;
+            }
+        }
         s_sb[lane] = sb;
         s_ss[lane] = ss;
     }
