@@ -58,13 +58,29 @@ struct ChainDev {
 // a constant divisor carries its exact power-of-two inverse (0: none).
 struct WUni {
     double r, a, zww, zwx;        // rho, alpha, z weight of w_i, of xi_i
-    double inv2r, invr, invzww, invzwx;
+    double inv2r, invr, invzww, invzwx;   // exact power-of-two inverses (0: none)
+    double rcp2r, rcpr, rcpzww, rcpzwx;   // refined reciprocals qdiv_rcp (0: none)
 };
 
-// x / y with the caller's exact power-of-two inverse of y (ddivq's test
-// made once per run): bitwise ddivq(x, y)
-__device__ __forceinline__ double dq_c(double x, double y, double inv) {
-    return inv != 0.0 ? x * inv : qdiv(x, y);
+// x / y for a run-constant divisor: the exact power-of-two inverse (ddivq's
+// test made once per run), else the quotient from y's refined reciprocal
+// computed once per run (qdiv_r), else the full inline division: bitwise
+// ddivq(x, y) in every case
+__device__ __forceinline__ double dq_c(double x, double y, double inv, double rcp) {
+    if (inv != 0.0) return x * inv;
+    if (rcp != 0.0) return qdiv_r(x, y, rcp);
+    return qdiv(x, y);
+}
+
+// refined reciprocals of the uniform form's constant divisors (one thread;
+// run at parameter sync): out[k] = qdiv_rcp(y[k]) for y within qdiv_r's
+// range, else 0
+__global__ void k_wuni_rcp(double y0, double y1, double y2, double y3, double* out) {
+    const double y[4] = {y0, y1, y2, y3};
+    for (int k = 0; k < 4; ++k) {
+        const int e = (int)((__double_as_longlong(y[k]) >> 52) & 0x7ff);
+        out[k] = (y[k] > 0.0 && (unsigned)(e - 128) <= 1792u) ? qdiv_rcp(y[k]) : 0.0;
+    }
 }
 
 constexpr int kChainThreads = 256;
@@ -359,7 +375,7 @@ __device__ __forceinline__ ChainWLoads chain_w_load(const PassB& b, const ChainD
     return L;
 }
 
-template <int D, bool UNI>
+template <int D, bool UNI, bool RCP>
 __device__ __forceinline__ void chain_w_point(const PassB& b, const ChainDev& c, int32_t i,
                                               int lane, double* sc, double* su,
                                               const ChainWLoads& L, const WUni& W,
@@ -394,8 +410,8 @@ __device__ __forceinline__ void chain_w_point(const PassB& b, const ChainDev& c,
     // ---- phase x (equalities first: their inputs die early) ----
     double x2, x3;
     if (UNI) {                                                    // prox_equality
-        x2 = dq_c(W.r * np_ + W.r * n2, W.r + W.r, W.inv2r);
-        x3 = dq_c(W.r * n3 + W.r * nn_, W.r + W.r, W.inv2r);
+        x2 = dq_c(W.r * np_ + W.r * n2, W.r + W.r, W.inv2r, RCP ? W.rcp2r : 0.0);
+        x3 = dq_c(W.r * n3 + W.r * nn_, W.r + W.r, W.inv2r, RCP ? W.rcp2r : 0.0);
     } else {
         x2 = ddivq(sc[kWRP] * np_ + sc[kWR + 2] * n2, sc[kWRP] + sc[kWR + 2]);
         x3 = ddivq(sc[kWR + 3] * n3 + sc[kWRN] * nn_, sc[kWR + 3] + sc[kWRN]);
@@ -416,7 +432,7 @@ __device__ __forceinline__ void chain_w_point(const PassB& b, const ChainDev& c,
     const double mu = ddivq(np_max0(slack), sc[kWDEN]);
     double x1, xbv, xx1;
     if (UNI) {                         // mu / rho: one divisor for all three
-        const double q = dq_c(mu, W.r, W.invr);
+        const double q = dq_c(mu, W.r, W.invr, RCP ? W.rcpr : 0.0);
         x1 = n1 + (q * Y) * X;
         xbv = nb + q * Y;
         xx1 = nx1 + q;
@@ -437,7 +453,7 @@ __device__ __forceinline__ void chain_w_point(const PassB& b, const ChainDev& c,
         res += m1 * r1;
         res += m2 * r2;
         res += m3 * r3;
-        const double zn = UNI ? dq_c(m0 * r0 + res, W.zww, W.invzww)
+        const double zn = UNI ? dq_c(m0 * r0 + res, W.zww, W.invzww, RCP ? W.rcpzww : 0.0)
                               : ddivq(m0 * r0 + res, sc[kWZWW]);
         b.z[zo] = zn;
         const double dz = zn - zi;
@@ -467,7 +483,7 @@ __device__ __forceinline__ void chain_w_point(const PassB& b, const ChainDev& c,
         const double mx0 = xx0 + ux0, mx1 = xx1 + ux1;
         double rs = 0.0;
         rs += mx1 * R3;
-        const double zx = UNI ? dq_c(mx0 * rx0 + rs, W.zwx, W.invzwx)
+        const double zx = UNI ? dq_c(mx0 * rx0 + rs, W.zwx, W.invzwx, RCP ? W.rcpzwx : 0.0)
                               : ddivq(mx0 * rx0 + rs, sc[kWZWX]);
         {
             b.z[c.zX + i] = zx;
@@ -488,7 +504,10 @@ __device__ __forceinline__ void chain_w_point(const PassB& b, const ChainDev& c,
     }
 }
 
-template <int D, bool UNI>
+// RCP (uniform weights with a divisor that is not a power of two): the
+// constant divisions use the per-run refined reciprocals; without it the
+// power-of-two form carries no reciprocal code (registers: 64 at the cap)
+template <int D, bool UNI, bool RCP = false>
 __global__ void __launch_bounds__(kChainThreads, FG_CHAIN_W_MINB) k_svm_chain_w(PassB b, ChainDev c,
                                                                 double* xb_out,
                                                                 int64_t part_off, WUni W) {
@@ -558,7 +577,7 @@ __global__ void __launch_bounds__(kChainThreads, FG_CHAIN_W_MINB) k_svm_chain_w(
         __syncwarp();                                  // previous point's reads done
         sc[lane] = sv;
         __syncwarp();
-        chain_w_point<D, UNI>(b, c, i, lane, sc, &s_u[warp][0][lane], L, W, xb_out, pp, dd, bad);
+        chain_w_point<D, UNI, RCP>(b, c, i, lane, sc, &s_u[warp][0][lane], L, W, xb_out, pp, dd, bad);
     }
     if (bad & 1u) flag_error(b.ctrl, it - 1, FG_PHASE_N, true);
     if (bad & 2u) flag_error(b.ctrl, it, FG_PHASE_X, true);

@@ -261,6 +261,7 @@ struct fg_plan {
     double* d_chain_wtab = nullptr;    // 3 x n per-point tables (weighted form)
     bool chain_uni = false;            // weighted form with uniform weights
     WUni wuni{};                       // its weights (fg_chain.cuh)
+    double* d_aux4 = nullptr;          // 4-double scratch (k_wuni_rcp)
     int32_t* d_flag = nullptr;         // scratch device flag
     unsigned long long* d_bad = nullptr;  // first non-finite ref index of a download
     int32_t* h_stop = nullptr;         // pinned stop-flag slots polled by fg_run
@@ -310,7 +311,7 @@ fg_plan::~fg_plan() {
                     d_lvars[4], d_lvprog[1], d_lvprog[2], d_lvprog[3], d_lvprog[4],
                     d_llist, d_lprog, d_prog, d_glist, d_gchunks, d_gcomps,
                     d_gwork, d_gcref, d_gwref, d_csum, d_gz, d_part, d_res2, d_ctrl, d_hist, d_chain_xx,
-                    d_chain_fnorm, d_chain_wtab, d_flag, d_bad, d_gcnt, d_ucnt, d_lexc[1], d_lexc[2], d_lexc[3],
+                    d_chain_fnorm, d_chain_wtab, d_aux4, d_flag, d_bad, d_gcnt, d_ucnt, d_lexc[1], d_lexc[2], d_lexc[3],
                     d_lexc[4],
                     d_planoff[1], d_planoff[2], d_planoff[3], d_planoff[4], d_plans,
                     d_rowdesc[1], d_rowdesc[2], d_rowdesc[3], d_rowdesc[4],
@@ -663,6 +664,9 @@ void chain_pass(fg_plan* p, int in, cudaStream_t st) {
         // points (degree 3) on the generic form in the next partial slot
         if (p->chain_unit)
             k_svm_chain_unit<32><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0);
+        else if (p->chain_uni && (p->wuni.rcp2r != 0.0 || p->wuni.rcpr != 0.0 ||
+                                  p->wuni.rcpzww != 0.0 || p->wuni.rcpzwx != 0.0))
+            k_svm_chain_w<32, true, true><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0, p->wuni);
         else if (p->chain_uni)
             k_svm_chain_w<32, true><<<G, kChainThreads, 0, st>>>(b, p->chain, p->d_x, 0, p->wuni);
         else
@@ -891,6 +895,7 @@ void detect_svm_chain(fg_plan* p, const std::vector<int32_t>& dim,
     k_chain_fnorm<<<(unsigned)((n + 255) / 256), 256, 0, p->stream>>>(c, p->d_chain_fnorm);
     if (cudaMalloc((void**)&p->d_chain_wtab, 3 * n * sizeof(double)) != cudaSuccess) return;
     c.wtab = p->d_chain_wtab;
+    if (cudaMalloc((void**)&p->d_aux4, 4 * sizeof(double)) != cudaSuccess) return;
     if (cudaStreamSynchronize(p->stream) != cudaSuccess) return;
     p->chain_fast = D == 32 && n >= 3 && p->chain_grid >= 2 && !getenv("FGADMM_CHAIN_GENERIC");
     p->chain_on = p->chain_grid > 0;
@@ -1693,7 +1698,19 @@ int fg_plan_sync_params(fg_plan* p, const double* rho, const double* alpha,
                         std::isnormal(1.0 / y)) ? 1.0 / y : 0.0;
             };
             const double r = rho[0];
-            w = WUni{r, alpha[0], zww, zwx, inv(r + r), inv(r), inv(zww), inv(zwx)};
+            w = WUni{r, alpha[0], zww, zwx, inv(r + r), inv(r), inv(zww), inv(zwx),
+                     0.0, 0.0, 0.0, 0.0};
+            // refined reciprocals of the divisors that are not powers of two,
+            // computed on the device with the kernels' own sequence
+            double* d4 = p->d_aux4;
+            k_wuni_rcp<<<1, 1, 0, st>>>(r + r, r, zww, zwx, d4);
+            double h4[4];
+            CK(cudaMemcpyAsync(h4, d4, sizeof(h4), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            w.rcp2r = w.inv2r != 0.0 ? 0.0 : h4[0];
+            w.rcpr = w.invr != 0.0 ? 0.0 : h4[1];
+            w.rcpzww = w.invzww != 0.0 ? 0.0 : h4[2];
+            w.rcpzwx = w.invzwx != 0.0 ? 0.0 : h4[3];
         }
         if (uni != p->chain_uni || std::memcmp(&w, &p->wuni, sizeof(w)) != 0) {
             p->chain_uni = uni;
