@@ -32,20 +32,24 @@ constexpr int kMpcKB = 5;                              // iterations per launch 
 constexpr int kMpcKBTail = 3;                          // shorter block for a run's tail
 constexpr int kMbF = 64;                               // factor slots
 constexpr int kMbThreads = kEdgeThreads;               // 256
-// K nv register tile: a thread computes 2 factors (lane, lane + 32) x the 5
-// rows r0 + 8k of its warp r0, so per column it loads 2 nv values (lane-
-// distinct) and 5 K values (warp-uniform broadcasts) for 10 FMAs: 9
-// shared-memory wavefronts instead of 12 for the 1-factor x 10-row tile
-// (ncu: the block kernel is bound by the shared-memory pipe).  Every
-// output is the same fma chain over the columns in the same order.
-constexpr int kMbRG = kMbThreads / 32;                 // 8 row groups (one per warp)
-constexpr int kMbKH = (kDynGemmMaxCols + kMbRG - 1) / kMbRG;   // 5 rows per thread
+// v = K nv on the fp64 tensor cores: V^T (rows x factors) = K (rows x
+// cols) . NV^T (cols x factors) as mma.sync.m8n8k4 f64 tiles, warp w owning
+// the 8 factors 8w.. (its 9 B fragments stay in registers) and looping over
+// the 5 row tiles of K (A fragments from shared memory).  The f64 MMA
+// accumulates each output as the sequential fma chain over k within a
+// k-step, and the k-steps run in column order, so every output is the SAME
+// fma chain over the columns as k_mpc_chain / k_mpc_dyn_gemm, bit for bit
+// (checked on the B200 against the scalar chain, including subnormal, inf,
+// NaN and signed-zero operands: tools/probe/dmma_check.cu).  ncu: the
+// scalar form was bound by shared-memory wavefronts (12 per 10 FMAs).
+constexpr int kMbMT = (kDynGemmMaxCols + 7) / 8;       // row tiles of K (rows padded to 40)
+constexpr int kMbKS = kDynGemmMaxCols;                 // K row stride (doubles)
 constexpr int kMbNN = kMbF + 1;                        // nodes staged per CTA (tile + 2 KB)
 
 inline size_t mpc_block_smem(int n0, int d) {
     const size_t cols = (size_t)(n0 + d);
-    return (cols * kMbRG * kMbKH + (size_t)kMbNN * 5 * n0 +
-            (size_t)kMbF * (cols + 1) + (size_t)kMbF * (2 * n0 + 1)) * sizeof(double);
+    return ((size_t)kMbMT * 8 * kMbKS + (size_t)kMbNN * 5 * n0 +
+            (size_t)kMbF * cols + (size_t)kMbF * (2 * n0 + 1)) * sizeof(double);
 }
 
 template <int KB, int N0, int DD>
@@ -57,10 +61,11 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mpc_block(PassB b, MpcChainDe
     extern __shared__ double gsm[];
     __shared__ double sm[2 * (kMbThreads / 32)];
     if (b.ctrl->stop) return;
-    constexpr int n0 = N0, d = DD, cols = N0 + DD, ld = cols + 1, ldo = 2 * N0 + 1;
-    constexpr int KH = kMbKH, RG = kMbRG;
-    double* Ks = gsm;                                   // [c][r0][k], row r = r0 + RG k
-    double* zs = Ks + cols * RG * KH;                   // [NN][n0]
+    constexpr int n0 = N0, d = DD, cols = N0 + DD, ld = cols, ldo = 2 * N0 + 1;
+    static_assert(cols % 4 == 0 && cols <= kMbKS, "k-steps of 4 columns");
+    static_assert(kMbF == 8 * (kMbThreads / 32), "one 8-factor tile per warp");
+    double* Ks = gsm;                                   // [MT*8][kMbKS] row-major, pad rows 0
+    double* zs = Ks + kMbMT * 8 * kMbKS;                // [NN][n0]
     double* us = zs + kMbNN * n0;                       // [NN][3][n0]
     double* nvs = us + kMbNN * 3 * n0;                  // [F][ld]
     double* outs = nvs + kMbF * ld;                     // [F][ldo]
@@ -78,8 +83,10 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mpc_block(PassB b, MpcChainDe
     // n0 at zN + t n0 ----
     for (int i = threadIdx.x; i < cols * cols; i += blockDim.x) {
         const int r = i / cols, cc = i - r * cols;
-        cp_async8(&Ks[(cc * RG + r % RG) * KH + r / RG], c.kmat + i);
+        cp_async8(&Ks[r * kMbKS + cc], c.kmat + i);
     }
+    for (int i = threadIdx.x; i < (kMbMT * 8 - cols) * kMbKS; i += blockDim.x)
+        Ks[cols * kMbKS + i] = 0.0;                     // pad rows of the last row tile
     {
         const double* __restrict__ uin = b.uin + c.pN + (int64_t)3 * a * n0;
         const double* __restrict__ zin = b.zin + c.zN + (int64_t)a * n0;
@@ -115,30 +122,27 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mpc_block(PassB b, MpcChainDe
             else outs[fl * ldo + n0 + q] = n;           // control of t+1 passes
         }
         __syncthreads();
-        {   // v = K nv: the fma chain of k_mpc_chain / k_mpc_dyn_gemm
-            const int fa = threadIdx.x & 31, fb = fa + 32, r0 = threadIdx.x >> 5;
-            const bool ha = fa < nf, hb = fb < nf;
-            double aa[KH], ab[KH];
+        {   // v = K nv: the fma chain of k_mpc_chain / k_mpc_dyn_gemm, as f64 MMAs
+            const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+            const int fb = 8 * w + (lane >> 2), kq = lane & 3;
+            double bf[cols / 4];
 #pragma unroll
-            for (int k = 0; k < KH; ++k) aa[k] = ab[k] = 0.0;
-            const double* nva = nvs + (ha ? fa : 0) * ld;
-            const double* nvb = nvs + (hb ? fb : 0) * ld;
-            for (int cc = 0; cc < cols; ++cc) {
-                const double va = nva[cc], vb = nvb[cc];
-                const double* kc = Ks + (cc * RG + r0) * KH;
+            for (int ks = 0; ks < cols / 4; ++ks) bf[ks] = nvs[fb * ld + 4 * ks + kq];
+            const int f0 = 8 * w + 2 * kq;
+#pragma unroll 1
+            for (int m = 0; m < kMbMT; ++m) {
+                const double* ka = Ks + (8 * m + (lane >> 2)) * kMbKS + kq;
+                double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-                for (int k = 0; k < KH; ++k) {
-                    const double kk = kc[k];
-                    aa[k] = __fma_rn(kk, va, aa[k]);
-                    ab[k] = __fma_rn(kk, vb, ab[k]);
+                for (int ks = 0; ks < cols / 4; ++ks) {
+                    const double a = ka[4 * ks];
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                                 : "+d"(d0), "+d"(d1) : "d"(a), "d"(bf[ks]));
                 }
-            }
-#pragma unroll
-            for (int k = 0; k < KH; ++k) {
-                const int r = r0 + RG * k;
+                const int r = 8 * m + (lane >> 2);
                 if (r < cols) {
-                    if (ha) outs[fa * ldo + r] = aa[k];
-                    if (hb) outs[fb * ldo + r] = ab[k];
+                    if (f0 < nf) outs[f0 * ldo + r] = d0;
+                    if (f0 + 1 < nf) outs[(f0 + 1) * ldo + r] = d1;
                 }
             }
         }
