@@ -42,18 +42,20 @@ constexpr int kMbThreads = kEdgeThreads;               // 256
 // (checked on the B200 against the scalar chain, including subnormal, inf,
 // NaN and signed-zero operands: tools/probe/dmma_check.cu).  ncu: the
 // scalar form was bound by shared-memory wavefronts (12 per 10 FMAs).
-constexpr int kMbMT = (kDynGemmMaxCols + 7) / 8;       // row tiles of K (rows padded to 40)
-constexpr int kMbKS = kDynGemmMaxCols;                 // K row stride (doubles)
+constexpr int kMbMT = (kDynGemmMaxCols + 7) / 8;       // row tiles of K (last one clamped)
+constexpr int kMbLD = 44;                              // factor row stride: nv, then v (aliased)
 constexpr int kMbNN = kMbF + 1;                        // nodes staged per CTA (tile + 2 KB)
 
+// K (cols x cols), z and the three u slots of the staged nodes, and one
+// factor row buffer holding nv (staging) and then v (K nv) in place: ~74 KB
+// at the 16/4 sizes, three CTAs per SM
 inline size_t mpc_block_smem(int n0, int d) {
     const size_t cols = (size_t)(n0 + d);
-    return ((size_t)kMbMT * 8 * kMbKS + (size_t)kMbNN * 5 * n0 +
-            (size_t)kMbF * cols + (size_t)kMbF * (2 * n0 + 1)) * sizeof(double);
+    return (cols * cols + (size_t)kMbNN * 4 * n0 + (size_t)kMbF * kMbLD) * sizeof(double);
 }
 
 template <int KB, int N0, int DD>
-__global__ void __launch_bounds__(kMbThreads, 2) k_mpc_block(PassB b, MpcChainDev c,
+__global__ void __launch_bounds__(kMbThreads, 3) k_mpc_block(PassB b, MpcChainDev c,
                                                              int32_t tile, double* bpart,
                                                              int64_t ntiles,
                                                              int64_t fault_it = 0) {
@@ -61,15 +63,18 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mpc_block(PassB b, MpcChainDe
     extern __shared__ double gsm[];
     __shared__ double sm[2 * (kMbThreads / 32)];
     if (b.ctrl->stop) return;
-    constexpr int n0 = N0, d = DD, cols = N0 + DD, ld = cols, ldo = 2 * N0 + 1;
-    static_assert(cols % 4 == 0 && cols <= kMbKS, "k-steps of 4 columns");
+    constexpr int n0 = N0, d = DD, cols = N0 + DD, ld = kMbLD, ldo = kMbLD;
+    static_assert(cols % 4 == 0 && cols <= 8 * kMbMT && 2 * n0 <= kMbLD, "tile sizes");
     static_assert(kMbF == 8 * (kMbThreads / 32), "one 8-factor tile per warp");
-    double* Ks = gsm;                                   // [MT*8][kMbKS] row-major, pad rows 0
-    double* zs = Ks + kMbMT * 8 * kMbKS;                // [NN][n0]
+    double* Ks = gsm;                                   // [cols][cols] row-major
+    double* zs = Ks + cols * cols;                      // [NN][n0]
     double* us = zs + kMbNN * n0;                       // [NN][3][n0]
+    // factor rows: nv of the two slots (cols 0 .. cols-1) and the control
+    // passed through to node t+1 (cols n0+d .. 2 n0-1); the MMA overwrites
+    // cols 0 .. cols-1 of the warp's own rows with v = K nv after reading nv
+    // into its fragments, so nv and v share the buffer
     double* nvs = us + kMbNN * 3 * n0;                  // [F][ld]
-    double* outs = nvs + kMbF * ld;                     // [F][ldo]
-    double* cs = outs + kMbF * ldo;                     // [NN][n0] cost diagonals
+    double* outs = nvs;
     const int T = c.T;
     const int t0 = blockIdx.x * tile;
     const int t1 = min(T + 1, t0 + tile);               // owned nodes [t0, t1)
@@ -77,26 +82,20 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mpc_block(PassB b, MpcChainDe
     const int bnd = min(T + 1, t1 + KB);                // staged nodes [a, bnd)
     const int NN = bnd - a;
     const int nf = NN - 1;                              // factors [a, bnd - 1)
-    // ---- stage K, the state of [a, bnd) and its cost diagonals with
+    // ---- stage K and the state of [a, bnd) with
     // asynchronous copies (every load in flight at once): node t's payload
     // is 3 n0 contiguous doubles at pN + 3 t n0 (node T has two slots), z
     // n0 at zN + t n0 ----
     for (int i = threadIdx.x; i < cols * cols; i += blockDim.x) {
         const int r = i / cols, cc = i - r * cols;
-        cp_async8(&Ks[r * kMbKS + cc], c.kmat + i);
+        cp_async8(&Ks[r * cols + cc], c.kmat + i);
     }
-    for (int i = threadIdx.x; i < (kMbMT * 8 - cols) * kMbKS; i += blockDim.x)
-        Ks[cols * kMbKS + i] = 0.0;                     // pad rows of the last row tile
     {
         const double* __restrict__ uin = b.uin + c.pN + (int64_t)3 * a * n0;
         const double* __restrict__ zin = b.zin + c.zN + (int64_t)a * n0;
         const int nu = NN * 3 * n0 - (bnd == T + 1 ? n0 : 0);
         for (int i = threadIdx.x; i < nu; i += blockDim.x) cp_async8(us + i, uin + i);
         for (int i = threadIdx.x; i < NN * n0; i += blockDim.x) cp_async8(zs + i, zin + i);
-        for (int i = threadIdx.x; i < NN * n0; i += blockDim.x) {
-            const int tl = i / n0, q = i - tl * n0;
-            cp_async8(cs + i, c.cost_fp + (int64_t)(a + tl) * c.cost_st + q);
-        }
         if (bnd == T + 1)
             for (int q = threadIdx.x; q < n0; q += blockDim.x) us[(NN - 1) * 3 * n0 + 2 * n0 + q] = 0.0;
     }
@@ -131,7 +130,10 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mpc_block(PassB b, MpcChainDe
             const int f0 = 8 * w + 2 * kq;
 #pragma unroll 1
             for (int m = 0; m < kMbMT; ++m) {
-                const double* ka = Ks + (8 * m + (lane >> 2)) * kMbKS + kq;
+                // rows past cols (the last tile) reuse row cols-1: their
+                // outputs are discarded and each output row depends only
+                // on its own A row
+                const double* ka = Ks + min(8 * m + (lane >> 2), cols - 1) * cols + kq;
                 double d0 = 0.0, d1 = 0.0;
 #pragma unroll
                 for (int ks = 0; ks < cols / 4; ++ks) {
@@ -160,7 +162,7 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mpc_block(PassB b, MpcChainDe
             u[1] = us[(tl * 3 + 1) * n0 + q];
             u[2] = us[(tl * 3 + 2) * n0 + q];
             const double n_c = zi - u[0];
-            x[0] = prox_mpc_cost(n_c, 1.0, cs[tl * n0 + q]);
+            x[0] = prox_mpc_cost(n_c, 1.0, __ldg(c.cost_fp + (int64_t)t * c.cost_st + q));
             bool bn = !finite(n_c);
             // rank 1: dyn_{t-1} slot 1 (node 0: dyn_0 slot 0); a halo node
             // without its factor computes a placeholder (never owned)
