@@ -263,9 +263,11 @@ __global__ void __launch_bounds__(kEdgeThreads, N0 > 0 ? 4 : 3) k_mpc_chain(Pass
     const int fA = max(0, t0 - 1), fB = min(c.T, t1);   // factors [fA, fB)
     const int nf = fB - fA;
     bool bn = false, bx = false, bm = false, bz = false, bu = false;
+    // compile-time sizes: K row-major for the f64 MMA (fits the same space)
     for (int i = threadIdx.x; i < cols * cols; i += blockDim.x) {
         const int r = i / cols, cc = i - r * cols;
-        Ks[(cc * RG + r % RG) * KH + r / RG] = c.kmat[i];
+        if (N0 > 0) Ks[i] = c.kmat[i];
+        else Ks[(cc * RG + r % RG) * KH + r / RG] = c.kmat[i];
     }
     const double* __restrict__ uin = b.uin;
     const double* __restrict__ zin = b.zin;
@@ -306,7 +308,35 @@ __global__ void __launch_bounds__(kEdgeThreads, N0 > 0 ? 4 : 3) k_mpc_chain(Pass
         }
     }
     __syncthreads();
-    {   // v = K nv: thread -> factor slot fl, rows r0 + RG k; every output is
+    if (N0 > 0) {
+        // v = K nv on the fp64 tensor cores (as k_mpc_block): warp w owns
+        // factor slots 8w..8w+7, B fragments in registers, A from K; each
+        // output is the same fma chain over the columns (bitwise)
+        static_assert(N0 == 0 || ((N0 + DD) % 4 == 0 && kMpcF == 8 * (kEdgeThreads / 32)), "tiles");
+        constexpr int C4 = N0 > 0 ? (N0 + DD) / 4 : 1;
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        const int fb = 8 * w + (lane >> 2), kq = lane & 3;
+        double bf[C4];
+#pragma unroll
+        for (int ks = 0; ks < C4; ++ks) bf[ks] = nvs[fb * ld + 4 * ks + kq];
+        const int f0 = 8 * w + 2 * kq;
+#pragma unroll 1
+        for (int m = 0; m < (4 * C4 + 7) / 8; ++m) {
+            const double* ka = Ks + min(8 * m + (lane >> 2), cols - 1) * cols + kq;
+            double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < C4; ++ks) {
+                const double av = ka[4 * ks];
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                             : "+d"(d0), "+d"(d1) : "d"(av), "d"(bf[ks]));
+            }
+            const int r = 8 * m + (lane >> 2);
+            if (r < cols) {
+                if (f0 < nf) outs[f0 * ldo + r] = d0;
+                if (f0 + 1 < nf) outs[(f0 + 1) * ldo + r] = d1;
+            }
+        }
+    } else {   // v = K nv: thread -> factor slot fl, rows r0 + RG k; every output is
         // the fma chain over columns 0..cols-1 of k_mpc_dyn_gemm (bitwise)
         const int fl = threadIdx.x % kMpcF, r0 = threadIdx.x / kMpcF;
         if (fl < nf) {
