@@ -690,8 +690,9 @@ def main():
                 "note": "the blocked chain reads its state once per launch; its "
                         "per-launch time is set by the fp64 dynamics products and "
                         "shared-memory traffic, not HBM",
-                "limiter": "shared-memory pipe: ncu L1/TEX 75% of peak, issue slots 54%, "
-                           "DRAM 4.6% (profiles/r02_ncu_mpc_block.md)"}
+                "limiter": "K nv on the fp64 tensor cores (mma.sync m8n8k4); the rest is "
+                           "shared-memory traffic (ncu L1/TEX 65%) and issue (52%); DRAM 6% "
+                           "(profiles/r02_ncu_mpc100k.md)"}
 
     # ---- end to end through the public API (host state in, host state out) ----
     # three calls, each from the same initial state; the median is reported
