@@ -521,6 +521,21 @@ def multi_gpu(args, fg, dist, rank, world, local):
         Et = torch.tensor([len(lg.edge_var)], device="cuda", dtype=torch.float64)
         dist.all_reduce(Et)
         E = int(Et.item())
+    elif args.workload.startswith("mpc"):
+        # strong scaling from the spec alone: each rank builds only its
+        # part (partition.mpc_rank_graph; equal to Partition(...).local)
+        from paper_1603_02526_b200.partition import mpc_rank_graph
+        T = 100_000
+        rng = np.random.default_rng(0)
+        A = 0.05 * rng.standard_normal((16, 16))
+        B = 0.1 * rng.standard_normal((16, 4))
+        q0 = rng.standard_normal(16)
+        spec = fg.MpcSpec(T, fg.LinearSystem(A, B), q0)
+        lg = mpc_rank_graph(spec, rank, world)
+        nr = NcclRank(None, rank, world, device=local, local=lg)
+        st = fg.init_state(lg)
+        info = {"horizon": T, "state_dim": 16, "input_dim": 4, "rank_graph": "mpc_rank_graph"}
+        E = 3 * T + 2
     else:
         g, st, info = build_instance(args.workload)
         nr = NcclRank(g, rank, world, device=local)
@@ -543,7 +558,7 @@ def multi_gpu(args, fg, dist, rank, world, local):
     # over ranks)
     lg = nr.local
     pinned = True
-    if weak:
+    if nr.part is None:
         # rank graphs hold the rank's own state: page-locked like the 1-GPU
         # arm, downloaded back into the same arrays (as run() does); if the
         # host cannot pin that much, the pageable state is used (slower e2e)

@@ -401,3 +401,101 @@ def svm_rank_graph(X, y, rank, world, lam=1.0, rho=1.0, alpha=1.0):
     g.cut_index = cut
     g.ncut = ncut if world > 1 else 0
     return g
+
+
+def _mpc_owners(T, world):
+    """Rank of every MPC factor under ``factor_owner``'s rule, from the
+    horizon alone: anchors are nodes in id order (locality_order keeps id
+    order: node t's key is t-1), a node's anchored load is cost (1 edge) +
+    dyn_t (2 edges) + init (1 edge, node 0), and the single-variable
+    factors follow their node's dynamics factors when those agree
+    (cost_T follows dyn_{T-1}).  Returns (cost, dyn, init) owners."""
+    load = np.full(T + 1, 3.0)
+    load[T] = 1.0
+    load[0] += 1.0
+    cum = np.cumsum(load)
+    total = cum[-1]
+    bounds = np.array([int(np.searchsorted(cum, total * r / world, side="left")) + 1
+                       for r in range(1, world)], dtype=np.int64)
+    node_owner = np.searchsorted(bounds, np.arange(T + 1), side="right").astype(np.int64)
+    dyn = node_owner[:T]
+    cost = node_owner.copy()
+    cost[T] = dyn[T - 1]                   # node T's only multi-variable factor
+    return cost, dyn, int(node_owner[0])
+
+
+def mpc_rank_graph(spec, rank, world):
+    """One rank's part of ``build_mpc(spec)`` built from the spec alone (no
+    global graph on the host).  Equals ``Partition(build_mpc(spec),
+    world).local(rank)``: the same local variables (a contiguous node range,
+    the boundary node of the next rank as a cut variable), the same factors
+    in creation order, GLOBAL ``z_weights`` and the canonical cut vector
+    (``tests/test_partition.py::test_mpc_rank_graph_equals_partition_local``)."""
+    from .graph import GraphBuilder
+    from .operators import MpcCost, MpcDyn, MpcInit
+    from ._pairwise import pairwise_sum
+    T = int(spec.horizon)
+    d, k = spec.system.state_dim, spec.system.control_dim
+    n0 = d + k
+    cost_o, dyn_o, init_o = _mpc_owners(T, world)
+    own_cost = np.nonzero(cost_o == rank)[0]
+    own_dyn = np.nonzero(dyn_o == rank)[0]
+    own_init = init_o == rank
+    used = np.unique(np.concatenate([own_cost, own_dyn, own_dyn + 1,
+                                     [0] if own_init else []]).astype(np.int64))
+    if len(used) == 0:
+        raise ValueError(f"rank {rank} of {world} owns no factor of a horizon-{T} MPC")
+    lo = int(used[0])
+    if not np.array_equal(used, np.arange(lo, lo + len(used))):
+        raise AssertionError("MPC rank nodes are not contiguous")
+    b = GraphBuilder()
+    nodes = b.declare_variables(n0, len(used))          # local node t - lo
+    diag = np.tile(np.concatenate([spec.q_diag, spec.r_diag]), (len(own_cost), 1))
+    diag[own_cost == T, :d] = spec.qf_diag
+    if len(own_cost):
+        b.add_factors(MpcCost, nodes[own_cost - lo][:, None], rho=spec.rho, alpha=spec.alpha,
+                      params={"diag": diag, "qdim": np.full(len(own_cost), d)},
+                      slot_dims=(n0,))
+    if len(own_dyn):
+        b.add_factors(MpcDyn, np.stack([nodes[own_dyn - lo], nodes[own_dyn + 1 - lo]], axis=1),
+                      rho=spec.rho, alpha=spec.alpha,
+                      params={"systems": [spec.system],
+                              "index": np.zeros(len(own_dyn), dtype=np.int64)},
+                      slot_dims=(n0, n0))
+    if own_init:
+        b.add_factor(MpcInit(spec.q0, k), [int(nodes[0 - lo])], rho=spec.rho, alpha=spec.alpha)
+    g = b.freeze()
+    # global z weights: node t's incident edges in creation order are
+    # [cost_t, dyn_{t-1} slot 1, dyn_t slot 0] (+ init at node 0; node T
+    # has no dyn_T), summed in NumPy's pairwise order (graph.py:216-222)
+    rho = float(spec.rho)
+    deg = np.full(T + 1, 3)
+    deg[T] = 2
+    w = {int(n): float(pairwise_sum(np.full(n, rho))) for n in np.unique(deg)}
+    zw = np.repeat(np.array([w[int(deg[t])] for t in used]), n0)
+    g.z_weights = zw
+    # cut nodes: incident factors on more than one rank
+    cut_node = np.zeros(T + 1, dtype=bool)
+    if world > 1:
+        owners = [cost_o]
+        prev = np.full(T + 1, -1)
+        prev[1:] = dyn_o                    # dyn_{t-1} at node t
+        nxt = np.full(T + 1, -1)
+        nxt[:T] = dyn_o                     # dyn_t at node t
+        init = np.full(T + 1, -1)
+        init[0] = init_o
+        allo = np.stack([cost_o, prev, nxt, init])
+        valid = allo >= 0
+        hi = np.where(valid, allo, -1).max(axis=0)
+        lo_o = np.where(valid, allo, world).min(axis=0)
+        cut_node = hi != lo_o
+        del owners
+    cut_nodes = np.nonzero(cut_node)[0]
+    cut = np.full(g.z_dim, -1, dtype=np.int64)
+    pos = {int(t): i for i, t in enumerate(cut_nodes)}
+    for j, t in enumerate(used):
+        if int(t) in pos:
+            cut[j * n0:(j + 1) * n0] = pos[int(t)] * n0 + np.arange(n0)
+    g.cut_index = cut
+    g.ncut = len(cut_nodes) * n0
+    return g

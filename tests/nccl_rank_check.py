@@ -36,12 +36,30 @@ def main():
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    g = graph(name)
-    st = fg.init_state(g, seed=7)
-    nr = NcclRank(g, rank, world, device=local)
-    nr.upload(st)
-    res, hist = nr.run(iters)
-    out = nr.gather_state(st)
+    if name == "mpc_rank":
+        # the rank graph built from the spec alone (no global graph)
+        from paper_1603_02526_b200.partition import mpc_rank_graph
+        rng = np.random.default_rng(0)
+        A = 0.05 * rng.standard_normal((16, 16))
+        B = 0.1 * rng.standard_normal((16, 4))
+        spec = fg.MpcSpec(2000, fg.LinearSystem(A, B), rng.standard_normal(16))
+        g = fg.build_mpc(spec)
+        lg = mpc_rank_graph(spec, rank, world)
+        st = fg.init_state(g, seed=7)
+        nr = NcclRank(None, rank, world, device=local, local=lg)
+        if world != 1:
+            raise SystemExit("mpc_rank check compares the gathered state at world 1 only")
+        nr.upload(st)
+        res, hist = nr.run(iters)
+        out = fg.AdmmState(*(np.empty_like(getattr(st, k)) for k in "xmzun"))
+        nr.plan.download(x=out.x, m=out.m, z=out.z, u=out.u, n=out.n)
+    else:
+        g = graph(name)
+        st = fg.init_state(g, seed=7)
+        nr = NcclRank(g, rank, world, device=local)
+        nr.upload(st)
+        res, hist = nr.run(iters)
+        out = nr.gather_state(st)
     if rank == 0:
         single = fg.AdmmState(*(getattr(st, k).copy() for k in "xmzun"))
         _sol, rep = fg.run(g, fg.RunConfig(max_iterations=iters), state=single)

@@ -249,3 +249,34 @@ def test_local_graph_follows_set_edge_params():
     assert lg.edge_rho[3] == 2.5 and lg.edge_alpha[3] == 0.75
     np.testing.assert_array_equal(lg.z_weights, g.z_weights[lg.global_z])
     np.testing.assert_array_equal(lg.rho_flat, np.repeat(lg.edge_rho, np.diff(lg.edge_offsets)))
+
+
+@pytest.mark.parametrize("T,world", [(2, 2), (5, 3), (40, 4), (333, 8), (100, 2)])
+def test_mpc_rank_graph_equals_partition_local(T, world):
+    """The per-rank MPC builder (no global graph on the host) emits exactly
+    the partitioner's local graph: variables, factors in creation order,
+    parameters, global z weights (rho != 1) and the canonical cut vector."""
+    from paper_1603_02526_b200.partition import Partition, mpc_rank_graph
+    rng = np.random.default_rng(0)
+    A, B = 0.05 * rng.standard_normal((4, 4)), 0.1 * rng.standard_normal((4, 2))
+    spec = fg.MpcSpec(T, fg.LinearSystem(A, B), rng.standard_normal(4), rho=1.5, alpha=0.8)
+    part = Partition(fg.build_mpc(spec), world)
+    for r in range(world):
+        lg = part.local(r)
+        if len(lg.edge_var) == 0:
+            with pytest.raises(ValueError):
+                mpc_rank_graph(spec, r, world)
+            continue
+        rg = mpc_rank_graph(spec, r, world)
+        for k in ("edge_var", "edge_offsets", "var_offsets", "edge_rho", "edge_alpha",
+                  "z_weights", "cut_index"):
+            np.testing.assert_array_equal(np.asarray(getattr(lg, k)), np.asarray(getattr(rg, k)),
+                                          err_msg=k)
+        assert lg.ncut == rg.ncut
+        assert len(lg.blocks) == len(rg.blocks)
+        for (c1, d1, _f1, v1, p1), (c2, d2, _f2, v2, p2) in zip(lg.blocks, rg.blocks):
+            assert c1.kind == c2.kind and tuple(d1) == tuple(d2)
+            np.testing.assert_array_equal(v1, v2)
+            for k in p1:
+                if k != "systems":
+                    np.testing.assert_array_equal(np.asarray(p1[k]), np.asarray(p2[k]))
