@@ -501,7 +501,9 @@ def multi_gpu(args, fg, dist, rank, world, local):
     own part (partition.svm_rank_graph; cut set:
     the bias and one weight copy per rank boundary); value = all ranks'
     edges x K / max-rank time.  Packing / MPC: strong scaling of the one
-    graph, partitioned by partition.Partition."""
+    graph; each rank builds only its part from the spec
+    (partition.packing_rank_graph / mpc_rank_graph, equal to
+    Partition(...).local(rank))."""
     import torch
     from paper_1603_02526_b200.distributed import NcclRank
     from paper_1603_02526_b200.partition import svm_rank_graph
@@ -536,6 +538,17 @@ def multi_gpu(args, fg, dist, rank, world, local):
         st = fg.init_state(lg)
         info = {"horizon": T, "state_dim": 16, "input_dim": 4, "rank_graph": "mpc_rank_graph"}
         E = 3 * T + 2
+    elif args.workload.startswith("pack"):
+        # strong scaling from the spec alone (partition.packing_rank_graph)
+        from paper_1603_02526_b200.partition import packing_rank_graph
+        n = 5000 if args.workload == "pack5000" else 100
+        spec = fg.PackingSpec(n)
+        lg = packing_rank_graph(spec, rank, world)
+        nr = NcclRank(None, rank, world, device=local, local=lg)
+        st = fg.packing_init(lg, spec, seed=0)
+        S = len(spec.planes)
+        info = {"disks": n, "init": "packing_init(seed=0)", "rank_graph": "packing_rank_graph"}
+        E = 4 * (n * (n - 1) // 2) + n + 2 * S * n
     else:
         g, st, info = build_instance(args.workload)
         nr = NcclRank(g, rank, world, device=local)

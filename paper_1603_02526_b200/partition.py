@@ -499,3 +499,111 @@ def mpc_rank_graph(spec, rank, world):
     g.cut_index = cut
     g.ncut = len(cut_nodes) * n0
     return g
+
+
+def _packing_owners(N, S):
+    """Ranks-independent pieces of ``factor_owner`` for ``build_packing``:
+    anchor positions are variable ids (locality_order keeps id order: every
+    variable meets disk 0's center, so all keys tie), center i = 2i, radius
+    i = 2i + 1; the anchored load of center i is 4 (N-1-i) collision edges
+    + 2 S wall edges, of radius i its radius factor (1 edge)."""
+    load = np.empty(2 * N)
+    load[0::2] = 4.0 * (N - 1 - np.arange(N)) + 2.0 * S
+    load[1::2] = 1.0
+    return np.cumsum(load)
+
+
+def packing_rank_graph(spec, rank, world):
+    """One rank's part of ``build_packing(spec)`` built from the spec alone
+    (no global graph on the host).  Equals ``Partition(build_packing(spec),
+    world).local(rank)``: collision pairs (i, j > i) for the rank's anchor
+    disks i in creation order, their walls and radius factors, the rank's
+    variables in id order, GLOBAL ``z_weights`` and the canonical cut
+    vector (``tests/test_partition.py::test_packing_rank_graph_equals_partition_local``)."""
+    from .graph import GraphBuilder
+    from .operators import Collision, Radius, Wall
+    from ._pairwise import pairwise_sum
+    N, S = int(spec.n), len(spec.planes)
+    cum = _packing_owners(N, S)
+    total = cum[-1]
+    bounds = np.array([int(np.searchsorted(cum, total * r / world, side="left")) + 1
+                       for r in range(1, world)], dtype=np.int64)
+    pos_owner = np.searchsorted(bounds, np.arange(2 * N), side="right").astype(np.int64)
+    c_own = pos_owner[0::2]                     # collisions (i, .) and walls of disk i
+    # radius i follows disk i's multi-variable factors when they agree
+    lo_o = np.minimum(np.where(np.arange(N) > 0, c_own[0], c_own), c_own)
+    prev = np.concatenate([[c_own[0]], c_own[:-1]])
+    hi_o = np.maximum(np.where(np.arange(N) > 0, prev, c_own), c_own)
+    r_own = np.where(lo_o == hi_o, lo_o, pos_owner[1::2])
+    coll = np.nonzero(c_own == rank)[0] if N > 1 else np.zeros(0, dtype=np.int64)
+    coll = coll[coll < N - 1]
+    walls = np.nonzero(c_own == rank)[0]
+    rads = np.nonzero(r_own == rank)[0]
+    # used variables (global ids): partners j > i of the collision anchors,
+    # the anchors, wall disks, radius variables
+    parts = [2 * walls, 2 * walls + 1, 2 * rads + 1]
+    if len(coll):
+        a = int(coll.min())
+        parts += [2 * coll, 2 * coll + 1, np.arange(2 * (a + 1), 2 * N)]
+    used = np.unique(np.concatenate(parts).astype(np.int64))
+    if len(used) == 0:
+        raise ValueError(f"rank {rank} of {world} owns no factor of a {N}-disk packing")
+    lid = np.full(2 * N, -1, dtype=np.int64)
+    lid[used] = np.arange(len(used))
+    b = GraphBuilder()
+    dims = np.where(used % 2 == 0, 2, 1)
+    for dm in dims:                              # declaration order = global id order
+        b.declare_variable(int(dm))
+    if len(coll):
+        ii = np.repeat(coll, N - 1 - coll)
+        starts = np.repeat(np.cumsum(N - 1 - coll) - (N - 1 - coll), N - 1 - coll)
+        jj = ii + 1 + (np.arange(len(ii)) - starts)
+        b.add_factors(Collision, np.stack([lid[2 * ii], lid[2 * ii + 1], lid[2 * jj],
+                                           lid[2 * jj + 1]], axis=1),
+                      rho=spec.rho, alpha=spec.alpha, slot_dims=(2, 1, 2, 1))
+    if len(rads):
+        b.add_factors(Radius, lid[2 * rads + 1][:, None], rho=spec.rho_radius, alpha=spec.alpha,
+                      params={"kappa": np.full(len(rads), float(spec.kappa))}, slot_dims=(1,))
+    if len(walls):
+        normals = np.stack([p.normal for p in spec.planes])
+        points = np.stack([p.point for p in spec.planes])
+        b.add_factors(Wall, np.stack([np.repeat(lid[2 * walls], S), np.repeat(lid[2 * walls + 1], S)],
+                                     axis=1),
+                      rho=spec.rho, alpha=spec.alpha,
+                      params={"Q": np.tile(normals, (len(walls), 1)),
+                              "V": np.tile(points, (len(walls), 1))},
+                      slot_dims=(2, 1))
+    g = b.freeze()
+    # global z weights: a center's incident edges are N-1 collisions then S
+    # walls; a radius's N-1 collisions, its radius factor, S walls
+    # (creation order), summed in NumPy's pairwise order
+    rho, rr = float(spec.rho), float(spec.rho_radius)
+    wc = float(pairwise_sum(np.full(N - 1 + S, rho)))
+    wr = float(pairwise_sum(np.concatenate([np.full(N - 1, rho), [rr], np.full(S, rho)])))
+    g.z_weights = np.concatenate([np.full(2, wc) if v % 2 == 0 else [wr] for v in used])
+    # cut variables: incident factors on more than one rank (owners are
+    # monotone in the anchor position, so a center j's collision owners span
+    # c_own[0] .. c_own[j-1] plus c_own[j])
+    idx = np.arange(N)
+    first = np.where(idx > 0, c_own[0], c_own)
+    cut_c = (first != c_own) if N > 1 else np.zeros(N, dtype=bool)
+    cut_r = cut_c | (r_own != c_own)
+    cut_var = np.empty(2 * N, dtype=bool)
+    cut_var[0::2] = cut_c
+    cut_var[1::2] = cut_r
+    zoff = np.zeros(2 * N + 1, dtype=np.int64)
+    zoff[1:] = np.cumsum(np.tile([2, 1], N))
+    cut_vars = np.nonzero(cut_var)[0]
+    cpos = np.zeros(2 * N, dtype=np.int64)
+    cpos[cut_vars] = np.cumsum(np.tile([2, 1], N)[cut_vars]) - np.tile([2, 1], N)[cut_vars]
+    cut = np.full(g.z_dim, -1, dtype=np.int64)
+    loff = np.asarray(g.var_offsets)
+    for j, v in enumerate(used):
+        if cut_var[v]:
+            dm = 2 if v % 2 == 0 else 1
+            cut[loff[j]:loff[j] + dm] = cpos[v] + np.arange(dm)
+    g.cut_index = cut
+    g.ncut = int(np.tile([2, 1], N)[cut_vars].sum())
+    g.global_var = used                         # for packing_init on the rank graph
+    del zoff
+    return g

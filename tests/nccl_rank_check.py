@@ -36,7 +36,20 @@ def main():
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if name == "mpc_rank":
+    if name == "pack_rank":
+        from paper_1603_02526_b200.partition import packing_rank_graph
+        spec = fg.PackingSpec(150)
+        g = fg.build_packing(spec)
+        lg = packing_rank_graph(spec, rank, world)
+        st = fg.init_state(g, seed=7)
+        nr = NcclRank(None, rank, world, device=local, local=lg)
+        if world != 1:
+            raise SystemExit("pack_rank check compares the gathered state at world 1 only")
+        nr.upload(st)
+        res, hist = nr.run(iters)
+        out = fg.AdmmState(*(np.empty_like(getattr(st, k)) for k in "xmzun"))
+        nr.plan.download(x=out.x, m=out.m, z=out.z, u=out.u, n=out.n)
+    elif name == "mpc_rank":
         # the rank graph built from the spec alone (no global graph)
         from paper_1603_02526_b200.partition import mpc_rank_graph
         rng = np.random.default_rng(0)

@@ -100,6 +100,26 @@ def test_multi_gpu_mpc_rank_graph_arm_at_one_rank(gpu):
 
 
 @pytest.mark.gpu
+def test_multi_gpu_packing_rank_graph_arm_at_one_rank(gpu):
+    """The strong-scaled packing arm builds its rank graph from the spec
+    alone (partition.packing_rank_graph) and runs it through NcclRank."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "1", "--master-addr", "127.0.0.1",
+                        "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--gpus", "1", "--partition", "--workload", "pack100",
+                        "--steps", "10", "--warmup", "3"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert d["scaling"] == "strong" and d["value"] > 0 and d["gpu_launches"] > 0
+    assert d["config"]["rank_graph"] == "packing_rank_graph" and d["config"]["edges"] == 20500
+
+
+@pytest.mark.gpu
 def test_multi_gpu_arm_line_at_one_rank(gpu):
     """The torchrun / NCCL arm (factor-partitioned SVM rank graph, NCCL
     all-gather inside the captured iteration) end to end at one rank."""

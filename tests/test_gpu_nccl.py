@@ -18,7 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("name", ["pack", "mpc", "svm", "mpc_rank"])
+@pytest.mark.parametrize("name", ["pack", "mpc", "svm", "mpc_rank", "pack_rank"])
 def test_nccl_rank_world1_matches_single_plan(gpu, name):
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))

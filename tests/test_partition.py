@@ -280,3 +280,38 @@ def test_mpc_rank_graph_equals_partition_local(T, world):
             for k in p1:
                 if k != "systems":
                     np.testing.assert_array_equal(np.asarray(p1[k]), np.asarray(p2[k]))
+
+
+@pytest.mark.parametrize("N,world", [(1, 2), (2, 3), (7, 4), (40, 3), (151, 8), (64, 7)])
+def test_packing_rank_graph_equals_partition_local(N, world):
+    """The per-rank packing builder (no global graph on the host) emits
+    exactly the partitioner's local graph -- including ranks whose boundary
+    falls between a disk's center and its radius -- and packing_init on it
+    is the scatter of the global packing_init state."""
+    from paper_1603_02526_b200.partition import Partition, packing_rank_graph
+    spec = fg.PackingSpec(N, rho=1.5, rho_radius=3.0, alpha=0.7)
+    g = fg.build_packing(spec)
+    part = Partition(g, world)
+    st = fg.packing_init(g, spec, seed=0) if N > 1 else None
+    for r in range(world):
+        lg = part.local(r)
+        if len(lg.edge_var) == 0:
+            with pytest.raises(ValueError):
+                packing_rank_graph(spec, r, world)
+            continue
+        rg = packing_rank_graph(spec, r, world)
+        for k in ("edge_var", "edge_offsets", "var_offsets", "edge_rho", "edge_alpha",
+                  "z_weights", "cut_index"):
+            np.testing.assert_array_equal(np.asarray(getattr(lg, k)), np.asarray(getattr(rg, k)),
+                                          err_msg=k)
+        assert lg.ncut == rg.ncut
+        assert len(lg.blocks) == len(rg.blocks)
+        for (c1, d1, _f1, v1, p1), (c2, d2, _f2, v2, p2) in zip(lg.blocks, rg.blocks):
+            assert c1.kind == c2.kind and tuple(d1) == tuple(d2)
+            np.testing.assert_array_equal(v1, v2)
+            for k in p1:
+                np.testing.assert_array_equal(np.asarray(p1[k]), np.asarray(p2[k]))
+        if st is not None:
+            rs = fg.packing_init(rg, spec, seed=0)
+            np.testing.assert_array_equal(np.asarray(st.z)[lg.global_z], rs.z)
+            np.testing.assert_array_equal(np.asarray(st.n)[lg.global_payload], rs.n)
