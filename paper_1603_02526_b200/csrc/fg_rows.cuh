@@ -11,7 +11,6 @@
 // a row's tree top and update (equal at best).
 #pragma once
 
-#include <cooperative_groups.h>
 
 #include "fg_tma.cuh"
 
