@@ -45,6 +45,7 @@ constexpr int kMbThreads = kEdgeThreads;               // 256
 constexpr int kMbMT = (kDynGemmMaxCols + 7) / 8;       // row tiles of K (last one clamped)
 constexpr int kMbLD = 44;                              // factor row stride: nv, then v (aliased)
 constexpr int kMbNN = kMbF + 1;                        // nodes staged per CTA (tile + 2 KB)
+constexpr int kMbEPT = (kMbNN * 20 + kMbThreads - 1) / kMbThreads;   // node components per thread (n0 <= 20)
 
 // K (cols x cols), z and the three u slots of the staged nodes, and one
 // factor row buffer holding nv (staging) and then v (K nv) in place: ~74 KB
@@ -64,7 +65,7 @@ __global__ void __launch_bounds__(kMbThreads, 3) k_mpc_block(PassB b, MpcChainDe
     __shared__ double sm[2 * (kMbThreads / 32)];
     if (b.ctrl->stop) return;
     constexpr int n0 = N0, d = DD, cols = N0 + DD, ld = kMbLD, ldo = kMbLD;
-    static_assert(cols % 4 == 0 && cols <= 8 * kMbMT && 2 * n0 <= kMbLD, "tile sizes");
+    static_assert(cols % 4 == 0 && cols <= 8 * kMbMT && 2 * n0 <= kMbLD && n0 <= 20, "tile sizes");
     static_assert(kMbF == 8 * (kMbThreads / 32), "one 8-factor tile per warp");
     double* Ks = gsm;                                   // [cols][cols] row-major
     double* zs = Ks + cols * cols;                      // [NN][n0]
@@ -105,6 +106,15 @@ __global__ void __launch_bounds__(kMbThreads, 3) k_mpc_block(PassB b, MpcChainDe
     const int64_t it0 = b.ctrl->iter;
     const double r3 = qdiv_rcp(3.0);                    // z = S / 3 without the runtime call
     bool bad = false;
+    // the cost diagonal of this thread's node components (the same ones in
+    // every iteration), held in registers across the KB iterations
+    double cst[kMbEPT];
+#pragma unroll
+    for (int jj = 0; jj < kMbEPT; ++jj) {
+        const int idx = threadIdx.x + jj * kMbThreads;
+        const int tl = idx / n0, q = idx - tl * n0;
+        cst[jj] = idx < NN * n0 ? __ldg(c.cost_fp + (int64_t)(a + tl) * c.cost_st + q) : 0.0;
+    }
     for (int i = 0; i < KB; ++i) {
         // ---- n of the dynamics factors (k_mpc_chain's staging) ----
         for (int idx = threadIdx.x; idx < nf * 2 * n0; idx += blockDim.x) {
@@ -151,7 +161,10 @@ __global__ void __launch_bounds__(kMbThreads, 3) k_mpc_block(PassB b, MpcChainDe
         __syncthreads();
         // ---- nodes: cost / init proxes, m, z, u (in place) ----
         double pp = 0.0, dd = 0.0;
-        for (int idx = threadIdx.x; idx < NN * n0; idx += blockDim.x) {
+#pragma unroll
+        for (int jj = 0; jj < kMbEPT; ++jj) {
+            const int idx = threadIdx.x + jj * kMbThreads;
+            if (idx >= NN * n0) break;
             const int tl = idx / n0, q = idx - tl * n0;
             const int t = a + tl;
             const bool own = t >= t0 && t < t1;
@@ -162,7 +175,7 @@ __global__ void __launch_bounds__(kMbThreads, 3) k_mpc_block(PassB b, MpcChainDe
             u[1] = us[(tl * 3 + 1) * n0 + q];
             u[2] = us[(tl * 3 + 2) * n0 + q];
             const double n_c = zi - u[0];
-            x[0] = prox_mpc_cost(n_c, 1.0, __ldg(c.cost_fp + (int64_t)t * c.cost_st + q));
+            x[0] = prox_mpc_cost(n_c, 1.0, cst[jj]);
             bool bn = !finite(n_c);
             // rank 1: dyn_{t-1} slot 1 (node 0: dyn_0 slot 0); a halo node
             // without its factor computes a placeholder (never owned)
