@@ -116,7 +116,9 @@ __global__ void __launch_bounds__(kMbThreads, 3) k_mpc_block(PassB b, MpcChainDe
         cst[jj] = idx < NN * n0 ? __ldg(c.cost_fp + (int64_t)(a + tl) * c.cost_st + q) : 0.0;
     }
     for (int i = 0; i < KB; ++i) {
-        // ---- n of the dynamics factors (k_mpc_chain's staging) ----
+        // ---- n of the dynamics factors (k_mpc_chain's staging): the first
+        // iteration here, later ones written by the previous node pass ----
+        if (i == 0)
         for (int idx = threadIdx.x; idx < nf * 2 * n0; idx += blockDim.x) {
             const int fl = idx / (2 * n0), cc = idx - fl * (2 * n0);
             const int f = a + fl;
@@ -207,17 +209,37 @@ __global__ void __launch_bounds__(kMbThreads, 3) k_mpc_block(PassB b, MpcChainDe
             bb |= !finite(zn);
             zs[tl * n0 + q] = zn;
             const double dz = zn - zi;
+            double un3[3];
 #pragma unroll
             for (int kk = 0; kk < 3; ++kk) {
+                un3[kk] = 0.0;
                 if (kk < deg) {
                     const double tt = x[kk] - zn;
                     const double un = u[kk] + tt;
+                    un3[kk] = un;
                     us[(tl * 3 + kk) * n0 + q] = un;
                     bb |= !finite(un);
                     if (own) {
                         pp += tt * tt;
                         dd += dz * dz;
                     }
+                }
+            }
+            // the next iteration's staging of this node's dynamics slots
+            // (same values the staging loop would read after the pass; each
+            // factor-row position is read above and rewritten here by the
+            // same thread, so the pass needs no extra barrier)
+            if (i + 1 < KB) {
+                if (tl < nf) {                          // slot 0 of factor tl
+                    const double n = zn - un3[t == 0 ? 1 : 2];
+                    bb |= !finite(n);
+                    nvs[tl * ld + q] = n;
+                }
+                if (tl >= 1) {                          // slot 1 of factor tl-1
+                    const double n = zn - un3[1];
+                    bb |= !finite(n);
+                    if (q < d) nvs[(tl - 1) * ld + n0 + q] = n;
+                    else outs[(tl - 1) * ldo + n0 + q] = n;   // control of t+1
                 }
             }
             bad |= own && bb;
