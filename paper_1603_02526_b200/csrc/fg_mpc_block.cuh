@@ -62,7 +62,6 @@ __global__ void __launch_bounds__(kMbThreads, 3) k_mpc_block(PassB b, MpcChainDe
                                                              int64_t fault_it = 0) {
     static_assert(KB % 2 == 1, "a block must flip the ping-pong slot");
     extern __shared__ double gsm[];
-    __shared__ double sm[2 * (kMbThreads / 32)];
     if (b.ctrl->stop) return;
     constexpr int n0 = N0, d = DD, cols = N0 + DD, ld = kMbLD, ldo = kMbLD;
     static_assert(cols % 4 == 0 && cols <= 8 * kMbMT && 2 * n0 <= kMbLD && n0 <= 20, "tile sizes");
@@ -76,6 +75,14 @@ __global__ void __launch_bounds__(kMbThreads, 3) k_mpc_block(PassB b, MpcChainDe
     // into its fragments, so nv and v share the buffer
     double* nvs = us + kMbNN * 3 * n0;                  // [F][ld]
     double* outs = nvs;
+    // per-iteration warp sums of the residual partials live in the unused
+    // columns 2 n0 .. ld-1 of the factor rows (KB x warps x 2 doubles)
+    static_assert(KB * (kMbThreads / 32) * 2 <= kMbF * (kMbLD - 2 * N0), "warp-sum slots");
+    auto wsum = [&](int i, int w, int k) -> double& {
+        const int f = (i * (kMbThreads / 32) + w) * 2 + k;
+        constexpr int per = kMbLD - 2 * N0;
+        return nvs[(f / per) * ld + 2 * n0 + f % per];
+    };
     const int T = c.T;
     const int t0 = blockIdx.x * tile;
     const int t1 = min(T + 1, t0 + tile);               // owned nodes [t0, t1)
@@ -244,12 +251,35 @@ __global__ void __launch_bounds__(kMbThreads, 3) k_mpc_block(PassB b, MpcChainDe
             }
             bad |= own && bb;
         }
-        block_sum2<kMbThreads>(pp, dd, sm);             // (its barriers also
-        if (threadIdx.x == 0) {                         //  order the next staging)
-            bpart[2 * ((int64_t)i * ntiles + blockIdx.x)] = pp;
-            bpart[2 * ((int64_t)i * ntiles + blockIdx.x) + 1] = dd;
+        // residual partials: block_sum2's warp stage now, its cross-warp
+        // stage for all KB iterations after the loop (same order, one
+        // barrier per iteration instead of three)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            pp += __shfl_xor_sync(kFull, pp, o);
+            dd += __shfl_xor_sync(kFull, dd, o);
         }
-        __syncthreads();
+        if ((threadIdx.x & 31) == 0) {
+            wsum(i, threadIdx.x >> 5, 0) = pp;
+            wsum(i, threadIdx.x >> 5, 1) = dd;
+        }
+        __syncthreads();                                // node pass done: next GEMM
+    }
+    if (threadIdx.x < 32) {
+        const int l = threadIdx.x;
+        for (int i = 0; i < KB; ++i) {
+            double pa = l < kMbThreads / 32 ? wsum(i, l, 0) : 0.0;
+            double da = l < kMbThreads / 32 ? wsum(i, l, 1) : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                pa += __shfl_xor_sync(kFull, pa, o);
+                da += __shfl_xor_sync(kFull, da, o);
+            }
+            if (l == 0) {
+                bpart[2 * ((int64_t)i * ntiles + blockIdx.x)] = pa;
+                bpart[2 * ((int64_t)i * ntiles + blockIdx.x) + 1] = da;
+            }
+        }
     }
     // fault injection for the replay test (FGADMM_MPC_BLOCK_FAULT=<iteration>)
     bad |= fault_it >= it0 && fault_it < it0 + KB;
