@@ -146,6 +146,9 @@ __global__ void __launch_bounds__(kMbThreads, 3) k_mpc_block(PassB b, MpcChainDe
             double bf[cols / 4];
 #pragma unroll
             for (int ks = 0; ks < cols / 4; ++ks) bf[ks] = nvs[fb * ld + 4 * ks + kq];
+            // every lane's nv reads precede any lane's v writes into the
+            // same (aliased) rows of this warp
+            __syncwarp();
             const int f0 = 8 * w + 2 * kq;
 #pragma unroll 1
             for (int m = 0; m < kMbMT; ++m) {
