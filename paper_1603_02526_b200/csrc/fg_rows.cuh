@@ -233,18 +233,36 @@ k_var_row_pipe(PassB b, const RowDesc* rdesc, const int32_t* prog, const int32_t
                 }
             }
         } else {
-            const int64_t nq = (hi - lo) * D;
-            for (int64_t q = threadIdx.x; q < nq; q += kRowThreads) {
-                const int64_t e = lo + q / D;
-                const int c = (int)(q - (e - lo) * D);
-                const bool ex = e == xe.rank;
-                const double t = X[q] - zn[c];
-                pp += t * t;
-                const double rd = ex ? xe.rho * dz[c] : dz[c];
-                dd += rd * rd;
-                const double un = U[q] + (ex ? t * xe.alpha : t);
-                b.uout[pb + lo * D + q] = un;
-                bu |= !finite(un);
+            if (D == 1) {
+                // 32-bit job-local indices (dim-1 rows: 2% faster); the
+                // exception edge, if in this job, as a job-local index
+                const int nq = (int)(hi - lo);
+                const int exl = (xe.rank >= lo && xe.rank < hi) ? (int)(xe.rank - lo) : -1;
+                double* __restrict__ uo = b.uout + pb + lo;
+                for (int q = threadIdx.x; q < nq; q += kRowThreads) {
+                    const bool ex = q == exl;
+                    const double t = X[q] - zn[0];
+                    pp += t * t;
+                    const double rd = ex ? xe.rho * dz[0] : dz[0];
+                    dd += rd * rd;
+                    const double un = U[q] + (ex ? t * xe.alpha : t);
+                    uo[q] = un;
+                    bu |= !finite(un);
+                }
+            } else {
+                const int64_t nq = (hi - lo) * D;
+                for (int64_t q = threadIdx.x; q < nq; q += kRowThreads) {
+                    const int64_t e = lo + q / D;
+                    const int c = (int)(q - (e - lo) * D);
+                    const bool ex = e == xe.rank;
+                    const double t = X[q] - zn[c];
+                    pp += t * t;
+                    const double rd = ex ? xe.rho * dz[c] : dz[c];
+                    dd += rd * rd;
+                    const double un = U[q] + (ex ? t * xe.alpha : t);
+                    b.uout[pb + lo * D + q] = un;
+                    bu |= !finite(un);
+                }
             }
         }
         __syncthreads();                               // stage s consumed
