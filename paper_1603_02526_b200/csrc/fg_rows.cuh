@@ -28,8 +28,9 @@ constexpr int kRowThreads = 256;
 // stage; consumers wait on the stage's mbarrier.  The phase-2 copies of
 // the first NS chunks are issued while phase 1 ends and warp 0 evaluates
 // the top of the tree and z, so the load stream never stops.  Stage size
-// SDB (doubles per array): 1280 at 4 CTAs/SM for dim-1 rows (pack N=5000
-// radius rows 0.137 vs 0.157 ms with three stages), 2048 at 3 CTAs/SM for
+// SDB (doubles per array): 1280 at 5 CTAs/SM for dim-1 rows (48 registers;
+// pack N=5000 radius rows 0.130 ms, 0.133 at 4 CTAs/SM, 0.157 with three
+// stages at 3), 2048 at 3 CTAs/SM for
 // dim >= 2 rows (center rows 0.254 vs 0.264 ms with 2 x 2560 at 2 CTAs/SM;
 // profiles/r01_rows_ab.md).  L2HINT: phase-1 copies are marked L2
 // evict_last (phase 2 reads the same bytes again), phase-2 copies
@@ -50,11 +51,11 @@ struct __align__(16) RowDesc {
 };
 
 constexpr int kPipeMidDoubles = 2048;               // dim >= 2 rows: 3 CTAs/SM
-constexpr int kPipeStageDoubles = 1280;             // dim-1 rows: 4 CTAs/SM
+constexpr int kPipeStageDoubles = 1280;             // dim-1 rows: 5 CTAs/SM
 constexpr int kPipeNS = 2;                          // stages
 
 template <int D, int SDB, bool L2HINT>
-__global__ void __launch_bounds__(kRowThreads, SDB <= kPipeStageDoubles ? 4 : 3)
+__global__ void __launch_bounds__(kRowThreads, SDB <= kPipeStageDoubles ? 5 : 3)
 k_var_row_pipe(PassB b, const RowDesc* rdesc, const int32_t* prog, const int32_t* plans,
                const LExc* exc, int64_t part_off) {
     extern __shared__ __align__(16) double pipe_smem[];
