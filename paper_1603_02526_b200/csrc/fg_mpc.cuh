@@ -131,9 +131,12 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_dyn_gemm(PassA a, Group
     // K stored as [c][r0][k] for row r = r0 + 2k: a thread's 20 rows of one
     // column are contiguous (16-byte loads)
     constexpr int KH = kDynGemmMaxCols / 2;
+    // cols a multiple of 4 (the 16/4 systems): K row-major for the f64 MMA
+    const bool mma = (cols & 3) == 0;
     for (int i = threadIdx.x; i < cols * cols; i += blockDim.x) {
         const int r = i / cols, c = i - r * cols;
-        Ks[(c * 2 + (r & 1)) * KH + (r >> 1)] = g.kmat[i];
+        if (mma) Ks[i] = g.kmat[i];
+        else Ks[(c * 2 + (r & 1)) * KH + (r >> 1)] = g.kmat[i];
     }
     // stage n: factor f's slot 0 (n0 values) and slot 1 (n0 values, the
     // first d enter the projection, the rest pass through to x).  The
@@ -161,8 +164,39 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_dyn_gemm(PassA a, Group
         else outs[f * ldo + n0 + cc] = n;                  // control of t+1 passes
     }
     __syncthreads();
+    if (mma) {
+        // out^T = K . nv^T as mma.sync.m8n8k4 f64 tiles (k_mpc_block's form):
+        // warp w owns the factor tiles w and w + 8; every output is the
+        // same fma chain over the columns as the scalar form below (bitwise)
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, kq = lane & 3;
+        const int C4 = cols >> 2;
+        for (int nt = w; nt < kDynGemmF / 8; nt += kEdgeThreads / 32) {
+            const int fb = 8 * nt + (lane >> 2);
+            double bf[kDynGemmMaxCols / 4];
+#pragma unroll
+            for (int ks = 0; ks < kDynGemmMaxCols / 4; ++ks)
+                bf[ks] = ks < C4 ? nvs[fb * ld + 4 * ks + kq] : 0.0;
+            const int f0 = 8 * nt + 2 * kq;
+            for (int m = 0; m < (cols + 7) / 8; ++m) {
+                const double* ka = Ks + min(8 * m + (lane >> 2), cols - 1) * cols + kq;
+                double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < kDynGemmMaxCols / 4; ++ks) {
+                    if (ks < C4) {
+                        const double av = ka[4 * ks];
+                        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                                     : "+d"(d0), "+d"(d1) : "d"(av), "d"(bf[ks]));
+                    }
+                }
+                const int r = 8 * m + (lane >> 2);
+                if (r < cols) {
+                    if (f0 < nf) outs[f0 * ldo + r] = d0;
+                    if (f0 + 1 < nf) outs[(f0 + 1) * ldo + r] = d1;
+                }
+            }
+        }
+    } else {
     // out[f][r] = sum_c K[r][c] nv[f][c]: thread -> factor f, rows r0 + 2k
-    {
         const int f = threadIdx.x & (kDynGemmF - 1), r0 = threadIdx.x >> 7;
         if (f < nf) {
             double acc[kDynGemmMaxCols / 2];
