@@ -777,7 +777,13 @@ def main():
                      "iteration": {"alg_bytes": iter_bytes,
                                    "survey_B_alg": survey_alg_bytes(g),
                                    "ms": iter_ms,
-                                   "GBps": iter_bytes / (iter_ms / 1e3) / 1e9}},
+                                   "GBps": iter_bytes / (iter_ms / 1e3) / 1e9},
+                     # EU/s against the two-pass roofline
+                     # (peak x E / B_alg); above 1 when the fused schedules
+                     # move fewer bytes than the two-pass minimum
+                     "survey_roofline_EUps": peak * 1e9 * E / survey_alg_bytes(g) * world,
+                     "value_over_survey_roofline":
+                         value / (peak * 1e9 * E / survey_alg_bytes(g) * world)},
         "kernels": {k: {"ms_avg": v[0] / v[1], "alg_bytes": kb.get(k.split("#")[0], 0)}
                     for k, v in prof.items()},
         "cpu_baseline": cpu,
