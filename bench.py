@@ -517,7 +517,7 @@ def multi_gpu(args, fg, dist, rank, world, local):
         n = int(nt.item())
         X, y = fg.gen_gaussian_arrays(n, 32, 4.0, seed=rank)
         lg = svm_rank_graph(X, y, rank, world, lam=1.0)
-        nr = NcclRank(None, rank, world, device=local, local=lg)
+        nr = NcclRank(None, rank, world, device=local, local=lg, transport=args.transport)
         st = fg.init_state(lg)
         info = {"points": n * world, "points_per_rank": n, "dim": 32, "init": "zeros"}
         Et = torch.tensor([len(lg.edge_var)], device="cuda", dtype=torch.float64)
@@ -534,7 +534,7 @@ def multi_gpu(args, fg, dist, rank, world, local):
         q0 = rng.standard_normal(16)
         spec = fg.MpcSpec(T, fg.LinearSystem(A, B), q0)
         lg = mpc_rank_graph(spec, rank, world)
-        nr = NcclRank(None, rank, world, device=local, local=lg)
+        nr = NcclRank(None, rank, world, device=local, local=lg, transport=args.transport)
         st = fg.init_state(lg)
         info = {"horizon": T, "state_dim": 16, "input_dim": 4, "rank_graph": "mpc_rank_graph"}
         E = 3 * T + 2
@@ -544,14 +544,14 @@ def multi_gpu(args, fg, dist, rank, world, local):
         n = 5000 if args.workload == "pack5000" else 100
         spec = fg.PackingSpec(n)
         lg = packing_rank_graph(spec, rank, world)
-        nr = NcclRank(None, rank, world, device=local, local=lg)
+        nr = NcclRank(None, rank, world, device=local, local=lg, transport=args.transport)
         st = fg.packing_init(lg, spec, seed=0)
         S = len(spec.planes)
         info = {"disks": n, "init": "packing_init(seed=0)", "rank_graph": "packing_rank_graph"}
         E = 4 * (n * (n - 1) // 2) + n + 2 * S * n
     else:
         g, st, info = build_instance(args.workload)
-        nr = NcclRank(g, rank, world, device=local)
+        nr = NcclRank(g, rank, world, device=local, transport=args.transport)
         E = len(g.edge_var)
     t_build = time.perf_counter() - t_build
     clk = ClockSampler(local)
@@ -611,8 +611,9 @@ def multi_gpu(args, fg, dist, rank, world, local):
                    "desc": (f"soft-margin linear SVM chain, {info['points_per_rank'] / 1e6:g}M points "
                             f"per GPU x 32 dims, weak-scaled (configs[4]: 8M per GPU, 64M at 8)"
                             if weak else WORKLOADS[args.workload]), **info,
-                   "edges": E, "parallelism": f"factor partition x{world} (NCCL all-gather "
+                   "edges": E, "parallelism": f"factor partition x{world} ({args.transport.upper()} all-gather "
                                               f"of {getattr(nr.local, 'ncut', 0)} cut components)",
+                   "transport": args.transport,
                    "local_edges": len(nr.local.edge_var), "build_seconds": round(t_build, 2),
                    "host_max_rss_gb": round(__import__("resource").getrusage(
                        __import__("resource").RUSAGE_SELF).ru_maxrss / 2**20, 1)},
@@ -639,6 +640,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--partition", action="store_true",
                     help="take the multi-GPU (NCCL partition) path even at one rank")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
+                    help="multi-GPU cut/residual exchange: NCCL all-gather, or peer-memory "
+                         "stores over NVLink with epoch flags (CUDA IPC)")
     ap.add_argument("--points-per-rank", type=int, default=None,
                     help="SVM points per rank of the weak-scaled multi-GPU run "
                          "(default configs[4]: 8M per GPU = 64M at 8 GPUs, fewer "

@@ -249,6 +249,19 @@ int fg_selftest_div(const double* x, const double* y, int64_t n, double* q,
 int fg_nccl_unique_id(const char* nccl_lib, char* out128);
 int fg_plan_attach_nccl(fg_plan* plan, const char* nccl_lib, const char* id128,
                         int32_t rank, int32_t world);
+/* Peer memory (one process per GPU, no collective library): every rank
+ * calls fg_p2p_export (allocates its receive buffer and flag array for
+ * `world` ranks; out128 = their two CUDA IPC handles), the caller
+ * all-gathers the handles (rank-major, world x 128 bytes), then every rank
+ * calls fg_plan_attach_p2p with them and the graph's global payload size.
+ * fg_run then stores each rank's cut and residual partials straight into
+ * every peer's receive buffer over NVLink and synchronises on per-rank
+ * epoch flags, inside the captured iteration (k_p2p_allgather); the rank-
+ * order sum is the same as the NCCL path's.  A rank that stops answering
+ * for 10 s fails the run with FG_ERR_CUDA instead of hanging. */
+int fg_p2p_export(fg_plan* plan, int32_t world, char* out128);
+int fg_plan_attach_p2p(fg_plan* plan, int32_t rank, int32_t world, const char* handles,
+                       int64_t payload_global);
 /* Local group: the G partition plans of one graph on ONE device, exchanged
  * by device copies (single-GPU validation of the partitioned algorithm).
  * Results are those of rank 0 (identical on all ranks). */

@@ -86,6 +86,8 @@ EXPORTS = {
     "fg_selftest_div": (C.c_int, [_dp, _dp, C.c_int64, _dp, _dp, C.c_int32]),
     "fg_nccl_unique_id": (C.c_int, [C.c_char_p, C.c_char_p]),
     "fg_plan_attach_nccl": (C.c_int, [_p, C.c_char_p, C.c_char_p, C.c_int32, C.c_int32]),
+    "fg_p2p_export": (C.c_int, [_p, C.c_int32, C.c_char_p]),
+    "fg_plan_attach_p2p": (C.c_int, [_p, C.c_int32, C.c_int32, C.c_char_p, C.c_int64]),
     "fg_group_run": (C.c_int, [C.POINTER(_p), C.c_int32, C.POINTER(RunConfig), _dp,
                                C.POINTER(RunResult)]),
     "fg_host_alloc": (C.c_int, [C.c_int64, C.POINTER(_p)]),

@@ -223,6 +223,16 @@ struct fg_plan {
     double* d_send = nullptr;          // [ncut] partials, then [4] residuals
     double* d_recv = nullptr;          // [world*ncut], then [world*4]
     void* nccl_comm = nullptr;         // ncclComm_t when attached
+    // peer-memory exchange (fg_plan_attach_p2p): every rank stores its
+    // partials straight into each peer's receive buffer and raises an epoch
+    // flag there; no collective library
+    int p2p = 0;
+    double** d_peer_recv = nullptr;            // [world] device pointers (own + opened IPC)
+    unsigned long long** d_peer_flags = nullptr;
+    unsigned long long* d_flags = nullptr;     // [world] this rank's flags (peers write)
+    unsigned long long* d_epoch = nullptr;     // exchanges done
+    std::vector<void*> ipc_opened;             // peer pointers to close
+    bool ranked() const { return nccl_comm != nullptr || p2p != 0; }
     int64_t Pglobal = 0;               // payload of the whole graph
     bool partitioned() const { return ncut > 0 || world > 1; }
     // residual partials
@@ -290,6 +300,7 @@ struct fg_plan {
     std::vector<double> phase_ms;      // [iterations x 5] x..n ms of the last profile run
     int64_t launches_per_iter = 0;     // iteration 1 of a run
     int64_t launches_later = 0;        // iterations 2.. (fused chain when on)
+    int64_t launches_ranked = 0;       // ranked plan: own kernel nodes per captured iteration
 
     VarTab vt() const { return VarTab{d_dim, d_deg, d_ebase, d_pbase, d_zbase}; }
     ~fg_plan();
@@ -303,6 +314,9 @@ static int settle_idle(fg_plan* p);  // pending upload check (defined with the u
 fg_plan::~fg_plan() {
     cudaSetDevice(device);
     if (nccl_comm) fg_nccl_release(nccl_comm);
+    for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
+    for (void* q : {(void*)d_peer_recv, (void*)d_peer_flags, (void*)d_flags, (void*)d_epoch})
+        if (q) cudaFree(q);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     void* ptrs[] = {d_dim, d_deg, d_ebase, d_pbase, d_zbase, d_zvar, d_vm2ref,
                     d_vmz, d_vmvar, d_refedge, d_rho, d_alpha, d_zw, d_x,
@@ -577,6 +591,10 @@ int64_t count_var_launches(const fg_plan* p) {
 // process for a local group of plans (fg_group_run).
 int exchange_nccl(fg_plan* p, const double* send, double* recv, size_t count,
                   cudaStream_t st);
+// all-gather of `count` doubles into d_recv + recv_off (rank-major), by
+// NCCL or through peer memory (fg_plan_attach_p2p)
+int exchange_cut(fg_plan* p, const double* send, size_t recv_off, size_t count,
+                 cudaStream_t st);
 
 void cut_finalize(fg_plan* p, int in, cudaStream_t st) {
     if (!p->ncutg) return;
@@ -647,7 +665,7 @@ void chain_pass(fg_plan* p, int in, cudaStream_t st) {
     if (p->mpc_chain) {
         // with reduce_fused the last CTA also runs the residual reduction
         // (not on an NCCL rank: part_mid / part_post reduce across ranks)
-        const FusedReduce fr = p->mpc_reduce_fused && !p->nccl_comm
+        const FusedReduce fr = p->mpc_reduce_fused && !p->ranked()
             ? FusedReduce{p->d_ucnt, p->npart, p->mpc_tiles, p->chain_grid, p->d_hist}
             : FusedReduce{nullptr, 0, 0, 0, nullptr};
         if (p->mpc.n0 == 20 && p->mpc.d == 16)         // configs[2]: state 16, input 4
@@ -730,11 +748,11 @@ bool chain_rest(fg_plan* p, int in, cudaStream_t st) {
 }
 
 void launch_iteration(fg_plan* p, int in, bool first, cudaStream_t st) {
-    if (p->nccl_comm) {
+    if (p->ranked()) {
         part_pre(p, in, first, st);
-        if (p->ncut) exchange_nccl(p, p->d_send, p->d_recv, (size_t)p->ncut, st);
+        if (p->ncut) exchange_cut(p, p->d_send, 0, (size_t)p->ncut, st);
         part_mid(p, in, first, st);
-        exchange_nccl(p, p->d_send + p->ncut, p->d_recv + (size_t)p->world * p->ncut, 4, st);
+        exchange_cut(p, p->d_send + p->ncut, (size_t)p->world * p->ncut, 4, st);
         part_post(p, st);
         return;
     }
@@ -760,6 +778,29 @@ int get_graph(fg_plan* p, int chunk, cudaGraphExec_t* out) {
     for (int i = 0; i < chunk; ++i) launch_iteration(p, (i & 1) ? 0 : 1, false, p->stream);
     cudaError_t e = cudaStreamEndCapture(p->stream, &graph);
     if (e != cudaSuccess) return fail(FG_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    if (p->ranked()) {
+        // a ranked iteration interleaves the partition passes with the
+        // exchanges: count this library's kernel nodes (not NCCL's)
+        size_t nn = 0;
+        cudaGraphGetNodes(graph, nullptr, &nn);
+        std::vector<cudaGraphNode_t> nodes(nn);
+        cudaGraphGetNodes(graph, nodes.data(), &nn);
+        int64_t own = 0;
+        for (auto nd : nodes) {
+            cudaGraphNodeType ty;
+            if (cudaGraphNodeGetType(nd, &ty) != cudaSuccess || ty != cudaGraphNodeTypeKernel)
+                continue;
+            cudaKernelNodeParams kp;
+            const char* name = nullptr;
+            if (cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess &&
+                cudaFuncGetName(&name, kp.func) == cudaSuccess && name &&
+                std::strncmp(name, "nccl", 4) == 0)
+                continue;
+            ++own;
+        }
+        cudaGetLastError();
+        p->launches_ranked = own / chunk;
+    }
     cudaGraphExec_t exec;
     e = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
@@ -1974,7 +2015,7 @@ int fg_state_upload(fg_plan* p, const double* z, const double* u, const double* 
         if (int rc = settle_upload(p, &mism)) return rc;
     }
     // multi-rank runs stay in lock step: no speculative first iterations
-    if (spec_upload_enabled() && !p->nccl_comm && spec_resources(p))
+    if (spec_upload_enabled() && !p->ranked() && spec_resources(p))
         return upload_speculative(p, z, u, n);
     CK(cudaMemcpyAsync(p->d_zb[0], z, p->Z * sizeof(double), cudaMemcpyHostToDevice, p->stream));
     upload_vm(p, u, p->d_u[0]);
@@ -2168,10 +2209,10 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
     h.dual_tol = cfg->dual_tol;
     h.scale = 1.0 / std::sqrt((double)p->P);
     h.max_iter = K;
-    if (p->ncut && !p->nccl_comm)
+    if (p->ncut && !p->ranked())
         return fail(FG_ERR_INVALID, "a partition plan runs through fg_plan_attach_nccl + "
                                     "fg_run or through fg_group_run");
-    if (p->nccl_comm) {
+    if (p->ranked()) {
         h.partitioned = 1;
         h.scale = 1.0 / std::sqrt((double)p->Pglobal);
     }
@@ -2193,8 +2234,10 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
     CK(cudaEventCreate(&ev1));
     double ms_a = 0, ms_b = 0, ms_r = 0;
     int64_t launches = 0;
+    const int64_t later_n = p->ranked() && p->launches_ranked ? p->launches_ranked
+                                                                 : p->launches_later;
     CK(cudaEventRecord(ev0, st));
-    if (cfg->timing && p->nccl_comm) {
+    if (cfg->timing && p->ranked()) {
         for (int64_t j = 1; j <= K; ++j) {
             launch_iteration(p, (int)((j - 1) & 1), (j == 1) && first_n, st);
             launches += p->launches_per_iter + 1;
@@ -2245,7 +2288,7 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
         cudaEvent_t e4[4];
         for (auto& e : e4) CK(cudaEventCreate(&e));
         CK(cudaEventRecord(e4[0], st));
-        if (p->nccl_comm) {
+        if (p->ranked()) {
             launch_iteration(p, 0, first_n, st);
             CK(cudaEventRecord(e4[1], st));
             CK(cudaEventRecord(e4[2], st));
@@ -2263,7 +2306,8 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
             launch_reduce(p, false, st);
         }
         CK(cudaEventRecord(e4[3], st));
-        launches += (p->chain_on && !first_n) ? p->launches_later : p->launches_per_iter;
+        launches += p->ranked() ? later_n
+                                : (p->chain_on && !first_n) ? p->launches_later : p->launches_per_iter;
         int64_t left = K - 1;
         int chunk = std::max(2, cfg->graph_chunk - (cfg->graph_chunk & 1));
         if (!p->h_stop) CK(cudaMallocHost((void**)&p->h_stop, 4 * sizeof(int32_t)));
@@ -2274,7 +2318,7 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
         int inflight = 0, slot = 0;
         bool stopped = false;
         const bool poll = cfg->primal_tol > 0.0 || cfg->dual_tol > 0.0;
-        if (p->mpc_chain && p->mpc_kb > 0 && !poll && !p->nccl_comm) {
+        if (p->mpc_chain && p->mpc_kb > 0 && !poll && !p->ranked()) {
             // fixed budget on the MPC chain: blocks of kMpcKB iterations,
             // the last iteration on the per-iteration kernel (its inputs
             // stay in memory for the x recomputation at download)
@@ -2293,7 +2337,7 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
             }
             for (; left > 0; --left, ++j) {
                 launch_iteration(p, (int)((j - 1) & 1), false, st);
-                launches += p->launches_later;
+                launches += later_n;
             }
         }
         while (left > 0 && !stopped) {
@@ -2313,7 +2357,7 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
                 n = 1;
                 launch_iteration(p, 1, false, st);   // iteration index even -> in=1
             }
-            launches += n * p->launches_later;
+            launches += n * later_n;
             left -= n;
             // Without tolerances the run cannot converge early: everything is
             // enqueued at once (after a failure the remaining kernels exit on
@@ -2360,6 +2404,8 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
         }
     }
     CK(cudaMemcpy(&h, p->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+    if (h.p2p_timeout)
+        return fail(FG_ERR_CUDA, "peer-memory exchange: a rank stopped answering (10 s)");
     if (h.blk_err) {
         // a temporally blocked launch met a non-finite value: it stopped the
         // run without writing, so its input slot is intact -- replay from
@@ -2372,7 +2418,7 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
         CK(cudaMemcpyAsync(p->d_ctrl, &h, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
         for (int64_t j = j0; j <= K; ++j) {
             launch_iteration(p, (int)((j - 1) & 1), false, st);
-            launches += p->launches_later;
+            launches += later_n;
         }
         CK(cudaStreamSynchronize(st));
         if (int rc = check_launch()) return rc;
@@ -2869,6 +2915,72 @@ int exchange_nccl(fg_plan* p, const double* send, double* recv, size_t count, cu
     return nccl_check(g_nccl.AllGather(send, recv, count, kNcclFloat64, p->nccl_comm, st),
                       "ncclAllGather");
 }
+
+// ---- all-gather through peer memory -----------------------------------------
+// One CTA: this rank's `count` partials are stored straight into slot `rank`
+// of every rank's receive buffer (NVLink peer stores; the own buffer is one
+// of them), made visible system-wide, then the epoch flag of this rank is
+// raised in every peer's flag array; the CTA finishes when every rank's flag
+// in its own array has reached the epoch.  The receive regions of the cut
+// and residual exchanges alternate, and a rank cannot start exchange e+2
+// before every rank has entered e+1, so no region is overwritten while a
+// rank still reads it.  A bounded wait (10 s of globaltimer) turns a lost
+// peer into a run error instead of a hang.
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* a) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* a, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void __launch_bounds__(1024) k_p2p_allgather(
+    const double* __restrict__ send, int64_t count, double* const* peer_recv, int64_t recv_off,
+    unsigned long long* const* peer_flags, const unsigned long long* my_flags,
+    unsigned long long* epoch, int32_t rank, int32_t world, Ctrl* ctrl) {
+    __shared__ unsigned long long s_ep;
+    __shared__ int s_fail;
+    if (ctrl->p2p_timeout) return;            // a peer was lost earlier in this chunk
+    if (threadIdx.x == 0) { s_ep = *epoch + 1; s_fail = 0; }
+    __syncthreads();
+    const unsigned long long ep = s_ep;
+    for (int r = 0; r < world; ++r) {
+        double* __restrict__ dst = peer_recv[r] + recv_off + (int64_t)rank * count;
+        for (int64_t i = threadIdx.x; i < count; i += blockDim.x) dst[i] = send[i];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        *epoch = ep;
+        for (int r = 0; r < world; ++r) st_release_sys(peer_flags[r] + rank, ep);
+    }
+    if (threadIdx.x < world) {
+        const unsigned long long t0 = globaltimer_ns();
+        while (ld_acquire_sys(my_flags + threadIdx.x) < ep) {
+            if (globaltimer_ns() - t0 > 10000000000ull) { s_fail = 1; break; }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && s_fail) {
+        ctrl->stop = 1;                       // fg_run reports the timeout
+        ctrl->p2p_timeout = 1;
+    }
+}
+
+int exchange_cut(fg_plan* p, const double* send, size_t recv_off, size_t count,
+                 cudaStream_t st) {
+    if (p->nccl_comm) return exchange_nccl(p, send, p->d_recv + recv_off, count, st);
+    k_p2p_allgather<<<1, 1024, 0, st>>>(send, (int64_t)count, p->d_peer_recv, (int64_t)recv_off,
+                                        p->d_peer_flags, p->d_flags, p->d_epoch, p->rank,
+                                        p->world, p->d_ctrl);
+    return 0;
+}
 }  // namespace
 
 extern "C" {
@@ -2913,6 +3025,75 @@ int fg_plan_attach_nccl(fg_plan* p, const char* nccl_lib, const char* id128, int
     if (p->d_recv) cudaFree(p->d_recv);
     p->d_recv = nullptr;
     if (int rc = dalloc(&p->d_recv, (size_t)world * (p->ncut + 4))) return rc;
+    for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
+    p->graphs.clear();
+    return 0;
+}
+
+// Peer-memory exchange, step 1: (re)allocate the receive buffer for `world`
+// ranks and the flag array, and export both as CUDA IPC handles
+// (out: 2 x 64 bytes).
+int fg_p2p_export(fg_plan* p, int32_t world, char* out128) {
+    CK(cudaSetDevice(p->device));
+    if (int rc = settle_idle(p)) return rc;
+    if (world < 1) return fail(FG_ERR_INVALID, "bad world");
+    if (p->d_recv) cudaFree(p->d_recv);
+    p->d_recv = nullptr;
+    if (int rc = dalloc(&p->d_recv, (size_t)world * (p->ncut + 4))) return rc;
+    if (p->d_flags) cudaFree(p->d_flags);
+    p->d_flags = nullptr;
+    if (int rc = dalloc(&p->d_flags, (size_t)world)) return rc;
+    CK(cudaMemset(p->d_flags, 0, world * sizeof(unsigned long long)));
+    if (!p->d_epoch && (dalloc(&p->d_epoch, 1) != 0)) return FG_ERR_CUDA;
+    CK(cudaMemset(p->d_epoch, 0, sizeof(unsigned long long)));
+    cudaIpcMemHandle_t h[2];
+    CK(cudaIpcGetMemHandle(&h[0], p->d_recv));
+    CK(cudaIpcGetMemHandle(&h[1], p->d_flags));
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    std::memcpy(out128, h, 128);
+    return 0;
+}
+
+// Step 2: attach the peers (all ranks' exported handles, rank-major,
+// world x 128 bytes; the own entry is used directly), the rank / world and
+// the global payload size (residual scale).  Every later fg_run exchanges
+// the cut partials and residual partials through peer memory inside the
+// captured iteration.  All ranks must have exported before any attaches.
+int fg_plan_attach_p2p(fg_plan* p, int32_t rank, int32_t world, const char* handles,
+                       int64_t payload_global) {
+    CK(cudaSetDevice(p->device));
+    if (int rc = settle_idle(p)) return rc;
+    if (world < 1 || rank < 0 || rank >= world || !p->d_flags)
+        return fail(FG_ERR_INVALID, "fg_p2p_export first; bad rank/world");
+    std::vector<double*> recv(world);
+    std::vector<unsigned long long*> flags(world);
+    for (int r = 0; r < world; ++r) {
+        if (r == rank) {
+            recv[r] = p->d_recv;
+            flags[r] = p->d_flags;
+            continue;
+        }
+        cudaIpcMemHandle_t h[2];
+        std::memcpy(h, handles + 128 * (size_t)r, 128);
+        void* a = nullptr;
+        void* f = nullptr;
+        CK(cudaIpcOpenMemHandle(&a, h[0], cudaIpcMemLazyEnablePeerAccess));
+        p->ipc_opened.push_back(a);
+        CK(cudaIpcOpenMemHandle(&f, h[1], cudaIpcMemLazyEnablePeerAccess));
+        p->ipc_opened.push_back(f);
+        recv[r] = (double*)a;
+        flags[r] = (unsigned long long*)f;
+    }
+    if (p->d_peer_recv) cudaFree(p->d_peer_recv);
+    if (p->d_peer_flags) cudaFree(p->d_peer_flags);
+    p->d_peer_recv = nullptr;
+    p->d_peer_flags = nullptr;
+    if (int rc = upload(&p->d_peer_recv, recv)) return rc;
+    if (int rc = upload(&p->d_peer_flags, flags)) return rc;
+    p->p2p = 1;
+    p->world = world;
+    p->rank = rank;
+    p->Pglobal = payload_global;
     for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
     p->graphs.clear();
     return 0;

@@ -5,9 +5,12 @@ exchanges the cut partial sums with device copies: it validates the
 partitioned algorithm on a single GPU against the one-plan result.
 
 ``NcclRank`` is the production path: one process per GPU (torchrun), each
-rank builds the same graph, keeps its own partition plan, and the plans
-all-gather the cut partials and residual partials with NCCL inside the
-CUDA-graph-captured iteration.  ``torch.distributed`` only broadcasts the
+rank builds the same graph (or only its part: partition.*_rank_graph),
+keeps its own partition plan, and the plans all-gather the cut partials
+and residual partials inside the CUDA-graph-captured iteration -- with
+NCCL (``transport="nccl"``) or by storing them straight into the peers'
+receive buffers over NVLink with epoch flags (``transport="p2p"``, CUDA
+IPC handles exchanged once through ``torch.distributed``).  ``torch.distributed`` only broadcasts the
 NCCL unique id and (for ``gather_state``) moves host arrays.
 
 Parity: non-cut variables are summed exactly as on one GPU; a cut
@@ -129,7 +132,8 @@ class NcclRank:
     graph is built on the host.
     """
 
-    def __init__(self, graph, rank, world, group=None, device=None, local=None):
+    def __init__(self, graph, rank, world, group=None, device=None, local=None,
+                 transport="nccl"):
         import torch.distributed as dist
         self.graph = graph
         self.rank, self.world = int(rank), int(world)
@@ -140,16 +144,33 @@ class NcclRank:
             self.part = None
             self.local = local
         self.plan = DevicePlan(self.local, device=device)
+        self.transport = transport
         lib = _native.load()
-        path = nccl_library()
-        bpath = path.encode() if path else None
-        uid = C.create_string_buffer(128)
-        if self.rank == 0:
-            _native.check(lib.fg_nccl_unique_id(bpath, uid))
-        obj = [bytes(uid.raw) if self.rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0, group=group)
-        _native.check(lib.fg_plan_attach_nccl(self.plan._h, bpath, obj[0], self.rank,
-                                              self.world))
+        if transport == "p2p":
+            # peer memory: export this rank's receive buffer and flags as
+            # CUDA IPC handles, all-gather them, attach the peers'
+            h = C.create_string_buffer(128)
+            _native.check(lib.fg_p2p_export(self.plan._h, self.world, h))
+            allh = [None] * self.world
+            dist.all_gather_object(allh, bytes(h.raw), group=group)
+            pay = [None] * self.world
+            dist.all_gather_object(pay, int(self.local.total_edge_payload), group=group)
+            buf = C.create_string_buffer(b"".join(allh), 128 * self.world)
+            _native.check(lib.fg_plan_attach_p2p(self.plan._h, self.rank, self.world, buf,
+                                                 int(sum(pay))))
+            dist.barrier(group=group)              # every rank attached before any run
+        elif transport == "nccl":
+            path = nccl_library()
+            bpath = path.encode() if path else None
+            uid = C.create_string_buffer(128)
+            if self.rank == 0:
+                _native.check(lib.fg_nccl_unique_id(bpath, uid))
+            obj = [bytes(uid.raw) if self.rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            _native.check(lib.fg_plan_attach_nccl(self.plan._h, bpath, obj[0], self.rank,
+                                                  self.world))
+        else:
+            raise ValueError(f"unknown transport {transport!r}")
         self._dist = dist
         self._group = group
 

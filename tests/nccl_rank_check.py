@@ -36,13 +36,17 @@ def main():
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # FG_TRANSPORT=p2p: exchange through CUDA IPC peer memory; FG_ONE_DEVICE=1
+    # puts every rank on device 0 (the one-GPU pool; NCCL refuses that)
+    transport = os.environ.get("FG_TRANSPORT", "nccl")
+    device = 0 if os.environ.get("FG_ONE_DEVICE") == "1" else local
     if name == "pack_rank":
         from paper_1603_02526_b200.partition import packing_rank_graph
         spec = fg.PackingSpec(150)
         g = fg.build_packing(spec)
         lg = packing_rank_graph(spec, rank, world)
         st = fg.init_state(g, seed=7)
-        nr = NcclRank(None, rank, world, device=local, local=lg)
+        nr = NcclRank(None, rank, world, device=device, local=lg, transport=transport)
         if world != 1:
             raise SystemExit("pack_rank check compares the gathered state at world 1 only")
         nr.upload(st)
@@ -59,7 +63,7 @@ def main():
         g = fg.build_mpc(spec)
         lg = mpc_rank_graph(spec, rank, world)
         st = fg.init_state(g, seed=7)
-        nr = NcclRank(None, rank, world, device=local, local=lg)
+        nr = NcclRank(None, rank, world, device=device, local=lg, transport=transport)
         if world != 1:
             raise SystemExit("mpc_rank check compares the gathered state at world 1 only")
         nr.upload(st)
@@ -69,10 +73,17 @@ def main():
     else:
         g = graph(name)
         st = fg.init_state(g, seed=7)
-        nr = NcclRank(g, rank, world, device=local)
+        nr = NcclRank(g, rank, world, device=device, transport=transport)
         nr.upload(st)
         res, hist = nr.run(iters)
         out = nr.gather_state(st)
+    group_bitwise = None
+    if rank == 0 and world > 1 and name in ("pack", "mpc", "svm"):
+        # the same partition run as a local group on one device: the
+        # exchange transport must not change a single bit
+        from paper_1603_02526_b200.distributed import LocalGroup
+        lgo, _r, _h = LocalGroup(g, world, device=device).run(iters, state=st)
+        group_bitwise = all(np.array_equal(getattr(out, k), getattr(lgo, k)) for k in "xmzun")
     if rank == 0:
         single = fg.AdmmState(*(getattr(st, k).copy() for k in "xmzun"))
         _sol, rep = fg.run(g, fg.RunConfig(max_iterations=iters), state=single)
@@ -84,6 +95,7 @@ def main():
                           "ncut": int(getattr(nr.local, "ncut", 0)),
                           "local_edges": int(len(nr.local.edge_var)),
                           "launches": int(res.launches), "rel_err": err,
+                          "transport": transport, "group_bitwise": group_bitwise,
                           "bitwise": all(np.array_equal(getattr(out, k), getattr(single, k))
                                          for k in "xmzun"),
                           "history_rows": int(len(hist))}))

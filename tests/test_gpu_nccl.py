@@ -33,3 +33,43 @@ def test_nccl_rank_world1_matches_single_plan(gpu, name):
     assert d["world"] == 1 and d["iterations"] == 12 and d["launches"] > 0
     assert d["history_rows"] == 12
     assert d["bitwise"], d["rel_err"]
+
+
+def _torchrun(name, nproc, env_extra, iters=12):
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ, **env_extra)
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", str(nproc), "--master-addr", "127.0.0.1",
+                        "--master-port", str(port),
+                        os.path.join(ROOT, "tests", "nccl_rank_check.py"), name, str(iters)],
+                       cwd=ROOT, capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+
+
+@pytest.mark.parametrize("name", ["pack", "mpc_rank"])
+def test_p2p_rank_world1_matches_single_plan(gpu, name):
+    """Peer-memory transport at one rank: the exchange kernel stores into
+    the rank's own receive buffer and raises its own flag."""
+    d = _torchrun(name, 1, {"FG_TRANSPORT": "p2p"})
+    assert d["transport"] == "p2p" and d["iterations"] == 12 and d["history_rows"] == 12
+    # counted from the captured graph's kernel nodes: partition passes and
+    # the exchange kernel every iteration
+    assert d["launches"] >= 3 * d["iterations"]
+    assert d["bitwise"], d["rel_err"]
+
+
+@pytest.mark.parametrize("name", ["pack", "mpc", "svm"])
+def test_p2p_two_ranks_one_device(gpu, name):
+    """Two processes, both on device 0, exchanging the cut and residual
+    partials through CUDA IPC peer memory inside the captured iteration --
+    the real multi-rank exchange the one-GPU pool can run (NCCL refuses two
+    ranks on one device).  The gathered state equals the same partition
+    run as a local group bit for bit, and the single-plan run to 1e-9."""
+    d = _torchrun(name, 2, {"FG_TRANSPORT": "p2p", "FG_ONE_DEVICE": "1"})
+    assert d["world"] == 2 and d["iterations"] == 12 and d["history_rows"] == 12
+    assert d["ncut"] > 0 and d["launches"] >= 4 * d["iterations"]
+    assert d["group_bitwise"] is True
+    assert max(d["rel_err"].values()) <= 1e-9, d["rel_err"]
