@@ -179,8 +179,8 @@ int fg_plan_sync_params(fg_plan* plan, const double* edge_rho,
  * flight (it is compared with z[zmap] - u on a copy stream while the next
  * fg_run starts from n = z - u, and fg_run repeats the run from the
  * uploaded state if they differ), so the n buffer must stay valid and
- * unchanged until the next call on the plan.  Plans attached to NCCL (and
- * FGADMM_SPEC_UPLOAD=0) upload all three synchronously. */
+ * unchanged until the next call on the plan.  Plans attached to NCCL or
+ * peer memory (and FGADMM_SPEC_UPLOAD=0) upload all three synchronously. */
 int fg_state_upload(fg_plan* plan, const double* z, const double* u,
                     const double* n);
 int fg_run(fg_plan* plan, const fg_run_config* cfg, double* history,
@@ -204,8 +204,10 @@ int fg_state_nonfinite(const fg_plan* plan, int64_t* out4);
 int fg_debug_download(fg_plan* plan, int32_t buffer, double* out_ref);
 /* Per-kernel device time of `iterations` fused iterations (after
  * fg_state_upload): labels[32*i], ms[i], counts[i] for each kernel slot of
- * one iteration (edge_<kind>..., var_*, reduce).  Profiling aid; the
- * arithmetic is exactly fg_run's. */
+ * one iteration (edge_<kind>..., var_*, reduce).  The first iteration of
+ * the timed sequence runs untimed when more follow (kernel loading), so
+ * counts[i] = iterations - 1 (generic) or - 2 (fused chain).  Profiling
+ * aid; the arithmetic is exactly fg_run's. */
 int fg_profile_kernels(fg_plan* plan, int64_t iterations, int32_t max_slots,
                        char* labels, double* ms, int64_t* counts,
                        int32_t* nslots);

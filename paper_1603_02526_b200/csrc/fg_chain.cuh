@@ -66,10 +66,23 @@ struct WUni {
 // test made once per run), else the quotient from y's refined reciprocal
 // computed once per run (qdiv_r), else the full inline division: bitwise
 // ddivq(x, y) in every case
+template <bool SC = false>
 __device__ __forceinline__ double dq_c(double x, double y, double inv, double rcp) {
     if (inv != 0.0) return x * inv;
-    if (rcp != 0.0) return qdiv_r(x, y, rcp);
-    return qdiv(x, y);
+    if (rcp != 0.0) return qdiv_r<SC>(x, y, rcp);
+    return qdiv<SC>(x, y);
+}
+
+// Constant-divisor mode of the uniform form (template argument CM):
+// kCmAny -- power-of-two inverse when given, else the inline division;
+// kCmRcp -- ... else the refined reciprocal; kCmPow2 -- every divisor has
+// its power-of-two inverse (rho a power of two: z weights 4r, 2r, 2r and r
+// all are), so the kernel carries no division code at these sites.
+enum : int { kCmAny = 0, kCmRcp = 1, kCmPow2 = 2 };
+template <int CM>
+__device__ __forceinline__ double dq_m(double x, double y, double inv, double rcp) {
+    if (CM == kCmPow2) return x * inv;
+    return dq_c<true>(x, y, inv, CM == kCmRcp ? rcp : 0.0);
 }
 
 // refined reciprocals of the uniform form's constant divisors (one thread;
@@ -375,7 +388,7 @@ __device__ __forceinline__ ChainWLoads chain_w_load(const PassB& b, const ChainD
     return L;
 }
 
-template <int D, bool UNI, bool RCP>
+template <int D, bool UNI, int CM>
 __device__ __forceinline__ void chain_w_point(const PassB& b, const ChainDev& c, int32_t i,
                                               int lane, double* sc, double* su,
                                               const ChainWLoads& L, const WUni& W,
@@ -410,11 +423,11 @@ __device__ __forceinline__ void chain_w_point(const PassB& b, const ChainDev& c,
     // ---- phase x (equalities first: their inputs die early) ----
     double x2, x3;
     if (UNI) {                                                    // prox_equality
-        x2 = dq_c(W.r * np_ + W.r * n2, W.r + W.r, W.inv2r, RCP ? W.rcp2r : 0.0);
-        x3 = dq_c(W.r * n3 + W.r * nn_, W.r + W.r, W.inv2r, RCP ? W.rcp2r : 0.0);
+        x2 = dq_m<CM>(W.r * np_ + W.r * n2, W.r + W.r, W.inv2r, W.rcp2r);
+        x3 = dq_m<CM>(W.r * n3 + W.r * nn_, W.r + W.r, W.inv2r, W.rcp2r);
     } else {
-        x2 = ddivq(sc[kWRP] * np_ + sc[kWR + 2] * n2, sc[kWRP] + sc[kWR + 2]);
-        x3 = ddivq(sc[kWR + 3] * n3 + sc[kWRN] * nn_, sc[kWR + 3] + sc[kWRN]);
+        x2 = ddivq<true>(sc[kWRP] * np_ + sc[kWR + 2] * n2, sc[kWRP] + sc[kWR + 2]);
+        x3 = ddivq<true>(sc[kWR + 3] * n3 + sc[kWRN] * nn_, sc[kWR + 3] + sc[kWRN]);
     }
     const double x0 = sc[kWFN] * n0;                              // prox_svm_norm
     const double pr = n1 * X;
@@ -429,16 +442,16 @@ __device__ __forceinline__ void chain_w_point(const PassB& b, const ChainDev& c,
     dot += __shfl_xor_sync(kFull, dot, 4);
     const double Y = sc[kWY];
     const double slack = (1.0 - nx1) - Y * (dot + nb);
-    const double mu = ddivq(np_max0(slack), sc[kWDEN]);
+    const double mu = ddivq<true>(np_max0(slack), sc[kWDEN]);
     double x1, xbv, xx1;
     if (UNI) {                         // mu / rho: one divisor for all three
-        const double q = dq_c(mu, W.r, W.invr, RCP ? W.rcpr : 0.0);
+        const double q = dq_m<CM>(mu, W.r, W.invr, W.rcpr);
         x1 = n1 + (q * Y) * X;
         xbv = nb + q * Y;
         xx1 = nx1 + q;
     } else {
         // mu/rho1, mu/rho_b, mu/rho_x1 on lanes 0, 1, 2 (one division for all)
-        const double q = ddivq(mu, sc[lane == 1 ? kWRB : (lane == 2 ? kWRX1 : kWR + 1)]);
+        const double q = ddivq<true>(mu, sc[lane == 1 ? kWRB : (lane == 2 ? kWRX1 : kWR + 1)]);
         x1 = n1 + (__shfl_sync(kFull, q, 0) * Y) * X;
         xbv = nb + __shfl_sync(kFull, q, 1) * Y;
         xx1 = nx1 + __shfl_sync(kFull, q, 2);
@@ -453,8 +466,8 @@ __device__ __forceinline__ void chain_w_point(const PassB& b, const ChainDev& c,
         res += m1 * r1;
         res += m2 * r2;
         res += m3 * r3;
-        const double zn = UNI ? dq_c(m0 * r0 + res, W.zww, W.invzww, RCP ? W.rcpzww : 0.0)
-                              : ddivq(m0 * r0 + res, sc[kWZWW]);
+        const double zn = UNI ? dq_m<CM>(m0 * r0 + res, W.zww, W.invzww, W.rcpzww)
+                              : ddivq<true>(m0 * r0 + res, sc[kWZWW]);
         b.z[zo] = zn;
         const double dz = zn - zi;
         const double t0 = x0 - zn, t1 = x1 - zn, t2 = x2 - zn, t3 = x3 - zn;
@@ -483,8 +496,8 @@ __device__ __forceinline__ void chain_w_point(const PassB& b, const ChainDev& c,
         const double mx0 = xx0 + ux0, mx1 = xx1 + ux1;
         double rs = 0.0;
         rs += mx1 * R3;
-        const double zx = UNI ? dq_c(mx0 * rx0 + rs, W.zwx, W.invzwx, RCP ? W.rcpzwx : 0.0)
-                              : ddivq(mx0 * rx0 + rs, sc[kWZWX]);
+        const double zx = UNI ? dq_m<CM>(mx0 * rx0 + rs, W.zwx, W.invzwx, W.rcpzwx)
+                              : ddivq<true>(mx0 * rx0 + rs, sc[kWZWX]);
         {
             b.z[c.zX + i] = zx;
             const double dzx = zx - zxi;
@@ -504,10 +517,10 @@ __device__ __forceinline__ void chain_w_point(const PassB& b, const ChainDev& c,
     }
 }
 
-// RCP (uniform weights with a divisor that is not a power of two): the
-// constant divisions use the per-run refined reciprocals; without it the
-// power-of-two form carries no reciprocal code (registers: 64 at the cap)
-template <int D, bool UNI, bool RCP = false>
+// CM (uniform weights): kCmPow2 when every constant divisor is a power of
+// two (no division code), kCmRcp when one is not and has a refined
+// reciprocal, else kCmAny (registers: 64 at the cap)
+template <int D, bool UNI, int CM = kCmAny>
 __global__ void __launch_bounds__(kChainThreads, FG_CHAIN_W_MINB) k_svm_chain_w(PassB b, ChainDev c,
                                                                 double* xb_out,
                                                                 int64_t part_off, WUni W) {
@@ -577,7 +590,7 @@ __global__ void __launch_bounds__(kChainThreads, FG_CHAIN_W_MINB) k_svm_chain_w(
         __syncwarp();                                  // previous point's reads done
         sc[lane] = sv;
         __syncwarp();
-        chain_w_point<D, UNI, RCP>(b, c, i, lane, sc, &s_u[warp][0][lane], L, W, xb_out, pp, dd, bad);
+        chain_w_point<D, UNI, CM>(b, c, i, lane, sc, &s_u[warp][0][lane], L, W, xb_out, pp, dd, bad);
     }
     if (bad & 1u) flag_error(b.ctrl, it - 1, FG_PHASE_N, true);
     if (bad & 2u) flag_error(b.ctrl, it, FG_PHASE_X, true);

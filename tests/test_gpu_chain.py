@@ -149,7 +149,7 @@ def test_chain_profile_labels(gpu, monkeypatch):
     plan.sync(g)
     plan.upload(st.z, st.u, st.n)
     prof = plan.profile_kernels(4)
-    assert "chain_svm" in prof and prof["chain_svm"][1] == 3
+    assert "chain_svm" in prof and prof["chain_svm"][1] == 2     # iteration 2 untimed (warm pass)
     assert not any(k.startswith("edge_") for k in prof)
 
 
