@@ -153,7 +153,7 @@ def test_chain_profile_labels(gpu, monkeypatch):
     assert not any(k.startswith("edge_") for k in prof)
 
 
-@pytest.mark.parametrize("rho,alpha", [(2.0, 1.0), (1.0, 1.5), (0.7, 1.3)])
+@pytest.mark.parametrize("rho,alpha", [(2.0, 1.0), (0.5, 1.3), (1.0, 1.5), (0.7, 1.3)])
 def test_chain_general_weights_bitwise(gpu, monkeypatch, rho, alpha):
     """Non-unit weights take the weighted form (weights loaded per point,
     per-point division tables); it stays bitwise equal to the per-kind
