@@ -8,6 +8,7 @@ TESTS=("tests/test_gpu_parity.py::test_packing_class_boundaries_bitwise_vs_oracl
        "tests/test_gpu_parity.py::test_star_quadratic_giant_bitwise"
        "tests/test_gpu_chain.py::test_chain_bitwise_equals_generic[33-32-7]"
        "tests/test_gpu_chain.py::test_chain_general_weights_bitwise[2.0-1.0]"
+       "tests/test_gpu_chain.py::test_chain_general_weights_bitwise[0.5-1.3]"
        "tests/test_gpu_chain.py::test_chain_general_weights_bitwise[0.7-1.3]"
        "tests/test_gpu_chain.py::test_chain_random_edge_weights_bitwise_and_oracle"
        "tests/test_gpu_parity.py::test_mpc_chain_bitwise_equals_per_kind"
