@@ -123,7 +123,6 @@ __global__ void __launch_bounds__(kEdgeThreads, 2) k_mpc_dyn_gemm(PassA a, Group
     double* nvs = Ks + cols * kDynGemmMaxCols;          // [F][ld]
     double* outs = nvs + kDynGemmF * ld;                // [F][2 n0 + 1]: x of both slots
     const BlockRef bk = g.blocks[blockIdx.x];
-    const RunHdr h = g.runs[bk.run];
     const SlotRun* sr = g.sruns + (int64_t)bk.run * g.nslots;
     const int64_t fl0 = bk.item0 / g.tpf;               // first factor (run-local)
     const int nf = (bk.item1 - bk.item0) / g.tpf;
