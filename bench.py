@@ -138,7 +138,6 @@ def kernel_bytes(graph, plan):
         # temporally blocked chain: the same compulsory bytes once per
         # launch of forms["mpc_block"] iterations (halo re-reads excluded)
         out["chain_mpc_block"] = P * 16 + Z * 24
-        out["reduce_block"] = 16 * forms["mpc_block"] * (Z // 20 // 45 + 1)
     return out
 
 

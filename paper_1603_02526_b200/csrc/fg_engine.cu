@@ -709,13 +709,16 @@ void chain_pass(fg_plan* p, int in, cudaStream_t st) {
 void launch_mpc_block(fg_plan* p, int in, int kb, cudaStream_t st) {
     PassB b{p->vt(), p->d_x, p->d_u[in], p->d_u[1 - in], nullptr, p->d_zb[1 - in],
             p->d_zb[in], p->d_rho, p->d_alpha, p->d_zw, p->d_ctrl, p->d_part, p->d_zvar};
+    // the block's reductions run in its last CTA (d_ucnt: no other counted
+    // kernel is in flight on an MPC-chain plan)
     if (kb == kMpcKB)
         k_mpc_block<kMpcKB, 20, 16><<<(unsigned)p->mpc_bntiles, kMbThreads, p->mpc_bsmem, st>>>(
-            b, p->mpc, p->mpc_btile, p->d_bpart, p->mpc_bntiles, p->mpc_fault);
+            b, p->mpc, p->mpc_btile, p->d_bpart, p->mpc_bntiles, p->mpc_fault, p->d_ucnt,
+            p->d_hist);
     else
         k_mpc_block<kMpcKBTail, 20, 16><<<(unsigned)p->mpc_bntiles, kMbThreads, p->mpc_bsmem, st>>>(
-            b, p->mpc, p->mpc_btile, p->d_bpart, p->mpc_bntiles, p->mpc_fault);
-    k_mpc_block_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_bpart, p->mpc_bntiles, kb, p->d_hist);
+            b, p->mpc, p->mpc_btile, p->d_bpart, p->mpc_bntiles, p->mpc_fault, p->d_ucnt,
+            p->d_hist);
 }
 
 // residual reduction of one iteration: a chain iteration leaves the small
@@ -2328,13 +2331,13 @@ int fg_run(fg_plan* p, const fg_run_config* cfg, double* history, fg_run_result*
             int64_t j = 2;
             while (left - 1 >= p->mpc_kb) {
                 launch_mpc_block(p, (int)((j - 1) & 1), kMpcKB, st);
-                launches += 2;
+                launches += 1;
                 left -= p->mpc_kb;
                 j += p->mpc_kb;
             }
             if (left - 1 >= kMpcKBTail) {            // a shorter block for the tail
                 launch_mpc_block(p, (int)((j - 1) & 1), kMpcKBTail, st);
-                launches += 2;
+                launches += 1;
                 left -= kMpcKBTail;
                 j += kMpcKBTail;
             }
@@ -2649,48 +2652,38 @@ int fg_profile_kernels(fg_plan* p, int64_t iterations, int32_t max_slots,
     p->mpc_reduce_fused = false;
     if (chain && p->mpc_chain && p->mpc_kb > 0) {
         // temporally blocked MPC chain: iteration 1 untimed, then blocks of
-        // kMpcKB iterations timed per launch (block kernel, its reduction);
-        // the tail iterations run untimed
+        // kMpcKB iterations timed per launch (the block kernel with its
+        // reductions in the last CTA, as fg_run launches it; the first block
+        // untimed when more follow); the tail iterations run untimed
         const int kb = p->mpc_kb;
         const int64_t nb = (iterations - 2) / kb;
         if (nb < 1) return fail(FG_ERR_INVALID, "profile of the blocked MPC chain needs "
                                                 "at least kMpcKB + 2 iterations");
-        if (max_slots < 2) return fail(FG_ERR_INVALID, "too many kernels for the output arrays");
-        std::vector<cudaEvent_t> ev(3 * nb);
+        if (max_slots < 1) return fail(FG_ERR_INVALID, "too many kernels for the output arrays");
+        const int64_t warm = nb >= 2 ? 1 : 0;
+        std::vector<cudaEvent_t> ev(2 * nb);
         for (auto& e : ev) CK(cudaEventCreate(&e));
         launch_iteration(p, 0, first_n, st);
         int64_t j = 2;
         for (int64_t i = 0; i < nb; ++i, j += kb) {
-            const int in = (int)((j - 1) & 1);
-            PassB b{p->vt(), p->d_x, p->d_u[in], p->d_u[1 - in], nullptr, p->d_zb[1 - in],
-                    p->d_zb[in], p->d_rho, p->d_alpha, p->d_zw, p->d_ctrl, p->d_part, p->d_zvar};
-            CK(cudaEventRecord(ev[3 * i], st));
-            k_mpc_block<kMpcKB, 20, 16><<<(unsigned)p->mpc_bntiles, kMbThreads, p->mpc_bsmem, st>>>(
-                b, p->mpc, p->mpc_btile, p->d_bpart, p->mpc_bntiles);
-            CK(cudaEventRecord(ev[3 * i + 1], st));
-            k_mpc_block_reduce<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_bpart, p->mpc_bntiles, kb,
-                                                   p->d_hist);
-            CK(cudaEventRecord(ev[3 * i + 2], st));
+            CK(cudaEventRecord(ev[2 * i], st));
+            launch_mpc_block(p, (int)((j - 1) & 1), kMpcKB, st);
+            CK(cudaEventRecord(ev[2 * i + 1], st));
         }
         for (; j <= iterations; ++j) launch_iteration(p, (int)((j - 1) & 1), false, st);
         CK(cudaStreamSynchronize(st));
         if (int rc = check_launch()) return rc;
-        ms[0] = ms[1] = 0.0;
-        for (int64_t i = 0; i < nb; ++i) {
+        ms[0] = 0.0;
+        for (int64_t i = warm; i < nb; ++i) {
             float t = 0;
-            cudaEventElapsedTime(&t, ev[3 * i], ev[3 * i + 1]);
+            cudaEventElapsedTime(&t, ev[2 * i], ev[2 * i + 1]);
             ms[0] += t;
-            cudaEventElapsedTime(&t, ev[3 * i + 1], ev[3 * i + 2]);
-            ms[1] += t;
         }
-        counts[0] = counts[1] = nb;
+        counts[0] = nb - warm;
         for (auto& e : ev) cudaEventDestroy(e);
-        const char* nm[2] = {"chain_mpc_block", "reduce_block"};
-        for (int i = 0; i < 2; ++i) {
-            std::memset(labels + 32 * i, 0, 32);
-            std::strncpy(labels + 32 * i, nm[i], 31);
-        }
-        *nslots = 2;
+        std::memset(labels, 0, 32);
+        std::strncpy(labels, "chain_mpc_block", 31);
+        *nslots = 1;
         Ctrl hc;
         CK(cudaMemcpy(&hc, p->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
         p->completed = hc.completed;

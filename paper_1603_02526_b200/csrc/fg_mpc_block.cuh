@@ -14,7 +14,7 @@
 // matrix-form dynamics v = K nv as the same fma chain, init, m, z in
 // NumPy's reduceat order, u), so the state is bitwise the per-iteration
 // chain's and therefore the per-kind path's.  Residual partials of the
-// owned nodes are written per iteration (k_mpc_block_reduce turns them
+// owned nodes are written per iteration (the last CTA turns them
 // into the history rows).  Any non-finite value of an owned node stops the
 // run and records the block (Ctrl::blk_err); the host then replays that
 // block iteration by iteration with the ordinary kernels, which raise the
@@ -55,11 +55,51 @@ inline size_t mpc_block_smem(int n0, int d) {
     return (cols * cols + (size_t)kMbNN * 4 * n0 + (size_t)kMbF * kMbLD) * sizeof(double);
 }
 
+// The KB iterations' residual reductions (history rows, iteration counter,
+// stop) in one CTA of NT threads: every iteration's tile partials loaded in
+// one pass (each accumulator sums its tiles in index order), then the block
+// sums and commits back to back.
+template <int NT>
+__device__ void mpc_block_commit(Ctrl* c, const double* bpart, int64_t ntiles, int kb,
+                                 double* hist, double* sm) {
+    double a[kMpcKB], bs[kMpcKB];
+#pragma unroll
+    for (int k = 0; k < kMpcKB; ++k) a[k] = bs[k] = 0.0;
+    for (int64_t i = threadIdx.x; i < ntiles; i += NT) {
+#pragma unroll
+        for (int k = 0; k < kMpcKB; ++k) {
+            if (k < kb) {
+                a[k] += __ldcg(bpart + 2 * ((int64_t)k * ntiles + i));
+                bs[k] += __ldcg(bpart + 2 * ((int64_t)k * ntiles + i) + 1);
+            }
+        }
+    }
+    // thread 0 keeps the control block in registers across the KB commits
+    CtrlIn in{};
+    if (threadIdx.x == 0) in = ctrl_in(c);
+#pragma unroll
+    for (int k = 0; k < kMpcKB; ++k) {
+        if (k < kb) {
+            block_sum2<NT>(a[k], bs[k], sm);
+            if (threadIdx.x == 0) {
+                reduce_commit(c, in, a[k], bs[k], hist);
+                ++in.it;
+            }
+        }
+    }
+}
+
+// `counter` non-null: the last CTA to finish runs the block's reductions
+// (mpc_block_commit) -- no separate reduction launch.  Every CTA that got
+// past the stop check counts itself, a faulting one included, and the last
+// one resets the counter; nothing is committed when a CTA stopped the run.
 template <int KB, int N0, int DD>
 __global__ void __launch_bounds__(kMbThreads, 3) k_mpc_block(PassB b, MpcChainDev c,
                                                              int32_t tile, double* bpart,
                                                              int64_t ntiles,
-                                                             int64_t fault_it = 0) {
+                                                             int64_t fault_it = 0,
+                                                             unsigned* counter = nullptr,
+                                                             double* hist = nullptr) {
     static_assert(KB % 2 == 1, "a block must flip the ping-pong slot");
     extern __shared__ double gsm[];
     if (b.ctrl->stop) return;
@@ -291,10 +331,8 @@ __global__ void __launch_bounds__(kMbThreads, 3) k_mpc_block(PassB b, MpcChainDe
             b.ctrl->blk_err = it0;
             b.ctrl->stop = 1;
         }
-        return;
-    }
-    // ---- owned nodes back to the output slot ----
-    {
+    } else {
+        // ---- owned nodes back to the output slot ----
         const int lo = t0 - a, nown = t1 - t0;
         double* __restrict__ uout = b.uout + c.pN + (int64_t)3 * t0 * n0;
         double* __restrict__ zout = b.z + c.zN + (int64_t)t0 * n0;
@@ -302,46 +340,19 @@ __global__ void __launch_bounds__(kMbThreads, 3) k_mpc_block(PassB b, MpcChainDe
         for (int i = threadIdx.x; i < nu; i += blockDim.x) uout[i] = us[lo * 3 * n0 + i];
         for (int i = threadIdx.x; i < nown * n0; i += blockDim.x) zout[i] = zs[lo * n0 + i];
     }
-}
-
-// History rows, iteration counter and completion of a block's KB
-// iterations (reduce_body per iteration over the tiles' partials, fixed
-// order).  Skipped when the block stopped the run.
-__global__ void __launch_bounds__(1024) k_mpc_block_reduce(Ctrl* c, const double* bpart,
-                                                           int64_t ntiles, int32_t kb,
-                                                           double* hist) {
-    __shared__ double sm[64];
-    __shared__ int s_stop;
-    if (threadIdx.x == 0) s_stop = c->stop;
-    __syncthreads();
-    if (s_stop) return;
-    // every iteration's partials are loaded in one pass (each accumulator
-    // sums its tiles in reduce_body's order), then the KB block sums and
-    // commits run back to back: one memory round trip instead of KB
-    double a[kMpcKB], bs[kMpcKB];
-#pragma unroll
-    for (int k = 0; k < kMpcKB; ++k) a[k] = bs[k] = 0.0;
-    for (int64_t i = threadIdx.x; i < ntiles; i += 1024) {
-#pragma unroll
-        for (int k = 0; k < kMpcKB; ++k) {
-            if (k < kb) {
-                a[k] += __ldcg(bpart + 2 * ((int64_t)k * ntiles + i));
-                bs[k] += __ldcg(bpart + 2 * ((int64_t)k * ntiles + i) + 1);
-            }
+    if (counter) {
+        __shared__ int s_last;
+        __shared__ double s_red[2 * (kMbThreads / 32)];
+        if (threadIdx.x == 0) {
+            __threadfence();                           // bpart / stop before the count
+            s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
         }
-    }
-    // thread 0 keeps the control block in registers across the KB commits
-    // (reduce_commit per iteration; no other kernel runs in between)
-    CtrlIn in{};
-    if (threadIdx.x == 0) in = ctrl_in(c);
-#pragma unroll
-    for (int k = 0; k < kMpcKB; ++k) {
-        if (k < kb) {
-            block_sum2<1024>(a[k], bs[k], sm);
-            if (threadIdx.x == 0) {
-                reduce_commit(c, in, a[k], bs[k], hist);
-                ++in.it;
-            }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            if (threadIdx.x == 0) *counter = 0u;
+            if (!*(volatile int32_t*)&b.ctrl->stop)
+                mpc_block_commit<kMbThreads>(b.ctrl, bpart, ntiles, KB, hist, s_red);
         }
     }
 }
