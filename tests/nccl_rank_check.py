@@ -40,6 +40,28 @@ def main():
     # puts every rank on device 0 (the one-GPU pool; NCCL refuses that)
     transport = os.environ.get("FG_TRANSPORT", "nccl")
     device = 0 if os.environ.get("FG_ONE_DEVICE") == "1" else local
+    if name == "lost_peer":
+        # every rank attaches; only rank 0 runs: its exchange waits for the
+        # other ranks' flags, gives up after the bounded wait and the run
+        # fails instead of hanging
+        import time
+        g = graph("pack")
+        st = fg.init_state(g, seed=7)
+        nr = NcclRank(g, rank, world, device=device, transport=transport)
+        out = {"name": name, "world": world}
+        if rank == 0:
+            nr.upload(st)
+            t0 = time.perf_counter()
+            try:
+                nr.run(iters)
+                out["error"] = None
+            except RuntimeError as e:
+                out["error"] = str(e)
+            out["seconds"] = time.perf_counter() - t0
+            print(json.dumps(out), flush=True)
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     if name == "pack_rank":
         from paper_1603_02526_b200.partition import packing_rank_graph
         spec = fg.PackingSpec(150)

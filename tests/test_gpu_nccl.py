@@ -73,3 +73,12 @@ def test_p2p_two_ranks_one_device(gpu, name):
     assert d["ncut"] > 0 and d["launches"] >= 4 * d["iterations"]
     assert d["group_bitwise"] is True
     assert max(d["rel_err"].values()) <= 1e-9, d["rel_err"]
+
+
+def test_p2p_lost_peer_fails_instead_of_hanging(gpu):
+    """A rank that attached but never runs: the other rank's exchange kernel
+    waits for its flags for the bounded 10 s, stops the run, and fg_run
+    reports the lost peer (no hung GPU)."""
+    d = _torchrun("lost_peer", 2, {"FG_TRANSPORT": "p2p", "FG_ONE_DEVICE": "1"}, iters=8)
+    assert d["error"] is not None and "stopped answering" in d["error"], d
+    assert 9.0 < d["seconds"] < 60.0, d
