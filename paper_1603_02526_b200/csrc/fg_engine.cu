@@ -595,6 +595,7 @@ int exchange_nccl(fg_plan* p, const double* send, double* recv, size_t count,
 // NCCL or through peer memory (fg_plan_attach_p2p)
 int exchange_cut(fg_plan* p, const double* send, size_t recv_off, size_t count,
                  cudaStream_t st);
+void launch_reduce_p2p(fg_plan* p, int64_t lo, int64_t hi, cudaStream_t st);
 
 void cut_finalize(fg_plan* p, int in, cudaStream_t st) {
     if (!p->ncutg) return;
@@ -633,11 +634,17 @@ void part_mid(fg_plan* p, int in, bool first, cudaStream_t st) {
         lo = chain_main_grid(p) + 1;
         hi = p->chain_grid;
     }
+    if (p->p2p) {
+        // peer memory: local sums, exchange and commit in one launch
+        launch_reduce_p2p(p, lo, hi, st);
+        return;
+    }
     k_reduce_local<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_send + p->ncut,
                                        lo, hi);
 }
 
 void part_post(fg_plan* p, cudaStream_t st) {
+    if (p->p2p) return;                       // committed by k_reduce_p2p
     k_reduce_final<<<1, 32, 0, st>>>(p->d_ctrl, p->d_recv + (size_t)p->world * p->ncut,
                                      p->world, p->d_hist);
 }
@@ -758,7 +765,7 @@ void launch_iteration(fg_plan* p, int in, bool first, cudaStream_t st) {
         part_pre(p, in, first, st);
         if (p->ncut) exchange_cut(p, p->d_send, 0, (size_t)p->ncut, st);
         part_mid(p, in, first, st);
-        exchange_cut(p, p->d_send + p->ncut, (size_t)p->world * p->ncut, 4, st);
+        if (!p->p2p) exchange_cut(p, p->d_send + p->ncut, (size_t)p->world * p->ncut, 4, st);
         part_post(p, st);
         return;
     }
@@ -2941,13 +2948,14 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     return t;
 }
 
-__global__ void __launch_bounds__(1024) k_p2p_allgather(
+// The exchange by one whole CTA (every thread calls it): true when a peer
+// was lost (the run is then stopped with p2p_timeout).
+__device__ __forceinline__ bool p2p_allgather_cta(
     const double* __restrict__ send, int64_t count, double* const* peer_recv, int64_t recv_off,
     unsigned long long* const* peer_flags, const unsigned long long* my_flags,
     unsigned long long* epoch, int32_t rank, int32_t world, Ctrl* ctrl) {
     __shared__ unsigned long long s_ep;
     __shared__ int s_fail;
-    if (ctrl->p2p_timeout) return;            // a peer was lost earlier in this chunk
     if (threadIdx.x == 0) { s_ep = *epoch + 1; s_fail = 0; }
     __syncthreads();
     const unsigned long long ep = s_ep;
@@ -2972,6 +2980,35 @@ __global__ void __launch_bounds__(1024) k_p2p_allgather(
         ctrl->stop = 1;                       // fg_run reports the timeout
         ctrl->p2p_timeout = 1;
     }
+    return s_fail != 0;
+}
+
+__global__ void __launch_bounds__(1024) k_p2p_allgather(
+    const double* __restrict__ send, int64_t count, double* const* peer_recv, int64_t recv_off,
+    unsigned long long* const* peer_flags, const unsigned long long* my_flags,
+    unsigned long long* epoch, int32_t rank, int32_t world, Ctrl* ctrl) {
+    if (ctrl->p2p_timeout) return;            // a peer was lost earlier in this chunk
+    p2p_allgather_cta(send, count, peer_recv, recv_off, peer_flags, my_flags, epoch, rank,
+                      world, ctrl);
+}
+
+// Peer-memory ranks: the residual step of an iteration in ONE launch --
+// this rank's partial sums (k_reduce_local's), their exchange through peer
+// memory, and the rank-order commit (k_reduce_final's) -- instead of three.
+__global__ void __launch_bounds__(1024) k_reduce_p2p(
+    Ctrl* c, const double* part, int64_t npart, double* send4, int64_t skip_lo, int64_t skip_hi,
+    double* const* peer_recv, int64_t recv_off, unsigned long long* const* peer_flags,
+    const unsigned long long* my_flags, unsigned long long* epoch, int32_t rank, int32_t world,
+    const double* recv4, double* hist) {
+    __shared__ double sm[64];
+    if (c->p2p_timeout) return;
+    reduce_local_body<1024>(c, part, npart, send4, skip_lo, skip_hi, sm);
+    __threadfence_block();
+    __syncthreads();                          // send4 (thread 0's stores) before the copy
+    if (p2p_allgather_cta(send4, 4, peer_recv, recv_off, peer_flags, my_flags, epoch, rank,
+                          world, c))
+        return;
+    if (threadIdx.x == 0) reduce_final_commit(c, recv4, world, hist);
 }
 
 int exchange_cut(fg_plan* p, const double* send, size_t recv_off, size_t count,
@@ -2981,6 +3018,13 @@ int exchange_cut(fg_plan* p, const double* send, size_t recv_off, size_t count,
                                         p->d_peer_flags, p->d_flags, p->d_epoch, p->rank,
                                         p->world, p->d_ctrl);
     return 0;
+}
+
+void launch_reduce_p2p(fg_plan* p, int64_t lo, int64_t hi, cudaStream_t st) {
+    k_reduce_p2p<<<1, 1024, 0, st>>>(p->d_ctrl, p->d_part, p->npart, p->d_send + p->ncut, lo, hi,
+                                     p->d_peer_recv, (int64_t)p->world * p->ncut, p->d_peer_flags,
+                                     p->d_flags, p->d_epoch, p->rank, p->world,
+                                     p->d_recv + (size_t)p->world * p->ncut, p->d_hist);
 }
 }  // namespace
 

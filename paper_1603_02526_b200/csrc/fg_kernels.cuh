@@ -514,17 +514,20 @@ __global__ void k_cut_finalize(PassB b, const int32_t* glist, const GComp* comps
 // Partitioned runs split the residual reduction: local sums (plus the local
 // error key) go to a 4-double send slot, are all-gathered, and every rank
 // combines them in rank order, so all ranks take the same stop decision.
-__global__ void __launch_bounds__(1024) k_reduce_local(Ctrl* c, const double* part,
-                                                       int64_t npart, double* send4,
-                                                       int64_t skip_lo = 0, int64_t skip_hi = 0) {
-    __shared__ double sm[64];
+// this rank's residual partial sums and error key -> send4[0..3]; one CTA
+// of NT threads
+template <int NT>
+__device__ __forceinline__ void reduce_local_body(const Ctrl* c, const double* part,
+                                                  int64_t npart, double* send4,
+                                                  int64_t skip_lo, int64_t skip_hi,
+                                                  double* sm) {
     double a = 0.0, bsum = 0.0;
-    for (int64_t i = threadIdx.x; i < npart; i += 1024) {
+    for (int64_t i = threadIdx.x; i < npart; i += NT) {
         if (i >= skip_lo && i < skip_hi) continue;
         a += part[2 * i];
         bsum += part[2 * i + 1];
     }
-    block_sum2<1024>(a, bsum, sm);
+    block_sum2<NT>(a, bsum, sm);
     if (threadIdx.x == 0) {
         send4[0] = a;
         send4[1] = bsum;
@@ -533,9 +536,18 @@ __global__ void __launch_bounds__(1024) k_reduce_local(Ctrl* c, const double* pa
     }
 }
 
-__global__ void k_reduce_final(Ctrl* c, const double* recv4, int32_t world,
-                               double* hist) {
-    if (threadIdx.x != 0 || c->stop == 1) return;
+__global__ void __launch_bounds__(1024) k_reduce_local(Ctrl* c, const double* part,
+                                                       int64_t npart, double* send4,
+                                                       int64_t skip_lo = 0, int64_t skip_hi = 0) {
+    __shared__ double sm[64];
+    reduce_local_body<1024>(c, part, npart, send4, skip_lo, skip_hi, sm);
+}
+
+// Rank-order combination of the all-gathered 4-double slots (thread 0):
+// residual norms, history row, error key, stop decision.
+__device__ __forceinline__ void reduce_final_commit(Ctrl* c, const double* recv4, int32_t world,
+                                                    double* hist) {
+    if (c->stop == 1) return;
     double a = recv4[0], bsum = recv4[1];
     unsigned long long err = (unsigned long long)__double_as_longlong(recv4[2]);
     for (int r = 1; r < world; ++r) {
@@ -563,6 +575,12 @@ __global__ void k_reduce_final(Ctrl* c, const double* recv4, int32_t world,
     if (dc) ok = ok && (dual <= c->dual_tol);
     if (ok) { c->converged = 1; c->stop = 1; }
     c->iter = it + 1;
+}
+
+__global__ void k_reduce_final(Ctrl* c, const double* recv4, int32_t world,
+                               double* hist) {
+    if (threadIdx.x != 0) return;
+    reduce_final_commit(c, recv4, world, hist);
 }
 
 // ===========================================================================

@@ -55,9 +55,10 @@ def test_p2p_rank_world1_matches_single_plan(gpu, name):
     the rank's own receive buffer and raises its own flag."""
     d = _torchrun(name, 1, {"FG_TRANSPORT": "p2p"})
     assert d["transport"] == "p2p" and d["iterations"] == 12 and d["history_rows"] == 12
-    # counted from the captured graph's kernel nodes: partition passes and
-    # the exchange kernel every iteration
-    assert d["launches"] >= 3 * d["iterations"]
+    # counted from the captured graph's kernel nodes: the partition passes
+    # and the residual step (local sums, exchange and commit in one
+    # k_reduce_p2p launch) every iteration
+    assert d["launches"] >= 2 * d["iterations"]
     assert d["bitwise"], d["rel_err"]
 
 
