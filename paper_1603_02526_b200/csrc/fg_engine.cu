@@ -591,11 +591,12 @@ int64_t count_var_launches(const fg_plan* p) {
 // process for a local group of plans (fg_group_run).
 int exchange_nccl(fg_plan* p, const double* send, double* recv, size_t count,
                   cudaStream_t st);
-// all-gather of `count` doubles into d_recv + recv_off (rank-major), by
-// NCCL or through peer memory (fg_plan_attach_p2p)
+// all-gather of `count` doubles into d_recv + recv_off (rank-major) by NCCL
+// (peer-memory ranks exchange inside k_cut_p2p / k_reduce_p2p instead)
 int exchange_cut(fg_plan* p, const double* send, size_t recv_off, size_t count,
                  cudaStream_t st);
 void launch_reduce_p2p(fg_plan* p, int64_t lo, int64_t hi, cudaStream_t st);
+void launch_cut_p2p(fg_plan* p, int in, cudaStream_t st);
 
 void cut_finalize(fg_plan* p, int in, cudaStream_t st) {
     if (!p->ncutg) return;
@@ -626,7 +627,7 @@ void part_pre(fg_plan* p, int in, bool first, cudaStream_t st) {
 
 // After the cut exchange, up to the residual exchange.
 void part_mid(fg_plan* p, int in, bool first, cudaStream_t st) {
-    cut_finalize(p, in, st);
+    if (!p->p2p) cut_finalize(p, in, st);   // peer memory: done by k_cut_p2p
     var_kernel<MODE_FUSED>(p, kSlotGiantUpdate, p->d_zb[in], p->d_zb[1 - in], p->d_u[in],
                            p->d_u[1 - in], nullptr, st);
     int64_t lo = 0, hi = 0;
@@ -763,7 +764,10 @@ bool chain_rest(fg_plan* p, int in, cudaStream_t st) {
 void launch_iteration(fg_plan* p, int in, bool first, cudaStream_t st) {
     if (p->ranked()) {
         part_pre(p, in, first, st);
-        if (p->ncut) exchange_cut(p, p->d_send, 0, (size_t)p->ncut, st);
+        if (p->ncut) {
+            if (p->p2p) launch_cut_p2p(p, in, st);      // exchange + cut z, one launch
+            else exchange_cut(p, p->d_send, 0, (size_t)p->ncut, st);
+        }
         part_mid(p, in, first, st);
         if (!p->p2p) exchange_cut(p, p->d_send + p->ncut, (size_t)p->world * p->ncut, 4, st);
         part_post(p, st);
@@ -2983,13 +2987,20 @@ __device__ __forceinline__ bool p2p_allgather_cta(
     return s_fail != 0;
 }
 
-__global__ void __launch_bounds__(1024) k_p2p_allgather(
-    const double* __restrict__ send, int64_t count, double* const* peer_recv, int64_t recv_off,
+// Peer-memory ranks: the cut exchange and the cut components' z (the rank-
+// order sums of the gathered partials, k_cut_finalize's) in ONE launch.
+__global__ void __launch_bounds__(1024) k_cut_p2p(
+    PassB b, const int32_t* glist, const GComp* comps, const int32_t* cutg, int64_t ncutg,
+    const double* send, int64_t ncut, double* const* peer_recv,
     unsigned long long* const* peer_flags, const unsigned long long* my_flags,
-    unsigned long long* epoch, int32_t rank, int32_t world, Ctrl* ctrl) {
-    if (ctrl->p2p_timeout) return;            // a peer was lost earlier in this chunk
-    p2p_allgather_cta(send, count, peer_recv, recv_off, peer_flags, my_flags, epoch, rank,
-                      world, ctrl);
+    unsigned long long* epoch, int32_t rank, int32_t world, const double* recv, double* gz) {
+    if (b.ctrl->p2p_timeout) return;
+    if (p2p_allgather_cta(send, ncut, peer_recv, 0, peer_flags, my_flags, epoch, rank, world,
+                          b.ctrl))
+        return;
+    if (b.ctrl->stop == 1) return;
+    for (int64_t t = threadIdx.x; t < ncutg; t += blockDim.x)
+        cut_finalize_one(b, glist, comps, cutg, t, recv, world, ncut, gz);
 }
 
 // Peer-memory ranks: the residual step of an iteration in ONE launch --
@@ -3013,11 +3024,15 @@ __global__ void __launch_bounds__(1024) k_reduce_p2p(
 
 int exchange_cut(fg_plan* p, const double* send, size_t recv_off, size_t count,
                  cudaStream_t st) {
-    if (p->nccl_comm) return exchange_nccl(p, send, p->d_recv + recv_off, count, st);
-    k_p2p_allgather<<<1, 1024, 0, st>>>(send, (int64_t)count, p->d_peer_recv, (int64_t)recv_off,
-                                        p->d_peer_flags, p->d_flags, p->d_epoch, p->rank,
-                                        p->world, p->d_ctrl);
-    return 0;
+    return exchange_nccl(p, send, p->d_recv + recv_off, count, st);
+}
+
+void launch_cut_p2p(fg_plan* p, int in, cudaStream_t st) {
+    PassB b{p->vt(), p->d_x, p->d_u[in], p->d_u[1 - in], nullptr, p->d_zb[1 - in],
+            p->d_zb[in], p->d_rho, p->d_alpha, p->d_zw, p->d_ctrl, p->d_part, p->d_zvar};
+    k_cut_p2p<<<1, 1024, 0, st>>>(b, p->d_glist, p->d_gcomps, p->d_cutg, p->ncutg, p->d_send,
+                                  p->ncut, p->d_peer_recv, p->d_peer_flags, p->d_flags,
+                                  p->d_epoch, p->rank, p->world, p->d_recv, p->d_gz);
 }
 
 void launch_reduce_p2p(fg_plan* p, int64_t lo, int64_t hi, cudaStream_t st) {

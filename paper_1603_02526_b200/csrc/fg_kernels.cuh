@@ -492,13 +492,10 @@ __global__ void __launch_bounds__(1024) k_reduce(Ctrl* c, const double* part,
 
 // Cut components after the exchange: rank-order sum of the all-gathered
 // partials (identical on every rank), then z as for a whole segment.
-__global__ void k_cut_finalize(PassB b, const int32_t* glist, const GComp* comps,
-                               const int32_t* cutg, int64_t ncutg,
-                               const double* recv, int32_t world, int64_t ncut,
-                               double* gz) {
-    if (b.ctrl->stop == 1) return;
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= ncutg) return;
+__device__ __forceinline__ void cut_finalize_one(const PassB& b, const int32_t* glist,
+                                                 const GComp* comps, const int32_t* cutg,
+                                                 int64_t t, const double* recv, int32_t world,
+                                                 int64_t ncut, double* gz) {
     const int32_t gi = cutg[t];
     const GComp gc = comps[gi];
     const int32_t k = glist[gi];
@@ -509,6 +506,16 @@ __global__ void k_cut_finalize(PassB b, const int32_t* glist, const GComp* comps
     gz[2 * gi + 1] = b.zin[k];
     b.z[k] = zn;
     if (!finite(zn)) flag_error(b.ctrl, b.ctrl->iter, FG_PHASE_Z, false);
+}
+
+__global__ void k_cut_finalize(PassB b, const int32_t* glist, const GComp* comps,
+                               const int32_t* cutg, int64_t ncutg,
+                               const double* recv, int32_t world, int64_t ncut,
+                               double* gz) {
+    if (b.ctrl->stop == 1) return;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ncutg) return;
+    cut_finalize_one(b, glist, comps, cutg, t, recv, world, ncut, gz);
 }
 
 // Partitioned runs split the residual reduction: local sums (plus the local
