@@ -258,9 +258,11 @@ int fg_plan_attach_nccl(fg_plan* plan, const char* nccl_lib, const char* id128,
  * calls fg_plan_attach_p2p with them and the graph's global payload size.
  * fg_run then stores each rank's cut and residual partials straight into
  * every peer's receive buffer over NVLink and synchronises on per-rank
- * epoch flags, inside the captured iteration (k_p2p_allgather); the rank-
- * order sum is the same as the NCCL path's.  A rank that stops answering
- * for 10 s fails the run with FG_ERR_CUDA instead of hanging. */
+ * epoch flags, inside the captured iteration -- fused with the kernels that
+ * consume the gathered values (k_cut_p2p, k_reduce_p2p); the rank-order sum
+ * is the same as the NCCL path's.  A rank that stops answering for 10 s
+ * fails the run with FG_ERR_CUDA instead of hanging.  A plan attaches to
+ * one exchange once (NCCL or peer memory); FG_ERR_INVALID otherwise. */
 int fg_p2p_export(fg_plan* plan, int32_t world, char* out128);
 int fg_plan_attach_p2p(fg_plan* plan, int32_t rank, int32_t world, const char* handles,
                        int64_t payload_global);

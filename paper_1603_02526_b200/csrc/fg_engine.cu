@@ -3059,6 +3059,8 @@ int fg_plan_attach_nccl(fg_plan* p, const char* nccl_lib, const char* id128, int
     if (int rc = settle_idle(p)) return rc;
     if (int rc = nccl_load(nccl_lib)) return rc;
     if (world < 1 || rank < 0 || rank >= world) return fail(FG_ERR_INVALID, "bad rank/world");
+    if (p->p2p || p->nccl_comm)
+        return fail(FG_ERR_INVALID, "plan already attached to an exchange");
     NcclId id;
     std::memcpy(id.internal, id128, 128);
     void* comm = nullptr;
@@ -3097,6 +3099,9 @@ int fg_p2p_export(fg_plan* p, int32_t world, char* out128) {
     CK(cudaSetDevice(p->device));
     if (int rc = settle_idle(p)) return rc;
     if (world < 1) return fail(FG_ERR_INVALID, "bad world");
+    // peers hold IPC mappings of an attached plan's buffers: never realloc them
+    if (p->p2p || p->nccl_comm)
+        return fail(FG_ERR_INVALID, "plan already attached to an exchange");
     if (p->d_recv) cudaFree(p->d_recv);
     p->d_recv = nullptr;
     if (int rc = dalloc(&p->d_recv, (size_t)world * (p->ncut + 4))) return rc;
@@ -3125,6 +3130,8 @@ int fg_plan_attach_p2p(fg_plan* p, int32_t rank, int32_t world, const char* hand
     if (int rc = settle_idle(p)) return rc;
     if (world < 1 || rank < 0 || rank >= world || !p->d_flags)
         return fail(FG_ERR_INVALID, "fg_p2p_export first; bad rank/world");
+    if (p->p2p || p->nccl_comm)
+        return fail(FG_ERR_INVALID, "plan already attached to an exchange");
     std::vector<double*> recv(world);
     std::vector<unsigned long long*> flags(world);
     for (int r = 0; r < world; ++r) {
