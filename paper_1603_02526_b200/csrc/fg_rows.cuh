@@ -17,6 +17,9 @@
 namespace fg {
 
 constexpr int kRowThreads = 256;
+#ifndef FG_ROW_FIXC
+#define FG_ROW_FIXC 1
+#endif
 
 // ---------------------------------------------------------------------------
 // Class-L rows, unit-weight form, one CTA per row with a TMA ring.
@@ -245,6 +248,28 @@ k_var_row_pipe(PassB b, const RowDesc* rdesc, const int32_t* prog, const int32_t
                     const double t = X[q] - zn[0];
                     pp += t * t;
                     const double rd = ex ? xe.rho * dz[0] : dz[0];
+                    dd += rd * rd;
+                    const double un = U[q] + (ex ? t * xe.alpha : t);
+                    uo[q] = un;
+                    bu |= !finite(un);
+                }
+            } else if (FG_ROW_FIXC && kRowThreads % D == 0) {
+                // D divides the block: thread t always meets component
+                // t % D, so z, dz and the exception edge's element are
+                // per-thread constants (no division, 32-bit indices)
+                const int nq = (int)((hi - lo) * D);
+                const int c = threadIdx.x % D;
+                double znc = zn[0], dzc = dz[0];
+#pragma unroll
+                for (int k = 1; k < D; ++k)
+                    if (c == k) { znc = zn[k]; dzc = dz[k]; }
+                const int exq = (xe.rank >= lo && xe.rank < hi) ? (int)(xe.rank - lo) * D + c : -1;
+                double* __restrict__ uo = b.uout + pb + lo * D;
+                for (int q = threadIdx.x; q < nq; q += kRowThreads) {
+                    const bool ex = q == exq;
+                    const double t = X[q] - znc;
+                    pp += t * t;
+                    const double rd = ex ? xe.rho * dzc : dzc;
                     dd += rd * rd;
                     const double un = U[q] + (ex ? t * xe.alpha : t);
                     uo[q] = un;
