@@ -28,7 +28,10 @@
 
 namespace fg {
 
-constexpr int kMpcKB = 5;                              // iterations per launch (odd)
+#ifndef FG_MPC_KB
+#define FG_MPC_KB 3
+#endif
+constexpr int kMpcKB = FG_MPC_KB;                      // iterations per launch (odd)
 constexpr int kMpcKBTail = 3;                          // shorter block for a run's tail
 constexpr int kMbF = 64;                               // factor slots
 constexpr int kMbThreads = kEdgeThreads;               // 256
