@@ -722,7 +722,7 @@ def main():
                         "per-launch time is set by the fp64 dynamics products and "
                         "shared-memory traffic, not HBM",
                 "limiter": "K nv on the fp64 tensor cores (mma.sync m8n8k4); the rest is "
-                           "shared-memory traffic (ncu L1/TEX 65%) and issue (52%); DRAM 6% "
+                           "shared-memory traffic and issue; DRAM 11% "
                            "(profiles/r02_ncu_mpc100k.md)"}
 
     # ---- end to end through the public API (host state in, host state out) ----
